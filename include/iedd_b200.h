@@ -1,0 +1,139 @@
+/*
+ * iedd_b200.h -- C-ABI of the B200 (sm_100a) Schwarz-PCG hot path.
+ *
+ * This is the drop-in boundary for the reference package iedd 0.1.0
+ * (/root/reference/pkg/src/iedd).  The reference is pure Python and binds no
+ * FFI; its duck-typed protocol (pcg.py:26-33 "_as_callable", spectrum.py:147,
+ * :161) is what these entry points replace.  The Python package
+ * paper_2108_12574_b200 binds them with ctypes.
+ *
+ * Conventions
+ *   - All double/int pointers named d_* are CUDA device pointers owned by the
+ *     caller unless the function creates a handle.  h_* pointers are host.
+ *   - All work is enqueued on the caller's stream (cudaStream_t passed as
+ *     void*).  Functions never synchronise the host except where they return
+ *     host scalars (ie_pcg_f64, ie_lanczos_f64, *_create with a bad_block out).
+ *   - Return codes: 0 ok; <0 argument error (the Python layer raises
+ *     ValueError with the reference's message); >0 numerical failure:
+ *       IE_ERR_NOT_SPD        subdomain Cholesky hit a non-positive pivot
+ *                             (NotPositiveDefinite, precond.py:197-200)
+ *       IE_ERR_BREAKDOWN      PCG p^T A p <= 0 or non-finite (pcg.py:99-103)
+ *       IE_ERR_NONFINITE      non-finite true residual (pcg.py:109-110)
+ *       IE_ERR_NO_RITZ        Lanczos produced no Ritz value (spectrum.py:188-189)
+ *       IE_ERR_CUDA           a CUDA runtime call failed (message via ie_last_error)
+ *   - Vectors are length N = n^dim in the reference's C order (last axis
+ *     fastest, geometry.py:42-44).
+ */
+#ifndef IEDD_B200_H
+#define IEDD_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define IE_OK 0
+#define IE_ERR_ARG (-1)
+#define IE_ERR_NOT_SPD 1
+#define IE_ERR_BREAKDOWN 2
+#define IE_ERR_NONFINITE 3
+#define IE_ERR_NO_RITZ 4
+#define IE_ERR_CUDA 5
+
+/* Operator metadata: replaces KernelOperator's scalar fields
+ * (kernel.py:110-162: grid.dim, grid.n_per_dim, lattice_spacing, weight,
+ * diag_value).  Entries are A_ij = weight * K(spacing * |a_i - a_j|) for
+ * i != j with integer multi-indices a, K = -log(r)/(2 pi) for dim 1, 2 and
+ * 1/(4 pi r) for dim 3 (kernel.py:146-149); A_ii = diag. */
+typedef struct ie_geom {
+    int32_t dim;
+    int32_t n;
+    double spacing;
+    double weight;
+    double diag;
+} ie_geom;
+
+/* ---------------------------------------------------------------- K1 ---- */
+typedef struct ie_matvec ie_matvec;
+
+/* Replaces ToeplitzMatvec.__init__ (toeplitz.py:19-32).  Builds the device
+ * log table used by the direct-sum kernel. */
+int ie_matvec_create(const ie_geom* g, ie_matvec** out);
+void ie_matvec_destroy(ie_matvec* m);
+
+/* Replaces ToeplitzMatvec.matvec (toeplitz.py:39-50), matrix-free:
+ * Y[:, c] = A[row_begin:row_end, :] X[:, c] for c < nrhs (nrhs in {1, 2}).
+ * X is N x nrhs column-major with leading dimension ldx (all N rows, full
+ * vector); Y receives rows row_begin..row_end-1 at Y + (row - row_begin)
+ * with leading dimension ldy.  Every row is summed in the same order for any
+ * row range and any nrhs, so results are bitwise independent of sharding and
+ * of RHS fusion. */
+int ie_matvec_f64(const ie_matvec* m, const double* d_X, int64_t ldx, int32_t nrhs,
+                  double* d_Y, int64_t ldy, int64_t row_begin, int64_t row_end,
+                  void* stream);
+
+/* Replaces KernelOperator.assemble_block (kernel.py:170-184):
+ * d_out (nr x nc row-major) = A[rows, cols]. */
+int ie_assemble_block_f64(const ie_geom* g, const int64_t* d_rows, int64_t nr,
+                          const int64_t* d_cols, int64_t nc, double* d_out, void* stream);
+
+/* ----------------------------------------------------------- K2 / K3 ---- */
+typedef struct ie_precond ie_precond;
+
+#define IE_VARIANT_PACKED_INVERSE 0  /* apply = packed symmetric A_k^{-1} matvec */
+#define IE_VARIANT_SUBST 1           /* apply = forward/back substitution with G_k */
+
+/* Replaces precond.from_decomposition(op, dec, backend="exact")
+ * (precond.py:157-215) + linalg.cholesky (linalg.py:36-45).
+ * Subdomains are given as CSR on the HOST: h_offsets[D+1], h_indices[...],
+ * each subdomain's index set sorted ascending (geometry.py:71-82).
+ * share_translated != 0 factorises one representative per translation class
+ * (blocks whose points are translates of each other are bitwise identical
+ * here, so this is exact).  On IE_ERR_NOT_SPD, *bad_block = the first
+ * failing subdomain id. */
+int ie_precond_create(const ie_geom* g, const int64_t* h_offsets, const int64_t* h_indices,
+                      int64_t D, int32_t variant, int32_t share_translated,
+                      ie_precond** out, int64_t* bad_block, void* stream);
+void ie_precond_destroy(ie_precond* p);
+
+/* Replaces Preconditioner.apply (precond.py:91-100): z = sum_k R_k^T A_k^{-1} R_k r,
+ * summed per point in ascending subdomain id from exact zeros. */
+int ie_precond_apply_f64(const ie_precond* p, const double* d_r, double* d_z, void* stream);
+
+/* Replaces Preconditioner.stats (precond.py:122-130) plus device footprint:
+ * out[0] = S (max block size), out[1] = reference memory_bytes (8*(s^2+s)
+ * summed), out[2] = device factor bytes, out[3] = number of factorised blocks,
+ * out[4] = D. */
+int ie_precond_stats(const ie_precond* p, int64_t* out5);
+
+/* ---------------------------------------------------------- K4 / K5 ---- */
+/* Replaces pcg.solve (pcg.py:54-136) for a native operator and
+ * preconditioner (precond may be NULL = identity, pcg.py:68).  f, u are
+ * device vectors of length N; u is overwritten with the iterate.
+ * h_history must hold max_iters+1 doubles; *n_it = number of entries - 1.
+ * h_flags[0] = converged, h_flags[1] = stagnated.  h_times[0] = t_pcg (s),
+ * h_times[1] = mean preconditioner-apply time t_s (s, device events).
+ * On IE_ERR_BREAKDOWN / IE_ERR_NONFINITE: *fail_iter, *fail_value hold the
+ * iteration and p^T A p (resp. residual). */
+int ie_pcg_f64(const ie_matvec* A, const ie_precond* T, const double* d_f, double* d_u,
+               double tol, int64_t max_iters, double* h_history, int64_t* n_it,
+               int32_t* h_flags, double* h_times, int64_t* fail_iter, double* fail_value,
+               void* stream);
+
+/* Replaces spectrum.extremal_eigenvalue_lanczos (spectrum.py:133-190):
+ * d_v0 = start vector (caller draws it from default_rng(seed), spectrum.py:148),
+ * which = 0 (min) / 1 (max).  *steps = Lanczos steps taken. */
+int ie_lanczos_f64(const ie_matvec* A, const ie_precond* T, const double* d_v0,
+                   int32_t which, int64_t max_iters, double rtol, double* lambda,
+                   int64_t* steps, void* stream);
+
+/* Last error text for IE_ERR_CUDA / IE_ERR_ARG (thread-local). */
+const char* ie_last_error(void);
+/* Number of this library's kernels launched so far (process-wide counter). */
+int64_t ie_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IEDD_B200_H */

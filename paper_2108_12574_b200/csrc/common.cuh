@@ -1,0 +1,114 @@
+// Shared device helpers for the Schwarz-PCG hot path (sm_100a).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <string>
+
+#include "../../include/iedd_b200.h"
+
+namespace ie {
+
+// ---------------------------------------------------------------- errors --
+void set_error(const std::string& msg);
+extern std::atomic<int64_t> g_launches;
+
+#define IE_CUDA(call)                                                        \
+    do {                                                                     \
+        cudaError_t _e = (call);                                             \
+        if (_e != cudaSuccess) {                                             \
+            ::ie::set_error(std::string(#call) + ": " + cudaGetErrorString(_e)); \
+            return IE_ERR_CUDA;                                              \
+        }                                                                    \
+    } while (0)
+
+#define IE_LAUNCHED()                                                         \
+    do {                                                                      \
+        ::ie::g_launches.fetch_add(1, std::memory_order_relaxed);             \
+        cudaError_t _e = cudaGetLastError();                                  \
+        if (_e != cudaSuccess) {                                              \
+            ::ie::set_error(std::string("kernel launch: ") + cudaGetErrorString(_e)); \
+            return IE_ERR_CUDA;                                               \
+        }                                                                     \
+    } while (0)
+
+constexpr int kNumSMs = 148;
+
+// ------------------------------------------------------------ log table --
+// log(d^2) for d^2 = m * s^2 with integer m >= 1 (dims 1 and 2):
+//   m = 2^e * f, f in [1,2); k = top 7 mantissa bits of f;
+//   c_k = 1/(1 + (k + 1/2)/128);  u = f*c_k - 1, |u| <= 2^-8;
+//   log(d^2) = T[e*128+k] + log1p(u),  T = e*ln2 - log(c_k) + 2*log(s)
+// T is rounded once from 80-bit arithmetic on the host.  log1p(u) is the
+// degree-6 Taylor polynomial (truncation <= 2^-56/7 absolute).
+constexpr int kLogK = 128;
+
+struct LogEntry {  // 16 B -> one LDS.128 per pair
+    double c;
+    double t;
+};
+
+// log1p(u) = u * q(u); returns q (degree-5 Horner), the caller folds u*q + t.
+__device__ __forceinline__ double log1p_q(double u) {
+    double q = -1.0 / 6.0;
+    q = fma(q, u, 1.0 / 5.0);
+    q = fma(q, u, -1.0 / 4.0);
+    q = fma(q, u, 1.0 / 3.0);
+    q = fma(q, u, -1.0 / 2.0);
+    return fma(q, u, 1.0);
+}
+
+// Split the normalised double m (>= 1) into the table index (relative to
+// the e=0 entry) and the reduced mantissa f in [1,2).
+__device__ __forceinline__ void log_split(double m, int& idx, double& f) {
+    const int hi = __double2hiint(m);
+    const int lo = __double2loint(m);
+    idx = (hi >> 13) - (1023 << 7);
+    f = __hiloint2double((hi & 0x000FFFFF) | 0x3FF00000, lo);
+}
+
+// log(m * s^2) with the table in shared or global memory.
+__device__ __forceinline__ double log_d2(const LogEntry* __restrict__ tab, double m) {
+    int idx;
+    double f;
+    log_split(m, idx, f);
+    const LogEntry e = tab[idx];
+    const double u = fma(f, e.c, -1.0);
+    return fma(log1p_q(u), u, e.t);
+}
+
+// Exact integer -> double for 0 <= m < 2^31 via the 2^52 magic constant
+// (one DADD instead of a conversion instruction).
+__device__ __forceinline__ double int_to_double_exact(int m) {
+    return __hiloint2double(0x43300000, m) - 4503599627370496.0;
+}
+
+// ------------------------------------------------------------ geometry --
+// Multi-index of global point i in C order (last axis fastest).
+template <int DIM>
+__device__ __forceinline__ void unravel(int64_t i, int n, int* a) {
+#pragma unroll
+    for (int d = DIM - 1; d >= 0; --d) {
+        a[d] = (int)(i % n);
+        i /= n;
+    }
+}
+
+// Entry A_ij from integer multi-index differences (shared by K1 epilogue
+// tests, block extraction K2 and ie_assemble_block_f64).
+struct EntryParams {
+    int dim;
+    double alpha;   // dims 1/2: -weight/(4 pi);  dim 3: weight/(4 pi s)
+    double diag;
+};
+
+__device__ __forceinline__ double entry_from_m(const EntryParams& P, const LogEntry* tab, int m) {
+    if (m == 0) return P.diag;
+    const double md = int_to_double_exact(m);
+    if (P.dim == 3) return P.alpha * rsqrt(md);
+    return P.alpha * log_d2(tab, md);
+}
+
+}  // namespace ie

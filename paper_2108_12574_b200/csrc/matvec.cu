@@ -1,0 +1,428 @@
+// K1: matrix-free FP64 kernel matvec (replaces ToeplitzMatvec.matvec,
+// /root/reference/pkg/src/iedd/toeplitz.py:39-50, whose entries are
+// kernel.py:170-184).
+//
+// y_i = diag * x_i + sum_{j != i} A_ij x_j,   A_ij = alpha * L(m_ij)
+//   dims 1/2: L(m) = log(m s^2) = log(d^2),      alpha = -w/(4 pi)
+//   dim 3:    L(m) = m^{-1/2},                   alpha = w/(4 pi s)
+// with m_ij = |a_i - a_j|^2 the squared integer lattice distance.  The pair
+// loop clamps m to >= 1, so the self pair contributes L(1) x_i, removed in
+// the epilogue: y_i = alpha*acc_i + (diag - alpha*L(1)) x_i.
+//
+// Layout: one thread owns R target rows; a CTA streams the source vector
+// through shared memory in tiles of TS points (NRHS doubles each, read as a
+// broadcast), and iterates each tile as runs along the last (contiguous)
+// lattice axis so the outer-axis distance is hoisted out of the pair loop.
+// The log table (16 B entries {c_k, T}) sits in shared memory.  Per-row sums:
+// plain FMA chain inside a tile, Neumaier-compensated across tiles, fixed
+// split order across CTAs -- identical for any row range and any NRHS.
+#include <math.h>
+
+#include <vector>
+
+#include "common.cuh"
+
+namespace ie {
+
+struct MatvecArgs {
+    const double* X;
+    int64_t ldx;
+    double* Y;
+    int64_t ldy;
+    double* W;  // split partials [split][row][rhs], or null when nsplit == 1
+    const LogEntry* tab;
+    int ntab;
+    int n;
+    int N;
+    int row_begin;
+    int nrows;
+    int TS;
+    int split_len;
+    double alpha;
+    double diag;
+};
+
+template <int DIM>
+__device__ __forceinline__ double pair_value(const LogEntry* tab, int m) {
+    const double md = int_to_double_exact(m);
+    if constexpr (DIM == 3) {
+        return rsqrt(md);
+    } else {
+        return log_d2(tab, md);
+    }
+}
+
+__device__ __forceinline__ void neumaier(double& s, double& c, double v) {
+    const double t = s + v;
+    c += (fabs(s) >= fabs(v)) ? ((s - t) + v) : ((v - t) + s);
+    s = t;
+}
+
+template <int DIM, int NRHS, int R>
+__global__ void __launch_bounds__(256) k_matvec(MatvecArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    LogEntry* stab = reinterpret_cast<LogEntry*>(smem);
+    double* xs = reinterpret_cast<double*>(smem + (DIM == 3 ? 0 : a.ntab * (int)sizeof(LogEntry)));
+    const int tid = threadIdx.x;
+    if constexpr (DIM != 3) {
+        for (int t = tid; t < a.ntab; t += blockDim.x) stab[t] = a.tab[t];
+    }
+
+    constexpr int NO = DIM > 1 ? DIM - 1 : 1;  // outer axes
+    int to[R][NO];
+    int tb[R];
+    int gi[R];
+    bool valid[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        const int row = blockIdx.x * blockDim.x * R + r * blockDim.x + tid;
+        valid[r] = row < a.nrows;
+        gi[r] = a.row_begin + (valid[r] ? row : a.nrows - 1);
+        int mi[DIM];
+        unravel<DIM>(gi[r], a.n, mi);
+#pragma unroll
+        for (int k = 0; k < NO; ++k) to[r][k] = (DIM > 1) ? mi[k] : 0;
+        tb[r] = mi[DIM - 1];
+    }
+
+    double s[R][NRHS], c[R][NRHS];
+#pragma unroll
+    for (int r = 0; r < R; ++r)
+#pragma unroll
+        for (int q = 0; q < NRHS; ++q) s[r][q] = c[r][q] = 0.0;
+
+    const int src0 = blockIdx.y * a.split_len;
+    const int src1 = min(a.N, src0 + a.split_len);
+    for (int j0 = src0; j0 < src1; j0 += a.TS) {
+        const int len = min(a.TS, src1 - j0);
+        __syncthreads();
+        for (int t = tid; t < len; t += blockDim.x) {
+#pragma unroll
+            for (int q = 0; q < NRHS; ++q) xs[t * NRHS + q] = a.X[q * a.ldx + j0 + t];
+        }
+        __syncthreads();
+
+        double ta[R][NRHS];
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int q = 0; q < NRHS; ++q) ta[r][q] = 0.0;
+
+        int j = j0;
+        while (j < j0 + len) {
+            const int outer = j / a.n;
+            const int d0 = j - outer * a.n;
+            const int L = min(a.n - d0, j0 + len - j);
+            int co[NO];
+            {
+                int o = outer;
+#pragma unroll
+                for (int k = NO - 1; k >= 0; --k) {
+                    co[k] = (DIM > 1) ? o % a.n : 0;
+                    o /= a.n;
+                }
+            }
+            int do2[R], db[R];
+#pragma unroll
+            for (int r = 0; r < R; ++r) {
+                int acc = 0;
+#pragma unroll
+                for (int k = 0; k < NO; ++k) {
+                    const int dd = to[r][k] - co[k];
+                    acc += dd * dd;
+                }
+                do2[r] = acc;
+                db[r] = tb[r] - d0;
+            }
+            const double* xp = xs + (j - j0) * NRHS;
+#pragma unroll 4
+            for (int t = 0; t < L; ++t) {
+                double xv[NRHS];
+                if constexpr (NRHS == 2) {
+                    const double2 x2 = reinterpret_cast<const double2*>(xp)[t];
+                    xv[0] = x2.x;
+                    xv[1] = x2.y;
+                } else {
+                    xv[0] = xp[t];
+                }
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    const int dbt = db[r] - t;
+                    const int m = max(dbt * dbt + do2[r], 1);
+                    const double v = pair_value<DIM>(stab, m);
+#pragma unroll
+                    for (int q = 0; q < NRHS; ++q) ta[r][q] = fma(v, xv[q], ta[r][q]);
+                }
+            }
+            j += L;
+        }
+#pragma unroll
+        for (int r = 0; r < R; ++r)
+#pragma unroll
+            for (int q = 0; q < NRHS; ++q) neumaier(s[r][q], c[r][q], ta[r][q]);
+    }
+
+    if (a.W != nullptr) {
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            if (!valid[r]) continue;
+            const int row = gi[r] - a.row_begin;
+#pragma unroll
+            for (int q = 0; q < NRHS; ++q)
+                a.W[((int64_t)blockIdx.y * a.nrows + row) * NRHS + q] = s[r][q] + c[r][q];
+        }
+        return;
+    }
+    const double lself = pair_value<DIM>(stab, 1);
+    const double corr = a.diag - a.alpha * lself;
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        if (!valid[r]) continue;
+        const int row = gi[r] - a.row_begin;
+#pragma unroll
+        for (int q = 0; q < NRHS; ++q) {
+            const double xi = a.X[q * a.ldx + gi[r]];
+            a.Y[q * a.ldy + row] = fma(a.alpha, s[r][q] + c[r][q], corr * xi);
+        }
+    }
+}
+
+// Sum split partials in split order and apply the epilogue.
+template <int DIM, int NRHS>
+__global__ void k_matvec_reduce(MatvecArgs a, int nsplit) {
+    const int row = blockIdx.x * blockDim.x + threadIdx.x;
+    if (row >= a.nrows) return;
+    double lself;
+    if constexpr (DIM == 3) {
+        lself = rsqrt(1.0);
+    } else {
+        lself = log_d2(a.tab, 1.0);
+    }
+    const double corr = a.diag - a.alpha * lself;
+    const int gi = a.row_begin + row;
+#pragma unroll
+    for (int q = 0; q < NRHS; ++q) {
+        double acc = 0.0;
+        for (int sp = 0; sp < nsplit; ++sp) acc += a.W[((int64_t)sp * a.nrows + row) * NRHS + q];
+        a.Y[q * a.ldy + row] = fma(a.alpha, acc, corr * a.X[q * a.ldx + gi]);
+    }
+}
+
+}  // namespace ie
+
+// ------------------------------------------------------------- host side --
+struct ie_matvec {
+    ie_geom g;
+    int N;
+    ie::LogEntry* d_tab;
+    int ntab;
+    double alpha;
+    // launch plan (depends on N only -> bitwise identical for any row range)
+    int R;
+    int TS;
+    int split_len;
+    int nsplit;
+    double* d_work;  // split partials, nsplit * N * 2 doubles
+};
+
+namespace ie {
+
+// Host-side log table in 80-bit arithmetic (see common.cuh).
+std::vector<LogEntry> build_log_table(const ie_geom& g, int* ntab_out) {
+    const long double s = (long double)g.spacing;
+    const long long mmax = (long long)g.dim * (long long)(g.n - 1) * (long long)(g.n - 1);
+    int emax = 0;
+    while ((1LL << (emax + 1)) <= mmax) ++emax;
+    const int ntab = (emax + 1) * kLogK;
+    std::vector<LogEntry> tab(ntab);
+    const long double ln2 = 0.693147180559945309417232121458176568L;
+    const long double two_log_s = 2.0L * logl(s);
+    for (int e = 0; e <= emax; ++e) {
+        for (int k = 0; k < kLogK; ++k) {
+            const double ck = 128.0 / (128.5 + (double)k);  // rounded once
+            const long double t = (long double)e * ln2 - logl((long double)ck) + two_log_s;
+            tab[e * kLogK + k] = LogEntry{ck, (double)t};
+        }
+    }
+    *ntab_out = ntab;
+    return tab;
+}
+
+EntryParams entry_params(const ie_geom& g) {
+    EntryParams P;
+    P.dim = g.dim;
+    P.diag = g.diag;
+    const double four_pi = 4.0 * M_PI;
+    P.alpha = (g.dim == 3) ? g.weight / (four_pi * g.spacing) : -g.weight / four_pi;
+    return P;
+}
+
+int make_log_table_device(const ie_geom& g, LogEntry** d_tab, int* ntab) {
+    std::vector<LogEntry> tab = build_log_table(g, ntab);
+    IE_CUDA(cudaMalloc(d_tab, tab.size() * sizeof(LogEntry)));
+    IE_CUDA(cudaMemcpy(*d_tab, tab.data(), tab.size() * sizeof(LogEntry), cudaMemcpyHostToDevice));
+    return IE_OK;
+}
+
+template <int DIM, int NRHS>
+static int launch_dim(const ie_matvec* m, MatvecArgs a, cudaStream_t st) {
+    const size_t smem = (DIM == 3 ? 0 : (size_t)m->ntab * sizeof(LogEntry)) + (size_t)m->TS * NRHS * sizeof(double);
+    const int threads = 256;
+    dim3 grid((a.nrows + threads * m->R - 1) / (threads * m->R), m->nsplit);
+    a.W = m->nsplit > 1 ? m->d_work : nullptr;
+    if (m->R == 2) {
+        auto kern = k_matvec<DIM, NRHS, 2>;
+        IE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kern<<<grid, threads, smem, st>>>(a);
+    } else {
+        auto kern = k_matvec<DIM, NRHS, 1>;
+        IE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kern<<<grid, threads, smem, st>>>(a);
+    }
+    IE_LAUNCHED();
+    if (m->nsplit > 1) {
+        k_matvec_reduce<DIM, NRHS><<<(a.nrows + 255) / 256, 256, 0, st>>>(a, m->nsplit);
+        IE_LAUNCHED();
+    }
+    return IE_OK;
+}
+
+int matvec_launch(const ie_matvec* m, const double* X, int64_t ldx, int nrhs, double* Y, int64_t ldy,
+                  int64_t row_begin, int64_t row_end, cudaStream_t st) {
+    MatvecArgs a;
+    a.X = X;
+    a.ldx = ldx;
+    a.Y = Y;
+    a.ldy = ldy;
+    a.W = nullptr;
+    a.tab = m->d_tab;
+    a.ntab = m->ntab;
+    a.n = m->g.n;
+    a.N = m->N;
+    a.row_begin = (int)row_begin;
+    a.nrows = (int)(row_end - row_begin);
+    a.TS = m->TS;
+    a.split_len = m->split_len;
+    a.alpha = m->alpha;
+    a.diag = m->g.diag;
+    if (a.nrows <= 0) return IE_OK;
+    switch (m->g.dim * 4 + nrhs) {
+        case 1 * 4 + 1: return launch_dim<1, 1>(m, a, st);
+        case 1 * 4 + 2: return launch_dim<1, 2>(m, a, st);
+        case 2 * 4 + 1: return launch_dim<2, 1>(m, a, st);
+        case 2 * 4 + 2: return launch_dim<2, 2>(m, a, st);
+        case 3 * 4 + 1: return launch_dim<3, 1>(m, a, st);
+        case 3 * 4 + 2: return launch_dim<3, 2>(m, a, st);
+    }
+    set_error("matvec: dim must be 1..3 and nrhs 1..2");
+    return IE_ERR_ARG;
+}
+
+// ---------------------------------------------------- assemble_block ----
+__global__ void k_assemble(int dim, int n, EntryParams P, const LogEntry* tab, const int64_t* rows,
+                           int64_t nr, const int64_t* cols, int64_t nc, double* out) {
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= nr * nc) return;
+    int64_t i = rows[e / nc], j = cols[e % nc];
+    int m = 0;
+    for (int d = 0; d < dim; ++d) {
+        const int dd = (int)(i % n) - (int)(j % n);
+        m += dd * dd;
+        i /= n;
+        j /= n;
+    }
+    out[e] = entry_from_m(P, tab, m);
+}
+
+}  // namespace ie
+
+extern "C" int ie_matvec_create(const ie_geom* g, ie_matvec** out) {
+    if (!g || !out || g->dim < 1 || g->dim > 3 || g->n < 2) {
+        ie::set_error("ie_matvec_create: bad geometry");
+        return IE_ERR_ARG;
+    }
+    const double Nd = pow((double)g->n, g->dim);
+    if (Nd >= 2147483647.0) {
+        ie::set_error("ie_matvec_create: N must be < 2^31");
+        return IE_ERR_ARG;
+    }
+    ie_matvec* m = new ie_matvec();
+    m->g = *g;
+    m->N = (int)Nd;
+    m->alpha = ie::entry_params(*g).alpha;
+    int rc = ie::make_log_table_device(*g, &m->d_tab, &m->ntab);
+    if (rc) {
+        delete m;
+        return rc;
+    }
+    // Launch plan from N only.
+    const int N = m->N;
+    m->R = N >= 131072 ? 2 : 1;
+    m->TS = N >= 65536 ? 1024 : 256;
+    const int tiles = (N + m->TS - 1) / m->TS;
+    const int ctas = (N + 256 * m->R - 1) / (256 * m->R);
+    int nsplit = (4 * ie::kNumSMs + ctas - 1) / ctas;
+    if (nsplit > tiles) nsplit = tiles;
+    if (nsplit < 1) nsplit = 1;
+    const int tiles_per_split = (tiles + nsplit - 1) / nsplit;
+    m->split_len = tiles_per_split * m->TS;
+    m->nsplit = (N + m->split_len - 1) / m->split_len;
+    m->d_work = nullptr;
+    if (m->nsplit > 1) {
+        cudaError_t e = cudaMalloc(&m->d_work, (size_t)m->nsplit * N * 2 * sizeof(double));
+        if (e != cudaSuccess) {
+            ie::set_error(std::string("ie_matvec_create: ") + cudaGetErrorString(e));
+            cudaFree(m->d_tab);
+            delete m;
+            return IE_ERR_CUDA;
+        }
+    }
+    *out = m;
+    return IE_OK;
+}
+
+extern "C" void ie_matvec_destroy(ie_matvec* m) {
+    if (!m) return;
+    cudaFree(m->d_tab);
+    if (m->d_work) cudaFree(m->d_work);
+    delete m;
+}
+
+extern "C" int ie_matvec_f64(const ie_matvec* m, const double* X, int64_t ldx, int32_t nrhs, double* Y,
+                             int64_t ldy, int64_t row_begin, int64_t row_end, void* stream) {
+    if (!m || !X || !Y || nrhs < 1 || nrhs > 2 || row_begin < 0 || row_end > m->N || row_begin > row_end ||
+        ldx < m->N || ldy < row_end - row_begin) {
+        ie::set_error("ie_matvec_f64: bad arguments");
+        return IE_ERR_ARG;
+    }
+    return ie::matvec_launch(m, X, ldx, nrhs, Y, ldy, row_begin, row_end, (cudaStream_t)stream);
+}
+
+extern "C" int ie_assemble_block_f64(const ie_geom* g, const int64_t* rows, int64_t nr, const int64_t* cols,
+                                     int64_t nc, double* out, void* stream) {
+    if (!g || g->dim < 1 || g->dim > 3 || nr < 0 || nc < 0) {
+        ie::set_error("ie_assemble_block_f64: bad arguments");
+        return IE_ERR_ARG;
+    }
+    if (nr == 0 || nc == 0) return IE_OK;
+    ie::LogEntry* tab;
+    int ntab;
+    int rc = ie::make_log_table_device(*g, &tab, &ntab);
+    if (rc) return rc;
+    const int64_t tot = nr * nc;
+    ie::k_assemble<<<(unsigned)((tot + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
+        g->dim, g->n, ie::entry_params(*g), tab, rows, nr, cols, nc, out);
+    cudaError_t e = cudaGetLastError();
+    ie::g_launches.fetch_add(1);
+    cudaStreamSynchronize((cudaStream_t)stream);
+    cudaFree(tab);
+    if (e != cudaSuccess) {
+        ie::set_error(cudaGetErrorString(e));
+        return IE_ERR_CUDA;
+    }
+    return IE_OK;
+}
+
+namespace ie {
+int matvec_N(const ie_matvec* m) { return m->N; }
+}  // namespace ie

@@ -1,0 +1,696 @@
+// K2 (block extraction + batched Cholesky) and K3 (Schwarz / block-Jacobi
+// apply) -- replaces precond.from_decomposition(backend="exact") and
+// Preconditioner.apply (/root/reference/pkg/src/iedd/precond.py:157-215,
+// :91-100) with linalg.cholesky / CholeskyFactor.solve (linalg.py:31-58).
+//
+// Build (one CTA per factorised block): gather the block's lattice points,
+// assemble A_k from integer distances (same entry formula as K1), factor
+// A_k = L L^T in place (right-looking, unblocked; in shared memory for
+// s <= kSmemMaxS, else in a global workspace), then
+//   variant PACKED_INVERSE: L^{-1} in place (LAPACK dtrti2 order) and
+//     A_k^{-1} = L^{-T} L^{-1}, stored as the packed upper triangle by columns
+//     (column j = A^{-1}[0..j, j] at j(j+1)/2);
+//   variant SUBST: G = L^T stored packed by rows (row i = G[i, i..s-1]) plus
+//     1/G_ii, for forward/back substitution.
+// Blocks whose point sets are translates of each other have bitwise equal
+// A_k (entries depend on integer differences only), so with
+// share_translated one representative per class is factorised.
+//
+// Apply: k_apply_* (one warp, or WPB warps, per block; lane-owned slots of
+// r_k and z_k in registers) writes z_k into a staging buffer; k_scatter sums,
+// per point, its <= 2^dim staged contributions in ascending block id starting
+// from 0.0 -- the reference's association order (precond.py:97-99), no
+// atomics.
+#include <math.h>
+
+#include <algorithm>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "common.cuh"
+
+namespace ie {
+
+std::vector<LogEntry> build_log_table(const ie_geom& g, int* ntab_out);
+EntryParams entry_params(const ie_geom& g);
+int make_log_table_device(const ie_geom& g, LogEntry** d_tab, int* ntab);
+int dot_chunks(int64_t n);
+
+constexpr int kSmemMaxS = 160;
+constexpr int kBuildThreads = 512;
+constexpr unsigned kFull = 0xffffffffu;
+
+struct BlockMeta {
+    int s;
+    int pad;
+    int64_t idx_off;  // into the per-block index pool (all D blocks)
+    int64_t fac_off;  // into the factor pool (aliased for translated blocks)
+    int64_t st_off;   // into the staging buffer
+};
+
+struct BuildArgs {
+    const int* idx;        // point indices of the factorised blocks
+    const int64_t* ioff;   // per factorised block
+    const int* sizes;
+    double* work;
+    const int64_t* wofs;   // workspace offset (-1: use shared memory)
+    double* fac;
+    const int64_t* fofs;
+    int* info;
+    const LogEntry* tab;
+    EntryParams P;
+    int n;
+    int dim;
+    int variant;
+};
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+    return v;
+}
+
+__global__ void __launch_bounds__(kBuildThreads) k_build(BuildArgs a) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int u = blockIdx.x;
+    const int s = a.sizes[u];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
+    int* coord = reinterpret_cast<int*>(smem);                              // s*3 ints
+    double* col = reinterpret_cast<double*>(smem + ((s * 3 * 4 + 15) / 16) * 16);  // s doubles
+    __shared__ int fail;
+    __shared__ double pivot;
+    double* A;
+    int lda;
+    if (a.wofs[u] < 0) {
+        A = col + s;
+        lda = s | 1;  // odd stride: column walks are bank-conflict free
+    } else {
+        A = a.work + a.wofs[u];
+        lda = s;
+    }
+    const int* idx = a.idx + a.ioff[u];
+    for (int p = tid; p < s; p += blockDim.x) {
+        int64_t gi = idx[p];
+        for (int d = a.dim - 1; d >= 0; --d) {
+            coord[p * 3 + d] = (int)(gi % a.n);
+            gi /= a.n;
+        }
+    }
+    if (tid == 0) fail = 0;
+    __syncthreads();
+    // assemble the lower triangle
+    for (int i = warp; i < s; i += nwarp) {
+        for (int k = lane; k <= i; k += 32) {
+            int m = 0;
+            for (int d = 0; d < a.dim; ++d) {
+                const int dd = coord[i * 3 + d] - coord[k * 3 + d];
+                m += dd * dd;
+            }
+            A[i * lda + k] = entry_from_m(a.P, a.tab, m);
+        }
+    }
+    __syncthreads();
+    // right-looking Cholesky, A = L L^T (LAPACK dpotf2 order: sqrt, scale by 1/ljj)
+    for (int j = 0; j < s; ++j) {
+        if (tid == 0) {
+            const double d = A[j * lda + j];
+            if (!(d > 0.0) || !isfinite(d)) {
+                fail = j + 1;
+            } else {
+                const double l = sqrt(d);
+                A[j * lda + j] = l;
+                pivot = 1.0 / l;
+            }
+        }
+        __syncthreads();
+        if (fail) break;
+        const double rp = pivot;
+        for (int i = j + 1 + tid; i < s; i += blockDim.x) {
+            const double v = A[i * lda + j] * rp;
+            A[i * lda + j] = v;
+            col[i] = v;
+        }
+        __syncthreads();
+        for (int i = j + 1 + warp; i < s; i += nwarp) {
+            const double lij = col[i];
+            for (int k = j + 1 + lane; k <= i; k += 32) A[i * lda + k] = fma(-lij, col[k], A[i * lda + k]);
+        }
+        __syncthreads();
+    }
+    if (fail) {
+        if (tid == 0) a.info[u] = fail;
+        return;
+    }
+    double* out = a.fac + a.fofs[u];
+    if (a.variant == IE_VARIANT_SUBST) {
+        // G = L^T packed by rows: row i = L[i..s-1][i] at i*s - i(i-1)/2; then 1/G_ii
+        for (int i = warp; i < s; i += nwarp) {
+            const int64_t off = (int64_t)i * s - (int64_t)i * (i - 1) / 2;
+            for (int k = i + lane; k < s; k += 32) out[off + (k - i)] = A[k * lda + i];
+        }
+        const int64_t dofs = (int64_t)s * (s + 1) / 2;
+        for (int i = tid; i < s; i += blockDim.x) out[dofs + i] = 1.0 / A[i * lda + i];
+        if (tid == 0) a.info[u] = 0;
+        return;
+    }
+    // L^{-1} in place (dtrti2, lower, non-unit)
+    for (int j = s - 1; j >= 0; --j) {
+        if (tid == 0) A[j * lda + j] = 1.0 / A[j * lda + j];
+        for (int i = j + 1 + tid; i < s; i += blockDim.x) col[i] = A[i * lda + j];
+        __syncthreads();
+        const double ajj = -A[j * lda + j];
+        for (int i = j + 1 + warp; i < s; i += nwarp) {
+            double x = 0.0;
+            for (int k = j + 1 + lane; k <= i; k += 32) x = fma(A[i * lda + k], col[k], x);
+            x = warp_sum(x);
+            if (lane == 0) A[i * lda + j] = ajj * x;
+        }
+        __syncthreads();
+    }
+    // A^{-1} = L^{-T} L^{-1}; lower element (i, j<=i) = sum_{k>=i} Li[k][i] Li[k][j]
+    const int64_t ntri = (int64_t)s * (s + 1) / 2;
+    for (int64_t p = tid; p < ntri; p += blockDim.x) {
+        int i = (int)((sqrt(8.0 * (double)p + 1.0) - 1.0) * 0.5);
+        while ((int64_t)i * (i + 1) / 2 > p) --i;
+        while ((int64_t)(i + 1) * (i + 2) / 2 <= p) ++i;
+        const int j = (int)(p - (int64_t)i * (i + 1) / 2);
+        double acc = 0.0;
+        for (int k = i; k < s; ++k) acc = fma(A[k * lda + i], A[k * lda + j], acc);
+        out[p] = acc;
+    }
+    if (tid == 0) a.info[u] = 0;
+}
+
+struct ApplyArgs {
+    const double* r;
+    double* staging;
+    const BlockMeta* meta;
+    const int* idx;
+    const double* fac;
+    int64_t D;
+    int wpb;  // warps per block
+    int bpc;  // blocks per CTA
+};
+
+// z_k = A_k^{-1} r_k with the packed upper triangle by columns: column j
+// contributes its dot with r[0..j] to z_j and r_j * A[0..j-1, j] to z[0..j-1].
+template <int T>
+__global__ void __launch_bounds__(256) k_apply_packed(ApplyArgs a) {
+    extern __shared__ double red[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int bl = warp / a.wpb, w = warp % a.wpb;
+    const int64_t k = (int64_t)blockIdx.x * a.bpc + bl;
+    const bool active = k < a.D;
+    BlockMeta bm;
+    if (active) bm = a.meta[k]; else bm.s = 0;
+    const int s = bm.s;
+    const int* idx = a.idx + (active ? bm.idx_off : 0);
+    const double* fac = a.fac + (active ? bm.fac_off : 0);
+    double rr[T], zz[T];
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+        const int i = 32 * t + lane;
+        rr[t] = (i < s) ? __ldg(a.r + idx[i]) : 0.0;
+        zz[t] = 0.0;
+    }
+#pragma unroll
+    for (int tj = 0; tj < T; ++tj) {
+        if (32 * tj < s) {
+            for (int jj = w; jj < 32; jj += a.wpb) {
+                const int j = 32 * tj + jj;
+                if (j >= s) break;
+                const double* colp = fac + ((int64_t)j * (j + 1)) / 2;
+                const double rj = __shfl_sync(kFull, rr[tj], jj);
+                double d = 0.0;
+#pragma unroll
+                for (int t = 0; t <= tj; ++t) {
+                    const int i = 32 * t + lane;
+                    if (t < tj || lane <= jj) {
+                        const double v = __ldg(colp + i);
+                        d = fma(v, rr[t], d);
+                        if (t < tj || lane < jj) zz[t] = fma(v, rj, zz[t]);
+                    }
+                }
+                d = warp_sum(d);
+                if (lane == jj) zz[tj] += d;
+            }
+        }
+    }
+    if (a.wpb == 1) {
+        if (active) {
+#pragma unroll
+            for (int t = 0; t < T; ++t) {
+                const int i = 32 * t + lane;
+                if (i < s) a.staging[bm.st_off + i] = zz[t];
+            }
+        }
+        return;
+    }
+    double* my = red + ((int64_t)(bl * a.wpb + w) * T) * 32;
+#pragma unroll
+    for (int t = 0; t < T; ++t) my[t * 32 + lane] = zz[t];
+    __syncthreads();
+    if (active && w == 0) {
+        const double* base = red + (int64_t)bl * a.wpb * T * 32;
+        for (int i = lane; i < s; i += 32) {
+            double acc = 0.0;
+            for (int q = 0; q < a.wpb; ++q) acc += base[(int64_t)q * T * 32 + i];
+            a.staging[bm.st_off + i] = acc;
+        }
+    }
+}
+
+// Forward (G^T y = r, row-axpy form) and back (G x = y, row-dot form)
+// substitution with the row-packed upper factor; one warp per block.
+template <int T>
+__global__ void __launch_bounds__(128) k_apply_subst(ApplyArgs a) {
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t k = (int64_t)blockIdx.x * a.bpc + warp;
+    if (k >= a.D) return;
+    const BlockMeta bm = a.meta[k];
+    const int s = bm.s;
+    const int* idx = a.idx + bm.idx_off;
+    const double* G = a.fac + bm.fac_off;
+    const double* rdiag = G + (int64_t)s * (s + 1) / 2;
+    double b[T];
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+        const int i = 32 * t + lane;
+        b[t] = (i < s) ? __ldg(a.r + idx[i]) : 0.0;
+    }
+    // forward: y_i = b_i / G_ii; b_j -= G_ij y_i (j > i)
+#pragma unroll
+    for (int ti = 0; ti < T; ++ti) {
+        if (32 * ti < s) {
+            for (int ii = 0; ii < 32; ++ii) {
+                const int i = 32 * ti + ii;
+                if (i >= s) break;
+                const double yi = __shfl_sync(kFull, b[ti], ii) * __ldg(rdiag + i);
+                const double* row = G + (int64_t)i * s - (int64_t)i * (i - 1) / 2 - i;  // row[j] = G[i][j]
+#pragma unroll
+                for (int t = ti; t < T; ++t) {
+                    const int j = 32 * t + lane;
+                    if (j > i && j < s) b[t] = fma(-__ldg(row + j), yi, b[t]);
+                }
+                if (lane == ii) b[ti] = yi;
+            }
+        }
+    }
+    // back: x_i = (y_i - sum_{j>i} G_ij x_j) / G_ii, i descending
+#pragma unroll
+    for (int ti = T - 1; ti >= 0; --ti) {
+        if (32 * ti < s) {
+            for (int ii = 31; ii >= 0; --ii) {
+                const int i = 32 * ti + ii;
+                if (i >= s) continue;
+                const double* row = G + (int64_t)i * s - (int64_t)i * (i - 1) / 2 - i;
+                double d = 0.0;
+#pragma unroll
+                for (int t = ti; t < T; ++t) {
+                    const int j = 32 * t + lane;
+                    if (j > i && j < s) d = fma(__ldg(row + j), b[t], d);
+                }
+                d = warp_sum(d);
+                if (lane == ii) b[ti] = (b[ti] - d) * __ldg(rdiag + i);
+            }
+        }
+    }
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+        const int i = 32 * t + lane;
+        if (i < s) a.staging[bm.st_off + i] = b[t];
+    }
+}
+
+// Per point: z_i = sum of its staged contributions in ascending block id.
+// Optionally also the fixed-chunk partials of r.z (for PCG's rho).
+constexpr int kChunk = 2048;
+__global__ void __launch_bounds__(256) k_scatter(const double* staging, const int* ptr, const int* pos, double* z,
+                                                 int N, const double* r, double* partials) {
+    __shared__ double sh[256];
+    const int base = blockIdx.x * kChunk;
+    double loc = 0.0;
+#pragma unroll
+    for (int e = 0; e < kChunk / 256; ++e) {
+        const int i = base + e * 256 + threadIdx.x;
+        if (i < N) {
+            double acc = 0.0;
+            for (int q = ptr[i]; q < ptr[i + 1]; ++q) acc += staging[pos[q]];
+            z[i] = acc;
+            if (r) loc = fma(r[i], acc, loc);
+        }
+    }
+    if (!r) return;
+    sh[threadIdx.x] = loc;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) partials[blockIdx.x] = sh[0];
+}
+
+}  // namespace ie
+
+// ------------------------------------------------------------- host side --
+struct ie_precond {
+    ie_geom g;
+    int N;
+    int64_t D;
+    int variant;
+    int smax;
+    int64_t ref_mem_bytes;
+    int64_t fac_bytes;
+    int64_t n_factored;
+    int64_t total_s;
+    ie::BlockMeta* d_meta;
+    int* d_idx;
+    double* d_fac;
+    double* d_staging;
+    int* d_ptr;
+    int* d_pos;
+    int T;
+    int wpb;
+    int bpc;
+};
+
+namespace ie {
+
+static int slots_for(int smax) {
+    const int t = (smax + 31) / 32;
+    const int opts[] = {1, 2, 3, 4, 5, 8, 16, 32};
+    for (int o : opts)
+        if (t <= o) return o;
+    return -1;
+}
+
+template <int T>
+static void launch_apply_T(const ie_precond* p, ApplyArgs a, cudaStream_t st) {
+    const int ctas = (int)((p->D + p->bpc - 1) / p->bpc);
+    if (p->variant == IE_VARIANT_SUBST) {
+        k_apply_subst<T><<<ctas, 32 * p->bpc, 0, st>>>(a);
+    } else {
+        const size_t sm = p->wpb > 1 ? (size_t)p->bpc * p->wpb * T * 32 * sizeof(double) : 0;
+        if (sm > 48 * 1024) cudaFuncSetAttribute(k_apply_packed<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        k_apply_packed<T><<<ctas, 32 * p->wpb * p->bpc, sm, st>>>(a);
+    }
+}
+
+int precond_apply(const ie_precond* p, const double* r, double* z, double* partials, cudaStream_t st) {
+    ApplyArgs a;
+    a.r = r;
+    a.staging = p->d_staging;
+    a.meta = p->d_meta;
+    a.idx = p->d_idx;
+    a.fac = p->d_fac;
+    a.D = p->D;
+    a.wpb = p->wpb;
+    a.bpc = p->bpc;
+    switch (p->T) {
+        case 1: launch_apply_T<1>(p, a, st); break;
+        case 2: launch_apply_T<2>(p, a, st); break;
+        case 3: launch_apply_T<3>(p, a, st); break;
+        case 4: launch_apply_T<4>(p, a, st); break;
+        case 5: launch_apply_T<5>(p, a, st); break;
+        case 8: launch_apply_T<8>(p, a, st); break;
+        case 16: launch_apply_T<16>(p, a, st); break;
+        case 32: launch_apply_T<32>(p, a, st); break;
+        default: set_error("apply: unsupported block size"); return IE_ERR_ARG;
+    }
+    IE_LAUNCHED();
+    const int nch = (p->N + kChunk - 1) / kChunk;
+    k_scatter<<<nch, 256, 0, st>>>(p->d_staging, p->d_ptr, p->d_pos, z, p->N, partials ? r : nullptr, partials);
+    IE_LAUNCHED();
+    return IE_OK;
+}
+
+}  // namespace ie
+
+extern "C" void ie_precond_destroy(ie_precond* p) {
+    if (!p) return;
+    cudaFree(p->d_meta);
+    cudaFree(p->d_idx);
+    cudaFree(p->d_fac);
+    cudaFree(p->d_staging);
+    cudaFree(p->d_ptr);
+    cudaFree(p->d_pos);
+    delete p;
+}
+
+#define IE_CHECK_BUILD(call)                                                      \
+    do {                                                                          \
+        cudaError_t _e = (call);                                                  \
+        if (_e != cudaSuccess) {                                                  \
+            ie::set_error(std::string(#call) + ": " + cudaGetErrorString(_e));    \
+            for (void* q : tmp) cudaFree(q);                                      \
+            ie_precond_destroy(p);                                                \
+            return IE_ERR_CUDA;                                                   \
+        }                                                                         \
+    } while (0)
+
+extern "C" int ie_precond_create(const ie_geom* g, const int64_t* h_offsets, const int64_t* h_indices, int64_t D,
+                                 int32_t variant, int32_t share_translated, ie_precond** out, int64_t* bad_block,
+                                 void* stream) {
+    if (!g || !h_offsets || !out || D < 1 || g->dim < 1 || g->dim > 3 ||
+        (variant != IE_VARIANT_PACKED_INVERSE && variant != IE_VARIANT_SUBST)) {
+        ie::set_error("ie_precond_create: bad arguments");
+        return IE_ERR_ARG;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    int64_t N = 1;
+    for (int d = 0; d < g->dim; ++d) N *= g->n;
+    // --- host bookkeeping: validation, translation classes, scatter CSR
+    std::vector<int> sizes(D);
+    int smax = 0;
+    int64_t total = 0, refmem = 0;
+    for (int64_t k = 0; k < D; ++k) {
+        const int64_t s = h_offsets[k + 1] - h_offsets[k];
+        if (s < 1 || s > (1 << 20)) {
+            ie::set_error("ie_precond_create: empty or oversized subdomain");
+            return IE_ERR_ARG;
+        }
+        for (int64_t q = h_offsets[k]; q < h_offsets[k + 1]; ++q) {
+            if (h_indices[q] < 0 || h_indices[q] >= N || (q > h_offsets[k] && h_indices[q] <= h_indices[q - 1])) {
+                ie::set_error("ie_precond_create: subdomain indices must be sorted, unique and in range");
+                return IE_ERR_ARG;
+            }
+        }
+        sizes[k] = (int)s;
+        smax = std::max(smax, (int)s);
+        total += s;
+        refmem += 8 * (s * s + s);
+    }
+    const int T = ie::slots_for(smax);
+    if (T < 0) {
+        ie::set_error("ie_precond_create: subdomains larger than 1024 points are not supported");
+        return IE_ERR_ARG;
+    }
+    // translation classes: signature = multi-index offsets from the first point
+    std::vector<int64_t> rep(D);
+    std::vector<int64_t> uniq;
+    {
+        std::unordered_map<std::string, int64_t> cls;
+        std::vector<int> sig;
+        for (int64_t k = 0; k < D; ++k) {
+            if (!share_translated) {
+                rep[k] = (int64_t)uniq.size();
+                uniq.push_back(k);
+                continue;
+            }
+            sig.clear();
+            sig.push_back(sizes[k]);
+            int64_t first = h_indices[h_offsets[k]];
+            int f[3];
+            {
+                int64_t t = first;
+                for (int d = g->dim - 1; d >= 0; --d) { f[d] = (int)(t % g->n); t /= g->n; }
+            }
+            for (int64_t q = h_offsets[k]; q < h_offsets[k + 1]; ++q) {
+                int64_t t = h_indices[q];
+                for (int d = g->dim - 1; d >= 0; --d) {
+                    sig.push_back((int)(t % g->n) - f[d]);
+                    t /= g->n;
+                }
+            }
+            std::string key(reinterpret_cast<const char*>(sig.data()), sig.size() * sizeof(int));
+            auto it = cls.find(key);
+            if (it == cls.end()) {
+                cls.emplace(key, (int64_t)uniq.size());
+                rep[k] = (int64_t)uniq.size();
+                uniq.push_back(k);
+            } else {
+                rep[k] = it->second;
+            }
+        }
+    }
+    const int64_t U = (int64_t)uniq.size();
+    auto fac_len = [&](int s) -> int64_t {
+        return (int64_t)s * (s + 1) / 2 + (variant == IE_VARIANT_SUBST ? s : 0);
+    };
+    std::vector<int64_t> ufofs(U), uioff(U), uwofs(U);
+    std::vector<int> usizes(U);
+    int64_t facn = 0, idxn = 0, workn = 0;
+    for (int64_t u = 0; u < U; ++u) {
+        const int s = sizes[uniq[u]];
+        usizes[u] = s;
+        ufofs[u] = facn;
+        facn += (fac_len(s) + 31) / 32 * 32;  // 256 B aligned factors
+        uioff[u] = idxn;
+        idxn += s;
+        if (s > ie::kSmemMaxS) {
+            uwofs[u] = workn;
+            workn += (int64_t)s * s;
+        } else {
+            uwofs[u] = -1;
+        }
+    }
+    std::vector<int> uidx(idxn);
+    for (int64_t u = 0; u < U; ++u) {
+        const int64_t k = uniq[u];
+        for (int q = 0; q < sizes[k]; ++q) uidx[uioff[u] + q] = (int)h_indices[h_offsets[k] + q];
+    }
+    std::vector<ie::BlockMeta> meta(D);
+    std::vector<int> allidx(total);
+    std::vector<int> cnt(N + 1, 0);
+    {
+        int64_t off = 0;
+        for (int64_t k = 0; k < D; ++k) {
+            meta[k].s = sizes[k];
+            meta[k].pad = 0;
+            meta[k].idx_off = off;
+            meta[k].fac_off = ufofs[rep[k]];
+            meta[k].st_off = off;
+            for (int q = 0; q < sizes[k]; ++q) {
+                const int gi = (int)h_indices[h_offsets[k] + q];
+                allidx[off + q] = gi;
+                cnt[gi + 1]++;
+            }
+            off += sizes[k];
+        }
+    }
+    for (int64_t i = 0; i < N; ++i) cnt[i + 1] += cnt[i];
+    std::vector<int> pos(total);
+    {
+        std::vector<int> fill(cnt.begin(), cnt.end() - 1);
+        for (int64_t q = 0; q < total; ++q) pos[fill[allidx[q]]++] = (int)q;  // ascending block id
+    }
+
+    ie_precond* p = new ie_precond();
+    p->g = *g;
+    p->N = (int)N;
+    p->D = D;
+    p->variant = variant;
+    p->smax = smax;
+    p->ref_mem_bytes = refmem;
+    p->fac_bytes = facn * 8;
+    p->n_factored = U;
+    p->total_s = total;
+    p->T = T;
+    if (smax <= ie::kSmemMaxS) {
+        p->wpb = 1;
+        p->bpc = 4;
+    } else {
+        p->wpb = (variant == IE_VARIANT_SUBST) ? 1 : 8;
+        p->bpc = 1;
+    }
+    std::vector<void*> tmp;
+    IE_CHECK_BUILD(cudaMalloc(&p->d_meta, D * sizeof(ie::BlockMeta)));
+    IE_CHECK_BUILD(cudaMalloc(&p->d_idx, total * sizeof(int)));
+    IE_CHECK_BUILD(cudaMalloc(&p->d_fac, std::max<int64_t>(facn, 1) * sizeof(double)));
+    IE_CHECK_BUILD(cudaMalloc(&p->d_staging, total * sizeof(double)));
+    IE_CHECK_BUILD(cudaMalloc(&p->d_ptr, (N + 1) * sizeof(int)));
+    IE_CHECK_BUILD(cudaMalloc(&p->d_pos, total * sizeof(int)));
+    IE_CHECK_BUILD(cudaMemcpyAsync(p->d_meta, meta.data(), D * sizeof(ie::BlockMeta), cudaMemcpyHostToDevice, st));
+    IE_CHECK_BUILD(cudaMemcpyAsync(p->d_idx, allidx.data(), total * sizeof(int), cudaMemcpyHostToDevice, st));
+    IE_CHECK_BUILD(cudaMemcpyAsync(p->d_ptr, cnt.data(), (N + 1) * sizeof(int), cudaMemcpyHostToDevice, st));
+    IE_CHECK_BUILD(cudaMemcpyAsync(p->d_pos, pos.data(), total * sizeof(int), cudaMemcpyHostToDevice, st));
+
+    // --- factorise the representatives
+    int *d_uidx, *d_usz, *d_info;
+    int64_t *d_uioff, *d_ufofs, *d_uwofs;
+    double* d_work = nullptr;
+    ie::LogEntry* d_tab;
+    int ntab;
+    IE_CHECK_BUILD(cudaMalloc(&d_uidx, idxn * sizeof(int)));
+    tmp.push_back(d_uidx);
+    IE_CHECK_BUILD(cudaMalloc(&d_usz, U * sizeof(int)));
+    tmp.push_back(d_usz);
+    IE_CHECK_BUILD(cudaMalloc(&d_info, U * sizeof(int)));
+    tmp.push_back(d_info);
+    IE_CHECK_BUILD(cudaMalloc(&d_uioff, U * sizeof(int64_t)));
+    tmp.push_back(d_uioff);
+    IE_CHECK_BUILD(cudaMalloc(&d_ufofs, U * sizeof(int64_t)));
+    tmp.push_back(d_ufofs);
+    IE_CHECK_BUILD(cudaMalloc(&d_uwofs, U * sizeof(int64_t)));
+    tmp.push_back(d_uwofs);
+    if (workn) {
+        IE_CHECK_BUILD(cudaMalloc(&d_work, workn * sizeof(double)));
+        tmp.push_back(d_work);
+    }
+    if (ie::make_log_table_device(*g, &d_tab, &ntab) != IE_OK) {
+        for (void* q : tmp) cudaFree(q);
+        ie_precond_destroy(p);
+        return IE_ERR_CUDA;
+    }
+    tmp.push_back(d_tab);
+    IE_CHECK_BUILD(cudaMemcpyAsync(d_uidx, uidx.data(), idxn * sizeof(int), cudaMemcpyHostToDevice, st));
+    IE_CHECK_BUILD(cudaMemcpyAsync(d_usz, usizes.data(), U * sizeof(int), cudaMemcpyHostToDevice, st));
+    IE_CHECK_BUILD(cudaMemcpyAsync(d_uioff, uioff.data(), U * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    IE_CHECK_BUILD(cudaMemcpyAsync(d_ufofs, ufofs.data(), U * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    IE_CHECK_BUILD(cudaMemcpyAsync(d_uwofs, uwofs.data(), U * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    ie::BuildArgs ba;
+    ba.idx = d_uidx;
+    ba.ioff = d_uioff;
+    ba.sizes = d_usz;
+    ba.work = d_work;
+    ba.wofs = d_uwofs;
+    ba.fac = p->d_fac;
+    ba.fofs = d_ufofs;
+    ba.info = d_info;
+    ba.tab = d_tab;
+    ba.P = ie::entry_params(*g);
+    ba.n = g->n;
+    ba.dim = g->dim;
+    ba.variant = variant;
+    const int sm_s = std::min(smax, ie::kSmemMaxS);
+    const size_t smem = ((size_t)sm_s * 3 * 4 + 15) / 16 * 16 + (size_t)sm_s * 8 +
+                        (smax <= ie::kSmemMaxS ? (size_t)sm_s * (sm_s | 1) * 8 : 0) +
+                        (smax > ie::kSmemMaxS ? ((size_t)smax * 3 * 4 + 15) / 16 * 16 + (size_t)smax * 8 : 0);
+    IE_CHECK_BUILD(cudaFuncSetAttribute(ie::k_build, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    ie::k_build<<<(unsigned)U, ie::kBuildThreads, smem, st>>>(ba);
+    IE_CHECK_BUILD(cudaGetLastError());
+    ie::g_launches.fetch_add(1);
+    std::vector<int> info(U);
+    IE_CHECK_BUILD(cudaMemcpyAsync(info.data(), d_info, U * sizeof(int), cudaMemcpyDeviceToHost, st));
+    IE_CHECK_BUILD(cudaStreamSynchronize(st));
+    for (void* q : tmp) cudaFree(q);
+    for (int64_t k = 0; k < D; ++k) {
+        if (info[rep[k]] != 0) {
+            if (bad_block) *bad_block = k;
+            ie_precond_destroy(p);
+            ie::set_error("subdomain Cholesky hit a non-positive pivot");
+            return IE_ERR_NOT_SPD;
+        }
+    }
+    *out = p;
+    return IE_OK;
+}
+
+extern "C" int ie_precond_apply_f64(const ie_precond* p, const double* r, double* z, void* stream) {
+    if (!p || !r || !z) {
+        ie::set_error("ie_precond_apply_f64: bad arguments");
+        return IE_ERR_ARG;
+    }
+    return ie::precond_apply(p, r, z, nullptr, (cudaStream_t)stream);
+}
+
+extern "C" int ie_precond_stats(const ie_precond* p, int64_t* out5) {
+    if (!p || !out5) return IE_ERR_ARG;
+    out5[0] = p->smax;
+    out5[1] = p->ref_mem_bytes;
+    out5[2] = p->fac_bytes;
+    out5[3] = p->n_factored;
+    out5[4] = p->D;
+    return IE_OK;
+}

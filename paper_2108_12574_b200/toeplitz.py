@@ -1,0 +1,96 @@
+"""Matrix-free operator application y = A x on the GPU.
+
+Drop-in for the reference's ToeplitzMatvec (/root/reference/pkg/src/iedd/
+toeplitz.py:11-57): same constructor argument, ``shape``, ``matvec`` (1-D
+float64 array of length N in, fresh array out, ValueError mentioning
+"length" otherwise) and ``@``.  The reference evaluates A x by circulant
+FFT; here K1 (csrc/matvec.cu) evaluates the log-r / 1/r kernel on the fly
+for every pair (BASELINE.json north star, component (1)).
+
+Device API: ``matvec_device(X, Y, nrhs, row_begin, row_end)`` takes torch
+CUDA float64 tensors and enqueues on the current stream without a host sync.
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+
+from . import _lib
+from .kernel import KernelOperator
+
+
+def to_device_vector(v, n: int):
+    """(torch CUDA float64 tensor, was_numpy).  Validates length n."""
+    torch = _lib.torch_cuda()
+    if isinstance(v, torch.Tensor):
+        if v.shape != (n,):
+            raise ValueError(f"expected vector of length {n}, got shape {tuple(v.shape)}")
+        t = v.to(device="cuda", dtype=torch.float64).contiguous()
+        return t, False
+    a = np.asarray(v, dtype=float)
+    if a.shape != (n,):
+        raise ValueError(f"expected vector of length {n}, got shape {a.shape}")
+    return torch.from_numpy(np.ascontiguousarray(a)).to("cuda", non_blocking=False), True
+
+
+def to_host(t, was_numpy: bool):
+    return t.cpu().numpy() if was_numpy else t
+
+
+class KernelMatvec:
+    """Direct-sum FP64 matvec with the kernel evaluated on the fly (K1)."""
+
+    def __init__(self, op: KernelOperator):
+        self.op = op
+        self.dim = op.grid.dim
+        self.n = op.grid.n_per_dim
+        self.N = op.n
+        self._lib = _lib.lib()
+        h = ctypes.c_void_p()
+        _lib.check(self._lib.ie_matvec_create(op.geom(), ctypes.byref(h)), "ToeplitzMatvec")
+        self._handle = h
+
+    def __del__(self):
+        h = getattr(self, "_handle", None)
+        if h is not None and h.value:
+            self._lib.ie_matvec_destroy(h)
+            self._handle = None
+
+    @property
+    def handle(self):
+        return self._handle
+
+    @property
+    def shape(self) -> tuple:
+        return (self.N, self.N)
+
+    def matvec_device(self, X, Y, nrhs: int = 1, row_begin: int = 0, row_end: int | None = None,
+                      ldx: int | None = None, ldy: int | None = None):
+        """Y[:, c] = A[row_begin:row_end] X[:, c] for c < nrhs, columns at
+        stride ldx / ldy (default N / row count).  No host synchronisation."""
+        row_end = self.N if row_end is None else row_end
+        ldx = self.N if ldx is None else ldx
+        ldy = (row_end - row_begin) if ldy is None else ldy
+        rc = self._lib.ie_matvec_f64(self._handle, _lib.ptr(X), ldx, nrhs, _lib.ptr(Y), ldy,
+                                     row_begin, row_end, _lib.stream_ptr())
+        _lib.check(rc, "matvec")
+        return Y
+
+    def matvec(self, v):
+        x, was_np = to_device_vector(v, self.N)
+        torch = _lib.torch_cuda()
+        y = torch.empty_like(x)
+        self.matvec_device(x, y)
+        return to_host(y, was_np)
+
+    def __matmul__(self, v):
+        return self.matvec(v)
+
+
+ToeplitzMatvec = KernelMatvec
+
+
+def build_matvec(op: KernelOperator) -> KernelMatvec:
+    return KernelMatvec(op)

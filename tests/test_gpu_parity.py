@@ -1,0 +1,372 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle and
+the golden vectors frozen from the reference.  Contract:
+  * matvec vs FFT / dense:            <= 1e-12 relative (2-norm)
+  * apply vs Preconditioner.apply:    <= 1e-12 relative
+  * PCG: n_it within +-1, solution <= 1e-10 relative (converged configs),
+         first 10 history entries <= 1e-6 relative
+  * Lanczos lambda:                   <= 1e-8 relative
+  * c5 (50 non-converged iterations): first 10 history <= 1e-8, u50 <= 1e-4,
+         final residual within 2x.
+"""
+
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle import iedd_oracle as O
+
+from .conftest import GOLDEN
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def ie():
+    import paper_2108_12574_b200 as pkg
+    return pkg
+
+
+def rel(a, b):
+    return np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(np.asarray(b))
+
+
+MV_CASES = ["2_8_span", "2_32_span", "2_16_cell", "3_8_cell", "1_16_cell", "2_32_cell", "3_4_cell",
+            "2_12_cell", "2_10_span"]
+
+
+class TestMatvec:
+    @pytest.mark.parametrize("case", MV_CASES)
+    def test_vs_golden(self, ie, golden, case):
+        g = golden("ref_small")
+        dim, n, lat = case.split("_")
+        op = ie.build_operator(ie.build_grid(int(dim), int(n)), lattice=lat)
+        mv = ie.ToeplitzMatvec(op)
+        x = g[f"mv_{case}_x"]
+        y = mv.matvec(x)
+        assert rel(y, g[f"mv_{case}_y"]) <= 1e-12
+        assert rel(y, g[f"mv_{case}_ydense"]) <= 1e-12
+
+    @pytest.mark.parametrize("case", MV_CASES)
+    def test_entries(self, ie, golden, case):
+        g = golden("ref_small")
+        dim, n, lat = case.split("_")
+        op = ie.build_operator(ie.build_grid(int(dim), int(n)), lattice=lat)
+        row0 = op.assemble_block(np.array([0]), np.arange(op.n))[0]
+        ref = g[f"mv_{case}_row0"]
+        assert np.max(np.abs(row0 - ref) / np.abs(ref).max()) <= 1e-14
+        assert row0[0] == op.diag_value
+
+    def test_dense_symmetric_and_oracle(self, ie):
+        op = ie.build_operator(ie.build_grid(2, 16), lattice="cell")
+        a = op.dense()
+        assert np.array_equal(a, a.T)
+        ref = O.build_operator(O.build_grid(2, 16), "cell").dense()
+        assert np.max(np.abs(a - ref)) <= 1e-14 * np.max(np.abs(ref))
+
+    @pytest.mark.parametrize("dim,n", [(2, 32), (2, 256), (3, 16), (1, 64)])
+    def test_two_rhs_and_row_ranges_bitwise(self, ie, dim, n):
+        import torch
+        op = ie.build_operator(ie.build_grid(dim, n), lattice="cell")
+        mv = ie.ToeplitzMatvec(op)
+        N = op.n
+        rng = np.random.default_rng(5)
+        X = torch.from_numpy(rng.standard_normal((2, N))).cuda()
+        Y2 = torch.empty_like(X)
+        mv.matvec_device(X, Y2, nrhs=2)
+        y0 = torch.empty(N, dtype=torch.float64, device="cuda")
+        y1 = torch.empty_like(y0)
+        mv.matvec_device(X[0], y0)
+        mv.matvec_device(X[1], y1)
+        assert torch.equal(Y2[0], y0) and torch.equal(Y2[1], y1)
+        # row-sharded evaluation (what each rank computes) is bitwise the same
+        for G in (2, 3, 8):
+            cuts = [N * g // G for g in range(G + 1)]
+            parts = []
+            for g in range(G):
+                yy = torch.empty(cuts[g + 1] - cuts[g], dtype=torch.float64, device="cuda")
+                mv.matvec_device(X[0], yy, row_begin=cuts[g], row_end=cuts[g + 1])
+                parts.append(yy)
+            assert torch.equal(torch.cat(parts), y0)
+
+    def test_matches_fft_large(self, ie):
+        # config-3 operator: 65,536 rows
+        op = ie.build_operator(ie.build_grid(2, 256), lattice="cell")
+        x = np.random.default_rng(1).standard_normal(op.n)
+        y = ie.ToeplitzMatvec(op).matvec(x)
+        yr = O.FFTMatvec(O.build_operator(O.build_grid(2, 256), "cell")).matvec(x)
+        assert rel(y, yr) <= 1e-12
+
+    def test_length_error(self, ie):
+        mv = ie.ToeplitzMatvec(ie.build_operator(ie.build_grid(2, 8)))
+        with pytest.raises(ValueError, match="length"):
+            mv.matvec(np.zeros(63))
+
+    def test_linearity_symmetry(self, ie, rng):
+        mv = ie.ToeplitzMatvec(ie.build_operator(ie.build_grid(3, 4)))
+        u, v = rng.standard_normal(64), rng.standard_normal(64)
+        lhs = mv.matvec(2.5 * u - 0.3 * v)
+        assert rel(lhs, 2.5 * mv.matvec(u) - 0.3 * mv.matvec(v)) <= 1e-13
+        mv2 = ie.ToeplitzMatvec(ie.build_operator(ie.build_grid(2, 16)))
+        a, b = rng.standard_normal(256), rng.standard_normal(256)
+        l, r = mv2.matvec(a) @ b, a @ mv2.matvec(b)
+        assert abs(l - r) <= 1e-12 * max(abs(l), abs(r))
+
+
+AP_CASES = ["2_32_4_1_schwarz_cell", "2_32_4_1_jacobi_cell", "2_16_2_1_schwarz_span", "3_8_2_1_schwarz_cell",
+            "2_64_8_2_schwarz_cell", "2_12_3_1_schwarz_cell"]
+
+
+class TestApply:
+    @pytest.mark.parametrize("case", AP_CASES)
+    @pytest.mark.parametrize("variant", ["packed_inverse", "subst"])
+    @pytest.mark.parametrize("share", [True, False])
+    def test_vs_golden(self, ie, golden, case, variant, share):
+        g = golden("ref_small")
+        dim, n, m, w, kind, lat = case.split("_")
+        grid = ie.build_grid(int(dim), int(n))
+        op = ie.build_operator(grid, lattice=lat)
+        pre = ie.from_decomposition(op, ie.build_decomposition(grid, int(m), int(w), kind), variant=variant,
+                                    share_translated=share)
+        z = pre.apply(g[f"ap_{case}_r"])
+        assert rel(z, g[f"ap_{case}_z"]) <= 1e-12
+
+    def test_share_is_bitwise_exact(self, ie, rng):
+        grid = ie.build_grid(2, 64)
+        op = ie.build_operator(grid, lattice="cell")
+        d = ie.build_decomposition(grid, 8, 2, "schwarz")
+        a = ie.from_decomposition(op, d, share_translated=True)
+        b = ie.from_decomposition(op, d, share_translated=False)
+        assert a.stats()["factored_blocks"] < b.stats()["factored_blocks"] == 64
+        r = rng.standard_normal(op.n)
+        assert np.array_equal(a.apply(r), b.apply(r))
+
+    def test_identity_and_errors(self, ie, rng):
+        pre = ie.identity(16)
+        f = rng.standard_normal(16)
+        assert np.array_equal(pre.apply(f), f)
+        grid = ie.build_grid(2, 16)
+        op = ie.build_operator(grid)
+        d = ie.build_decomposition(grid, 2, 1, "schwarz")
+        with pytest.raises(ValueError, match="rskel"):
+            ie.from_decomposition(op, d, dense_limit=10)
+        with pytest.raises(ValueError, match="backend"):
+            ie.from_decomposition(op, d, backend="qr")
+        pre = ie.from_decomposition(op, ie.build_decomposition(grid, 2, 1, "jacobi"))
+        with pytest.raises(ValueError):
+            pre.apply(np.zeros(op.n - 1))
+
+    def test_single_subdomain_exact_solve(self, ie, rng):
+        grid = ie.build_grid(2, 8)
+        op = ie.build_operator(grid)
+        pre = ie.from_decomposition(op, ie.build_decomposition(grid, 1, 0, "jacobi"))
+        f = rng.standard_normal(op.n)
+        u = pre.apply(f)
+        a = O.build_operator(O.build_grid(2, 8)).dense()
+        assert np.linalg.norm(a @ u - f) <= 1e-10 * np.linalg.norm(f)
+
+    @pytest.mark.parametrize("kind", ["jacobi", "schwarz"])
+    def test_symmetric_spd(self, ie, rng, kind):
+        grid = ie.build_grid(2, 16)
+        op = ie.build_operator(grid)
+        pre = ie.from_decomposition(op, ie.build_decomposition(grid, 4, 1, kind))
+        u, v = rng.standard_normal(op.n), rng.standard_normal(op.n)
+        l, r = pre.apply(u) @ v, u @ pre.apply(v)
+        assert abs(l - r) <= 1e-10 * max(abs(l), abs(r))
+        for _ in range(5):
+            f = rng.standard_normal(op.n)
+            assert f @ pre.apply(f) > 0
+
+    def test_3d_large_blocks(self, ie, rng):
+        # config-4 blocks (s up to 1000): apply vs oracle
+        grid = ie.build_grid(3, 32)
+        op = ie.build_operator(grid, lattice="cell")
+        d = ie.build_decomposition(grid, 4, 1, "schwarz")
+        og = O.build_grid(3, 32)
+        opre = O.SchwarzPrecond(O.build_operator(og, "cell"), O.build_decomposition(og, 4, 1, "schwarz"))
+        r = rng.standard_normal(op.n)
+        zr = opre.apply(r)
+        for variant in ("packed_inverse", "subst"):
+            pre = ie.from_decomposition(op, d, variant=variant)
+            assert rel(pre.apply(r), zr) <= 1e-12
+
+
+def _pcg_check(rep, u, g, kind, u_tol=1e-10):
+    n_it = int(g[f"{kind}_meta"][0])
+    assert abs(rep.n_it - n_it) <= 1, (rep.n_it, n_it)
+    assert rep.converged == bool(g[f"{kind}_meta"][1])
+    h = np.array(rep.residual_history)
+    hr = g[f"{kind}_hist"]
+    m = min(10, len(h), len(hr))
+    assert np.max(np.abs(h[:m] - hr[:m]) / hr[:m]) <= 1e-6
+    assert len(h) == rep.n_it + 1 and h[0] == 1.0 and rep.achieved_residual == h[-1]
+    if u_tol is not None:
+        assert rel(u, g[f"{kind}_u"]) <= u_tol
+
+
+class TestPCG:
+    def test_c1(self, ie, golden):
+        g = golden("ref_c1")
+        grid = ie.build_grid(2, 32)
+        op = ie.build_operator(grid, lattice="cell")
+        mv = ie.ToeplitzMatvec(op)
+        f = np.random.default_rng(0).standard_normal(op.n)
+        for kind in ("schwarz", "jacobi"):
+            for variant in ("packed_inverse", "subst"):
+                pre = ie.from_decomposition(op, ie.build_decomposition(grid, 4, 1, kind), variant=variant)
+                u, rep = ie.solve(mv, pre, f, tol=1e-10)
+                _pcg_check(rep, u, g, kind)
+                assert rep.t_pcg > 0 and rep.t_s > 0
+
+    def test_c3(self, ie, golden):
+        g = golden("ref_c3")
+        grid = ie.build_grid(2, 256)
+        op = ie.build_operator(grid, lattice="cell")
+        pre = ie.from_decomposition(op, ie.build_decomposition(grid, 32, 2, "schwarz"))
+        f = np.random.default_rng(1).standard_normal(op.n)
+        u, rep = ie.solve(ie.ToeplitzMatvec(op), pre, f, tol=1e-10)
+        _pcg_check(rep, u, g, "schwarz")
+
+    def test_c4(self, ie, golden):
+        g = golden("ref_c4")
+        grid = ie.build_grid(3, 32)
+        op = ie.build_operator(grid, lattice="cell")
+        mv = ie.ToeplitzMatvec(op)
+        pre = ie.from_decomposition(op, ie.build_decomposition(grid, 4, 1, "schwarz"))
+        f = np.random.default_rng(2).standard_normal(op.n)
+        u, rep = ie.solve(mv, pre, f, tol=1e-10)
+        _pcg_check(rep, u, g, "schwarz")
+        lam, steps = ie.extremal_eigenvalue_lanczos(mv, pre, op.n, which="min", max_iters=200,
+                                                    return_steps=True)
+        lr, calls = g["lam_schwarz_min"]
+        assert abs(lam - lr) <= 1e-8 * abs(lr)
+
+    @pytest.mark.slow
+    def test_c5_50_iterations(self, ie, golden):
+        g = golden("ref_c5")
+        grid = ie.build_grid(2, 1024)
+        op = ie.build_operator(grid, lattice="cell")
+        pre = ie.from_decomposition(op, ie.build_decomposition(grid, 128, 2, "schwarz"))
+        f = np.random.default_rng(3).standard_normal(op.n)
+        u, rep = ie.solve(ie.ToeplitzMatvec(op), pre, f, tol=1e-10, max_iters=50)
+        assert rep.n_it == 50 and not rep.converged
+        h, hr = np.array(rep.residual_history), g["schwarz_hist"]
+        assert np.max(np.abs(h[:10] - hr[:10]) / hr[:10]) <= 1e-8
+        ur = g["schwarz_u"].astype(np.float64)
+        assert rel(u, ur) <= 1e-4
+        assert 0.5 <= rep.achieved_residual / hr[-1] <= 2.0
+
+    @pytest.mark.parametrize("name", ["t16_jacobi_random", "t16_schwarz_random", "g16_jacobi_noise",
+                                      "g16_schwarz_noise", "g8_3d_jacobi_noise", "g8_3d_schwarz_noise",
+                                      "stag8_schwarz", "cap16_jacobi"])
+    def test_small_goldens(self, ie, golden, name):
+        g = golden("ref_pcg_small")
+        dim, n, m, w, kind, tol, mi = {
+            "t16_jacobi_random": (2, 16, 2, 1, "jacobi", 1e-12, None),
+            "t16_schwarz_random": (2, 16, 2, 1, "schwarz", 1e-12, None),
+            "g16_jacobi_noise": (2, 16, 2, 1, "jacobi", 1e-12, None),
+            "g16_schwarz_noise": (2, 16, 2, 1, "schwarz", 1e-12, None),
+            "g8_3d_jacobi_noise": (3, 8, 2, 1, "jacobi", 1e-12, None),
+            "g8_3d_schwarz_noise": (3, 8, 2, 1, "schwarz", 1e-12, None),
+            "stag8_schwarz": (2, 8, 2, 1, "schwarz", 1e-30, 5000),
+            "cap16_jacobi": (2, 16, 2, 1, "jacobi", 1e-12, 5),
+        }[name]
+        grid = ie.build_grid(dim, n)
+        op = ie.build_operator(grid)
+        pre = ie.from_decomposition(op, ie.build_decomposition(grid, m, w, kind))
+        u, rep = ie.solve(ie.ToeplitzMatvec(op), pre, g[name + "_f"], tol=tol, max_iters=mi)
+        n_it, conv, stag = g[name + "_meta"]
+        assert rep.converged == bool(conv) and rep.stagnated == bool(stag)
+        if name == "stag8_schwarz":
+            assert rep.stagnated and rep.achieved_residual > 1e-30
+        elif name == "cap16_jacobi":
+            assert rep.n_it == 5 and not rep.converged
+        else:
+            assert abs(rep.n_it - n_it) <= 1
+            assert rel(u, g[name + "_u"]) <= 1e-9
+
+    def test_golden_iteration_suites(self, ie):
+        with open(os.path.join(GOLDEN, "ref_goldens.json")) as fh:
+            suites = json.load(fh)
+        for sname in ("iterations-2d", "iterations-3d"):
+            s = suites[sname]
+            for case in s["cases"]:
+                if case["kind"] == "cbd":
+                    continue
+                grid = ie.build_grid(case["dim"], case["n"])
+                op = ie.build_operator(grid)
+                mv = ie.ToeplitzMatvec(op)
+                pre = ie.from_decomposition(op, ie.build_decomposition(grid, case["m"], case["overlap"],
+                                                                       case["kind"]))
+                f, _ = ie.make_rhs(mv, op.n, mode=s["rhs"], seed=s["seed"])
+                _, rep = ie.solve(mv, pre, f, tol=s["tol"])
+                assert rep.converged and abs(rep.n_it - case["n_it"]) <= s["tol_iters"], (sname, case, rep.n_it)
+
+    def test_trivial_and_zero(self, ie):
+        u, rep = ie.solve(lambda v: v, None, np.array([3.0]), tol=1e-12)
+        assert rep.n_it == 1 and rep.converged and u[0] == pytest.approx(3.0)
+        u, rep = ie.solve(lambda v: v, None, np.zeros(4))
+        assert rep.n_it == 0 and rep.converged and np.all(u == 0)
+        with pytest.raises(ValueError):
+            ie.solve(lambda v: v, None, np.ones(3), tol=0.0)
+        # native path, zero rhs
+        op = ie.build_operator(ie.build_grid(2, 8))
+        u, rep = ie.solve(ie.ToeplitzMatvec(op), None, np.zeros(64))
+        assert rep.n_it == 0 and rep.converged and rep.residual_history == [0.0]
+
+    def test_unpreconditioned_native(self, ie):
+        grid = ie.build_grid(2, 8)
+        op = ie.build_operator(grid)
+        mv = ie.ToeplitzMatvec(op)
+        f, _ = ie.make_rhs(mv, op.n, seed=0)
+        u, rep = ie.solve(mv, None, f, tol=1e-12, max_iters=2 * op.n)
+        ou, orep = O.pcg(O.FFTMatvec(O.build_operator(O.build_grid(2, 8))), None, f, tol=1e-12,
+                         max_iters=2 * op.n)
+        assert rep.converged and abs(rep.n_it - orep.n_it) <= 1
+
+    def test_breakdown_raises(self, ie):
+        with pytest.raises(FloatingPointError, match="breakdown"):
+            ie.solve(lambda v: -v, None, np.ones(4), tol=1e-12)
+
+    def test_deterministic(self, ie):
+        grid = ie.build_grid(2, 16)
+        op = ie.build_operator(grid)
+        mv = ie.ToeplitzMatvec(op)
+        pre = ie.from_decomposition(op, ie.build_decomposition(grid, 4, 1, "schwarz"))
+        f, _ = ie.make_rhs(mv, op.n, seed=7)
+        u1, r1 = ie.solve(mv, pre, f, tol=1e-12)
+        u2, r2 = ie.solve(mv, pre, f, tol=1e-12)
+        assert r1.residual_history == r2.residual_history and np.array_equal(u1, u2)
+
+
+class TestLanczos:
+    def test_c2(self, ie, golden):
+        g = golden("ref_c2")
+        grid = ie.build_grid(2, 64)
+        op = ie.build_operator(grid, lattice="cell")
+        mv = ie.ToeplitzMatvec(op)
+        for kind in ("schwarz", "jacobi"):
+            pre = ie.from_decomposition(op, ie.build_decomposition(grid, 8, 1, kind))
+            for which in ("min", "max"):
+                lam = ie.extremal_eigenvalue_lanczos(mv, pre, op.n, which=which, max_iters=300)
+                lr = float(g[f"lam_{kind}_{which}"][0])
+                assert abs(lam - lr) <= 1e-8 * abs(lr), (kind, which, lam, lr)
+
+    def test_small_vs_dense(self, ie, golden):
+        g = golden("ref_lanczos_small")
+        for name, (dim, n, m, kind, which) in {"j16max": (2, 16, 2, "jacobi", "max"),
+                                                "s16min": (2, 16, 4, "schwarz", "min"),
+                                                "s8_3dmin": (3, 8, 2, "schwarz", "min")}.items():
+            grid = ie.build_grid(dim, n)
+            op = ie.build_operator(grid)
+            pre = ie.from_decomposition(op, ie.build_decomposition(grid, m, 1, kind))
+            lam = ie.extremal_eigenvalue_lanczos(ie.ToeplitzMatvec(op), pre, op.n, which=which)
+            lam_ref, _, dmin, dmax = g[name]
+            assert abs(lam - lam_ref) <= 1e-8 * abs(lam_ref)
+            assert abs(lam - (dmin if which == "min" else dmax)) <= 1e-6
+
+    def test_bad_which(self, ie):
+        op = ie.build_operator(ie.build_grid(2, 8))
+        with pytest.raises(ValueError, match="which"):
+            ie.extremal_eigenvalue_lanczos(ie.ToeplitzMatvec(op), ie.identity(64), 64, which="mid")
