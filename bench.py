@@ -1,0 +1,317 @@
+"""Benchmark: Schwarz-PCG iterations/s on BASELINE.json config 5 (2D n=1024,
+N=1,048,576, cell lattice, D=128x128 subdomains, 2-line overlap, f ~ N(0,1)
+seed 3), plus the K1 direct-sum kernel's pair-evals/s against the measured
+FP64 issue roofline.
+
+A "step" is one PCG iteration of that 50-iteration run: one fused 2-RHS
+A-pass over [p_k, u_{k-1}] (N^2 kernel pair evaluations), the dot products,
+the vector updates and one Schwarz apply.  Timing follows the repo contract:
+W untimed warm-up iterations, then exactly K iterations timed with CUDA
+events on the launching stream (barrier + synchronize on both sides, max over
+ranks).  Inputs (the 8 MB iterate vectors) are re-read from HBM each pass;
+the per-step working set (factor pool + 10 vectors) exceeds the 126 MB L2
+only without translation sharing, so the config records l2 "not flushed".
+
+  python bench.py [--gpus N --steps K --warmup W]          # our arm
+  python bench.py --impl reference [--steps K --warmup W]  # CPU oracle arm
+
+Multi-GPU (torchrun, N > 1): rows and subdomains are sharded by
+paper_2108_12574_b200.distributed (NCCL all-gather of the iterate, fixed-chunk
+dot partials); see DESIGN.md.
+"""
+
+from __future__ import annotations
+
+import argparse
+import ctypes
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "Schwarz-PCG iter/s + kernel-matvec pair-evals/s (FP64) vs roofline, 1/2/4/8 GPU"
+CFG = dict(dim=2, n=1024, m=128, w=2, seed=3)
+WORKLOAD = "config5: 2D Laplace single-layer, n=1024 (N=1048576), cell lattice, Schwarz D=128x128 w=2, f~N(0,1) seed 3"
+K1_FP64_PER_PAIR_2RHS = 10  # SASS count of the 2-RHS inner loop (72 DFMA + 8 DADD per 8 pairs)
+
+
+def _peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as fh:
+            return json.load(fh)
+    except OSError:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                smax = float(parts[1])
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def run_ours(args):
+    import torch
+
+    import paper_2108_12574_b200 as ie
+    from paper_2108_12574_b200 import _lib
+
+    ws, rank, local = _dist()
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        from paper_2108_12574_b200 import distributed as D
+        return D.bench_sharded(args, METRIC, CFG, WORKLOAD)
+
+    st = torch.cuda.current_stream()
+    grid = ie.build_grid(CFG["dim"], CFG["n"])
+    op = ie.build_operator(grid, lattice="cell")
+    mv = ie.ToeplitzMatvec(op)
+    dec = ie.build_decomposition(grid, CFG["m"], CFG["w"], "schwarz")
+    t0 = time.perf_counter()
+    pre = ie.from_decomposition(op, dec, share_translated=not args.no_share)
+    torch.cuda.synchronize()
+    t_build = time.perf_counter() - t0
+    N = op.n
+    f_host = np.random.default_rng(CFG["seed"]).standard_normal(N)
+    f = torch.from_numpy(f_host).cuda()
+
+    L = _lib.lib()
+    peak_dfma = ctypes.c_double(0.0)
+    _lib.check(L.ie_fp64_peak(ctypes.byref(peak_dfma), _lib.stream_ptr()), "fp64 peak")
+    fp64_peak_tflops = 2.0 * peak_dfma.value / 1e12
+
+    def solve_dev(iters):
+        return ie.solve(mv, pre, f, tol=1e-10, max_iters=iters)
+
+    # warm-up: W iterations (untimed)
+    solve_dev(max(args.warmup, 1))
+    torch.cuda.synchronize()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    # timed: exactly K iterations, device events on the launching stream
+    n0 = _lib.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(st)
+    u, rep = solve_dev(args.steps)
+    e1.record(st)
+    torch.cuda.synchronize()
+    launches = _lib.launch_count() - n0
+    ms = e0.elapsed_time(e1)
+    assert rep.n_it == args.steps, rep.n_it
+
+    # K1 alone: 2-RHS A-pass launches timed with events (roofline)
+    X = torch.from_numpy(np.random.default_rng(9).standard_normal((2, N))).cuda()
+    Y = torch.empty_like(X)
+    mv.matvec_device(X, Y, nrhs=2)
+    reps = max(2, min(5, args.steps))
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    torch.cuda.synchronize()
+    ev[0].record(st)
+    for _ in range(reps):
+        mv.matvec_device(X, Y, nrhs=2)
+    ev[1].record(st)
+    torch.cuda.synchronize()
+    pass_ms = ev[0].elapsed_time(ev[1]) / reps
+    pairs = float(N) * float(N)
+    pair_rate = pairs / (pass_ms * 1e-3)
+    k1_tflops = pair_rate * K1_FP64_PER_PAIR_2RHS * 2 / 1e12
+
+    # preconditioner apply alone (HBM roofline of K3)
+    r = torch.from_numpy(np.random.default_rng(10).standard_normal(N)).cuda()
+    z = torch.empty_like(r)
+    pre.apply_device(r, z)
+    ev2 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    torch.cuda.synchronize()
+    ev2[0].record(st)
+    for _ in range(20):
+        pre.apply_device(r, z)
+    ev2[1].record(st)
+    torch.cuda.synchronize()
+    apply_ms = ev2[0].elapsed_time(ev2[1]) / 20
+    st_ = pre.stats()
+    clk = clocks.stop()
+
+    # end to end through the public API with host numpy buffers
+    t0 = time.perf_counter()
+    u_h, rep_h = ie.solve(mv, pre, f_host, tol=1e-10, max_iters=args.steps)
+    t_e2e = time.perf_counter() - t0
+
+    peaks = _peaks()
+    out = {
+        "metric": METRIC,
+        "value": args.steps / (ms * 1e-3),
+        "unit": "iter/s",
+        "n_gpus": 1,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms / args.steps,
+        "higher_is_better": True,
+        "scaling": "strong",
+        "vs_baseline": None,
+        "dtype": "f64",
+        "data": "synthetic (BASELINE.json config 5, seeded)",
+        "config": {"workload": WORKLOAD, "N": N, "subdomains": dec.n_subdomains,
+                   "matvec": "K1 direct sum (N^2 pairs, 2 RHS per pass)",
+                   "share_translated": not args.no_share, "l2": "not flushed; per-pass source stream 16 MB",
+                   "precond_build_s": t_build, "parallelism": "single GPU"},
+        "pair_evals_per_s": pair_rate,
+        "k1_pass_ms": pass_ms,
+        "apply_ms": apply_ms,
+        "roofline": {"bound": "fp64", "achieved": k1_tflops, "peak": fp64_peak_tflops, "unit": "TFLOP/s",
+                     "frac": k1_tflops / fp64_peak_tflops, "traffic": None,
+                     "kernel": "k_matvec<2,2,2> (2-RHS A-pass)",
+                     "note": "flops = 2 x FP64 pipe instructions (10/pair in SASS); peak = live DFMA microbenchmark",
+                     "share_of_step": pass_ms / (ms / args.steps)},
+        "apply_roofline": {"bound": "hbm", "unit": "GB/s",
+                           "algorithmic_bytes": _apply_bytes(dec, N, not args.no_share),
+                           "achieved": _apply_bytes(dec, N, not args.no_share) / (apply_ms * 1e-3) / 1e9,
+                           "peak": peaks.get("hbm_gbs"), "factor_bytes_device": st_["device_bytes"]},
+        "e2e": {"value": args.steps / t_e2e, "unit": "iter/s", "h2d_bytes_per_step": 8 * N / args.steps,
+                "d2h_bytes_per_step": (8 * N + 8 * (args.steps + 1)) / args.steps,
+                "note": "pcg.solve(numpy f) -> numpy u: one H2D of f and one D2H of u per solve of K steps"},
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
+    if out["apply_roofline"]["peak"]:
+        out["apply_roofline"]["frac"] = out["apply_roofline"]["achieved"] / out["apply_roofline"]["peak"]
+    if not args.no_cpu:
+        out["cpu_baseline"] = cpu_baseline(max(1, min(3, args.steps)))
+    print(json.dumps(out))
+    return out
+
+
+def _apply_bytes(dec, N, shared):
+    """K3 algorithmic bytes: packed factors (once per block) + r in, z out."""
+    fac = sum(s.size * (s.size + 1) // 2 * 8 for s in dec.subdomains)
+    return fac + 16 * N
+
+
+def _oracle_setup():
+    from oracle import iedd_oracle as O
+    grid = O.build_grid(CFG["dim"], CFG["n"])
+    op = O.build_operator(grid, "cell")
+    t0 = time.perf_counter()
+    pre = O.SchwarzPrecond(op, O.build_decomposition(grid, CFG["m"], CFG["w"], "schwarz"))
+    t_build = time.perf_counter() - t0
+    mv = O.FFTMatvec(op)
+    f = np.random.default_rng(CFG["seed"]).standard_normal(op.n)
+    return O, mv, pre, f, t_build
+
+
+def cpu_baseline(iters: int):
+    """The CPU oracle (numpy/scipy port of the reference, FFT matvec,
+    per-block triangular solves) timed on this host: `iters` PCG iterations."""
+    O, mv, pre, f, t_build = _oracle_setup()
+    t0 = time.perf_counter()
+    _, rep = O.pcg(mv, pre, f, tol=1e-10, max_iters=iters)
+    dt = time.perf_counter() - t0
+    return {"value": rep.n_it / dt, "unit": "iter/s", "cores": 1, "kind": "port",
+            "sample": f"{rep.n_it} PCG iterations of config 5 (oracle: FFT matvec + per-block scipy "
+                      f"solve_triangular), build {t_build:.1f}s excluded",
+            "host_cores_available": len(os.sched_getaffinity(0))}
+
+
+def run_reference(args):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return None
+    O, mv, pre, f, t_build = _oracle_setup()
+    if args.warmup:
+        O.pcg(mv, pre, f, tol=1e-10, max_iters=args.warmup)
+    t0 = time.perf_counter()
+    _, rep = O.pcg(mv, pre, f, tol=1e-10, max_iters=args.steps)
+    dt = time.perf_counter() - t0
+    v = rep.n_it / dt
+    out = {"metric": METRIC, "value": v, "unit": "iter/s", "n_gpus": ws, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": 1e3 * dt / rep.n_it, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE.json config 5)",
+           "impl": "reference",
+           "config": {"workload": WORKLOAD, "N": int(f.size), "precond_build_s": t_build,
+                      "parallelism": "host CPU (reference algorithm port)"},
+           "cpu_baseline": {"value": v, "unit": "iter/s", "cores": 1, "kind": "port",
+                            "sample": f"{rep.n_it} PCG iterations of config 5 after {args.warmup} warm-up"},
+           "e2e": {"value": v, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+    return out
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-share", action="store_true", help="factorise every block (no translation sharing)")
+    ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -128,6 +128,10 @@ int ie_lanczos_f64(const ie_matvec* A, const ie_precond* T, const double* d_v0,
                    int32_t which, int64_t max_iters, double rtol, double* lambda,
                    int64_t* steps, void* stream);
 
+/* FP64 issue-peak microbenchmark: DFMA instructions (lane ops) per second
+ * over all SMs -- the roofline denominator for K1. */
+int ie_fp64_peak(double* dfma_per_s, void* stream);
+
 /* Last error text for IE_ERR_CUDA / IE_ERR_ARG (thread-local). */
 const char* ie_last_error(void);
 /* Number of this library's kernels launched so far (process-wide counter). */

@@ -14,3 +14,44 @@ void set_error(const std::string& msg) { t_err = msg; }
 
 extern "C" const char* ie_last_error(void) { return ie::t_err.c_str(); }
 extern "C" int64_t ie_launch_count(void) { return ie::g_launches.load(); }
+
+// ----------------------------------------------------------------------
+// FP64 issue-peak microbenchmark (roofline denominator for K1; not in
+// MEASURED_PEAKS.json): 8 independent DFMA chains per thread, all SMs.
+namespace ie {
+__global__ void __launch_bounds__(256) k_dfma_peak(double* out, int iters, double a, double b) {
+    double x[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = threadIdx.x * 1e-3 + k;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) x[k] = fma(x[k], a, b);
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += x[k];
+    if (s == 1234.5678) out[0] = s;  // keep the chains live
+}
+}  // namespace ie
+
+extern "C" int ie_fp64_peak(double* dfma_per_s, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    double* d;
+    IE_CUDA(cudaMalloc(&d, 8));
+    cudaEvent_t e0, e1;
+    IE_CUDA(cudaEventCreate(&e0));
+    IE_CUDA(cudaEventCreate(&e1));
+    const int blocks = ie::kNumSMs * 8, threads = 256, iters = 4096;
+    for (int rep = 0; rep < 2; ++rep) ie::k_dfma_peak<<<blocks, threads, 0, st>>>(d, iters, 0.999999, 1e-7);
+    IE_CUDA(cudaEventRecord(e0, st));
+    ie::k_dfma_peak<<<blocks, threads, 0, st>>>(d, iters, 0.999999, 1e-7);
+    IE_CUDA(cudaEventRecord(e1, st));
+    IE_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    IE_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    *dfma_per_s = (double)blocks * threads * iters * 8 / (ms * 1e-3);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(d);
+    return IE_OK;
+}

@@ -261,6 +261,40 @@ __global__ void __launch_bounds__(256) k_apply_packed(ApplyArgs a) {
     }
 }
 
+// Blocks larger than 1024 points (reference dense_limit allows 4096): one
+// CTA per block, r_k and z_k in shared memory, two passes over the packed
+// columns -- dot part (column j -> z_j, warp-exclusive) then axpy part
+// (row tile -> z_i, warp-exclusive).  Reads the factor twice; only the
+// small-D golden geometries use it.
+__global__ void __launch_bounds__(256) k_apply_large(ApplyArgs a) {
+    extern __shared__ double sm[];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+    const BlockMeta bm = a.meta[blockIdx.x];
+    const int s = bm.s;
+    const int* idx = a.idx + bm.idx_off;
+    const double* fac = a.fac + bm.fac_off;
+    double* rs = sm;
+    double* zs = sm + s;
+    for (int i = threadIdx.x; i < s; i += blockDim.x) rs[i] = __ldg(a.r + idx[i]);
+    __syncthreads();
+    for (int j = warp; j < s; j += nw) {
+        const double* colp = fac + ((int64_t)j * (j + 1)) / 2;
+        double d = 0.0;
+        for (int i = lane; i <= j; i += 32) d = fma(__ldg(colp + i), rs[i], d);
+        d = warp_sum(d);
+        if (lane == 0) zs[j] = d;
+    }
+    __syncthreads();
+    for (int i0 = warp * 32; i0 < s; i0 += nw * 32) {
+        const int i = i0 + lane;
+        double acc = 0.0;
+        for (int j = i0 + 1; j < s; ++j) {
+            if (i < j) acc = fma(__ldg(fac + ((int64_t)j * (j + 1)) / 2 + i), rs[j], acc);
+        }
+        if (i < s) a.staging[bm.st_off + i] = zs[i] + acc;
+    }
+}
+
 // Forward (G^T y = r, row-axpy form) and back (G x = y, row-dot form)
 // substitution with the row-packed upper factor; one warp per block.
 template <int T>
@@ -407,6 +441,16 @@ int precond_apply(const ie_precond* p, const double* r, double* z, double* parti
     a.D = p->D;
     a.wpb = p->wpb;
     a.bpc = p->bpc;
+    if (p->T > 32) {
+        const size_t sm = (size_t)2 * p->smax * sizeof(double);
+        if (sm > 48 * 1024) cudaFuncSetAttribute(k_apply_large, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        k_apply_large<<<(unsigned)p->D, 256, sm, st>>>(a);
+        IE_LAUNCHED();
+        const int nch2 = (p->N + kChunk - 1) / kChunk;
+        k_scatter<<<nch2, 256, 0, st>>>(p->d_staging, p->d_ptr, p->d_pos, z, p->N, partials ? r : nullptr, partials);
+        IE_LAUNCHED();
+        return IE_OK;
+    }
     switch (p->T) {
         case 1: launch_apply_T<1>(p, a, st); break;
         case 2: launch_apply_T<2>(p, a, st); break;
@@ -481,10 +525,13 @@ extern "C" int ie_precond_create(const ie_geom* g, const int64_t* h_offsets, con
         total += s;
         refmem += 8 * (s * s + s);
     }
-    const int T = ie::slots_for(smax);
+    int T = ie::slots_for(smax);
     if (T < 0) {
-        ie::set_error("ie_precond_create: subdomains larger than 1024 points are not supported");
-        return IE_ERR_ARG;
+        if (variant == IE_VARIANT_SUBST) {
+            ie::set_error("ie_precond_create: variant 'subst' supports subdomains up to 1024 points");
+            return IE_ERR_ARG;
+        }
+        T = 64;  // large-block path (k_apply_large)
     }
     // translation classes: signature = multi-index offsets from the first point
     std::vector<int64_t> rep(D);
@@ -653,10 +700,13 @@ extern "C" int ie_precond_create(const ie_geom* g, const int64_t* h_offsets, con
     ba.n = g->n;
     ba.dim = g->dim;
     ba.variant = variant;
-    const int sm_s = std::min(smax, ie::kSmemMaxS);
-    const size_t smem = ((size_t)sm_s * 3 * 4 + 15) / 16 * 16 + (size_t)sm_s * 8 +
-                        (smax <= ie::kSmemMaxS ? (size_t)sm_s * (sm_s | 1) * 8 : 0) +
-                        (smax > ie::kSmemMaxS ? ((size_t)smax * 3 * 4 + 15) / 16 * 16 + (size_t)smax * 8 : 0);
+    size_t smem = 0;
+    for (int64_t u = 0; u < U; ++u) {
+        const size_t su = (size_t)usizes[u];
+        size_t need = (su * 3 * 4 + 15) / 16 * 16 + su * 8;
+        if (usizes[u] <= ie::kSmemMaxS) need += su * (su | 1) * 8;
+        smem = std::max(smem, need);
+    }
     IE_CHECK_BUILD(cudaFuncSetAttribute(ie::k_build, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     ie::k_build<<<(unsigned)U, ie::kBuildThreads, smem, st>>>(ba);
     IE_CHECK_BUILD(cudaGetLastError());
