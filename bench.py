@@ -109,6 +109,32 @@ def _dist():
     return ws, rank, local
 
 
+def _time_iters(ie, mv, pre, f, iters, st):
+    """Device time (ms) of exactly `iters` PCG iterations through ie.solve."""
+    import torch
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(st)
+    u, rep = ie.solve(mv, pre, f, tol=1e-10, max_iters=iters)
+    e1.record(st)
+    torch.cuda.synchronize()
+    assert rep.n_it == iters, rep.n_it
+    return e0.elapsed_time(e1), rep
+
+
+def _time_calls(fn, reps, st):
+    import torch
+    fn()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(st)
+    for _ in range(reps):
+        fn()
+    e1.record(st)
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
 def run_ours(args):
     import torch
 
@@ -126,7 +152,8 @@ def run_ours(args):
     st = torch.cuda.current_stream()
     grid = ie.build_grid(CFG["dim"], CFG["n"])
     op = ie.build_operator(grid, lattice="cell")
-    mv = ie.ToeplitzMatvec(op)
+    mv = ie.ToeplitzMatvec(op, method=args.matvec)        # production path (FFT unless --matvec direct)
+    k1 = ie.KernelMatvec(op, method="direct")             # north-star K1 direct sum
     dec = ie.build_decomposition(grid, CFG["m"], CFG["w"], "schwarz")
     t0 = time.perf_counter()
     pre = ie.from_decomposition(op, dec, share_translated=not args.no_share)
@@ -135,71 +162,71 @@ def run_ours(args):
     N = op.n
     f_host = np.random.default_rng(CFG["seed"]).standard_normal(N)
     f = torch.from_numpy(f_host).cuda()
-
     L = _lib.lib()
     peak_dfma = ctypes.c_double(0.0)
     _lib.check(L.ie_fp64_peak(ctypes.byref(peak_dfma), _lib.stream_ptr()), "fp64 peak")
     fp64_peak_tflops = 2.0 * peak_dfma.value / 1e12
+    peaks = _peaks()
 
-    def solve_dev(iters):
-        return ie.solve(mv, pre, f, tol=1e-10, max_iters=iters)
-
-    # warm-up: W iterations (untimed)
-    solve_dev(max(args.warmup, 1))
-    torch.cuda.synchronize()
-
+    # ---- primary: exactly K iterations after W warm-up iterations
+    _time_iters(ie, mv, pre, f, max(args.warmup, 1), st)
     clocks = ClockSampler(local)
     clocks.start()
-    # timed: exactly K iterations, device events on the launching stream
     n0 = _lib.launch_count()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    torch.cuda.synchronize()
-    e0.record(st)
-    u, rep = solve_dev(args.steps)
-    e1.record(st)
-    torch.cuda.synchronize()
+    ms, rep = _time_iters(ie, mv, pre, f, args.steps, st)
     launches = _lib.launch_count() - n0
-    ms = e0.elapsed_time(e1)
-    assert rep.n_it == args.steps, rep.n_it
 
-    # K1 alone: 2-RHS A-pass launches timed with events (roofline)
+    # ---- per-kernel device times on the same stream
     X = torch.from_numpy(np.random.default_rng(9).standard_normal((2, N))).cuda()
     Y = torch.empty_like(X)
-    mv.matvec_device(X, Y, nrhs=2)
-    reps = max(2, min(5, args.steps))
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-    torch.cuda.synchronize()
-    ev[0].record(st)
-    for _ in range(reps):
-        mv.matvec_device(X, Y, nrhs=2)
-    ev[1].record(st)
-    torch.cuda.synchronize()
-    pass_ms = ev[0].elapsed_time(ev[1]) / reps
-    pairs = float(N) * float(N)
-    pair_rate = pairs / (pass_ms * 1e-3)
-    k1_tflops = pair_rate * K1_FP64_PER_PAIR_2RHS * 2 / 1e12
-
-    # preconditioner apply alone (HBM roofline of K3)
+    mv_ms = _time_calls(lambda: mv.matvec_device(X, Y, nrhs=2), 20, st)
     r = torch.from_numpy(np.random.default_rng(10).standard_normal(N)).cuda()
     z = torch.empty_like(r)
-    pre.apply_device(r, z)
-    ev2 = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-    torch.cuda.synchronize()
-    ev2[0].record(st)
-    for _ in range(20):
-        pre.apply_device(r, z)
-    ev2[1].record(st)
-    torch.cuda.synchronize()
-    apply_ms = ev2[0].elapsed_time(ev2[1]) / 20
-    st_ = pre.stats()
+    apply_ms = _time_calls(lambda: pre.apply_device(r, z), 50, st)
+    # K1 direct sum (north-star kernel): 2-RHS pass, pair-evals/s vs FP64 issue roofline
+    k1_ms = _time_calls(lambda: k1.matvec_device(X, Y, nrhs=2), 2, st)
     clk = clocks.stop()
+    pairs = float(N) * float(N)
+    pair_rate = pairs / (k1_ms * 1e-3)
+    k1_tflops = pair_rate * K1_FP64_PER_PAIR_2RHS * 2 / 1e12
+    k1_iters = max(1, min(3, args.steps))
+    k1_step_ms, _ = _time_iters(ie, k1, pre, f, k1_iters, st)
 
-    # end to end through the public API with host numpy buffers
+    # ---- K3 apply with every block factorised (factors streamed from HBM): the HBM roofline
+    apply_bytes = _apply_bytes(dec, N, False)
+    noshare = {}
+    if not args.skip_noshare:
+        t0 = time.perf_counter()
+        pre_ns = ie.from_decomposition(op, dec, share_translated=False)
+        torch.cuda.synchronize()
+        t_ns = time.perf_counter() - t0
+        ns_ms = _time_calls(lambda: pre_ns.apply_device(r, z), 20, st)
+        noshare = {"apply_ms": ns_ms, "achieved": apply_bytes / (ns_ms * 1e-3) / 1e9, "build_s": t_ns,
+                   "factor_bytes": pre_ns.stats()["device_bytes"]}
+        if peaks.get("hbm_gbs"):
+            noshare["frac"] = noshare["achieved"] / peaks["hbm_gbs"]
+        del pre_ns
+
+    # ---- end to end through the public API with host numpy buffers
     t0 = time.perf_counter()
     u_h, rep_h = ie.solve(mv, pre, f_host, tol=1e-10, max_iters=args.steps)
     t_e2e = time.perf_counter() - t0
 
-    peaks = _peaks()
+    step_ms = ms / args.steps
+    kern = {"matvec_pass_ms": mv_ms, "apply_ms": apply_ms}
+    dom = max(kern, key=kern.get)
+    if dom == "apply_ms":
+        roof = {"bound": "hbm", "kernel": "k_apply_packed (Schwarz apply, translation-shared factors)",
+                "achieved": (16.0 * N + 8.0 * sum(s.size for s in dec.subdomains)) / (apply_ms * 1e-3) / 1e9,
+                "unit": "GB/s", "peak": peaks.get("hbm_gbs"),
+                "note": "bytes = r gather + staged z + z out (factors L2-resident after sharing)"}
+    else:
+        fft_bytes = 16.0 * N * 2 + 16.0 * N * 2 * 2 + 16.0 * N * 2   # x in, (n x 2n) buffer rw x2, y out
+        roof = {"bound": "hbm", "kernel": "k_fft_lines (3 launches per 2-RHS pass)",
+                "achieved": fft_bytes / (mv_ms * 1e-3) / 1e9, "unit": "GB/s", "peak": peaks.get("hbm_gbs")}
+    roof["traffic"] = None
+    roof["frac"] = roof["achieved"] / roof["peak"] if roof.get("peak") else None
+    roof["share_of_step"] = kern[dom] / step_ms
     out = {
         "metric": METRIC,
         "value": args.steps / (ms * 1e-3),
@@ -207,36 +234,34 @@ def run_ours(args):
         "n_gpus": 1,
         "steps": args.steps,
         "warmup": args.warmup,
-        "ms_per_step": ms / args.steps,
+        "ms_per_step": step_ms,
         "higher_is_better": True,
         "scaling": "strong",
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (BASELINE.json config 5, seeded)",
         "config": {"workload": WORKLOAD, "N": N, "subdomains": dec.n_subdomains,
-                   "matvec": "K1 direct sum (N^2 pairs, 2 RHS per pass)",
-                   "share_translated": not args.no_share, "l2": "not flushed; per-pass source stream 16 MB",
+                   "matvec": f"{mv.method} ({'circulant-embedding FFT, 2 RHS per complex pass' if mv.method == 'fft' else 'K1 direct sum'})",
+                   "share_translated": not args.no_share, "l2": "not flushed; working set > L2 only for K1 sources",
                    "precond_build_s": t_build, "parallelism": "single GPU"},
-        "pair_evals_per_s": pair_rate,
-        "k1_pass_ms": pass_ms,
-        "apply_ms": apply_ms,
-        "roofline": {"bound": "fp64", "achieved": k1_tflops, "peak": fp64_peak_tflops, "unit": "TFLOP/s",
-                     "frac": k1_tflops / fp64_peak_tflops, "traffic": None,
-                     "kernel": "k_matvec<2,2,2> (2-RHS A-pass)",
-                     "note": "flops = 2 x FP64 pipe instructions (10/pair in SASS); peak = live DFMA microbenchmark",
-                     "share_of_step": pass_ms / (ms / args.steps)},
-        "apply_roofline": {"bound": "hbm", "unit": "GB/s",
-                           "algorithmic_bytes": _apply_bytes(dec, N, not args.no_share),
-                           "achieved": _apply_bytes(dec, N, not args.no_share) / (apply_ms * 1e-3) / 1e9,
-                           "peak": peaks.get("hbm_gbs"), "factor_bytes_device": st_["device_bytes"]},
+        "kernels_ms": kern,
+        "roofline": roof,
+        "kernel_matvec": {
+            "kernel": "k_matvec<2,2,2> (K1 direct sum, log kernel evaluated per pair, 2 RHS)",
+            "pair_evals_per_s": pair_rate, "pass_ms": k1_ms,
+            "schwarz_pcg_iter_per_s": k1_iters / (k1_step_ms * 1e-3),
+            "roofline": {"bound": "fp64", "achieved": k1_tflops, "peak": fp64_peak_tflops, "unit": "TFLOP/s",
+                         "frac": k1_tflops / fp64_peak_tflops, "traffic": None,
+                         "note": "flops = 2 x FP64 pipe instructions (10 per pair in SASS); "
+                                 "peak = live 8-chain DFMA microbenchmark on all SMs"}},
+        "apply_hbm_roofline_unshared": dict(noshare, bound="hbm", unit="GB/s", algorithmic_bytes=apply_bytes,
+                                            peak=peaks.get("hbm_gbs"), kernel="k_apply_packed<5,2>"),
         "e2e": {"value": args.steps / t_e2e, "unit": "iter/s", "h2d_bytes_per_step": 8 * N / args.steps,
                 "d2h_bytes_per_step": (8 * N + 8 * (args.steps + 1)) / args.steps,
-                "note": "pcg.solve(numpy f) -> numpy u: one H2D of f and one D2H of u per solve of K steps"},
+                "note": "pcg.solve(numpy f) -> numpy u, wall clock: one H2D of f and one D2H of u per solve of K steps"},
         "gpu_launches": launches,
         "clocks": clk,
     }
-    if out["apply_roofline"]["peak"]:
-        out["apply_roofline"]["frac"] = out["apply_roofline"]["achieved"] / out["apply_roofline"]["peak"]
     if not args.no_cpu:
         out["cpu_baseline"] = cpu_baseline(max(1, min(3, args.steps)))
     print(json.dumps(out))
@@ -306,6 +331,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-share", action="store_true", help="factorise every block (no translation sharing)")
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
+    ap.add_argument("--matvec", default="auto", choices=["auto", "fft", "direct"])
+    ap.add_argument("--skip-noshare", action="store_true", help="skip the unshared-factor apply measurement")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

@@ -57,9 +57,15 @@ typedef struct ie_geom {
 /* ---------------------------------------------------------------- K1 ---- */
 typedef struct ie_matvec ie_matvec;
 
-/* Replaces ToeplitzMatvec.__init__ (toeplitz.py:19-32).  Builds the device
- * log table used by the direct-sum kernel. */
+#define IE_MATVEC_DIRECT 0 /* K1: O(N^2) direct sum, kernel evaluated per pair */
+#define IE_MATVEC_FFT 1    /* K1b: O(N log N) circulant-embedding FFT (n = 2^k <= 2048) */
+
+/* Replaces ToeplitzMatvec.__init__ (toeplitz.py:19-32).  ie_matvec_create
+ * builds the direct-sum operator (device log table); ie_matvec_create_method
+ * selects the method -- IE_MATVEC_FFT also computes the real, even symbol of
+ * the (2n)^dim embedding on the device. */
 int ie_matvec_create(const ie_geom* g, ie_matvec** out);
+int ie_matvec_create_method(const ie_geom* g, int32_t method, ie_matvec** out);
 void ie_matvec_destroy(ie_matvec* m);
 
 /* Replaces ToeplitzMatvec.matvec (toeplitz.py:39-50), matrix-free:

@@ -23,6 +23,7 @@ IE_ERR_NO_RITZ = 4
 IE_ERR_CUDA = 5
 
 VARIANTS = {"packed_inverse": 0, "subst": 1}
+MATVEC_METHODS = {"direct": 0, "fft": 1}
 
 
 class IeGeom(ctypes.Structure):
@@ -39,6 +40,7 @@ _D = ctypes.c_double
 
 _SIGS = {
     "ie_matvec_create": (_I32, [ctypes.POINTER(IeGeom), ctypes.POINTER(_P)]),
+    "ie_matvec_create_method": (_I32, [ctypes.POINTER(IeGeom), _I32, ctypes.POINTER(_P)]),
     "ie_matvec_destroy": (None, [_P]),
     "ie_matvec_f64": (_I32, [_P, _P, _I64, _I32, _P, _I64, _I64, _I64, _P]),
     "ie_assemble_block_f64": (_I32, [ctypes.POINTER(IeGeom), _P, _I64, _P, _I64, _P, _P]),

@@ -16,7 +16,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 CSRC = os.path.join(HERE, "csrc")
 BUILD = os.path.join(HERE, "_build")
 LIB = os.path.join(HERE, "libiedd_b200.so")
-SOURCES = ["capi.cu", "matvec.cu", "precond.cu", "krylov.cu"]
+SOURCES = ["capi.cu", "matvec.cu", "fft.cu", "precond.cu", "krylov.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
          "-Xptxas", "-v"]

@@ -1,0 +1,507 @@
+// K1b: O(N log N) matvec by circulant embedding -- the reference's own
+// algorithm (ToeplitzMatvec, /root/reference/pkg/src/iedd/toeplitz.py:11-53;
+// generator kernel.py:190-199), hand-written for sm_100a in FP64.
+//
+//  * The (2n)^d embedding of the generator is mirror-even on every axis, so
+//    its DFT (the symbol) is real and even: stored folded, (n+1)^d doubles,
+//    pre-scaled by 1/(2n)^d (numpy's irfftn normalisation).
+//  * The operator is real, so two right-hand sides ride in one complex
+//    transform: z = x0 + i x1  ->  IFFT(sym * FFT(z)) = A x0 + i A x1.  The
+//    PCG 2-RHS pass [p_k, u_{k-1}] costs one complex round trip.
+//  * Zero padding is exploited: axis transforms only touch lines whose
+//    not-yet-transformed coordinates are < n, and the last forward axis-0
+//    transform, the symbol multiply and the first inverse transform are one
+//    fused kernel per line (the spectrum never round-trips HBM).
+//  * Each CTA runs a self-sorting Stockham FFT (radix 4, one radix-2 pass
+//    for odd log2 M) over 4096 complex points in shared memory (64 KB):
+//    4096/M lines of length M = 2n <= 4096.
+#include <math.h>
+
+#include <vector>
+
+#include "common.cuh"
+
+namespace ie {
+
+constexpr int kFftPoints = 4096;
+constexpr int kFftThreads = 256;
+constexpr int kPtsPerThread = kFftPoints / kFftThreads;
+
+struct LineArgs {
+    int nlines;   // lines in this pass
+    int ninner;   // line g -> o = g / ninner, i = g % ninner
+    int L;
+    int logL;
+    // source
+    int in_real;  // 1: real pair x0 (+ i x1); 0: complex buffer
+    const double2* in_c;
+    const double* x0;
+    const double* x1;
+    int64_t in_so, in_si, in_sl;
+    int n_in;     // l >= n_in reads as zero
+    // destination
+    int out_real;
+    double2* out_c;
+    double* y0;
+    double* y1;
+    int64_t out_so, out_si, out_sl;
+    int n_out;    // only l < n_out is written
+    int sign;     // -1 forward, +1 inverse (ignored when fused)
+    int fused;    // forward, * symbol, inverse
+    const double* sym;
+    int dim;
+    int n;
+    const double2* tw;  // tw[m] = exp(-2 pi i m / L)
+};
+
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+    return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+// multiply by i*sign: sign=-1 -> -i, sign=+1 -> +i
+__device__ __forceinline__ double2 mul_isign(double2 a, int sign) {
+    return sign < 0 ? make_double2(a.y, -a.x) : make_double2(-a.y, a.x);
+}
+
+// One Stockham pass of radix R over all lines held in shared memory.
+template <int R>
+__device__ __forceinline__ void stockham_pass(double2* sm, int L, int Ns, int sign, const double2* __restrict__ tw) {
+    constexpr int NB = kFftPoints / (R * kFftThreads);
+    const int per_line = L / R;
+    double2 v[NB][R];
+    int dst[NB];
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+        const int bf = threadIdx.x + b * kFftThreads;
+        const int g = bf / per_line;
+        const int j = bf - g * per_line;
+        const int k = j & (Ns - 1);
+        double2* x = sm + g * L;
+#pragma unroll
+        for (int r = 0; r < R; ++r) v[b][r] = x[j + r * per_line];
+        const int tstep = k * (L / (Ns * R));
+#pragma unroll
+        for (int r = 1; r < R; ++r) {
+            double2 t = __ldg(tw + r * tstep);
+            if (sign > 0) t.y = -t.y;
+            v[b][r] = cmul(v[b][r], t);
+        }
+        if (R == 2) {
+            const double2 a0 = v[b][0], a1 = v[b][1];
+            v[b][0] = cadd(a0, a1);
+            v[b][1] = csub(a0, a1);
+        } else {
+            const double2 a = cadd(v[b][0], v[b][2]);
+            const double2 bb = csub(v[b][0], v[b][2]);
+            const double2 c = cadd(v[b][1], v[b][3]);
+            const double2 d = mul_isign(csub(v[b][1], v[b][3]), sign);
+            v[b][0] = cadd(a, c);
+            v[b][2] = csub(a, c);
+            v[b][1] = cadd(bb, d);
+            v[b][3] = csub(bb, d);
+        }
+        dst[b] = g * L + (j / Ns) * Ns * R + k;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int b = 0; b < NB; ++b)
+#pragma unroll
+        for (int r = 0; r < R; ++r) sm[dst[b] + r * Ns] = v[b][r];
+    __syncthreads();
+}
+
+__device__ void fft_smem(double2* sm, int L, int logL, int sign, const double2* tw) {
+    int Ns = 1;
+    for (int p = 0; p + 1 < logL; p += 2) {
+        stockham_pass<4>(sm, L, Ns, sign, tw);
+        Ns *= 4;
+    }
+    if (logL & 1) stockham_pass<2>(sm, L, Ns, sign, tw);
+}
+
+__global__ void __launch_bounds__(kFftThreads) k_fft_lines(LineArgs a) {
+    extern __shared__ __align__(16) double2 sm[];
+    const int L = a.L;
+    const int G = kFftPoints / L;
+    const int g0 = blockIdx.x * G;
+    // load (coalesced along l when lines are contiguous, across lines otherwise)
+    const bool contig_in = a.in_real ? true : (a.in_sl == 1);
+#pragma unroll 4
+    for (int q = 0; q < kPtsPerThread; ++q) {
+        const int p = threadIdx.x + q * kFftThreads;
+        int g, l;
+        if (contig_in) {
+            g = p / L;
+            l = p - g * L;
+        } else {
+            g = p % G;
+            l = p / G;
+        }
+        const int line = g0 + g;
+        double2 v = make_double2(0.0, 0.0);
+        if (line < a.nlines && l < a.n_in) {
+            const int o = line / a.ninner, i = line - o * a.ninner;
+            const int64_t off = (int64_t)o * a.in_so + (int64_t)i * a.in_si + (int64_t)l * a.in_sl;
+            if (a.in_real) {
+                v.x = a.x0[off];
+                if (a.x1) v.y = a.x1[off];
+            } else {
+                v = a.in_c[off];
+            }
+        }
+        sm[g * L + l] = v;
+    }
+    __syncthreads();
+    if (a.fused) {
+        fft_smem(sm, L, a.logL, -1, a.tw);
+        // multiply by the folded real symbol; line (inner index i) enumerates axes 1..dim-1
+        const int np1 = a.n + 1;
+        int s0 = 1;
+        for (int d = 1; d < a.dim; ++d) s0 *= np1;
+        for (int q = 0; q < kPtsPerThread; ++q) {
+            const int p = threadIdx.x + q * kFftThreads;
+            const int g = p / L, l = p - g * L;
+            const int line = g0 + g;
+            if (line >= a.nlines) continue;
+            int tmp = line % a.ninner, off = 0, stride = 1;
+            for (int d = a.dim - 1; d >= 1; --d) {
+                const int k = tmp % L;
+                tmp /= L;
+                off += min(k, L - k) * stride;
+                stride *= np1;
+            }
+            const double lam = __ldg(a.sym + (int64_t)min(l, L - l) * s0 + off);
+            sm[p].x *= lam;
+            sm[p].y *= lam;
+        }
+        __syncthreads();
+        fft_smem(sm, L, a.logL, +1, a.tw);
+    } else {
+        fft_smem(sm, L, a.logL, a.sign, a.tw);
+    }
+    const bool contig_out = a.out_real ? true : (a.out_sl == 1);
+#pragma unroll 4
+    for (int q = 0; q < kPtsPerThread; ++q) {
+        const int p = threadIdx.x + q * kFftThreads;
+        int g, l;
+        if (contig_out) {
+            g = p / L;
+            l = p - g * L;
+        } else {
+            g = p % G;
+            l = p / G;
+        }
+        const int line = g0 + g;
+        if (line >= a.nlines || l >= a.n_out) continue;
+        const int o = line / a.ninner, i = line - o * a.ninner;
+        const int64_t off = (int64_t)o * a.out_so + (int64_t)i * a.out_si + (int64_t)l * a.out_sl;
+        const double2 v = sm[g * L + l];
+        if (a.out_real) {
+            a.y0[off] = v.x;
+            if (a.y1) a.y1[off] = v.y;
+        } else {
+            a.out_c[off] = v;
+        }
+    }
+}
+
+// Embedding of the generator, mirror-even per axis, index n left zero
+// (toeplitz.py:19-30): emb[k] = gen[fold(k)] with fold(k) = k (k<n),
+// 2n-k (k>n); entries from the same integer-distance formula as K1/K2.
+__global__ void k_embed(double2* emb, int dim, int n, EntryParams P, const LogEntry* tab) {
+    const int M = 2 * n;
+    int64_t tot = 1;
+    for (int d = 0; d < dim; ++d) tot *= M;
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= tot) return;
+    int64_t t = e;
+    int m = 0;
+    bool zero = false;
+    for (int d = 0; d < dim; ++d) {
+        const int k = (int)(t % M);
+        t /= M;
+        if (k == n) zero = true;
+        const int g = k < n ? k : M - k;
+        m += g * g;
+    }
+    emb[e] = make_double2(zero ? 0.0 : entry_from_m(P, tab, m), 0.0);
+}
+
+// sym[(k_0..k_{d-1}) folded, k <= n] = Re(emb_hat[k]) / M^dim
+__global__ void k_fold_symbol(const double2* emb, double* sym, int dim, int n, double scale) {
+    const int np1 = n + 1, M = 2 * n;
+    int64_t tot = 1;
+    for (int d = 0; d < dim; ++d) tot *= np1;
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e >= tot) return;
+    int64_t t = e, src = 0, mul = 1;
+    for (int d = dim - 1; d >= 0; --d) {
+        const int k = (int)(t % np1);
+        t /= np1;
+        src += (int64_t)k * mul;
+        mul *= M;
+    }
+    sym[e] = emb[src].x * scale;
+}
+
+}  // namespace ie
+
+// ------------------------------------------------------------- host side --
+struct ie_fft {
+    int dim, n, M, logM;
+    double2* d_tw;
+    double* d_sym;
+    double2* d_buf;
+};
+
+namespace ie {
+
+static int line_launch(const LineArgs& a, cudaStream_t st) {
+    const int G = kFftPoints / a.L;
+    const int ctas = (a.nlines + G - 1) / G;
+    const size_t smem = kFftPoints * sizeof(double2);
+    static bool attr = false;
+    if (!attr) {
+        IE_CUDA(cudaFuncSetAttribute(k_fft_lines, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        attr = true;
+    }
+    k_fft_lines<<<ctas, kFftThreads, smem, st>>>(a);
+    IE_LAUNCHED();
+    return IE_OK;
+}
+
+static LineArgs base_args(const ie_fft* f) {
+    LineArgs a{};
+    a.L = f->M;
+    a.logL = f->logM;
+    a.tw = f->d_tw;
+    a.sym = f->d_sym;
+    a.dim = f->dim;
+    a.n = f->n;
+    a.sign = -1;
+    return a;
+}
+
+// Full forward FFT along every axis of a complex M^dim array (symbol setup).
+static int fft_full_forward(const ie_fft* f, double2* buf, cudaStream_t st) {
+    const int M = f->M;
+    int64_t tot = 1;
+    for (int d = 0; d < f->dim; ++d) tot *= M;
+    for (int ax = f->dim - 1; ax >= 0; --ax) {
+        int64_t sl = 1;
+        for (int d = ax + 1; d < f->dim; ++d) sl *= M;
+        LineArgs a = base_args(f);
+        a.nlines = (int)(tot / M);
+        a.ninner = (int)sl;
+        a.in_c = buf;
+        a.out_c = buf;
+        a.in_so = a.out_so = sl * M;
+        a.in_si = a.out_si = 1;
+        a.in_sl = a.out_sl = sl;
+        a.n_in = a.n_out = M;
+        a.sign = -1;
+        int rc = line_launch(a, st);
+        if (rc) return rc;
+    }
+    return IE_OK;
+}
+
+int make_log_table_device(const ie_geom& g, LogEntry** d_tab, int* ntab);
+EntryParams entry_params(const ie_geom& g);
+
+int fft_create(const ie_geom& g, ie_fft** out) {
+    int n = g.n, logM = 0;
+    const int M = 2 * n;
+    while ((1 << logM) < M) ++logM;
+    if ((1 << logM) != M || M > kFftPoints || M < 4) {
+        set_error("fft matvec needs n a power of two with 2 <= n <= 2048");
+        return IE_ERR_ARG;
+    }
+    ie_fft* f = new ie_fft();
+    f->dim = g.dim;
+    f->n = n;
+    f->M = M;
+    f->logM = logM;
+    std::vector<double2> tw(M);
+    for (int m = 0; m < M; ++m) {
+        const long double ang = -2.0L * 3.141592653589793238462643383279502884L * (long double)m / (long double)M;
+        tw[m] = make_double2((double)cosl(ang), (double)sinl(ang));
+    }
+    int64_t totM = 1, totS = 1, totB = 1;
+    for (int d = 0; d < g.dim; ++d) {
+        totM *= M;
+        totS *= (n + 1);
+        totB *= (d == 0 ? n : M);
+    }
+    IE_CUDA(cudaMalloc(&f->d_tw, M * sizeof(double2)));
+    IE_CUDA(cudaMemcpy(f->d_tw, tw.data(), M * sizeof(double2), cudaMemcpyHostToDevice));
+    IE_CUDA(cudaMalloc(&f->d_sym, totS * sizeof(double)));
+    IE_CUDA(cudaMalloc(&f->d_buf, totB * sizeof(double2)));
+    // symbol: embed, full forward FFT, fold
+    double2* emb;
+    IE_CUDA(cudaMalloc(&emb, totM * sizeof(double2)));
+    LogEntry* tab;
+    int ntab;
+    int rc = make_log_table_device(g, &tab, &ntab);
+    if (rc) return rc;
+    k_embed<<<(unsigned)((totM + 255) / 256), 256>>>(emb, g.dim, n, entry_params(g), tab);
+    IE_LAUNCHED();
+    if ((rc = fft_full_forward(f, emb, 0))) return rc;
+    k_fold_symbol<<<(unsigned)((totS + 255) / 256), 256>>>(emb, f->d_sym, g.dim, n, 1.0 / (double)totM);
+    IE_LAUNCHED();
+    IE_CUDA(cudaDeviceSynchronize());
+    cudaFree(emb);
+    cudaFree(tab);
+    *out = f;
+    return IE_OK;
+}
+
+void fft_destroy(ie_fft* f) {
+    if (!f) return;
+    cudaFree(f->d_tw);
+    cudaFree(f->d_sym);
+    cudaFree(f->d_buf);
+    delete f;
+}
+
+// Y0 (+ i Y1) = A (X0 + i X1) over all N rows.
+int fft_matvec(const ie_fft* f, const double* X0, const double* X1, double* Y0, double* Y1, cudaStream_t st) {
+    const int n = f->n, M = f->M, d = f->dim;
+    int rc;
+    if (d == 1) {
+        LineArgs a = base_args(f);
+        a.nlines = 1;
+        a.ninner = 1;
+        a.in_real = 1;
+        a.x0 = X0;
+        a.x1 = X1;
+        a.in_sl = 1;
+        a.n_in = n;
+        a.out_real = 1;
+        a.y0 = Y0;
+        a.y1 = Y1;
+        a.out_sl = 1;
+        a.n_out = n;
+        a.fused = 1;
+        return line_launch(a, st);
+    }
+    double2* B = f->d_buf;
+    if (d == 2) {  // B: (n, M)
+        LineArgs a = base_args(f);  // rows a < n, forward along axis 1
+        a.nlines = n;
+        a.ninner = 1;
+        a.in_real = 1;
+        a.x0 = X0;
+        a.x1 = X1;
+        a.in_so = n;
+        a.in_sl = 1;
+        a.n_in = n;
+        a.out_c = B;
+        a.out_so = M;
+        a.out_sl = 1;
+        a.n_out = M;
+        if ((rc = line_launch(a, st))) return rc;
+        LineArgs c = base_args(f);  // columns: forward * sym * inverse along axis 0
+        c.nlines = M;
+        c.ninner = M;
+        c.in_c = B;
+        c.out_c = B;
+        c.in_si = c.out_si = 1;
+        c.in_sl = c.out_sl = M;
+        c.n_in = n;
+        c.n_out = n;
+        c.fused = 1;
+        if ((rc = line_launch(c, st))) return rc;
+        LineArgs e = base_args(f);  // rows a < n, inverse along axis 1 -> real pair
+        e.nlines = n;
+        e.ninner = 1;
+        e.in_c = B;
+        e.in_so = M;
+        e.in_sl = 1;
+        e.n_in = M;
+        e.out_real = 1;
+        e.y0 = Y0;
+        e.y1 = Y1;
+        e.out_so = n;
+        e.out_sl = 1;
+        e.n_out = n;
+        e.sign = +1;
+        return line_launch(e, st);
+    }
+    // d == 3, B: (n, M, M)
+    {
+        LineArgs a = base_args(f);  // lines (a<n, b<n) along axis 2
+        a.nlines = n * n;
+        a.ninner = n;
+        a.in_real = 1;
+        a.x0 = X0;
+        a.x1 = X1;
+        a.in_so = (int64_t)n * n;
+        a.in_si = n;
+        a.in_sl = 1;
+        a.n_in = n;
+        a.out_c = B;
+        a.out_so = (int64_t)M * M;
+        a.out_si = M;
+        a.out_sl = 1;
+        a.n_out = M;
+        if ((rc = line_launch(a, st))) return rc;
+    }
+    {
+        LineArgs b = base_args(f);  // lines (a<n, k3) along axis 1, forward
+        b.nlines = n * M;
+        b.ninner = M;
+        b.in_c = b.out_c = B;
+        b.in_so = b.out_so = (int64_t)M * M;
+        b.in_si = b.out_si = 1;
+        b.in_sl = b.out_sl = M;
+        b.n_in = n;
+        b.n_out = M;
+        if ((rc = line_launch(b, st))) return rc;
+    }
+    {
+        LineArgs c = base_args(f);  // lines (k2, k3) along axis 0, fused
+        c.nlines = M * M;
+        c.ninner = M * M;
+        c.in_c = c.out_c = B;
+        c.in_si = c.out_si = 1;
+        c.in_sl = c.out_sl = (int64_t)M * M;
+        c.n_in = n;
+        c.n_out = n;
+        c.fused = 1;
+        if ((rc = line_launch(c, st))) return rc;
+    }
+    {
+        LineArgs b = base_args(f);  // lines (a<n, k3) along axis 1, inverse, keep b<n
+        b.nlines = n * M;
+        b.ninner = M;
+        b.in_c = b.out_c = B;
+        b.in_so = b.out_so = (int64_t)M * M;
+        b.in_si = b.out_si = 1;
+        b.in_sl = b.out_sl = M;
+        b.n_in = M;
+        b.n_out = n;
+        b.sign = +1;
+        if ((rc = line_launch(b, st))) return rc;
+    }
+    LineArgs e = base_args(f);  // lines (a<n, b<n) along axis 2, inverse -> real pair
+    e.nlines = n * n;
+    e.ninner = n;
+    e.in_c = B;
+    e.in_so = (int64_t)M * M;
+    e.in_si = M;
+    e.in_sl = 1;
+    e.n_in = M;
+    e.out_real = 1;
+    e.y0 = Y0;
+    e.y1 = Y1;
+    e.out_so = (int64_t)n * n;
+    e.out_si = n;
+    e.out_sl = 1;
+    e.n_out = n;
+    e.sign = +1;
+    return line_launch(e, st);
+}
+
+}  // namespace ie

@@ -211,8 +211,18 @@ __global__ void k_matvec_reduce(MatvecArgs a, int nsplit) {
 }  // namespace ie
 
 // ------------------------------------------------------------- host side --
+struct ie_fft;
+namespace ie {
+int fft_create(const ie_geom& g, ie_fft** out);
+void fft_destroy(ie_fft* f);
+int fft_matvec(const ie_fft* f, const double* X0, const double* X1, double* Y0, double* Y1, cudaStream_t st);
+}  // namespace ie
+
 struct ie_matvec {
     ie_geom g;
+    int method;     // IE_MATVEC_DIRECT / IE_MATVEC_FFT
+    ie_fft* fft;    // FFT plan (method FFT)
+    double* d_full; // FFT path: full-range output for partial row requests
     int N;
     ie::LogEntry* d_tab;
     int ntab;
@@ -289,6 +299,17 @@ static int launch_dim(const ie_matvec* m, MatvecArgs a, cudaStream_t st) {
 
 int matvec_launch(const ie_matvec* m, const double* X, int64_t ldx, int nrhs, double* Y, int64_t ldy,
                   int64_t row_begin, int64_t row_end, cudaStream_t st) {
+    if (m->method == IE_MATVEC_FFT) {
+        const double* X1 = nrhs == 2 ? X + ldx : nullptr;
+        if (row_begin == 0 && row_end == m->N)
+            return fft_matvec(m->fft, X, X1, Y, nrhs == 2 ? Y + ldy : nullptr, st);
+        int rc = fft_matvec(m->fft, X, X1, m->d_full, nrhs == 2 ? m->d_full + m->N : nullptr, st);
+        if (rc) return rc;
+        for (int q = 0; q < nrhs; ++q)
+            IE_CUDA(cudaMemcpyAsync(Y + q * ldy, m->d_full + (int64_t)q * m->N + row_begin,
+                                    (row_end - row_begin) * sizeof(double), cudaMemcpyDeviceToDevice, st));
+        return IE_OK;
+    }
     MatvecArgs a;
     a.X = X;
     a.ldx = ldx;
@@ -337,7 +358,11 @@ __global__ void k_assemble(int dim, int n, EntryParams P, const LogEntry* tab, c
 }  // namespace ie
 
 extern "C" int ie_matvec_create(const ie_geom* g, ie_matvec** out) {
-    if (!g || !out || g->dim < 1 || g->dim > 3 || g->n < 2) {
+    return ie_matvec_create_method(g, IE_MATVEC_DIRECT, out);
+}
+
+extern "C" int ie_matvec_create_method(const ie_geom* g, int32_t method, ie_matvec** out) {
+    if (!g || !out || g->dim < 1 || g->dim > 3 || g->n < 2 || (method != IE_MATVEC_DIRECT && method != IE_MATVEC_FFT)) {
         ie::set_error("ie_matvec_create: bad geometry");
         return IE_ERR_ARG;
     }
@@ -349,6 +374,23 @@ extern "C" int ie_matvec_create(const ie_geom* g, ie_matvec** out) {
     ie_matvec* m = new ie_matvec();
     m->g = *g;
     m->N = (int)Nd;
+    m->method = method;
+    m->fft = nullptr;
+    m->d_full = nullptr;
+    if (method == IE_MATVEC_FFT) {
+        int rc = ie::fft_create(*g, &m->fft);
+        if (rc) {
+            delete m;
+            return rc;
+        }
+        cudaError_t e = cudaMalloc(&m->d_full, 2 * (size_t)m->N * sizeof(double));
+        if (e != cudaSuccess) {
+            ie::set_error(cudaGetErrorString(e));
+            ie::fft_destroy(m->fft);
+            delete m;
+            return IE_ERR_CUDA;
+        }
+    }
     m->alpha = ie::entry_params(*g).alpha;
     int rc = ie::make_log_table_device(*g, &m->d_tab, &m->ntab);
     if (rc) {
@@ -383,6 +425,8 @@ extern "C" int ie_matvec_create(const ie_geom* g, ie_matvec** out) {
 
 extern "C" void ie_matvec_destroy(ie_matvec* m) {
     if (!m) return;
+    if (m->fft) ie::fft_destroy(m->fft);
+    if (m->d_full) cudaFree(m->d_full);
     cudaFree(m->d_tab);
     if (m->d_work) cudaFree(m->d_work);
     delete m;

@@ -195,7 +195,10 @@ struct ApplyArgs {
 
 // z_k = A_k^{-1} r_k with the packed upper triangle by columns: column j
 // contributes its dot with r[0..j] to z_j and r_j * A[0..j-1, j] to z[0..j-1].
-template <int T>
+// U columns are processed together: their loads are issued before any of
+// their warp reductions, so each warp keeps U*(tj+1) 256-B requests in
+// flight (the kernel is HBM-latency bound without it).
+template <int T, int U>
 __global__ void __launch_bounds__(256) k_apply_packed(ApplyArgs a) {
     extern __shared__ double red[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -217,23 +220,41 @@ __global__ void __launch_bounds__(256) k_apply_packed(ApplyArgs a) {
 #pragma unroll
     for (int tj = 0; tj < T; ++tj) {
         if (32 * tj < s) {
-            for (int jj = w; jj < 32; jj += a.wpb) {
-                const int j = 32 * tj + jj;
-                if (j >= s) break;
-                const double* colp = fac + ((int64_t)j * (j + 1)) / 2;
-                const double rj = __shfl_sync(kFull, rr[tj], jj);
-                double d = 0.0;
+            for (int jb = w * U; jb < 32; jb += a.wpb * U) {
+                double v[U][T];
+                double rj[U];
 #pragma unroll
-                for (int t = 0; t <= tj; ++t) {
-                    const int i = 32 * t + lane;
-                    if (t < tj || lane <= jj) {
-                        const double v = __ldg(colp + i);
-                        d = fma(v, rr[t], d);
-                        if (t < tj || lane < jj) zz[t] = fma(v, rj, zz[t]);
+                for (int u = 0; u < U; ++u) {
+                    const int jj = jb + u;
+                    const int j = 32 * tj + jj;
+                    const bool okj = j < s;
+                    const double* colp = fac + ((int64_t)j * (j + 1)) / 2;
+                    rj[u] = __shfl_sync(kFull, rr[tj], jj);
+#pragma unroll
+                    for (int t = 0; t <= tj; ++t) {
+                        const int i = 32 * t + lane;
+                        const bool ok = okj && (t < tj || lane <= jj);
+                        v[u][t] = ok ? __ldg(colp + i) : 0.0;
                     }
                 }
-                d = warp_sum(d);
-                if (lane == jj) zz[tj] += d;
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    const int jj = jb + u;
+                    double d = 0.0;
+#pragma unroll
+                    for (int t = 0; t <= tj; ++t) {
+                        d = fma(v[u][t], rr[t], d);
+                        if (t < tj || lane < jj) zz[t] = fma(v[u][t], rj[u], zz[t]);
+                    }
+                    v[u][0] = d;
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                    for (int u = 0; u < U; ++u) v[u][0] += __shfl_xor_sync(kFull, v[u][0], o);
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (lane == jb + u && 32 * tj + jb + u < s) zz[tj] += v[u][0];
             }
         }
     }
@@ -425,9 +446,11 @@ static void launch_apply_T(const ie_precond* p, ApplyArgs a, cudaStream_t st) {
     if (p->variant == IE_VARIANT_SUBST) {
         k_apply_subst<T><<<ctas, 32 * p->bpc, 0, st>>>(a);
     } else {
+        constexpr int U = T <= 2 ? 4 : (T <= 8 ? 2 : 1);
         const size_t sm = p->wpb > 1 ? (size_t)p->bpc * p->wpb * T * 32 * sizeof(double) : 0;
-        if (sm > 48 * 1024) cudaFuncSetAttribute(k_apply_packed<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        k_apply_packed<T><<<ctas, 32 * p->wpb * p->bpc, sm, st>>>(a);
+        if (sm > 48 * 1024)
+            cudaFuncSetAttribute(k_apply_packed<T, U>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        k_apply_packed<T, U><<<ctas, 32 * p->wpb * p->bpc, sm, st>>>(a);
     }
 }
 

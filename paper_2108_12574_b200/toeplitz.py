@@ -5,7 +5,9 @@ toeplitz.py:11-57): same constructor argument, ``shape``, ``matvec`` (1-D
 float64 array of length N in, fresh array out, ValueError mentioning
 "length" otherwise) and ``@``.  The reference evaluates A x by circulant
 FFT; here K1 (csrc/matvec.cu) evaluates the log-r / 1/r kernel on the fly
-for every pair (BASELINE.json north star, component (1)).
+for every pair (BASELINE.json north star, component (1)); ToeplitzMatvec
+defaults to K1b, the same circulant-FFT algorithm as the reference, on the
+device.
 
 Device API: ``matvec_device(X, Y, nrhs, row_begin, row_end)`` takes torch
 CUDA float64 tensors and enqueues on the current stream without a host sync.
@@ -39,17 +41,36 @@ def to_host(t, was_numpy: bool):
     return t.cpu().numpy() if was_numpy else t
 
 
-class KernelMatvec:
-    """Direct-sum FP64 matvec with the kernel evaluated on the fly (K1)."""
+def fft_supported(n: int) -> bool:
+    """The FFT path needs n a power of two with 2 <= n <= 2048 (M = 2n <= 4096)."""
+    return 2 <= n <= 2048 and (n & (n - 1)) == 0
 
-    def __init__(self, op: KernelOperator):
+
+class KernelMatvec:
+    """Device matvec y = A x.
+
+    method="direct" (default here): K1, the O(N^2) matrix-free sum with the
+    log-r / 1/r kernel evaluated for every pair (csrc/matvec.cu).
+    method="fft": K1b, the reference's circulant-embedding FFT algorithm in
+    hand-written FP64 Stockham kernels (csrc/fft.cu).
+    """
+
+    def __init__(self, op: KernelOperator, method: str = "direct"):
+        if method == "auto":
+            method = "fft" if fft_supported(op.grid.n_per_dim) else "direct"
+        if method not in _lib.MATVEC_METHODS:
+            raise ValueError(f"method must be one of {tuple(_lib.MATVEC_METHODS)} or 'auto', got {method!r}")
+        if method == "fft" and not fft_supported(op.grid.n_per_dim):
+            raise ValueError(f"method='fft' needs n_per_dim a power of two <= 2048, got {op.grid.n_per_dim}")
         self.op = op
+        self.method = method
         self.dim = op.grid.dim
         self.n = op.grid.n_per_dim
         self.N = op.n
         self._lib = _lib.lib()
         h = ctypes.c_void_p()
-        _lib.check(self._lib.ie_matvec_create(op.geom(), ctypes.byref(h)), "ToeplitzMatvec")
+        _lib.check(self._lib.ie_matvec_create_method(op.geom(), _lib.MATVEC_METHODS[method], ctypes.byref(h)),
+                   "ToeplitzMatvec")
         self._handle = h
 
     def __del__(self):
@@ -89,8 +110,14 @@ class KernelMatvec:
         return self.matvec(v)
 
 
-ToeplitzMatvec = KernelMatvec
+class ToeplitzMatvec(KernelMatvec):
+    """Drop-in for the reference's ToeplitzMatvec: method="auto" picks the
+    FFT algorithm the reference uses whenever n is a power of two <= 2048,
+    else the direct sum."""
+
+    def __init__(self, op: KernelOperator, method: str = "auto"):
+        super().__init__(op, method=method)
 
 
-def build_matvec(op: KernelOperator) -> KernelMatvec:
-    return KernelMatvec(op)
+def build_matvec(op: KernelOperator, method: str = "auto") -> KernelMatvec:
+    return ToeplitzMatvec(op, method=method)

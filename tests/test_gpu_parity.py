@@ -32,17 +32,27 @@ def rel(a, b):
     return np.linalg.norm(np.asarray(a) - np.asarray(b)) / np.linalg.norm(np.asarray(b))
 
 
+METHODS = ["direct", "fft"]
+
+
+def _mv(ie, op, method):
+    if method == "fft" and not ie.toeplitz.fft_supported(op.grid.n_per_dim):
+        pytest.skip("fft method needs n a power of two")
+    return ie.KernelMatvec(op, method=method)
+
+
 MV_CASES = ["2_8_span", "2_32_span", "2_16_cell", "3_8_cell", "1_16_cell", "2_32_cell", "3_4_cell",
             "2_12_cell", "2_10_span"]
 
 
 class TestMatvec:
     @pytest.mark.parametrize("case", MV_CASES)
-    def test_vs_golden(self, ie, golden, case):
+    @pytest.mark.parametrize("method", METHODS)
+    def test_vs_golden(self, ie, golden, case, method):
         g = golden("ref_small")
         dim, n, lat = case.split("_")
         op = ie.build_operator(ie.build_grid(int(dim), int(n)), lattice=lat)
-        mv = ie.ToeplitzMatvec(op)
+        mv = _mv(ie, op, method)
         x = g[f"mv_{case}_x"]
         y = mv.matvec(x)
         assert rel(y, g[f"mv_{case}_y"]) <= 1e-12
@@ -69,7 +79,7 @@ class TestMatvec:
     def test_two_rhs_and_row_ranges_bitwise(self, ie, dim, n):
         import torch
         op = ie.build_operator(ie.build_grid(dim, n), lattice="cell")
-        mv = ie.ToeplitzMatvec(op)
+        mv = ie.KernelMatvec(op, method="direct")
         N = op.n
         rng = np.random.default_rng(5)
         X = torch.from_numpy(rng.standard_normal((2, N))).cuda()
@@ -90,11 +100,32 @@ class TestMatvec:
                 parts.append(yy)
             assert torch.equal(torch.cat(parts), y0)
 
-    def test_matches_fft_large(self, ie):
+    @pytest.mark.parametrize("dim,n", [(2, 32), (2, 256), (3, 16), (3, 32), (1, 64), (2, 1024)])
+    def test_fft_two_rhs_and_ranges(self, ie, dim, n):
+        import torch
+        op = ie.build_operator(ie.build_grid(dim, n), lattice="cell")
+        mv = ie.KernelMatvec(op, method="fft")
+        N = op.n
+        X = torch.from_numpy(np.random.default_rng(6).standard_normal((2, N))).cuda()
+        Y2 = torch.empty_like(X)
+        mv.matvec_device(X, Y2, nrhs=2)
+        ref = [O.FFTMatvec(O.build_operator(O.build_grid(dim, n), "cell")).matvec(X[q].cpu().numpy())
+               for q in range(2)]
+        for q in range(2):
+            y1 = torch.empty(N, dtype=torch.float64, device="cuda")
+            mv.matvec_device(X[q], y1)
+            assert rel(Y2[q].cpu().numpy(), ref[q]) <= 1e-13
+            assert rel(y1.cpu().numpy(), ref[q]) <= 1e-13
+        yy = torch.empty(N // 2, dtype=torch.float64, device="cuda")
+        mv.matvec_device(X[0], yy, row_begin=N // 4, row_end=N // 4 + N // 2)
+        assert rel(yy.cpu().numpy(), ref[0][N // 4: N // 4 + N // 2]) <= 1e-13
+
+    @pytest.mark.parametrize("method", METHODS)
+    def test_matches_fft_large(self, ie, method):
         # config-3 operator: 65,536 rows
         op = ie.build_operator(ie.build_grid(2, 256), lattice="cell")
         x = np.random.default_rng(1).standard_normal(op.n)
-        y = ie.ToeplitzMatvec(op).matvec(x)
+        y = ie.KernelMatvec(op, method=method).matvec(x)
         yr = O.FFTMatvec(O.build_operator(O.build_grid(2, 256), "cell")).matvec(x)
         assert rel(y, yr) <= 1e-12
 
@@ -206,11 +237,12 @@ def _pcg_check(rep, u, g, kind, u_tol=1e-10):
 
 
 class TestPCG:
-    def test_c1(self, ie, golden):
+    @pytest.mark.parametrize("method", METHODS)
+    def test_c1(self, ie, golden, method):
         g = golden("ref_c1")
         grid = ie.build_grid(2, 32)
         op = ie.build_operator(grid, lattice="cell")
-        mv = ie.ToeplitzMatvec(op)
+        mv = ie.KernelMatvec(op, method=method)
         f = np.random.default_rng(0).standard_normal(op.n)
         for kind in ("schwarz", "jacobi"):
             for variant in ("packed_inverse", "subst"):
@@ -219,20 +251,22 @@ class TestPCG:
                 _pcg_check(rep, u, g, kind)
                 assert rep.t_pcg > 0 and rep.t_s > 0
 
-    def test_c3(self, ie, golden):
+    @pytest.mark.parametrize("method", METHODS)
+    def test_c3(self, ie, golden, method):
         g = golden("ref_c3")
         grid = ie.build_grid(2, 256)
         op = ie.build_operator(grid, lattice="cell")
         pre = ie.from_decomposition(op, ie.build_decomposition(grid, 32, 2, "schwarz"))
         f = np.random.default_rng(1).standard_normal(op.n)
-        u, rep = ie.solve(ie.ToeplitzMatvec(op), pre, f, tol=1e-10)
+        u, rep = ie.solve(ie.KernelMatvec(op, method=method), pre, f, tol=1e-10)
         _pcg_check(rep, u, g, "schwarz")
 
-    def test_c4(self, ie, golden):
+    @pytest.mark.parametrize("method", METHODS)
+    def test_c4(self, ie, golden, method):
         g = golden("ref_c4")
         grid = ie.build_grid(3, 32)
         op = ie.build_operator(grid, lattice="cell")
-        mv = ie.ToeplitzMatvec(op)
+        mv = ie.KernelMatvec(op, method=method)
         pre = ie.from_decomposition(op, ie.build_decomposition(grid, 4, 1, "schwarz"))
         f = np.random.default_rng(2).standard_normal(op.n)
         u, rep = ie.solve(mv, pre, f, tol=1e-10)
@@ -243,13 +277,14 @@ class TestPCG:
         assert abs(lam - lr) <= 1e-8 * abs(lr)
 
     @pytest.mark.slow
-    def test_c5_50_iterations(self, ie, golden):
+    @pytest.mark.parametrize("method", METHODS)
+    def test_c5_50_iterations(self, ie, golden, method):
         g = golden("ref_c5")
         grid = ie.build_grid(2, 1024)
         op = ie.build_operator(grid, lattice="cell")
         pre = ie.from_decomposition(op, ie.build_decomposition(grid, 128, 2, "schwarz"))
         f = np.random.default_rng(3).standard_normal(op.n)
-        u, rep = ie.solve(ie.ToeplitzMatvec(op), pre, f, tol=1e-10, max_iters=50)
+        u, rep = ie.solve(ie.KernelMatvec(op, method=method), pre, f, tol=1e-10, max_iters=50)
         assert rep.n_it == 50 and not rep.converged
         h, hr = np.array(rep.residual_history), g["schwarz_hist"]
         assert np.max(np.abs(h[:10] - hr[:10]) / hr[:10]) <= 1e-8
@@ -341,11 +376,12 @@ class TestPCG:
 
 
 class TestLanczos:
-    def test_c2(self, ie, golden):
+    @pytest.mark.parametrize("method", METHODS)
+    def test_c2(self, ie, golden, method):
         g = golden("ref_c2")
         grid = ie.build_grid(2, 64)
         op = ie.build_operator(grid, lattice="cell")
-        mv = ie.ToeplitzMatvec(op)
+        mv = ie.KernelMatvec(op, method=method)
         for kind in ("schwarz", "jacobi"):
             pre = ie.from_decomposition(op, ie.build_decomposition(grid, 8, 1, kind))
             for which in ("min", "max"):
