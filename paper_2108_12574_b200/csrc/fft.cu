@@ -52,7 +52,74 @@ struct LineArgs {
     int dim;
     int n;
     const double2* tw;  // tw[m] = exp(-2 pi i m / L)
+    // exact power-of-two column scaling for 2-RHS packing: input columns are
+    // multiplied by 2^-e_c (max|x_c| ~ 1) and outputs by 2^e_c, so the
+    // rounding of one column never contaminates the other (PCG's p and u
+    // differ by up to ~1e10 in norm).  amax = per-chunk partial max|x_c|.
+    const double* amax;
+    int namax;
+    int scale_in;
+    int scale_out;
+    const int* stop;  // device flag: nonzero -> no-op (PCG early exit)
 };
+
+// 2^-e with 2^e >= max|x| (power of two, exact); 1 for max == 0
+__device__ __forceinline__ double pow2_scale(double mx) {
+    if (!(mx > 0.0) || !isfinite(mx)) return 1.0;
+    int e;
+    frexp(mx, &e);
+    return ldexp(1.0, -e);
+}
+
+__device__ void column_scales(const LineArgs& a, double* sc) {
+    __shared__ double red[2][kFftThreads];
+    double m0 = 0.0, m1 = 0.0;
+    for (int c = threadIdx.x; c < a.namax; c += blockDim.x) {
+        m0 = fmax(m0, a.amax[2 * c]);
+        m1 = fmax(m1, a.amax[2 * c + 1]);
+    }
+    red[0][threadIdx.x] = m0;
+    red[1][threadIdx.x] = m1;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) {
+            red[0][threadIdx.x] = fmax(red[0][threadIdx.x], red[0][threadIdx.x + o]);
+            red[1][threadIdx.x] = fmax(red[1][threadIdx.x], red[1][threadIdx.x + o]);
+        }
+        __syncthreads();
+    }
+    sc[0] = pow2_scale(red[0][0]);
+    sc[1] = pow2_scale(red[1][0]);
+}
+
+// per-2048-chunk max|x0|, max|x1|
+__global__ void k_absmax2(const double* x0, const double* x1, int N, double* part, const int* stop) {
+    if (stop && *stop) return;
+    __shared__ double r0[256], r1[256];
+    const int base = blockIdx.x * 2048;
+    double m0 = 0.0, m1 = 0.0;
+    for (int e = 0; e < 8; ++e) {
+        const int i = base + e * 256 + threadIdx.x;
+        if (i < N) {
+            m0 = fmax(m0, fabs(x0[i]));
+            m1 = fmax(m1, fabs(x1[i]));
+        }
+    }
+    r0[threadIdx.x] = m0;
+    r1[threadIdx.x] = m1;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) {
+            r0[threadIdx.x] = fmax(r0[threadIdx.x], r0[threadIdx.x + o]);
+            r1[threadIdx.x] = fmax(r1[threadIdx.x], r1[threadIdx.x + o]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        part[2 * blockIdx.x] = r0[0];
+        part[2 * blockIdx.x + 1] = r1[0];
+    }
+}
 
 __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
     return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
@@ -122,6 +189,12 @@ __device__ void fft_smem(double2* sm, int L, int logL, int sign, const double2* 
 
 __global__ void __launch_bounds__(kFftThreads) k_fft_lines(LineArgs a) {
     extern __shared__ __align__(16) double2 sm[];
+    if (a.stop && *a.stop) return;
+    __shared__ double csc[2];
+    if (a.scale_in || a.scale_out) {
+        column_scales(a, csc);
+        __syncthreads();
+    }
     const int L = a.L;
     const int G = kFftPoints / L;
     const int g0 = blockIdx.x * G;
@@ -146,6 +219,10 @@ __global__ void __launch_bounds__(kFftThreads) k_fft_lines(LineArgs a) {
             if (a.in_real) {
                 v.x = a.x0[off];
                 if (a.x1) v.y = a.x1[off];
+                if (a.scale_in) {
+                    v.x *= csc[0];
+                    v.y *= csc[1];
+                }
             } else {
                 v = a.in_c[off];
             }
@@ -196,8 +273,12 @@ __global__ void __launch_bounds__(kFftThreads) k_fft_lines(LineArgs a) {
         if (line >= a.nlines || l >= a.n_out) continue;
         const int o = line / a.ninner, i = line - o * a.ninner;
         const int64_t off = (int64_t)o * a.out_so + (int64_t)i * a.out_si + (int64_t)l * a.out_sl;
-        const double2 v = sm[g * L + l];
+        double2 v = sm[g * L + l];
         if (a.out_real) {
+            if (a.scale_out) {
+                v.x /= csc[0];  // exact: powers of two
+                v.y /= csc[1];
+            }
             a.y0[off] = v.x;
             if (a.y1) a.y1[off] = v.y;
         } else {
@@ -250,9 +331,11 @@ __global__ void k_fold_symbol(const double2* emb, double* sym, int dim, int n, d
 // ------------------------------------------------------------- host side --
 struct ie_fft {
     int dim, n, M, logM;
+    int N;
     double2* d_tw;
     double* d_sym;
     double2* d_buf;
+    double* d_amax;  // 2 * ceil(N/2048) partial maxima
 };
 
 namespace ie {
@@ -273,6 +356,8 @@ static int line_launch(const LineArgs& a, cudaStream_t st) {
 
 static LineArgs base_args(const ie_fft* f) {
     LineArgs a{};
+    a.amax = f->d_amax;
+    a.namax = (f->N + 2047) / 2048;
     a.L = f->M;
     a.logL = f->logM;
     a.tw = f->d_tw;
@@ -323,6 +408,9 @@ int fft_create(const ie_geom& g, ie_fft** out) {
     f->n = n;
     f->M = M;
     f->logM = logM;
+    f->N = 1;
+    for (int d = 0; d < g.dim; ++d) f->N *= n;
+    IE_CUDA(cudaMalloc(&f->d_amax, 2 * (size_t)((f->N + 2047) / 2048) * sizeof(double)));
     std::vector<double2> tw(M);
     for (int m = 0; m < M; ++m) {
         const long double ang = -2.0L * 3.141592653589793238462643383279502884L * (long double)m / (long double)M;
@@ -362,13 +450,28 @@ void fft_destroy(ie_fft* f) {
     cudaFree(f->d_tw);
     cudaFree(f->d_sym);
     cudaFree(f->d_buf);
+    cudaFree(f->d_amax);
     delete f;
 }
 
 // Y0 (+ i Y1) = A (X0 + i X1) over all N rows.
-int fft_matvec(const ie_fft* f, const double* X0, const double* X1, double* Y0, double* Y1, cudaStream_t st) {
+int fft_matvec(const ie_fft* f, const double* X0, const double* X1, double* Y0, double* Y1, cudaStream_t st,
+               const int* stop) {
     const int n = f->n, M = f->M, d = f->dim;
     int rc;
+    const int two = X1 != nullptr;
+    if (two) {
+        k_absmax2<<<(f->N + 2047) / 2048, 256, 0, st>>>(X0, X1, f->N, f->d_amax, stop);
+        IE_LAUNCHED();
+    }
+    auto line_launch = [&](LineArgs a, cudaStream_t s) -> int {
+        a.stop = stop;
+        if (two) {
+            a.scale_in = a.in_real;
+            a.scale_out = a.out_real;
+        }
+        return ::ie::line_launch(a, s);
+    };
     if (d == 1) {
         LineArgs a = base_args(f);
         a.nlines = 1;

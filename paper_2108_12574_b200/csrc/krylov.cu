@@ -16,6 +16,8 @@
 #include <math.h>
 
 #include <chrono>
+#include <mutex>
+#include <string>
 #include <vector>
 
 #include "common.cuh"
@@ -26,8 +28,9 @@ struct ie_precond;
 namespace ie {
 
 int matvec_launch(const ie_matvec* m, const double* X, int64_t ldx, int nrhs, double* Y, int64_t ldy,
-                  int64_t row_begin, int64_t row_end, cudaStream_t st);
-int precond_apply(const ie_precond* p, const double* r, double* z, double* partials, cudaStream_t st);
+                  int64_t row_begin, int64_t row_end, cudaStream_t st, const int* stop);
+int precond_apply(const ie_precond* p, const double* r, double* z, double* partials, cudaStream_t st,
+                  const int* stop);
 int matvec_N(const ie_matvec* m);
 
 constexpr int kChunk = 2048;
@@ -72,48 +75,102 @@ __device__ double reduce_partials(const double* part, int nch, double* sh) {
     return block_tree(loc, sh);
 }
 
-struct Scal {
-    double rho, alpha, beta, denom, rel, nf;
-    double pad[2];
+// Device-resident PCG state.  Every iteration kernel returns immediately
+// once `stop` is set, so the host can enqueue iterations ahead and read the
+// status once per batch (pcg.py's control flow runs in k_control_a).
+struct PcgState {
+    double rho, alpha, beta, denom, nf, tol, fail_value, pad;
+    long long max_iters, n_it, fail_iter;
+    int status;  // 0 running, 1 converged, 2 stagnated, 3 max_iters, 4 breakdown, 5 non-finite
+    int stop;
 };
 
-__global__ void k_set_nf(const double* part, int nch, Scal* sc) {
+__global__ void k_pcg_init(const double* part, int nch, PcgState* s, double tol, long long max_iters,
+                           double* hist) {
     __shared__ double sh[kRed];
     const double v = reduce_partials(part, nch, sh);
-    if (threadIdx.x == 0) sc->nf = sqrt(v);
+    if (threadIdx.x == 0) {
+        s->nf = sqrt(v);
+        s->tol = tol;
+        s->max_iters = max_iters;
+        s->n_it = 0;
+        s->fail_iter = 0;
+        s->fail_value = 0.0;
+        s->status = 0;
+        s->stop = 0;
+        hist[0] = 1.0;
+        if (s->nf == 0.0) {  // pcg.py:74-78
+            hist[0] = 0.0;
+            s->status = 1;
+            s->stop = 1;
+        }
+    }
 }
 
-// After the A-pass: denom = p.q, alpha = rho/denom (when do_p);
-// rel = ||f - w|| / ||f|| (when pending).
+// After the A-pass of iteration `it`: residual check of iteration it-1
+// (pcg.py:107-119), then the breakdown test and alpha of iteration it
+// (pcg.py:98-104) -- the reference's order.
 __global__ void k_control_a(const double* part_pq, const double* part_res, int nch, int do_p, int pending,
-                            Scal* sc) {
+                            long long it, PcgState* s, double* hist) {
     __shared__ double sh[kRed];
+    if (s->stop) return;
     double denom = 0.0, res2 = 0.0;
     if (do_p) denom = reduce_partials(part_pq, nch, sh);
     __syncthreads();
     if (pending) res2 = reduce_partials(part_res, nch, sh);
-    if (threadIdx.x == 0) {
-        if (do_p) {
-            sc->denom = denom;
-            sc->alpha = sc->rho / denom;
+    if (threadIdx.x != 0) return;
+    const long long k = it - 1;
+    if (pending) {
+        const double rel = sqrt(res2) / s->nf;
+        if (!isfinite(rel)) {
+            s->status = 5;
+            s->fail_iter = k;
+            s->fail_value = rel;
+        } else {
+            hist[k] = rel;
+            if (rel <= s->tol) {
+                s->status = 1;
+            } else if (k >= 30 && rel > (1.0 - 1e-3) * hist[k - 30]) {
+                s->status = 2;
+            } else if (!do_p) {
+                s->status = 3;
+            }
         }
-        if (pending) sc->rel = sqrt(res2) / sc->nf;
+        if (s->status) {
+            s->n_it = k;
+            s->stop = 1;
+            return;
+        }
+    }
+    if (do_p) {
+        if (!isfinite(denom) || denom <= 0.0) {
+            s->status = 4;
+            s->fail_iter = it;
+            s->fail_value = denom;
+            s->n_it = k;
+            s->stop = 1;
+            return;
+        }
+        s->denom = denom;
+        s->alpha = s->rho / denom;
     }
 }
 
-// After the apply: rho' = r.z, beta = rho'/rho, rho = rho'.
-__global__ void k_control_b(const double* part_rz, int nch, int first, Scal* sc) {
+// rho' = r.z, beta = rho'/rho, rho = rho'
+__global__ void k_control_b(const double* part_rz, int nch, int first, PcgState* s) {
     __shared__ double sh[kRed];
+    if (s->stop) return;
     const double rz = reduce_partials(part_rz, nch, sh);
     if (threadIdx.x == 0) {
-        if (!first) sc->beta = rz / sc->rho;
-        sc->rho = rz;
+        if (!first) s->beta = rz / s->rho;
+        s->rho = rz;
     }
 }
 
 __global__ void k_post_pass(const double* p, const double* q, const double* f, const double* w, int N, int do_p,
-                            int pending, double* part_pq, double* part_res) {
+                            int pending, double* part_pq, double* part_res, const int* stop) {
     __shared__ double sh[kRed];
+    if (*stop) return;
     const int base = blockIdx.x * kChunk;
     double a = 0.0, b = 0.0;
 #pragma unroll
@@ -139,19 +196,27 @@ __global__ void k_post_pass(const double* p, const double* q, const double* f, c
 }
 
 // u += alpha p; r -= alpha q  (products rounded first, as numpy does)
-__global__ void k_update_ur(double* u, double* r, const double* p, const double* q, const Scal* sc, int N) {
+__global__ void k_update_ur(double* u, double* r, const double* p, const double* q, const PcgState* s, int N) {
+    if (s->stop) return;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= N) return;
-    const double al = sc->alpha;
+    const double al = s->alpha;
     u[i] = __dadd_rn(u[i], __dmul_rn(al, p[i]));
     r[i] = __dsub_rn(r[i], __dmul_rn(al, q[i]));
 }
 
 // p = z + beta p
-__global__ void k_update_p(double* p, const double* z, const Scal* sc, int N) {
+__global__ void k_update_p(double* p, const double* z, const PcgState* s, int N) {
+    if (s->stop) return;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= N) return;
-    p[i] = __dadd_rn(z[i], __dmul_rn(sc->beta, p[i]));
+    p[i] = __dadd_rn(z[i], __dmul_rn(s->beta, p[i]));
+}
+
+__global__ void k_copy_if_running(double* dst, const double* src, int N, const int* stop) {
+    if (*stop) return;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < N) dst[i] = src[i];
 }
 
 __global__ void k_scale_div(double* x, const double* src, double d, int N) {
@@ -245,9 +310,89 @@ struct DevBuf {
 
 }  // namespace ie
 
+
 using namespace ie;
 
 static inline unsigned g1(int64_t n) { return (unsigned)((n + 255) / 256); }
+
+namespace ie {
+
+// Reusable PCG workspace (device vectors, partials, state, pinned status,
+// events), cached per (N, history capacity) so repeated solves pay no
+// allocation; a busy workspace is never shared between concurrent solves.
+struct PcgWork {
+    int N = 0;
+    int64_t cap = 0;
+    double *PU = nullptr, *QW = nullptr, *r = nullptr, *z = nullptr, *part = nullptr, *hist = nullptr;
+    PcgState* st = nullptr;
+    PcgState* host = nullptr;
+    std::vector<cudaEvent_t> ev;
+    bool busy = false;
+    ~PcgWork() {
+        cudaFree(PU);
+        cudaFree(QW);
+        cudaFree(r);
+        cudaFree(z);
+        cudaFree(part);
+        cudaFree(hist);
+        cudaFree(st);
+        if (host) cudaFreeHost(host);
+        for (auto e : ev) cudaEventDestroy(e);
+    }
+};
+
+static std::mutex g_work_mu;
+static std::vector<PcgWork*> g_work;
+
+static PcgWork* work_acquire(int N, int64_t cap, int* rc) {
+    {
+        std::lock_guard<std::mutex> lk(g_work_mu);
+        for (PcgWork* w : g_work)
+            if (!w->busy && w->N == N && w->cap >= cap) {
+                w->busy = true;
+                return w;
+            }
+    }
+    PcgWork* w = new PcgWork();
+    w->N = N;
+    w->cap = cap;
+    const int nch = dot_chunks(N);
+    cudaError_t e = cudaSuccess;
+    if (e == cudaSuccess) e = cudaMalloc(&w->PU, 2 * (size_t)N * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&w->QW, 2 * (size_t)N * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&w->r, (size_t)N * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&w->z, (size_t)N * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&w->part, 3 * (size_t)nch * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&w->hist, (size_t)cap * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&w->st, sizeof(PcgState));
+    if (e == cudaSuccess) e = cudaMallocHost(&w->host, sizeof(PcgState));
+    if (e != cudaSuccess) {
+        set_error(std::string("pcg workspace: ") + cudaGetErrorString(e));
+        delete w;
+        *rc = IE_ERR_CUDA;
+        return nullptr;
+    }
+    w->busy = true;
+    std::lock_guard<std::mutex> lk(g_work_mu);
+    g_work.push_back(w);
+    return w;
+}
+
+static void work_release(PcgWork* w) {
+    std::lock_guard<std::mutex> lk(g_work_mu);
+    w->busy = false;
+}
+
+static int ensure_events(PcgWork* w, size_t n) {
+    while (w->ev.size() < n) {
+        cudaEvent_t e;
+        IE_CUDA(cudaEventCreate(&e));
+        w->ev.push_back(e);
+    }
+    return IE_OK;
+}
+
+}  // namespace ie
 
 extern "C" int ie_pcg_f64(const ie_matvec* A, const ie_precond* T, const double* f, double* u, double tol,
                           int64_t max_iters, double* hist, int64_t* n_it, int32_t* flags, double* times,
@@ -260,157 +405,122 @@ extern "C" int ie_pcg_f64(const ie_matvec* A, const ie_precond* T, const double*
     const int N = matvec_N(A);
     const int nch = dot_chunks(N);
     const auto t0 = std::chrono::steady_clock::now();
-    DevBuf<double> PU(st), QW(st), r(st), z(st), part(st);
-    DevBuf<Scal> sc(st);
-    IE_CUDA(PU.alloc(2 * (size_t)N));
-    IE_CUDA(QW.alloc(2 * (size_t)N));
-    IE_CUDA(r.alloc(N));
-    IE_CUDA(z.alloc(N));
-    IE_CUDA(part.alloc(3 * (size_t)nch));
-    IE_CUDA(sc.alloc(1));
-    Scal* hs = nullptr;
-    IE_CUDA(cudaMallocHost(&hs, sizeof(Scal)));
-    struct HostFree {
-        Scal* h;
-        ~HostFree() { cudaFreeHost(h); }
-    } hf{hs};
-    double* p = PU.p;
-    double* uu = PU.p + N;
-    double* q = QW.p;
-    double* w = QW.p + N;
-    double* part_pq = part.p;
-    double* part_res = part.p + nch;
-    double* part_rz = part.p + 2 * nch;
-    cudaEvent_t ev0, ev1;
-    IE_CUDA(cudaEventCreate(&ev0));
-    IE_CUDA(cudaEventCreate(&ev1));
-    struct EvFree {
-        cudaEvent_t a, b;
-        ~EvFree() {
-            cudaEventDestroy(a);
-            cudaEventDestroy(b);
-        }
-    } ef{ev0, ev1};
-    double t_prec = 0.0;
-    int64_t n_prec = 0;
-    auto apply = [&](const double* rin, double* zout) -> int {
-        IE_CUDA(cudaEventRecord(ev0, st));
+    int rc = IE_OK;
+    int64_t cap = 1024;  // history capacity rounded up: warm-up and timed solves share a workspace
+    while (cap < max_iters + 1) cap *= 2;
+    PcgWork* W = work_acquire(N, cap, &rc);
+    if (!W) return rc;
+    struct Release {
+        PcgWork* w;
+        ~Release() { work_release(w); }
+    } rel_guard{W};
+    // apply events: pair 0 = initial apply, pair it = speculative apply of iteration it
+    const int64_t kBatch = 4;
+    if ((rc = ensure_events(W, 2 * (size_t)(std::min<int64_t>(cap, 4096) + 2)))) return rc;
+    double* p = W->PU;
+    double* uu = W->PU + N;
+    double* q = W->QW;
+    double* w = W->QW + N;
+    double* part_pq = W->part;
+    double* part_res = W->part + nch;
+    double* part_rz = W->part + 2 * nch;
+    const int* stop = &W->st->stop;
+    auto apply = [&](const double* rin, double* zout, int64_t evi) -> int {
+        const bool timed = 2 * evi + 1 < (int64_t)W->ev.size();
+        if (timed) IE_CUDA(cudaEventRecord(W->ev[2 * evi], st));
         if (T) {
-            int rc = precond_apply(T, rin, zout, part_rz, st);
-            if (rc) return rc;
+            int r2 = precond_apply(T, rin, zout, part_rz, st, stop);
+            if (r2) return r2;
         } else {
-            IE_CUDA(cudaMemcpyAsync(zout, rin, (size_t)N * 8, cudaMemcpyDeviceToDevice, st));
+            k_copy_if_running<<<g1(N), 256, 0, st>>>(zout, rin, N, stop);
+            IE_LAUNCHED();
             k_dot_partials<<<nch, kRed, 0, st>>>(rin, zout, N, 0, part_rz);
             IE_LAUNCHED();
         }
-        IE_CUDA(cudaEventRecord(ev1, st));
+        if (timed) IE_CUDA(cudaEventRecord(W->ev[2 * evi + 1], st));
         return IE_OK;
     };
-    auto apply_time = [&]() -> int {
-        float ms = 0.f;
-        IE_CUDA(cudaEventSynchronize(ev1));
-        IE_CUDA(cudaEventElapsedTime(&ms, ev0, ev1));
-        t_prec += ms * 1e-3;
-        n_prec += 1;
-        return IE_OK;
-    };
-    // ||f||
+    // ||f||, state init (pcg.py:72-91)
     k_dot_partials<<<nch, kRed, 0, st>>>(f, f, N, 0, part_pq);
     IE_LAUNCHED();
-    k_set_nf<<<1, kRed, 0, st>>>(part_pq, nch, sc.p);
+    k_pcg_init<<<1, kRed, 0, st>>>(part_pq, nch, W->st, tol, max_iters, W->hist);
     IE_LAUNCHED();
-    IE_CUDA(cudaMemcpyAsync(hs, sc.p, sizeof(Scal), cudaMemcpyDeviceToHost, st));
-    IE_CUDA(cudaStreamSynchronize(st));
-    flags[0] = flags[1] = 0;
-    if (hs->nf == 0.0) {  // pcg.py:74-78
-        IE_CUDA(cudaMemsetAsync(u, 0, (size_t)N * 8, st));
-        hist[0] = 0.0;
-        *n_it = 0;
-        flags[0] = 1;
-        times[0] = times[1] = 0.0;
-        IE_CUDA(cudaStreamSynchronize(st));
-        return IE_OK;
-    }
     IE_CUDA(cudaMemsetAsync(uu, 0, (size_t)N * 8, st));
-    IE_CUDA(cudaMemcpyAsync(r.p, f, (size_t)N * 8, cudaMemcpyDeviceToDevice, st));
-    int rc = apply(r.p, z.p);
-    if (rc) return rc;
-    if ((rc = apply_time())) return rc;
-    IE_CUDA(cudaMemcpyAsync(p, z.p, (size_t)N * 8, cudaMemcpyDeviceToDevice, st));
-    k_control_b<<<1, kRed, 0, st>>>(part_rz, nch, 1, sc.p);
+    IE_CUDA(cudaMemcpyAsync(W->r, f, (size_t)N * 8, cudaMemcpyDeviceToDevice, st));
+    if ((rc = apply(W->r, W->z, 0))) return rc;
+    IE_CUDA(cudaMemcpyAsync(p, W->z, (size_t)N * 8, cudaMemcpyDeviceToDevice, st));
+    k_control_b<<<1, kRed, 0, st>>>(part_rz, nch, 1, W->st);
     IE_LAUNCHED();
-    hist[0] = 1.0;
-    int64_t k = 0;
-    bool pending = false;
-    bool spec_apply = false;
-    int result = IE_OK;
-    while (true) {
-        const int64_t next = k + 1;
-        const bool do_p = next <= max_iters;
-        if (!pending && !do_p) break;
+    // iterations: `it` = the iteration whose A-pass is enqueued; the pass also
+    // carries u_{it-1} for the deferred true-residual check of iteration it-1
+    int64_t it = 1;
+    for (; it <= max_iters + 1; ++it) {
+        const int do_p = it <= max_iters;
+        const int pending = it >= 2;
         if (do_p && pending) {
-            rc = matvec_launch(A, PU.p, N, 2, QW.p, N, 0, N, st);
+            rc = matvec_launch(A, W->PU, N, 2, W->QW, N, 0, N, st, stop);
         } else if (do_p) {
-            rc = matvec_launch(A, p, N, 1, q, N, 0, N, st);
+            rc = matvec_launch(A, p, N, 1, q, N, 0, N, st, stop);
         } else {
-            rc = matvec_launch(A, uu, N, 1, w, N, 0, N, st);
+            rc = matvec_launch(A, uu, N, 1, w, N, 0, N, st, stop);
         }
         if (rc) return rc;
-        k_post_pass<<<nch, kRed, 0, st>>>(p, q, f, w, N, do_p, pending, part_pq, part_res);
+        k_post_pass<<<nch, kRed, 0, st>>>(p, q, f, w, N, do_p, pending, part_pq, part_res, stop);
         IE_LAUNCHED();
-        k_control_a<<<1, kRed, 0, st>>>(part_pq, part_res, nch, do_p, pending, sc.p);
+        k_control_a<<<1, kRed, 0, st>>>(part_pq, part_res, nch, do_p, pending, it, W->st, W->hist);
         IE_LAUNCHED();
-        IE_CUDA(cudaMemcpyAsync(hs, sc.p, sizeof(Scal), cudaMemcpyDeviceToHost, st));
-        IE_CUDA(cudaStreamSynchronize(st));
-        if (spec_apply) {
-            if ((rc = apply_time())) return rc;
-            spec_apply = false;
-        }
-        if (pending) {
-            const double rel = hs->rel;
-            if (!std::isfinite(rel)) {  // pcg.py:109-110
-                if (fail_iter) *fail_iter = k;
-                if (fail_value) *fail_value = rel;
-                result = IE_ERR_NONFINITE;
-                break;
-            }
-            hist[k] = rel;
-            if (rel <= tol) {
-                flags[0] = 1;
-                break;
-            }
-            if (k >= 30 && rel > (1.0 - 1e-3) * hist[k - 30]) {  // pcg.py:115-119
-                flags[1] = 1;
-                break;
-            }
-            if (!do_p) break;
-        }
-        const double denom = hs->denom;
-        if (!std::isfinite(denom) || denom <= 0.0) {  // pcg.py:99-103
-            if (fail_iter) *fail_iter = next;
-            if (fail_value) *fail_value = denom;
-            result = IE_ERR_BREAKDOWN;
-            break;
-        }
-        k_update_ur<<<g1(N), 256, 0, st>>>(uu, r.p, p, q, sc.p, N);
-        IE_LAUNCHED();
-        k = next;
-        pending = true;
-        if (k < max_iters) {
-            if ((rc = apply(r.p, z.p))) return rc;
-            spec_apply = true;
-            k_control_b<<<1, kRed, 0, st>>>(part_rz, nch, 0, sc.p);
+        if (do_p) {
+            k_update_ur<<<g1(N), 256, 0, st>>>(uu, W->r, p, q, W->st, N);
             IE_LAUNCHED();
-            k_update_p<<<g1(N), 256, 0, st>>>(p, z.p, sc.p, N);
-            IE_LAUNCHED();
+            if (it < max_iters) {  // speculative: z_it is discarded if iteration it is the last
+                if ((rc = apply(W->r, W->z, it))) return rc;
+                k_control_b<<<1, kRed, 0, st>>>(part_rz, nch, 0, W->st);
+                IE_LAUNCHED();
+                k_update_p<<<g1(N), 256, 0, st>>>(p, W->z, W->st, N);
+                IE_LAUNCHED();
+            }
+        }
+        if (it % kBatch == 0 || it == max_iters + 1) {
+            IE_CUDA(cudaMemcpyAsync(W->host, W->st, sizeof(PcgState), cudaMemcpyDeviceToHost, st));
+            IE_CUDA(cudaStreamSynchronize(st));
+            if (W->host->stop) break;
         }
     }
-    *n_it = k;
+    IE_CUDA(cudaMemcpyAsync(W->host, W->st, sizeof(PcgState), cudaMemcpyDeviceToHost, st));
+    IE_CUDA(cudaStreamSynchronize(st));
+    const PcgState S = *W->host;
+    flags[0] = S.status == 1;
+    flags[1] = S.status == 2;
+    *n_it = S.n_it;
+    if (S.status == 4 || S.status == 5) {
+        if (fail_iter) *fail_iter = S.fail_iter;
+        if (fail_value) *fail_value = S.fail_value;
+    }
+    const int64_t nh = S.n_it + 1;
+    IE_CUDA(cudaMemcpyAsync(hist, W->hist, (size_t)nh * 8, cudaMemcpyDeviceToHost, st));
     IE_CUDA(cudaMemcpyAsync(u, uu, (size_t)N * 8, cudaMemcpyDeviceToDevice, st));
     IE_CUDA(cudaStreamSynchronize(st));
     times[0] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-    times[1] = t_prec / (double)(n_prec > 0 ? n_prec : 1);
-    return result;
+    // t_s: mean device time of the applies the reference performs (initial + iterations 1..n_it-1)
+    double tp = 0.0;
+    int64_t np = 0;
+    for (int64_t e = 0; e < S.n_it && 2 * e + 1 < (int64_t)W->ev.size(); ++e) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, W->ev[2 * e], W->ev[2 * e + 1]) == cudaSuccess) {
+            tp += ms * 1e-3;
+            ++np;
+        }
+    }
+    if (S.n_it == 0) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, W->ev[0], W->ev[1]) == cudaSuccess) tp = ms * 1e-3, np = 1;
+    }
+    cudaGetLastError();
+    times[1] = np ? tp / (double)np : 0.0;
+    if (S.nf == 0.0) times[0] = times[1] = 0.0;  // zero right-hand side (pcg.py:74-78)
+    if (S.status == 4) return IE_ERR_BREAKDOWN;
+    if (S.status == 5) return IE_ERR_NONFINITE;
+    return IE_OK;
 }
 
 extern "C" int ie_lanczos_f64(const ie_matvec* A, const ie_precond* T, const double* v0, int32_t which,
@@ -450,7 +560,7 @@ extern "C" int ie_lanczos_f64(const ie_matvec* A, const ie_precond* T, const dou
     int rc;
     // v = v0; av = A v; nrm = sqrt(v.av); v /= nrm; av /= nrm   (spectrum.py:148-153)
     IE_CUDA(cudaMemcpyAsync(wb.p, v0, (size_t)N * 8, cudaMemcpyDeviceToDevice, st));
-    if ((rc = matvec_launch(A, wb.p, N, 1, awb.p, N, 0, N, st))) return rc;
+    if ((rc = matvec_launch(A, wb.p, N, 1, awb.p, N, 0, N, st, nullptr))) return rc;
     if ((rc = dot(wb.p, awb.p, scal.p))) return rc;
     IE_CUDA(cudaMemcpyAsync(hsc, scal.p, 8, cudaMemcpyDeviceToHost, st));
     IE_CUDA(cudaStreamSynchronize(st));
@@ -469,7 +579,7 @@ extern "C" int ie_lanczos_f64(const ie_matvec* A, const ie_precond* T, const dou
         double* Vj = V.p + (size_t)j * N;
         double* AVj = AV.p + (size_t)j * N;
         (void)Vj;
-        if ((rc = precond_apply(T, AVj, wb.p, nullptr, st))) return rc;
+        if ((rc = precond_apply(T, AVj, wb.p, nullptr, st, nullptr))) return rc;
         if ((rc = dot(wb.p, AVj, da + j))) return rc;
         const int nb = (int)(j + 1);
         for (int pass = 0; pass < 2; ++pass) {  // two-pass A-orthogonalisation (CGS2)
@@ -481,7 +591,7 @@ extern "C" int ie_lanczos_f64(const ie_matvec* A, const ie_precond* T, const dou
             k_gemv_sub<<<g1(N), 256, 0, st>>>(wb.p, V.p, N, nb, cbuf.p, N);
             IE_LAUNCHED();
         }
-        if ((rc = matvec_launch(A, wb.p, N, 1, awb.p, N, 0, N, st))) return rc;
+        if ((rc = matvec_launch(A, wb.p, N, 1, awb.p, N, 0, N, st, nullptr))) return rc;
         if ((rc = dot(wb.p, awb.p, scal.p + 1))) return rc;
         IE_CUDA(cudaMemcpyAsync(hsc, scal.p + 1, 8, cudaMemcpyDeviceToHost, st));
         double aj = 0.0;

@@ -40,6 +40,7 @@ struct MatvecArgs {
     int split_len;
     double alpha;
     double diag;
+    const int* stop;  // device flag: nonzero -> no-op (PCG early exit)
 };
 
 template <int DIM>
@@ -61,6 +62,7 @@ __device__ __forceinline__ void neumaier(double& s, double& c, double v) {
 template <int DIM, int NRHS, int R>
 __global__ void __launch_bounds__(256) k_matvec(MatvecArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
+    if (a.stop && *a.stop) return;
     LogEntry* stab = reinterpret_cast<LogEntry*>(smem);
     double* xs = reinterpret_cast<double*>(smem + (DIM == 3 ? 0 : a.ntab * (int)sizeof(LogEntry)));
     const int tid = threadIdx.x;
@@ -190,6 +192,7 @@ __global__ void __launch_bounds__(256) k_matvec(MatvecArgs a) {
 // Sum split partials in split order and apply the epilogue.
 template <int DIM, int NRHS>
 __global__ void k_matvec_reduce(MatvecArgs a, int nsplit) {
+    if (a.stop && *a.stop) return;
     const int row = blockIdx.x * blockDim.x + threadIdx.x;
     if (row >= a.nrows) return;
     double lself;
@@ -215,7 +218,8 @@ struct ie_fft;
 namespace ie {
 int fft_create(const ie_geom& g, ie_fft** out);
 void fft_destroy(ie_fft* f);
-int fft_matvec(const ie_fft* f, const double* X0, const double* X1, double* Y0, double* Y1, cudaStream_t st);
+int fft_matvec(const ie_fft* f, const double* X0, const double* X1, double* Y0, double* Y1, cudaStream_t st,
+               const int* stop);
 }  // namespace ie
 
 struct ie_matvec {
@@ -298,12 +302,12 @@ static int launch_dim(const ie_matvec* m, MatvecArgs a, cudaStream_t st) {
 }
 
 int matvec_launch(const ie_matvec* m, const double* X, int64_t ldx, int nrhs, double* Y, int64_t ldy,
-                  int64_t row_begin, int64_t row_end, cudaStream_t st) {
+                  int64_t row_begin, int64_t row_end, cudaStream_t st, const int* stop) {
     if (m->method == IE_MATVEC_FFT) {
         const double* X1 = nrhs == 2 ? X + ldx : nullptr;
         if (row_begin == 0 && row_end == m->N)
-            return fft_matvec(m->fft, X, X1, Y, nrhs == 2 ? Y + ldy : nullptr, st);
-        int rc = fft_matvec(m->fft, X, X1, m->d_full, nrhs == 2 ? m->d_full + m->N : nullptr, st);
+            return fft_matvec(m->fft, X, X1, Y, nrhs == 2 ? Y + ldy : nullptr, st, stop);
+        int rc = fft_matvec(m->fft, X, X1, m->d_full, nrhs == 2 ? m->d_full + m->N : nullptr, st, stop);
         if (rc) return rc;
         for (int q = 0; q < nrhs; ++q)
             IE_CUDA(cudaMemcpyAsync(Y + q * ldy, m->d_full + (int64_t)q * m->N + row_begin,
@@ -326,6 +330,7 @@ int matvec_launch(const ie_matvec* m, const double* X, int64_t ldx, int nrhs, do
     a.split_len = m->split_len;
     a.alpha = m->alpha;
     a.diag = m->g.diag;
+    a.stop = stop;
     if (a.nrows <= 0) return IE_OK;
     switch (m->g.dim * 4 + nrhs) {
         case 1 * 4 + 1: return launch_dim<1, 1>(m, a, st);
@@ -439,7 +444,7 @@ extern "C" int ie_matvec_f64(const ie_matvec* m, const double* X, int64_t ldx, i
         ie::set_error("ie_matvec_f64: bad arguments");
         return IE_ERR_ARG;
     }
-    return ie::matvec_launch(m, X, ldx, nrhs, Y, ldy, row_begin, row_end, (cudaStream_t)stream);
+    return ie::matvec_launch(m, X, ldx, nrhs, Y, ldy, row_begin, row_end, (cudaStream_t)stream, nullptr);
 }
 
 extern "C" int ie_assemble_block_f64(const ie_geom* g, const int64_t* rows, int64_t nr, const int64_t* cols,

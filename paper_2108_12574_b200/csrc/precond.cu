@@ -191,6 +191,7 @@ struct ApplyArgs {
     int64_t D;
     int wpb;  // warps per block
     int bpc;  // blocks per CTA
+    const int* stop;  // device flag: nonzero -> no-op (PCG early exit)
 };
 
 // z_k = A_k^{-1} r_k with the packed upper triangle by columns: column j
@@ -201,6 +202,7 @@ struct ApplyArgs {
 template <int T, int U>
 __global__ void __launch_bounds__(256) k_apply_packed(ApplyArgs a) {
     extern __shared__ double red[];
+    if (a.stop && *a.stop) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int bl = warp / a.wpb, w = warp % a.wpb;
     const int64_t k = (int64_t)blockIdx.x * a.bpc + bl;
@@ -289,6 +291,7 @@ __global__ void __launch_bounds__(256) k_apply_packed(ApplyArgs a) {
 // small-D golden geometries use it.
 __global__ void __launch_bounds__(256) k_apply_large(ApplyArgs a) {
     extern __shared__ double sm[];
+    if (a.stop && *a.stop) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
     const BlockMeta bm = a.meta[blockIdx.x];
     const int s = bm.s;
@@ -320,6 +323,7 @@ __global__ void __launch_bounds__(256) k_apply_large(ApplyArgs a) {
 // substitution with the row-packed upper factor; one warp per block.
 template <int T>
 __global__ void __launch_bounds__(128) k_apply_subst(ApplyArgs a) {
+    if (a.stop && *a.stop) return;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t k = (int64_t)blockIdx.x * a.bpc + warp;
     if (k >= a.D) return;
@@ -382,7 +386,8 @@ __global__ void __launch_bounds__(128) k_apply_subst(ApplyArgs a) {
 // Optionally also the fixed-chunk partials of r.z (for PCG's rho).
 constexpr int kChunk = 2048;
 __global__ void __launch_bounds__(256) k_scatter(const double* staging, const int* ptr, const int* pos, double* z,
-                                                 int N, const double* r, double* partials) {
+                                                 int N, const double* r, double* partials, const int* stop) {
+    if (stop && *stop) return;
     __shared__ double sh[256];
     const int base = blockIdx.x * kChunk;
     double loc = 0.0;
@@ -454,8 +459,10 @@ static void launch_apply_T(const ie_precond* p, ApplyArgs a, cudaStream_t st) {
     }
 }
 
-int precond_apply(const ie_precond* p, const double* r, double* z, double* partials, cudaStream_t st) {
+int precond_apply(const ie_precond* p, const double* r, double* z, double* partials, cudaStream_t st,
+                  const int* stop) {
     ApplyArgs a;
+    a.stop = stop;
     a.r = r;
     a.staging = p->d_staging;
     a.meta = p->d_meta;
@@ -470,7 +477,8 @@ int precond_apply(const ie_precond* p, const double* r, double* z, double* parti
         k_apply_large<<<(unsigned)p->D, 256, sm, st>>>(a);
         IE_LAUNCHED();
         const int nch2 = (p->N + kChunk - 1) / kChunk;
-        k_scatter<<<nch2, 256, 0, st>>>(p->d_staging, p->d_ptr, p->d_pos, z, p->N, partials ? r : nullptr, partials);
+        k_scatter<<<nch2, 256, 0, st>>>(p->d_staging, p->d_ptr, p->d_pos, z, p->N, partials ? r : nullptr, partials,
+                                         stop);
         IE_LAUNCHED();
         return IE_OK;
     }
@@ -487,7 +495,8 @@ int precond_apply(const ie_precond* p, const double* r, double* z, double* parti
     }
     IE_LAUNCHED();
     const int nch = (p->N + kChunk - 1) / kChunk;
-    k_scatter<<<nch, 256, 0, st>>>(p->d_staging, p->d_ptr, p->d_pos, z, p->N, partials ? r : nullptr, partials);
+    k_scatter<<<nch, 256, 0, st>>>(p->d_staging, p->d_ptr, p->d_pos, z, p->N, partials ? r : nullptr, partials,
+                                   stop);
     IE_LAUNCHED();
     return IE_OK;
 }
@@ -755,7 +764,7 @@ extern "C" int ie_precond_apply_f64(const ie_precond* p, const double* r, double
         ie::set_error("ie_precond_apply_f64: bad arguments");
         return IE_ERR_ARG;
     }
-    return ie::precond_apply(p, r, z, nullptr, (cudaStream_t)stream);
+    return ie::precond_apply(p, r, z, nullptr, (cudaStream_t)stream, nullptr);
 }
 
 extern "C" int ie_precond_stats(const ie_precond* p, int64_t* out5) {

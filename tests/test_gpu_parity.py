@@ -223,9 +223,9 @@ class TestApply:
             assert rel(pre.apply(r), zr) <= 1e-12
 
 
-def _pcg_check(rep, u, g, kind, u_tol=1e-10):
+def _pcg_check(rep, u, g, kind, u_tol=1e-10, it_tol=1):
     n_it = int(g[f"{kind}_meta"][0])
-    assert abs(rep.n_it - n_it) <= 1, (rep.n_it, n_it)
+    assert abs(rep.n_it - n_it) <= it_tol, (rep.n_it, n_it)
     assert rep.converged == bool(g[f"{kind}_meta"][1])
     h = np.array(rep.residual_history)
     hr = g[f"{kind}_hist"]
@@ -259,7 +259,11 @@ class TestPCG:
         pre = ie.from_decomposition(op, ie.build_decomposition(grid, 32, 2, "schwarz"))
         f = np.random.default_rng(1).standard_normal(op.n)
         u, rep = ie.solve(ie.KernelMatvec(op, method=method), pre, f, tol=1e-10)
-        _pcg_check(rep, u, g, "schwarz")
+        # config 3 ends on a knife edge (residuals bounce around tol in the last
+        # iterations): a pure 1e-16..1e-14 random perturbation of the oracle's
+        # own matvec moves n_it 58 -> 59 (tools/diag notes in DESIGN.md), and the
+        # direct sum (row error 6e-16 median vs FFT 2e-16) lands at 60.
+        _pcg_check(rep, u, g, "schwarz", it_tol=2)
 
     @pytest.mark.parametrize("method", METHODS)
     def test_c4(self, ie, golden, method):
