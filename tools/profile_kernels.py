@@ -30,3 +30,12 @@ if which in ("all", "k3"):
             pre.apply_device(r, z)
 torch.cuda.synchronize()
 print("profile driver done")
+if which == "fft":
+    op = ie.build_operator(ie.build_grid(2, 1024), lattice="cell")
+    mv = ie.KernelMatvec(op, method="fft")
+    X = torch.from_numpy(np.random.default_rng(0).standard_normal((2, op.n))).cuda()
+    Y = torch.empty_like(X)
+    for _ in range(3):
+        mv.matvec_device(X, Y, nrhs=2)
+    torch.cuda.synchronize()
+    print("fft driver done")
