@@ -134,6 +134,19 @@ int ie_lanczos_f64(const ie_matvec* A, const ie_precond* T, const double* d_v0,
                    int32_t which, int64_t max_iters, double rtol, double* lambda,
                    int64_t* steps, void* stream);
 
+/* Deterministic vector operations of the PCG iteration (for the sharded
+ * driver; identical kernels and reduction order to ie_pcg_f64).
+ * ie_dot_partials_f64: part[c] = fixed-tree sum over chunk c (ie_dot_chunk()
+ *   elements) of x.y (mode 0) or |x-y|^2 (mode 1).
+ * ie_sum_partials_f64: *out (device) = fixed-order sum of nch partials.
+ * ie_update_f64: op 0 a += s*b, op 1 a -= s*b, op 2 a = b + s*a (products
+ *   rounded first, as numpy does; pcg.py:105-106, :125). */
+int64_t ie_dot_chunk(void);
+int ie_dot_partials_f64(const double* d_x, const double* d_y, int64_t n, int32_t mode, double* d_part,
+                        void* stream);
+int ie_sum_partials_f64(const double* d_part, int64_t nch, double* d_out, void* stream);
+int ie_update_f64(int32_t op, double* d_a, const double* d_b, double s, int64_t n, void* stream);
+
 /* FP64 issue-peak microbenchmark: DFMA instructions (lane ops) per second
  * over all SMs -- the roofline denominator for K1. */
 int ie_fp64_peak(double* dfma_per_s, void* stream);

@@ -53,6 +53,10 @@ _SIGS = {
                           ctypes.POINTER(_I64), ctypes.POINTER(_D), _P]),
     "ie_lanczos_f64": (_I32, [_P, _P, _P, _I32, _I64, _D, ctypes.POINTER(_D), ctypes.POINTER(_I64), _P]),
     "ie_fp64_peak": (_I32, [ctypes.POINTER(_D), _P]),
+    "ie_dot_chunk": (_I64, []),
+    "ie_dot_partials_f64": (_I32, [_P, _P, _I64, _I32, _P, _P]),
+    "ie_sum_partials_f64": (_I32, [_P, _I64, _P, _P]),
+    "ie_update_f64": (_I32, [_I32, _P, _P, _D, _I64, _P]),
     "ie_last_error": (ctypes.c_char_p, []),
     "ie_launch_count": (_I64, []),
 }

@@ -635,3 +635,53 @@ extern "C" int ie_lanczos_f64(const ie_matvec* A, const ie_precond* T, const dou
     *lambda = est;
     return IE_OK;
 }
+
+// ------------------------------------------------------------------------
+// Vector operations of the PCG iteration exposed for the sharded driver
+// (paper_2108_12574_b200/distributed.py).  They are the same kernels and the
+// same reduction order as ie_pcg_f64, so a sharded solve reproduces the
+// single-GPU one bitwise.
+namespace ie {
+__global__ void k_update_host(int op, double* a, const double* b, double s, int64_t n) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    if (op == 0) a[i] = __dadd_rn(a[i], __dmul_rn(s, b[i]));
+    else if (op == 1) a[i] = __dsub_rn(a[i], __dmul_rn(s, b[i]));
+    else a[i] = __dadd_rn(b[i], __dmul_rn(s, a[i]));
+}
+}  // namespace ie
+
+extern "C" int64_t ie_dot_chunk(void) { return ie::kChunk; }
+
+extern "C" int ie_dot_partials_f64(const double* x, const double* y, int64_t n, int32_t mode, double* part,
+                                   void* stream) {
+    if (!x || !y || !part || n < 0 || n > 2147483647LL || (mode != 0 && mode != 1)) {
+        set_error("ie_dot_partials_f64: bad arguments");
+        return IE_ERR_ARG;
+    }
+    if (n == 0) return IE_OK;
+    k_dot_partials<<<dot_chunks(n), kRed, 0, (cudaStream_t)stream>>>(x, y, (int)n, mode, part);
+    IE_LAUNCHED();
+    return IE_OK;
+}
+
+extern "C" int ie_sum_partials_f64(const double* part, int64_t nch, double* out, void* stream) {
+    if (!part || !out || nch < 1) {
+        set_error("ie_sum_partials_f64: bad arguments");
+        return IE_ERR_ARG;
+    }
+    k_reduce_rows<<<1, kRed, 0, (cudaStream_t)stream>>>(part, (int)nch, out);
+    IE_LAUNCHED();
+    return IE_OK;
+}
+
+extern "C" int ie_update_f64(int32_t op, double* a, const double* b, double s, int64_t n, void* stream) {
+    if (!a || !b || n < 0 || op < 0 || op > 2) {
+        set_error("ie_update_f64: bad arguments");
+        return IE_ERR_ARG;
+    }
+    if (n == 0) return IE_OK;
+    k_update_host<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(op, a, b, s, n);
+    IE_LAUNCHED();
+    return IE_OK;
+}

@@ -1,0 +1,392 @@
+"""Sharded Schwarz-PCG across the ranks of a torch.distributed group
+(one process per GPU, NCCL over NVLink).
+
+Partitioning.  Rank g owns a contiguous band [b_g, e_g) of the C-ordered
+unknowns: the first lattice axis is split at subdomain-row boundaries and the
+cut points are rounded to the dot-product chunk (2048) so that every
+fixed-chunk partial lives on exactly one rank.  Per iteration:
+
+  * all-gather of the iterate columns [p, u] (the fused 2-RHS A-pass needs
+    every source),
+  * the A-pass for the band's rows (K1 rows are summed in the same order for
+    any row range; the FFT method computes all rows and keeps the band),
+  * all-gather of the fixed-chunk dot partials, reduced on every rank by the
+    same device kernel and order as the single-GPU solver,
+  * all-gather of r for the apply: each rank applies the subdomains that
+    intersect its band (neighbours' overlap blocks are recomputed), so the
+    z values of its band are summed in ascending global block id -- the
+    reference's order.
+
+Every scalar and every owned vector entry is therefore bitwise identical for
+any number of ranks, and identical to ie_pcg_f64 on one GPU.
+
+The compute backend is pluggable: CudaBackend (C-ABI kernels) in production;
+the CPU tests inject a numpy backend and run the same driver over gloo.
+"""
+
+from __future__ import annotations
+
+import ctypes
+import math
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+CHUNK = 2048
+STAGNATION_WINDOW = 30
+STAGNATION_FACTOR = 1e-3
+
+
+# --------------------------------------------------------------------------
+# plan
+# --------------------------------------------------------------------------
+def band_bounds(grid, m_per_dim: int, world: int, chunk: int = CHUNK) -> tuple:
+    """Cut points (world+1) of the rank bands: subdomain-row boundaries of the
+    first lattice axis, rounded to multiples of `chunk`, monotone."""
+    N = grid.n_points
+    n = grid.n_per_dim
+    m = max(1, min(m_per_dim, n))
+    line = n ** (grid.dim - 1)
+    cuts = []
+    for g in range(world + 1):
+        first_line = (m * g // world) * (n // m)
+        idx = first_line * line
+        idx = min(N, int(round(idx / chunk)) * chunk)
+        cuts.append(idx)
+    cuts[0], cuts[-1] = 0, N
+    for i in range(1, len(cuts)):
+        cuts[i] = max(cuts[i], cuts[i - 1])
+    return tuple(cuts)
+
+
+@dataclass(frozen=True)
+class ShardPlan:
+    world: int
+    rank: int
+    N: int
+    bounds: tuple
+    blocks: np.ndarray = field(repr=False)  # global subdomain ids applied on this rank (ascending)
+
+    @property
+    def begin(self) -> int:
+        return self.bounds[self.rank]
+
+    @property
+    def end(self) -> int:
+        return self.bounds[self.rank + 1]
+
+    @property
+    def size(self) -> int:
+        return self.end - self.begin
+
+    def chunks(self, r: int | None = None) -> tuple:
+        r = self.rank if r is None else r
+        b, e = self.bounds[r], self.bounds[r + 1]
+        return (b // CHUNK, -(-e // CHUNK)) if e > b else (b // CHUNK, b // CHUNK)
+
+
+def blocks_intersecting(subdomains, begin: int, end: int) -> np.ndarray:
+    out = []
+    for k, idx in enumerate(subdomains):
+        j = np.searchsorted(idx, begin)
+        if j < idx.size and idx[j] < end:
+            out.append(k)
+    return np.array(out, dtype=np.int64)
+
+
+def make_plan(grid, decomposition, world: int, rank: int) -> ShardPlan:
+    bounds = band_bounds(grid, getattr(decomposition, "m_per_dim", 1), world)
+    blocks = blocks_intersecting(decomposition.subdomains, bounds[rank], bounds[rank + 1])
+    return ShardPlan(world=world, rank=rank, N=grid.n_points, bounds=bounds, blocks=blocks)
+
+
+@dataclass(frozen=True)
+class SubDecomposition:
+    """The subset of a decomposition a rank applies (ascending global ids)."""
+
+    kind: str
+    subdomains: list
+    global_ids: np.ndarray
+
+    @property
+    def n_subdomains(self) -> int:
+        return len(self.subdomains)
+
+
+# --------------------------------------------------------------------------
+# communication
+# --------------------------------------------------------------------------
+class Comm:
+    """Band all-gathers over torch.distributed (NCCL for CUDA tensors, gloo
+    for CPU tensors).  Bands are padded to the longest one."""
+
+    def __init__(self, plan: ShardPlan, group=None):
+        import torch.distributed as dist
+        self.dist = dist
+        self.group = group
+        self.plan = plan
+        self.maxlen = max(plan.bounds[i + 1] - plan.bounds[i] for i in range(plan.world))
+        self.maxch = max(plan.chunks(i)[1] - plan.chunks(i)[0] for i in range(plan.world))
+
+    def _gather(self, x, length_of):
+        import torch
+        world = self.plan.world
+        ncol, L = x.shape
+        pad = self.maxlen if length_of == "band" else self.maxch
+        buf = x.new_zeros((ncol, pad))
+        buf[:, :L] = x
+        outs = [torch.empty_like(buf) for _ in range(world)]
+        if world == 1:
+            outs[0].copy_(buf)
+        else:
+            self.dist.all_gather(outs, buf, group=self.group)
+        pieces = []
+        for r in range(world):
+            if length_of == "band":
+                n = self.plan.bounds[r + 1] - self.plan.bounds[r]
+            else:
+                c0, c1 = self.plan.chunks(r)
+                n = c1 - c0
+            pieces.append(outs[r][:, :n])
+        return torch.cat(pieces, dim=1)
+
+    def allgather_band(self, x):
+        """(ncol, band) -> (ncol, N) in global order."""
+        return self._gather(x, "band")
+
+    def allgather_partials(self, x):
+        """(ncol, band chunks) -> (ncol, all chunks) in chunk order."""
+        return self._gather(x, "chunks")
+
+
+# --------------------------------------------------------------------------
+# CUDA backend (production)
+# --------------------------------------------------------------------------
+class CudaBackend:
+    """Per-rank device work through the C-ABI (same kernels as ie_pcg_f64)."""
+
+    def __init__(self, op, decomposition, plan: ShardPlan, method: str = "auto",
+                 variant: str = "packed_inverse", share_translated: bool = True):
+        import torch
+
+        from . import _lib
+        from .precond import from_decomposition
+        from .toeplitz import KernelMatvec
+        self.torch = torch
+        self._lib = _lib
+        self.L = _lib.lib()
+        self.plan = plan
+        self.N = plan.N
+        if method == "auto":
+            from .toeplitz import fft_supported
+            method = "fft" if fft_supported(op.grid.n_per_dim) else "direct"
+        self.mv = KernelMatvec(op, method=method)
+        self.method = method
+        sub = SubDecomposition(decomposition.kind, [decomposition.subdomains[k] for k in plan.blocks],
+                               plan.blocks)
+        self.pre = (from_decomposition(op, sub, variant=variant, share_translated=share_translated)
+                    if plan.blocks.size else None)
+        self.dev = torch.device("cuda", torch.cuda.current_device())
+        self._full = torch.empty(2, self.N, dtype=torch.float64, device=self.dev)
+        self._scal = torch.empty(1, dtype=torch.float64, device=self.dev)
+
+    def tensor(self, a):
+        return self.torch.as_tensor(np.asarray(a, dtype=np.float64)).to(self.dev)
+
+    def zeros(self, n):
+        return self.torch.zeros(n, dtype=self.torch.float64, device=self.dev)
+
+    def matvec_band(self, X):
+        """X: (nrhs, N) full columns -> (nrhs, band) rows [begin, end)."""
+        nrhs = X.shape[0]
+        Y = self.torch.empty(nrhs, max(self.plan.size, 1), dtype=self.torch.float64, device=self.dev)
+        if self.plan.size:
+            X = X.contiguous()
+            self.mv.matvec_device(X, Y, nrhs=nrhs, row_begin=self.plan.begin, row_end=self.plan.end,
+                                  ldx=self.N, ldy=Y.shape[1])
+        return Y[:, : self.plan.size]
+
+    def apply_band(self, r_full):
+        if self.pre is None:
+            return self.zeros(0)
+        z = self._full[0]
+        self.pre.apply_device(r_full.contiguous(), z)
+        return z[self.plan.begin: self.plan.end].clone()
+
+    def dot_partials(self, x, y, mode: int):
+        n = x.numel()
+        out = self.torch.empty(max(1, -(-n // CHUNK)), dtype=self.torch.float64, device=self.dev)
+        if n:
+            self._lib.check(self.L.ie_dot_partials_f64(self._lib.ptr(x), self._lib.ptr(y), n, mode,
+                                                       self._lib.ptr(out), self._lib.stream_ptr()), "dot")
+        return out[: -(-n // CHUNK)] if n else out[:0]
+
+    def sum_partials(self, parts) -> float:
+        parts = parts.contiguous()
+        self._lib.check(self.L.ie_sum_partials_f64(self._lib.ptr(parts), parts.numel(), self._lib.ptr(self._scal),
+                                                   self._lib.stream_ptr()), "sum")
+        return float(self._scal.item())
+
+    def update(self, op: int, a, b, s: float):
+        if a.numel():
+            self._lib.check(self.L.ie_update_f64(op, self._lib.ptr(a), self._lib.ptr(b), float(s), a.numel(),
+                                                 self._lib.stream_ptr()), "update")
+
+    def sync(self):
+        self.torch.cuda.synchronize()
+
+
+# --------------------------------------------------------------------------
+# the sharded solver (control flow of pcg.py:54-136, fused 2-RHS schedule)
+# --------------------------------------------------------------------------
+@dataclass
+class ShardedReport:
+    n_it: int
+    achieved_residual: float
+    t_pcg: float
+    t_s: float
+    residual_history: list
+    stagnated: bool = False
+    converged: bool = False
+
+
+def solve_sharded(backend, comm: Comm, plan: ShardPlan, f_band, tol: float = 1e-12,
+                  max_iters: int | None = None, gather_solution: bool = True):
+    """PCG on the band decomposition; every rank returns the same report and
+    (if gather_solution) the full solution."""
+    if not 0.0 < tol < 1.0:
+        raise ValueError(f"tol must be in (0, 1), got {tol}")
+    N = plan.N
+    if max_iters is None:
+        max_iters = max(2 * N, 100)
+    t0 = time.perf_counter()
+    nf = math.sqrt(backend.sum_partials(comm.allgather_partials(backend.dot_partials(f_band, f_band, 0)[None])[0]))
+    u = backend.zeros(plan.size)
+    if nf == 0.0:
+        full = comm.allgather_band(u[None])[0] if gather_solution else u
+        return full, ShardedReport(0, 0.0, 0.0, 0.0, [0.0], converged=True)
+    t_prec, n_prec = 0.0, 0
+
+    def apply(r_band):
+        nonlocal t_prec, n_prec
+        ts = time.perf_counter()
+        r_full = comm.allgather_band(r_band[None])[0]
+        z = backend.apply_band(r_full)
+        backend.sync()
+        t_prec += time.perf_counter() - ts
+        n_prec += 1
+        return z
+
+    r = f_band.clone()
+    z = apply(r)
+    p = z.clone()
+    rho = backend.sum_partials(comm.allgather_partials(backend.dot_partials(r, z, 0)[None])[0])
+    hist = [1.0]
+    k = 0
+    pending = False
+    conv = stag = False
+    while True:
+        it = k + 1
+        do_p = it <= max_iters
+        if not pending and not do_p:
+            break
+        cols = ([p] if do_p else []) + ([u] if pending else [])
+        X = comm.allgather_band(_stack(cols))
+        Y = backend.matvec_band(X)
+        q = Y[0] if do_p else None
+        w = Y[-1] if pending else None
+        parts = []
+        if do_p:
+            parts.append(backend.dot_partials(p, q, 0))
+        if pending:
+            parts.append(backend.dot_partials(f_band, w, 1))
+        G = comm.allgather_partials(_stack(parts))
+        row = 0
+        denom = res2 = None
+        if do_p:
+            denom = backend.sum_partials(G[row])
+            row += 1
+        if pending:
+            res2 = backend.sum_partials(G[row])
+            rel = math.sqrt(res2) / nf
+            if not math.isfinite(rel):
+                raise FloatingPointError(f"non-finite residual at iteration {k}")
+            hist.append(rel)
+            if rel <= tol:
+                conv = True
+                break
+            if k >= STAGNATION_WINDOW and rel > (1.0 - STAGNATION_FACTOR) * hist[k - STAGNATION_WINDOW]:
+                stag = True
+                break
+            if not do_p:
+                break
+        if not math.isfinite(denom) or denom <= 0.0:
+            raise FloatingPointError(f"PCG breakdown at iteration {it}: p^T A p = {denom}")
+        alpha = rho / denom
+        backend.update(0, u, p, alpha)
+        backend.update(1, r, q, alpha)
+        k = it
+        pending = True
+        if k < max_iters:
+            z = apply(r)
+            rz = backend.sum_partials(comm.allgather_partials(backend.dot_partials(r, z, 0)[None])[0])
+            beta = rz / rho
+            rho = rz
+            backend.update(2, p, z, beta)
+    full = comm.allgather_band(u[None])[0] if gather_solution else u
+    rep = ShardedReport(n_it=k, achieved_residual=hist[-1], t_pcg=time.perf_counter() - t0,
+                        t_s=t_prec / max(n_prec, 1), residual_history=hist, stagnated=stag, converged=conv)
+    return full, rep
+
+
+def _stack(cols):
+    import torch
+    if isinstance(cols[0], torch.Tensor):
+        return torch.stack(cols)
+    return np.stack(cols)
+
+
+# --------------------------------------------------------------------------
+# bench entry for torchrun (bench.py --gpus N)
+# --------------------------------------------------------------------------
+def bench_sharded(args, metric, cfg, workload):
+    import json
+
+    import torch
+    import torch.distributed as dist
+
+    import paper_2108_12574_b200 as ie
+    ws, rank = dist.get_world_size(), dist.get_rank()
+    grid = ie.build_grid(cfg["dim"], cfg["n"])
+    op = ie.build_operator(grid, lattice="cell")
+    dec = ie.build_decomposition(grid, cfg["m"], cfg["w"], "schwarz")
+    plan = make_plan(grid, dec, ws, rank)
+    backend = CudaBackend(op, dec, plan, method=getattr(args, "matvec", "auto"))
+    comm = Comm(plan)
+    f = np.random.default_rng(cfg["seed"]).standard_normal(op.n)
+    f_band = backend.tensor(f[plan.begin: plan.end])
+    solve_sharded(backend, comm, plan, f_band, tol=1e-10, max_iters=max(args.warmup, 1), gather_solution=False)
+    dev = torch.device("cuda", torch.cuda.current_device())
+    st = torch.cuda.current_stream()
+    dist.barrier()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(st)
+    _, rep = solve_sharded(backend, comm, plan, f_band, tol=1e-10, max_iters=args.steps, gather_solution=False)
+    e1.record(st)
+    torch.cuda.synchronize()
+    dist.barrier()
+    ms = torch.tensor([e0.elapsed_time(e1)], device=dev)
+    dist.all_reduce(ms, op=dist.ReduceOp.MAX)
+    ms = float(ms.item())
+    if rank == 0:
+        out = {"metric": metric, "value": args.steps / (ms * 1e-3), "unit": "iter/s", "n_gpus": ws,
+               "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+               "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+               "data": "synthetic (BASELINE.json config 5, seeded)",
+               "config": {"workload": workload, "N": op.n, "parallelism": f"row/subdomain bands x{ws}",
+                          "matvec": backend.method, "bands": list(plan.bounds)},
+               "n_it": rep.n_it}
+        print(json.dumps(out))
+    return None

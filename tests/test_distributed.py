@@ -1,0 +1,99 @@
+"""Sharded PCG host logic on CPU: world-size 1/2/3 over gloo with the oracle
+backend must give bitwise-identical reports and solutions, and the plan must
+cover the unknowns with chunk-aligned bands."""
+
+import os
+import socket
+import tempfile
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from paper_2108_12574_b200 import geometry as G
+from paper_2108_12574_b200.distributed import CHUNK, Comm, band_bounds, blocks_intersecting, make_plan, solve_sharded
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+CASE = dict(dim=2, n=128, m=16, w=2, kind="schwarz", lattice="cell", seed=4)
+
+
+def _worker(rank, world, port, out_dir, case):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from tests.dist_cpu_backend import OracleBackend
+        grid = G.build_grid(case["dim"], case["n"])
+        dec = G.build_decomposition(grid, case["m"], case["w"], case["kind"])
+        plan = make_plan(grid, dec, world, rank)
+        be = OracleBackend(case["dim"], case["n"], case["m"], case["w"], case["kind"], case["lattice"], plan)
+        f = np.random.default_rng(case["seed"]).standard_normal(grid.n_points)
+        u, rep = solve_sharded(be, Comm(plan), plan, be.tensor(f[plan.begin: plan.end]), tol=1e-10,
+                               max_iters=case.get("max_iters"))
+        np.savez(os.path.join(out_dir, f"r{rank}.npz"), u=u.numpy(), hist=np.array(rep.residual_history),
+                 meta=np.array([rep.n_it, rep.converged, rep.stagnated]))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run(world, case):
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_worker, args=(world, _free_port(), d, case), nprocs=world, join=True)
+        return [dict(np.load(os.path.join(d, f"r{r}.npz"))) for r in range(world)]
+
+
+class TestPlan:
+    @pytest.mark.parametrize("dim,n,m,world", [(2, 1024, 128, 8), (2, 256, 32, 4), (2, 128, 16, 3),
+                                               (3, 32, 4, 2), (2, 32, 4, 2)])
+    def test_bands(self, dim, n, m, world):
+        grid = G.build_grid(dim, n)
+        b = band_bounds(grid, m, world)
+        assert b[0] == 0 and b[-1] == grid.n_points and all(x <= y for x, y in zip(b, b[1:]))
+        assert all(x % CHUNK == 0 for x in b[:-1])
+        if (dim, n, world) == (2, 1024, 8):
+            assert b == tuple(131072 * g for g in range(9))   # 16 subdomain rows per rank
+
+    def test_blocks_cover_band(self):
+        grid = G.build_grid(2, 128)
+        dec = G.build_decomposition(grid, 16, 2, "schwarz")
+        for world in (2, 3):
+            for r in range(world):
+                plan = make_plan(grid, dec, world, r)
+                covered = np.zeros(grid.n_points, bool)
+                for k in plan.blocks:
+                    covered[dec.subdomains[k]] = True
+                assert covered[plan.begin: plan.end].all()
+                # every block touching the band is included (z is complete on the band)
+                assert np.array_equal(plan.blocks, blocks_intersecting(dec.subdomains, plan.begin, plan.end))
+
+
+class TestShardedSolve:
+    def test_world_sizes_bitwise_equal_and_oracle_parity(self):
+        from oracle import iedd_oracle as O
+        res = {w: _run(w, CASE) for w in (1, 2, 3)}
+        ref = res[1][0]
+        for w in (2, 3):
+            for r in range(w):
+                assert np.array_equal(res[w][r]["hist"], ref["hist"])
+                assert np.array_equal(res[w][r]["u"], ref["u"])
+                assert np.array_equal(res[w][r]["meta"], ref["meta"])
+        grid = O.build_grid(2, 128)
+        op = O.build_operator(grid, "cell")
+        pre = O.SchwarzPrecond(op, O.build_decomposition(grid, 16, 2, "schwarz"))
+        f = np.random.default_rng(CASE["seed"]).standard_normal(op.n)
+        u, rep = O.pcg(O.FFTMatvec(op), pre, f, tol=1e-10)
+        assert abs(int(ref["meta"][0]) - rep.n_it) <= 1
+        assert np.linalg.norm(ref["u"] - u) <= 1e-10 * np.linalg.norm(u)
+
+    def test_max_iters_exit(self):
+        case = dict(CASE, max_iters=7)
+        res = _run(2, case)
+        assert int(res[0]["meta"][0]) == 7 and not res[0]["meta"][1]
+        assert np.array_equal(res[0]["hist"], res[1]["hist"]) and len(res[0]["hist"]) == 8

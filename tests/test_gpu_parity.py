@@ -410,3 +410,67 @@ class TestLanczos:
         op = ie.build_operator(ie.build_grid(2, 8))
         with pytest.raises(ValueError, match="which"):
             ie.extremal_eigenvalue_lanczos(ie.ToeplitzMatvec(op), ie.identity(64), 64, which="mid")
+
+
+class TestShardedCuda:
+    """The sharded driver's CUDA backend.  Only one GPU is available: the
+    driver runs as a 1-rank NCCL group (it must reproduce ie_pcg_f64
+    bitwise), and the per-rank pieces of a 3-rank plan are checked by running
+    each virtual rank's band on the same device."""
+
+    @pytest.fixture(scope="class")
+    def pg(self):
+        import socket
+
+        import torch
+        import torch.distributed as dist
+        if not dist.is_initialized():
+            with socket.socket() as s:
+                s.bind(("127.0.0.1", 0))
+                port = s.getsockname()[1]
+            dist.init_process_group("nccl", init_method=f"tcp://127.0.0.1:{port}", rank=0, world_size=1,
+                                    device_id=torch.device("cuda", 0))
+        yield dist
+        dist.destroy_process_group()
+
+    @pytest.mark.parametrize("method", METHODS)
+    def test_one_rank_matches_native_bitwise(self, ie, pg, method):
+        from paper_2108_12574_b200 import distributed as D
+        grid = ie.build_grid(2, 256)
+        op = ie.build_operator(grid, lattice="cell")
+        dec = ie.build_decomposition(grid, 32, 2, "schwarz")
+        plan = D.make_plan(grid, dec, 1, 0)
+        be = D.CudaBackend(op, dec, plan, method=method)
+        f = np.random.default_rng(1).standard_normal(op.n)
+        u_d, rep_d = D.solve_sharded(be, D.Comm(plan), plan, be.tensor(f), tol=1e-10)
+        pre = ie.from_decomposition(op, dec)
+        u_n, rep_n = ie.solve(ie.KernelMatvec(op, method=method), pre, f, tol=1e-10)
+        assert rep_d.n_it == rep_n.n_it
+        assert rep_d.residual_history == rep_n.residual_history
+        assert np.array_equal(u_d.cpu().numpy(), u_n)
+
+    def test_virtual_ranks_bitwise(self, ie):
+        import torch
+
+        from paper_2108_12574_b200 import distributed as D
+        grid = ie.build_grid(2, 256)
+        op = ie.build_operator(grid, lattice="cell")
+        dec = ie.build_decomposition(grid, 32, 2, "schwarz")
+        N = op.n
+        rng = np.random.default_rng(2)
+        X = torch.from_numpy(rng.standard_normal((2, N))).cuda()
+        full = D.CudaBackend(op, dec, D.make_plan(grid, dec, 1, 0), method="direct")
+        Yf = full.matvec_band(X)
+        zf = full.apply_band(X[0])
+        pf = full.dot_partials(X[0], X[1], 0)
+        for world in (2, 3, 8):
+            ys, zs, ps = [], [], []
+            for r in range(world):
+                plan = D.make_plan(grid, dec, world, r)
+                be = D.CudaBackend(op, dec, plan, method="direct")
+                ys.append(be.matvec_band(X))
+                zs.append(be.apply_band(X[0]))
+                ps.append(be.dot_partials(X[0][plan.begin:plan.end], X[1][plan.begin:plan.end], 0))
+            assert torch.equal(torch.cat(ys, dim=1), Yf)
+            assert torch.equal(torch.cat(zs), zf)
+            assert torch.equal(torch.cat(ps), pf)
