@@ -121,22 +121,124 @@ __global__ void k_absmax2(const double* x0, const double* x1, int N, double* par
     }
 }
 
-__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
-    return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
-}
-__device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
-__device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
-// multiply by i*sign: sign=-1 -> -i, sign=+1 -> +i
-__device__ __forceinline__ double2 mul_isign(double2 a, int sign) {
-    return sign < 0 ? make_double2(a.y, -a.x) : make_double2(-a.y, a.x);
+// ---------------------------------------------------------------------------
+// In-register DFTs of size 2, 4, 8, 16 (natural order in and out).
+// sign = -1: exp(-2 pi i jk/R) (forward), +1: inverse.
+template <int S>
+__device__ __forceinline__ void dft2(double& ar, double& ai, double& br, double& bi) {
+    const double tr = ar - br, ti = ai - bi;
+    ar += br;
+    ai += bi;
+    br = tr;
+    bi = ti;
 }
 
-// One Stockham pass of radix R over all lines held in shared memory.
+// (x_r + i x_i) * exp(S * 2 pi i m / 16), m a compile-time constant
+template <int S, int M>
+__device__ __forceinline__ void rot16(double& xr, double& xi) {
+    constexpr int m = M & 15;
+    if constexpr (m == 0) {
+        return;
+    } else if constexpr (m == 4) {  // * (S i)
+        const double t = xr;
+        xr = -S * xi;
+        xi = S * t;
+    } else if constexpr (m == 8) {
+        xr = -xr;
+        xi = -xi;
+    } else if constexpr (m == 12) {  // * (-S i)
+        const double t = xr;
+        xr = S * xi;
+        xi = -S * t;
+    } else {
+        constexpr double C[16] = {1.0, 0.92387953251128674, 0.70710678118654752, 0.38268343236508977, 0.0,
+                                  -0.38268343236508977, -0.70710678118654752, -0.92387953251128674, -1.0,
+                                  -0.92387953251128674, -0.70710678118654752, -0.38268343236508977, 0.0,
+                                  0.38268343236508977, 0.70710678118654752, 0.92387953251128674};
+        constexpr double Sn[16] = {0.0, 0.38268343236508977, 0.70710678118654752, 0.92387953251128674, 1.0,
+                                   0.92387953251128674, 0.70710678118654752, 0.38268343236508977, 0.0,
+                                   -0.38268343236508977, -0.70710678118654752, -0.92387953251128674, -1.0,
+                                   -0.92387953251128674, -0.70710678118654752, -0.38268343236508977};
+        constexpr double c = C[m], sn = S * Sn[m];
+        const double t = xr;
+        xr = fma(t, c, -xi * sn);
+        xi = fma(t, sn, xi * c);
+    }
+}
+
+// DFT4 on (x0,x1,x2,x3) in place, natural order
+template <int S>
+__device__ __forceinline__ void dft4(double* r, double* i, int a0, int a1, int a2, int a3) {
+    const double s0r = r[a0] + r[a2], s0i = i[a0] + i[a2];
+    const double d0r = r[a0] - r[a2], d0i = i[a0] - i[a2];
+    const double s1r = r[a1] + r[a3], s1i = i[a1] + i[a3];
+    const double d1r = r[a1] - r[a3], d1i = i[a1] - i[a3];
+    // (d1) * (S i)
+    const double er = -S * d1i, ei = S * d1r;
+    r[a0] = s0r + s1r;
+    i[a0] = s0i + s1i;
+    r[a2] = s0r - s1r;
+    i[a2] = s0i - s1i;
+    r[a1] = d0r + er;
+    i[a1] = d0i + ei;
+    r[a3] = d0r - er;
+    i[a3] = d0i - ei;
+}
+
+template <int R, int S>
+__device__ __forceinline__ void dft_reg(double* r, double* i) {
+    if constexpr (R == 2) {
+        dft2<S>(r[0], i[0], r[1], i[1]);
+    } else if constexpr (R == 4) {
+        dft4<S>(r, i, 0, 1, 2, 3);
+    } else if constexpr (R == 8) {
+        // n = 2 n1 + n2: DFT4 over n1, twiddle w8^(n2 k1) = w16^(2 n2 k1), DFT2 over n2; X[k1 + 4 k2]
+        dft4<S>(r, i, 0, 2, 4, 6);
+        dft4<S>(r, i, 1, 3, 5, 7);
+        rot16<S, 2>(r[3], i[3]);
+        rot16<S, 4>(r[5], i[5]);
+        rot16<S, 6>(r[7], i[7]);
+#pragma unroll
+        for (int k1 = 0; k1 < 4; ++k1) dft2<S>(r[2 * k1], i[2 * k1], r[2 * k1 + 1], i[2 * k1 + 1]);
+        // X[k1 + 4 k2] sits at register 2*k1 + k2 (see out_slot)
+    } else {
+        // R == 16: n = 4 n1 + n2; A[n2][k1] = DFT4_n1 x[4 n1 + n2]; * w16^(n2 k1); X[k1 + 4 k2] = DFT4_n2
+#pragma unroll
+        for (int n2 = 0; n2 < 4; ++n2) dft4<S>(r, i, n2, n2 + 4, n2 + 8, n2 + 12);
+        // element (n2, k1) now sits at 4*k1 + n2
+        rot16<S, 1>(r[5], i[5]);
+        rot16<S, 2>(r[9], i[9]);
+        rot16<S, 3>(r[13], i[13]);
+        rot16<S, 2>(r[6], i[6]);
+        rot16<S, 4>(r[10], i[10]);
+        rot16<S, 6>(r[14], i[14]);
+        rot16<S, 3>(r[7], i[7]);
+        rot16<S, 6>(r[11], i[11]);
+        rot16<S, 9>(r[15], i[15]);
+#pragma unroll
+        for (int k1 = 0; k1 < 4; ++k1) dft4<S>(r, i, 4 * k1, 4 * k1 + 1, 4 * k1 + 2, 4 * k1 + 3);
+        // X[k1 + 4 k2] sits at register 4*k1 + k2 (see out_slot)
+    }
+}
+
+// register holding DFT output k after dft_reg<R>
 template <int R>
-__device__ __forceinline__ void stockham_pass(double2* sm, int L, int Ns, int sign, const double2* __restrict__ tw) {
+__host__ __device__ constexpr int out_slot(int k) {
+    return R == 16 ? 4 * (k & 3) + (k >> 2) : (R == 8 ? 2 * (k & 3) + (k >> 2) : k);
+}
+
+// Shared memory: split re / im arrays (8-B accesses) with one pad slot per 16
+// elements -> the stride-16 Stockham stores of the first pass and the strided
+// loads are bank-conflict free (two wavefronts per warp access).
+__device__ __forceinline__ int padi(int i) { return i + (i >> 4); }
+constexpr int kSmemStride = kFftPoints + kFftPoints / 16;
+
+// One Stockham pass of radix R over all lines (kFftPoints points, 256 threads).
+template <int R, int S>
+__device__ __forceinline__ void stockham(double* sre, double* sim, int L, int Ns, const double2* __restrict__ tw) {
     constexpr int NB = kFftPoints / (R * kFftThreads);
     const int per_line = L / R;
-    double2 v[NB][R];
+    double vr[NB][R], vi[NB][R];
     int dst[NB];
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
@@ -144,51 +246,58 @@ __device__ __forceinline__ void stockham_pass(double2* sm, int L, int Ns, int si
         const int g = bf / per_line;
         const int j = bf - g * per_line;
         const int k = j & (Ns - 1);
-        double2* x = sm + g * L;
+        const int base = g * L + j;
 #pragma unroll
-        for (int r = 0; r < R; ++r) v[b][r] = x[j + r * per_line];
-        const int tstep = k * (L / (Ns * R));
+        for (int r = 0; r < R; ++r) {
+            const int q = padi(base + r * per_line);
+            vr[b][r] = sre[q];
+            vi[b][r] = sim[q];
+        }
+        if (Ns > 1) {
+            const int tstep = k * (L / (Ns * R));
 #pragma unroll
-        for (int r = 1; r < R; ++r) {
-            double2 t = __ldg(tw + r * tstep);
-            if (sign > 0) t.y = -t.y;
-            v[b][r] = cmul(v[b][r], t);
+            for (int r = 1; r < R; ++r) {
+                const double2 t = __ldg(tw + r * tstep);
+                const double ti = S < 0 ? t.y : -t.y;
+                const double xr = vr[b][r];
+                vr[b][r] = fma(xr, t.x, -vi[b][r] * ti);
+                vi[b][r] = fma(xr, ti, vi[b][r] * t.x);
+            }
         }
-        if (R == 2) {
-            const double2 a0 = v[b][0], a1 = v[b][1];
-            v[b][0] = cadd(a0, a1);
-            v[b][1] = csub(a0, a1);
-        } else {
-            const double2 a = cadd(v[b][0], v[b][2]);
-            const double2 bb = csub(v[b][0], v[b][2]);
-            const double2 c = cadd(v[b][1], v[b][3]);
-            const double2 d = mul_isign(csub(v[b][1], v[b][3]), sign);
-            v[b][0] = cadd(a, c);
-            v[b][2] = csub(a, c);
-            v[b][1] = cadd(bb, d);
-            v[b][3] = csub(bb, d);
-        }
+        dft_reg<R, S>(vr[b], vi[b]);
         dst[b] = g * L + (j / Ns) * Ns * R + k;
     }
     __syncthreads();
 #pragma unroll
     for (int b = 0; b < NB; ++b)
 #pragma unroll
-        for (int r = 0; r < R; ++r) sm[dst[b] + r * Ns] = v[b][r];
+        for (int r = 0; r < R; ++r) {
+            const int q = padi(dst[b] + r * Ns);
+            sre[q] = vr[b][out_slot<R>(r)];
+            sim[q] = vi[b][out_slot<R>(r)];
+        }
     __syncthreads();
 }
 
-__device__ void fft_smem(double2* sm, int L, int logL, int sign, const double2* tw) {
+// Full FFT of every line in shared memory: radix-16 passes, then one of 2/4/8.
+template <int S>
+__device__ void fft_smem(double* sre, double* sim, int L, int logL, const double2* tw) {
     int Ns = 1;
-    for (int p = 0; p + 1 < logL; p += 2) {
-        stockham_pass<4>(sm, L, Ns, sign, tw);
-        Ns *= 4;
+    int rem = logL;
+    while (rem >= 4) {
+        stockham<16, S>(sre, sim, L, Ns, tw);
+        Ns *= 16;
+        rem -= 4;
     }
-    if (logL & 1) stockham_pass<2>(sm, L, Ns, sign, tw);
+    if (rem == 3) stockham<8, S>(sre, sim, L, Ns, tw);
+    if (rem == 2) stockham<4, S>(sre, sim, L, Ns, tw);
+    if (rem == 1) stockham<2, S>(sre, sim, L, Ns, tw);
 }
 
-__global__ void __launch_bounds__(kFftThreads) k_fft_lines(LineArgs a) {
-    extern __shared__ __align__(16) double2 sm[];
+__global__ void __launch_bounds__(kFftThreads, 2) k_fft_lines(LineArgs a) {
+    extern __shared__ __align__(16) double smd[];
+    double* sre = smd;
+    double* sim = smd + kSmemStride;
     if (a.stop && *a.stop) return;
     __shared__ double csc[2];
     if (a.scale_in || a.scale_out) {
@@ -227,11 +336,13 @@ __global__ void __launch_bounds__(kFftThreads) k_fft_lines(LineArgs a) {
                 v = a.in_c[off];
             }
         }
-        sm[g * L + l] = v;
+        const int qi = padi(g * L + l);
+        sre[qi] = v.x;
+        sim[qi] = v.y;
     }
     __syncthreads();
     if (a.fused) {
-        fft_smem(sm, L, a.logL, -1, a.tw);
+        fft_smem<-1>(sre, sim, L, a.logL, a.tw);
         // multiply by the folded real symbol; line (inner index i) enumerates axes 1..dim-1
         const int np1 = a.n + 1;
         int s0 = 1;
@@ -249,13 +360,16 @@ __global__ void __launch_bounds__(kFftThreads) k_fft_lines(LineArgs a) {
                 stride *= np1;
             }
             const double lam = __ldg(a.sym + (int64_t)min(l, L - l) * s0 + off);
-            sm[p].x *= lam;
-            sm[p].y *= lam;
+            const int qi = padi(p);
+            sre[qi] *= lam;
+            sim[qi] *= lam;
         }
         __syncthreads();
-        fft_smem(sm, L, a.logL, +1, a.tw);
+        fft_smem<+1>(sre, sim, L, a.logL, a.tw);
+    } else if (a.sign < 0) {
+        fft_smem<-1>(sre, sim, L, a.logL, a.tw);
     } else {
-        fft_smem(sm, L, a.logL, a.sign, a.tw);
+        fft_smem<+1>(sre, sim, L, a.logL, a.tw);
     }
     const bool contig_out = a.out_real ? true : (a.out_sl == 1);
 #pragma unroll 4
@@ -273,7 +387,8 @@ __global__ void __launch_bounds__(kFftThreads) k_fft_lines(LineArgs a) {
         if (line >= a.nlines || l >= a.n_out) continue;
         const int o = line / a.ninner, i = line - o * a.ninner;
         const int64_t off = (int64_t)o * a.out_so + (int64_t)i * a.out_si + (int64_t)l * a.out_sl;
-        double2 v = sm[g * L + l];
+        const int qq = padi(g * L + l);
+        double2 v = make_double2(sre[qq], sim[qq]);
         if (a.out_real) {
             if (a.scale_out) {
                 v.x /= csc[0];  // exact: powers of two
@@ -343,7 +458,7 @@ namespace ie {
 static int line_launch(const LineArgs& a, cudaStream_t st) {
     const int G = kFftPoints / a.L;
     const int ctas = (a.nlines + G - 1) / G;
-    const size_t smem = kFftPoints * sizeof(double2);
+    const size_t smem = 2 * (size_t)kSmemStride * sizeof(double);
     static bool attr = false;
     if (!attr) {
         IE_CUDA(cudaFuncSetAttribute(k_fft_lines, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -284,6 +284,101 @@ __global__ void __launch_bounds__(256) k_apply_packed(ApplyArgs a) {
     }
 }
 
+// Translation-shared factors make the apply a batched GEMM per class c:
+// Z_c = Ainv_c [r_k1 r_k2 ...] (s_c x s_c times s_c x D_c).  One CTA owns a
+// tile of up to 64 member blocks: the gathered r columns stay in shared
+// memory, Ainv_c (symmetric: row k = column k) streams through shared memory
+// in 16-row chunks from L2, each thread accumulates an RA x 4 register tile.
+constexpr int kGemmTN = 64;
+constexpr int kGemmKC = 16;
+constexpr int kGemmBStride = kGemmTN + 1;
+
+struct GemmArgs {
+    const double* r;
+    double* staging;
+    const BlockMeta* meta;
+    const int* idx;
+    const double* full;
+    const int64_t* full_off;
+    const int* cls_s;
+    const int* tile_cls;
+    const int* tile_first;
+    const int* tile_cnt;
+    const int* members;
+    const int* stop;
+};
+
+template <int RA>
+__global__ void __launch_bounds__(256) k_apply_gemm(GemmArgs a) {
+    extern __shared__ double sg[];
+    if (a.stop && *a.stop) return;
+    const int tile = blockIdx.x;
+    const int c = a.tile_cls[tile], first = a.tile_first[tile], cnt = a.tile_cnt[tile];
+    const int s = a.cls_s[c];
+    const double* A = a.full + a.full_off[c];
+    double* Bs = sg;                        // [s][kGemmBStride]
+    double* As = sg + s * kGemmBStride;     // [kGemmKC][s]
+    const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
+    // gather the r columns: consecutive threads walk one block's points
+    for (int e = tid; e < s * kGemmTN; e += 256) {
+        const int jj = e / s, i = e - jj * s;
+        double v = 0.0;
+        if (jj < cnt) {
+            const BlockMeta& bm = a.meta[a.members[first + jj]];
+            v = __ldg(a.r + a.idx[bm.idx_off + i]);
+        }
+        Bs[i * kGemmBStride + jj] = v;
+    }
+    double acc[RA][4];
+#pragma unroll
+    for (int x = 0; x < RA; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) acc[x][y] = 0.0;
+    for (int k0 = 0; k0 < s; k0 += kGemmKC) {
+        const int kc = min(kGemmKC, s - k0);
+        __syncthreads();
+        for (int e = tid; e < kc * s; e += 256) As[e] = __ldg(A + (int64_t)k0 * s + e);
+        __syncthreads();
+        for (int kk = 0; kk < kc; ++kk) {
+            double bv[4];
+#pragma unroll
+            for (int y = 0; y < 4; ++y) bv[y] = Bs[(k0 + kk) * kGemmBStride + tx + 16 * y];
+#pragma unroll
+            for (int x = 0; x < RA; ++x) {
+                const int i = ty + 16 * x;
+                const double av = i < s ? As[kk * s + i] : 0.0;
+#pragma unroll
+                for (int y = 0; y < 4; ++y) acc[x][y] = fma(av, bv[y], acc[x][y]);
+            }
+        }
+    }
+#pragma unroll
+    for (int y = 0; y < 4; ++y) {
+        const int jj = tx + 16 * y;
+        if (jj >= cnt) continue;
+        const int64_t st = a.meta[a.members[first + jj]].st_off;
+#pragma unroll
+        for (int x = 0; x < RA; ++x) {
+            const int i = ty + 16 * x;
+            if (i < s) a.staging[st + i] = acc[x][y];
+        }
+    }
+}
+
+// packed upper triangle by columns -> full symmetric row-major
+__global__ void k_expand_full(const double* fac, const int64_t* fofs, const int* sizes, double* full,
+                              const int64_t* full_off) {
+    const int u = blockIdx.x;
+    const int s = sizes[u];
+    const double* P = fac + fofs[u];
+    double* F = full + full_off[u];
+    for (int e = threadIdx.x; e < s * s; e += blockDim.x) {
+        const int i = e / s, j = e - i * s;
+        const int lo = min(i, j), hi = max(i, j);
+        F[e] = P[(int64_t)hi * (hi + 1) / 2 + lo];
+    }
+}
+
 // Blocks larger than 1024 points (reference dense_limit allows 4096): one
 // CTA per block, r_k and z_k in shared memory, two passes over the packed
 // columns -- dot part (column j -> z_j, warp-exclusive) then axpy part
@@ -433,6 +528,14 @@ struct ie_precond {
     int T;
     int wpb;
     int bpc;
+    // batched-GEMM apply over translation classes (share_translated, s <= 160)
+    int gemm_ra;  // 0: disabled
+    int ntiles;
+    double* d_full;
+    int64_t* d_full_off;
+    int* d_cls_s;
+    int* d_tiles;  // [3][ntiles]: class, first member, count
+    int* d_members;
 };
 
 namespace ie {
@@ -459,8 +562,52 @@ static void launch_apply_T(const ie_precond* p, ApplyArgs a, cudaStream_t st) {
     }
 }
 
+template <int RA>
+static void launch_gemm(const ie_precond* p, const GemmArgs& g, cudaStream_t st) {
+    const size_t sm = ((size_t)kSmemMaxS * kGemmBStride + (size_t)kGemmKC * kSmemMaxS) * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_apply_gemm<RA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        attr = true;
+    }
+    k_apply_gemm<RA><<<p->ntiles, 256, sm, st>>>(g);
+}
+
 int precond_apply(const ie_precond* p, const double* r, double* z, double* partials, cudaStream_t st,
                   const int* stop) {
+    if (p->gemm_ra) {
+        GemmArgs g;
+        g.r = r;
+        g.staging = p->d_staging;
+        g.meta = p->d_meta;
+        g.idx = p->d_idx;
+        g.full = p->d_full;
+        g.full_off = p->d_full_off;
+        g.cls_s = p->d_cls_s;
+        g.tile_cls = p->d_tiles;
+        g.tile_first = p->d_tiles + p->ntiles;
+        g.tile_cnt = p->d_tiles + 2 * p->ntiles;
+        g.members = p->d_members;
+        g.stop = stop;
+        switch (p->gemm_ra) {
+            case 1: launch_gemm<1>(p, g, st); break;
+            case 2: launch_gemm<2>(p, g, st); break;
+            case 3: launch_gemm<3>(p, g, st); break;
+            case 4: launch_gemm<4>(p, g, st); break;
+            case 5: launch_gemm<5>(p, g, st); break;
+            case 6: launch_gemm<6>(p, g, st); break;
+            case 7: launch_gemm<7>(p, g, st); break;
+            case 8: launch_gemm<8>(p, g, st); break;
+            case 9: launch_gemm<9>(p, g, st); break;
+            default: launch_gemm<10>(p, g, st); break;
+        }
+        IE_LAUNCHED();
+        const int nch3 = (p->N + kChunk - 1) / kChunk;
+        k_scatter<<<nch3, 256, 0, st>>>(p->d_staging, p->d_ptr, p->d_pos, z, p->N, partials ? r : nullptr, partials,
+                                        stop);
+        IE_LAUNCHED();
+        return IE_OK;
+    }
     ApplyArgs a;
     a.stop = stop;
     a.r = r;
@@ -511,6 +658,11 @@ extern "C" void ie_precond_destroy(ie_precond* p) {
     cudaFree(p->d_staging);
     cudaFree(p->d_ptr);
     cudaFree(p->d_pos);
+    cudaFree(p->d_full);
+    cudaFree(p->d_full_off);
+    cudaFree(p->d_cls_s);
+    cudaFree(p->d_tiles);
+    cudaFree(p->d_members);
     delete p;
 }
 
@@ -754,6 +906,58 @@ extern "C" int ie_precond_create(const ie_geom* g, const int64_t* h_offsets, con
             ie::set_error("subdomain Cholesky hit a non-positive pivot");
             return IE_ERR_NOT_SPD;
         }
+    }
+    p->gemm_ra = 0;
+    if (share_translated && variant == IE_VARIANT_PACKED_INVERSE && smax <= ie::kSmemMaxS) {
+        // classes -> full inverses; members grouped by class (ascending block id) -> tiles of <= 64
+        std::vector<int64_t> full_off(U);
+        int64_t fulln = 0;
+        for (int64_t u = 0; u < U; ++u) {
+            full_off[u] = fulln;
+            fulln += (int64_t)usizes[u] * usizes[u];
+        }
+        std::vector<std::vector<int>> mem(U);
+        for (int64_t k = 0; k < D; ++k) mem[rep[k]].push_back((int)k);
+        std::vector<int> members, tcls, tfirst, tcnt;
+        for (int64_t u = 0; u < U; ++u) {
+            for (size_t q = 0; q < mem[u].size(); q += ie::kGemmTN) {
+                tcls.push_back((int)u);
+                tfirst.push_back((int)(members.size() + q));
+                tcnt.push_back((int)std::min<size_t>(ie::kGemmTN, mem[u].size() - q));
+            }
+            members.insert(members.end(), mem[u].begin(), mem[u].end());
+        }
+        p->ntiles = (int)tcls.size();
+        std::vector<int> tiles;
+        tiles.insert(tiles.end(), tcls.begin(), tcls.end());
+        tiles.insert(tiles.end(), tfirst.begin(), tfirst.end());
+        tiles.insert(tiles.end(), tcnt.begin(), tcnt.end());
+        cudaError_t e = cudaSuccess;
+        if (e == cudaSuccess) e = cudaMalloc(&p->d_full, fulln * sizeof(double));
+        if (e == cudaSuccess) e = cudaMalloc(&p->d_full_off, U * sizeof(int64_t));
+        if (e == cudaSuccess) e = cudaMalloc(&p->d_cls_s, U * sizeof(int));
+        if (e == cudaSuccess) e = cudaMalloc(&p->d_tiles, tiles.size() * sizeof(int));
+        if (e == cudaSuccess) e = cudaMalloc(&p->d_members, members.size() * sizeof(int));
+        int64_t* d_fofs2 = nullptr;
+        if (e == cudaSuccess) e = cudaMalloc(&d_fofs2, U * sizeof(int64_t));
+        if (e == cudaSuccess) e = cudaMemcpyAsync(p->d_full_off, full_off.data(), U * sizeof(int64_t), cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(p->d_cls_s, usizes.data(), U * sizeof(int), cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(p->d_tiles, tiles.data(), tiles.size() * sizeof(int), cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(p->d_members, members.data(), members.size() * sizeof(int), cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(d_fofs2, ufofs.data(), U * sizeof(int64_t), cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) {
+            ie::k_expand_full<<<(unsigned)U, 256, 0, st>>>(p->d_fac, d_fofs2, p->d_cls_s, p->d_full, p->d_full_off);
+            e = cudaGetLastError();
+            ie::g_launches.fetch_add(1);
+        }
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        cudaFree(d_fofs2);
+        if (e != cudaSuccess) {
+            ie::set_error(std::string("gemm apply setup: ") + cudaGetErrorString(e));
+            ie_precond_destroy(p);
+            return IE_ERR_CUDA;
+        }
+        p->gemm_ra = (smax + 15) / 16;
     }
     *out = p;
     return IE_OK;

@@ -163,15 +163,28 @@ class TestApply:
         z = pre.apply(g[f"ap_{case}_r"])
         assert rel(z, g[f"ap_{case}_z"]) <= 1e-12
 
-    def test_share_is_bitwise_exact(self, ie, rng):
+    def test_share_translated(self, ie, rng):
+        # shared factors are bitwise those of the individual blocks (same integer
+        # distances); the shared apply is a per-class GEMM, so it agrees with the
+        # per-block kernel to rounding (different association order)
         grid = ie.build_grid(2, 64)
         op = ie.build_operator(grid, lattice="cell")
         d = ie.build_decomposition(grid, 8, 2, "schwarz")
         a = ie.from_decomposition(op, d, share_translated=True)
         b = ie.from_decomposition(op, d, share_translated=False)
-        assert a.stats()["factored_blocks"] < b.stats()["factored_blocks"] == 64
+        assert a.stats()["factored_blocks"] == 4 and b.stats()["factored_blocks"] == 64
         r = rng.standard_normal(op.n)
-        assert np.array_equal(a.apply(r), b.apply(r))
+        assert rel(a.apply(r), b.apply(r)) <= 1e-14
+        c = ie.from_decomposition(op, d, share_translated=True, variant="subst")
+        assert rel(c.apply(r), b.apply(r)) <= 1e-13
+
+    def test_gemm_apply_deterministic(self, ie, rng):
+        grid = ie.build_grid(2, 256)
+        op = ie.build_operator(grid, lattice="cell")
+        a = ie.from_decomposition(op, ie.build_decomposition(grid, 32, 2, "schwarz"))
+        r = rng.standard_normal(op.n)
+        z1 = a.apply(r)
+        assert np.array_equal(z1, a.apply(r))
 
     def test_identity_and_errors(self, ie, rng):
         pre = ie.identity(16)
@@ -223,7 +236,11 @@ class TestApply:
             assert rel(pre.apply(r), zr) <= 1e-12
 
 
-def _pcg_check(rep, u, g, kind, u_tol=1e-10, it_tol=1):
+def _pcg_check(rep, u, g, kind, u_tol=1e-10, it_tol=2):
+    # n_it contract +-2: the last residuals of config 1 Jacobi / config 3 hover
+    # at tol (1.05e-10 vs 1e-10); valid rounding choices (oracle PCG with the
+    # device apply and direct matvec, the native FFT solver, ...) land on
+    # 77-80 where the reference has 78 (tools/diag_c1.py).
     n_it = int(g[f"{kind}_meta"][0])
     assert abs(rep.n_it - n_it) <= it_tol, (rep.n_it, n_it)
     assert rep.converged == bool(g[f"{kind}_meta"][1])
@@ -263,7 +280,7 @@ class TestPCG:
         # iterations): a pure 1e-16..1e-14 random perturbation of the oracle's
         # own matvec moves n_it 58 -> 59 (tools/diag notes in DESIGN.md), and the
         # direct sum (row error 6e-16 median vs FFT 2e-16) lands at 60.
-        _pcg_check(rep, u, g, "schwarz", it_tol=2)
+        _pcg_check(rep, u, g, "schwarz")
 
     @pytest.mark.parametrize("method", METHODS)
     def test_c4(self, ie, golden, method):
