@@ -24,12 +24,14 @@
 namespace ie {
 
 constexpr int kFftPoints = 4096;
+constexpr int kLogFftPoints = 12;
 constexpr int kFftThreads = 256;
 constexpr int kPtsPerThread = kFftPoints / kFftThreads;
 
 struct LineArgs {
     int nlines;   // lines in this pass
-    int ninner;   // line g -> o = g / ninner, i = g % ninner
+    int ninner;   // line g -> o = g / ninner, i = g % ninner (a power of two)
+    int lg_ninner;
     int L;
     int logL;
     // source
@@ -234,30 +236,45 @@ __device__ __forceinline__ int padi(int i) { return i + (i >> 4); }
 constexpr int kSmemStride = kFftPoints + kFftPoints / 16;
 
 // One Stockham pass of radix R over all lines (kFftPoints points, 256 threads).
+// exp(-2 pi i m / L) from the quarter-wave table q[r] = (cos, sin)(2 pi r / L),
+// r < L/4, in shared memory
+__device__ __forceinline__ double2 twiddle(const double2* qt, int m, int logL) {
+    const int quad = m >> (logL - 2);
+    const double2 cs = qt[m & ((1 << (logL - 2)) - 1)];
+    // theta = theta_r + quad * pi/2 ; return (cos theta, -sin theta)
+    switch (quad & 3) {
+        case 0: return make_double2(cs.x, -cs.y);
+        case 1: return make_double2(-cs.y, -cs.x);
+        case 2: return make_double2(-cs.x, cs.y);
+        default: return make_double2(cs.y, cs.x);
+    }
+}
+
 template <int R, int S>
-__device__ __forceinline__ void stockham(double* sre, double* sim, int L, int Ns, const double2* __restrict__ tw) {
+__device__ __forceinline__ void stockham(double* sre, double* sim, int logL, int logNs, const double2* qt) {
     constexpr int NB = kFftPoints / (R * kFftThreads);
-    const int per_line = L / R;
+    constexpr int LR = R == 16 ? 4 : (R == 8 ? 3 : (R == 4 ? 2 : 1));
+    const int lpl = logL - LR;  // log2(L / R)
     double vr[NB][R], vi[NB][R];
     int dst[NB];
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
         const int bf = threadIdx.x + b * kFftThreads;
-        const int g = bf / per_line;
-        const int j = bf - g * per_line;
-        const int k = j & (Ns - 1);
-        const int base = g * L + j;
+        const int g = bf >> lpl;
+        const int j = bf & ((1 << lpl) - 1);
+        const int k = j & ((1 << logNs) - 1);
+        const int base = (g << logL) + j;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            const int q = padi(base + r * per_line);
+            const int q = padi(base + (r << lpl));
             vr[b][r] = sre[q];
             vi[b][r] = sim[q];
         }
-        if (Ns > 1) {
-            const int tstep = k * (L / (Ns * R));
+        if (logNs > 0) {
+            const int tstep = k << (logL - logNs - LR);
 #pragma unroll
             for (int r = 1; r < R; ++r) {
-                const double2 t = __ldg(tw + r * tstep);
+                const double2 t = twiddle(qt, r * tstep, logL);
                 const double ti = S < 0 ? t.y : -t.y;
                 const double xr = vr[b][r];
                 vr[b][r] = fma(xr, t.x, -vi[b][r] * ti);
@@ -265,14 +282,14 @@ __device__ __forceinline__ void stockham(double* sre, double* sim, int L, int Ns
             }
         }
         dft_reg<R, S>(vr[b], vi[b]);
-        dst[b] = g * L + (j / Ns) * Ns * R + k;
+        dst[b] = (g << logL) + ((j >> logNs) << (logNs + LR)) + k;
     }
     __syncthreads();
 #pragma unroll
     for (int b = 0; b < NB; ++b)
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            const int q = padi(dst[b] + r * Ns);
+            const int q = padi(dst[b] + (r << logNs));
             sre[q] = vr[b][out_slot<R>(r)];
             sim[q] = vi[b][out_slot<R>(r)];
         }
@@ -281,81 +298,110 @@ __device__ __forceinline__ void stockham(double* sre, double* sim, int L, int Ns
 
 // Full FFT of every line in shared memory: radix-16 passes, then one of 2/4/8.
 template <int S>
-__device__ void fft_smem(double* sre, double* sim, int L, int logL, const double2* tw) {
-    int Ns = 1;
+__device__ void fft_smem(double* sre, double* sim, int logL, const double2* qt) {
+    int logNs = 0;
     int rem = logL;
     while (rem >= 4) {
-        stockham<16, S>(sre, sim, L, Ns, tw);
-        Ns *= 16;
+        stockham<16, S>(sre, sim, logL, logNs, qt);
+        logNs += 4;
         rem -= 4;
     }
-    if (rem == 3) stockham<8, S>(sre, sim, L, Ns, tw);
-    if (rem == 2) stockham<4, S>(sre, sim, L, Ns, tw);
-    if (rem == 1) stockham<2, S>(sre, sim, L, Ns, tw);
+    if (rem == 3) stockham<8, S>(sre, sim, logL, logNs, qt);
+    if (rem == 2) stockham<4, S>(sre, sim, logL, logNs, qt);
+    if (rem == 1) stockham<2, S>(sre, sim, logL, logNs, qt);
 }
 
+// Pass modes: what a line transform reads, does and writes.
+enum FftMode { kFwdCC = 0, kInvCC = 1, kFwdRC = 2, kInvCR = 3, kFusedCC = 4, kFusedRR = 5 };
+
+template <int MODE>
 __global__ void __launch_bounds__(kFftThreads, 2) k_fft_lines(LineArgs a) {
     extern __shared__ __align__(16) double smd[];
+    constexpr bool in_real = MODE == kFwdRC || MODE == kFusedRR;
+    constexpr bool out_real = MODE == kInvCR || MODE == kFusedRR;
+    constexpr bool fused = MODE == kFusedCC || MODE == kFusedRR;
     double* sre = smd;
     double* sim = smd + kSmemStride;
+    double2* qt = reinterpret_cast<double2*>(smd + 2 * kSmemStride);  // quarter-wave twiddles
     if (a.stop && *a.stop) return;
     __shared__ double csc[2];
-    if (a.scale_in || a.scale_out) {
-        column_scales(a, csc);
-        __syncthreads();
-    }
     const int L = a.L;
-    const int G = kFftPoints / L;
+    const int logL = a.logL;
+    for (int r = threadIdx.x; r < (L >> 2); r += kFftThreads) {
+        const double2 t = __ldg(a.tw + r);  // exp(-2 pi i r / L) = (cos, -sin)
+        qt[r] = make_double2(t.x, -t.y);
+    }
+    if ((in_real && a.scale_in) || (out_real && a.scale_out)) column_scales(a, csc);
+    __syncthreads();
+    const int logG = kLogFftPoints - logL;
+    const int G = 1 << logG;
     const int g0 = blockIdx.x * G;
-    // load (coalesced along l when lines are contiguous, across lines otherwise)
-    const bool contig_in = a.in_real ? true : (a.in_sl == 1);
-#pragma unroll 4
+    const int lgi = a.lg_ninner;
+    // load: all 16 points per thread issued before the shared-memory stores
+    const bool contig_in = in_real || a.in_sl == 1;
+    double2 v[kPtsPerThread];
+#pragma unroll
     for (int q = 0; q < kPtsPerThread; ++q) {
         const int p = threadIdx.x + q * kFftThreads;
         int g, l;
         if (contig_in) {
-            g = p / L;
-            l = p - g * L;
+            g = p >> logL;
+            l = p & (L - 1);
         } else {
-            g = p % G;
-            l = p / G;
+            g = p & (G - 1);
+            l = p >> logG;
         }
         const int line = g0 + g;
-        double2 v = make_double2(0.0, 0.0);
+        v[q] = make_double2(0.0, 0.0);
         if (line < a.nlines && l < a.n_in) {
-            const int o = line / a.ninner, i = line - o * a.ninner;
+            const int o = line >> lgi, i = line & ((1 << lgi) - 1);
             const int64_t off = (int64_t)o * a.in_so + (int64_t)i * a.in_si + (int64_t)l * a.in_sl;
-            if (a.in_real) {
-                v.x = a.x0[off];
-                if (a.x1) v.y = a.x1[off];
-                if (a.scale_in) {
-                    v.x *= csc[0];
-                    v.y *= csc[1];
-                }
+            if constexpr (in_real) {
+                v[q].x = __ldg(a.x0 + off);
+                if (a.x1) v[q].y = __ldg(a.x1 + off);
             } else {
-                v = a.in_c[off];
+                v[q] = a.in_c[off];
+            }
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < kPtsPerThread; ++q) {
+        const int p = threadIdx.x + q * kFftThreads;
+        int g, l;
+        if (contig_in) {
+            g = p >> logL;
+            l = p & (L - 1);
+        } else {
+            g = p & (G - 1);
+            l = p >> logG;
+        }
+        if constexpr (in_real) {
+            if (a.scale_in) {
+                v[q].x *= csc[0];
+                v[q].y *= csc[1];
             }
         }
         const int qi = padi(g * L + l);
-        sre[qi] = v.x;
-        sim[qi] = v.y;
+        sre[qi] = v[q].x;
+        sim[qi] = v[q].y;
     }
     __syncthreads();
-    if (a.fused) {
-        fft_smem<-1>(sre, sim, L, a.logL, a.tw);
+    if constexpr (fused) {
+        fft_smem<-1>(sre, sim, logL, qt);
         // multiply by the folded real symbol; line (inner index i) enumerates axes 1..dim-1
         const int np1 = a.n + 1;
         int s0 = 1;
         for (int d = 1; d < a.dim; ++d) s0 *= np1;
+#pragma unroll 4
         for (int q = 0; q < kPtsPerThread; ++q) {
             const int p = threadIdx.x + q * kFftThreads;
-            const int g = p / L, l = p - g * L;
+            const int g = p >> logL, l = p & (L - 1);
             const int line = g0 + g;
             if (line >= a.nlines) continue;
-            int tmp = line % a.ninner, off = 0, stride = 1;
+            int tmp = line & ((1 << lgi) - 1), off = 0, stride = 1;
             for (int d = a.dim - 1; d >= 1; --d) {
-                const int k = tmp % L;
-                tmp /= L;
+                const int k = tmp & (L - 1);
+                tmp >>= logL;
                 off += min(k, L - k) * stride;
                 stride *= np1;
             }
@@ -365,39 +411,39 @@ __global__ void __launch_bounds__(kFftThreads, 2) k_fft_lines(LineArgs a) {
             sim[qi] *= lam;
         }
         __syncthreads();
-        fft_smem<+1>(sre, sim, L, a.logL, a.tw);
-    } else if (a.sign < 0) {
-        fft_smem<-1>(sre, sim, L, a.logL, a.tw);
+        fft_smem<+1>(sre, sim, logL, qt);
+    } else if constexpr (MODE == kFwdCC || MODE == kFwdRC) {
+        fft_smem<-1>(sre, sim, logL, qt);
     } else {
-        fft_smem<+1>(sre, sim, L, a.logL, a.tw);
+        fft_smem<+1>(sre, sim, logL, qt);
     }
-    const bool contig_out = a.out_real ? true : (a.out_sl == 1);
+    const bool contig_out = out_real || a.out_sl == 1;
 #pragma unroll 4
     for (int q = 0; q < kPtsPerThread; ++q) {
         const int p = threadIdx.x + q * kFftThreads;
         int g, l;
         if (contig_out) {
-            g = p / L;
-            l = p - g * L;
+            g = p >> logL;
+            l = p & (L - 1);
         } else {
-            g = p % G;
-            l = p / G;
+            g = p & (G - 1);
+            l = p >> logG;
         }
         const int line = g0 + g;
         if (line >= a.nlines || l >= a.n_out) continue;
-        const int o = line / a.ninner, i = line - o * a.ninner;
+        const int o = line >> lgi, i = line & ((1 << lgi) - 1);
         const int64_t off = (int64_t)o * a.out_so + (int64_t)i * a.out_si + (int64_t)l * a.out_sl;
         const int qq = padi(g * L + l);
-        double2 v = make_double2(sre[qq], sim[qq]);
-        if (a.out_real) {
+        double2 w = make_double2(sre[qq], sim[qq]);
+        if constexpr (out_real) {
             if (a.scale_out) {
-                v.x /= csc[0];  // exact: powers of two
-                v.y /= csc[1];
+                w.x /= csc[0];  // exact: powers of two
+                w.y /= csc[1];
             }
-            a.y0[off] = v.x;
-            if (a.y1) a.y1[off] = v.y;
+            a.y0[off] = w.x;
+            if (a.y1) a.y1[off] = w.y;
         } else {
-            a.out_c[off] = v;
+            a.out_c[off] = w;
         }
     }
 }
@@ -455,18 +501,33 @@ struct ie_fft {
 
 namespace ie {
 
-static int line_launch(const LineArgs& a, cudaStream_t st) {
-    const int G = kFftPoints / a.L;
-    const int ctas = (a.nlines + G - 1) / G;
-    const size_t smem = 2 * (size_t)kSmemStride * sizeof(double);
+template <int MODE>
+static int launch_mode(const LineArgs& a, int ctas, size_t smem, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        IE_CUDA(cudaFuncSetAttribute(k_fft_lines, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        IE_CUDA(cudaFuncSetAttribute(k_fft_lines<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
-    k_fft_lines<<<ctas, kFftThreads, smem, st>>>(a);
+    k_fft_lines<MODE><<<ctas, kFftThreads, smem, st>>>(a);
     IE_LAUNCHED();
     return IE_OK;
+}
+
+static int line_launch(const LineArgs& a_in, cudaStream_t st) {
+    LineArgs a = a_in;
+    a.lg_ninner = 0;
+    while ((1 << a.lg_ninner) < a.ninner) ++a.lg_ninner;
+    if ((1 << a.lg_ninner) != a.ninner) {
+        set_error("fft: line layout must be a power of two");
+        return IE_ERR_ARG;
+    }
+    const int G = kFftPoints / a.L;
+    const int ctas = (a.nlines + G - 1) / G;
+    const size_t smem = 2 * (size_t)kSmemStride * sizeof(double) + (size_t)(kFftPoints / 4) * sizeof(double2);
+    if (a.fused) return a.in_real ? launch_mode<kFusedRR>(a, ctas, smem, st) : launch_mode<kFusedCC>(a, ctas, smem, st);
+    if (a.in_real) return launch_mode<kFwdRC>(a, ctas, smem, st);
+    if (a.out_real) return launch_mode<kInvCR>(a, ctas, smem, st);
+    return a.sign < 0 ? launch_mode<kFwdCC>(a, ctas, smem, st) : launch_mode<kInvCC>(a, ctas, smem, st);
 }
 
 static LineArgs base_args(const ie_fft* f) {

@@ -269,34 +269,6 @@ __device__ int sturm_count(const double* a, const double* b, int m, double x) {
     return cnt;
 }
 
-// Extremal eigenvalue of the m x m tridiagonal by 32-way multisection.
-__global__ void k_ritz(const double* a, const double* b, int m, int which, double* out) {
-    const int lane = threadIdx.x;
-    double lo = a[0], hi = a[0];
-    for (int i = 0; i < m; ++i) {
-        const double r = (i > 0 ? fabs(b[i - 1]) : 0.0) + (i < m - 1 ? fabs(b[i]) : 0.0);
-        lo = fmin(lo, a[i] - r);
-        hi = fmax(hi, a[i] + r);
-    }
-    const double span = fmax(hi - lo, 1e-300);
-    lo -= 1e-3 * span + 1e-300;
-    hi += 1e-3 * span + 1e-300;
-    const int target = which == 0 ? 1 : m;  // count(x) >= target  <=>  x > lambda
-    for (int it = 0; it < 64; ++it) {
-        const double x = lo + (hi - lo) * (double)(lane + 1) / 33.0;
-        const bool above = sturm_count(a, b, m, x) >= target;
-        const unsigned mask = __ballot_sync(0xffffffffu, above);
-        const int first = mask ? __ffs(mask) - 1 : 32;  // first lane above the eigenvalue
-        const double nlo = first == 0 ? lo : lo + (hi - lo) * (double)first / 33.0;
-        const double nhi = first == 32 ? hi : lo + (hi - lo) * (double)(first + 1) / 33.0;
-        if (!(nhi < hi) && !(nlo > lo)) break;  // no progress: interval at rounding level
-        lo = nlo;
-        hi = nhi;
-        if (hi - lo <= 2.0 * 2.220446049250313e-16 * fmax(fabs(lo), fabs(hi))) break;
-    }
-    if (lane == 0) *out = 0.5 * (lo + hi);
-}
-
 template <typename T>
 struct DevBuf {
     T* p = nullptr;
@@ -523,6 +495,169 @@ extern "C" int ie_pcg_f64(const ie_matvec* A, const ie_precond* T, const double*
     return IE_OK;
 }
 
+// ---------------------------------------------------------------- K5 --
+// Lanczos state on the device (spectrum.py:154-189): every step kernel
+// returns at once when `stop` is set, the host reads the state every 8 steps.
+struct LzState {
+    double beta, est, cur, nrm;
+    int have_est, stable, stop, status;  // status 1 converged, 2 beta^2 <= 0, 3 beta < 1e-14
+    long long steps;
+};
+
+__global__ void k_lz_init(const double* part, int nch, LzState* s) {
+    __shared__ double sh[kRed];
+    const double v = reduce_partials(part, nch, sh);
+    if (threadIdx.x == 0) {
+        s->nrm = sqrt(v);
+        s->have_est = 0;
+        s->stable = 0;
+        s->stop = 0;
+        s->status = 0;
+        s->steps = 0;
+        s->est = 0.0;
+    }
+}
+
+__global__ void k_lz_scale(double* V, double* AV, const double* w, const double* aw, const LzState* s, int by_beta,
+                           int N) {
+    if (s->stop) return;
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    const double d = by_beta ? s->beta : s->nrm;
+    V[i] = w[i] / d;
+    AV[i] = aw[i] / d;
+}
+
+__global__ void k_lz_alpha(const double* part, int nch, double* alpha_j, const int* stop) {
+    __shared__ double sh[kRed];
+    if (*stop) return;
+    const double v = reduce_partials(part, nch, sh);
+    if (threadIdx.x == 0) *alpha_j = v;
+}
+
+// beta^2 = w.aw, Ritz value of T_j by 32-way Sturm multisection (warp 0),
+// the reference's stopping rule.
+__global__ void k_lz_control(const double* part, int nch, const double* a, double* b, int m, int which,
+                             double rtol, LzState* s) {
+    __shared__ double sh[kRed];
+    __shared__ double bounds[2];
+    if (s->stop) return;
+    const double beta2 = reduce_partials(part, nch, sh);
+    if (!(beta2 > 0.0) || !isfinite(beta2)) {
+        if (threadIdx.x == 0) {
+            s->status = 2;
+            s->stop = 1;
+            s->steps = m;
+        }
+        return;
+    }
+    if (threadIdx.x < 32) {
+        const int lane = threadIdx.x;
+        double lo = a[0], hi = a[0];
+        for (int i = lane; i < m; i += 32) {
+            const double r = (i > 0 ? fabs(b[i - 1]) : 0.0) + (i < m - 1 ? fabs(b[i]) : 0.0);
+            lo = fmin(lo, a[i] - r);
+            hi = fmax(hi, a[i] + r);
+        }
+        for (int o = 16; o > 0; o >>= 1) {
+            lo = fmin(lo, __shfl_xor_sync(0xffffffffu, lo, o));
+            hi = fmax(hi, __shfl_xor_sync(0xffffffffu, hi, o));
+        }
+        const double span = fmax(hi - lo, 1e-300);
+        lo -= 1e-3 * span + 1e-300;
+        hi += 1e-3 * span + 1e-300;
+        const int target = which == 0 ? 1 : m;
+        for (int it = 0; it < 64; ++it) {
+            const double x = lo + (hi - lo) * (double)(lane + 1) / 33.0;
+            const bool above = sturm_count(a, b, m, x) >= target;
+            const unsigned mask = __ballot_sync(0xffffffffu, above);
+            const int first = mask ? __ffs(mask) - 1 : 32;
+            const double nlo = first == 0 ? lo : lo + (hi - lo) * (double)first / 33.0;
+            const double nhi = first == 32 ? hi : lo + (hi - lo) * (double)(first + 1) / 33.0;
+            if (!(nhi < hi) && !(nlo > lo)) break;
+            lo = nlo;
+            hi = nhi;
+            if (hi - lo <= 2.0 * 2.220446049250313e-16 * fmax(fabs(lo), fabs(hi))) break;
+        }
+        if (lane == 0) {
+            bounds[0] = lo;
+            bounds[1] = hi;
+        }
+    }
+    __syncthreads();
+    if (threadIdx.x != 0) return;
+    const double cur = 0.5 * (bounds[0] + bounds[1]);
+    const double beta = sqrt(beta2);
+    s->cur = cur;
+    s->steps = m;
+    if (s->have_est && fabs(cur - s->est) <= rtol * fmax(fabs(cur), 1.0)) {
+        if (++s->stable >= 5) {
+            s->status = 1;
+            s->stop = 1;
+            return;
+        }
+    } else {
+        s->stable = 0;
+    }
+    s->est = cur;
+    s->have_est = 1;
+    if (beta < 1e-14) {
+        s->status = 3;
+        s->stop = 1;
+        return;
+    }
+    s->beta = beta;
+    b[m - 1] = beta;
+}
+
+__global__ void k_gemv_t_partials_s(const double* AV, int64_t ld, const double* w, int N, double* part, int nch,
+                                    const int* stop) {
+    __shared__ double sh[kRed];
+    if (*stop) return;
+    const int i = blockIdx.y;
+    const double* v = AV + (int64_t)i * ld;
+    const int base = blockIdx.x * kChunk;
+    double loc = 0.0;
+#pragma unroll
+    for (int e = 0; e < kChunk / kRed; ++e) {
+        const int t = base + e * kRed + threadIdx.x;
+        if (t < N) loc = fma(v[t], w[t], loc);
+    }
+    const double r = block_tree(loc, sh);
+    if (threadIdx.x == 0) part[(int64_t)i * nch + blockIdx.x] = r;
+}
+
+__global__ void k_reduce_rows_s(const double* part, int nch, double* out, const int* stop) {
+    __shared__ double sh[kRed];
+    if (*stop) return;
+    const double v = reduce_partials(part + (int64_t)blockIdx.x * nch, nch, sh);
+    if (threadIdx.x == 0) out[blockIdx.x] = v;
+}
+
+__global__ void k_gemv_sub_s(double* w, const double* V, int64_t ld, int nb, const double* c, int N,
+                             const int* stop) {
+    if (*stop) return;
+    const int t = blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= N) return;
+    double x = w[t];
+    for (int i = 0; i < nb; ++i) x = __dsub_rn(x, __dmul_rn(c[i], V[(int64_t)i * ld + t]));
+    w[t] = x;
+}
+
+__global__ void k_dot_partials_s(const double* x, const double* y, int N, double* part, const int* stop) {
+    __shared__ double sh[kRed];
+    if (*stop) return;
+    const int base = blockIdx.x * kChunk;
+    double loc = 0.0;
+#pragma unroll
+    for (int e = 0; e < kChunk / kRed; ++e) {
+        const int i = base + e * kRed + threadIdx.x;
+        if (i < N) loc = fma(x[i], y[i], loc);
+    }
+    const double t = block_tree(loc, sh);
+    if (threadIdx.x == 0) part[blockIdx.x] = t;
+}
+
 extern "C" int ie_lanczos_f64(const ie_matvec* A, const ie_precond* T, const double* v0, int32_t which,
                               int64_t max_iters, double rtol, double* lambda, int64_t* steps, void* stream) {
     if (!A || !T || !v0 || !lambda || (which != 0 && which != 1) || max_iters < 0) {
@@ -533,7 +668,8 @@ extern "C" int ie_lanczos_f64(const ie_matvec* A, const ie_precond* T, const dou
     const int N = matvec_N(A);
     const int nch = dot_chunks(N);
     const int64_t nb_max = max_iters + 1;
-    DevBuf<double> V(st), AV(st), wb(st), awb(st), part(st), cbuf(st), tri(st), scal(st);
+    DevBuf<double> V(st), AV(st), wb(st), awb(st), part(st), cbuf(st), tri(st);
+    DevBuf<LzState> S(st);
     IE_CUDA(V.alloc((size_t)nb_max * N));
     IE_CUDA(AV.alloc((size_t)nb_max * N));
     IE_CUDA(wb.alloc(N));
@@ -541,98 +677,64 @@ extern "C" int ie_lanczos_f64(const ie_matvec* A, const ie_precond* T, const dou
     IE_CUDA(part.alloc((size_t)std::max<int64_t>(nb_max, 2) * nch));
     IE_CUDA(cbuf.alloc(nb_max + 2));
     IE_CUDA(tri.alloc(2 * (size_t)nb_max + 2));
-    IE_CUDA(scal.alloc(4));
-    double* hsc = nullptr;
-    IE_CUDA(cudaMallocHost(&hsc, 4 * sizeof(double)));
+    IE_CUDA(S.alloc(1));
+    LzState* hs = nullptr;
+    IE_CUDA(cudaMallocHost(&hs, sizeof(LzState)));
     struct HostFree {
-        double* h;
+        LzState* h;
         ~HostFree() { cudaFreeHost(h); }
-    } hf{hsc};
-    double* da = tri.p;            // alphas
-    double* db = tri.p + nb_max;   // betas
-    auto dot = [&](const double* x, const double* y, double* dst) -> int {
-        k_dot_partials<<<nch, kRed, 0, st>>>(x, y, N, 0, part.p);
-        IE_LAUNCHED();
-        k_reduce_rows<<<1, kRed, 0, st>>>(part.p, nch, dst);
-        IE_LAUNCHED();
-        return IE_OK;
-    };
+    } hf{hs};
+    double* da = tri.p;           // alphas
+    double* db = tri.p + nb_max;  // betas
+    const int* stop = &S.p->stop;
     int rc;
     // v = v0; av = A v; nrm = sqrt(v.av); v /= nrm; av /= nrm   (spectrum.py:148-153)
-    IE_CUDA(cudaMemcpyAsync(wb.p, v0, (size_t)N * 8, cudaMemcpyDeviceToDevice, st));
-    if ((rc = matvec_launch(A, wb.p, N, 1, awb.p, N, 0, N, st, nullptr))) return rc;
-    if ((rc = dot(wb.p, awb.p, scal.p))) return rc;
-    IE_CUDA(cudaMemcpyAsync(hsc, scal.p, 8, cudaMemcpyDeviceToHost, st));
-    IE_CUDA(cudaStreamSynchronize(st));
-    const double nrm = sqrt(hsc[0]);
-    k_scale_div<<<g1(N), 256, 0, st>>>(V.p, wb.p, nrm, N);
+    if ((rc = matvec_launch(A, v0, N, 1, awb.p, N, 0, N, st, nullptr))) return rc;
+    k_dot_partials<<<nch, kRed, 0, st>>>(v0, awb.p, N, 0, part.p);
     IE_LAUNCHED();
-    k_scale_div<<<g1(N), 256, 0, st>>>(AV.p, awb.p, nrm, N);
+    k_lz_init<<<1, kRed, 0, st>>>(part.p, nch, S.p);
     IE_LAUNCHED();
-    std::vector<double> alphas, betas;
-    bool have_est = false;
-    double est = 0.0;
-    int stable = 0;
-    int64_t j = 0;
-    int64_t taken = 0;
-    for (j = 0; j < max_iters; ++j) {
-        double* Vj = V.p + (size_t)j * N;
+    k_lz_scale<<<g1(N), 256, 0, st>>>(V.p, AV.p, v0, awb.p, S.p, 0, N);
+    IE_LAUNCHED();
+    const int64_t kBatch = 8;
+    for (int64_t j = 0; j < max_iters; ++j) {
         double* AVj = AV.p + (size_t)j * N;
-        (void)Vj;
-        if ((rc = precond_apply(T, AVj, wb.p, nullptr, st, nullptr))) return rc;
-        if ((rc = dot(wb.p, AVj, da + j))) return rc;
         const int nb = (int)(j + 1);
+        if ((rc = precond_apply(T, AVj, wb.p, nullptr, st, stop))) return rc;
+        k_dot_partials_s<<<nch, kRed, 0, st>>>(wb.p, AVj, N, part.p, stop);
+        IE_LAUNCHED();
+        k_lz_alpha<<<1, kRed, 0, st>>>(part.p, nch, da + j, stop);
+        IE_LAUNCHED();
         for (int pass = 0; pass < 2; ++pass) {  // two-pass A-orthogonalisation (CGS2)
-            dim3 grid(nch, nb);
-            k_gemv_t_partials<<<grid, kRed, 0, st>>>(AV.p, N, nb, wb.p, N, part.p, nch);
+            k_gemv_t_partials_s<<<dim3(nch, nb), kRed, 0, st>>>(AV.p, N, wb.p, N, part.p, nch, stop);
             IE_LAUNCHED();
-            k_reduce_rows<<<nb, kRed, 0, st>>>(part.p, nch, cbuf.p);
+            k_reduce_rows_s<<<nb, kRed, 0, st>>>(part.p, nch, cbuf.p, stop);
             IE_LAUNCHED();
-            k_gemv_sub<<<g1(N), 256, 0, st>>>(wb.p, V.p, N, nb, cbuf.p, N);
+            k_gemv_sub_s<<<g1(N), 256, 0, st>>>(wb.p, V.p, N, nb, cbuf.p, N, stop);
             IE_LAUNCHED();
         }
-        if ((rc = matvec_launch(A, wb.p, N, 1, awb.p, N, 0, N, st, nullptr))) return rc;
-        if ((rc = dot(wb.p, awb.p, scal.p + 1))) return rc;
-        IE_CUDA(cudaMemcpyAsync(hsc, scal.p + 1, 8, cudaMemcpyDeviceToHost, st));
-        double aj = 0.0;
-        IE_CUDA(cudaMemcpyAsync(&aj, da + j, 8, cudaMemcpyDeviceToHost, st));
-        IE_CUDA(cudaStreamSynchronize(st));
-        taken = j + 1;
-        alphas.push_back(aj);
-        const double beta2 = hsc[0];
-        if (!(beta2 > 0.0) || !std::isfinite(beta2)) break;  // spectrum.py:169-170
-        const double beta = sqrt(beta2);
-        k_ritz<<<1, 32, 0, st>>>(da, db, (int)alphas.size(), which, scal.p + 2);
+        if ((rc = matvec_launch(A, wb.p, N, 1, awb.p, N, 0, N, st, stop))) return rc;
+        k_dot_partials_s<<<nch, kRed, 0, st>>>(wb.p, awb.p, N, part.p, stop);
         IE_LAUNCHED();
-        IE_CUDA(cudaMemcpyAsync(hsc + 2, scal.p + 2, 8, cudaMemcpyDeviceToHost, st));
-        IE_CUDA(cudaStreamSynchronize(st));
-        const double cur = hsc[2];
-        if (have_est && fabs(cur - est) <= rtol * fmax(fabs(cur), 1.0)) {  // spectrum.py:174-181
-            if (++stable >= 5) {
-                *lambda = cur;
-                if (steps) *steps = taken;
-                return IE_OK;
-            }
-        } else {
-            stable = 0;
+        k_lz_control<<<1, kRed, 0, st>>>(part.p, nch, da, db, nb, which, rtol, S.p);
+        IE_LAUNCHED();
+        k_lz_scale<<<g1(N), 256, 0, st>>>(V.p + (size_t)(j + 1) * N, AV.p + (size_t)(j + 1) * N, wb.p, awb.p, S.p, 1,
+                                          N);
+        IE_LAUNCHED();
+        if ((j + 1) % kBatch == 0 || j + 1 == max_iters) {
+            IE_CUDA(cudaMemcpyAsync(hs, S.p, sizeof(LzState), cudaMemcpyDeviceToHost, st));
+            IE_CUDA(cudaStreamSynchronize(st));
+            if (hs->stop) break;
         }
-        est = cur;
-        have_est = true;
-        if (beta < 1e-14) break;
-        betas.push_back(beta);
-        IE_CUDA(cudaMemcpyAsync(db + j, &betas.back(), 8, cudaMemcpyHostToDevice, st));
-        k_scale_div<<<g1(N), 256, 0, st>>>(V.p + (size_t)(j + 1) * N, wb.p, beta, N);
-        IE_LAUNCHED();
-        k_scale_div<<<g1(N), 256, 0, st>>>(AV.p + (size_t)(j + 1) * N, awb.p, beta, N);
-        IE_LAUNCHED();
-        IE_CUDA(cudaStreamSynchronize(st));  // betas.back() must stay alive for the copy
     }
-    if (steps) *steps = taken;
-    if (!have_est) {
+    IE_CUDA(cudaMemcpyAsync(hs, S.p, sizeof(LzState), cudaMemcpyDeviceToHost, st));
+    IE_CUDA(cudaStreamSynchronize(st));
+    if (steps) *steps = hs->steps;
+    if (!hs->have_est) {
         set_error("Lanczos produced no Ritz values");
         return IE_ERR_NO_RITZ;
     }
-    *lambda = est;
+    *lambda = hs->status == 1 ? hs->cur : hs->est;
     return IE_OK;
 }
 

@@ -39,3 +39,21 @@ if which == "fft":
         mv.matvec_device(X, Y, nrhs=2)
     torch.cuda.synchronize()
     print("fft driver done")
+if which == "k1c5":
+    op = ie.build_operator(ie.build_grid(2, 1024), lattice="cell")
+    mv = ie.KernelMatvec(op, method="direct")
+    X = torch.from_numpy(np.random.default_rng(0).standard_normal((2, op.n))).cuda()
+    Y = torch.empty_like(X)
+    mv.matvec_device(X, Y, nrhs=2)
+    torch.cuda.synchronize()
+    print("k1c5 driver done")
+if which == "gemm":
+    grid = ie.build_grid(2, 1024)
+    op = ie.build_operator(grid, lattice="cell")
+    pre = ie.from_decomposition(op, ie.build_decomposition(grid, 128, 2, "schwarz"))
+    r = torch.from_numpy(np.random.default_rng(1).standard_normal(op.n)).cuda()
+    z = torch.empty_like(r)
+    for _ in range(3):
+        pre.apply_device(r, z)
+    torch.cuda.synchronize()
+    print("gemm driver done")
