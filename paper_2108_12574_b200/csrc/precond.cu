@@ -22,6 +22,7 @@
 // from 0.0 -- the reference's association order (precond.py:97-99), no
 // atomics.
 #include <math.h>
+#include <stdlib.h>
 
 #include <algorithm>
 #include <string>
@@ -38,6 +39,7 @@ int make_log_table_device(const ie_geom& g, LogEntry** d_tab, int* ntab);
 int dot_chunks(int64_t n);
 
 constexpr int kSmemMaxS = 160;
+constexpr int kChunk = 2048;  // dot-product chunk (same as krylov.cu)
 constexpr int kBuildThreads = 512;
 constexpr unsigned kFull = 0xffffffffu;
 
@@ -290,11 +292,12 @@ __global__ void __launch_bounds__(256) k_apply_packed(ApplyArgs a) {
 // memory, Ainv_c (symmetric: row k = column k) streams through shared memory
 // in 16-row chunks from L2, each thread accumulates an RA x 4 register tile.
 constexpr int kGemmTN = 64;
-constexpr int kGemmKC = 16;
-constexpr int kGemmBStride = kGemmTN + 1;
+constexpr int kGemmKC = 8;
+
 
 struct GemmArgs {
     const double* r;
+    const double* rg;  // r gathered into the staging layout (k_gather)
     double* staging;
     const BlockMeta* meta;
     const int* idx;
@@ -308,49 +311,96 @@ struct GemmArgs {
     const int* stop;
 };
 
+// smem layout: Bs[jj][kGemmBRow] column-major gathered r (row stride s+1 keeps
+// the 16 tx lanes on distinct banks), As[2][kGemmKC][16*RA] double-buffered
+// A chunks (rows beyond s zero-filled once, so the inner loop has no predicates).
+__device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
+
 template <int RA>
-__global__ void __launch_bounds__(256) k_apply_gemm(GemmArgs a) {
+__global__ void __launch_bounds__(256, 2) k_apply_gemm(GemmArgs a) {
     extern __shared__ double sg[];
     if (a.stop && *a.stop) return;
+    constexpr int AP = 16 * RA;  // padded A row length
     const int tile = blockIdx.x;
     const int c = a.tile_cls[tile], first = a.tile_first[tile], cnt = a.tile_cnt[tile];
     const int s = a.cls_s[c];
+    const int bst = s + 1;
     const double* A = a.full + a.full_off[c];
-    double* Bs = sg;                        // [s][kGemmBStride]
-    double* As = sg + s * kGemmBStride;     // [kGemmKC][s]
+    double* Bs = sg;                                  // [64][s+1]
+    double* As = sg + ((kGemmTN * bst + 1) & ~1);     // [2][KC][AP]
     const int tid = threadIdx.x, ty = tid >> 4, tx = tid & 15;
-    // gather the r columns: consecutive threads walk one block's points
+    auto load_chunk = [&](int buf, int k0) {
+        double* dst = As + buf * kGemmKC * AP;
+        const int kc = min(kGemmKC, s - k0);
+        for (int e = tid; e < kc * s; e += 256) {
+            const int kk = e / s, i = e - kk * s;
+            cp_async8(dst + kk * AP + i, A + (int64_t)(k0 + kk) * s + i);
+        }
+        cp_async_commit();
+    };
+    // zero the padding once (rows i >= s of both buffers, and whole k rows >= kc of the last chunk)
+    for (int e = tid; e < 2 * kGemmKC * AP; e += 256) As[e] = 0.0;
+    __syncthreads();
+    load_chunk(0, 0);
+    // B columns: the member blocks' gathered r (contiguous s doubles each)
+    __shared__ int64_t colbase[kGemmTN];
+    if (tid < kGemmTN) colbase[tid] = tid < cnt ? a.meta[a.members[first + tid]].st_off : -1;
+    __syncthreads();
     for (int e = tid; e < s * kGemmTN; e += 256) {
         const int jj = e / s, i = e - jj * s;
-        double v = 0.0;
-        if (jj < cnt) {
-            const BlockMeta& bm = a.meta[a.members[first + jj]];
-            v = __ldg(a.r + a.idx[bm.idx_off + i]);
+        if (colbase[jj] >= 0) {
+            cp_async8(Bs + jj * bst + i, a.rg + colbase[jj] + i);
+        } else {
+            Bs[jj * bst + i] = 0.0;
         }
-        Bs[i * kGemmBStride + jj] = v;
     }
+    cp_async_commit();
     double acc[RA][4];
 #pragma unroll
     for (int x = 0; x < RA; ++x)
 #pragma unroll
         for (int y = 0; y < 4; ++y) acc[x][y] = 0.0;
+    const double* b0 = Bs + tx * bst;
+    int buf = 0;
     for (int k0 = 0; k0 < s; k0 += kGemmKC) {
+        cp_async_wait_all();
+        __syncthreads();
+        if (k0 + kGemmKC < s) load_chunk(buf ^ 1, k0 + kGemmKC);
+        const double* ap = As + buf * kGemmKC * AP + ty;
+        const double* bp = b0 + k0;
         const int kc = min(kGemmKC, s - k0);
-        __syncthreads();
-        for (int e = tid; e < kc * s; e += 256) As[e] = __ldg(A + (int64_t)k0 * s + e);
-        __syncthreads();
-        for (int kk = 0; kk < kc; ++kk) {
-            double bv[4];
+        if (kc == kGemmKC) {
 #pragma unroll
-            for (int y = 0; y < 4; ++y) bv[y] = Bs[(k0 + kk) * kGemmBStride + tx + 16 * y];
+            for (int kk = 0; kk < kGemmKC; ++kk) {
+                double bv[4], av[RA];
 #pragma unroll
-            for (int x = 0; x < RA; ++x) {
-                const int i = ty + 16 * x;
-                const double av = i < s ? As[kk * s + i] : 0.0;
+                for (int y = 0; y < 4; ++y) bv[y] = bp[kk + 16 * y * bst];
 #pragma unroll
-                for (int y = 0; y < 4; ++y) acc[x][y] = fma(av, bv[y], acc[x][y]);
+                for (int x = 0; x < RA; ++x) av[x] = ap[kk * AP + 16 * x];
+#pragma unroll
+                for (int x = 0; x < RA; ++x)
+#pragma unroll
+                    for (int y = 0; y < 4; ++y) acc[x][y] = fma(av[x], bv[y], acc[x][y]);
+            }
+        } else {
+            for (int kk = 0; kk < kc; ++kk) {
+                double bv[4], av[RA];
+#pragma unroll
+                for (int y = 0; y < 4; ++y) bv[y] = bp[kk + 16 * y * bst];
+#pragma unroll
+                for (int x = 0; x < RA; ++x) av[x] = ap[kk * AP + 16 * x];
+#pragma unroll
+                for (int x = 0; x < RA; ++x)
+#pragma unroll
+                    for (int y = 0; y < 4; ++y) acc[x][y] = fma(av[x], bv[y], acc[x][y]);
             }
         }
+        buf ^= 1;
     }
 #pragma unroll
     for (int y = 0; y < 4; ++y) {
@@ -363,6 +413,109 @@ __global__ void __launch_bounds__(256) k_apply_gemm(GemmArgs a) {
             if (i < s) a.staging[st + i] = acc[x][y];
         }
     }
+}
+
+// ---------------------------------------------------------------------------
+// FP64 tensor-core variant of the class GEMM: mma.sync.m8n8k4.f64 (SASS DMMA),
+// 256 FMAs per warp instruction.  CTA = 8 warps = 2 (row halves) x 4 (column
+// quarters); warp tile = MT m8-tiles x 2 n8-tiles.  A chunks of 8 k-rows flow
+// through a 3-stage cp.async ring; padded strides (== 4 mod 16 doubles) make
+// the fragment loads two-wavefront (conflict-free) accesses.
+// Fragment layouts (PTX ISA, m8n8k4 .f64): a0 = A[lane>>2][lane&3],
+// b0 = B[lane&3][lane>>2], c{0,1} = C[lane>>2][2*(lane&3)+{0,1}].
+__device__ __forceinline__ void dmma884(double& c0, double& c1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                 : "+d"(c0), "+d"(c1)
+                 : "d"(a), "d"(b));
+}
+
+constexpr int kDmmaStages = 3;
+
+__host__ __device__ constexpr int pad4mod16(int x) { return x + ((4 - (x & 15)) & 15); }
+
+template <int MT>
+__global__ void __launch_bounds__(256, 2) k_apply_dmma(GemmArgs a) {
+    extern __shared__ double sg[];
+    if (a.stop && *a.stop) return;
+    constexpr int AP = pad4mod16(16 * MT);  // A row stride (k-major rows of length >= 2*8*MT)
+    const int tile = blockIdx.x;
+    const int c = a.tile_cls[tile], first = a.tile_first[tile], cnt = a.tile_cnt[tile];
+    const int s = a.cls_s[c];
+    const int bst = pad4mod16((s + kGemmKC - 1) / kGemmKC * kGemmKC);  // covers every k the chunks touch
+    const double* A = a.full + a.full_off[c];
+    double* Bs = sg;                                // [64][bst] column-major gathered r
+    double* As = sg + kGemmTN * bst;                // [stages][KC][AP]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int rh = warp & 1, cq = warp >> 1;
+    __shared__ int64_t colbase[kGemmTN];
+    if (tid < kGemmTN) colbase[tid] = tid < cnt ? a.meta[a.members[first + tid]].st_off : -1;
+    // zero A ring (padding rows/cols stay zero) and B (k >= s, missing columns)
+    for (int e = tid; e < kDmmaStages * kGemmKC * AP; e += 256) As[e] = 0.0;
+    for (int e = tid; e < kGemmTN * bst; e += 256) Bs[e] = 0.0;
+    __syncthreads();
+    for (int e = tid; e < s * kGemmTN; e += 256) {
+        const int jj = e / s, i = e - jj * s;
+        if (colbase[jj] >= 0) cp_async8(Bs + jj * bst + i, a.rg + colbase[jj] + i);
+    }
+    cp_async_commit();
+    const int nchunks = (s + kGemmKC - 1) / kGemmKC;
+    auto load_chunk = [&](int ch) {
+        if (ch < nchunks) {
+            double* dst = As + (ch % kDmmaStages) * kGemmKC * AP;
+            const int k0 = ch * kGemmKC;
+            const int kc = min(kGemmKC, s - k0);
+            for (int e = tid; e < kc * s; e += 256) {
+                const int kk = e / s, i = e - kk * s;
+                cp_async8(dst + kk * AP + i, A + (int64_t)(k0 + kk) * s + i);
+            }
+        }
+        cp_async_commit();  // always commit (possibly empty) so group counting stays uniform
+    };
+    for (int ch = 0; ch < kDmmaStages - 1; ++ch) load_chunk(ch);
+    double acc[MT][2][2];
+#pragma unroll
+    for (int m = 0; m < MT; ++m)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) acc[m][nt][0] = acc[m][nt][1] = 0.0;
+    const int arow = rh * 8 * MT + (lane >> 2);  // + 8 m
+    const int kq = lane & 3;
+    const double* bcol0 = Bs + (cq * 16 + (lane >> 2)) * bst + kq;
+    const double* bcol1 = bcol0 + 8 * bst;
+    for (int ch = 0; ch < nchunks; ++ch) {
+        // wait until chunk ch (and the B gather) has landed
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(kDmmaStages - 2));
+        __syncthreads();
+        load_chunk(ch + kDmmaStages - 1);
+        // slot of chunk ch - 1 is overwritten only after the barrier above
+        const double* ac = As + (ch % kDmmaStages) * kGemmKC * AP;
+#pragma unroll
+        for (int ks = 0; ks < kGemmKC / 4; ++ks) {
+            const int kg = ch * kGemmKC + ks * 4;
+            const double b0 = bcol0[kg];
+            const double b1 = bcol1[kg];
+            const double* ap = ac + (ks * 4 + kq) * AP + arow;
+#pragma unroll
+            for (int m = 0; m < MT; ++m) {
+                const double av = ap[8 * m];
+                dmma884(acc[m][0][0], acc[m][0][1], av, b0);
+                dmma884(acc[m][1][0], acc[m][1][1], av, b1);
+            }
+        }
+    }
+    // store: C[row][col] with row = rh*8*MT + 8m + (lane>>2), col = cq*16 + 8nt + 2*(lane&3) + i
+#pragma unroll
+    for (int nt = 0; nt < 2; ++nt)
+#pragma unroll
+        for (int i2 = 0; i2 < 2; ++i2) {
+            const int jj = cq * 16 + 8 * nt + 2 * (lane & 3) + i2;
+            if (jj >= cnt) continue;
+            const int64_t st = colbase[jj];
+#pragma unroll
+            for (int m = 0; m < MT; ++m) {
+                const int row = rh * 8 * MT + 8 * m + (lane >> 2);
+                if (row < s) a.staging[st + row] = acc[m][nt][i2];
+            }
+        }
 }
 
 // packed upper triangle by columns -> full symmetric row-major
@@ -477,9 +630,52 @@ __global__ void __launch_bounds__(128) k_apply_subst(ApplyArgs a) {
     }
 }
 
+// rg[e] = r[idx[e]] over the concatenated block index lists (staging layout)
+__global__ void k_gather(const double* r, const int* idx, double* rg, int64_t total, const int* stop) {
+    if (stop && *stop) return;
+    const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (e < total) rg[e] = __ldg(r + idx[e]);
+}
+
+// Per point: z_i = sum of its <= MM staged contributions in ascending block id
+// (fixed-width position table, -1 padded: one dependent load level less than CSR).
+template <int MM>
+__global__ void __launch_bounds__(256) k_scatter_fixed(const double* staging, const int* pos, double* z, int N,
+                                                       const double* r, double* partials, const int* stop) {
+    if (stop && *stop) return;
+    __shared__ double sh[256];
+    const int base = blockIdx.x * kChunk;
+    double loc = 0.0;
+#pragma unroll 2
+    for (int e = 0; e < kChunk / 256; ++e) {
+        const int i = base + e * 256 + threadIdx.x;
+        if (i < N) {
+            int pp[MM];
+#pragma unroll
+            for (int q = 0; q < MM; ++q) pp[q] = pos[(int64_t)q * N + i];
+            double v[MM];
+#pragma unroll
+            for (int q = 0; q < MM; ++q) v[q] = pp[q] >= 0 ? staging[pp[q]] : 0.0;
+            double acc = 0.0;
+#pragma unroll
+            for (int q = 0; q < MM; ++q)
+                if (pp[q] >= 0) acc += v[q];
+            z[i] = acc;
+            if (r) loc = fma(r[i], acc, loc);
+        }
+    }
+    if (!r) return;
+    sh[threadIdx.x] = loc;
+    __syncthreads();
+    for (int o = 128; o > 0; o >>= 1) {
+        if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) partials[blockIdx.x] = sh[0];
+}
+
 // Per point: z_i = sum of its staged contributions in ascending block id.
 // Optionally also the fixed-chunk partials of r.z (for PCG's rho).
-constexpr int kChunk = 2048;
 __global__ void __launch_bounds__(256) k_scatter(const double* staging, const int* ptr, const int* pos, double* z,
                                                  int N, const double* r, double* partials, const int* stop) {
     if (stop && *stop) return;
@@ -536,6 +732,10 @@ struct ie_precond {
     int* d_cls_s;
     int* d_tiles;  // [3][ntiles]: class, first member, count
     int* d_members;
+    double* d_rg;  // r gathered into the staging layout (GEMM path)
+    int use_dmma;  // FP64 tensor-core (mma.sync m8n8k4) class GEMM
+    int mm;        // fixed-width scatter table width (power of two <= 8), 0: CSR
+    int* d_posfix; // [mm][N] staged positions, -1 padded
 };
 
 namespace ie {
@@ -562,9 +762,37 @@ static void launch_apply_T(const ie_precond* p, ApplyArgs a, cudaStream_t st) {
     }
 }
 
+static int scatter_launch(const ie_precond* p, const double* r, double* z, double* partials, cudaStream_t st,
+                          const int* stop) {
+    const int nch = (p->N + kChunk - 1) / kChunk;
+    const double* rr = partials ? r : nullptr;
+    switch (p->mm) {
+        case 1: k_scatter_fixed<1><<<nch, 256, 0, st>>>(p->d_staging, p->d_posfix, z, p->N, rr, partials, stop); break;
+        case 2: k_scatter_fixed<2><<<nch, 256, 0, st>>>(p->d_staging, p->d_posfix, z, p->N, rr, partials, stop); break;
+        case 4: k_scatter_fixed<4><<<nch, 256, 0, st>>>(p->d_staging, p->d_posfix, z, p->N, rr, partials, stop); break;
+        case 8: k_scatter_fixed<8><<<nch, 256, 0, st>>>(p->d_staging, p->d_posfix, z, p->N, rr, partials, stop); break;
+        default: k_scatter<<<nch, 256, 0, st>>>(p->d_staging, p->d_ptr, p->d_pos, z, p->N, rr, partials, stop);
+    }
+    IE_LAUNCHED();
+    return IE_OK;
+}
+
+template <int MT>
+static void launch_dmma(const ie_precond* p, const GemmArgs& g, cudaStream_t st) {
+    constexpr int AP = pad4mod16(16 * MT);
+    const int bst = pad4mod16((kSmemMaxS + kGemmKC - 1) / kGemmKC * kGemmKC);
+    const size_t sm = ((size_t)kGemmTN * bst + (size_t)kDmmaStages * kGemmKC * AP) * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_apply_dmma<MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        attr = true;
+    }
+    k_apply_dmma<MT><<<p->ntiles, 256, sm, st>>>(g);
+}
+
 template <int RA>
 static void launch_gemm(const ie_precond* p, const GemmArgs& g, cudaStream_t st) {
-    const size_t sm = ((size_t)kSmemMaxS * kGemmBStride + (size_t)kGemmKC * kSmemMaxS) * sizeof(double);
+    const size_t sm = ((size_t)kGemmTN * (kSmemMaxS + 1) + 2 + 2 * (size_t)kGemmKC * 16 * RA) * sizeof(double);
     static bool attr = false;
     if (!attr) {
         cudaFuncSetAttribute(k_apply_gemm<RA>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -576,8 +804,11 @@ static void launch_gemm(const ie_precond* p, const GemmArgs& g, cudaStream_t st)
 int precond_apply(const ie_precond* p, const double* r, double* z, double* partials, cudaStream_t st,
                   const int* stop) {
     if (p->gemm_ra) {
+        k_gather<<<(unsigned)((p->total_s + 255) / 256), 256, 0, st>>>(r, p->d_idx, p->d_rg, p->total_s, stop);
+        IE_LAUNCHED();
         GemmArgs g;
         g.r = r;
+        g.rg = p->d_rg;
         g.staging = p->d_staging;
         g.meta = p->d_meta;
         g.idx = p->d_idx;
@@ -589,6 +820,22 @@ int precond_apply(const ie_precond* p, const double* r, double* z, double* parti
         g.tile_cnt = p->d_tiles + 2 * p->ntiles;
         g.members = p->d_members;
         g.stop = stop;
+        if (p->use_dmma) {
+            switch ((((p->smax + 7) / 8) + 1) / 2) {
+                case 1: launch_dmma<1>(p, g, st); break;
+                case 2: launch_dmma<2>(p, g, st); break;
+                case 3: launch_dmma<3>(p, g, st); break;
+                case 4: launch_dmma<4>(p, g, st); break;
+                case 5: launch_dmma<5>(p, g, st); break;
+                case 6: launch_dmma<6>(p, g, st); break;
+                case 7: launch_dmma<7>(p, g, st); break;
+                case 8: launch_dmma<8>(p, g, st); break;
+                case 9: launch_dmma<9>(p, g, st); break;
+                default: launch_dmma<10>(p, g, st); break;
+            }
+            IE_LAUNCHED();
+            return scatter_launch(p, r, z, partials, st, stop);
+        }
         switch (p->gemm_ra) {
             case 1: launch_gemm<1>(p, g, st); break;
             case 2: launch_gemm<2>(p, g, st); break;
@@ -602,11 +849,7 @@ int precond_apply(const ie_precond* p, const double* r, double* z, double* parti
             default: launch_gemm<10>(p, g, st); break;
         }
         IE_LAUNCHED();
-        const int nch3 = (p->N + kChunk - 1) / kChunk;
-        k_scatter<<<nch3, 256, 0, st>>>(p->d_staging, p->d_ptr, p->d_pos, z, p->N, partials ? r : nullptr, partials,
-                                        stop);
-        IE_LAUNCHED();
-        return IE_OK;
+        return scatter_launch(p, r, z, partials, st, stop);
     }
     ApplyArgs a;
     a.stop = stop;
@@ -623,11 +866,7 @@ int precond_apply(const ie_precond* p, const double* r, double* z, double* parti
         if (sm > 48 * 1024) cudaFuncSetAttribute(k_apply_large, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         k_apply_large<<<(unsigned)p->D, 256, sm, st>>>(a);
         IE_LAUNCHED();
-        const int nch2 = (p->N + kChunk - 1) / kChunk;
-        k_scatter<<<nch2, 256, 0, st>>>(p->d_staging, p->d_ptr, p->d_pos, z, p->N, partials ? r : nullptr, partials,
-                                         stop);
-        IE_LAUNCHED();
-        return IE_OK;
+        return scatter_launch(p, r, z, partials, st, stop);
     }
     switch (p->T) {
         case 1: launch_apply_T<1>(p, a, st); break;
@@ -641,11 +880,7 @@ int precond_apply(const ie_precond* p, const double* r, double* z, double* parti
         default: set_error("apply: unsupported block size"); return IE_ERR_ARG;
     }
     IE_LAUNCHED();
-    const int nch = (p->N + kChunk - 1) / kChunk;
-    k_scatter<<<nch, 256, 0, st>>>(p->d_staging, p->d_ptr, p->d_pos, z, p->N, partials ? r : nullptr, partials,
-                                   stop);
-    IE_LAUNCHED();
-    return IE_OK;
+    return scatter_launch(p, r, z, partials, st, stop);
 }
 
 }  // namespace ie
@@ -663,6 +898,8 @@ extern "C" void ie_precond_destroy(ie_precond* p) {
     cudaFree(p->d_cls_s);
     cudaFree(p->d_tiles);
     cudaFree(p->d_members);
+    cudaFree(p->d_rg);
+    cudaFree(p->d_posfix);
     delete p;
 }
 
@@ -807,6 +1044,17 @@ extern "C" int ie_precond_create(const ie_geom* g, const int64_t* h_offsets, con
         for (int64_t q = 0; q < total; ++q) pos[fill[allidx[q]]++] = (int)q;  // ascending block id
     }
 
+    int mmax = 0;
+    for (int64_t i = 0; i < N; ++i) mmax = std::max(mmax, cnt[i + 1] - cnt[i]);
+    int mm = 0;
+    std::vector<int> posfix;
+    if (mmax <= 8) {
+        mm = 1;
+        while (mm < mmax) mm *= 2;
+        posfix.assign((size_t)mm * N, -1);
+        for (int64_t i = 0; i < N; ++i)
+            for (int q = cnt[i]; q < cnt[i + 1]; ++q) posfix[(size_t)(q - cnt[i]) * N + i] = pos[q];
+    }
     ie_precond* p = new ie_precond();
     p->g = *g;
     p->N = (int)N;
@@ -836,6 +1084,11 @@ extern "C" int ie_precond_create(const ie_geom* g, const int64_t* h_offsets, con
     IE_CHECK_BUILD(cudaMemcpyAsync(p->d_idx, allidx.data(), total * sizeof(int), cudaMemcpyHostToDevice, st));
     IE_CHECK_BUILD(cudaMemcpyAsync(p->d_ptr, cnt.data(), (N + 1) * sizeof(int), cudaMemcpyHostToDevice, st));
     IE_CHECK_BUILD(cudaMemcpyAsync(p->d_pos, pos.data(), total * sizeof(int), cudaMemcpyHostToDevice, st));
+    p->mm = mm;
+    if (mm) {
+        IE_CHECK_BUILD(cudaMalloc(&p->d_posfix, posfix.size() * sizeof(int)));
+        IE_CHECK_BUILD(cudaMemcpyAsync(p->d_posfix, posfix.data(), posfix.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+    }
 
     // --- factorise the representatives
     int *d_uidx, *d_usz, *d_info;
@@ -938,6 +1191,7 @@ extern "C" int ie_precond_create(const ie_geom* g, const int64_t* h_offsets, con
         if (e == cudaSuccess) e = cudaMalloc(&p->d_cls_s, U * sizeof(int));
         if (e == cudaSuccess) e = cudaMalloc(&p->d_tiles, tiles.size() * sizeof(int));
         if (e == cudaSuccess) e = cudaMalloc(&p->d_members, members.size() * sizeof(int));
+        if (e == cudaSuccess) e = cudaMalloc(&p->d_rg, total * sizeof(double));
         int64_t* d_fofs2 = nullptr;
         if (e == cudaSuccess) e = cudaMalloc(&d_fofs2, U * sizeof(int64_t));
         if (e == cudaSuccess) e = cudaMemcpyAsync(p->d_full_off, full_off.data(), U * sizeof(int64_t), cudaMemcpyHostToDevice, st);
@@ -958,6 +1212,8 @@ extern "C" int ie_precond_create(const ie_geom* g, const int64_t* h_offsets, con
             return IE_ERR_CUDA;
         }
         p->gemm_ra = (smax + 15) / 16;
+        const char* env = getenv("IEDD_B200_APPLY_GEMM");
+        p->use_dmma = !(env && std::string(env) == "dfma");
     }
     *out = p;
     return IE_OK;
