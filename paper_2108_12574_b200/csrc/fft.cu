@@ -250,8 +250,11 @@ __device__ __forceinline__ double2 twiddle(const double2* qt, int m, int logL) {
     }
 }
 
+// Twiddles of the Ns = 16 pass, radix-major: t16[r * 16 + k] = exp(-2 pi i r k / (16 R)).
+// (Through the quarter-wave table, the 16 k-lanes of that pass would hit one bank.)
 template <int R, int S>
-__device__ __forceinline__ void stockham(double* sre, double* sim, int logL, int logNs, const double2* qt) {
+__device__ __forceinline__ void stockham(double* sre, double* sim, int logL, int logNs, const double2* qt,
+                                         const double2* t16) {
     constexpr int NB = kFftPoints / (R * kFftThreads);
     constexpr int LR = R == 16 ? 4 : (R == 8 ? 3 : (R == 4 ? 2 : 1));
     const int lpl = logL - LR;  // log2(L / R)
@@ -274,7 +277,7 @@ __device__ __forceinline__ void stockham(double* sre, double* sim, int logL, int
             const int tstep = k << (logL - logNs - LR);
 #pragma unroll
             for (int r = 1; r < R; ++r) {
-                const double2 t = twiddle(qt, r * tstep, logL);
+                const double2 t = logNs == 4 ? t16[r * 16 + k] : twiddle(qt, r * tstep, logL);
                 const double ti = S < 0 ? t.y : -t.y;
                 const double xr = vr[b][r];
                 vr[b][r] = fma(xr, t.x, -vi[b][r] * ti);
@@ -298,17 +301,17 @@ __device__ __forceinline__ void stockham(double* sre, double* sim, int logL, int
 
 // Full FFT of every line in shared memory: radix-16 passes, then one of 2/4/8.
 template <int S>
-__device__ void fft_smem(double* sre, double* sim, int logL, const double2* qt) {
+__device__ void fft_smem(double* sre, double* sim, int logL, const double2* qt, const double2* t16) {
     int logNs = 0;
     int rem = logL;
     while (rem >= 4) {
-        stockham<16, S>(sre, sim, logL, logNs, qt);
+        stockham<16, S>(sre, sim, logL, logNs, qt, t16);
         logNs += 4;
         rem -= 4;
     }
-    if (rem == 3) stockham<8, S>(sre, sim, logL, logNs, qt);
-    if (rem == 2) stockham<4, S>(sre, sim, logL, logNs, qt);
-    if (rem == 1) stockham<2, S>(sre, sim, logL, logNs, qt);
+    if (rem == 3) stockham<8, S>(sre, sim, logL, logNs, qt, t16);
+    if (rem == 2) stockham<4, S>(sre, sim, logL, logNs, qt, t16);
+    if (rem == 1) stockham<2, S>(sre, sim, logL, logNs, qt, t16);
 }
 
 // Pass modes: what a line transform reads, does and writes.
@@ -323,6 +326,7 @@ __global__ void __launch_bounds__(kFftThreads, 2) k_fft_lines(LineArgs a) {
     double* sre = smd;
     double* sim = smd + kSmemStride;
     double2* qt = reinterpret_cast<double2*>(smd + 2 * kSmemStride);  // quarter-wave twiddles
+    double2* t16 = qt + (kFftPoints / 4);                              // Ns = 16 pass twiddles
     if (a.stop && *a.stop) return;
     __shared__ double csc[2];
     const int L = a.L;
@@ -330,6 +334,14 @@ __global__ void __launch_bounds__(kFftThreads, 2) k_fft_lines(LineArgs a) {
     for (int r = threadIdx.x; r < (L >> 2); r += kFftThreads) {
         const double2 t = __ldg(a.tw + r);  // exp(-2 pi i r / L) = (cos, -sin)
         qt[r] = make_double2(t.x, -t.y);
+    }
+    if (logL > 4) {
+        // radix of the Ns = 16 pass: 16 if logL >= 8, else 2^(logL-4)
+        const int lr2 = logL >= 8 ? 4 : logL - 4;
+        for (int e = threadIdx.x; e < (16 << lr2); e += kFftThreads) {
+            const int r = e >> 4, k = e & 15;
+            t16[e] = __ldg(a.tw + ((r * k) << (logL - 4 - lr2)));
+        }
     }
     if ((in_real && a.scale_in) || (out_real && a.scale_out)) column_scales(a, csc);
     __syncthreads();
@@ -387,7 +399,7 @@ __global__ void __launch_bounds__(kFftThreads, 2) k_fft_lines(LineArgs a) {
     }
     __syncthreads();
     if constexpr (fused) {
-        fft_smem<-1>(sre, sim, logL, qt);
+        fft_smem<-1>(sre, sim, logL, qt, t16);
         // multiply by the folded real symbol; line (inner index i) enumerates axes 1..dim-1
         const int np1 = a.n + 1;
         int s0 = 1;
@@ -411,11 +423,11 @@ __global__ void __launch_bounds__(kFftThreads, 2) k_fft_lines(LineArgs a) {
             sim[qi] *= lam;
         }
         __syncthreads();
-        fft_smem<+1>(sre, sim, logL, qt);
+        fft_smem<+1>(sre, sim, logL, qt, t16);
     } else if constexpr (MODE == kFwdCC || MODE == kFwdRC) {
-        fft_smem<-1>(sre, sim, logL, qt);
+        fft_smem<-1>(sre, sim, logL, qt, t16);
     } else {
-        fft_smem<+1>(sre, sim, logL, qt);
+        fft_smem<+1>(sre, sim, logL, qt, t16);
     }
     const bool contig_out = out_real || a.out_sl == 1;
 #pragma unroll 4
@@ -523,7 +535,7 @@ static int line_launch(const LineArgs& a_in, cudaStream_t st) {
     }
     const int G = kFftPoints / a.L;
     const int ctas = (a.nlines + G - 1) / G;
-    const size_t smem = 2 * (size_t)kSmemStride * sizeof(double) + (size_t)(kFftPoints / 4) * sizeof(double2);
+    const size_t smem = 2 * (size_t)kSmemStride * sizeof(double) + (size_t)(kFftPoints / 4 + 256) * sizeof(double2);
     if (a.fused) return a.in_real ? launch_mode<kFusedRR>(a, ctas, smem, st) : launch_mode<kFusedCC>(a, ctas, smem, st);
     if (a.in_real) return launch_mode<kFwdRC>(a, ctas, smem, st);
     if (a.out_real) return launch_mode<kInvCR>(a, ctas, smem, st);
