@@ -644,16 +644,17 @@ void fft_destroy(ie_fft* f) {
 
 // Y0 (+ i Y1) = A (X0 + i X1) over all N rows.
 int fft_matvec(const ie_fft* f, const double* X0, const double* X1, double* Y0, double* Y1, cudaStream_t st,
-               const int* stop) {
+               const int* stop, const double* amax_ext) {
     const int n = f->n, M = f->M, d = f->dim;
     int rc;
     const int two = X1 != nullptr;
-    if (two) {
+    if (two && !amax_ext) {
         k_absmax2<<<(f->N + 2047) / 2048, 256, 0, st>>>(X0, X1, f->N, f->d_amax, stop);
         IE_LAUNCHED();
     }
     auto line_launch = [&](LineArgs a, cudaStream_t s) -> int {
         a.stop = stop;
+        if (amax_ext) a.amax = amax_ext;
         if (two) {
             a.scale_in = a.in_real;
             a.scale_out = a.out_real;

@@ -28,7 +28,8 @@ struct ie_precond;
 namespace ie {
 
 int matvec_launch(const ie_matvec* m, const double* X, int64_t ldx, int nrhs, double* Y, int64_t ldy,
-                  int64_t row_begin, int64_t row_end, cudaStream_t st, const int* stop);
+                  int64_t row_begin, int64_t row_end, cudaStream_t st, const int* stop,
+                  const double* amax = nullptr);
 int precond_apply(const ie_precond* p, const double* r, double* z, double* partials, cudaStream_t st,
                   const int* stop);
 int matvec_N(const ie_matvec* m);
@@ -79,7 +80,8 @@ __device__ double reduce_partials(const double* part, int nch, double* sh) {
 // once `stop` is set, so the host can enqueue iterations ahead and read the
 // status once per batch (pcg.py's control flow runs in k_control_a).
 struct PcgState {
-    double rho, alpha, beta, denom, nf, tol, fail_value, pad;
+    double rho[2];  // rho_j = r_j . z_j in slot j & 1 (read and written by different launches)
+    double alpha, beta, denom, nf, tol, fail_value;
     long long max_iters, n_it, fail_iter;
     int status;  // 0 running, 1 converged, 2 stagnated, 3 max_iters, 4 breakdown, 5 non-finite
     int stop;
@@ -87,6 +89,7 @@ struct PcgState {
 
 __global__ void k_pcg_init(const double* part, int nch, PcgState* s, double tol, long long max_iters,
                            double* hist) {
+    // (rho_0 is set by k_pcg_rho0 after the first apply)
     __shared__ double sh[kRed];
     const double v = reduce_partials(part, nch, sh);
     if (threadIdx.x == 0) {
@@ -105,6 +108,118 @@ __global__ void k_pcg_init(const double* part, int nch, PcgState* s, double tol,
             s->stop = 1;
         }
     }
+}
+
+// Fused control + update kernels (one CTA per 2048-element chunk).  Every
+// CTA reduces the same fixed-chunk partials in the same order, so all CTAs
+// take the same decision; CTA 0 records it in the state.
+__device__ __forceinline__ double chunk_absmax(double v, double* sh) {
+    sh[threadIdx.x] = v;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) sh[threadIdx.x] = fmax(sh[threadIdx.x], sh[threadIdx.x + o]);
+        __syncthreads();
+    }
+    return sh[0];
+}
+
+// After the A-pass of iteration `it`: residual / stagnation check of
+// iteration it-1 (pcg.py:107-119), breakdown test of iteration it
+// (pcg.py:99-103), alpha, then u += alpha p, r -= alpha q and max|u| per chunk.
+__global__ void __launch_bounds__(kRed) k_iter_a(const double* part_pq, const double* part_res, int nch, int do_p,
+                                                 int pending, long long it, PcgState* s, double* hist, double* u,
+                                                 double* r, const double* p, const double* q, int N, double* amax) {
+    __shared__ double sh[kRed];
+    __shared__ int decided;
+    if (s->stop) return;
+    double denom = 0.0, res2 = 0.0;
+    if (do_p) denom = reduce_partials(part_pq, nch, sh);
+    __syncthreads();
+    if (pending) res2 = reduce_partials(part_res, nch, sh);
+    if (threadIdx.x == 0) {
+        const long long k = it - 1;
+        int status = 0;
+        double rel = 0.0;
+        if (pending) {
+            rel = sqrt(res2) / s->nf;
+            if (!isfinite(rel)) status = 5;
+            else if (rel <= s->tol) status = 1;
+            else if (k >= 30 && rel > (1.0 - 1e-3) * hist[k - 30]) status = 2;
+            else if (!do_p) status = 3;
+        }
+        if (!status && do_p && (!isfinite(denom) || denom <= 0.0)) status = 4;
+        decided = status;
+        if (blockIdx.x == 0) {
+            if (pending && status != 5) hist[k] = rel;
+            if (status) {
+                s->status = status;
+                s->n_it = k;
+                if (status == 5) {
+                    s->fail_iter = k;
+                    s->fail_value = rel;
+                } else if (status == 4) {
+                    s->fail_iter = it;
+                    s->fail_value = denom;
+                }
+                s->stop = 1;
+            } else if (do_p) {
+                s->denom = denom;
+                s->alpha = s->rho[(it - 1) & 1] / denom;
+            }
+        }
+    }
+    __syncthreads();
+    if (decided || !do_p) return;
+    const double al = s->rho[(it - 1) & 1] / denom;
+    const int base = blockIdx.x * kChunk;
+    double m = 0.0;
+#pragma unroll
+    for (int e = 0; e < kChunk / kRed; ++e) {
+        const int i = base + e * kRed + threadIdx.x;
+        if (i < N) {
+            const double un = __dadd_rn(u[i], __dmul_rn(al, p[i]));
+            u[i] = un;
+            r[i] = __dsub_rn(r[i], __dmul_rn(al, q[i]));
+            m = fmax(m, fabs(un));
+        }
+    }
+    m = chunk_absmax(m, sh);
+    if (threadIdx.x == 0) amax[2 * blockIdx.x + 1] = m;
+}
+
+// After the apply: rho_it = r.z, beta = rho_it / rho_{it-1}, p = z + beta p,
+// max|p| per chunk.
+__global__ void __launch_bounds__(kRed) k_iter_b(const double* part_rz, int nch, long long it, PcgState* s,
+                                                 double* p, const double* z, int N, double* amax) {
+    __shared__ double sh[kRed];
+    if (s->stop) return;
+    const double rz = reduce_partials(part_rz, nch, sh);
+    const double beta = rz / s->rho[(it - 1) & 1];
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        s->beta = beta;
+        s->rho[it & 1] = rz;
+    }
+    const int base = blockIdx.x * kChunk;
+    double m = 0.0;
+#pragma unroll
+    for (int e = 0; e < kChunk / kRed; ++e) {
+        const int i = base + e * kRed + threadIdx.x;
+        if (i < N) {
+            const double pn = __dadd_rn(z[i], __dmul_rn(beta, p[i]));
+            p[i] = pn;
+            m = fmax(m, fabs(pn));
+        }
+    }
+    __syncthreads();
+    m = chunk_absmax(m, sh);
+    if (threadIdx.x == 0) amax[2 * blockIdx.x] = m;
+}
+
+__global__ void k_pcg_rho0(const double* part_rz, int nch, PcgState* s) {
+    __shared__ double sh[kRed];
+    if (s->stop) return;
+    const double rz = reduce_partials(part_rz, nch, sh);
+    if (threadIdx.x == 0) s->rho[0] = rz;
 }
 
 // After the A-pass of iteration `it`: residual check of iteration it-1
@@ -152,7 +267,7 @@ __global__ void k_control_a(const double* part_pq, const double* part_res, int n
             return;
         }
         s->denom = denom;
-        s->alpha = s->rho / denom;
+        s->alpha = s->rho[(it - 1) & 1] / denom;
     }
 }
 
@@ -162,8 +277,8 @@ __global__ void k_control_b(const double* part_rz, int nch, int first, PcgState*
     if (s->stop) return;
     const double rz = reduce_partials(part_rz, nch, sh);
     if (threadIdx.x == 0) {
-        if (!first) s->beta = rz / s->rho;
-        s->rho = rz;
+        if (!first) s->beta = rz / s->rho[0];
+        s->rho[0] = rz;
     }
 }
 
@@ -296,6 +411,7 @@ struct PcgWork {
     int N = 0;
     int64_t cap = 0;
     double *PU = nullptr, *QW = nullptr, *r = nullptr, *z = nullptr, *part = nullptr, *hist = nullptr;
+    double* amax = nullptr;  // per-chunk max|p|, max|u| (2-RHS FFT column scaling)
     PcgState* st = nullptr;
     PcgState* host = nullptr;
     std::vector<cudaEvent_t> ev;
@@ -307,6 +423,7 @@ struct PcgWork {
         cudaFree(z);
         cudaFree(part);
         cudaFree(hist);
+        cudaFree(amax);
         cudaFree(st);
         if (host) cudaFreeHost(host);
         for (auto e : ev) cudaEventDestroy(e);
@@ -336,6 +453,7 @@ static PcgWork* work_acquire(int N, int64_t cap, int* rc) {
     if (e == cudaSuccess) e = cudaMalloc(&w->z, (size_t)N * 8);
     if (e == cudaSuccess) e = cudaMalloc(&w->part, 3 * (size_t)nch * 8);
     if (e == cudaSuccess) e = cudaMalloc(&w->hist, (size_t)cap * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&w->amax, 2 * (size_t)nch * 8);
     if (e == cudaSuccess) e = cudaMalloc(&w->st, sizeof(PcgState));
     if (e == cudaSuccess) e = cudaMallocHost(&w->host, sizeof(PcgState));
     if (e != cudaSuccess) {
@@ -421,7 +539,7 @@ extern "C" int ie_pcg_f64(const ie_matvec* A, const ie_precond* T, const double*
     IE_CUDA(cudaMemcpyAsync(W->r, f, (size_t)N * 8, cudaMemcpyDeviceToDevice, st));
     if ((rc = apply(W->r, W->z, 0))) return rc;
     IE_CUDA(cudaMemcpyAsync(p, W->z, (size_t)N * 8, cudaMemcpyDeviceToDevice, st));
-    k_control_b<<<1, kRed, 0, st>>>(part_rz, nch, 1, W->st);
+    k_pcg_rho0<<<1, kRed, 0, st>>>(part_rz, nch, W->st);
     IE_LAUNCHED();
     // iterations: `it` = the iteration whose A-pass is enqueued; the pass also
     // carries u_{it-1} for the deferred true-residual check of iteration it-1
@@ -430,7 +548,7 @@ extern "C" int ie_pcg_f64(const ie_matvec* A, const ie_precond* T, const double*
         const int do_p = it <= max_iters;
         const int pending = it >= 2;
         if (do_p && pending) {
-            rc = matvec_launch(A, W->PU, N, 2, W->QW, N, 0, N, st, stop);
+            rc = matvec_launch(A, W->PU, N, 2, W->QW, N, 0, N, st, stop, W->amax);
         } else if (do_p) {
             rc = matvec_launch(A, p, N, 1, q, N, 0, N, st, stop);
         } else {
@@ -439,18 +557,13 @@ extern "C" int ie_pcg_f64(const ie_matvec* A, const ie_precond* T, const double*
         if (rc) return rc;
         k_post_pass<<<nch, kRed, 0, st>>>(p, q, f, w, N, do_p, pending, part_pq, part_res, stop);
         IE_LAUNCHED();
-        k_control_a<<<1, kRed, 0, st>>>(part_pq, part_res, nch, do_p, pending, it, W->st, W->hist);
+        k_iter_a<<<nch, kRed, 0, st>>>(part_pq, part_res, nch, do_p, pending, it, W->st, W->hist, uu, W->r, p, q, N,
+                                       W->amax);
         IE_LAUNCHED();
-        if (do_p) {
-            k_update_ur<<<g1(N), 256, 0, st>>>(uu, W->r, p, q, W->st, N);
+        if (do_p && it < max_iters) {  // speculative: z_it is discarded if iteration it is the last
+            if ((rc = apply(W->r, W->z, it))) return rc;
+            k_iter_b<<<nch, kRed, 0, st>>>(part_rz, nch, it, W->st, p, W->z, N, W->amax);
             IE_LAUNCHED();
-            if (it < max_iters) {  // speculative: z_it is discarded if iteration it is the last
-                if ((rc = apply(W->r, W->z, it))) return rc;
-                k_control_b<<<1, kRed, 0, st>>>(part_rz, nch, 0, W->st);
-                IE_LAUNCHED();
-                k_update_p<<<g1(N), 256, 0, st>>>(p, W->z, W->st, N);
-                IE_LAUNCHED();
-            }
         }
         if (it % kBatch == 0 || it == max_iters + 1) {
             IE_CUDA(cudaMemcpyAsync(W->host, W->st, sizeof(PcgState), cudaMemcpyDeviceToHost, st));

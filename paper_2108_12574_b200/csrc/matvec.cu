@@ -219,7 +219,7 @@ namespace ie {
 int fft_create(const ie_geom& g, ie_fft** out);
 void fft_destroy(ie_fft* f);
 int fft_matvec(const ie_fft* f, const double* X0, const double* X1, double* Y0, double* Y1, cudaStream_t st,
-               const int* stop);
+               const int* stop, const double* amax);
 }  // namespace ie
 
 struct ie_matvec {
@@ -302,12 +302,12 @@ static int launch_dim(const ie_matvec* m, MatvecArgs a, cudaStream_t st) {
 }
 
 int matvec_launch(const ie_matvec* m, const double* X, int64_t ldx, int nrhs, double* Y, int64_t ldy,
-                  int64_t row_begin, int64_t row_end, cudaStream_t st, const int* stop) {
+                  int64_t row_begin, int64_t row_end, cudaStream_t st, const int* stop, const double* amax) {
     if (m->method == IE_MATVEC_FFT) {
         const double* X1 = nrhs == 2 ? X + ldx : nullptr;
         if (row_begin == 0 && row_end == m->N)
-            return fft_matvec(m->fft, X, X1, Y, nrhs == 2 ? Y + ldy : nullptr, st, stop);
-        int rc = fft_matvec(m->fft, X, X1, m->d_full, nrhs == 2 ? m->d_full + m->N : nullptr, st, stop);
+            return fft_matvec(m->fft, X, X1, Y, nrhs == 2 ? Y + ldy : nullptr, st, stop, amax);
+        int rc = fft_matvec(m->fft, X, X1, m->d_full, nrhs == 2 ? m->d_full + m->N : nullptr, st, stop, amax);
         if (rc) return rc;
         for (int q = 0; q < nrhs; ++q)
             IE_CUDA(cudaMemcpyAsync(Y + q * ldy, m->d_full + (int64_t)q * m->N + row_begin,
@@ -444,7 +444,7 @@ extern "C" int ie_matvec_f64(const ie_matvec* m, const double* X, int64_t ldx, i
         ie::set_error("ie_matvec_f64: bad arguments");
         return IE_ERR_ARG;
     }
-    return ie::matvec_launch(m, X, ldx, nrhs, Y, ldy, row_begin, row_end, (cudaStream_t)stream, nullptr);
+    return ie::matvec_launch(m, X, ldx, nrhs, Y, ldy, row_begin, row_end, (cudaStream_t)stream, nullptr, nullptr);
 }
 
 extern "C" int ie_assemble_block_f64(const ie_geom* g, const int64_t* rows, int64_t nr, const int64_t* cols,

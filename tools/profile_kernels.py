@@ -57,3 +57,11 @@ if which == "gemm":
         pre.apply_device(r, z)
     torch.cuda.synchronize()
     print("gemm driver done")
+if which == "k1n512":
+    op = ie.build_operator(ie.build_grid(2, 512), lattice="cell")
+    mv = ie.KernelMatvec(op, method="direct")
+    X = torch.from_numpy(np.random.default_rng(0).standard_normal((2, op.n))).cuda()
+    Y = torch.empty_like(X)
+    mv.matvec_device(X, Y, nrhs=2)
+    torch.cuda.synchronize()
+    print("k1n512 done")
