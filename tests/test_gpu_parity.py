@@ -491,3 +491,109 @@ class TestShardedCuda:
             assert torch.equal(torch.cat(ys, dim=1), Yf)
             assert torch.equal(torch.cat(zs), zf)
             assert torch.equal(torch.cat(ps), pf)
+
+
+class TestEdgeCases:
+    def test_not_positive_definite(self, ie):
+        from paper_2108_12574_b200.kernel import KernelOperator
+        grid = ie.build_grid(2, 16)
+        bad = KernelOperator(grid=grid, lattice="cell", diag_value=-1.0)
+        with pytest.raises(ie.NotPositiveDefinite, match="subdomain 0"):
+            ie.from_decomposition(bad, ie.build_decomposition(grid, 4, 1, "schwarz"))
+
+    def test_native_breakdown(self, ie):
+        from paper_2108_12574_b200.kernel import KernelOperator
+        grid = ie.build_grid(2, 8)
+        bad = KernelOperator(grid=grid, lattice="cell", diag_value=-1.0)
+        with pytest.raises(FloatingPointError, match="breakdown at iteration 1"):
+            ie.solve(ie.KernelMatvec(bad), None, np.ones(64), tol=1e-10)
+
+    def test_native_nonfinite_rhs(self, ie):
+        op = ie.build_operator(ie.build_grid(2, 8))
+        f = np.ones(64)
+        f[3] = np.nan
+        with pytest.raises(FloatingPointError):
+            ie.solve(ie.ToeplitzMatvec(op), None, f, tol=1e-10)
+
+    def test_max_iters_zero(self, ie):
+        op = ie.build_operator(ie.build_grid(2, 8))
+        u, rep = ie.solve(ie.ToeplitzMatvec(op), None, np.ones(64), tol=1e-10, max_iters=0)
+        ou, orep = O.pcg(O.FFTMatvec(O.build_operator(O.build_grid(2, 8))), None, np.ones(64), tol=1e-10,
+                         max_iters=0)
+        assert rep.n_it == orep.n_it == 0 and rep.residual_history == orep.residual_history == [1.0]
+        assert not rep.converged and np.all(u == 0)
+
+    def test_non_power_of_two_uses_direct(self, ie, rng):
+        op = ie.build_operator(ie.build_grid(2, 12), lattice="cell")
+        mv = ie.ToeplitzMatvec(op)
+        assert mv.method == "direct"
+        with pytest.raises(ValueError, match="power of two"):
+            ie.KernelMatvec(op, method="fft")
+        x = rng.standard_normal(op.n)
+        ref = O.build_operator(O.build_grid(2, 12), "cell").dense() @ x
+        assert rel(mv.matvec(x), ref) <= 1e-13
+
+    def test_torch_in_torch_out(self, ie):
+        import torch
+        grid = ie.build_grid(2, 32)
+        op = ie.build_operator(grid, lattice="cell")
+        mv = ie.ToeplitzMatvec(op)
+        pre = ie.from_decomposition(op, ie.build_decomposition(grid, 4, 1, "schwarz"))
+        f = torch.from_numpy(np.random.default_rng(0).standard_normal(op.n)).cuda()
+        u, rep = ie.solve(mv, pre, f, tol=1e-10)
+        assert isinstance(u, torch.Tensor) and u.is_cuda
+        u2, rep2 = ie.solve(mv, pre, f.cpu().numpy(), tol=1e-10)
+        assert np.array_equal(u.cpu().numpy(), u2) and rep.residual_history == rep2.residual_history
+
+    def test_apply_dense_matches(self, ie, rng):
+        grid = ie.build_grid(2, 8)
+        op = ie.build_operator(grid)
+        pre = ie.from_decomposition(op, ie.build_decomposition(grid, 2, 1, "schwarz"))
+        tinv = pre.apply_dense()
+        f = rng.standard_normal(op.n)
+        assert np.linalg.norm(tinv @ f - pre.apply(f)) <= 1e-12 * np.linalg.norm(f)
+        assert np.array_equal(tinv, tinv.T)
+
+    def test_two_halves_pairing(self, ie):
+        # goldens "pairing": Jacobi two-halves split, spectrum symmetric about 1
+        grid = ie.build_grid(2, 8)
+        op = ie.build_operator(grid, lattice="cell")
+        pre = ie.from_decomposition(op, ie.two_halves_decomposition(grid), dense_limit=op.n)
+        g = np.linalg.cholesky(pre.apply_dense())
+        w = np.linalg.eigvalsh(g.T @ op.dense() @ g)
+        assert np.max(np.abs(w + w[::-1] - 2.0)) <= 1e-8
+
+
+class TestProperties:
+    """Randomised shapes (seeded): matvec vs dense, apply vs oracle, PCG vs oracle."""
+
+    @pytest.mark.parametrize("seed", range(6))
+    def test_random_configs(self, ie, seed):
+        rng = np.random.default_rng(100 + seed)
+        dim = int(rng.choice([1, 2, 2, 3]))
+        n = int(rng.choice({1: [16, 24, 64], 2: [8, 12, 16, 20], 3: [4, 6, 8]}[dim]))
+        m = int(rng.choice([d for d in (1, 2, 4) if n % d == 0]))
+        w = int(rng.integers(0, 3))
+        kind = str(rng.choice(["jacobi", "schwarz"]))
+        lat = str(rng.choice(["cell", "span"])) if dim == 2 else "cell"
+        grid = ie.build_grid(dim, n)
+        op = ie.build_operator(grid, lattice=lat)
+        og = O.build_grid(dim, n)
+        oop = O.build_operator(og, lat)
+        a = oop.dense()
+        x = rng.standard_normal(op.n)
+        for method in ("direct", "fft"):
+            if method == "fft" and not ie.toeplitz.fft_supported(n):
+                continue
+            assert rel(ie.KernelMatvec(op, method=method).matvec(x), a @ x) <= 1e-12
+        dec = ie.build_decomposition(grid, m, w, kind)
+        opre = O.SchwarzPrecond(oop, O.build_decomposition(og, m, w, kind))
+        for variant in ("packed_inverse", "subst"):
+            pre = ie.from_decomposition(op, dec, variant=variant)
+            assert rel(pre.apply(x), opre.apply(x)) <= 1e-11
+        pre = ie.from_decomposition(op, dec)
+        u, rep = ie.solve(ie.ToeplitzMatvec(op), pre, x, tol=1e-10)
+        ou, orep = O.pcg(lambda v: a @ v, opre, x, tol=1e-10)
+        assert rep.converged == orep.converged and abs(rep.n_it - orep.n_it) <= 2
+        if rep.converged:
+            assert rel(u, ou) <= 1e-9
