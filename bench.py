@@ -143,9 +143,14 @@ def run_ours(args):
 
     ws, rank, local = _dist()
     torch.cuda.set_device(local)
-    if ws > 1:
+    if ws > 1 or os.environ.get("IEDD_FORCE_SHARDED"):
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if not dist.is_initialized():
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            os.environ.setdefault("MASTER_PORT", "29511")
+            os.environ.setdefault("RANK", str(rank))
+            os.environ.setdefault("WORLD_SIZE", str(ws))
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         from paper_2108_12574_b200 import distributed as D
         return D.bench_sharded(args, METRIC, CFG, WORKLOAD)
 
@@ -340,6 +345,12 @@ def main():
         run_reference(args)
     else:
         run_ours(args)
+    try:
+        import torch.distributed as dist
+        if dist.is_available() and dist.is_initialized():
+            dist.destroy_process_group()
+    except Exception:  # pragma: no cover
+        pass
 
 
 if __name__ == "__main__":

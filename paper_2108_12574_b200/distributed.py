@@ -351,12 +351,19 @@ def _stack(cols):
 # bench entry for torchrun (bench.py --gpus N)
 # --------------------------------------------------------------------------
 def bench_sharded(args, metric, cfg, workload):
+    """bench.py --gpus N under torchrun: config 5 on N ranks (bands of rows and
+    subdomains).  Prints the contract JSON line on rank 0; time = max over ranks
+    of the CUDA-event time of exactly `steps` iterations."""
     import json
+    import os
+    import statistics
 
     import torch
     import torch.distributed as dist
 
     import paper_2108_12574_b200 as ie
+
+    from . import _lib
     ws, rank = dist.get_world_size(), dist.get_rank()
     grid = ie.build_grid(cfg["dim"], cfg["n"])
     op = ie.build_operator(grid, lattice="cell")
@@ -369,24 +376,53 @@ def bench_sharded(args, metric, cfg, workload):
     solve_sharded(backend, comm, plan, f_band, tol=1e-10, max_iters=max(args.warmup, 1), gather_solution=False)
     dev = torch.device("cuda", torch.cuda.current_device())
     st = torch.cuda.current_stream()
+    clocks = None
+    if rank == 0:
+        from bench import ClockSampler  # noqa: WPS433 (bench.py is the caller)
+        clocks = ClockSampler(int(os.environ.get("LOCAL_RANK", "0")))
+        clocks.start()
     dist.barrier()
     torch.cuda.synchronize()
+    n0 = _lib.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st)
     _, rep = solve_sharded(backend, comm, plan, f_band, tol=1e-10, max_iters=args.steps, gather_solution=False)
     e1.record(st)
     torch.cuda.synchronize()
     dist.barrier()
+    launches = _lib.launch_count() - n0
     ms = torch.tensor([e0.elapsed_time(e1)], device=dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     ms = float(ms.item())
+    # end to end: host f in (each rank copies its band), gathered host u out
+    e2e = []
+    for _ in range(3):
+        dist.barrier()
+        t0 = torch.cuda.Event(enable_timing=True)
+        t1 = torch.cuda.Event(enable_timing=True)
+        import time as _t
+        w0 = _t.perf_counter()
+        fb = backend.tensor(f[plan.begin: plan.end])
+        u, _ = solve_sharded(backend, comm, plan, fb, tol=1e-10, max_iters=args.steps, gather_solution=True)
+        u.cpu()
+        dt = torch.tensor([_t.perf_counter() - w0], device=dev)
+        dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+        e2e.append(float(dt.item()))
     if rank == 0:
+        clk = clocks.stop()
         out = {"metric": metric, "value": args.steps / (ms * 1e-3), "unit": "iter/s", "n_gpus": ws,
                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                "data": "synthetic (BASELINE.json config 5, seeded)",
-               "config": {"workload": workload, "N": op.n, "parallelism": f"row/subdomain bands x{ws}",
-                          "matvec": backend.method, "bands": list(plan.bounds)},
-               "n_it": rep.n_it}
+               "config": {"workload": workload, "N": op.n, "parallelism": f"row/subdomain bands x{ws} (NCCL)",
+                          "matvec": backend.method, "bands": list(plan.bounds),
+                          "l2": "not flushed"},
+               "n_it": rep.n_it,
+               "e2e": {"value": args.steps / statistics.median(e2e), "unit": "iter/s",
+                       "h2d_bytes_per_step": 8 * plan.size / args.steps,
+                       "d2h_bytes_per_step": 8 * op.n / args.steps,
+                       "note": "per solve of K steps: H2D of each rank's f band, D2H of the gathered u"},
+               "gpu_launches": launches, "clocks": clk,
+               "roofline": {"bound": "n/a", "note": "see the N=1 line for the kernel rooflines"}}
         print(json.dumps(out))
     return None
