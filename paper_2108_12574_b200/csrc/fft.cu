@@ -73,8 +73,9 @@ __device__ __forceinline__ double pow2_scale(double mx) {
     return ldexp(1.0, -e);
 }
 
+template <int TPB>
 __device__ void column_scales(const LineArgs& a, double* sc) {
-    __shared__ double red[2][kFftThreads];
+    __shared__ double red[2][TPB];
     double m0 = 0.0, m1 = 0.0;
     for (int c = threadIdx.x; c < a.namax; c += blockDim.x) {
         m0 = fmax(m0, a.amax[2 * c]);
@@ -252,17 +253,17 @@ __device__ __forceinline__ double2 twiddle(const double2* qt, int m, int logL) {
 
 // Twiddles of the Ns = 16 pass, radix-major: t16[r * 16 + k] = exp(-2 pi i r k / (16 R)).
 // (Through the quarter-wave table, the 16 k-lanes of that pass would hit one bank.)
-template <int R, int S>
+template <int R, int S, int TPB>
 __device__ __forceinline__ void stockham(double* sre, double* sim, int logL, int logNs, const double2* qt,
                                          const double2* t16) {
-    constexpr int NB = kFftPoints / (R * kFftThreads);
+    constexpr int NB = 16 / R;  // 16 points per thread
     constexpr int LR = R == 16 ? 4 : (R == 8 ? 3 : (R == 4 ? 2 : 1));
     const int lpl = logL - LR;  // log2(L / R)
     double vr[NB][R], vi[NB][R];
     int dst[NB];
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
-        const int bf = threadIdx.x + b * kFftThreads;
+        const int bf = threadIdx.x + b * TPB;
         const int g = bf >> lpl;
         const int j = bf & ((1 << lpl) - 1);
         const int k = j & ((1 << logNs) - 1);
@@ -300,61 +301,64 @@ __device__ __forceinline__ void stockham(double* sre, double* sim, int logL, int
 }
 
 // Full FFT of every line in shared memory: radix-16 passes, then one of 2/4/8.
-template <int S>
+template <int S, int TPB>
 __device__ void fft_smem(double* sre, double* sim, int logL, const double2* qt, const double2* t16) {
     int logNs = 0;
     int rem = logL;
     while (rem >= 4) {
-        stockham<16, S>(sre, sim, logL, logNs, qt, t16);
+        stockham<16, S, TPB>(sre, sim, logL, logNs, qt, t16);
         logNs += 4;
         rem -= 4;
     }
-    if (rem == 3) stockham<8, S>(sre, sim, logL, logNs, qt, t16);
-    if (rem == 2) stockham<4, S>(sre, sim, logL, logNs, qt, t16);
-    if (rem == 1) stockham<2, S>(sre, sim, logL, logNs, qt, t16);
+    if (rem == 3) stockham<8, S, TPB>(sre, sim, logL, logNs, qt, t16);
+    if (rem == 2) stockham<4, S, TPB>(sre, sim, logL, logNs, qt, t16);
+    if (rem == 1) stockham<2, S, TPB>(sre, sim, logL, logNs, qt, t16);
 }
 
 // Pass modes: what a line transform reads, does and writes.
 enum FftMode { kFwdCC = 0, kInvCC = 1, kFwdRC = 2, kInvCR = 3, kFusedCC = 4, kFusedRR = 5 };
 
-template <int MODE>
-__global__ void __launch_bounds__(kFftThreads, 2) k_fft_lines(LineArgs a) {
+template <int MODE, int TPB>
+__global__ void __launch_bounds__(TPB, 2) k_fft_lines(LineArgs a) {
+    constexpr int PTS = 16 * TPB;  // points per CTA
+    constexpr int LOGPTS = TPB == 256 ? 12 : 9;
+    constexpr int SSTR = PTS + PTS / 16;
     extern __shared__ __align__(16) double smd[];
     constexpr bool in_real = MODE == kFwdRC || MODE == kFusedRR;
     constexpr bool out_real = MODE == kInvCR || MODE == kFusedRR;
     constexpr bool fused = MODE == kFusedCC || MODE == kFusedRR;
     double* sre = smd;
-    double* sim = smd + kSmemStride;
-    double2* qt = reinterpret_cast<double2*>(smd + 2 * kSmemStride);  // quarter-wave twiddles
-    double2* t16 = qt + (kFftPoints / 4);                              // Ns = 16 pass twiddles
+    double* sim = smd + SSTR;
+    double2* qt = reinterpret_cast<double2*>(smd + 2 * SSTR);  // quarter-wave twiddles
+    double2* t16 = qt + (PTS / 4);                              // Ns = 16 pass twiddles
     if (a.stop && *a.stop) return;
     __shared__ double csc[2];
     const int L = a.L;
     const int logL = a.logL;
-    for (int r = threadIdx.x; r < (L >> 2); r += kFftThreads) {
+    for (int r = threadIdx.x; r < (L >> 2); r += TPB) {
         const double2 t = __ldg(a.tw + r);  // exp(-2 pi i r / L) = (cos, -sin)
         qt[r] = make_double2(t.x, -t.y);
     }
     if (logL > 4) {
         // radix of the Ns = 16 pass: 16 if logL >= 8, else 2^(logL-4)
         const int lr2 = logL >= 8 ? 4 : logL - 4;
-        for (int e = threadIdx.x; e < (16 << lr2); e += kFftThreads) {
+        for (int e = threadIdx.x; e < (16 << lr2); e += TPB) {
             const int r = e >> 4, k = e & 15;
             t16[e] = __ldg(a.tw + ((r * k) << (logL - 4 - lr2)));
         }
     }
-    if ((in_real && a.scale_in) || (out_real && a.scale_out)) column_scales(a, csc);
+    if ((in_real && a.scale_in) || (out_real && a.scale_out)) column_scales<TPB>(a, csc);
     __syncthreads();
-    const int logG = kLogFftPoints - logL;
+    const int logG = LOGPTS - logL;
     const int G = 1 << logG;
     const int g0 = blockIdx.x * G;
     const int lgi = a.lg_ninner;
     // load: all 16 points per thread issued before the shared-memory stores
     const bool contig_in = in_real || a.in_sl == 1;
-    double2 v[kPtsPerThread];
+    double2 v[16];
 #pragma unroll
-    for (int q = 0; q < kPtsPerThread; ++q) {
-        const int p = threadIdx.x + q * kFftThreads;
+    for (int q = 0; q < 16; ++q) {
+        const int p = threadIdx.x + q * TPB;
         int g, l;
         if (contig_in) {
             g = p >> logL;
@@ -377,8 +381,8 @@ __global__ void __launch_bounds__(kFftThreads, 2) k_fft_lines(LineArgs a) {
         }
     }
 #pragma unroll
-    for (int q = 0; q < kPtsPerThread; ++q) {
-        const int p = threadIdx.x + q * kFftThreads;
+    for (int q = 0; q < 16; ++q) {
+        const int p = threadIdx.x + q * TPB;
         int g, l;
         if (contig_in) {
             g = p >> logL;
@@ -399,14 +403,14 @@ __global__ void __launch_bounds__(kFftThreads, 2) k_fft_lines(LineArgs a) {
     }
     __syncthreads();
     if constexpr (fused) {
-        fft_smem<-1>(sre, sim, logL, qt, t16);
+        fft_smem<-1, TPB>(sre, sim, logL, qt, t16);
         // multiply by the folded real symbol; line (inner index i) enumerates axes 1..dim-1
         const int np1 = a.n + 1;
         int s0 = 1;
         for (int d = 1; d < a.dim; ++d) s0 *= np1;
 #pragma unroll 4
-        for (int q = 0; q < kPtsPerThread; ++q) {
-            const int p = threadIdx.x + q * kFftThreads;
+        for (int q = 0; q < 16; ++q) {
+            const int p = threadIdx.x + q * TPB;
             const int g = p >> logL, l = p & (L - 1);
             const int line = g0 + g;
             if (line >= a.nlines) continue;
@@ -423,16 +427,16 @@ __global__ void __launch_bounds__(kFftThreads, 2) k_fft_lines(LineArgs a) {
             sim[qi] *= lam;
         }
         __syncthreads();
-        fft_smem<+1>(sre, sim, logL, qt, t16);
+        fft_smem<+1, TPB>(sre, sim, logL, qt, t16);
     } else if constexpr (MODE == kFwdCC || MODE == kFwdRC) {
-        fft_smem<-1>(sre, sim, logL, qt, t16);
+        fft_smem<-1, TPB>(sre, sim, logL, qt, t16);
     } else {
-        fft_smem<+1>(sre, sim, logL, qt, t16);
+        fft_smem<+1, TPB>(sre, sim, logL, qt, t16);
     }
     const bool contig_out = out_real || a.out_sl == 1;
 #pragma unroll 4
-    for (int q = 0; q < kPtsPerThread; ++q) {
-        const int p = threadIdx.x + q * kFftThreads;
+    for (int q = 0; q < 16; ++q) {
+        const int p = threadIdx.x + q * TPB;
         int g, l;
         if (contig_out) {
             g = p >> logL;
@@ -513,16 +517,28 @@ struct ie_fft {
 
 namespace ie {
 
-template <int MODE>
-static int launch_mode(const LineArgs& a, int ctas, size_t smem, cudaStream_t st) {
+template <int MODE, int TPB>
+static int launch_mode(const LineArgs& a, cudaStream_t st) {
+    constexpr int PTS = 16 * TPB;
+    const int G = PTS / a.L;
+    const int ctas = (a.nlines + G - 1) / G;
+    const size_t smem = 2 * (size_t)(PTS + PTS / 16) * sizeof(double) + (size_t)(PTS / 4 + 256) * sizeof(double2);
     static bool attr = false;
     if (!attr) {
-        IE_CUDA(cudaFuncSetAttribute(k_fft_lines<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        IE_CUDA(cudaFuncSetAttribute(k_fft_lines<MODE, TPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         attr = true;
     }
-    k_fft_lines<MODE><<<ctas, kFftThreads, smem, st>>>(a);
+    k_fft_lines<MODE, TPB><<<ctas, TPB, smem, st>>>(a);
     IE_LAUNCHED();
     return IE_OK;
+}
+
+template <int TPB>
+static int launch_modes(const LineArgs& a, cudaStream_t st) {
+    if (a.fused) return a.in_real ? launch_mode<kFusedRR, TPB>(a, st) : launch_mode<kFusedCC, TPB>(a, st);
+    if (a.in_real) return launch_mode<kFwdRC, TPB>(a, st);
+    if (a.out_real) return launch_mode<kInvCR, TPB>(a, st);
+    return a.sign < 0 ? launch_mode<kFwdCC, TPB>(a, st) : launch_mode<kInvCC, TPB>(a, st);
 }
 
 static int line_launch(const LineArgs& a_in, cudaStream_t st) {
@@ -533,13 +549,11 @@ static int line_launch(const LineArgs& a_in, cudaStream_t st) {
         set_error("fft: line layout must be a power of two");
         return IE_ERR_ARG;
     }
-    const int G = kFftPoints / a.L;
-    const int ctas = (a.nlines + G - 1) / G;
-    const size_t smem = 2 * (size_t)kSmemStride * sizeof(double) + (size_t)(kFftPoints / 4 + 256) * sizeof(double2);
-    if (a.fused) return a.in_real ? launch_mode<kFusedRR>(a, ctas, smem, st) : launch_mode<kFusedCC>(a, ctas, smem, st);
-    if (a.in_real) return launch_mode<kFwdRC>(a, ctas, smem, st);
-    if (a.out_real) return launch_mode<kInvCR>(a, ctas, smem, st);
-    return a.sign < 0 ? launch_mode<kFwdCC>(a, ctas, smem, st) : launch_mode<kInvCC>(a, ctas, smem, st);
+    // 256-thread CTAs (4096 points) unless that leaves the GPU under-filled and
+    // the lines fit a 32-thread CTA (512 points)
+    const long long big_ctas = ((long long)a.nlines * a.L + 4095) / 4096;
+    if (a.L <= 512 && big_ctas < 2 * kNumSMs) return launch_modes<32>(a, st);
+    return launch_modes<256>(a, st);
 }
 
 static LineArgs base_args(const ie_fft* f) {
