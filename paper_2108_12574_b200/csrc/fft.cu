@@ -254,23 +254,29 @@ __device__ __forceinline__ double2 twiddle(const double2* qt, int m, int logL) {
 // Twiddles of the Ns = 16 pass, radix-major: t16[r * 16 + k] = exp(-2 pi i r k / (16 R)).
 // (Through the quarter-wave table, the 16 k-lanes of that pass would hit one bank.)
 template <int R, int S, int TPB>
-__device__ __forceinline__ void stockham(double* sre, double* sim, int logL, int logNs, const double2* qt,
+__device__ __forceinline__ void stockham(double* sre, double* sim, int logL, int logNs, const double2* tws,
                                          const double2* t16) {
     constexpr int NB = 16 / R;  // 16 points per thread
     constexpr int LR = R == 16 ? 4 : (R == 8 ? 3 : (R == 4 ? 2 : 1));
     const int lpl = logL - LR;  // log2(L / R)
+    const int pl = 1 << lpl;
+    // padded strides: padi(x + r*c) = padi(x) + r*(c + c/16) when c % 16 == 0 and
+    // x % 16 + r*c stays in the same 16-block for c == 1 (first pass stores)
+    const int ld_stride = pl >= 16 ? pl + (pl >> 4) : pl;
+    const int Ns = 1 << logNs;
+    const int st_stride = Ns >= 16 ? Ns + (Ns >> 4) : Ns;
     double vr[NB][R], vi[NB][R];
     int dst[NB];
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
         const int bf = threadIdx.x + b * TPB;
         const int g = bf >> lpl;
-        const int j = bf & ((1 << lpl) - 1);
-        const int k = j & ((1 << logNs) - 1);
-        const int base = (g << logL) + j;
+        const int j = bf & (pl - 1);
+        const int k = j & (Ns - 1);
+        const int base = padi((g << logL) + j);
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            const int q = padi(base + (r << lpl));
+            const int q = pl >= 16 ? base + r * ld_stride : padi((g << logL) + j + (r << lpl));
             vr[b][r] = sre[q];
             vi[b][r] = sim[q];
         }
@@ -278,7 +284,7 @@ __device__ __forceinline__ void stockham(double* sre, double* sim, int logL, int
             const int tstep = k << (logL - logNs - LR);
 #pragma unroll
             for (int r = 1; r < R; ++r) {
-                const double2 t = logNs == 4 ? t16[r * 16 + k] : twiddle(qt, r * tstep, logL);
+                const double2 t = logNs == 4 ? t16[r * 16 + k] : tws[r * tstep];
                 const double ti = S < 0 ? t.y : -t.y;
                 const double xr = vr[b][r];
                 vr[b][r] = fma(xr, t.x, -vi[b][r] * ti);
@@ -286,33 +292,32 @@ __device__ __forceinline__ void stockham(double* sre, double* sim, int logL, int
             }
         }
         dft_reg<R, S>(vr[b], vi[b]);
-        dst[b] = (g << logL) + ((j >> logNs) << (logNs + LR)) + k;
+        dst[b] = padi((g << logL) + ((j >> logNs) << (logNs + LR)) + k);
     }
     __syncthreads();
 #pragma unroll
     for (int b = 0; b < NB; ++b)
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            const int q = padi(dst[b] + (r << logNs));
+            const int q = dst[b] + r * st_stride;
             sre[q] = vr[b][out_slot<R>(r)];
             sim[q] = vi[b][out_slot<R>(r)];
         }
     __syncthreads();
 }
 
-// Full FFT of every line in shared memory: radix-16 passes, then one of 2/4/8.
 template <int S, int TPB>
-__device__ void fft_smem(double* sre, double* sim, int logL, const double2* qt, const double2* t16) {
+__device__ void fft_smem(double* sre, double* sim, int logL, const double2* tws, const double2* t16) {
     int logNs = 0;
     int rem = logL;
     while (rem >= 4) {
-        stockham<16, S, TPB>(sre, sim, logL, logNs, qt, t16);
+        stockham<16, S, TPB>(sre, sim, logL, logNs, tws, t16);
         logNs += 4;
         rem -= 4;
     }
-    if (rem == 3) stockham<8, S, TPB>(sre, sim, logL, logNs, qt, t16);
-    if (rem == 2) stockham<4, S, TPB>(sre, sim, logL, logNs, qt, t16);
-    if (rem == 1) stockham<2, S, TPB>(sre, sim, logL, logNs, qt, t16);
+    if (rem == 3) stockham<8, S, TPB>(sre, sim, logL, logNs, tws, t16);
+    if (rem == 2) stockham<4, S, TPB>(sre, sim, logL, logNs, tws, t16);
+    if (rem == 1) stockham<2, S, TPB>(sre, sim, logL, logNs, tws, t16);
 }
 
 // Pass modes: what a line transform reads, does and writes.
@@ -329,16 +334,13 @@ __global__ void __launch_bounds__(TPB, 2) k_fft_lines(LineArgs a) {
     constexpr bool fused = MODE == kFusedCC || MODE == kFusedRR;
     double* sre = smd;
     double* sim = smd + SSTR;
-    double2* qt = reinterpret_cast<double2*>(smd + 2 * SSTR);  // quarter-wave twiddles
-    double2* t16 = qt + (PTS / 4);                              // Ns = 16 pass twiddles
+    double2* qt = reinterpret_cast<double2*>(smd + 2 * SSTR);  // full twiddle table exp(-2 pi i m / L)
+    double2* t16 = qt + a.L;                                    // Ns = 16 pass twiddles
     if (a.stop && *a.stop) return;
     __shared__ double csc[2];
     const int L = a.L;
     const int logL = a.logL;
-    for (int r = threadIdx.x; r < (L >> 2); r += TPB) {
-        const double2 t = __ldg(a.tw + r);  // exp(-2 pi i r / L) = (cos, -sin)
-        qt[r] = make_double2(t.x, -t.y);
-    }
+    for (int r = threadIdx.x; r < L; r += TPB) qt[r] = __ldg(a.tw + r);
     if (logL > 4) {
         // radix of the Ns = 16 pass: 16 if logL >= 8, else 2^(logL-4)
         const int lr2 = logL >= 8 ? 4 : logL - 4;
@@ -522,10 +524,11 @@ static int launch_mode(const LineArgs& a, cudaStream_t st) {
     constexpr int PTS = 16 * TPB;
     const int G = PTS / a.L;
     const int ctas = (a.nlines + G - 1) / G;
-    const size_t smem = 2 * (size_t)(PTS + PTS / 16) * sizeof(double) + (size_t)(PTS / 4 + 256) * sizeof(double2);
+    const size_t smem = 2 * (size_t)(PTS + PTS / 16) * sizeof(double) + (size_t)(a.L + 256) * sizeof(double2);
     static bool attr = false;
     if (!attr) {
-        IE_CUDA(cudaFuncSetAttribute(k_fft_lines<MODE, TPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        const size_t smax = 2 * (size_t)(PTS + PTS / 16) * sizeof(double) + (size_t)(PTS + 256) * sizeof(double2);
+        IE_CUDA(cudaFuncSetAttribute(k_fft_lines<MODE, TPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
         attr = true;
     }
     k_fft_lines<MODE, TPB><<<ctas, TPB, smem, st>>>(a);
