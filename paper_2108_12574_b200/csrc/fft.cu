@@ -16,6 +16,7 @@
 //    for odd log2 M) over 4096 complex points in shared memory (64 KB):
 //    4096/M lines of length M = 2n <= 4096.
 #include <math.h>
+#include <stdlib.h>
 
 #include <vector>
 
@@ -340,7 +341,20 @@ __global__ void __launch_bounds__(TPB, 2) k_fft_lines(LineArgs a) {
     __shared__ double csc[2];
     const int L = a.L;
     const int logL = a.logL;
-    for (int r = threadIdx.x; r < L; r += TPB) qt[r] = __ldg(a.tw + r);
+    {
+        // twiddle table: all loads of a thread in flight together
+        double2 tv[16];
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            const int r = threadIdx.x + q * TPB;
+            if (r < L) tv[q] = __ldg(a.tw + r);
+        }
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            const int r = threadIdx.x + q * TPB;
+            if (r < L) qt[r] = tv[q];
+        }
+    }
     if (logL > 4) {
         // radix of the Ns = 16 pass: 16 if logL >= 8, else 2^(logL-4)
         const int lr2 = logL >= 8 ? 4 : logL - 4;
@@ -406,16 +420,18 @@ __global__ void __launch_bounds__(TPB, 2) k_fft_lines(LineArgs a) {
     __syncthreads();
     if constexpr (fused) {
         fft_smem<-1, TPB>(sre, sim, logL, qt, t16);
-        // multiply by the folded real symbol; line (inner index i) enumerates axes 1..dim-1
+        // multiply by the folded real symbol; line (inner index i) enumerates axes 1..dim-1.
+        // A thread's 16 points lie on at most 16 lines: per-point line offsets first,
+        // then all 16 symbol loads in flight, then the multiplies.
         const int np1 = a.n + 1;
         int s0 = 1;
         for (int d = 1; d < a.dim; ++d) s0 *= np1;
-#pragma unroll 4
+        double lam[16];
+#pragma unroll
         for (int q = 0; q < 16; ++q) {
             const int p = threadIdx.x + q * TPB;
             const int g = p >> logL, l = p & (L - 1);
             const int line = g0 + g;
-            if (line >= a.nlines) continue;
             int tmp = line & ((1 << lgi) - 1), off = 0, stride = 1;
             for (int d = a.dim - 1; d >= 1; --d) {
                 const int k = tmp & (L - 1);
@@ -423,10 +439,13 @@ __global__ void __launch_bounds__(TPB, 2) k_fft_lines(LineArgs a) {
                 off += min(k, L - k) * stride;
                 stride *= np1;
             }
-            const double lam = __ldg(a.sym + (int64_t)min(l, L - l) * s0 + off);
-            const int qi = padi(p);
-            sre[qi] *= lam;
-            sim[qi] *= lam;
+            lam[q] = line < a.nlines ? __ldg(a.sym + (int64_t)min(l, L - l) * s0 + off) : 0.0;
+        }
+#pragma unroll
+        for (int q = 0; q < 16; ++q) {
+            const int qi = padi(threadIdx.x + q * TPB);
+            sre[qi] *= lam[q];
+            sim[qi] *= lam[q];
         }
         __syncthreads();
         fft_smem<+1, TPB>(sre, sim, logL, qt, t16);
