@@ -24,7 +24,8 @@ from .kernel import KernelOperator
 
 
 def to_device_vector(v, n: int):
-    """(torch CUDA float64 tensor, was_numpy).  Validates length n."""
+    """(torch CUDA float64 tensor, was_numpy).  Validates length n.  A numpy
+    input backed by pinned (page-locked) memory is copied by DMA directly."""
     torch = _lib.torch_cuda()
     if isinstance(v, torch.Tensor):
         if v.shape != (n,):
@@ -38,6 +39,7 @@ def to_device_vector(v, n: int):
 
 
 def to_host(t, was_numpy: bool):
+    """Device result -> fresh numpy array (the reference returns fresh arrays)."""
     return t.cpu().numpy() if was_numpy else t
 
 
