@@ -222,66 +222,6 @@ __global__ void k_pcg_rho0(const double* part_rz, int nch, PcgState* s) {
     if (threadIdx.x == 0) s->rho[0] = rz;
 }
 
-// After the A-pass of iteration `it`: residual check of iteration it-1
-// (pcg.py:107-119), then the breakdown test and alpha of iteration it
-// (pcg.py:98-104) -- the reference's order.
-__global__ void k_control_a(const double* part_pq, const double* part_res, int nch, int do_p, int pending,
-                            long long it, PcgState* s, double* hist) {
-    __shared__ double sh[kRed];
-    if (s->stop) return;
-    double denom = 0.0, res2 = 0.0;
-    if (do_p) denom = reduce_partials(part_pq, nch, sh);
-    __syncthreads();
-    if (pending) res2 = reduce_partials(part_res, nch, sh);
-    if (threadIdx.x != 0) return;
-    const long long k = it - 1;
-    if (pending) {
-        const double rel = sqrt(res2) / s->nf;
-        if (!isfinite(rel)) {
-            s->status = 5;
-            s->fail_iter = k;
-            s->fail_value = rel;
-        } else {
-            hist[k] = rel;
-            if (rel <= s->tol) {
-                s->status = 1;
-            } else if (k >= 30 && rel > (1.0 - 1e-3) * hist[k - 30]) {
-                s->status = 2;
-            } else if (!do_p) {
-                s->status = 3;
-            }
-        }
-        if (s->status) {
-            s->n_it = k;
-            s->stop = 1;
-            return;
-        }
-    }
-    if (do_p) {
-        if (!isfinite(denom) || denom <= 0.0) {
-            s->status = 4;
-            s->fail_iter = it;
-            s->fail_value = denom;
-            s->n_it = k;
-            s->stop = 1;
-            return;
-        }
-        s->denom = denom;
-        s->alpha = s->rho[(it - 1) & 1] / denom;
-    }
-}
-
-// rho' = r.z, beta = rho'/rho, rho = rho'
-__global__ void k_control_b(const double* part_rz, int nch, int first, PcgState* s) {
-    __shared__ double sh[kRed];
-    if (s->stop) return;
-    const double rz = reduce_partials(part_rz, nch, sh);
-    if (threadIdx.x == 0) {
-        if (!first) s->beta = rz / s->rho[0];
-        s->rho[0] = rz;
-    }
-}
-
 __global__ void k_post_pass(const double* p, const double* q, const double* f, const double* w, int N, int do_p,
                             int pending, double* part_pq, double* part_res, const int* stop) {
     __shared__ double sh[kRed];
@@ -310,65 +250,16 @@ __global__ void k_post_pass(const double* p, const double* q, const double* f, c
     }
 }
 
-// u += alpha p; r -= alpha q  (products rounded first, as numpy does)
-__global__ void k_update_ur(double* u, double* r, const double* p, const double* q, const PcgState* s, int N) {
-    if (s->stop) return;
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= N) return;
-    const double al = s->alpha;
-    u[i] = __dadd_rn(u[i], __dmul_rn(al, p[i]));
-    r[i] = __dsub_rn(r[i], __dmul_rn(al, q[i]));
-}
-
-// p = z + beta p
-__global__ void k_update_p(double* p, const double* z, const PcgState* s, int N) {
-    if (s->stop) return;
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= N) return;
-    p[i] = __dadd_rn(z[i], __dmul_rn(s->beta, p[i]));
-}
-
 __global__ void k_copy_if_running(double* dst, const double* src, int N, const int* stop) {
     if (*stop) return;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < N) dst[i] = src[i];
 }
 
-__global__ void k_scale_div(double* x, const double* src, double d, int N) {
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < N) x[i] = src[i] / d;
-}
-
-// Lanczos: c_i = AV_i . w for i < nb (partials per (i, chunk))
-__global__ void __launch_bounds__(kRed) k_gemv_t_partials(const double* AV, int64_t ld, int nb, const double* w,
-                                                          int N, double* part, int nch) {
-    __shared__ double sh[kRed];
-    const int i = blockIdx.y;
-    const double* v = AV + (int64_t)i * ld;
-    const int base = blockIdx.x * kChunk;
-    double loc = 0.0;
-#pragma unroll
-    for (int e = 0; e < kChunk / kRed; ++e) {
-        const int t = base + e * kRed + threadIdx.x;
-        if (t < N) loc = fma(v[t], w[t], loc);
-    }
-    const double s = block_tree(loc, sh);
-    if (threadIdx.x == 0) part[(int64_t)i * nch + blockIdx.x] = s;
-}
-
 __global__ void k_reduce_rows(const double* part, int nch, double* out) {
     __shared__ double sh[kRed];
     const double v = reduce_partials(part + (int64_t)blockIdx.x * nch, nch, sh);
     if (threadIdx.x == 0) out[blockIdx.x] = v;
-}
-
-// w -= sum_i c_i V_i  (ascending i, products rounded first)
-__global__ void k_gemv_sub(double* w, const double* V, int64_t ld, int nb, const double* c, int N) {
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= N) return;
-    double x = w[t];
-    for (int i = 0; i < nb; ++i) x = __dsub_rn(x, __dmul_rn(c[i], V[(int64_t)i * ld + t]));
-    w[t] = x;
 }
 
 // Sturm count of eigenvalues < x for the symmetric tridiagonal (a, b).
