@@ -1171,12 +1171,14 @@ extern "C" int ie_precond_create(const ie_geom* g, const int64_t* h_offsets, con
         }
         std::vector<std::vector<int>> mem(U);
         for (int64_t k = 0; k < D; ++k) mem[rep[k]].push_back((int)k);
+        // tile width: about D / (2 CTAs x 148 SMs) blocks, so the tiles fill one wave
+        const int64_t tw = std::max<int64_t>(8, std::min<int64_t>(ie::kGemmTN, (D + 2 * ie::kNumSMs - 1) / (2 * ie::kNumSMs)));
         std::vector<int> members, tcls, tfirst, tcnt;
         for (int64_t u = 0; u < U; ++u) {
-            for (size_t q = 0; q < mem[u].size(); q += ie::kGemmTN) {
+            for (size_t q = 0; q < mem[u].size(); q += (size_t)tw) {
                 tcls.push_back((int)u);
                 tfirst.push_back((int)(members.size() + q));
-                tcnt.push_back((int)std::min<size_t>(ie::kGemmTN, mem[u].size() - q));
+                tcnt.push_back((int)std::min<size_t>((size_t)tw, mem[u].size() - q));
             }
             members.insert(members.end(), mem[u].begin(), mem[u].end());
         }
