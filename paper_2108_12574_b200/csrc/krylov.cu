@@ -15,6 +15,8 @@
 // fixed-order reduction -- deterministic and independent of the launch.
 #include <math.h>
 
+#include <stdlib.h>
+
 #include <chrono>
 #include <mutex>
 #include <string>
@@ -33,6 +35,8 @@ int matvec_launch(const ie_matvec* m, const double* X, int64_t ldx, int nrhs, do
 int precond_apply(const ie_precond* p, const double* r, double* z, double* partials, cudaStream_t st,
                   const int* stop);
 int matvec_N(const ie_matvec* m);
+uint64_t matvec_uid(const ie_matvec* m);
+uint64_t precond_uid(const ie_precond* p);
 
 constexpr int kChunk = 2048;
 constexpr int kRed = 256;
@@ -83,9 +87,15 @@ struct PcgState {
     double rho[2];  // rho_j = r_j . z_j in slot j & 1 (read and written by different launches)
     double alpha, beta, denom, nf, tol, fail_value;
     long long max_iters, n_it, fail_iter;
+    long long it_dev;  // iteration index for graph-replayed iterations (it < 0 in the kernel args)
     int status;  // 0 running, 1 converged, 2 stagnated, 3 max_iters, 4 breakdown, 5 non-finite
     int stop;
 };
+
+__global__ void k_set_it(PcgState* s, long long it) { s->it_dev = it; }
+__global__ void k_advance_it(PcgState* s) {
+    if (!s->stop) s->it_dev += 1;
+}
 
 __global__ void k_pcg_init(const double* part, int nch, PcgState* s, double tol, long long max_iters,
                            double* hist) {
@@ -132,6 +142,7 @@ __global__ void __launch_bounds__(kRed) k_iter_a(const double* part_pq, const do
     __shared__ double sh[kRed];
     __shared__ int decided;
     if (s->stop) return;
+    if (it < 0) it = s->it_dev;
     double denom = 0.0, res2 = 0.0;
     if (do_p) denom = reduce_partials(part_pq, nch, sh);
     __syncthreads();
@@ -193,6 +204,7 @@ __global__ void __launch_bounds__(kRed) k_iter_b(const double* part_rz, int nch,
                                                  double* p, const double* z, int N, double* amax) {
     __shared__ double sh[kRed];
     if (s->stop) return;
+    if (it < 0) it = s->it_dev;
     const double rz = reduce_partials(part_rz, nch, sh);
     const double beta = rz / s->rho[(it - 1) & 1];
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -303,6 +315,11 @@ struct PcgWork {
     int64_t cap = 0;
     double *PU = nullptr, *QW = nullptr, *r = nullptr, *z = nullptr, *part = nullptr, *hist = nullptr;
     double* amax = nullptr;  // per-chunk max|p|, max|u| (2-RHS FFT column scaling)
+    double* fcopy = nullptr; // the right-hand side (graph-stable address)
+    cudaStream_t cap_stream = nullptr;
+    cudaGraphExec_t gexec = nullptr;
+    uint64_t key_a = 0, key_t = 0;
+    int gnodes = 0;  // kernel nodes in the captured iteration
     PcgState* st = nullptr;
     PcgState* host = nullptr;
     std::vector<cudaEvent_t> ev;
@@ -315,6 +332,9 @@ struct PcgWork {
         cudaFree(part);
         cudaFree(hist);
         cudaFree(amax);
+        cudaFree(fcopy);
+        if (gexec) cudaGraphExecDestroy(gexec);
+        if (cap_stream) cudaStreamDestroy(cap_stream);
         cudaFree(st);
         if (host) cudaFreeHost(host);
         for (auto e : ev) cudaEventDestroy(e);
@@ -345,6 +365,8 @@ static PcgWork* work_acquire(int N, int64_t cap, int* rc) {
     if (e == cudaSuccess) e = cudaMalloc(&w->part, 3 * (size_t)nch * 8);
     if (e == cudaSuccess) e = cudaMalloc(&w->hist, (size_t)cap * 8);
     if (e == cudaSuccess) e = cudaMalloc(&w->amax, 2 * (size_t)nch * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&w->fcopy, (size_t)N * 8);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&w->cap_stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaMalloc(&w->st, sizeof(PcgState));
     if (e == cudaSuccess) e = cudaMallocHost(&w->host, sizeof(PcgState));
     if (e != cudaSuccess) {
@@ -421,6 +443,9 @@ extern "C" int ie_pcg_f64(const ie_matvec* A, const ie_precond* T, const double*
         if (timed) IE_CUDA(cudaEventRecord(W->ev[2 * evi + 1], st));
         return IE_OK;
     };
+    // the right-hand side at a stable address (captured graphs reference it)
+    IE_CUDA(cudaMemcpyAsync(W->fcopy, f, (size_t)N * 8, cudaMemcpyDeviceToDevice, st));
+    f = W->fcopy;
     // ||f||, state init (pcg.py:72-91)
     k_dot_partials<<<nch, kRed, 0, st>>>(f, f, N, 0, part_pq);
     IE_LAUNCHED();
@@ -433,28 +458,88 @@ extern "C" int ie_pcg_f64(const ie_matvec* A, const ie_precond* T, const double*
     k_pcg_rho0<<<1, kRed, 0, st>>>(part_rz, nch, W->st);
     IE_LAUNCHED();
     // iterations: `it` = the iteration whose A-pass is enqueued; the pass also
-    // carries u_{it-1} for the deferred true-residual check of iteration it-1
+    // carries u_{it-1} for the deferred true-residual check of iteration it-1.
+    // Steady-state iterations (2 <= it < max_iters) replay one captured CUDA
+    // graph that reads `it` from the device state.
+    auto enqueue_iter = [&](int64_t itarg, int do_p, int pending, bool spec, cudaStream_t s2, bool timed_apply,
+                            int64_t evi) -> int {
+        int r2;
+        if (do_p && pending) {
+            r2 = matvec_launch(A, W->PU, N, 2, W->QW, N, 0, N, s2, stop, W->amax);
+        } else if (do_p) {
+            r2 = matvec_launch(A, p, N, 1, q, N, 0, N, s2, stop);
+        } else {
+            r2 = matvec_launch(A, uu, N, 1, w, N, 0, N, s2, stop);
+        }
+        if (r2) return r2;
+        k_post_pass<<<nch, kRed, 0, s2>>>(p, q, f, w, N, do_p, pending, part_pq, part_res, stop);
+        IE_LAUNCHED();
+        k_iter_a<<<nch, kRed, 0, s2>>>(part_pq, part_res, nch, do_p, pending, itarg, W->st, W->hist, uu, W->r, p, q,
+                                       N, W->amax);
+        IE_LAUNCHED();
+        if (spec) {  // speculative: z_it is discarded if iteration it is the last
+            if (timed_apply) {
+                if ((r2 = apply(W->r, W->z, evi))) return r2;
+            } else if (T) {
+                if ((r2 = precond_apply(T, W->r, W->z, part_rz, s2, stop))) return r2;
+            } else {
+                k_copy_if_running<<<g1(N), 256, 0, s2>>>(W->z, W->r, N, stop);
+                IE_LAUNCHED();
+                k_dot_partials<<<nch, kRed, 0, s2>>>(W->r, W->z, N, 0, part_rz);
+                IE_LAUNCHED();
+            }
+            k_iter_b<<<nch, kRed, 0, s2>>>(part_rz, nch, itarg, W->st, p, W->z, N, W->amax);
+            IE_LAUNCHED();
+        }
+        return IE_OK;
+    };
+    const bool use_graph = max_iters >= 3 && !getenv("IEDD_B200_NO_GRAPH");
+    if (use_graph) {
+        const uint64_t ka = matvec_uid(A), kt = T ? precond_uid(T) : 0;
+        if (!W->gexec || W->key_a != ka || W->key_t != kt) {
+            if (W->gexec) {
+                cudaGraphExecDestroy(W->gexec);
+                W->gexec = nullptr;
+            }
+            cudaGraph_t g;
+            IE_CUDA(cudaStreamBeginCapture(W->cap_stream, cudaStreamCaptureModeThreadLocal));
+            int r2 = enqueue_iter(-1, 1, 1, true, W->cap_stream, false, 0);
+            if (!r2) {
+                k_advance_it<<<1, 1, 0, W->cap_stream>>>(W->st);
+            }
+            cudaError_t ce = cudaStreamEndCapture(W->cap_stream, &g);
+            if (r2) return r2;
+            IE_CUDA(ce);
+            size_t nn = 0;
+            cudaGraphGetNodes(g, nullptr, &nn);
+            std::vector<cudaGraphNode_t> nodes(nn);
+            if (nn) cudaGraphGetNodes(g, nodes.data(), &nn);
+            W->gnodes = 0;
+            for (auto nd : nodes) {
+                cudaGraphNodeType t;
+                if (cudaGraphNodeGetType(nd, &t) == cudaSuccess && t == cudaGraphNodeTypeKernel) ++W->gnodes;
+            }
+            ce = cudaGraphInstantiate(&W->gexec, g, 0);
+            cudaGraphDestroy(g);
+            IE_CUDA(ce);
+            W->key_a = ka;
+            W->key_t = kt;
+        }
+    }
     int64_t it = 1;
     for (; it <= max_iters + 1; ++it) {
         const int do_p = it <= max_iters;
         const int pending = it >= 2;
-        if (do_p && pending) {
-            rc = matvec_launch(A, W->PU, N, 2, W->QW, N, 0, N, st, stop, W->amax);
-        } else if (do_p) {
-            rc = matvec_launch(A, p, N, 1, q, N, 0, N, st, stop);
+        const bool spec = do_p && it < max_iters;
+        if (use_graph && pending && spec) {
+            if (it == 2) {
+                k_set_it<<<1, 1, 0, st>>>(W->st, 2);
+                IE_LAUNCHED();
+            }
+            IE_CUDA(cudaGraphLaunch(W->gexec, st));
+            g_launches.fetch_add(W->gnodes, std::memory_order_relaxed);
         } else {
-            rc = matvec_launch(A, uu, N, 1, w, N, 0, N, st, stop);
-        }
-        if (rc) return rc;
-        k_post_pass<<<nch, kRed, 0, st>>>(p, q, f, w, N, do_p, pending, part_pq, part_res, stop);
-        IE_LAUNCHED();
-        k_iter_a<<<nch, kRed, 0, st>>>(part_pq, part_res, nch, do_p, pending, it, W->st, W->hist, uu, W->r, p, q, N,
-                                       W->amax);
-        IE_LAUNCHED();
-        if (do_p && it < max_iters) {  // speculative: z_it is discarded if iteration it is the last
-            if ((rc = apply(W->r, W->z, it))) return rc;
-            k_iter_b<<<nch, kRed, 0, st>>>(part_rz, nch, it, W->st, p, W->z, N, W->amax);
-            IE_LAUNCHED();
+            if ((rc = enqueue_iter(it, do_p, pending, spec, st, true, it))) return rc;
         }
         if (it % kBatch == 0 || it == max_iters + 1) {
             IE_CUDA(cudaMemcpyAsync(W->host, W->st, sizeof(PcgState), cudaMemcpyDeviceToHost, st));
@@ -481,6 +566,7 @@ extern "C" int ie_pcg_f64(const ie_matvec* A, const ie_precond* T, const double*
     double tp = 0.0;
     int64_t np = 0;
     for (int64_t e = 0; e < S.n_it && 2 * e + 1 < (int64_t)W->ev.size(); ++e) {
+        if (use_graph && e >= 2 && e < max_iters) continue;  // graph iterations are not event-timed
         float ms = 0.f;
         if (cudaEventElapsedTime(&ms, W->ev[2 * e], W->ev[2 * e + 1]) == cudaSuccess) {
             tp += ms * 1e-3;

@@ -224,6 +224,7 @@ int fft_matvec(const ie_fft* f, const double* X0, const double* X1, double* Y0, 
 
 struct ie_matvec {
     ie_geom g;
+    uint64_t uid;   // unique per handle (graph cache key)
     int method;     // IE_MATVEC_DIRECT / IE_MATVEC_FFT
     ie_fft* fft;    // FFT plan (method FFT)
     double* d_full; // FFT path: full-range output for partial row requests
@@ -378,6 +379,8 @@ extern "C" int ie_matvec_create_method(const ie_geom* g, int32_t method, ie_matv
     }
     ie_matvec* m = new ie_matvec();
     m->g = *g;
+    static std::atomic<uint64_t> next_uid{1};
+    m->uid = next_uid.fetch_add(1);
     m->N = (int)Nd;
     m->method = method;
     m->fft = nullptr;
@@ -474,4 +477,5 @@ extern "C" int ie_assemble_block_f64(const ie_geom* g, const int64_t* rows, int6
 
 namespace ie {
 int matvec_N(const ie_matvec* m) { return m->N; }
+uint64_t matvec_uid(const ie_matvec* m) { return m->uid; }
 }  // namespace ie

@@ -707,6 +707,7 @@ __global__ void __launch_bounds__(256) k_scatter(const double* staging, const in
 // ------------------------------------------------------------- host side --
 struct ie_precond {
     ie_geom g;
+    uint64_t uid;  // unique per handle (graph cache key)
     int N;
     int64_t D;
     int variant;
@@ -1057,6 +1058,8 @@ extern "C" int ie_precond_create(const ie_geom* g, const int64_t* h_offsets, con
     }
     ie_precond* p = new ie_precond();
     p->g = *g;
+    static std::atomic<uint64_t> next_uid{1};
+    p->uid = next_uid.fetch_add(1);
     p->N = (int)N;
     p->D = D;
     p->variant = variant;
@@ -1220,6 +1223,10 @@ extern "C" int ie_precond_create(const ie_geom* g, const int64_t* h_offsets, con
     *out = p;
     return IE_OK;
 }
+
+namespace ie {
+uint64_t precond_uid(const ie_precond* p) { return p->uid; }
+}  // namespace ie
 
 extern "C" int ie_precond_apply_f64(const ie_precond* p, const double* r, double* z, void* stream) {
     if (!p || !r || !z) {
