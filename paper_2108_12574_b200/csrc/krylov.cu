@@ -586,12 +586,15 @@ extern "C" int ie_pcg_f64(const ie_matvec* A, const ie_precond* T, const double*
 }
 
 // ---------------------------------------------------------------- K5 --
-// Lanczos state on the device (spectrum.py:154-189): every step kernel
-// returns at once when `stop` is set, the host reads the state every 8 steps.
+// Lanczos state on the device (spectrum.py:154-189).  Every step kernel reads
+// the step index j from the state and returns at once when `stop` is set, so
+// one captured CUDA graph replays every step; the host reads the state every
+// 8 steps.  Grids are sized for the largest basis and exit early above j.
 struct LzState {
     double beta, est, cur, nrm;
     int have_est, stable, stop, status;  // status 1 converged, 2 beta^2 <= 0, 3 beta < 1e-14
     long long steps;
+    long long j;  // current step (basis vectors 0..j)
 };
 
 __global__ void k_lz_init(const double* part, int nch, LzState* s) {
@@ -605,33 +608,58 @@ __global__ void k_lz_init(const double* part, int nch, LzState* s) {
         s->status = 0;
         s->steps = 0;
         s->est = 0.0;
+        s->j = 0;
     }
 }
 
-__global__ void k_lz_scale(double* V, double* AV, const double* w, const double* aw, const LzState* s, int by_beta,
+// V[0] = v0 / nrm, AV[0] = av / nrm, avj = AV[0]
+__global__ void k_lz_first(double* V, double* AV, double* avj, const double* w, const double* aw, const LzState* s,
                            int N) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= N) return;
+    const double d = s->nrm;
+    V[i] = w[i] / d;
+    const double a = aw[i] / d;
+    AV[i] = a;
+    avj[i] = a;
+}
+
+// V[j+1] = w / beta, AV[j+1] = aw / beta, avj = AV[j+1]  (spectrum.py:186-187)
+__global__ void k_lz_next(double* V, double* AV, double* avj, const double* w, const double* aw, const LzState* s,
+                          int N) {
     if (s->stop) return;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= N) return;
-    const double d = by_beta ? s->beta : s->nrm;
-    V[i] = w[i] / d;
-    AV[i] = aw[i] / d;
+    const int64_t off = (s->j + 1) * (int64_t)N;
+    const double d = s->beta;
+    V[off + i] = w[i] / d;
+    const double a = aw[i] / d;
+    AV[off + i] = a;
+    avj[i] = a;
 }
 
-__global__ void k_lz_alpha(const double* part, int nch, double* alpha_j, const int* stop) {
-    __shared__ double sh[kRed];
-    if (*stop) return;
-    const double v = reduce_partials(part, nch, sh);
-    if (threadIdx.x == 0) *alpha_j = v;
+__global__ void k_lz_advance(LzState* s) {
+    if (!s->stop) s->j += 1;
 }
 
-// beta^2 = w.aw, Ritz value of T_j by 32-way Sturm multisection (warp 0),
-// the reference's stopping rule.
-__global__ void k_lz_control(const double* part, int nch, const double* a, double* b, int m, int which,
-                             double rtol, LzState* s) {
+__global__ void k_lz_alpha(const double* part, int nch, double* alphas, const LzState* s) {
     __shared__ double sh[kRed];
-    __shared__ double bounds[2];
     if (s->stop) return;
+    const double v = reduce_partials(part, nch, sh);
+    if (threadIdx.x == 0) alphas[s->j] = v;
+}
+
+// beta^2 = w.aw, Ritz value of T_j by 256-way Sturm multisection, the
+// reference's stopping rule.  Cauchy interlacing bounds the new extremal
+// Ritz value by the previous one (lambda_min(T_m) <= lambda_min(T_{m-1}),
+// lambda_max(T_m) >= lambda_max(T_{m-1})), which brackets one side.
+__global__ void __launch_bounds__(kRed) k_lz_control(const double* part, int nch, const double* a, double* b,
+                                                     int which, double rtol, LzState* s) {
+    __shared__ double sh[kRed];
+    __shared__ double br[2];
+    __shared__ unsigned above_mask[kRed / 32];
+    if (s->stop) return;
+    const int m = (int)(s->j + 1);
     const double beta2 = reduce_partials(part, nch, sh);
     if (!(beta2 > 0.0) || !isfinite(beta2)) {
         if (threadIdx.x == 0) {
@@ -641,8 +669,8 @@ __global__ void k_lz_control(const double* part, int nch, const double* a, doubl
         }
         return;
     }
-    if (threadIdx.x < 32) {
-        const int lane = threadIdx.x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (warp == 0) {
         double lo = a[0], hi = a[0];
         for (int i = lane; i < m; i += 32) {
             const double r = (i > 0 ? fabs(b[i - 1]) : 0.0) + (i < m - 1 ? fabs(b[i]) : 0.0);
@@ -656,27 +684,44 @@ __global__ void k_lz_control(const double* part, int nch, const double* a, doubl
         const double span = fmax(hi - lo, 1e-300);
         lo -= 1e-3 * span + 1e-300;
         hi += 1e-3 * span + 1e-300;
-        const int target = which == 0 ? 1 : m;
-        for (int it = 0; it < 64; ++it) {
-            const double x = lo + (hi - lo) * (double)(lane + 1) / 33.0;
-            const bool above = sturm_count(a, b, m, x) >= target;
-            const unsigned mask = __ballot_sync(0xffffffffu, above);
-            const int first = mask ? __ffs(mask) - 1 : 32;
-            const double nlo = first == 0 ? lo : lo + (hi - lo) * (double)first / 33.0;
-            const double nhi = first == 32 ? hi : lo + (hi - lo) * (double)(first + 1) / 33.0;
-            if (!(nhi < hi) && !(nlo > lo)) break;
-            lo = nlo;
-            hi = nhi;
-            if (hi - lo <= 2.0 * 2.220446049250313e-16 * fmax(fabs(lo), fabs(hi))) break;
-        }
         if (lane == 0) {
-            bounds[0] = lo;
-            bounds[1] = hi;
+            if (s->have_est) {  // interlacing bound (with a small rounding margin)
+                const double e = s->est, mg = 1e-12 * fabs(e) + 1e-300;
+                if (which == 0 && e + mg < hi && e + mg > lo) hi = e + mg;
+                if (which == 1 && e - mg > lo && e - mg < hi) lo = e - mg;
+            }
+            br[0] = lo;
+            br[1] = hi;
         }
     }
     __syncthreads();
-    if (threadIdx.x != 0) return;
-    const double cur = 0.5 * (bounds[0] + bounds[1]);
+    const int target = which == 0 ? 1 : m;  // count(x) >= target  <=>  x > lambda
+    for (int it = 0; it < 16; ++it) {
+        const double lo = br[0], hi = br[1];
+        const double x = lo + (hi - lo) * (double)(tid + 1) / (double)(kRed + 1);
+        const bool above = sturm_count(a, b, m, x) >= target;
+        const unsigned mk = __ballot_sync(0xffffffffu, above);
+        if (lane == 0) above_mask[warp] = mk;
+        __syncthreads();
+        if (tid == 0) {
+            int first = kRed;
+            for (int w2 = 0; w2 < kRed / 32; ++w2)
+                if (above_mask[w2]) {
+                    first = w2 * 32 + __ffs(above_mask[w2]) - 1;
+                    break;
+                }
+            const double nlo = first == 0 ? lo : lo + (hi - lo) * (double)first / (double)(kRed + 1);
+            const double nhi = first == kRed ? hi : lo + (hi - lo) * (double)(first + 1) / (double)(kRed + 1);
+            br[0] = nlo;
+            br[1] = nhi;
+        }
+        __syncthreads();
+        const double nlo = br[0], nhi = br[1];
+        if ((!(nhi < hi) && !(nlo > lo)) || nhi - nlo <= 2.0 * 2.220446049250313e-16 * fmax(fabs(nlo), fabs(nhi)))
+            break;
+    }
+    if (tid != 0) return;
+    const double cur = 0.5 * (br[0] + br[1]);
     const double beta = sqrt(beta2);
     s->cur = cur;
     s->steps = m;
@@ -700,12 +745,11 @@ __global__ void k_lz_control(const double* part, int nch, const double* a, doubl
     b[m - 1] = beta;
 }
 
-__global__ void k_gemv_t_partials_s(const double* AV, int64_t ld, const double* w, int N, double* part, int nch,
-                                    const int* stop) {
+// c_i = AV_i . w for i <= j (grid rows above j exit)
+__global__ void k_lz_gemv_t(const double* AV, const double* w, int N, double* part, int nch, const LzState* s) {
     __shared__ double sh[kRed];
-    if (*stop) return;
-    const int i = blockIdx.y;
-    const double* v = AV + (int64_t)i * ld;
+    if (s->stop || blockIdx.y > s->j) return;
+    const double* v = AV + (int64_t)blockIdx.y * N;
     const int base = blockIdx.x * kChunk;
     double loc = 0.0;
 #pragma unroll
@@ -714,29 +758,42 @@ __global__ void k_gemv_t_partials_s(const double* AV, int64_t ld, const double* 
         if (t < N) loc = fma(v[t], w[t], loc);
     }
     const double r = block_tree(loc, sh);
-    if (threadIdx.x == 0) part[(int64_t)i * nch + blockIdx.x] = r;
+    if (threadIdx.x == 0) part[(int64_t)blockIdx.y * nch + blockIdx.x] = r;
 }
 
-__global__ void k_reduce_rows_s(const double* part, int nch, double* out, const int* stop) {
+__global__ void k_lz_reduce_rows(const double* part, int nch, double* out, const LzState* s) {
     __shared__ double sh[kRed];
-    if (*stop) return;
+    if (s->stop || blockIdx.x > s->j) return;
     const double v = reduce_partials(part + (int64_t)blockIdx.x * nch, nch, sh);
     if (threadIdx.x == 0) out[blockIdx.x] = v;
 }
 
-__global__ void k_gemv_sub_s(double* w, const double* V, int64_t ld, int nb, const double* c, int N,
-                             const int* stop) {
-    if (*stop) return;
-    const int t = blockIdx.x * blockDim.x + threadIdx.x;
-    if (t >= N) return;
-    double x = w[t];
-    for (int i = 0; i < nb; ++i) x = __dsub_rn(x, __dmul_rn(c[i], V[(int64_t)i * ld + t]));
-    w[t] = x;
+// w -= sum_{i<=j} c_i V_i: a CTA owns 32 consecutive entries, its 8 warps
+// take basis vectors i = warp (mod 8), and the partial sums are combined in
+// warp order (fixed association: deterministic).
+__global__ void __launch_bounds__(256) k_lz_gemv_sub(double* w, const double* V, const double* c, int N,
+                                                     const LzState* s) {
+    __shared__ double part8[8][32];
+    if (s->stop) return;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int t = blockIdx.x * 32 + lane;
+    const int nb = (int)(s->j + 1);
+    double acc = 0.0;
+    if (t < N)
+        for (int i = warp; i < nb; i += 8) acc = fma(c[i], V[(int64_t)i * N + t], acc);
+    part8[warp][lane] = acc;
+    __syncthreads();
+    if (warp == 0 && t < N) {
+        double tot = 0.0;
+#pragma unroll
+        for (int q = 0; q < 8; ++q) tot += part8[q][lane];
+        w[t] -= tot;
+    }
 }
 
-__global__ void k_dot_partials_s(const double* x, const double* y, int N, double* part, const int* stop) {
+__global__ void k_lz_dot(const double* x, const double* y, int N, double* part, const LzState* s) {
     __shared__ double sh[kRed];
-    if (*stop) return;
+    if (s->stop) return;
     const int base = blockIdx.x * kChunk;
     double loc = 0.0;
 #pragma unroll
@@ -758,22 +815,20 @@ extern "C" int ie_lanczos_f64(const ie_matvec* A, const ie_precond* T, const dou
     const int N = matvec_N(A);
     const int nch = dot_chunks(N);
     const int64_t nb_max = max_iters + 1;
-    DevBuf<double> V(st), AV(st), wb(st), awb(st), part(st), cbuf(st), tri(st);
+    DevBuf<double> V(st), AV(st), wb(st), awb(st), avj(st), part(st), cbuf(st), tri(st);
     DevBuf<LzState> S(st);
     IE_CUDA(V.alloc((size_t)nb_max * N));
     IE_CUDA(AV.alloc((size_t)nb_max * N));
     IE_CUDA(wb.alloc(N));
     IE_CUDA(awb.alloc(N));
+    IE_CUDA(avj.alloc(N));
     IE_CUDA(part.alloc((size_t)std::max<int64_t>(nb_max, 2) * nch));
     IE_CUDA(cbuf.alloc(nb_max + 2));
     IE_CUDA(tri.alloc(2 * (size_t)nb_max + 2));
     IE_CUDA(S.alloc(1));
-    LzState* hs = nullptr;
-    IE_CUDA(cudaMallocHost(&hs, sizeof(LzState)));
-    struct HostFree {
-        LzState* h;
-        ~HostFree() { cudaFreeHost(h); }
-    } hf{hs};
+    // pinned status buffer, one per host thread (allocated once)
+    static thread_local LzState* hs = nullptr;
+    if (!hs) IE_CUDA(cudaMallocHost(&hs, sizeof(LzState)));
     double* da = tri.p;           // alphas
     double* db = tri.p + nb_max;  // betas
     const int* stop = &S.p->stop;
@@ -784,33 +839,73 @@ extern "C" int ie_lanczos_f64(const ie_matvec* A, const ie_precond* T, const dou
     IE_LAUNCHED();
     k_lz_init<<<1, kRed, 0, st>>>(part.p, nch, S.p);
     IE_LAUNCHED();
-    k_lz_scale<<<g1(N), 256, 0, st>>>(V.p, AV.p, v0, awb.p, S.p, 0, N);
+    k_lz_first<<<g1(N), 256, 0, st>>>(V.p, AV.p, avj.p, v0, awb.p, S.p, N);
     IE_LAUNCHED();
-    const int64_t kBatch = 8;
-    for (int64_t j = 0; j < max_iters; ++j) {
-        double* AVj = AV.p + (size_t)j * N;
-        const int nb = (int)(j + 1);
-        if ((rc = precond_apply(T, AVj, wb.p, nullptr, st, stop))) return rc;
-        k_dot_partials_s<<<nch, kRed, 0, st>>>(wb.p, AVj, N, part.p, stop);
+    // one Lanczos step (spectrum.py:160-187) on stream s2
+    auto step = [&](cudaStream_t s2) -> int {
+        int r2;
+        if ((r2 = precond_apply(T, avj.p, wb.p, nullptr, s2, stop))) return r2;
+        k_lz_dot<<<nch, kRed, 0, s2>>>(wb.p, avj.p, N, part.p, S.p);
         IE_LAUNCHED();
-        k_lz_alpha<<<1, kRed, 0, st>>>(part.p, nch, da + j, stop);
+        k_lz_alpha<<<1, kRed, 0, s2>>>(part.p, nch, da, S.p);
         IE_LAUNCHED();
         for (int pass = 0; pass < 2; ++pass) {  // two-pass A-orthogonalisation (CGS2)
-            k_gemv_t_partials_s<<<dim3(nch, nb), kRed, 0, st>>>(AV.p, N, wb.p, N, part.p, nch, stop);
+            k_lz_gemv_t<<<dim3(nch, (unsigned)nb_max), kRed, 0, s2>>>(AV.p, wb.p, N, part.p, nch, S.p);
             IE_LAUNCHED();
-            k_reduce_rows_s<<<nb, kRed, 0, st>>>(part.p, nch, cbuf.p, stop);
+            k_lz_reduce_rows<<<(unsigned)nb_max, kRed, 0, s2>>>(part.p, nch, cbuf.p, S.p);
             IE_LAUNCHED();
-            k_gemv_sub_s<<<g1(N), 256, 0, st>>>(wb.p, V.p, N, nb, cbuf.p, N, stop);
+            k_lz_gemv_sub<<<(unsigned)((N + 31) / 32), 256, 0, s2>>>(wb.p, V.p, cbuf.p, N, S.p);
             IE_LAUNCHED();
         }
-        if ((rc = matvec_launch(A, wb.p, N, 1, awb.p, N, 0, N, st, stop))) return rc;
-        k_dot_partials_s<<<nch, kRed, 0, st>>>(wb.p, awb.p, N, part.p, stop);
+        if ((r2 = matvec_launch(A, wb.p, N, 1, awb.p, N, 0, N, s2, stop))) return r2;
+        k_lz_dot<<<nch, kRed, 0, s2>>>(wb.p, awb.p, N, part.p, S.p);
         IE_LAUNCHED();
-        k_lz_control<<<1, kRed, 0, st>>>(part.p, nch, da, db, nb, which, rtol, S.p);
+        k_lz_control<<<1, kRed, 0, s2>>>(part.p, nch, da, db, which, rtol, S.p);
         IE_LAUNCHED();
-        k_lz_scale<<<g1(N), 256, 0, st>>>(V.p + (size_t)(j + 1) * N, AV.p + (size_t)(j + 1) * N, wb.p, awb.p, S.p, 1,
-                                          N);
+        k_lz_next<<<g1(N), 256, 0, s2>>>(V.p, AV.p, avj.p, wb.p, awb.p, S.p, N);
         IE_LAUNCHED();
+        k_lz_advance<<<1, 1, 0, s2>>>(S.p);
+        IE_LAUNCHED();
+        return IE_OK;
+    };
+    // the first kGraphAfter steps are launched directly (short runs never pay the
+    // capture); longer runs replay one captured step graph
+    constexpr int64_t kGraphAfter = 16;
+    cudaGraphExec_t gexec = nullptr;
+    cudaStream_t cap = nullptr;
+    int gnodes = 0;
+    struct GraphFree {
+        cudaGraphExec_t* e;
+        cudaStream_t* c;
+        ~GraphFree() {
+            if (*e) cudaGraphExecDestroy(*e);
+            if (*c) cudaStreamDestroy(*c);
+        }
+    } gf{&gexec, &cap};
+    const bool graph_ok = !getenv("IEDD_B200_NO_GRAPH");
+    const int64_t kBatch = 8;
+    for (int64_t j = 0; j < max_iters; ++j) {
+        if (graph_ok && j >= kGraphAfter && !gexec) {
+            IE_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+            cudaGraph_t g;
+            IE_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
+            rc = step(cap);
+            cudaError_t ce = cudaStreamEndCapture(cap, &g);
+            if (rc) return rc;
+            IE_CUDA(ce);
+            size_t nn = 0;
+            cudaGraphGetNodes(g, nullptr, &nn);
+            gnodes = (int)nn;
+            ce = cudaGraphInstantiate(&gexec, g, 0);
+            cudaGraphDestroy(g);
+            IE_CUDA(ce);
+        }
+        if (gexec) {
+            IE_CUDA(cudaGraphLaunch(gexec, st));
+            g_launches.fetch_add(gnodes, std::memory_order_relaxed);
+        } else if ((rc = step(st))) {
+            return rc;
+        }
         if ((j + 1) % kBatch == 0 || j + 1 == max_iters) {
             IE_CUDA(cudaMemcpyAsync(hs, S.p, sizeof(LzState), cudaMemcpyDeviceToHost, st));
             IE_CUDA(cudaStreamSynchronize(st));
