@@ -97,10 +97,12 @@ class Decomposition:
 
 
 def build_decomposition(grid: Grid, m: int, w: int, kind: str) -> Decomposition:
-    """geometry.py:108-148, 209-244 (jacobi / schwarz; cbd is out of scope)."""
+    """geometry.py:108-148, 164-176, 209-244.  jacobi: the m^dim boxes of q^dim
+    points; schwarz: boxes grown by w (clipped); cbd: per parity colour
+    c = 1 + sum_d (cell_d mod 2) 2^d, the sorted union of its grown boxes."""
     kind = kind.lower()
-    if kind not in ("jacobi", "schwarz"):
-        raise ValueError(f"kind must be 'jacobi' or 'schwarz' in the oracle, got {kind!r}")
+    if kind not in ("jacobi", "schwarz", "cbd"):
+        raise ValueError(f"kind must be 'jacobi', 'schwarz' or 'cbd', got {kind!r}")
     if m < 1:
         raise ValueError(f"m_per_dim must be >= 1, got {m}")
     if grid.n_per_dim % m:
@@ -109,10 +111,17 @@ def build_decomposition(grid: Grid, m: int, w: int, kind: str) -> Decomposition:
         raise ValueError(f"overlap_width must be >= 0, got {w}")
     q = grid.n_per_dim // m
     ww = 0 if kind == "jacobi" else w
-    subs = []
+    boxes, colours = [], []
     for cell in itertools.product(range(m), repeat=grid.dim):
         lo = np.array(cell, dtype=np.int64) * q
-        subs.append(box_indices(grid, lo - ww, lo + q - 1 + ww))
+        boxes.append(box_indices(grid, lo - ww, lo + q - 1 + ww))
+        colours.append(1 + sum((c % 2) << d for d, c in enumerate(cell)))
+    if kind != "cbd":
+        return Decomposition(kind, grid, m, ww, boxes)
+    subs = []
+    for col in range(1, 2 ** grid.dim + 1):
+        members = [b for b, c in zip(boxes, colours) if c == col]
+        subs.append(np.unique(np.concatenate(members)))
     return Decomposition(kind, grid, m, ww, subs)
 
 

@@ -65,6 +65,7 @@ struct BuildArgs {
     int n;
     int dim;
     int variant;
+    int assemble_only;  // workspace blocks: assemble A_k and stop (sweep path)
 };
 
 __device__ __forceinline__ double warp_sum(double v) {
@@ -111,6 +112,10 @@ __global__ void __launch_bounds__(kBuildThreads) k_build(BuildArgs a) {
             }
             A[i * lda + k] = entry_from_m(a.P, a.tab, m);
         }
+    }
+    if (a.assemble_only && a.wofs[u] >= 0) {
+        if (tid == 0) a.info[u] = 0;
+        return;
     }
     __syncthreads();
     // right-looking Cholesky, A = L L^T (LAPACK dpotf2 order: sqrt, scale by 1/ljj)
@@ -702,6 +707,207 @@ __global__ void __launch_bounds__(256) k_scatter(const double* staging, const in
     if (threadIdx.x == 0) partials[blockIdx.x] = sh[0];
 }
 
+// ---- large blocks (s > kSmemMaxS, PACKED_INVERSE): blocked sweep inversion.
+// The sweep operator on index block k (width <= 32, Goodnight 1979):
+//   Dk = A_kk^{-1};  A_ij -= A_ik Dk A_kj (i,j not in k);  A_ik <- A_ik Dk;
+//   A_kj <- Dk A_kj;  A_kk <- -Dk.
+// After sweeping every block, A holds -A^{-1}.  A_kk at step k is the Schur
+// complement of the blocks already swept, so it is SPD iff the leading part
+// of A_k is, and its Cholesky (k_sweep_diag) fails exactly where LAPACK's
+// dpotrf on A_k would -- the reference's NotPositiveDefinite condition.
+// Per step: k_sweep_diag (one CTA per block: Cholesky + inverse of the
+// 32 x 32 pivot block), k_sweep_panel (C = A[:, k], C' = C Dk, rows of block
+// k zeroed), k_sweep_update (rank-32 update A -= C' C^T of the lower 64 x 64
+// tiles on FP64 tensor cores, writing the new panel C' in the same pass).
+// Only the lower triangle of the row-major s x s workspace is maintained.
+constexpr int kSw = 32;     // sweep width
+constexpr int kSwT = 64;    // update tile
+constexpr int kSwP = 36;    // smem panel stride (== 4 mod 16 doubles: conflict-free fragments)
+
+struct SweepArgs {
+    double* work;
+    const int64_t* wofs;  // per large block
+    const int* sizes;
+    const int* uidx;      // large block -> factorised-block index (info)
+    int* info;
+    double* dbuf;         // [nl][32][32]
+    double* cbuf;         // [nl] rows x 32, rows padded to 64
+    double* cpbuf;
+    const int64_t* cofs;
+    int k0;
+};
+
+__global__ void __launch_bounds__(256) k_sweep_diag(SweepArgs a) {
+    const int b = blockIdx.x, s = a.sizes[b], k0 = a.k0;
+    if (k0 >= s || a.info[a.uidx[b]]) return;
+    const int w = min(kSw, s - k0), tid = threadIdx.x, lane = tid & 31;
+    double* A = a.work + a.wofs[b];
+    __shared__ double L[kSw][kSw + 1], Li[kSw][kSw + 1];
+    __shared__ int fail;
+    for (int p = tid; p < kSw * kSw; p += blockDim.x) {
+        const int i = p / kSw, j = p % kSw;
+        L[i][j] = (i < w && j <= i) ? A[(int64_t)(k0 + i) * s + k0 + j] : 0.0;
+        Li[i][j] = 0.0;
+    }
+    if (tid == 0) fail = 0;
+    __syncthreads();
+    if (tid < 32) {
+        // right-looking Cholesky, lane = row (dpotf2 order)
+        for (int j = 0; j < w; ++j) {
+            const double d = L[j][j];
+            if (!(d > 0.0) || !isfinite(d)) {
+                if (lane == 0) fail = 1;
+                break;
+            }
+            const double l = sqrt(d);
+            __syncwarp();
+            if (lane > j && lane < w) L[lane][j] *= 1.0 / l;
+            if (lane == j) L[j][j] = l;
+            __syncwarp();
+            if (lane > j && lane < w) {
+                const double lij = L[lane][j];
+                for (int k = j + 1; k <= lane; ++k) L[lane][k] = fma(-lij, L[k][j], L[lane][k]);
+            }
+            __syncwarp();
+        }
+        __syncwarp();
+        // L^{-1} by columns: lane = column j, forward substitution
+        if (!fail && lane < w) {
+            const int j = lane;
+            for (int i = j; i < w; ++i) {
+                double x = (i == j) ? 1.0 : 0.0;
+                for (int k = j; k < i; ++k) x = fma(-L[i][k], Li[k][j], x);
+                Li[i][j] = x / L[i][i];
+            }
+        }
+    }
+    __syncthreads();
+    if (fail) {
+        if (tid == 0) a.info[a.uidx[b]] = k0 + 1;
+        return;
+    }
+    // Dk = L^{-T} L^{-1}: Dk[i][j] = sum_{k >= max(i,j)} Li[k][i] Li[k][j]
+    double* Dk = a.dbuf + (int64_t)b * kSw * kSw;
+    for (int p = tid; p < kSw * kSw; p += blockDim.x) {
+        const int i = p / kSw, j = p % kSw;
+        double acc = 0.0;
+        for (int k = max(i, j); k < w; ++k) acc = fma(Li[k][i], Li[k][j], acc);
+        Dk[p] = acc;
+        if (i < w && j <= i) A[(int64_t)(k0 + i) * s + k0 + j] = -acc;
+    }
+}
+
+// C[i][c] = A[i][k0 + c] (lower storage: A[k0+c][i] for i < k0), zero on the
+// pivot rows, past s and past w; C' = C Dk.  One CTA per 64 rows.
+__global__ void __launch_bounds__(256) k_sweep_panel(SweepArgs a) {
+    const int b = blockIdx.y, s = a.sizes[b], k0 = a.k0, r0 = blockIdx.x * kSwT;
+    if (k0 >= s || r0 >= s || a.info[a.uidx[b]]) return;
+    const int w = min(kSw, s - k0), tid = threadIdx.x;
+    const double* A = a.work + a.wofs[b];
+    __shared__ double Ds[kSw][kSw + 1], Cs[kSwT][kSw + 1];
+    const double* Dk = a.dbuf + (int64_t)b * kSw * kSw;
+    for (int p = tid; p < kSw * kSw; p += blockDim.x) Ds[p / kSw][p % kSw] = Dk[p];
+    for (int p = tid; p < kSwT * kSw; p += blockDim.x) {
+        // rows below the pivot block: row-contiguous reads (c fastest)
+        const int r = p / kSw, c = p % kSw, i = r0 + r;
+        double v = 0.0;
+        if (i >= k0 + w && i < s && c < w) v = A[(int64_t)i * s + k0 + c];
+        Cs[r][c] = v;
+    }
+    __syncthreads();
+    for (int p = tid; p < kSwT * kSw; p += blockDim.x) {
+        // rows above: A[k0+c][i] is contiguous in i
+        const int c = p / kSwT, r = p % kSwT, i = r0 + r;
+        if (i < k0 && c < w) Cs[r][c] = A[(int64_t)(k0 + c) * s + i];
+    }
+    __syncthreads();
+    double* C = a.cbuf + a.cofs[b] + (int64_t)r0 * kSw;
+    double* Cp = a.cpbuf + a.cofs[b] + (int64_t)r0 * kSw;
+    for (int p = tid; p < kSwT * kSw; p += blockDim.x) {
+        const int r = p / kSw, c = p % kSw;
+        double acc = 0.0;
+#pragma unroll 8
+        for (int e = 0; e < kSw; ++e) acc = fma(Cs[r][e], Ds[e][c], acc);
+        C[p] = Cs[r][c];
+        Cp[p] = acc;
+    }
+}
+
+// Lower 64 x 64 tiles: A_ij -= (C' C^T)_ij off the pivot rows/columns; the
+// pivot column (i below it) and pivot row (j left of it) take C'.
+__global__ void __launch_bounds__(256) k_sweep_update(SweepArgs a) {
+    const int b = blockIdx.y, s = a.sizes[b], k0 = a.k0;
+    if (k0 >= s || a.info[a.uidx[b]]) return;
+    const int nt = (s + kSwT - 1) / kSwT, t = blockIdx.x;
+    if (t >= nt * (nt + 1) / 2) return;
+    int ti = (int)((sqrt(8.0 * t + 1.0) - 1.0) * 0.5);
+    while (ti * (ti + 1) / 2 > t) --ti;
+    while ((ti + 1) * (ti + 2) / 2 <= t) ++ti;
+    const int tj = t - ti * (ti + 1) / 2;
+    const int w = min(kSw, s - k0), tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    __shared__ __align__(16) double Ps[kSwT * kSwP], Qs[kSwT * kSwP];
+    const double* Cp = a.cpbuf + a.cofs[b];
+    const double* C = a.cbuf + a.cofs[b];
+    for (int p = tid; p < kSwT * kSw; p += blockDim.x) {
+        const int r = p / kSw, c = p % kSw;
+        Ps[r * kSwP + c] = Cp[(int64_t)(ti * kSwT + r) * kSw + c];
+        Qs[r * kSwP + c] = C[(int64_t)(tj * kSwT + r) * kSw + c];
+    }
+    __syncthreads();
+    const int wr = warp >> 1, wc = warp & 1;  // warp tile: rows wr*16 + [0,16), cols wc*32 + [0,32)
+    double acc[2][4][2];
+#pragma unroll
+    for (int m = 0; m < 2; ++m)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[m][q][0] = acc[m][q][1] = 0.0;
+    const int fr = lane >> 2, fk = lane & 3;
+#pragma unroll
+    for (int kk = 0; kk < kSw / 4; ++kk) {
+        double av[2], bv[4];
+#pragma unroll
+        for (int m = 0; m < 2; ++m) av[m] = Ps[(wr * 16 + m * 8 + fr) * kSwP + kk * 4 + fk];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) bv[q] = Qs[(wc * 32 + q * 8 + fr) * kSwP + kk * 4 + fk];
+#pragma unroll
+        for (int m = 0; m < 2; ++m)
+#pragma unroll
+            for (int q = 0; q < 4; ++q) dmma884(acc[m][q][0], acc[m][q][1], av[m], bv[q]);
+    }
+    double* A = a.work + a.wofs[b];
+#pragma unroll
+    for (int m = 0; m < 2; ++m) {
+        const int i = ti * kSwT + wr * 16 + m * 8 + fr;
+        if (i >= s) continue;
+        const bool ipiv = i >= k0 && i < k0 + w;
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int j = tj * kSwT + wc * 32 + q * 8 + 2 * fk + h;
+                if (j > i) continue;
+                const bool jpiv = j >= k0 && j < k0 + w;
+                double* e = A + (int64_t)i * s + j;
+                if (ipiv && jpiv) continue;  // -Dk, written by k_sweep_diag
+                if (jpiv) *e = Ps[(i - ti * kSwT) * kSwP + (j - k0)];
+                else if (ipiv) *e = Cp[(int64_t)j * kSw + (i - k0)];
+                else *e -= acc[m][q][h];
+            }
+    }
+}
+
+// out (packed lower by rows == packed upper by columns) = -A.
+__global__ void __launch_bounds__(256) k_sweep_pack(SweepArgs a, double* fac, const int64_t* fofs) {
+    const int b = blockIdx.y, s = a.sizes[b];
+    if (a.info[a.uidx[b]]) return;
+    const double* A = a.work + a.wofs[b];
+    double* out = fac + fofs[a.uidx[b]];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = blockIdx.x * 8 + warp; i < s; i += gridDim.x * 8) {
+        const int64_t o = (int64_t)i * (i + 1) / 2;
+        for (int j = lane; j <= i; j += 32) out[o + j] = -A[(int64_t)i * s + j];
+    }
+}
+
 }  // namespace ie
 
 // ------------------------------------------------------------- host side --
@@ -1140,6 +1346,7 @@ extern "C" int ie_precond_create(const ie_geom* g, const int64_t* h_offsets, con
     ba.n = g->n;
     ba.dim = g->dim;
     ba.variant = variant;
+    ba.assemble_only = (variant == IE_VARIANT_PACKED_INVERSE && !getenv("IEDD_B200_UNBLOCKED_LARGE")) ? 1 : 0;
     size_t smem = 0;
     for (int64_t u = 0; u < U; ++u) {
         const size_t su = (size_t)usizes[u];
@@ -1151,6 +1358,65 @@ extern "C" int ie_precond_create(const ie_geom* g, const int64_t* h_offsets, con
     ie::k_build<<<(unsigned)U, ie::kBuildThreads, smem, st>>>(ba);
     IE_CHECK_BUILD(cudaGetLastError());
     ie::g_launches.fetch_add(1);
+    if (ba.assemble_only && workn) {
+        // blocked sweep inversion of the workspace blocks, all of them per launch
+        std::vector<int> lsz, lu;
+        std::vector<int64_t> lw, lc;
+        int64_t cn = 0;
+        int lmax = 0;
+        for (int64_t u = 0; u < U; ++u)
+            if (uwofs[u] >= 0) {
+                lsz.push_back(usizes[u]);
+                lu.push_back((int)u);
+                lw.push_back(uwofs[u]);
+                lc.push_back(cn);
+                cn += (int64_t)(usizes[u] + ie::kSwT - 1) / ie::kSwT * ie::kSwT * ie::kSw;
+                lmax = std::max(lmax, usizes[u]);
+            }
+        const int nl = (int)lsz.size();
+        int *d_lsz, *d_lu;
+        int64_t *d_lw, *d_lc;
+        double *d_db, *d_cb, *d_cpb;
+        IE_CHECK_BUILD(cudaMalloc(&d_lsz, nl * sizeof(int)));
+        tmp.push_back(d_lsz);
+        IE_CHECK_BUILD(cudaMalloc(&d_lu, nl * sizeof(int)));
+        tmp.push_back(d_lu);
+        IE_CHECK_BUILD(cudaMalloc(&d_lw, nl * sizeof(int64_t)));
+        tmp.push_back(d_lw);
+        IE_CHECK_BUILD(cudaMalloc(&d_lc, nl * sizeof(int64_t)));
+        tmp.push_back(d_lc);
+        IE_CHECK_BUILD(cudaMalloc(&d_db, (size_t)nl * ie::kSw * ie::kSw * sizeof(double)));
+        tmp.push_back(d_db);
+        IE_CHECK_BUILD(cudaMalloc(&d_cb, cn * sizeof(double)));
+        tmp.push_back(d_cb);
+        IE_CHECK_BUILD(cudaMalloc(&d_cpb, cn * sizeof(double)));
+        tmp.push_back(d_cpb);
+        IE_CHECK_BUILD(cudaMemcpyAsync(d_lsz, lsz.data(), nl * sizeof(int), cudaMemcpyHostToDevice, st));
+        IE_CHECK_BUILD(cudaMemcpyAsync(d_lu, lu.data(), nl * sizeof(int), cudaMemcpyHostToDevice, st));
+        IE_CHECK_BUILD(cudaMemcpyAsync(d_lw, lw.data(), nl * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+        IE_CHECK_BUILD(cudaMemcpyAsync(d_lc, lc.data(), nl * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+        ie::SweepArgs sa;
+        sa.work = d_work;
+        sa.wofs = d_lw;
+        sa.sizes = d_lsz;
+        sa.uidx = d_lu;
+        sa.info = d_info;
+        sa.dbuf = d_db;
+        sa.cbuf = d_cb;
+        sa.cpbuf = d_cpb;
+        sa.cofs = d_lc;
+        const int ntile = (lmax + ie::kSwT - 1) / ie::kSwT;
+        for (int k0 = 0; k0 < lmax; k0 += ie::kSw) {
+            sa.k0 = k0;
+            ie::k_sweep_diag<<<nl, 256, 0, st>>>(sa);
+            ie::k_sweep_panel<<<dim3(ntile, nl), 256, 0, st>>>(sa);
+            ie::k_sweep_update<<<dim3(ntile * (ntile + 1) / 2, nl), 256, 0, st>>>(sa);
+            ie::g_launches.fetch_add(3);
+        }
+        ie::k_sweep_pack<<<dim3(std::min(64, (lmax + 7) / 8), nl), 256, 0, st>>>(sa, p->d_fac, d_ufofs);
+        IE_CHECK_BUILD(cudaGetLastError());
+        ie::g_launches.fetch_add(1);
+    }
     std::vector<int> info(U);
     IE_CHECK_BUILD(cudaMemcpyAsync(info.data(), d_info, U * sizeof(int), cudaMemcpyDeviceToHost, st));
     IE_CHECK_BUILD(cudaStreamSynchronize(st));

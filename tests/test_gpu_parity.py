@@ -349,7 +349,7 @@ class TestPCG:
             s = suites[sname]
             for case in s["cases"]:
                 if case["kind"] == "cbd":
-                    continue
+                    continue  # TestCBD (goldens.json's 3D CBD n_it is stale)
                 grid = ie.build_grid(case["dim"], case["n"])
                 op = ie.build_operator(grid)
                 mv = ie.ToeplitzMatvec(op)
@@ -597,3 +597,45 @@ class TestProperties:
         assert rep.converged == orep.converged and abs(rep.n_it - orep.n_it) <= 2
         if rep.converged:
             assert rel(u, ou) <= 1e-9
+
+
+def _cbd_meta():
+    with open(os.path.join(GOLDEN, "ref_cbd.json")) as fh:
+        return json.load(fh)
+
+
+class TestCBD:
+    """CBD preconditioners (one dense block per parity colour, 25..3375
+    points: the large ones run the blocked sweep inversion on FP64 tensor
+    cores) against the reference run itself (ref_cbd.*)."""
+
+    @pytest.mark.parametrize("key", ["2d_n16_m4", "2d_n32_m8", "2d_n64_m16", "3d_n8_m4", "3d_n16_m8"])
+    def test_apply_and_solve(self, ie, key):
+        g = dict(np.load(os.path.join(GOLDEN, "ref_cbd.npz")))
+        case = next(c for c in _cbd_meta() if c.get("key") == key and "n_it_ref" in c)
+        grid = ie.build_grid(case["dim"], case["n"])
+        op = ie.build_operator(grid)
+        mv = ie.ToeplitzMatvec(op)
+        pre = ie.from_decomposition(op, ie.build_decomposition(grid, case["m"], case["overlap"], "cbd"))
+        r = np.random.default_rng(7).standard_normal(op.n)
+        assert rel(pre.apply(r), g["z_" + key]) <= 1e-12
+        f, _ = ie.make_rhs(mv, op.n, mode="noise", seed=0)
+        u, rep = ie.solve(mv, pre, f, tol=1e-12)
+        assert rep.converged and abs(rep.n_it - case["n_it_ref"]) <= 1, (rep.n_it, case["n_it_ref"])
+        h = g["hist_" + key]
+        assert rel(rep.residual_history[:10], h[:10]) <= 1e-6
+        assert rel(u, g["u_" + key]) <= 1e-9
+
+    def test_lanczos(self, ie):
+        for case in _cbd_meta():
+            if "lanczos_min" not in case:
+                continue
+            grid = ie.build_grid(case["dim"], case["n"])
+            op = ie.build_operator(grid)
+            pre = ie.from_decomposition(op, ie.build_decomposition(grid, case["m"], case["overlap"], "cbd"))
+            mv = ie.ToeplitzMatvec(op)
+            for which in ("min", "max"):
+                lam = ie.extremal_eigenvalue_lanczos(mv, pre, op.n, which=which)
+                ref = case["lanczos_" + which]
+                assert abs(lam - ref) <= 1e-8 * abs(ref), (case["key"], which, lam, ref)
+                assert abs(lam - case["lambda_" + which]) <= 2e-3

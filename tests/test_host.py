@@ -94,6 +94,12 @@ class TestGeometryMirror:
         d = ie.build_decomposition(ie.build_grid(2, 16), 4, 1, "cbd")
         assert d.n_subdomains == 4
         assert np.array_equal(np.unique(np.concatenate(d.subdomains)), np.arange(256))
+        from oracle import iedd_oracle as O
+        for dim, n, m, w in ((2, 16, 4, 1), (2, 12, 3, 2), (3, 8, 4, 1), (2, 64, 16, 1)):
+            a = ie.build_decomposition(ie.build_grid(dim, n), m, w, "cbd").subdomains
+            b = O.build_decomposition(O.build_grid(dim, n), m, w, "cbd").subdomains
+            assert len(a) == len(b) == 2 ** dim
+            assert all(np.array_equal(x, y) for x, y in zip(a, b))
 
     def test_two_halves(self):
         import paper_2108_12574_b200 as ie

@@ -163,11 +163,11 @@ class TestGoldenVectors:
 
 
 class TestReferenceGoldenSuites:
-    """goldens.json suites on the hot path (jacobi/schwarz rows only)."""
+    """goldens.json suites on the hot path (jacobi / schwarz / cbd rows)."""
 
     @pytest.mark.parametrize("suite,case", [
         (name, c) for name in ("spectrum-2d", "spectrum-3d", "schwarz-scaling-2d")
-        for c in _suites()[name]["cases"] if c["kind"] != "cbd"],   # CBD out of scope (SURVEY 2)
+        for c in _suites()[name]["cases"]],
         ids=lambda x: x if isinstance(x, str) else f"{x['dim']}d_n{x['n']}_m{x['m']}_{x['kind']}")
     def test_spectrum_suites(self, suite, case):
         if case["n"] ** case["dim"] > 1024 and not os.environ.get("IEDD_SLOW"):
@@ -186,7 +186,7 @@ class TestReferenceGoldenSuites:
             s = suites[name]
             for case in s["cases"]:
                 if case["kind"] == "cbd":
-                    continue
+                    continue  # TestCBD: goldens.json's 3D CBD n_it is stale (the reference gives 22/21)
                 grid = O.build_grid(case["dim"], case["n"])
                 op = O.build_operator(grid)
                 mv = O.FFTMatvec(op)
@@ -218,3 +218,44 @@ def test_oracle_vs_live_reference_geometry():
             a = geometry.build_decomposition(geometry.build_grid(dim, n), m, w, kind).subdomains
             b = O.build_decomposition(O.build_grid(dim, n), m, w, kind).subdomains
             assert len(a) == len(b) and all(np.array_equal(x, y) for x, y in zip(a, b))
+
+
+def _cbd_meta():
+    with open(os.path.join(GOLDEN, "ref_cbd.json")) as fh:
+        return json.load(fh)
+
+
+class TestCBD:
+    """Colour-block-diagonal rows (geometry.py:164-176, 227-235) against the
+    reference run itself (tools/gen_goldens.py --only cbd -> ref_cbd.*)."""
+
+    def test_solve_rows(self):
+        g = dict(np.load(os.path.join(GOLDEN, "ref_cbd.npz")))
+        for case in _cbd_meta():
+            if "n_it_ref" not in case or case["n"] ** case["dim"] > 1024:
+                continue
+            grid = O.build_grid(case["dim"], case["n"])
+            op = O.build_operator(grid)
+            mv = O.FFTMatvec(op)
+            pre = O.SchwarzPrecond(op, O.build_decomposition(grid, case["m"], case["overlap"], "cbd"))
+            r = np.random.default_rng(7).standard_normal(op.n)
+            z = g["z_" + case["key"]]
+            assert np.linalg.norm(pre.apply(r) - z) <= 1e-12 * np.linalg.norm(z)
+            f, _ = O.make_rhs(mv, op.n, mode="noise", seed=0)
+            u, rep = O.pcg(mv, pre, f, tol=1e-12)
+            assert rep.converged and rep.n_it == case["n_it_ref"], case
+            assert np.linalg.norm(u - g["u_" + case["key"]]) <= 1e-10 * np.linalg.norm(u)
+
+    def test_stale_golden_rows(self):
+        # the reference's own goldens.json lists n_it 27 for both 3D CBD rows;
+        # the reference computes 22 and 21 (outside its +-2), so parity is
+        # anchored on the reference run, not that number
+        rows = {c["key"]: c for c in _cbd_meta() if "n_it_ref" in c}
+        assert rows["3d_n8_m4"]["n_it"] == 27 and rows["3d_n8_m4"]["n_it_ref"] == 22
+        assert rows["3d_n16_m8"]["n_it_ref"] == 21
+
+    def test_lanczos_rows_vs_suite(self):
+        for case in _cbd_meta():
+            if "lanczos_min" in case:
+                assert abs(case["lanczos_min"] - case["lambda_min"]) <= 2e-3
+                assert abs(case["lanczos_max"] - case["lambda_max"]) <= 2e-3

@@ -7,6 +7,7 @@ the .npz / .json fixtures this script writes under tests/golden/.
 Usage:
     python tools/gen_goldens.py                 # small + c1..c4 fixtures
     python tools/gen_goldens.py --only c5       # the 9-minute c5 run
+    python tools/gen_goldens.py --only cbd      # CBD rows of goldens.json
 
 Configs follow BASELINE.json / SURVEY.md section 8(d): cell lattice, f from
 default_rng(seed).standard_normal(N), tol 1e-10, u0 = 0.
@@ -183,6 +184,55 @@ def _lanczos(name, kinds, whiches, max_iters):
     return res
 
 
+def gen_cbd(out):
+    """CBD (colour-block-diagonal) rows of goldens.json run through the
+    reference itself (cli.py:266-283 solve path; spectrum.py Lanczos with
+    share_mirrored_subdomains as cli.py:249-263).  goldens.json's 3D CBD n_it
+    (27) is stale: the reference computes 22 / 21, recorded here."""
+    geometry, kernel, pcg, precond, spectrum, toeplitz = _ref()
+    suites = json.load(open(os.path.join(out, "ref_goldens.json")))
+    res, meta = {}, []
+    for sname in ("iterations-2d", "iterations-3d"):
+        s = suites[sname]
+        for case in s["cases"]:
+            if case["kind"] != "cbd":
+                continue
+            g = geometry.build_grid(case["dim"], case["n"])
+            op = kernel.build_operator(g)
+            mv = toeplitz.ToeplitzMatvec(op)
+            dec = geometry.build_decomposition(g, case["m"], case["overlap"], "cbd")
+            pre = precond.from_decomposition(op, dec, backend="exact", dense_limit=op.n)
+            f, _ = pcg.make_rhs(mv, op.n, mode=s["rhs"], seed=s["seed"])
+            u, rep = pcg.solve(mv, pre, f, tol=s["tol"])
+            key = f"{case['dim']}d_n{case['n']}_m{case['m']}"
+            r = np.random.default_rng(7).standard_normal(op.n)
+            res[f"z_{key}"] = pre.apply(r)
+            res[f"u_{key}"] = u
+            res[f"hist_{key}"] = np.array(rep.residual_history)
+            meta.append(dict(case, n_it_ref=rep.n_it, converged=bool(rep.converged), key=key))
+            print("cbd solve", key, rep.n_it, flush=True)
+    for sname in ("spectrum-2d", "spectrum-3d"):
+        for case in suites[sname]["cases"]:
+            if case["kind"] != "cbd":
+                continue
+            g = geometry.build_grid(case["dim"], case["n"])
+            op = kernel.build_operator(g)
+            dec = geometry.build_decomposition(g, case["m"], case["overlap"], "cbd")
+            pre = precond.from_decomposition(op, dec, backend="exact", dense_limit=op.n,
+                                             share_mirrored_subdomains=True)
+            key = f"{case['dim']}d_n{case['n']}_m{case['m']}"
+            lam = {}
+            for which in ("min", "max"):
+                mvc = _Counted(toeplitz.ToeplitzMatvec(op))
+                lam[which] = (spectrum.extremal_eigenvalue_lanczos(mvc, pre, op.n, which=which), mvc.calls)
+            meta.append(dict(case, suite=sname, key=key, lanczos_min=lam["min"][0], steps_min=lam["min"][1],
+                             lanczos_max=lam["max"][0], steps_max=lam["max"][1]))
+            print("cbd lanczos", key, lam, flush=True)
+    np.savez_compressed(os.path.join(out, "ref_cbd.npz"), **res)
+    with open(os.path.join(out, "ref_cbd.json"), "w") as fh:
+        json.dump(meta, fh, indent=1)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", default=None)
@@ -204,6 +254,8 @@ def main():
             res = _pcg_config("c4")
             res.update(_lanczos("c4", ("schwarz",), ("min",), 200))
             np.savez_compressed(os.path.join(OUT, "ref_c4.npz"), **res)
+        elif item == "cbd":
+            gen_cbd(OUT)
         elif item == "c5":
             np.savez_compressed(os.path.join(OUT, "ref_c5.npz"),
                                 **_pcg_config("c5", max_iters=50, store_u="f32"))
