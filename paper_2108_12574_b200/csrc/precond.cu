@@ -537,39 +537,93 @@ __global__ void k_expand_full(const double* fac, const int64_t* fofs, const int*
     }
 }
 
-// Blocks larger than 1024 points (reference dense_limit allows 4096): one
-// CTA per block, r_k and z_k in shared memory, two passes over the packed
-// columns -- dot part (column j -> z_j, warp-exclusive) then axpy part
-// (row tile -> z_i, warp-exclusive).  Reads the factor twice; only the
-// small-D golden geometries use it.
-__global__ void __launch_bounds__(256) k_apply_large(ApplyArgs a) {
+// Large blocks (above 1024 points, up to the reference's dense_limit 4096):
+// the packed upper-by-columns factor is the packed LOWER triangle by rows, so
+// row i = A^{-1}[i][0..i] is contiguous.  CTA (x, block k) streams the rows of
+// chunks x and nch-1-x (kBigRows each, so every CTA has the same work):
+// thread t owns columns j = t + 256q (r_j and the column accumulator in
+// registers) and, per row, adds A[i][j] r_j to the row dot (warp-reduced into
+// smem) and A[i][j] r_i to column j < i.  Each CTA writes its s-long partial
+// (column sums + its rows' dots) to its own slot; k_apply_big_sum adds the
+// slots in ascending order (deterministic, no atomics).  Every factor byte is
+// read once.
+constexpr int kBigRows = 16;  // rows per chunk; a CTA takes chunks c and nch-1-c (balanced)
+constexpr int kBigQ = 16;     // 256 * 16 = 4096 columns
+
+__device__ __forceinline__ int big_chunks(int s) { return (s + kBigRows - 1) / kBigRows; }
+__device__ __forceinline__ int big_slots(int s) { return (big_chunks(s) + 1) / 2; }
+
+__global__ void __launch_bounds__(256) k_apply_big(ApplyArgs a, double* part, const int64_t* pofs) {
     extern __shared__ double sm[];
     if (a.stop && *a.stop) return;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, nw = blockDim.x >> 5;
-    const BlockMeta bm = a.meta[blockIdx.x];
-    const int s = bm.s;
+    const int64_t k = blockIdx.y;
+    const BlockMeta bm = a.meta[k];
+    const int s = bm.s, x = blockIdx.x;
+    if (x >= big_slots(s)) return;
+    const int c1 = x, c2 = big_chunks(s) - 1 - x;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int* idx = a.idx + bm.idx_off;
     const double* fac = a.fac + bm.fac_off;
     double* rs = sm;
-    double* zs = sm + s;
-    for (int i = threadIdx.x; i < s; i += blockDim.x) rs[i] = __ldg(a.r + idx[i]);
+    double* red = sm + s;  // [2 * kBigRows][8]
+    for (int i = tid; i < s; i += blockDim.x) rs[i] = __ldg(a.r + idx[i]);
     __syncthreads();
-    for (int j = warp; j < s; j += nw) {
-        const double* colp = fac + ((int64_t)j * (j + 1)) / 2;
-        double d = 0.0;
-        for (int i = lane; i <= j; i += 32) d = fma(__ldg(colp + i), rs[i], d);
-        d = warp_sum(d);
-        if (lane == 0) zs[j] = d;
+    double rj[kBigQ], acc[kBigQ];
+#pragma unroll
+    for (int q = 0; q < kBigQ; ++q) {
+        const int j = tid + 256 * q;
+        rj[q] = (j < s) ? rs[j] : 0.0;
+        acc[q] = 0.0;
     }
-    __syncthreads();
-    for (int i0 = warp * 32; i0 < s; i0 += nw * 32) {
-        const int i = i0 + lane;
-        double acc = 0.0;
-        for (int j = i0 + 1; j < s; ++j) {
-            if (i < j) acc = fma(__ldg(fac + ((int64_t)j * (j + 1)) / 2 + i), rs[j], acc);
+    for (int rr = 0; rr < 2 * kBigRows; ++rr) {
+        const int i = (rr < kBigRows) ? c1 * kBigRows + rr : c2 * kBigRows + rr - kBigRows;
+        if (i >= s || (rr >= kBigRows && c2 == c1)) continue;
+        const double ri = rs[i];
+        const double* row = fac + (int64_t)i * (i + 1) / 2;
+        double v[kBigQ];
+#pragma unroll
+        for (int q = 0; q < kBigQ; ++q) {
+            const int j = tid + 256 * q;
+            v[q] = (j <= i) ? __ldg(row + j) : 0.0;
         }
-        if (i < s) a.staging[bm.st_off + i] = zs[i] + acc;
+        double d = 0.0;
+#pragma unroll
+        for (int q = 0; q < kBigQ; ++q) {
+            const int j = tid + 256 * q;
+            d = fma(v[q], rj[q], d);
+            if (j < i) acc[q] = fma(v[q], ri, acc[q]);
+        }
+        d = warp_sum(d);
+        if (lane == 0) red[rr * 8 + warp] = d;
     }
+    __syncthreads();
+    double* out = part + pofs[k] + (int64_t)x * s;
+#pragma unroll
+    for (int q = 0; q < kBigQ; ++q) {
+        const int j = tid + 256 * q;
+        if (j < s) {
+            double y = acc[q];
+            const int c = j / kBigRows;
+            if (c == c1 || c == c2) {
+                const double* rd = red + ((c == c1 ? 0 : kBigRows) + j - c * kBigRows) * 8;
+                y += ((rd[0] + rd[1]) + (rd[2] + rd[3])) + ((rd[4] + rd[5]) + (rd[6] + rd[7]));
+            }
+            out[j] = y;
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_apply_big_sum(ApplyArgs a, const double* part, const int64_t* pofs) {
+    if (a.stop && *a.stop) return;
+    const int64_t k = blockIdx.y;
+    const BlockMeta bm = a.meta[k];
+    const int s = bm.s, j = blockIdx.x * 256 + threadIdx.x;
+    if (j >= s) return;
+    const int nch = big_slots(s);
+    const double* p = part + pofs[k] + j;
+    double x = 0.0;
+    for (int c = 0; c < nch; ++c) x += p[(int64_t)c * s];
+    a.staging[bm.st_off + j] = x;
 }
 
 // Forward (G^T y = r, row-axpy form) and back (G x = y, row-dot form)
@@ -943,6 +997,8 @@ struct ie_precond {
     int use_dmma;  // FP64 tensor-core (mma.sync m8n8k4) class GEMM
     int mm;        // fixed-width scatter table width (power of two <= 8), 0: CSR
     int* d_posfix; // [mm][N] staged positions, -1 padded
+    double* d_part = nullptr;      // k_apply_big per-chunk partials
+    int64_t* d_pofs = nullptr;     // per block offset into d_part
 };
 
 namespace ie {
@@ -1068,10 +1124,13 @@ int precond_apply(const ie_precond* p, const double* r, double* z, double* parti
     a.D = p->D;
     a.wpb = p->wpb;
     a.bpc = p->bpc;
-    if (p->T > 32) {
-        const size_t sm = (size_t)2 * p->smax * sizeof(double);
-        if (sm > 48 * 1024) cudaFuncSetAttribute(k_apply_large, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-        k_apply_large<<<(unsigned)p->D, 256, sm, st>>>(a);
+    if (p->d_part) {
+        const size_t sm = (size_t)p->smax * sizeof(double) + 2 * kBigRows * 8 * sizeof(double);
+        if (sm > 48 * 1024) cudaFuncSetAttribute(k_apply_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+        const int slots = ((p->smax + kBigRows - 1) / kBigRows + 1) / 2;
+        k_apply_big<<<dim3(slots, (unsigned)p->D), 256, sm, st>>>(a, p->d_part, p->d_pofs);
+        IE_LAUNCHED();
+        k_apply_big_sum<<<dim3((p->smax + 255) / 256, (unsigned)p->D), 256, 0, st>>>(a, p->d_part, p->d_pofs);
         IE_LAUNCHED();
         return scatter_launch(p, r, z, partials, st, stop);
     }
@@ -1107,6 +1166,8 @@ extern "C" void ie_precond_destroy(ie_precond* p) {
     cudaFree(p->d_members);
     cudaFree(p->d_rg);
     cudaFree(p->d_posfix);
+    cudaFree(p->d_part);
+    cudaFree(p->d_pofs);
     delete p;
 }
 
@@ -1159,7 +1220,7 @@ extern "C" int ie_precond_create(const ie_geom* g, const int64_t* h_offsets, con
             ie::set_error("ie_precond_create: variant 'subst' supports subdomains up to 1024 points");
             return IE_ERR_ARG;
         }
-        T = 64;  // large-block path (k_apply_large)
+        T = 64;  // large-block path (k_apply_big)
     }
     // translation classes: signature = multi-index offsets from the first point
     std::vector<int64_t> rep(D);
@@ -1289,6 +1350,23 @@ extern "C" int ie_precond_create(const ie_geom* g, const int64_t* h_offsets, con
     IE_CHECK_BUILD(cudaMalloc(&p->d_staging, total * sizeof(double)));
     IE_CHECK_BUILD(cudaMalloc(&p->d_ptr, (N + 1) * sizeof(int)));
     IE_CHECK_BUILD(cudaMalloc(&p->d_pos, total * sizeof(int)));
+    {
+        // row-chunked multi-CTA apply for large blocks (required above 1024 points)
+        int big_min = 1024;
+        if (const char* e = getenv("IEDD_B200_BIG_MIN_S")) big_min = atoi(e);
+        if (variant == IE_VARIANT_PACKED_INVERSE && smax > big_min) {
+            std::vector<int64_t> pofs(D);
+            int64_t pn = 0;
+            for (int64_t k = 0; k < D; ++k) {
+                pofs[k] = pn;
+                pn += (int64_t)(((sizes[k] + ie::kBigRows - 1) / ie::kBigRows + 1) / 2) * sizes[k];
+            }
+            IE_CHECK_BUILD(cudaMalloc(&p->d_part, std::max<int64_t>(pn, 1) * sizeof(double)));
+            IE_CHECK_BUILD(cudaMalloc(&p->d_pofs, D * sizeof(int64_t)));
+            IE_CHECK_BUILD(cudaMemcpyAsync(p->d_pofs, pofs.data(), D * sizeof(int64_t), cudaMemcpyHostToDevice, st));
+            IE_CHECK_BUILD(cudaStreamSynchronize(st));
+        }
+    }
     IE_CHECK_BUILD(cudaMemcpyAsync(p->d_meta, meta.data(), D * sizeof(ie::BlockMeta), cudaMemcpyHostToDevice, st));
     IE_CHECK_BUILD(cudaMemcpyAsync(p->d_idx, allidx.data(), total * sizeof(int), cudaMemcpyHostToDevice, st));
     IE_CHECK_BUILD(cudaMemcpyAsync(p->d_ptr, cnt.data(), (N + 1) * sizeof(int), cudaMemcpyHostToDevice, st));

@@ -51,6 +51,24 @@ for name, (dim, n, m, w, seed, kinds) in {"c1": (2, 32, 4, 1, 0, ("schwarz", "ja
             out[f"{name} {kind} pcg [{method}]"] = dict(n_it=rep.n_it, ref_n_it=int(g[f"{kind}_meta"][0]),
                                                        t_s=t, ref_t_pcg_s=ref_t, speedup=ref_t / t,
                                                        t_build_s=t_f, ref_t_f_s=float(g[f"{kind}_times"][0]))
+with open(os.path.join(GOLD, "ref_cbd.json")) as fh:
+    cbd = {c["key"]: c for c in json.load(fh) if "n_it_ref" in c}
+for key in ("2d_n64_m16", "3d_n16_m8"):
+    c = cbd[key]
+    grid = ie.build_grid(c["dim"], c["n"])
+    op = ie.build_operator(grid)
+    mv = ie.ToeplitzMatvec(op)
+    dec = ie.build_decomposition(grid, c["m"], c["overlap"], "cbd")
+    ie.from_decomposition(op, dec)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    pre = ie.from_decomposition(op, dec)
+    torch.cuda.synchronize()
+    t_f = time.perf_counter() - t0
+    f, _ = ie.make_rhs(mv, op.n, mode="noise", seed=0)
+    t, (u, rep) = timed(lambda: ie.solve(mv, pre, f, tol=1e-12))
+    out[f"cbd {key} pcg"] = dict(n_it=rep.n_it, ref_n_it=c["n_it_ref"], t_s=t, ref_t_pcg_s=c["t_pcg_s"],
+                                 t_build_s=t_f, ref_t_f_s=c["t_factor_s"], smax=int(max(s.size for s in dec.subdomains)))
 for name, (dim, n, m, w, kinds, mi) in {"c2": (2, 64, 8, 1, ("schwarz", "jacobi"), 300),
                                         "c4": (3, 32, 4, 1, ("schwarz",), 200)}.items():
     grid = ie.build_grid(dim, n)

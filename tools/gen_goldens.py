@@ -209,7 +209,8 @@ def gen_cbd(out):
             res[f"z_{key}"] = pre.apply(r)
             res[f"u_{key}"] = u
             res[f"hist_{key}"] = np.array(rep.residual_history)
-            meta.append(dict(case, n_it_ref=rep.n_it, converged=bool(rep.converged), key=key))
+            meta.append(dict(case, n_it_ref=rep.n_it, converged=bool(rep.converged), key=key,
+                             t_factor_s=pre.t_factor, t_pcg_s=rep.t_pcg))
             print("cbd solve", key, rep.n_it, flush=True)
     for sname in ("spectrum-2d", "spectrum-3d"):
         for case in suites[sname]["cases"]:
