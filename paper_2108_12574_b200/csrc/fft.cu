@@ -285,7 +285,8 @@ __device__ __forceinline__ void stockham(double* sre, double* sim, int logL, int
             const int tstep = k << (logL - logNs - LR);
 #pragma unroll
             for (int r = 1; r < R; ++r) {
-                const double2 t = logNs == 4 ? t16[r * 16 + k] : tws[r * tstep];
+                // logNs == 8 (the last pass when L > 256): tstep == k, table radix-major
+                const double2 t = logNs == 4 ? t16[r * 16 + k] : tws[(r << 8) + (tstep & 255)];
                 const double ti = S < 0 ? t.y : -t.y;
                 const double xr = vr[b][r];
                 vr[b][r] = fma(xr, t.x, -vi[b][r] * ti);
@@ -335,7 +336,9 @@ __global__ void __launch_bounds__(TPB, 2) k_fft_lines(LineArgs a) {
     constexpr bool fused = MODE == kFusedCC || MODE == kFusedRR;
     double* sre = smd;
     double* sim = smd + SSTR;
-    double2* qt = reinterpret_cast<double2*>(smd + 2 * SSTR);  // full twiddle table exp(-2 pi i m / L)
+    // Ns = 256 pass twiddles, radix-major: qt[r * 256 + k] = exp(-2 pi i r k / L), r < L / 256
+    // (consecutive k on consecutive lanes: conflict-free, unlike tw[r * k])
+    double2* qt = reinterpret_cast<double2*>(smd + 2 * SSTR);
     double2* t16 = qt + a.L;                                    // Ns = 16 pass twiddles
     if (a.stop && *a.stop) return;
     __shared__ double csc[2];
@@ -347,7 +350,7 @@ __global__ void __launch_bounds__(TPB, 2) k_fft_lines(LineArgs a) {
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
             const int r = threadIdx.x + q * TPB;
-            if (r < L) tv[q] = __ldg(a.tw + r);
+            if (r < L) tv[q] = __ldg(a.tw + (logL > 8 ? (r >> 8) * (r & 255) : r));
         }
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
