@@ -256,7 +256,7 @@ __device__ __forceinline__ double2 twiddle(const double2* qt, int m, int logL) {
 // (Through the quarter-wave table, the 16 k-lanes of that pass would hit one bank.)
 template <int R, int S, int TPB>
 __device__ __forceinline__ void stockham(double* sre, double* sim, int logL, int logNs, const double2* tws,
-                                         const double2* t16) {
+                                         const double2* t16, int skw) {
     constexpr int NB = 16 / R;  // 16 points per thread
     constexpr int LR = R == 16 ? 4 : (R == 8 ? 3 : (R == 4 ? 2 : 1));
     const int lpl = logL - LR;  // log2(L / R)
@@ -274,10 +274,10 @@ __device__ __forceinline__ void stockham(double* sre, double* sim, int logL, int
         const int g = bf >> lpl;
         const int j = bf & (pl - 1);
         const int k = j & (Ns - 1);
-        const int base = padi((g << logL) + j);
+        const int base = padi((g << logL) + j) + g * skw;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            const int q = pl >= 16 ? base + r * ld_stride : padi((g << logL) + j + (r << lpl));
+            const int q = pl >= 16 ? base + r * ld_stride : padi((g << logL) + j + (r << lpl)) + g * skw;
             vr[b][r] = sre[q];
             vi[b][r] = sim[q];
         }
@@ -294,7 +294,7 @@ __device__ __forceinline__ void stockham(double* sre, double* sim, int logL, int
             }
         }
         dft_reg<R, S>(vr[b], vi[b]);
-        dst[b] = padi((g << logL) + ((j >> logNs) << (logNs + LR)) + k);
+        dst[b] = padi((g << logL) + ((j >> logNs) << (logNs + LR)) + k) + g * skw;
     }
     __syncthreads();
 #pragma unroll
@@ -309,17 +309,17 @@ __device__ __forceinline__ void stockham(double* sre, double* sim, int logL, int
 }
 
 template <int S, int TPB>
-__device__ void fft_smem(double* sre, double* sim, int logL, const double2* tws, const double2* t16) {
+__device__ void fft_smem(double* sre, double* sim, int logL, const double2* tws, const double2* t16, int skw) {
     int logNs = 0;
     int rem = logL;
     while (rem >= 4) {
-        stockham<16, S, TPB>(sre, sim, logL, logNs, tws, t16);
+        stockham<16, S, TPB>(sre, sim, logL, logNs, tws, t16, skw);
         logNs += 4;
         rem -= 4;
     }
-    if (rem == 3) stockham<8, S, TPB>(sre, sim, logL, logNs, tws, t16);
-    if (rem == 2) stockham<4, S, TPB>(sre, sim, logL, logNs, tws, t16);
-    if (rem == 1) stockham<2, S, TPB>(sre, sim, logL, logNs, tws, t16);
+    if (rem == 3) stockham<8, S, TPB>(sre, sim, logL, logNs, tws, t16, skw);
+    if (rem == 2) stockham<4, S, TPB>(sre, sim, logL, logNs, tws, t16, skw);
+    if (rem == 1) stockham<2, S, TPB>(sre, sim, logL, logNs, tws, t16, skw);
 }
 
 // Pass modes: what a line transform reads, does and writes.
@@ -329,7 +329,7 @@ template <int MODE, int TPB>
 __global__ void __launch_bounds__(TPB, 2) k_fft_lines(LineArgs a) {
     constexpr int PTS = 16 * TPB;  // points per CTA
     constexpr int LOGPTS = TPB == 256 ? 12 : 9;
-    constexpr int SSTR = PTS + PTS / 16;
+    constexpr int SSTR = PTS + PTS / 16 + 16;  // + line skew
     extern __shared__ __align__(16) double smd[];
     constexpr bool in_real = MODE == kFwdRC || MODE == kFusedRR;
     constexpr bool out_real = MODE == kInvCR || MODE == kFusedRR;
@@ -344,32 +344,29 @@ __global__ void __launch_bounds__(TPB, 2) k_fft_lines(LineArgs a) {
     __shared__ double csc[2];
     const int L = a.L;
     const int logL = a.logL;
-    {
-        // twiddle table: all loads of a thread in flight together
-        double2 tv[16];
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-            const int r = threadIdx.x + q * TPB;
-            if (r < L) tv[q] = __ldg(a.tw + (logL > 8 ? (r >> 8) * (r & 255) : r));
-        }
-#pragma unroll
-        for (int q = 0; q < 16; ++q) {
-            const int r = threadIdx.x + q * TPB;
-            if (r < L) qt[r] = tv[q];
-        }
+    // twiddle tables by cp.async (no registers, overlaps the line loads below)
+    for (int r = threadIdx.x; r < L; r += TPB) {
+        const double2* src = a.tw + (logL > 8 ? (r >> 8) * (r & 255) : r);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"((unsigned)__cvta_generic_to_shared(qt + r)),
+                     "l"(src));
     }
     if (logL > 4) {
         // radix of the Ns = 16 pass: 16 if logL >= 8, else 2^(logL-4)
         const int lr2 = logL >= 8 ? 4 : logL - 4;
         for (int e = threadIdx.x; e < (16 << lr2); e += TPB) {
             const int r = e >> 4, k = e & 15;
-            t16[e] = __ldg(a.tw + ((r * k) << (logL - 4 - lr2)));
+            asm volatile("cp.async.ca.shared.global [%0], [%1], 16;\n" ::"r"(
+                             (unsigned)__cvta_generic_to_shared(t16 + e)),
+                         "l"(a.tw + ((r * k) << (logL - 4 - lr2))));
         }
     }
-    if ((in_real && a.scale_in) || (out_real && a.scale_out)) column_scales<TPB>(a, csc);
-    __syncthreads();
+    asm volatile("cp.async.commit_group;\n" ::);
     const int logG = LOGPTS - logL;
     const int G = 1 << logG;
+    // per-line skew of 16/G doubles: in the strided (column) modes a warp's
+    // lanes cover G lines at the same l, whose padded offsets would otherwise
+    // share a bank pair (line pitch L + L/16 == 0 mod 16 words)
+    const int skw = logG <= 4 ? (16 >> logG) : 0;
     const int g0 = blockIdx.x * G;
     const int lgi = a.lg_ninner;
     // load: all 16 points per thread issued before the shared-memory stores
@@ -399,6 +396,9 @@ __global__ void __launch_bounds__(TPB, 2) k_fft_lines(LineArgs a) {
             }
         }
     }
+    if ((in_real && a.scale_in) || (out_real && a.scale_out)) column_scales<TPB>(a, csc);
+    asm volatile("cp.async.wait_group 0;\n" ::);
+    __syncthreads();
 #pragma unroll
     for (int q = 0; q < 16; ++q) {
         const int p = threadIdx.x + q * TPB;
@@ -416,13 +416,13 @@ __global__ void __launch_bounds__(TPB, 2) k_fft_lines(LineArgs a) {
                 v[q].y *= csc[1];
             }
         }
-        const int qi = padi(g * L + l);
+        const int qi = padi(g * L + l) + g * skw;
         sre[qi] = v[q].x;
         sim[qi] = v[q].y;
     }
     __syncthreads();
     if constexpr (fused) {
-        fft_smem<-1, TPB>(sre, sim, logL, qt, t16);
+        fft_smem<-1, TPB>(sre, sim, logL, qt, t16, skw);
         // multiply by the folded real symbol; line (inner index i) enumerates axes 1..dim-1.
         // A thread's 16 points lie on at most 16 lines: per-point line offsets first,
         // then all 16 symbol loads in flight, then the multiplies.
@@ -446,16 +446,17 @@ __global__ void __launch_bounds__(TPB, 2) k_fft_lines(LineArgs a) {
         }
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
-            const int qi = padi(threadIdx.x + q * TPB);
+            const int pp = threadIdx.x + q * TPB;
+            const int qi = padi(pp) + (pp >> logL) * skw;
             sre[qi] *= lam[q];
             sim[qi] *= lam[q];
         }
         __syncthreads();
-        fft_smem<+1, TPB>(sre, sim, logL, qt, t16);
+        fft_smem<+1, TPB>(sre, sim, logL, qt, t16, skw);
     } else if constexpr (MODE == kFwdCC || MODE == kFwdRC) {
-        fft_smem<-1, TPB>(sre, sim, logL, qt, t16);
+        fft_smem<-1, TPB>(sre, sim, logL, qt, t16, skw);
     } else {
-        fft_smem<+1, TPB>(sre, sim, logL, qt, t16);
+        fft_smem<+1, TPB>(sre, sim, logL, qt, t16, skw);
     }
     const bool contig_out = out_real || a.out_sl == 1;
 #pragma unroll 4
@@ -473,7 +474,7 @@ __global__ void __launch_bounds__(TPB, 2) k_fft_lines(LineArgs a) {
         if (line >= a.nlines || l >= a.n_out) continue;
         const int o = line >> lgi, i = line & ((1 << lgi) - 1);
         const int64_t off = (int64_t)o * a.out_so + (int64_t)i * a.out_si + (int64_t)l * a.out_sl;
-        const int qq = padi(g * L + l);
+        const int qq = padi(g * L + l) + g * skw;
         double2 w = make_double2(sre[qq], sim[qq]);
         if constexpr (out_real) {
             if (a.scale_out) {
@@ -546,10 +547,10 @@ static int launch_mode(const LineArgs& a, cudaStream_t st) {
     constexpr int PTS = 16 * TPB;
     const int G = PTS / a.L;
     const int ctas = (a.nlines + G - 1) / G;
-    const size_t smem = 2 * (size_t)(PTS + PTS / 16) * sizeof(double) + (size_t)(a.L + 256) * sizeof(double2);
+    const size_t smem = 2 * (size_t)(PTS + PTS / 16 + 16) * sizeof(double) + (size_t)(a.L + 256) * sizeof(double2);
     static bool attr = false;
     if (!attr) {
-        const size_t smax = 2 * (size_t)(PTS + PTS / 16) * sizeof(double) + (size_t)(PTS + 256) * sizeof(double2);
+        const size_t smax = 2 * (size_t)(PTS + PTS / 16 + 16) * sizeof(double) + (size_t)(PTS + 256) * sizeof(double2);
         IE_CUDA(cudaFuncSetAttribute(k_fft_lines<MODE, TPB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smax));
         attr = true;
     }
