@@ -458,9 +458,31 @@ __global__ void __launch_bounds__(256, 2) k_apply_dmma(GemmArgs a) {
     for (int e = tid; e < kDmmaStages * kGemmKC * AP; e += 256) As[e] = 0.0;
     for (int e = tid; e < kGemmTN * bst; e += 256) Bs[e] = 0.0;
     __syncthreads();
-    for (int e = tid; e < s * kGemmTN; e += 256) {
-        const int jj = e / s, i = e - jj * s;
-        if (colbase[jj] >= 0) cp_async8(Bs + jj * bst + i, a.rg + colbase[jj] + i);
+    if (a.rg) {
+        for (int e = tid; e < s * kGemmTN; e += 256) {
+            const int jj = e / s, i = e - jj * s;
+            if (colbase[jj] >= 0) cp_async8(Bs + jj * bst + i, a.rg + colbase[jj] + i);
+        }
+    } else {
+        // gather straight from r through the block's point indices: four index
+        // loads in flight per thread, then their cp.async copies
+        for (int e0 = tid; e0 < s * kGemmTN; e0 += 4 * 256) {
+            int gi[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int e = e0 + u * 256;
+                const int jj = e / s;
+                gi[u] = (e < s * kGemmTN && colbase[jj] >= 0) ? __ldg(a.idx + colbase[jj] + (e - jj * s)) : -1;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int e = e0 + u * 256;
+                if (gi[u] >= 0) {
+                    const int jj = e / s;
+                    cp_async8(Bs + jj * bst + (e - jj * s), a.r + gi[u]);
+                }
+            }
+        }
     }
     cp_async_commit();
     const int nchunks = (s + kGemmKC - 1) / kGemmKC;
@@ -995,6 +1017,7 @@ struct ie_precond {
     int* d_members;
     double* d_rg;  // r gathered into the staging layout (GEMM path)
     int use_dmma;  // FP64 tensor-core (mma.sync m8n8k4) class GEMM
+    int dmma_pregather = 0;  // IEDD_B200_PREGATHER=1: separate k_gather pass (comparison)
     int mm;        // fixed-width scatter table width (power of two <= 8), 0: CSR
     int* d_posfix; // [mm][N] staged positions, -1 padded
     double* d_part = nullptr;      // k_apply_big per-chunk partials
@@ -1067,11 +1090,15 @@ static void launch_gemm(const ie_precond* p, const GemmArgs& g, cudaStream_t st)
 int precond_apply(const ie_precond* p, const double* r, double* z, double* partials, cudaStream_t st,
                   const int* stop) {
     if (p->gemm_ra) {
-        k_gather<<<(unsigned)((p->total_s + 255) / 256), 256, 0, st>>>(r, p->d_idx, p->d_rg, p->total_s, stop);
-        IE_LAUNCHED();
+        // the DMMA kernel gathers its r columns itself; the FFMA variant reads them pre-gathered
+        const bool pre = !p->use_dmma || p->dmma_pregather;
+        if (pre) {
+            k_gather<<<(unsigned)((p->total_s + 255) / 256), 256, 0, st>>>(r, p->d_idx, p->d_rg, p->total_s, stop);
+            IE_LAUNCHED();
+        }
         GemmArgs g;
         g.r = r;
-        g.rg = p->d_rg;
+        g.rg = pre ? p->d_rg : nullptr;
         g.staging = p->d_staging;
         g.meta = p->d_meta;
         g.idx = p->d_idx;
@@ -1563,6 +1590,7 @@ extern "C" int ie_precond_create(const ie_geom* g, const int64_t* h_offsets, con
         p->gemm_ra = (smax + 15) / 16;
         const char* env = getenv("IEDD_B200_APPLY_GEMM");
         p->use_dmma = !(env && std::string(env) == "dfma");
+        p->dmma_pregather = getenv("IEDD_B200_PREGATHER") ? 1 : 0;
     }
     *out = p;
     return IE_OK;
