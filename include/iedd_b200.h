@@ -79,6 +79,33 @@ int ie_matvec_f64(const ie_matvec* m, const double* d_X, int64_t ldx, int32_t nr
                   double* d_Y, int64_t ldy, int64_t row_begin, int64_t row_end,
                   void* stream);
 
+/* Band (slab) passes of the FFT method for the sharded solver (2D, SURVEY.md
+ * 8(e)); together they are ToeplitzMatvec.matvec (toeplitz.py:39-50) split
+ * across ranks with two all-to-all transposes in between.  Rank g owns grid
+ * rows [row_begin, row_end) (whole rows, point indices); the 2n spectrum
+ * columns are cut into `parts` slabs of Mc = 2n / parts (a power of two).
+ *   band_fwd: X (nrhs columns, ldx, band rows only) -> d_out, complex
+ *             (nrows * 2n), destination-major: slab h at h * nrows * Mc;
+ *   band_cols: d_buf = every grid row of columns [col_begin, col_end),
+ *             row-major (n x ncols complex), in place: forward * symbol * inverse;
+ *   band_inv: d_in (destination-major as band_fwd wrote it, after the reverse
+ *             transpose) -> Y (band rows, ldy, nrhs columns).
+ * With nrhs == 2 the exact power-of-two column scaling of the 2-RHS packing
+ * uses d_amax = the GLOBAL per-2048-chunk partial maxima (2 * namax doubles,
+ * namax = ceil(N / 2048), [2c] = max|x0|, [2c+1] = max|x1|), so every rank
+ * scales identically and the result is bitwise that of ie_matvec_f64. */
+int ie_matvec_band_fwd_f64(const ie_matvec* m, const double* d_X, int64_t ldx, int32_t nrhs,
+                           int64_t row_begin, int64_t row_end, int32_t parts, void* d_out,
+                           const double* d_amax, int64_t namax, void* stream);
+int ie_matvec_band_cols_f64(const ie_matvec* m, void* d_buf, int64_t col_begin, int64_t col_end,
+                            void* stream);
+int ie_matvec_band_inv_f64(const ie_matvec* m, const void* d_in, int64_t row_begin, int64_t row_end,
+                           int32_t parts, double* d_Y, int64_t ldy, int32_t nrhs, const double* d_amax,
+                           int64_t namax, void* stream);
+/* Per-2048-chunk partial maxima of |x0| and |x1| (x1 = x0 + ldx) over n
+ * entries starting at a chunk boundary: d_out[2c], d_out[2c + 1]. */
+int ie_absmax_partials_f64(const double* d_X, int64_t ldx, int64_t n, double* d_out, void* stream);
+
 /* Replaces KernelOperator.assemble_block (kernel.py:170-184):
  * d_out (nr x nc row-major) = A[rows, cols]. */
 int ie_assemble_block_f64(const ie_geom* g, const int64_t* d_rows, int64_t nr,

@@ -43,6 +43,10 @@ _SIGS = {
     "ie_matvec_create_method": (_I32, [ctypes.POINTER(IeGeom), _I32, ctypes.POINTER(_P)]),
     "ie_matvec_destroy": (None, [_P]),
     "ie_matvec_f64": (_I32, [_P, _P, _I64, _I32, _P, _I64, _I64, _I64, _P]),
+    "ie_matvec_band_fwd_f64": (_I32, [_P, _P, _I64, _I32, _I64, _I64, _I32, _P, _P, _I64, _P]),
+    "ie_matvec_band_cols_f64": (_I32, [_P, _P, _I64, _I64, _P]),
+    "ie_matvec_band_inv_f64": (_I32, [_P, _P, _I64, _I64, _I32, _P, _I64, _I32, _P, _I64, _P]),
+    "ie_absmax_partials_f64": (_I32, [_P, _I64, _I64, _P, _P]),
     "ie_assemble_block_f64": (_I32, [ctypes.POINTER(IeGeom), _P, _I64, _P, _I64, _P, _P]),
     "ie_precond_create": (_I32, [ctypes.POINTER(IeGeom), _P, _P, _I64, _I32, _I32, ctypes.POINTER(_P),
                                  ctypes.POINTER(_I64), _P]),

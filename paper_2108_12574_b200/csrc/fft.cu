@@ -41,6 +41,8 @@ struct LineArgs {
     const double* x0;
     const double* x1;
     int64_t in_so, in_si, in_sl;
+    int in_lsplit;   // >= 0: l = (l >> in_lsplit) blocks of stride in_sh (band layouts); -1: none
+    int64_t in_sh;
     int n_in;     // l >= n_in reads as zero
     // destination
     int out_real;
@@ -48,7 +50,10 @@ struct LineArgs {
     double* y0;
     double* y1;
     int64_t out_so, out_si, out_sl;
+    int out_lsplit;
+    int64_t out_sh;
     int n_out;    // only l < n_out is written
+    int line0;    // global index of line 0 along the symbol axis (band column pass)
     int sign;     // -1 forward, +1 inverse (ignored when fused)
     int fused;    // forward, * symbol, inverse
     const double* sym;
@@ -387,7 +392,10 @@ __global__ void __launch_bounds__(TPB, 2) k_fft_lines(LineArgs a) {
         v[q] = make_double2(0.0, 0.0);
         if (line < a.nlines && l < a.n_in) {
             const int o = line >> lgi, i = line & ((1 << lgi) - 1);
-            const int64_t off = (int64_t)o * a.in_so + (int64_t)i * a.in_si + (int64_t)l * a.in_sl;
+            const int64_t off = (int64_t)o * a.in_so + (int64_t)i * a.in_si +
+                                (a.in_lsplit < 0 ? (int64_t)l * a.in_sl
+                                                 : (int64_t)(l >> a.in_lsplit) * a.in_sh +
+                                                       (int64_t)(l & ((1 << a.in_lsplit) - 1)) * a.in_sl);
             if constexpr (in_real) {
                 v[q].x = __ldg(a.x0 + off);
                 if (a.x1) v[q].y = __ldg(a.x1 + off);
@@ -435,7 +443,7 @@ __global__ void __launch_bounds__(TPB, 2) k_fft_lines(LineArgs a) {
             const int p = threadIdx.x + q * TPB;
             const int g = p >> logL, l = p & (L - 1);
             const int line = g0 + g;
-            int tmp = line & ((1 << lgi) - 1), off = 0, stride = 1;
+            int tmp = (line & ((1 << lgi) - 1)) + a.line0, off = 0, stride = 1;
             for (int d = a.dim - 1; d >= 1; --d) {
                 const int k = tmp & (L - 1);
                 tmp >>= logL;
@@ -473,7 +481,10 @@ __global__ void __launch_bounds__(TPB, 2) k_fft_lines(LineArgs a) {
         const int line = g0 + g;
         if (line >= a.nlines || l >= a.n_out) continue;
         const int o = line >> lgi, i = line & ((1 << lgi) - 1);
-        const int64_t off = (int64_t)o * a.out_so + (int64_t)i * a.out_si + (int64_t)l * a.out_sl;
+        const int64_t off = (int64_t)o * a.out_so + (int64_t)i * a.out_si +
+                            (a.out_lsplit < 0 ? (int64_t)l * a.out_sl
+                                              : (int64_t)(l >> a.out_lsplit) * a.out_sh +
+                                                    (int64_t)(l & ((1 << a.out_lsplit) - 1)) * a.out_sl);
         const int qq = padi(g * L + l) + g * skw;
         double2 w = make_double2(sre[qq], sim[qq]);
         if constexpr (out_real) {
@@ -593,6 +604,7 @@ static LineArgs base_args(const ie_fft* f) {
     a.dim = f->dim;
     a.n = f->n;
     a.sign = -1;
+    a.in_lsplit = a.out_lsplit = -1;
     return a;
 }
 
@@ -680,6 +692,115 @@ void fft_destroy(ie_fft* f) {
     cudaFree(f->d_buf);
     cudaFree(f->d_amax);
     delete f;
+}
+
+// ---- 2D band (slab) decomposition of the same three passes, for the sharded
+// solver: rank g owns grid rows [row0, row0 + nrows); the M = 2n spectrum
+// columns are split into `parts` slabs of Mc = M / parts.
+//   band_fwd:  rows of the band, forward along axis 1, written destination-
+//              major: out[(h * nrows + r) * Mc + c_local] (column c = h*Mc + c_local)
+//              -- slab h is one contiguous all-to-all send block;
+//   band_cols: after the all-to-all, buf[r * Mc + c_local] holds every grid row
+//              r of columns [c0, c0 + ncols): fused forward * symbol * inverse;
+//   band_inv:  after the reverse all-to-all, in[(h * nrows + r) * Mc + c_local]:
+//              inverse along axis 1 of the band rows -> real pair.
+// Every line goes through the same kernel with the same data as fft_matvec, so
+// the result is bitwise that of the single-GPU pass for any `parts`.
+static int band_check(const ie_fft* f, int parts) {
+    if (f->dim != 2 || parts < 1 || f->M % parts || ((f->M / parts) & (f->M / parts - 1))) {
+        set_error("fft band passes: 2D operator, parts a power of two dividing 2n");
+        return IE_ERR_ARG;
+    }
+    return IE_OK;
+}
+
+int fft_band_fwd(const ie_fft* f, const double* X0, const double* X1, int nrows, int parts, double2* out,
+                 const double* amax, int namax, cudaStream_t st) {
+    int rc = band_check(f, parts);
+    if (rc) return rc;
+    const int n = f->n, Mc = f->M / parts;
+    int lg = 0;
+    while ((1 << lg) < Mc) ++lg;
+    LineArgs a = base_args(f);
+    a.nlines = nrows;
+    a.ninner = 1;
+    a.in_real = 1;
+    a.x0 = X0;
+    a.x1 = X1;
+    a.in_so = n;
+    a.in_sl = 1;
+    a.n_in = n;
+    a.out_c = out;
+    a.out_so = Mc;
+    a.out_sl = 1;
+    a.out_lsplit = lg;
+    a.out_sh = (int64_t)nrows * Mc;
+    a.n_out = f->M;
+    if (X1) {
+        a.amax = amax;
+        a.namax = namax;
+        a.scale_in = 1;
+    }
+    return line_launch(a, st);
+}
+
+int fft_band_cols(const ie_fft* f, double2* buf, int c0, int ncols, cudaStream_t st) {
+    int rc = band_check(f, 1);
+    if (rc) return rc;
+    if (ncols <= 0 || (ncols & (ncols - 1)) || c0 < 0 || c0 + ncols > f->M) {
+        set_error("fft band_cols: column slab must be a power of two inside [0, 2n)");
+        return IE_ERR_ARG;
+    }
+    LineArgs c = base_args(f);
+    c.nlines = ncols;
+    c.ninner = ncols;
+    c.line0 = c0;
+    c.in_c = buf;
+    c.out_c = buf;
+    c.in_si = c.out_si = 1;
+    c.in_sl = c.out_sl = ncols;
+    c.n_in = f->n;
+    c.n_out = f->n;
+    c.fused = 1;
+    return line_launch(c, st);
+}
+
+int fft_band_inv(const ie_fft* f, const double2* in, int nrows, int parts, double* Y0, double* Y1,
+                 const double* amax, int namax, cudaStream_t st) {
+    int rc = band_check(f, parts);
+    if (rc) return rc;
+    const int n = f->n, Mc = f->M / parts;
+    int lg = 0;
+    while ((1 << lg) < Mc) ++lg;
+    LineArgs e = base_args(f);
+    e.nlines = nrows;
+    e.ninner = 1;
+    e.in_c = in;
+    e.in_so = Mc;
+    e.in_sl = 1;
+    e.in_lsplit = lg;
+    e.in_sh = (int64_t)nrows * Mc;
+    e.n_in = f->M;
+    e.out_real = 1;
+    e.y0 = Y0;
+    e.y1 = Y1;
+    e.out_so = n;
+    e.out_sl = 1;
+    e.n_out = n;
+    e.sign = +1;
+    if (Y1) {
+        e.amax = amax;
+        e.namax = namax;
+        e.scale_out = 1;
+    }
+    return line_launch(e, st);
+}
+
+int fft_absmax2(const double* X0, const double* X1, int64_t N, double* part, cudaStream_t st) {
+    if (N <= 0) return IE_OK;
+    k_absmax2<<<(unsigned)((N + 2047) / 2048), 256, 0, st>>>(X0, X1, (int)N, part, nullptr);
+    IE_LAUNCHED();
+    return IE_OK;
 }
 
 // Y0 (+ i Y1) = A (X0 + i X1) over all N rows.

@@ -220,6 +220,12 @@ int fft_create(const ie_geom& g, ie_fft** out);
 void fft_destroy(ie_fft* f);
 int fft_matvec(const ie_fft* f, const double* X0, const double* X1, double* Y0, double* Y1, cudaStream_t st,
                const int* stop, const double* amax);
+int fft_band_fwd(const ie_fft* f, const double* X0, const double* X1, int nrows, int parts, double2* out,
+                 const double* amax, int namax, cudaStream_t st);
+int fft_band_cols(const ie_fft* f, double2* buf, int c0, int ncols, cudaStream_t st);
+int fft_band_inv(const ie_fft* f, const double2* in, int nrows, int parts, double* Y0, double* Y1,
+                 const double* amax, int namax, cudaStream_t st);
+int fft_absmax2(const double* X0, const double* X1, int64_t N, double* part, cudaStream_t st);
 }  // namespace ie
 
 struct ie_matvec {
@@ -448,6 +454,61 @@ extern "C" int ie_matvec_f64(const ie_matvec* m, const double* X, int64_t ldx, i
         return IE_ERR_ARG;
     }
     return ie::matvec_launch(m, X, ldx, nrhs, Y, ldy, row_begin, row_end, (cudaStream_t)stream, nullptr, nullptr);
+}
+
+// ---- band (slab) passes of the FFT method, for the sharded solver
+static bool band_ok(const ie_matvec* m, int64_t row_begin, int64_t row_end, int32_t parts, int32_t nrhs) {
+    if (!m || m->method != IE_MATVEC_FFT || m->g.dim != 2 || nrhs < 1 || nrhs > 2 || parts < 1 || row_begin < 0 ||
+        row_end > m->N || row_begin > row_end || row_begin % m->g.n || row_end % m->g.n) {
+        ie::set_error("band FFT pass: FFT operator in 2D, whole grid rows, nrhs in {1, 2}");
+        return false;
+    }
+    return true;
+}
+
+extern "C" int ie_matvec_band_fwd_f64(const ie_matvec* m, const double* X, int64_t ldx, int32_t nrhs,
+                                      int64_t row_begin, int64_t row_end, int32_t parts, void* out,
+                                      const double* amax, int64_t namax, void* stream) {
+    if (!band_ok(m, row_begin, row_end, parts, nrhs) || !X || !out || ldx < row_end - row_begin ||
+        (nrhs == 2 && (!amax || namax != (m->N + 2047) / 2048))) {
+        if (m && X && out) ie::set_error("ie_matvec_band_fwd_f64: bad arguments");
+        return IE_ERR_ARG;
+    }
+    const int nrows = (int)((row_end - row_begin) / m->g.n);
+    if (!nrows) return IE_OK;
+    return ie::fft_band_fwd(m->fft, X, nrhs == 2 ? X + ldx : nullptr, nrows, parts, (double2*)out, amax, (int)namax,
+                            (cudaStream_t)stream);
+}
+
+extern "C" int ie_matvec_band_cols_f64(const ie_matvec* m, void* buf, int64_t col_begin, int64_t col_end,
+                                       void* stream) {
+    if (!band_ok(m, 0, 0, 1, 1) || !buf || col_begin < 0 || col_end <= col_begin) {
+        ie::set_error("ie_matvec_band_cols_f64: bad arguments");
+        return IE_ERR_ARG;
+    }
+    return ie::fft_band_cols(m->fft, (double2*)buf, (int)col_begin, (int)(col_end - col_begin), (cudaStream_t)stream);
+}
+
+extern "C" int ie_matvec_band_inv_f64(const ie_matvec* m, const void* in, int64_t row_begin, int64_t row_end,
+                                      int32_t parts, double* Y, int64_t ldy, int32_t nrhs, const double* amax,
+                                      int64_t namax, void* stream) {
+    if (!band_ok(m, row_begin, row_end, parts, nrhs) || !in || !Y || ldy < row_end - row_begin ||
+        (nrhs == 2 && (!amax || namax != (m->N + 2047) / 2048))) {
+        if (m && in && Y) ie::set_error("ie_matvec_band_inv_f64: bad arguments");
+        return IE_ERR_ARG;
+    }
+    const int nrows = (int)((row_end - row_begin) / m->g.n);
+    if (!nrows) return IE_OK;
+    return ie::fft_band_inv(m->fft, (const double2*)in, nrows, parts, Y, nrhs == 2 ? Y + ldy : nullptr, amax,
+                            (int)namax, (cudaStream_t)stream);
+}
+
+extern "C" int ie_absmax_partials_f64(const double* X, int64_t ldx, int64_t n, double* out, void* stream) {
+    if (!X || !out || n < 0 || ldx < n) {
+        ie::set_error("ie_absmax_partials_f64: bad arguments");
+        return IE_ERR_ARG;
+    }
+    return ie::fft_absmax2(X, X + ldx, n, out, (cudaStream_t)stream);
 }
 
 extern "C" int ie_assemble_block_f64(const ie_geom* g, const int64_t* rows, int64_t nr, const int64_t* cols,

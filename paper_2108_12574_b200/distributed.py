@@ -6,10 +6,13 @@ unknowns: the first lattice axis is split at subdomain-row boundaries and the
 cut points are rounded to the dot-product chunk (2048) so that every
 fixed-chunk partial lives on exactly one rank.  Per iteration:
 
-  * all-gather of the iterate columns [p, u] (the fused 2-RHS A-pass needs
-    every source),
-  * the A-pass for the band's rows (K1 rows are summed in the same order for
-    any row range; the FFT method computes all rows and keeps the band),
+  * the fused 2-RHS A-pass [p, u] -> [q, w] for the band's rows:
+      - FFT method, 2D (BandFFT): row FFTs of the band, an all-to-all
+        transpose to column slabs, column FFT * symbol * inverse, the reverse
+        all-to-all, inverse row FFTs -- no rank ever holds the whole iterate;
+      - otherwise (K1 direct sum, 3D FFT): all-gather of [p, u], then the
+        band's rows (K1 rows are summed in the same order for any row range;
+        the replicated FFT computes all rows and keeps the band),
   * all-gather of the fixed-chunk dot partials, reduced on every rank by the
     same device kernel and order as the single-GPU solver,
   * all-gather of r for the apply: each rank applies the subdomains that
@@ -36,6 +39,13 @@ import numpy as np
 CHUNK = 2048
 STAGNATION_WINDOW = 30
 STAGNATION_FACTOR = 1e-3
+
+
+def dist_fft_disabled() -> bool:
+    """IEDD_B200_NO_DIST_FFT=1: replicate the FFT on every rank (all-gather of
+    the iterate) instead of the band decomposition (comparison runs)."""
+    import os
+    return bool(os.environ.get("IEDD_B200_NO_DIST_FFT"))
 
 
 # --------------------------------------------------------------------------
@@ -151,6 +161,18 @@ class Comm:
             pieces.append(outs[r][:, :n])
         return torch.cat(pieces, dim=1)
 
+    def alltoall(self, send, send_counts, recv_counts):
+        """Flat variable-size all-to-all: block h of `send` (send_counts[h]
+        elements, rank order) goes to rank h; the blocks received are
+        concatenated in rank order."""
+        out = send.new_empty(int(sum(recv_counts)))
+        if self.plan.world == 1:
+            out.copy_(send)
+        else:
+            self.dist.all_to_all_single(out, send.contiguous(), [int(c) for c in recv_counts],
+                                        [int(c) for c in send_counts], group=self.group)
+        return out
+
     def allgather_band(self, x):
         """(ncol, band) -> (ncol, N) in global order."""
         return self._gather(x, "band")
@@ -158,6 +180,98 @@ class Comm:
     def allgather_partials(self, x):
         """(ncol, band chunks) -> (ncol, all chunks) in chunk order."""
         return self._gather(x, "chunks")
+
+
+# --------------------------------------------------------------------------
+# distributed FFT matvec (2D): row bands, two all-to-all transposes
+# --------------------------------------------------------------------------
+class BandFFT:
+    """ToeplitzMatvec.matvec (toeplitz.py:39-50) across the rank bands without
+    gathering the iterate.  Rank g holds grid rows [a_g, b_g); the 2n spectrum
+    columns are split into G slabs of Mc = 2n / G.
+
+      1. row FFTs of the band, written destination-major (slab h contiguous);
+      2. all-to-all: rank g receives every grid row of its column slab;
+      3. column FFT * symbol * inverse FFT of the slab;
+      4. reverse all-to-all: rank g receives its rows of every slab;
+      5. inverse row FFTs -> the band of A x.
+
+    With two right-hand sides the exact power-of-two column scaling uses the
+    all-gathered per-chunk maxima, so every rank scales identically.  The
+    per-line arithmetic is that of the single-GPU pass (same kernels, same
+    data), so the result does not depend on G.  Per iteration and rank this
+    moves 2 x 16 * n * (2n) / G bytes instead of all-gathering [p, u]."""
+
+    def __init__(self, stages, plan: ShardPlan, n: int):
+        self.st = stages
+        self.plan = plan
+        self.n = n
+        self.G = plan.world
+        self.M = 2 * n
+        self.Mc = self.M // self.G
+        self.rows = [((plan.bounds[h + 1] - plan.bounds[h]) // n) for h in range(self.G)]
+        self.row0 = sum(self.rows[: plan.rank])
+
+    @staticmethod
+    def supported(grid, plan: ShardPlan) -> bool:
+        n, G = grid.n_per_dim, plan.world
+        M = 2 * n
+        return (grid.dim == 2 and M % G == 0 and (M // G) & (M // G - 1) == 0
+                and all(b % n == 0 for b in plan.bounds))
+
+    def matvec(self, comm, Xb):
+        """Xb: (ncol, band) -> (ncol, band) = rows [begin, end) of A x."""
+        ncol = Xb.shape[0]
+        amax = None
+        if ncol == 2:
+            part = self.st.absmax(Xb)                                    # (nch_band, 2)
+            amax = comm.allgather_partials(part.T.contiguous()).T.contiguous().reshape(-1)
+        g, G, Mc = self.plan.rank, self.G, self.Mc
+        mine = self.rows[g]
+        b1 = self.st.band_fwd(Xb, mine, G, amax)                          # (G, mine, Mc) complex
+        b2 = comm.alltoall(b1, [2 * mine * Mc] * G, [2 * r * Mc for r in self.rows])
+        self.st.band_cols(b2, g * Mc, Mc)                                 # (n, Mc) complex
+        b3 = comm.alltoall(b2, [2 * r * Mc for r in self.rows], [2 * mine * Mc] * G)
+        return self.st.band_inv(b3, mine, G, ncol, amax)
+
+
+class CudaBandStages:
+    """The band passes through the C-ABI (ie_matvec_band_*)."""
+
+    def __init__(self, mv, plan: ShardPlan):
+        import torch
+
+        from . import _lib
+        self.torch, self._lib, self.L = torch, _lib, _lib.lib()
+        self.mv, self.plan = mv, plan
+        self.namax = -(-plan.N // CHUNK)
+
+    def absmax(self, Xb):
+        n = Xb.shape[1]
+        out = self.torch.empty(max(1, -(-n // CHUNK)), 2, dtype=self.torch.float64, device=Xb.device)
+        self._lib.check(self.L.ie_absmax_partials_f64(self._lib.ptr(Xb), Xb.stride(0), n, self._lib.ptr(out),
+                                                      self._lib.stream_ptr()), "absmax")
+        return out[: -(-n // CHUNK)]
+
+    def band_fwd(self, Xb, nrows, parts, amax):
+        out = self.torch.empty(2 * nrows * self.mv.n * 2, dtype=self.torch.float64, device=Xb.device)
+        self._lib.check(self.L.ie_matvec_band_fwd_f64(
+            self.mv.handle, self._lib.ptr(Xb), Xb.stride(0), Xb.shape[0], self.plan.begin, self.plan.end, parts,
+            self._lib.ptr(out), self._lib.ptr(amax) if amax is not None else None, self.namax,
+            self._lib.stream_ptr()), "band_fwd")
+        return out
+
+    def band_cols(self, buf, c0, ncols):
+        self._lib.check(self.L.ie_matvec_band_cols_f64(self.mv.handle, self._lib.ptr(buf), c0, c0 + ncols,
+                                                       self._lib.stream_ptr()), "band_cols")
+
+    def band_inv(self, buf, nrows, parts, ncol, amax):
+        Y = self.torch.empty(ncol, self.plan.size, dtype=self.torch.float64, device=buf.device)
+        self._lib.check(self.L.ie_matvec_band_inv_f64(
+            self.mv.handle, self._lib.ptr(buf), self.plan.begin, self.plan.end, parts, self._lib.ptr(Y),
+            self.plan.size, ncol, self._lib.ptr(amax) if amax is not None else None, self.namax,
+            self._lib.stream_ptr()), "band_inv")
+        return Y
 
 
 # --------------------------------------------------------------------------
@@ -183,6 +297,8 @@ class CudaBackend:
             method = "fft" if fft_supported(op.grid.n_per_dim) else "direct"
         self.mv = KernelMatvec(op, method=method)
         self.method = method
+        self.band = (BandFFT(CudaBandStages(self.mv, plan), plan, op.grid.n_per_dim)
+                     if method == "fft" and BandFFT.supported(op.grid, plan) and not dist_fft_disabled() else None)
         sub = SubDecomposition(decomposition.kind, [decomposition.subdomains[k] for k in plan.blocks],
                                plan.blocks)
         self.pre = (from_decomposition(op, sub, variant=variant, share_translated=share_translated)
@@ -206,6 +322,13 @@ class CudaBackend:
             self.mv.matvec_device(X, Y, nrhs=nrhs, row_begin=self.plan.begin, row_end=self.plan.end,
                                   ldx=self.N, ldy=Y.shape[1])
         return Y[:, : self.plan.size]
+
+    def matvec_cols(self, comm, Xb):
+        """Band columns in, band rows of A x out (distributed FFT, or
+        all-gather + the band rows of the full-range pass)."""
+        if self.band is not None:
+            return self.band.matvec(comm, Xb.contiguous())
+        return self.matvec_band(comm.allgather_band(Xb))
 
     def apply_band(self, r_full):
         if self.pre is None:
@@ -292,8 +415,7 @@ def solve_sharded(backend, comm: Comm, plan: ShardPlan, f_band, tol: float = 1e-
         if not pending and not do_p:
             break
         cols = ([p] if do_p else []) + ([u] if pending else [])
-        X = comm.allgather_band(_stack(cols))
-        Y = backend.matvec_band(X)
+        Y = backend.matvec_cols(comm, _stack(cols))
         q = Y[0] if do_p else None
         w = Y[-1] if pending else None
         parts = []

@@ -6,15 +6,71 @@ import numpy as np
 import torch
 
 from oracle import iedd_oracle as O
-from paper_2108_12574_b200.distributed import CHUNK
+from paper_2108_12574_b200.distributed import CHUNK, BandFFT
+
+
+def _pow2_scale(mx):
+    if not (mx > 0.0) or not np.isfinite(mx):
+        return 1.0
+    return float(np.ldexp(1.0, -int(np.ceil(np.log2(mx)))))
+
+
+class NumpyBandStages:
+    """The four band passes of BandFFT in numpy (pocketfft per line), on the
+    same buffer layouts as the CUDA passes (complex as interleaved float64)."""
+
+    def __init__(self, op, plan):
+        self.plan = plan
+        n = op.grid.n_per_dim
+        self.n, self.M = n, 2 * n
+        emb = np.zeros((self.M, self.M))
+        emb[:n, :n] = op.generator()
+        emb[n + 1:, :] = emb[n - 1:0:-1, :]
+        emb[:, n + 1:] = emb[:, n - 1:0:-1]
+        self.sym = np.fft.fft2(emb).real
+
+    def absmax(self, Xb):
+        x = Xb.numpy()
+        out = [[np.abs(x[0, c:c + CHUNK]).max(), np.abs(x[1, c:c + CHUNK]).max()]
+               for c in range(0, x.shape[1], CHUNK)]
+        return torch.tensor(out, dtype=torch.float64).reshape(-1, 2)
+
+    def _scales(self, amax):
+        a = amax.numpy().reshape(-1, 2)
+        return _pow2_scale(a[:, 0].max()), _pow2_scale(a[:, 1].max())
+
+    def band_fwd(self, Xb, nrows, parts, amax):
+        x = Xb.numpy().reshape(Xb.shape[0], nrows, self.n)
+        z = x[0].astype(complex)
+        if Xb.shape[0] == 2:
+            s0, s1 = self._scales(amax)
+            z = x[0] * s0 + 1j * (x[1] * s1)
+        f = np.fft.fft(z, n=self.M, axis=1)                      # (nrows, M)
+        out = f.reshape(nrows, parts, self.M // parts).transpose(1, 0, 2)
+        return torch.from_numpy(np.ascontiguousarray(out).view(np.float64).reshape(-1).copy())
+
+    def band_cols(self, buf, c0, ncols):
+        b = buf.numpy().view(complex).reshape(self.n, ncols)
+        f = np.fft.fft(b, n=self.M, axis=0) * self.sym[:, c0:c0 + ncols]
+        b[:] = np.fft.ifft(f, axis=0)[: self.n]
+
+    def band_inv(self, buf, nrows, parts, ncol, amax):
+        b = buf.numpy().view(complex).reshape(parts, nrows, self.M // parts).transpose(1, 0, 2)
+        y = np.fft.ifft(b.reshape(nrows, self.M), axis=1)[:, : self.n].reshape(-1)
+        if ncol == 2:
+            s0, s1 = self._scales(amax)
+            return torch.from_numpy(np.stack([y.real / s0, y.imag / s1]))
+        return torch.from_numpy(y.real[None].copy())
 
 
 class OracleBackend:
-    def __init__(self, dim, n, m, w, kind, lattice, plan):
+    def __init__(self, dim, n, m, w, kind, lattice, plan, dist_fft=False):
         self.plan = plan
         grid = O.build_grid(dim, n)
         self.op = O.build_operator(grid, lattice)
         self.mv = O.FFTMatvec(self.op)
+        self.band = (BandFFT(NumpyBandStages(self.op, plan), plan, n)
+                     if dist_fft and BandFFT.supported(grid, plan) else None)
         dec = O.build_decomposition(grid, m, w, kind)
         sub = O.Decomposition(kind, grid, m, w, [dec.subdomains[k] for k in plan.blocks])
         self.pre = O.SchwarzPrecond(self.op, sub) if plan.blocks.size else None
@@ -29,6 +85,11 @@ class OracleBackend:
     def matvec_band(self, X):
         Y = np.stack([self.mv.matvec(X[c].numpy())[self.plan.begin: self.plan.end] for c in range(X.shape[0])])
         return torch.from_numpy(Y)
+
+    def matvec_cols(self, comm, Xb):
+        if self.band is not None:
+            return self.band.matvec(comm, Xb.contiguous())
+        return self.matvec_band(comm.allgather_band(Xb))
 
     def apply_band(self, r_full):
         if self.pre is None:

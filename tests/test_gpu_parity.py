@@ -436,7 +436,8 @@ class TestShardedCuda:
     each virtual rank's band on the same device."""
 
     @pytest.fixture(scope="class")
-    def pg(self):
+    @staticmethod
+    def pg():
         import socket
 
         import torch
@@ -491,6 +492,43 @@ class TestShardedCuda:
             assert torch.equal(torch.cat(ys, dim=1), Yf)
             assert torch.equal(torch.cat(zs), zf)
             assert torch.equal(torch.cat(ps), pf)
+
+
+    @pytest.mark.parametrize("n", [256, 1024])
+    def test_band_fft_virtual_ranks_bitwise(self, ie, n):
+        """The distributed FFT's CUDA passes (ie_matvec_band_*) for G = 2, 4, 8
+        virtual ranks, the all-to-all transposes done by slicing on the one
+        device: bitwise equal to the single-GPU 2-RHS FFT pass."""
+        import torch
+
+        from paper_2108_12574_b200 import distributed as D
+        grid = ie.build_grid(2, n)
+        op = ie.build_operator(grid, lattice="cell")
+        dec = ie.build_decomposition(grid, n // 8, 2, "schwarz")
+        mv = ie.KernelMatvec(op, method="fft")
+        N, M = op.n, 2 * n
+        rng = np.random.default_rng(5)
+        X = torch.from_numpy(np.stack([rng.standard_normal(N), 1e-7 * rng.standard_normal(N)])).cuda()
+        Yf = torch.empty_like(X)
+        mv.matvec_device(X, Yf, nrhs=2)
+        for world in (1, 2, 4, 8):
+            plans = [D.make_plan(grid, dec, world, r) for r in range(world)]
+            assert D.BandFFT.supported(grid, plans[0])
+            st = [D.CudaBandStages(mv, pl) for pl in plans]
+            bands = [X[:, pl.begin:pl.end].contiguous() for pl in plans]
+            amax = torch.cat([s_.absmax(b) for s_, b in zip(st, bands)]).reshape(-1)
+            rows = [(pl.end - pl.begin) // n for pl in plans]
+            Mc = M // world
+            b1 = [s_.band_fwd(b, r, world, amax).view(world, r, Mc, 2) for s_, b, r in zip(st, bands, rows)]
+            b2 = [torch.cat([b1[g][h] for g in range(world)]).contiguous().view(-1) for h in range(world)]
+            for h in range(world):
+                st[h].band_cols(b2[h], h * Mc, Mc)
+            cols = [b.view(n, Mc, 2) for b in b2]
+            r0 = np.cumsum([0] + rows)
+            b3 = [torch.cat([cols[h][r0[g]:r0[g + 1]] for h in range(world)]).contiguous().view(-1)
+                  for g in range(world)]
+            Y = torch.cat([st[g].band_inv(b3[g], rows[g], world, 2, amax) for g in range(world)], dim=1)
+            assert torch.equal(Y, Yf), world
 
 
 class TestEdgeCases:
