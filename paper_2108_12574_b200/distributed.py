@@ -462,6 +462,68 @@ def solve_sharded(backend, comm: Comm, plan: ShardPlan, f_band, tol: float = 1e-
     return full, rep
 
 
+def lanczos_sharded(backend, comm: Comm, plan: ShardPlan, which: str = "min", max_iters: int = 400,
+                    rtol: float = 1e-9, seed: int = 0, return_steps: bool = False):
+    """Extremal eigenvalue of T^{-1}A by Lanczos in the A-inner product
+    (spectrum.py:133-190) on the band decomposition: the basis V and A V are
+    kept as band rows; every inner product is a fixed-chunk partial all-gather
+    summed in global chunk order (so alphas, betas and the Ritz value are
+    identical on every rank and for every G); the full reorthogonalisation is
+    classical Gram-Schmidt applied twice (one partial all-gather per pass for
+    all coefficients), the update w -= c_i v_i applied in ascending i."""
+    import numpy as np
+    from scipy.linalg import eigvalsh_tridiagonal
+
+    if which not in ("min", "max"):
+        raise ValueError(f"which must be 'min' or 'max', got {which!r}")
+
+    def dot(x, y):
+        return backend.sum_partials(comm.allgather_partials(backend.dot_partials(x, y, 0)[None])[0])
+
+    v = backend.tensor(np.random.default_rng(seed).standard_normal(plan.N)[plan.begin: plan.end])
+    av = backend.matvec_cols(comm, v[None])[0]
+    nrm = math.sqrt(dot(v, av))
+    V = [v / nrm]
+    AV = [av / nrm]
+    alphas, betas = [], []
+    estimate = None
+    stable = 0
+    steps = 1
+    for j in range(max_iters):
+        w = backend.apply_band(comm.allgather_band(AV[j][None])[0])
+        alphas.append(dot(w, AV[j]))
+        for _ in range(2):
+            parts = _stack([backend.dot_partials(w, avi, 0) for avi in AV])
+            G = comm.allgather_partials(parts)
+            coef = [backend.sum_partials(G[i]) for i in range(len(AV))]
+            for c, vi in zip(coef, V):
+                backend.update(0, w, vi, -c)
+        aw = backend.matvec_cols(comm, w[None])[0]
+        steps += 1
+        beta2 = dot(w, aw)
+        if beta2 <= 0 or not math.isfinite(beta2):
+            break
+        beta = math.sqrt(beta2)
+        ritz = eigvalsh_tridiagonal(np.array(alphas), np.array(betas))
+        current = float(ritz[0] if which == "min" else ritz[-1])
+        if estimate is not None and abs(current - estimate) <= rtol * max(abs(current), 1.0):
+            stable += 1
+            if stable >= 5:
+                estimate = current
+                break
+        else:
+            stable = 0
+        estimate = current
+        if beta < 1e-14:
+            break
+        betas.append(beta)
+        V.append(w / beta)
+        AV.append(aw / beta)
+    if estimate is None:
+        raise RuntimeError("Lanczos produced no Ritz values")
+    return (estimate, steps) if return_steps else estimate
+
+
 def _stack(cols):
     import torch
     if isinstance(cols[0], torch.Tensor):

@@ -13,7 +13,8 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 from paper_2108_12574_b200 import geometry as G
-from paper_2108_12574_b200.distributed import CHUNK, Comm, band_bounds, blocks_intersecting, make_plan, solve_sharded
+from paper_2108_12574_b200.distributed import (CHUNK, Comm, band_bounds, blocks_intersecting, lanczos_sharded,
+                                               make_plan, solve_sharded)
 
 
 def _free_port():
@@ -44,6 +45,32 @@ def _worker(rank, world, port, out_dir, case):
                  meta=np.array([rep.n_it, rep.converged, rep.stagnated]))
     finally:
         dist.destroy_process_group()
+
+
+def _lz_worker(rank, world, port, out_dir, case):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from tests.dist_cpu_backend import OracleBackend
+        grid = G.build_grid(case["dim"], case["n"])
+        dec = G.build_decomposition(grid, case["m"], case["w"], case["kind"])
+        plan = make_plan(grid, dec, world, rank)
+        be = OracleBackend(case["dim"], case["n"], case["m"], case["w"], case["kind"], case["lattice"], plan,
+                           dist_fft=True)
+        out = []
+        for which in ("min", "max"):
+            lam, steps = lanczos_sharded(be, Comm(plan), plan, which=which, max_iters=case["max_iters"],
+                                         return_steps=True)
+            out += [lam, steps]
+        np.save(os.path.join(out_dir, f"r{rank}.npy"), np.array(out))
+    finally:
+        dist.destroy_process_group()
+
+
+def _run_lz(world, case):
+    with tempfile.TemporaryDirectory() as d:
+        mp.spawn(_lz_worker, args=(world, _free_port(), d, case), nprocs=world, join=True)
+        return [np.load(os.path.join(d, f"r{r}.npy")) for r in range(world)]
 
 
 def _run(world, case):
@@ -148,3 +175,23 @@ class TestShardedSolve:
         res = _run(2, case)
         assert int(res[0]["meta"][0]) == 7 and not res[0]["meta"][1]
         assert np.array_equal(res[0]["hist"], res[1]["hist"]) and len(res[0]["hist"]) == 8
+
+
+class TestShardedLanczos:
+    def test_world_sizes_bitwise_equal_and_oracle_parity(self):
+        """Lanczos (spectrum.py:133-190) on the band decomposition over gloo:
+        lambda_min / lambda_max and step counts identical for G = 1, 2, 4 and
+        within 1e-8 of the oracle's Lanczos."""
+        from oracle import iedd_oracle as O
+        case = dict(dim=2, n=64, m=8, w=1, kind="schwarz", lattice="cell", max_iters=300)
+        res = {w: _run_lz(w, case) for w in (1, 2, 4)}
+        ref = res[1][0]
+        for w in (2, 4):
+            for r in range(w):
+                assert np.array_equal(res[w][r], ref)
+        grid = O.build_grid(2, 64)
+        op = O.build_operator(grid, "cell")
+        pre = O.SchwarzPrecond(op, O.build_decomposition(grid, 8, 1, "schwarz"))
+        for k, which in enumerate(("min", "max")):
+            lam = O.lanczos_extremal(O.FFTMatvec(op), pre, op.n, which=which, max_iters=300)
+            assert abs(ref[2 * k] - lam) <= 1e-8 * abs(lam)

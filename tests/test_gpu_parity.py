@@ -494,6 +494,22 @@ class TestShardedCuda:
             assert torch.equal(torch.cat(ps), pf)
 
 
+    def test_one_rank_lanczos(self, ie, pg, golden):
+        """lanczos_sharded through the CUDA backend (band FFT, NCCL group of
+        one) against the reference's c2 Lambdas."""
+        from paper_2108_12574_b200 import distributed as D
+        g = golden("ref_c2")
+        grid = ie.build_grid(2, 64)
+        op = ie.build_operator(grid, lattice="cell")
+        dec = ie.build_decomposition(grid, 8, 1, "schwarz")
+        plan = D.make_plan(grid, dec, 1, 0)
+        be = D.CudaBackend(op, dec, plan, method="fft")
+        assert be.band is not None
+        for which in ("min", "max"):
+            lam = D.lanczos_sharded(be, D.Comm(plan), plan, which=which, max_iters=300)
+            ref = float(g[f"lam_schwarz_{which}"][0])
+            assert abs(lam - ref) <= 1e-8 * abs(ref)
+
     @pytest.mark.parametrize("n", [256, 1024])
     def test_band_fft_virtual_ranks_bitwise(self, ie, n):
         """The distributed FFT's CUDA passes (ie_matvec_band_*) for G = 2, 4, 8
