@@ -15,10 +15,10 @@ fixed-chunk partial lives on exactly one rank.  Per iteration:
         the replicated FFT computes all rows and keeps the band),
   * all-gather of the fixed-chunk dot partials, reduced on every rank by the
     same device kernel and order as the single-GPU solver,
-  * all-gather of r for the apply: each rank applies the subdomains that
-    intersect its band (neighbours' overlap blocks are recomputed), so the
-    z values of its band are summed in ascending global block id -- the
-    reference's order.
+  * r-halo exchange for the apply (one all-to-all in which only neighbouring
+    bands send): each rank applies the subdomains that intersect its band
+    (neighbours' overlap blocks are recomputed), so the z values of its band
+    are summed in ascending global block id -- the reference's order.
 
 Every scalar and every owned vector entry is therefore bitwise identical for
 any number of ranks, and identical to ie_pcg_f64 on one GPU.
@@ -77,6 +77,7 @@ class ShardPlan:
     N: int
     bounds: tuple
     blocks: np.ndarray = field(repr=False)  # global subdomain ids applied on this rank (ascending)
+    need: tuple = ()  # per rank: [lo, hi) of the points its blocks touch (band + halo)
 
     @property
     def begin(self) -> int:
@@ -107,8 +108,18 @@ def blocks_intersecting(subdomains, begin: int, end: int) -> np.ndarray:
 
 def make_plan(grid, decomposition, world: int, rank: int) -> ShardPlan:
     bounds = band_bounds(grid, getattr(decomposition, "m_per_dim", 1), world)
-    blocks = blocks_intersecting(decomposition.subdomains, bounds[rank], bounds[rank + 1])
-    return ShardPlan(world=world, rank=rank, N=grid.n_points, bounds=bounds, blocks=blocks)
+    subs = decomposition.subdomains
+    lo_k = np.array([int(s[0]) if s.size else 0 for s in subs])     # index sets are sorted
+    hi_k = np.array([int(s[-1]) + 1 if s.size else 0 for s in subs])
+    need, blocks = [], None
+    for g in range(world):
+        bg = blocks_intersecting(subs, bounds[g], bounds[g + 1])
+        if g == rank:
+            blocks = bg
+        lo = min([bounds[g]] + [int(lo_k[k]) for k in bg])
+        hi = max([bounds[g + 1]] + [int(hi_k[k]) for k in bg])
+        need.append((lo, hi))
+    return ShardPlan(world=world, rank=rank, N=grid.n_points, bounds=bounds, blocks=blocks, need=tuple(need))
 
 
 @dataclass(frozen=True)
@@ -171,6 +182,40 @@ class Comm:
         else:
             self.dist.all_to_all_single(out, send.contiguous(), [int(c) for c in recv_counts],
                                         [int(c) for c in send_counts], group=self.group)
+        return out
+
+    def halo(self, x, out):
+        """Band vector x -> out (length N) holding every entry this rank's
+        blocks read: its band plus the halo [need_lo, begin) and [end,
+        need_hi) from the neighbouring bands (one all-to-all; only
+        neighbours exchange non-empty blocks).  Entries outside stay stale."""
+        p = self.plan
+        g = p.rank
+        lo_g, hi_g = p.need[g] if p.need else (0, p.N)
+
+        def inter(a0, a1, b0, b1):
+            return max(a0, b0), min(a1, b1)
+
+        sends, scount, rcount, rpos = [], [], [], []
+        for h in range(p.world):
+            lo_h, hi_h = p.need[h] if p.need else (0, p.N)
+            a, b = inter(p.begin, p.end, lo_h, hi_h)
+            n_s = max(0, b - a) if h != g else 0
+            sends.append(x[a - p.begin: a - p.begin + n_s])
+            scount.append(n_s)
+            a2, b2 = inter(p.bounds[h], p.bounds[h + 1], lo_g, hi_g)
+            n_r = max(0, b2 - a2) if h != g else 0
+            rcount.append(n_r)
+            rpos.append(a2)
+        out[p.begin: p.end] = x
+        if p.world > 1:
+            import torch
+            recv = self.alltoall(torch.cat(sends), scount, rcount)
+            off = 0
+            for h in range(p.world):
+                if rcount[h]:
+                    out[rpos[h]: rpos[h] + rcount[h]] = recv[off: off + rcount[h]]
+                    off += rcount[h]
         return out
 
     def allgather_band(self, x):
@@ -390,11 +435,12 @@ def solve_sharded(backend, comm: Comm, plan: ShardPlan, f_band, tol: float = 1e-
         full = comm.allgather_band(u[None])[0] if gather_solution else u
         return full, ShardedReport(0, 0.0, 0.0, 0.0, [0.0], converged=True)
     t_prec, n_prec = 0.0, 0
+    r_buf = backend.zeros(N)
 
     def apply(r_band):
         nonlocal t_prec, n_prec
         ts = time.perf_counter()
-        r_full = comm.allgather_band(r_band[None])[0]
+        r_full = comm.halo(r_band, r_buf)
         z = backend.apply_band(r_full)
         backend.sync()
         t_prec += time.perf_counter() - ts
@@ -480,6 +526,7 @@ def lanczos_sharded(backend, comm: Comm, plan: ShardPlan, which: str = "min", ma
     def dot(x, y):
         return backend.sum_partials(comm.allgather_partials(backend.dot_partials(x, y, 0)[None])[0])
 
+    r_buf = backend.zeros(plan.N)
     v = backend.tensor(np.random.default_rng(seed).standard_normal(plan.N)[plan.begin: plan.end])
     av = backend.matvec_cols(comm, v[None])[0]
     nrm = math.sqrt(dot(v, av))
@@ -490,7 +537,7 @@ def lanczos_sharded(backend, comm: Comm, plan: ShardPlan, which: str = "min", ma
     stable = 0
     steps = 1
     for j in range(max_iters):
-        w = backend.apply_band(comm.allgather_band(AV[j][None])[0])
+        w = backend.apply_band(comm.halo(AV[j], r_buf))
         alphas.append(dot(w, AV[j]))
         for _ in range(2):
             parts = _stack([backend.dot_partials(w, avi, 0) for avi in AV])
