@@ -16,8 +16,9 @@ only without translation sharing, so the config records l2 "not flushed".
   python bench.py --impl reference [--steps K --warmup W]  # CPU oracle arm
 
 Multi-GPU (torchrun, N > 1): rows and subdomains are sharded by
-paper_2108_12574_b200.distributed (NCCL all-gather of the iterate, fixed-chunk
-dot partials); see DESIGN.md.
+paper_2108_12574_b200.distributed (2D FFT over row bands with two NCCL
+all-to-all transposes, r-halo exchange for the apply, all-gathered fixed-chunk
+dot partials), plus the K1 direct sum on each rank's rows; see DESIGN.md.
 """
 
 from __future__ import annotations
@@ -229,7 +230,7 @@ def run_ours(args):
     if dom == "apply_ms":
         s_sum = sum(s.size for s in dec.subdomains)
         s2 = sum(float(s.size) ** 2 for s in dec.subdomains)
-        roof = {"bound": "fp64-tensor", "kernel": "k_gather + k_apply_dmma (DMMA class GEMM) + k_scatter_fixed",
+        roof = {"bound": "fp64-tensor", "kernel": "k_apply_dmma (DMMA class GEMM, gathers its r columns) + k_scatter_fixed",
                 "achieved": 2.0 * s2 / (apply_ms * 1e-3) / 1e12, "unit": "TFLOP/s", "peak": fp64_peak_tflops,
                 "traffic": None, "note": f"flops = 2 sum_k s_k^2 (Sigma s = {s_sum})"}
     else:
@@ -346,7 +347,7 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-share", action="store_true", help="factorise every block (no translation sharing)")

@@ -639,6 +639,22 @@ def bench_sharded(args, metric, cfg, workload):
         dt = torch.tensor([_t.perf_counter() - w0], device=dev)
         dist.all_reduce(dt, op=dist.ReduceOp.MAX)
         e2e.append(float(dt.item()))
+    # K1 direct sum on this rank's band rows (the north-star kernel matvec:
+    # compute-bound, N^2 / G pairs per rank): aggregate pair-evals/s
+    from .toeplitz import KernelMatvec
+    k1 = KernelMatvec(op, method="direct")
+    Xk = torch.from_numpy(np.random.default_rng(9).standard_normal((2, op.n))).to(dev)
+    Yk = torch.empty(2, max(plan.size, 1), dtype=torch.float64, device=dev)
+    k1.matvec_device(Xk, Yk, nrhs=2, row_begin=plan.begin, row_end=plan.end, ldy=Yk.shape[1])
+    torch.cuda.synchronize()
+    dist.barrier()
+    e0.record(st)
+    k1.matvec_device(Xk, Yk, nrhs=2, row_begin=plan.begin, row_end=plan.end, ldy=Yk.shape[1])
+    e1.record(st)
+    torch.cuda.synchronize()
+    k1_ms = torch.tensor([e0.elapsed_time(e1)], device=dev)
+    dist.all_reduce(k1_ms, op=dist.ReduceOp.MAX)
+    k1_ms = float(k1_ms.item())
     if rank == 0:
         clk = clocks.stop()
         out = {"metric": metric, "value": args.steps / (ms * 1e-3), "unit": "iter/s", "n_gpus": ws,
@@ -654,6 +670,9 @@ def bench_sharded(args, metric, cfg, workload):
                        "d2h_bytes_per_step": 8 * op.n / args.steps,
                        "note": "per solve of K steps: H2D of each rank's f band, D2H of the gathered u"},
                "gpu_launches": launches, "clocks": clk,
+               "kernel_matvec": {"kernel": "k_matvec<2,2,2> on each rank's band rows (sources all-gathered)",
+                                 "pass_ms": k1_ms, "pair_evals_per_s": float(op.n) ** 2 / (k1_ms * 1e-3),
+                                 "note": "max over ranks of one 2-RHS pass; N^2 pairs in total"},
                "roofline": {"bound": "n/a", "note": "see the N=1 line for the kernel rooflines"}}
         print(json.dumps(out))
     return None
