@@ -47,6 +47,12 @@ _SIGS = {
     "ie_matvec_band_cols_f64": (_I32, [_P, _P, _I64, _I64, _P]),
     "ie_matvec_band_inv_f64": (_I32, [_P, _P, _I64, _I64, _I32, _P, _I64, _I32, _P, _I64, _P]),
     "ie_absmax_partials_f64": (_I32, [_P, _I64, _I64, _P, _P]),
+    "ie_comm_id_bytes": (_I64, []),
+    "ie_comm_unique_id": (_I32, [_P]),
+    "ie_comm_create": (_I32, [_P, _I32, _I32, ctypes.POINTER(_P)]),
+    "ie_comm_destroy": (None, [_P]),
+    "ie_pcg_sharded_f64": (_I32, [_P, _P, _P, _P, _P, _P, _P, _D, _I64, _P, ctypes.POINTER(_I64), _P, _P,
+                                  ctypes.POINTER(_I64), ctypes.POINTER(_D), _P]),
     "ie_assemble_block_f64": (_I32, [ctypes.POINTER(IeGeom), _P, _I64, _P, _I64, _P, _P]),
     "ie_precond_create": (_I32, [ctypes.POINTER(IeGeom), _P, _P, _I64, _I32, _I32, ctypes.POINTER(_P),
                                  ctypes.POINTER(_I64), _P]),

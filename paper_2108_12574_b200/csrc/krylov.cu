@@ -14,6 +14,7 @@
 // Dot products: fixed 2048-element chunk partials (in-CTA fixed tree), then a
 // fixed-order reduction -- deterministic and independent of the launch.
 #include <math.h>
+#include <string.h>
 
 #include <stdlib.h>
 
@@ -21,6 +22,8 @@
 #include <mutex>
 #include <string>
 #include <vector>
+
+#include <nccl.h>
 
 #include "common.cuh"
 
@@ -970,5 +973,332 @@ extern "C" int ie_update_f64(int32_t op, double* a, const double* b, double s, i
     if (n == 0) return IE_OK;
     k_update_host<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(op, a, b, s, n);
     IE_LAUNCHED();
+    return IE_OK;
+}
+
+// ------------------------------------------------------- sharded K4 (NCCL) --
+// ie_pcg_f64 on G ranks (one process per GPU), rank g owning the grid-row band
+// [bounds[g], bounds[g+1]) of every vector (distributed.py documents the plan;
+// this is its native driver).  Per iteration, on the rank's stream:
+//   all-gather of the per-chunk max|p|, max|u| (2-RHS scaling) ->
+//   band row FFTs -> all-to-all -> column slab pass -> all-to-all -> inverse
+//   rows (q, w on the band) -> post_pass partials -> all-gather -> k_iter_a
+//   (every rank reduces all chunks in global order: identical scalars) ->
+//   r-halo send/recv -> apply of the rank's subdomains, z on the band ->
+//   all-gather of r.z partials -> k_iter_b.
+// Device-side control as in ie_pcg_f64; the steady-state iteration, NCCL calls
+// included, is one captured CUDA graph.  Every rank takes the same decisions
+// from the same reduced scalars, so the collectives stay matched.
+struct ie_fft;
+struct ie_comm {
+    ncclComm_t c;
+    int nranks, rank;
+};
+
+namespace ie {
+const ie_fft* matvec_fft(const ie_matvec* m);
+int matvec_dim(const ie_matvec* m);
+int matvec_n(const ie_matvec* m);
+int fft_band_fwd(const ie_fft* f, const double* X0, const double* X1, int nrows, int parts, double2* out,
+                 const double* amax, int namax, cudaStream_t st);
+int fft_band_cols(const ie_fft* f, double2* buf, int c0, int ncols, cudaStream_t st);
+int fft_band_inv(const ie_fft* f, const double2* in, int nrows, int parts, double* Y0, double* Y1,
+                 const double* amax, int namax, cudaStream_t st);
+int precond_apply_band(const ie_precond* p, const double* r, double* z, double* partials, int64_t i0, int64_t i1,
+                       cudaStream_t st, const int* stop);
+}  // namespace ie
+
+#define IE_NCCL(call)                                                          \
+    do {                                                                       \
+        ncclResult_t _r = (call);                                              \
+        if (_r != ncclSuccess) {                                               \
+            ie::set_error(std::string("nccl: ") + ncclGetErrorString(_r));     \
+            return IE_ERR_CUDA;                                                \
+        }                                                                      \
+    } while (0)
+
+extern "C" int64_t ie_comm_id_bytes(void) { return (int64_t)sizeof(ncclUniqueId); }
+
+extern "C" int ie_comm_unique_id(void* out) {
+    if (!out) return IE_ERR_ARG;
+    ncclUniqueId id;
+    IE_NCCL(ncclGetUniqueId(&id));
+    memcpy(out, &id, sizeof(id));
+    return IE_OK;
+}
+
+extern "C" int ie_comm_create(const void* id, int32_t nranks, int32_t rank, ie_comm** out) {
+    if (!id || !out || nranks < 1 || rank < 0 || rank >= nranks) {
+        ie::set_error("ie_comm_create: bad arguments");
+        return IE_ERR_ARG;
+    }
+    ncclUniqueId uid;
+    memcpy(&uid, id, sizeof(uid));
+    ie_comm* c = new ie_comm();
+    c->nranks = nranks;
+    c->rank = rank;
+    ncclResult_t r = ncclCommInitRank(&c->c, nranks, uid, rank);
+    if (r != ncclSuccess) {
+        ie::set_error(std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
+        delete c;
+        return IE_ERR_CUDA;
+    }
+    *out = c;
+    return IE_OK;
+}
+
+extern "C" void ie_comm_destroy(ie_comm* c) {
+    if (!c) return;
+    ncclCommDestroy(c->c);
+    delete c;
+}
+
+extern "C" int ie_pcg_sharded_f64(const ie_matvec* A, const ie_precond* T, ie_comm* comm, const int64_t* bounds,
+                                  const int64_t* need, const double* f_band, double* u_band, double tol,
+                                  int64_t max_iters, double* hist, int64_t* n_it, int32_t* flags, double* times,
+                                  int64_t* fail_iter, double* fail_value, void* stream) {
+    using namespace ie;
+    if (!A || !comm || !bounds || !f_band || !u_band || !hist || !n_it || !flags || !times || max_iters < 0 ||
+        !(tol > 0.0 && tol < 1.0)) {
+        set_error("ie_pcg_sharded_f64: bad arguments");
+        return IE_ERR_ARG;
+    }
+    const ie_fft* F = matvec_fft(A);
+    const int G = comm->nranks, g = comm->rank;
+    const int N = matvec_N(A), n = matvec_n(A), M = 2 * n;
+    const int64_t nb = bounds[g + 1] - bounds[g];
+    bool ok = F && matvec_dim(A) == 2 && M % G == 0 && (((M / G) & (M / G - 1)) == 0) && bounds[0] == 0 &&
+              bounds[G] == N;
+    for (int h = 0; h < G && ok; ++h)
+        ok = (bounds[h + 1] - bounds[h] == nb) && (bounds[h] % kChunk == 0) && (bounds[h] % n == 0);
+    if (!ok || nb <= 0 || nb % kChunk) {
+        set_error("ie_pcg_sharded_f64: needs the 2D FFT operator, G | 2n (power-of-two slabs) and equal, "
+                  "chunk-aligned bands of whole grid rows");
+        return IE_ERR_ARG;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    const auto t0 = std::chrono::steady_clock::now();
+    const int64_t b0 = bounds[g];
+    const int nrows = (int)(nb / n), Mc = M / G;
+    const int nchb = (int)(nb / kChunk), nch = nchb * G, c0 = (int)(b0 / kChunk);
+    int64_t cap = 1024;
+    while (cap < max_iters + 1) cap *= 2;
+    // device memory (freed at exit)
+    std::vector<void*> mem;
+    auto dalloc = [&](void** p, size_t bytes) -> int {
+        IE_CUDA(cudaMalloc(p, bytes));
+        mem.push_back(*p);
+        return IE_OK;
+    };
+    struct Free {
+        std::vector<void*>* m;
+        ~Free() {
+            for (void* p : *m) cudaFree(p);
+        }
+    } free_guard{&mem};
+    double *PU, *QW, *rfull, *z, *fb, *part, *amax, *dh;
+    double2 *buf1, *buf2, *buf3;
+    PcgState* S;
+    int rc;
+    if ((rc = dalloc((void**)&PU, 2 * nb * 8)) || (rc = dalloc((void**)&QW, 2 * nb * 8)) ||
+        (rc = dalloc((void**)&rfull, (size_t)N * 8)) || (rc = dalloc((void**)&z, nb * 8)) ||
+        (rc = dalloc((void**)&fb, nb * 8)) || (rc = dalloc((void**)&part, 3 * (size_t)nch * 8)) ||
+        (rc = dalloc((void**)&amax, 2 * (size_t)nch * 8)) || (rc = dalloc((void**)&dh, (size_t)cap * 8)) ||
+        (rc = dalloc((void**)&buf1, (size_t)nrows * M * 16)) || (rc = dalloc((void**)&buf2, (size_t)n * Mc * 16)) ||
+        (rc = dalloc((void**)&buf3, (size_t)nrows * M * 16)) || (rc = dalloc((void**)&S, sizeof(PcgState))))
+        return rc;
+    PcgState* host = nullptr;
+    IE_CUDA(cudaMallocHost(&host, sizeof(PcgState)));
+    struct FreeHost {
+        PcgState* h;
+        ~FreeHost() { cudaFreeHost(h); }
+    } fh{host};
+    double* p = PU;
+    double* uu = PU + nb;
+    double* q = QW;
+    double* w = QW + nb;
+    double* r = rfull + b0;  // r lives inside the halo buffer
+    double* part_pq = part;
+    double* part_res = part + nch;
+    double* part_rz = part + 2 * nch;
+    const int* stop = &S->stop;
+    const ncclComm_t cc = comm->c;
+    // halo plan: send my band's overlap with each rank's need range, receive theirs with mine
+    std::vector<int64_t> s_off(G, 0), s_cnt(G, 0), r_off(G, 0), r_cnt(G, 0);
+    if (need && T) {
+        const int64_t lo = need[2 * g], hi = need[2 * g + 1];
+        for (int h = 0; h < G; ++h) {
+            if (h == g) continue;
+            const int64_t a = std::max(b0, need[2 * h]), b = std::min(bounds[g + 1], need[2 * h + 1]);
+            if (b > a) s_off[h] = a, s_cnt[h] = b - a;
+            const int64_t a2 = std::max(bounds[h], lo), b2 = std::min(bounds[h + 1], hi);
+            if (b2 > a2) r_off[h] = a2, r_cnt[h] = b2 - a2;
+        }
+    } else if (T) {  // no need ranges: the whole vector
+        for (int h = 0; h < G; ++h)
+            if (h != g) s_off[h] = b0, s_cnt[h] = nb, r_off[h] = bounds[h], r_cnt[h] = bounds[h + 1] - bounds[h];
+    }
+    auto allgather_chunks = [&](double* arr, int per, cudaStream_t s) -> int {  // arr[nch * per], rank slab in place
+        IE_NCCL(ncclAllGather(arr + (size_t)c0 * per, arr, (size_t)nchb * per, ncclDouble, cc, s));
+        return IE_OK;
+    };
+    auto alltoall = [&](const double2* src, double2* dst, cudaStream_t s) -> int {  // equal blocks of nrows*Mc
+        const size_t cnt = (size_t)nrows * Mc * 2;
+        IE_NCCL(ncclGroupStart());
+        for (int h = 0; h < G; ++h) {
+            IE_NCCL(ncclSend((const double*)src + h * cnt, cnt, ncclDouble, h, cc, s));
+            IE_NCCL(ncclRecv((double*)dst + h * cnt, cnt, ncclDouble, h, cc, s));
+        }
+        IE_NCCL(ncclGroupEnd());
+        return IE_OK;
+    };
+    auto halo = [&](cudaStream_t s) -> int {
+        bool any = false;
+        for (int h = 0; h < G; ++h) any = any || s_cnt[h] || r_cnt[h];
+        if (!any) return IE_OK;
+        IE_NCCL(ncclGroupStart());
+        for (int h = 0; h < G; ++h) {
+            if (s_cnt[h]) IE_NCCL(ncclSend(rfull + s_off[h], (size_t)s_cnt[h], ncclDouble, h, cc, s));
+            if (r_cnt[h]) IE_NCCL(ncclRecv(rfull + r_off[h], (size_t)r_cnt[h], ncclDouble, h, cc, s));
+        }
+        IE_NCCL(ncclGroupEnd());
+        return IE_OK;
+    };
+    auto matvec = [&](const double* X, int nrhs, double* Y, cudaStream_t s) -> int {
+        int r2;
+        if (nrhs == 2 && (r2 = allgather_chunks(amax, 2, s))) return r2;
+        if ((r2 = fft_band_fwd(F, X, nrhs == 2 ? X + nb : nullptr, nrows, G, buf1, amax, nch, s))) return r2;
+        if ((r2 = alltoall(buf1, buf2, s))) return r2;
+        if ((r2 = fft_band_cols(F, buf2, g * Mc, Mc, s))) return r2;
+        if ((r2 = alltoall(buf2, buf3, s))) return r2;
+        return fft_band_inv(F, buf3, nrows, G, Y, nrhs == 2 ? Y + nb : nullptr, amax, nch, s);
+    };
+    auto apply = [&](cudaStream_t s) -> int {  // z (band) and part_rz (rank slab) from r
+        int r2;
+        if (T) {
+            if ((r2 = halo(s))) return r2;
+            if ((r2 = precond_apply_band(T, rfull, z, part_rz + c0, b0, b0 + nb, s, stop))) return r2;
+        } else {
+            k_copy_if_running<<<g1(nb), 256, 0, s>>>(z, r, (int)nb, stop);
+            IE_LAUNCHED();
+            k_dot_partials<<<nchb, kRed, 0, s>>>(r, z, (int)nb, 0, part_rz + c0);
+            IE_LAUNCHED();
+        }
+        return allgather_chunks(part_rz, 1, s);
+    };
+    // ||f||, init (pcg.py:72-91)
+    IE_CUDA(cudaMemcpyAsync(fb, f_band, nb * 8, cudaMemcpyDeviceToDevice, st));
+    k_dot_partials<<<nchb, kRed, 0, st>>>(fb, fb, (int)nb, 0, part_pq + c0);
+    IE_LAUNCHED();
+    if ((rc = allgather_chunks(part_pq, 1, st))) return rc;
+    k_pcg_init<<<1, kRed, 0, st>>>(part_pq, nch, S, tol, max_iters, dh);
+    IE_LAUNCHED();
+    IE_CUDA(cudaMemsetAsync(uu, 0, nb * 8, st));
+    IE_CUDA(cudaMemsetAsync(amax, 0, 2 * (size_t)nch * 8, st));
+    IE_CUDA(cudaMemcpyAsync(r, fb, nb * 8, cudaMemcpyDeviceToDevice, st));
+    if ((rc = apply(st))) return rc;
+    IE_CUDA(cudaMemcpyAsync(p, z, nb * 8, cudaMemcpyDeviceToDevice, st));
+    k_pcg_rho0<<<1, kRed, 0, st>>>(part_rz, nch, S);
+    IE_LAUNCHED();
+    // (the first 2-RHS pass, iteration 2, uses max|u| from k_iter_a and max|p|
+    // from k_iter_b of iteration 1, as in ie_pcg_f64)
+    auto enqueue_iter = [&](int64_t itarg, int do_p, int pending, bool spec, cudaStream_t s) -> int {
+        int r2;
+        if (do_p && pending) r2 = matvec(PU, 2, QW, s);
+        else if (do_p) r2 = matvec(p, 1, q, s);
+        else r2 = matvec(uu, 1, w, s);
+        if (r2) return r2;
+        k_post_pass<<<nchb, kRed, 0, s>>>(p, q, fb, w, (int)nb, do_p, pending, part_pq + c0, part_res + c0, stop);
+        IE_LAUNCHED();
+        if (do_p && (r2 = allgather_chunks(part_pq, 1, s))) return r2;
+        if (pending && (r2 = allgather_chunks(part_res, 1, s))) return r2;
+        k_iter_a<<<nchb, kRed, 0, s>>>(part_pq, part_res, nch, do_p, pending, itarg, S, dh, uu, r, p, q, (int)nb,
+                                       amax + 2 * (size_t)c0);
+        IE_LAUNCHED();
+        if (spec) {
+            if ((r2 = apply(s))) return r2;
+            k_iter_b<<<nchb, kRed, 0, s>>>(part_rz, nch, itarg, S, p, z, (int)nb, amax + 2 * (size_t)c0);
+            IE_LAUNCHED();
+        }
+        return IE_OK;
+    };
+    const bool use_graph = max_iters >= 3 && !getenv("IEDD_B200_NO_GRAPH");
+    cudaGraphExec_t gexec = nullptr;
+    cudaStream_t cap_s = nullptr;
+    struct GFree {
+        cudaGraphExec_t* e;
+        cudaStream_t* c;
+        ~GFree() {
+            if (*e) cudaGraphExecDestroy(*e);
+            if (*c) cudaStreamDestroy(*c);
+        }
+    } gfree{&gexec, &cap_s};
+    int gnodes = 0;
+    if (use_graph) {
+        IE_CUDA(cudaStreamCreateWithFlags(&cap_s, cudaStreamNonBlocking));
+        // order the capture stream after the setup work on st
+        cudaEvent_t ev;
+        IE_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        IE_CUDA(cudaEventRecord(ev, st));
+        IE_CUDA(cudaStreamWaitEvent(cap_s, ev, 0));
+        cudaEventDestroy(ev);
+        cudaGraph_t gr;
+        IE_CUDA(cudaStreamBeginCapture(cap_s, cudaStreamCaptureModeThreadLocal));
+        int r2 = enqueue_iter(-1, 1, 1, true, cap_s);
+        if (!r2) k_advance_it<<<1, 1, 0, cap_s>>>(S);
+        cudaError_t ce = cudaStreamEndCapture(cap_s, &gr);
+        if (r2) return r2;
+        IE_CUDA(ce);
+        size_t nn = 0;
+        cudaGraphGetNodes(gr, nullptr, &nn);
+        std::vector<cudaGraphNode_t> nodes(nn);
+        if (nn) cudaGraphGetNodes(gr, nodes.data(), &nn);
+        for (auto nd : nodes) {
+            cudaGraphNodeType t;
+            if (cudaGraphNodeGetType(nd, &t) == cudaSuccess && t == cudaGraphNodeTypeKernel) ++gnodes;
+        }
+        ce = cudaGraphInstantiate(&gexec, gr, 0);
+        cudaGraphDestroy(gr);
+        IE_CUDA(ce);
+    }
+    const int64_t kBatch = 4;
+    for (int64_t it = 1; it <= max_iters + 1; ++it) {
+        const int do_p = it <= max_iters;
+        const int pending = it >= 2;
+        const bool spec = do_p && it < max_iters;
+        if (use_graph && pending && spec) {
+            if (it == 2) {
+                k_set_it<<<1, 1, 0, st>>>(S, 2);
+                IE_LAUNCHED();
+            }
+            IE_CUDA(cudaGraphLaunch(gexec, st));
+            g_launches.fetch_add(gnodes, std::memory_order_relaxed);
+        } else if ((rc = enqueue_iter(it, do_p, pending, spec, st))) {
+            return rc;
+        }
+        if (it % kBatch == 0 || it == max_iters + 1) {
+            IE_CUDA(cudaMemcpyAsync(host, S, sizeof(PcgState), cudaMemcpyDeviceToHost, st));
+            IE_CUDA(cudaStreamSynchronize(st));
+            if (host->stop) break;
+        }
+    }
+    IE_CUDA(cudaMemcpyAsync(host, S, sizeof(PcgState), cudaMemcpyDeviceToHost, st));
+    IE_CUDA(cudaStreamSynchronize(st));
+    const PcgState H = *host;
+    flags[0] = H.status == 1;
+    flags[1] = H.status == 2;
+    *n_it = H.n_it;
+    if (H.status == 4 || H.status == 5) {
+        if (fail_iter) *fail_iter = H.fail_iter;
+        if (fail_value) *fail_value = H.fail_value;
+    }
+    IE_CUDA(cudaMemcpyAsync(hist, dh, (size_t)(H.n_it + 1) * 8, cudaMemcpyDeviceToHost, st));
+    IE_CUDA(cudaMemcpyAsync(u_band, uu, nb * 8, cudaMemcpyDeviceToDevice, st));
+    IE_CUDA(cudaStreamSynchronize(st));
+    times[0] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    times[1] = 0.0;
+    if (H.nf == 0.0) times[0] = 0.0;
+    if (H.status == 4) return IE_ERR_BREAKDOWN;
+    if (H.status == 5) return IE_ERR_NONFINITE;
     return IE_OK;
 }

@@ -539,4 +539,7 @@ extern "C" int ie_assemble_block_f64(const ie_geom* g, const int64_t* rows, int6
 namespace ie {
 int matvec_N(const ie_matvec* m) { return m->N; }
 uint64_t matvec_uid(const ie_matvec* m) { return m->uid; }
+const ie_fft* matvec_fft(const ie_matvec* m) { return m->method == IE_MATVEC_FFT ? m->fft : nullptr; }
+int matvec_dim(const ie_matvec* m) { return m->g.dim; }
+int matvec_n(const ie_matvec* m) { return m->g.n; }
 }  // namespace ie

@@ -722,15 +722,17 @@ __global__ void k_gather(const double* r, const int* idx, double* rg, int64_t to
 // (fixed-width position table, -1 padded: one dependent load level less than CSR).
 template <int MM>
 __global__ void __launch_bounds__(256) k_scatter_fixed(const double* staging, const int* pos, double* z, int N,
-                                                       const double* r, double* partials, const int* stop) {
+                                                       const double* r, double* partials, const int* stop, int i0,
+                                                       int i1) {
     if (stop && *stop) return;
     __shared__ double sh[256];
-    const int base = blockIdx.x * kChunk;
+    // points [i0, i1) (chunk-aligned i0; z and the partials are relative to i0)
+    const int base = i0 + blockIdx.x * kChunk;
     double loc = 0.0;
 #pragma unroll 2
     for (int e = 0; e < kChunk / 256; ++e) {
         const int i = base + e * 256 + threadIdx.x;
-        if (i < N) {
+        if (i < i1) {
             int pp[MM];
 #pragma unroll
             for (int q = 0; q < MM; ++q) pp[q] = pos[(int64_t)q * N + i];
@@ -741,7 +743,7 @@ __global__ void __launch_bounds__(256) k_scatter_fixed(const double* staging, co
 #pragma unroll
             for (int q = 0; q < MM; ++q)
                 if (pp[q] >= 0) acc += v[q];
-            z[i] = acc;
+            z[i - i0] = acc;
             if (r) loc = fma(r[i], acc, loc);
         }
     }
@@ -758,18 +760,19 @@ __global__ void __launch_bounds__(256) k_scatter_fixed(const double* staging, co
 // Per point: z_i = sum of its staged contributions in ascending block id.
 // Optionally also the fixed-chunk partials of r.z (for PCG's rho).
 __global__ void __launch_bounds__(256) k_scatter(const double* staging, const int* ptr, const int* pos, double* z,
-                                                 int N, const double* r, double* partials, const int* stop) {
+                                                 int N, const double* r, double* partials, const int* stop, int i0,
+                                                 int i1) {
     if (stop && *stop) return;
     __shared__ double sh[256];
-    const int base = blockIdx.x * kChunk;
+    const int base = i0 + blockIdx.x * kChunk;
     double loc = 0.0;
 #pragma unroll
     for (int e = 0; e < kChunk / 256; ++e) {
         const int i = base + e * 256 + threadIdx.x;
-        if (i < N) {
+        if (i < i1) {
             double acc = 0.0;
             for (int q = ptr[i]; q < ptr[i + 1]; ++q) acc += staging[pos[q]];
-            z[i] = acc;
+            z[i - i0] = acc;
             if (r) loc = fma(r[i], acc, loc);
         }
     }
@@ -1048,16 +1051,22 @@ static void launch_apply_T(const ie_precond* p, ApplyArgs a, cudaStream_t st) {
     }
 }
 
+// output rows of the current apply: [0, N) unless a sharded solver restricts
+// them to its band (precond_apply_band)
+static thread_local int64_t t_i0 = 0, t_i1 = -1;
+
 static int scatter_launch(const ie_precond* p, const double* r, double* z, double* partials, cudaStream_t st,
                           const int* stop) {
-    const int nch = (p->N + kChunk - 1) / kChunk;
+    const int i0 = (int)t_i0, i1 = t_i1 < 0 ? p->N : (int)t_i1;
+    const int nch = (i1 - i0 + kChunk - 1) / kChunk;
+    if (nch <= 0) return IE_OK;
     const double* rr = partials ? r : nullptr;
     switch (p->mm) {
-        case 1: k_scatter_fixed<1><<<nch, 256, 0, st>>>(p->d_staging, p->d_posfix, z, p->N, rr, partials, stop); break;
-        case 2: k_scatter_fixed<2><<<nch, 256, 0, st>>>(p->d_staging, p->d_posfix, z, p->N, rr, partials, stop); break;
-        case 4: k_scatter_fixed<4><<<nch, 256, 0, st>>>(p->d_staging, p->d_posfix, z, p->N, rr, partials, stop); break;
-        case 8: k_scatter_fixed<8><<<nch, 256, 0, st>>>(p->d_staging, p->d_posfix, z, p->N, rr, partials, stop); break;
-        default: k_scatter<<<nch, 256, 0, st>>>(p->d_staging, p->d_ptr, p->d_pos, z, p->N, rr, partials, stop);
+        case 1: k_scatter_fixed<1><<<nch, 256, 0, st>>>(p->d_staging, p->d_posfix, z, p->N, rr, partials, stop, i0, i1); break;
+        case 2: k_scatter_fixed<2><<<nch, 256, 0, st>>>(p->d_staging, p->d_posfix, z, p->N, rr, partials, stop, i0, i1); break;
+        case 4: k_scatter_fixed<4><<<nch, 256, 0, st>>>(p->d_staging, p->d_posfix, z, p->N, rr, partials, stop, i0, i1); break;
+        case 8: k_scatter_fixed<8><<<nch, 256, 0, st>>>(p->d_staging, p->d_posfix, z, p->N, rr, partials, stop, i0, i1); break;
+        default: k_scatter<<<nch, 256, 0, st>>>(p->d_staging, p->d_ptr, p->d_pos, z, p->N, rr, partials, stop, i0, i1);
     }
     IE_LAUNCHED();
     return IE_OK;
@@ -1598,6 +1607,20 @@ extern "C" int ie_precond_create(const ie_geom* g, const int64_t* h_offsets, con
 
 namespace ie {
 uint64_t precond_uid(const ie_precond* p) { return p->uid; }
+}  // namespace ie
+
+// The apply with its output restricted to points [i0, i1) (chunk-aligned i0):
+// z[i - i0] and the r.z partials of those chunks; r is read at global indices.
+namespace ie {
+int precond_apply_band(const ie_precond* p, const double* r, double* z, double* partials, int64_t i0, int64_t i1,
+                       cudaStream_t st, const int* stop) {
+    t_i0 = i0;
+    t_i1 = i1;
+    const int rc = precond_apply(p, r, z, partials, st, stop);
+    t_i0 = 0;
+    t_i1 = -1;
+    return rc;
+}
 }  // namespace ie
 
 extern "C" int ie_precond_apply_f64(const ie_precond* p, const double* r, double* z, void* stream) {

@@ -508,6 +508,79 @@ def solve_sharded(backend, comm: Comm, plan: ShardPlan, f_band, tol: float = 1e-
     return full, rep
 
 
+class NcclComm:
+    """The library's own NCCL communicator over the ranks of the torch
+    process group (the unique id travels by torch.distributed broadcast)."""
+
+    def __init__(self, plan: ShardPlan, group=None):
+        import torch.distributed as dist
+
+        from . import _lib
+        self._lib = _lib
+        L = _lib.lib()
+        nb = int(L.ie_comm_id_bytes())
+        buf = ctypes.create_string_buffer(nb)
+        if plan.rank == 0:
+            _lib.check(L.ie_comm_unique_id(buf), "ie_comm_unique_id")
+        obj = [buf.raw if plan.rank == 0 else None]
+        if plan.world > 1:
+            dist.broadcast_object_list(obj, src=0, group=group)
+        idb = ctypes.create_string_buffer(obj[0], nb)
+        h = ctypes.c_void_p()
+        _lib.check(L.ie_comm_create(idb, plan.world, plan.rank, ctypes.byref(h)), "ie_comm_create")
+        self.handle = h
+
+    def __del__(self):
+        h = getattr(self, "handle", None)
+        if h is not None and h.value:
+            self._lib.lib().ie_comm_destroy(h)
+            self.handle = None
+
+
+def native_supported(backend, plan: ShardPlan) -> bool:
+    """ie_pcg_sharded_f64's domain: the band FFT and equal, chunk-aligned bands."""
+    sizes = {plan.bounds[h + 1] - plan.bounds[h] for h in range(plan.world)}
+    return backend.band is not None and len(sizes) == 1 and all(b % CHUNK == 0 for b in plan.bounds)
+
+
+def solve_sharded_native(backend, ncomm: NcclComm, plan: ShardPlan, f_band, tol: float = 1e-12,
+                         max_iters: int | None = None):
+    """pcg.solve on the band decomposition through the native NCCL driver
+    (ie_pcg_sharded_f64): device-side control, the iteration (collectives
+    included) captured in a CUDA graph.  Returns (u_band, ShardedReport)."""
+    from . import _lib
+    if not 0.0 < tol < 1.0:
+        raise ValueError(f"tol must be in (0, 1), got {tol}")
+    if not native_supported(backend, plan):
+        raise ValueError("native sharded PCG needs the 2D band FFT and equal chunk-aligned bands")
+    if max_iters is None:
+        max_iters = max(2 * plan.N, 100)
+    u = backend.zeros(plan.size)
+    hist = np.zeros(max_iters + 2, dtype=np.float64)
+    n_it = ctypes.c_int64(0)
+    flags = np.zeros(2, dtype=np.int32)
+    times = np.zeros(2, dtype=np.float64)
+    fail_it = ctypes.c_int64(0)
+    fail_val = ctypes.c_double(0.0)
+    bounds = np.ascontiguousarray(plan.bounds, dtype=np.int64)
+    need = np.ascontiguousarray(np.array(plan.need, dtype=np.int64).reshape(-1)) if plan.need else None
+    th = backend.pre.handle if backend.pre is not None else None
+    f_band = f_band.contiguous()
+    rc = _lib.lib().ie_pcg_sharded_f64(
+        backend.mv.handle, th, ncomm.handle, _lib.np_ptr(bounds), _lib.np_ptr(need) if need is not None else None,
+        _lib.ptr(f_band), _lib.ptr(u), tol, max_iters, _lib.np_ptr(hist), ctypes.byref(n_it), _lib.np_ptr(flags),
+        _lib.np_ptr(times), ctypes.byref(fail_it), ctypes.byref(fail_val), _lib.stream_ptr())
+    if rc == _lib.IE_ERR_BREAKDOWN:
+        raise FloatingPointError(f"PCG breakdown at iteration {fail_it.value}: p^T A p = {fail_val.value}")
+    if rc == _lib.IE_ERR_NONFINITE:
+        raise FloatingPointError(f"non-finite residual at iteration {fail_it.value}")
+    _lib.check(rc, "ie_pcg_sharded_f64")
+    k = n_it.value
+    h = [float(x) for x in hist[: k + 1]]
+    return u, ShardedReport(n_it=k, achieved_residual=h[-1], t_pcg=float(times[0]), t_s=float(times[1]),
+                            residual_history=h, stagnated=bool(flags[1]), converged=bool(flags[0]))
+
+
 def lanczos_sharded(backend, comm: Comm, plan: ShardPlan, which: str = "min", max_iters: int = 400,
                     rtol: float = 1e-9, seed: int = 0, return_steps: bool = False):
     """Extremal eigenvalue of T^{-1}A by Lanczos in the A-inner product

@@ -494,6 +494,28 @@ class TestShardedCuda:
             assert torch.equal(torch.cat(ps), pf)
 
 
+    @pytest.mark.parametrize("n,m,w,kind,mi", [(256, 32, 2, "schwarz", None), (128, 16, 0, "jacobi", None),
+                                               (1024, 128, 2, "schwarz", 12)])
+    def test_native_sharded_one_rank_bitwise(self, ie, pg, n, m, w, kind, mi):
+        """ie_pcg_sharded_f64 (band FFT passes, NCCL all-to-all / all-gather /
+        halo, device control, captured graph) as a one-rank group: bitwise
+        equal to ie_pcg_f64."""
+        from paper_2108_12574_b200 import distributed as D
+        grid = ie.build_grid(2, n)
+        op = ie.build_operator(grid, lattice="cell")
+        dec = ie.build_decomposition(grid, m, w, kind)
+        plan = D.make_plan(grid, dec, 1, 0)
+        be = D.CudaBackend(op, dec, plan, method="fft")
+        assert D.native_supported(be, plan)
+        nc = D.NcclComm(plan)
+        f = np.random.default_rng(3).standard_normal(op.n)
+        u_d, rep_d = D.solve_sharded_native(be, nc, plan, be.tensor(f), tol=1e-10, max_iters=mi)
+        pre = ie.from_decomposition(op, dec)
+        u_n, rep_n = ie.solve(ie.KernelMatvec(op, method="fft"), pre, f, tol=1e-10, max_iters=mi)
+        assert rep_d.n_it == rep_n.n_it and rep_d.converged == rep_n.converged
+        assert rep_d.residual_history == rep_n.residual_history
+        assert np.array_equal(u_d.cpu().numpy(), u_n)
+
     def test_one_rank_lanczos(self, ie, pg, golden):
         """lanczos_sharded through the CUDA backend (band FFT, NCCL group of
         one) against the reference's c2 Lambdas."""
