@@ -102,32 +102,6 @@ int ie_matvec_band_cols_f64(const ie_matvec* m, void* d_buf, int64_t col_begin, 
 int ie_matvec_band_inv_f64(const ie_matvec* m, const void* d_in, int64_t row_begin, int64_t row_end,
                            int32_t parts, double* d_Y, int64_t ldy, int32_t nrhs, const double* d_amax,
                            int64_t namax, void* stream);
-/* ------------------------------------------------ sharded K4 (NCCL) ---- */
-typedef struct ie_comm ie_comm;
-
-/* NCCL communicator of the rank group (one process per GPU): rank 0 makes the
- * id (ie_comm_id_bytes() bytes), the host broadcasts it (torch.distributed in
- * distributed.py), every rank calls ie_comm_create. */
-int64_t ie_comm_id_bytes(void);
-int ie_comm_unique_id(void* out);
-int ie_comm_create(const void* id, int32_t nranks, int32_t rank, ie_comm** out);
-void ie_comm_destroy(ie_comm* c);
-
-/* Replaces pcg.solve (pcg.py:54-136) on G ranks: rank g owns points
- * [h_bounds[g], h_bounds[g+1]) of every vector (equal, chunk-aligned bands of
- * whole grid rows; 2D FFT operator with G | 2n).  T_local is the rank's
- * preconditioner (the subdomains intersecting its band, ascending global ids,
- * NULL = identity); h_need[2h], h_need[2h+1] bound the points rank h's blocks
- * read (the r-halo).  Per iteration: band FFT with two all-to-alls, r-halo
- * send/recv, all-gathered fixed-chunk dot partials; device-side control and a
- * captured iteration graph as ie_pcg_f64, whose result it reproduces bitwise
- * for any G.  h_times[1] (mean apply time) is not measured (0). */
-int ie_pcg_sharded_f64(const ie_matvec* A, const ie_precond* T_local, ie_comm* comm,
-                       const int64_t* h_bounds, const int64_t* h_need, const double* d_f_band,
-                       double* d_u_band, double tol, int64_t max_iters, double* h_history,
-                       int64_t* n_it, int32_t* h_flags, double* h_times, int64_t* fail_iter,
-                       double* fail_value, void* stream);
-
 /* Per-2048-chunk partial maxima of |x0| and |x1| (x1 = x0 + ldx) over n
  * entries starting at a chunk boundary: d_out[2c], d_out[2c + 1]. */
 int ie_absmax_partials_f64(const double* d_X, int64_t ldx, int64_t n, double* d_out, void* stream);
@@ -179,6 +153,33 @@ int ie_pcg_f64(const ie_matvec* A, const ie_precond* T, const double* d_f, doubl
                double tol, int64_t max_iters, double* h_history, int64_t* n_it,
                int32_t* h_flags, double* h_times, int64_t* fail_iter, double* fail_value,
                void* stream);
+
+/* ------------------------------------------------ sharded K4 (NCCL) ---- */
+typedef struct ie_comm ie_comm;
+
+/* NCCL communicator of the rank group (one process per GPU): rank 0 makes the
+ * id (ie_comm_id_bytes() bytes), the host broadcasts it (torch.distributed in
+ * distributed.py), every rank calls ie_comm_create. */
+int64_t ie_comm_id_bytes(void);
+int ie_comm_unique_id(void* out);
+int ie_comm_create(const void* id, int32_t nranks, int32_t rank, ie_comm** out);
+void ie_comm_destroy(ie_comm* c);
+
+/* Replaces pcg.solve (pcg.py:54-136) on G ranks: rank g owns points
+ * [h_bounds[g], h_bounds[g+1]) of every vector (equal, chunk-aligned bands of
+ * whole grid rows; 2D FFT operator with G | 2n).  T_local is the rank's
+ * preconditioner (the subdomains intersecting its band, ascending global ids,
+ * NULL = identity); h_need[2h], h_need[2h+1] bound the points rank h's blocks
+ * read (the r-halo).  Per iteration: band FFT with two all-to-alls, r-halo
+ * send/recv, all-gathered fixed-chunk dot partials; device-side control and a
+ * captured iteration graph as ie_pcg_f64, whose result it reproduces bitwise
+ * for any G.  h_times[1] (mean apply time) is not measured (0). */
+int ie_pcg_sharded_f64(const ie_matvec* A, const ie_precond* T_local, ie_comm* comm,
+                       const int64_t* h_bounds, const int64_t* h_need, const double* d_f_band,
+                       double* d_u_band, double tol, int64_t max_iters, double* h_history,
+                       int64_t* n_it, int32_t* h_flags, double* h_times, int64_t* fail_iter,
+                       double* fail_value, void* stream);
+
 
 /* Replaces spectrum.extremal_eigenvalue_lanczos (spectrum.py:133-190):
  * d_v0 = start vector (caller draws it from default_rng(seed), spectrum.py:148),

@@ -990,9 +990,35 @@ extern "C" int ie_update_f64(int32_t op, double* a, const double* b, double s, i
 // included, is one captured CUDA graph.  Every rank takes the same decisions
 // from the same reduced scalars, so the collectives stay matched.
 struct ie_fft;
+namespace ie {
+// Device workspace + captured iteration graph of the sharded driver, cached on
+// the communicator for repeated solves with the same operator / bands.
+struct ShardWork {
+    uint64_t key_a = 0, key_t = 0;
+    int64_t nb = 0, b0 = 0, cap = 0;
+    double *PU = nullptr, *QW = nullptr, *rfull = nullptr, *z = nullptr, *fb = nullptr, *part = nullptr;
+    double *amax = nullptr, *dh = nullptr;
+    double2 *buf1 = nullptr, *buf2 = nullptr, *buf3 = nullptr;
+    PcgState* S = nullptr;
+    PcgState* host = nullptr;
+    cudaGraphExec_t gexec = nullptr;
+    cudaStream_t cap_s = nullptr;
+    int gnodes = 0;
+    ~ShardWork() {
+        for (void* p : {(void*)PU, (void*)QW, (void*)rfull, (void*)z, (void*)fb, (void*)part, (void*)amax,
+                        (void*)dh, (void*)buf1, (void*)buf2, (void*)buf3, (void*)S})
+            if (p) cudaFree(p);
+        if (host) cudaFreeHost(host);
+        if (gexec) cudaGraphExecDestroy(gexec);
+        if (cap_s) cudaStreamDestroy(cap_s);
+    }
+};
+}  // namespace ie
+
 struct ie_comm {
     ncclComm_t c;
     int nranks, rank;
+    ie::ShardWork* work = nullptr;
 };
 
 namespace ie {
@@ -1049,6 +1075,7 @@ extern "C" int ie_comm_create(const void* id, int32_t nranks, int32_t rank, ie_c
 
 extern "C" void ie_comm_destroy(ie_comm* c) {
     if (!c) return;
+    delete c->work;
     ncclCommDestroy(c->c);
     delete c;
 }
@@ -1083,36 +1110,41 @@ extern "C" int ie_pcg_sharded_f64(const ie_matvec* A, const ie_precond* T, ie_co
     const int nchb = (int)(nb / kChunk), nch = nchb * G, c0 = (int)(b0 / kChunk);
     int64_t cap = 1024;
     while (cap < max_iters + 1) cap *= 2;
-    // device memory (freed at exit)
-    std::vector<void*> mem;
-    auto dalloc = [&](void** p, size_t bytes) -> int {
-        IE_CUDA(cudaMalloc(p, bytes));
-        mem.push_back(*p);
-        return IE_OK;
-    };
-    struct Free {
-        std::vector<void*>* m;
-        ~Free() {
-            for (void* p : *m) cudaFree(p);
+    const uint64_t ka = matvec_uid(A), kt = T ? precond_uid(T) : 0;
+    ShardWork* W = comm->work;
+    if (!W || W->key_a != ka || W->key_t != kt || W->nb != nb || W->b0 != b0 || W->cap < cap) {
+        delete W;
+        comm->work = W = new ShardWork();
+        W->key_a = ka;
+        W->key_t = kt;
+        W->nb = nb;
+        W->b0 = b0;
+        W->cap = cap;
+        const bool one = G == 1;  // one rank: the transposes are the identity (buffers aliased)
+        IE_CUDA(cudaMalloc(&W->PU, 2 * nb * 8));
+        IE_CUDA(cudaMalloc(&W->QW, 2 * nb * 8));
+        IE_CUDA(cudaMalloc(&W->rfull, (size_t)N * 8));
+        IE_CUDA(cudaMalloc(&W->z, nb * 8));
+        IE_CUDA(cudaMalloc(&W->fb, nb * 8));
+        IE_CUDA(cudaMalloc(&W->part, 3 * (size_t)nch * 8));
+        IE_CUDA(cudaMalloc(&W->amax, 2 * (size_t)nch * 8));
+        IE_CUDA(cudaMalloc(&W->dh, (size_t)cap * 8));
+        IE_CUDA(cudaMalloc(&W->buf1, (size_t)nrows * M * 16));
+        if (!one) {
+            IE_CUDA(cudaMalloc(&W->buf2, (size_t)n * Mc * 16));
+            IE_CUDA(cudaMalloc(&W->buf3, (size_t)nrows * M * 16));
         }
-    } free_guard{&mem};
-    double *PU, *QW, *rfull, *z, *fb, *part, *amax, *dh;
-    double2 *buf1, *buf2, *buf3;
-    PcgState* S;
+        IE_CUDA(cudaMalloc(&W->S, sizeof(PcgState)));
+        IE_CUDA(cudaMallocHost(&W->host, sizeof(PcgState)));
+    }
     int rc;
-    if ((rc = dalloc((void**)&PU, 2 * nb * 8)) || (rc = dalloc((void**)&QW, 2 * nb * 8)) ||
-        (rc = dalloc((void**)&rfull, (size_t)N * 8)) || (rc = dalloc((void**)&z, nb * 8)) ||
-        (rc = dalloc((void**)&fb, nb * 8)) || (rc = dalloc((void**)&part, 3 * (size_t)nch * 8)) ||
-        (rc = dalloc((void**)&amax, 2 * (size_t)nch * 8)) || (rc = dalloc((void**)&dh, (size_t)cap * 8)) ||
-        (rc = dalloc((void**)&buf1, (size_t)nrows * M * 16)) || (rc = dalloc((void**)&buf2, (size_t)n * Mc * 16)) ||
-        (rc = dalloc((void**)&buf3, (size_t)nrows * M * 16)) || (rc = dalloc((void**)&S, sizeof(PcgState))))
-        return rc;
-    PcgState* host = nullptr;
-    IE_CUDA(cudaMallocHost(&host, sizeof(PcgState)));
-    struct FreeHost {
-        PcgState* h;
-        ~FreeHost() { cudaFreeHost(h); }
-    } fh{host};
+    double *PU = W->PU, *QW = W->QW, *rfull = W->rfull, *z = W->z, *fb = W->fb, *part = W->part;
+    double *amax = W->amax, *dh = W->dh;
+    double2* buf1 = W->buf1;
+    double2* buf2 = G == 1 ? W->buf1 : W->buf2;
+    double2* buf3 = G == 1 ? W->buf1 : W->buf3;
+    PcgState* S = W->S;
+    PcgState* host = W->host;
     double* p = PU;
     double* uu = PU + nb;
     double* q = QW;
@@ -1143,6 +1175,7 @@ extern "C" int ie_pcg_sharded_f64(const ie_matvec* A, const ie_precond* T, ie_co
         return IE_OK;
     };
     auto alltoall = [&](const double2* src, double2* dst, cudaStream_t s) -> int {  // equal blocks of nrows*Mc
+        if (G == 1) return IE_OK;  // identity transpose, aliased buffers
         const size_t cnt = (size_t)nrows * Mc * 2;
         IE_NCCL(ncclGroupStart());
         for (int h = 0; h < G; ++h) {
@@ -1223,19 +1256,9 @@ extern "C" int ie_pcg_sharded_f64(const ie_matvec* A, const ie_precond* T, ie_co
         return IE_OK;
     };
     const bool use_graph = max_iters >= 3 && !getenv("IEDD_B200_NO_GRAPH");
-    cudaGraphExec_t gexec = nullptr;
-    cudaStream_t cap_s = nullptr;
-    struct GFree {
-        cudaGraphExec_t* e;
-        cudaStream_t* c;
-        ~GFree() {
-            if (*e) cudaGraphExecDestroy(*e);
-            if (*c) cudaStreamDestroy(*c);
-        }
-    } gfree{&gexec, &cap_s};
-    int gnodes = 0;
-    if (use_graph) {
-        IE_CUDA(cudaStreamCreateWithFlags(&cap_s, cudaStreamNonBlocking));
+    if (use_graph && !W->gexec) {
+        if (!W->cap_s) IE_CUDA(cudaStreamCreateWithFlags(&W->cap_s, cudaStreamNonBlocking));
+        cudaStream_t cap_s = W->cap_s;
         // order the capture stream after the setup work on st
         cudaEvent_t ev;
         IE_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
@@ -1253,14 +1276,17 @@ extern "C" int ie_pcg_sharded_f64(const ie_matvec* A, const ie_precond* T, ie_co
         cudaGraphGetNodes(gr, nullptr, &nn);
         std::vector<cudaGraphNode_t> nodes(nn);
         if (nn) cudaGraphGetNodes(gr, nodes.data(), &nn);
+        W->gnodes = 0;
         for (auto nd : nodes) {
             cudaGraphNodeType t;
-            if (cudaGraphNodeGetType(nd, &t) == cudaSuccess && t == cudaGraphNodeTypeKernel) ++gnodes;
+            if (cudaGraphNodeGetType(nd, &t) == cudaSuccess && t == cudaGraphNodeTypeKernel) ++W->gnodes;
         }
-        ce = cudaGraphInstantiate(&gexec, gr, 0);
+        ce = cudaGraphInstantiate(&W->gexec, gr, 0);
         cudaGraphDestroy(gr);
         IE_CUDA(ce);
     }
+    cudaGraphExec_t gexec = W->gexec;
+    const int gnodes = W->gnodes;
     const int64_t kBatch = 4;
     for (int64_t it = 1; it <= max_iters + 1; ++it) {
         const int do_p = it <= max_iters;

@@ -677,7 +677,17 @@ def bench_sharded(args, metric, cfg, workload):
     comm = Comm(plan)
     f = np.random.default_rng(cfg["seed"]).standard_normal(op.n)
     f_band = backend.tensor(f[plan.begin: plan.end])
-    solve_sharded(backend, comm, plan, f_band, tol=1e-10, max_iters=max(args.warmup, 1), gather_solution=False)
+    native = native_supported(backend, plan) and not os.environ.get("IEDD_B200_PY_SHARDED")
+    if native:
+        ncomm = NcclComm(plan)
+
+        def run(fb, iters, gather):
+            u, rep = solve_sharded_native(backend, ncomm, plan, fb, tol=1e-10, max_iters=iters)
+            return (comm.allgather_band(u[None])[0] if gather else u), rep
+    else:
+        def run(fb, iters, gather):
+            return solve_sharded(backend, comm, plan, fb, tol=1e-10, max_iters=iters, gather_solution=gather)
+    run(f_band, max(args.warmup, 1), False)
     dev = torch.device("cuda", torch.cuda.current_device())
     st = torch.cuda.current_stream()
     clocks = None
@@ -690,7 +700,7 @@ def bench_sharded(args, metric, cfg, workload):
     n0 = _lib.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st)
-    _, rep = solve_sharded(backend, comm, plan, f_band, tol=1e-10, max_iters=args.steps, gather_solution=False)
+    _, rep = run(f_band, args.steps, False)
     e1.record(st)
     torch.cuda.synchronize()
     dist.barrier()
@@ -707,7 +717,7 @@ def bench_sharded(args, metric, cfg, workload):
         import time as _t
         w0 = _t.perf_counter()
         fb = backend.tensor(f[plan.begin: plan.end])
-        u, _ = solve_sharded(backend, comm, plan, fb, tol=1e-10, max_iters=args.steps, gather_solution=True)
+        u, _ = run(fb, args.steps, True)
         u.cpu()
         dt = torch.tensor([_t.perf_counter() - w0], device=dev)
         dist.all_reduce(dt, op=dist.ReduceOp.MAX)
@@ -735,6 +745,7 @@ def bench_sharded(args, metric, cfg, workload):
                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                "data": "synthetic (BASELINE.json config 5, seeded)",
                "config": {"workload": workload, "N": op.n, "parallelism": f"row/subdomain bands x{ws} (NCCL)",
+                          "driver": "native ie_pcg_sharded_f64" if native else "python solve_sharded",
                           "matvec": backend.method, "bands": list(plan.bounds),
                           "l2": "not flushed"},
                "n_it": rep.n_it,
