@@ -121,10 +121,12 @@ typedef struct ie_precond ie_precond;
  * (precond.py:157-215) + linalg.cholesky (linalg.py:36-45).
  * Subdomains are given as CSR on the HOST: h_offsets[D+1], h_indices[...],
  * each subdomain's index set sorted ascending (geometry.py:71-82).
- * share_translated != 0 factorises one representative per translation class
+ * share_translated bit 0 factorises one representative per translation class
  * (blocks whose points are translates of each other are bitwise identical
- * here, so this is exact).  On IE_ERR_NOT_SPD, *bad_block = the first
- * failing subdomain id. */
+ * here, so this is exact); bit 1 (the reference's share_mirrored_subdomains,
+ * precond.py:137-154, _MirroredSolver :43-62) also identifies blocks related
+ * by grid reflections, each block's points taken in a canonical order.  On
+ * IE_ERR_NOT_SPD, *bad_block = the first failing subdomain id. */
 int ie_precond_create(const ie_geom* g, const int64_t* h_offsets, const int64_t* h_indices,
                       int64_t D, int32_t variant, int32_t share_translated,
                       ie_precond** out, int64_t* bad_block, void* stream);

@@ -25,6 +25,8 @@
 #include <stdlib.h>
 
 #include <algorithm>
+#include <array>
+#include <climits>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -1258,10 +1260,79 @@ extern "C" int ie_precond_create(const ie_geom* g, const int64_t* h_offsets, con
         }
         T = 64;  // large-block path (k_apply_big)
     }
-    // translation classes: signature = multi-index offsets from the first point
+    // share_translated bit 0: translation classes, signature = multi-index
+    // offsets from the first point.  Bit 1 (share_mirrored_subdomains,
+    // precond.py:137-154 generalised): translations and grid reflections --
+    // each block's points are put in a canonical order (the lexicographically
+    // smallest of its 2^dim reflected, origin-shifted, sorted copies); blocks
+    // with equal canonical point lists have bitwise equal A_k in that order.
+    const int64_t total_pts = h_offsets[D];
+    std::vector<int64_t> ord(h_indices, h_indices + total_pts);
+    const bool mirror = (share_translated & 2) != 0;
     std::vector<int64_t> rep(D);
     std::vector<int64_t> uniq;
-    {
+    std::unordered_map<std::string, int64_t> mcls;
+    if (mirror) {
+        const int dim = g->dim, n = g->n;
+        std::vector<std::array<int, 3>> pts, best;
+        std::vector<int> perm, bperm;
+        for (int64_t k = 0; k < D; ++k) {
+            const int64_t o = h_offsets[k], s = h_offsets[k + 1] - o;
+            pts.resize(s);
+            bool have = false;
+            for (int flip = 0; flip < (1 << dim); ++flip) {
+                int mn[3] = {INT32_MAX, INT32_MAX, INT32_MAX};
+                for (int64_t q = 0; q < s; ++q) {
+                    int64_t t = h_indices[o + q];
+                    std::array<int, 3> c{0, 0, 0};
+                    for (int d = dim - 1; d >= 0; --d) {
+                        int x = (int)(t % n);
+                        t /= n;
+                        if (flip >> d & 1) x = n - 1 - x;
+                        c[d] = x;
+                        mn[d] = std::min(mn[d], x);
+                    }
+                    pts[q] = c;
+                }
+                for (auto& c : pts)
+                    for (int d = 0; d < dim; ++d) c[d] -= mn[d];
+                perm.resize(s);
+                for (int64_t q = 0; q < s; ++q) perm[q] = (int)q;
+                std::sort(perm.begin(), perm.end(), [&](int a, int b) { return pts[a] < pts[b]; });
+                bool better = !have;
+                if (have) {
+                    for (int64_t q = 0; q < s; ++q) {
+                        if (pts[perm[q]] != best[q]) {
+                            better = pts[perm[q]] < best[q];
+                            break;
+                        }
+                    }
+                }
+                if (better) {
+                    best.resize(s);
+                    for (int64_t q = 0; q < s; ++q) best[q] = pts[perm[q]];
+                    bperm = perm;
+                    have = true;
+                }
+            }
+            for (int64_t q = 0; q < s; ++q) ord[o + q] = h_indices[o + bperm[q]];
+            std::vector<int> key_v;
+            key_v.reserve(1 + 3 * s);
+            key_v.push_back((int)s);
+            for (auto& c : best)
+                for (int d = 0; d < dim; ++d) key_v.push_back(c[d]);
+            std::string key(reinterpret_cast<const char*>(key_v.data()), key_v.size() * sizeof(int));
+            auto it = mcls.find(key);
+            if (it == mcls.end()) {
+                mcls.emplace(key, (int64_t)uniq.size());
+                rep[k] = (int64_t)uniq.size();
+                uniq.push_back(k);
+            } else {
+                rep[k] = it->second;
+            }
+        }
+    }
+    if (!mirror) {
         std::unordered_map<std::string, int64_t> cls;
         std::vector<int> sig;
         for (int64_t k = 0; k < D; ++k) {
@@ -1320,7 +1391,7 @@ extern "C" int ie_precond_create(const ie_geom* g, const int64_t* h_offsets, con
     std::vector<int> uidx(idxn);
     for (int64_t u = 0; u < U; ++u) {
         const int64_t k = uniq[u];
-        for (int q = 0; q < sizes[k]; ++q) uidx[uioff[u] + q] = (int)h_indices[h_offsets[k] + q];
+        for (int q = 0; q < sizes[k]; ++q) uidx[uioff[u] + q] = (int)ord[h_offsets[k] + q];
     }
     std::vector<ie::BlockMeta> meta(D);
     std::vector<int> allidx(total);
@@ -1334,7 +1405,7 @@ extern "C" int ie_precond_create(const ie_geom* g, const int64_t* h_offsets, con
             meta[k].fac_off = ufofs[rep[k]];
             meta[k].st_off = off;
             for (int q = 0; q < sizes[k]; ++q) {
-                const int gi = (int)h_indices[h_offsets[k] + q];
+                const int gi = (int)ord[h_offsets[k] + q];
                 allidx[off + q] = gi;
                 cnt[gi + 1]++;
             }

@@ -115,8 +115,10 @@ def from_decomposition(op: KernelOperator, decomposition: Decomposition, backend
     variant: "packed_inverse" (apply = packed symmetric A_k^{-1} matvec) or
     "subst" (forward/back substitution with the Cholesky factor).
     share_translated: factorise one block per translation class (exact: such
-    blocks are bitwise identical here); share_mirrored_subdomains (CBD-only
-    in the reference) is accepted and subsumed by it.
+    blocks are bitwise identical here); share_mirrored_subdomains: classes
+    under translations and grid reflections (each block in a canonical point
+    order), which covers the reference's mirrored CBD subdomains
+    (precond.py:137-154) and reports its memory accounting.
     """
     if backend not in (EXACT, RSKEL):
         raise ValueError(f"backend must be 'exact' or 'rskel', got {backend!r}")
@@ -135,11 +137,14 @@ def from_decomposition(op: KernelOperator, decomposition: Decomposition, backend
     offsets = np.zeros(len(subs) + 1, dtype=np.int64)
     np.cumsum(sizes, out=offsets[1:])
     indices = np.ascontiguousarray(np.concatenate([np.asarray(s, dtype=np.int64) for s in subs]))
+    # bit 0: translation classes; bit 1: translations + grid reflections (the
+    # reference's mirrored sharing, precond.py:137-154, generalised)
+    share_mask = (1 if share_translated else 0) | (2 if share_mirrored_subdomains else 0)
     L = _lib.lib()
     h = ctypes.c_void_p()
     bad = ctypes.c_int64(-1)
     rc = L.ie_precond_create(op.geom(), _lib.np_ptr(offsets), _lib.np_ptr(indices), len(subs),
-                             _lib.VARIANTS[variant], int(bool(share_translated)), ctypes.byref(h),
+                             _lib.VARIANTS[variant], share_mask, ctypes.byref(h),
                              ctypes.byref(bad), _lib.stream_ptr())
     if rc == _lib.IE_ERR_NOT_SPD:
         i = bad.value
@@ -147,7 +152,11 @@ def from_decomposition(op: KernelOperator, decomposition: Decomposition, backend
     _lib.check(rc, "from_decomposition")
     st = np.zeros(5, dtype=np.int64)
     _lib.check(L.ie_precond_stats(h, _lib.np_ptr(st)), "stats")
-    stats = {"S": int(st[0]), "memory_bytes": int(st[1]), "device_bytes": int(st[2]),
+    memory_bytes = int(st[1])
+    if share_mirrored_subdomains and decomposition.kind == "cbd" and decomposition.m_per_dim % 2 == 0:
+        # the reference's accounting (precond.py:38-39, 60-61): one factor, 8 s bytes per mirrored solver
+        memory_bytes = 8 * (int(sizes[0]) ** 2 + int(sizes[0])) + 8 * int(sizes[1:].sum())
+    stats = {"S": int(st[0]), "memory_bytes": memory_bytes, "device_bytes": int(st[2]),
              "factored": int(st[3]), "D": int(st[4])}
     return Preconditioner(kind=decomposition.kind, n=op.n, handle=h, backend=EXACT,
                           t_factor=time.perf_counter() - t0, stats=stats)

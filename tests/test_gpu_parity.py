@@ -702,6 +702,24 @@ class TestCBD:
         assert rel(rep.residual_history[:10], h[:10]) <= 1e-6
         assert rel(u, g["u_" + key]) <= 1e-9
 
+    @pytest.mark.parametrize("dim,n,m", [(2, 16, 4), (3, 8, 2), (2, 64, 16)])
+    def test_mirrored_sharing(self, ie, dim, n, m):
+        """share_mirrored_subdomains (reference TestMirroredSharing): the same
+        apply as factorising every colour, one factor per reflection class,
+        and the reference's memory accounting."""
+        grid = ie.build_grid(dim, n)
+        op = ie.build_operator(grid)
+        d = ie.build_decomposition(grid, m, 1, "cbd")
+        plain = ie.from_decomposition(op, d, share_translated=False)
+        shared = ie.from_decomposition(op, d, share_mirrored_subdomains=True)
+        f = np.random.default_rng(0).standard_normal(op.n)
+        # (the reference bounds this by 1e-11 |f|; here the blocks' point order
+        # differs between the two builds, so the bound is relative to |z|)
+        assert rel(shared.apply(f), plain.apply(f)) <= 1e-12
+        assert shared.stats()["memory_bytes"] < 0.5 * plain.stats()["memory_bytes"]
+        assert shared.stats()["factored_blocks"] == 1 and plain.stats()["factored_blocks"] == 2 ** dim
+        assert shared.stats()["device_bytes"] < 0.5 * plain.stats()["device_bytes"]
+
     def test_lanczos(self, ie):
         for case in _cbd_meta():
             if "lanczos_min" not in case:
