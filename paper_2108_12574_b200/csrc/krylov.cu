@@ -35,6 +35,7 @@ namespace ie {
 int matvec_launch(const ie_matvec* m, const double* X, int64_t ldx, int nrhs, double* Y, int64_t ldy,
                   int64_t row_begin, int64_t row_end, cudaStream_t st, const int* stop,
                   const double* amax = nullptr);
+int precond_prepare_stream(const ie_precond* p, cudaStream_t st);
 int precond_apply(const ie_precond* p, const double* r, double* z, double* partials, cudaStream_t st,
                   const int* stop);
 int matvec_N(const ie_matvec* m);
@@ -505,6 +506,7 @@ extern "C" int ie_pcg_f64(const ie_matvec* A, const ie_precond* T, const double*
                 W->gexec = nullptr;
             }
             cudaGraph_t g;
+            if (T && (rc = precond_prepare_stream(T, W->cap_stream))) return rc;
             IE_CUDA(cudaStreamBeginCapture(W->cap_stream, cudaStreamCaptureModeThreadLocal));
             int r2 = enqueue_iter(-1, 1, 1, true, W->cap_stream, false, 0);
             if (!r2) {
@@ -890,6 +892,7 @@ extern "C" int ie_lanczos_f64(const ie_matvec* A, const ie_precond* T, const dou
     for (int64_t j = 0; j < max_iters; ++j) {
         if (graph_ok && j >= kGraphAfter && !gexec) {
             IE_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
+            if (T && precond_prepare_stream(T, cap)) return IE_ERR_CUDA;
             cudaGraph_t g;
             IE_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
             rc = step(cap);
@@ -1265,6 +1268,7 @@ extern "C" int ie_pcg_sharded_f64(const ie_matvec* A, const ie_precond* T, ie_co
         IE_CUDA(cudaEventRecord(ev, st));
         IE_CUDA(cudaStreamWaitEvent(cap_s, ev, 0));
         cudaEventDestroy(ev);
+        if (T && (rc = precond_prepare_stream(T, cap_s))) return rc;
         cudaGraph_t gr;
         IE_CUDA(cudaStreamBeginCapture(cap_s, cudaStreamCaptureModeThreadLocal));
         int r2 = enqueue_iter(-1, 1, 1, true, cap_s);

@@ -27,6 +27,7 @@
 #include <algorithm>
 #include <array>
 #include <climits>
+#include <mutex>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -1027,9 +1028,50 @@ struct ie_precond {
     int* d_posfix; // [mm][N] staged positions, -1 padded
     double* d_part = nullptr;      // k_apply_big per-chunk partials
     int64_t* d_pofs = nullptr;     // per block offset into d_part
+    int64_t part_n = 0;
+    // per-stream apply workspaces (staging, pre-gathered r, big-block partials):
+    // the buffers above belong to the first stream that applies the handle;
+    // other streams get their own, so concurrent applies do not share scratch
+    std::mutex ws_mu;
+    bool ws0_claimed = false;
+    cudaStream_t ws0_stream = nullptr;
+    struct Ws {
+        double *staging = nullptr, *rg = nullptr, *part = nullptr;
+    };
+    std::vector<std::pair<cudaStream_t, Ws>> ws_extra;
 };
 
 namespace ie {
+
+static ie_precond::Ws apply_ws(ie_precond* p, cudaStream_t st) {
+    std::lock_guard<std::mutex> lk(p->ws_mu);
+    if (!p->ws0_claimed) {
+        p->ws0_claimed = true;
+        p->ws0_stream = st;
+    }
+    if (st == p->ws0_stream) return ie_precond::Ws{p->d_staging, p->d_rg, p->d_part};
+    for (auto& e : p->ws_extra)
+        if (e.first == st) return e.second;
+    ie_precond::Ws w;
+    bool ok = cudaMalloc(&w.staging, std::max<int64_t>(p->total_s, 1) * sizeof(double)) == cudaSuccess;
+    if (ok && p->d_rg) ok = cudaMalloc(&w.rg, std::max<int64_t>(p->total_s, 1) * sizeof(double)) == cudaSuccess;
+    if (ok && p->d_part) ok = cudaMalloc(&w.part, std::max<int64_t>(p->part_n, 1) * sizeof(double)) == cudaSuccess;
+    if (!ok) {
+        cudaFree(w.staging);
+        cudaFree(w.rg);
+        cudaFree(w.part);
+        cudaGetLastError();
+        set_error("precond apply: out of device memory for a per-stream workspace");
+        return ie_precond::Ws{};
+    }
+    p->ws_extra.emplace_back(st, w);
+    return w;
+}
+
+// Allocate the stream's apply workspace now (before a graph capture on it).
+int precond_prepare_stream(const ie_precond* p, cudaStream_t st) {
+    return apply_ws(const_cast<ie_precond*>(p), st).staging ? IE_OK : IE_ERR_CUDA;
+}
 
 static int slots_for(int smax) {
     const int t = (smax + 31) / 32;
@@ -1057,18 +1099,18 @@ static void launch_apply_T(const ie_precond* p, ApplyArgs a, cudaStream_t st) {
 // them to its band (precond_apply_band)
 static thread_local int64_t t_i0 = 0, t_i1 = -1;
 
-static int scatter_launch(const ie_precond* p, const double* r, double* z, double* partials, cudaStream_t st,
-                          const int* stop) {
+static int scatter_launch(const ie_precond* p, const double* staging, const double* r, double* z,
+                          double* partials, cudaStream_t st, const int* stop) {
     const int i0 = (int)t_i0, i1 = t_i1 < 0 ? p->N : (int)t_i1;
     const int nch = (i1 - i0 + kChunk - 1) / kChunk;
     if (nch <= 0) return IE_OK;
     const double* rr = partials ? r : nullptr;
     switch (p->mm) {
-        case 1: k_scatter_fixed<1><<<nch, 256, 0, st>>>(p->d_staging, p->d_posfix, z, p->N, rr, partials, stop, i0, i1); break;
-        case 2: k_scatter_fixed<2><<<nch, 256, 0, st>>>(p->d_staging, p->d_posfix, z, p->N, rr, partials, stop, i0, i1); break;
-        case 4: k_scatter_fixed<4><<<nch, 256, 0, st>>>(p->d_staging, p->d_posfix, z, p->N, rr, partials, stop, i0, i1); break;
-        case 8: k_scatter_fixed<8><<<nch, 256, 0, st>>>(p->d_staging, p->d_posfix, z, p->N, rr, partials, stop, i0, i1); break;
-        default: k_scatter<<<nch, 256, 0, st>>>(p->d_staging, p->d_ptr, p->d_pos, z, p->N, rr, partials, stop, i0, i1);
+        case 1: k_scatter_fixed<1><<<nch, 256, 0, st>>>(staging, p->d_posfix, z, p->N, rr, partials, stop, i0, i1); break;
+        case 2: k_scatter_fixed<2><<<nch, 256, 0, st>>>(staging, p->d_posfix, z, p->N, rr, partials, stop, i0, i1); break;
+        case 4: k_scatter_fixed<4><<<nch, 256, 0, st>>>(staging, p->d_posfix, z, p->N, rr, partials, stop, i0, i1); break;
+        case 8: k_scatter_fixed<8><<<nch, 256, 0, st>>>(staging, p->d_posfix, z, p->N, rr, partials, stop, i0, i1); break;
+        default: k_scatter<<<nch, 256, 0, st>>>(staging, p->d_ptr, p->d_pos, z, p->N, rr, partials, stop, i0, i1);
     }
     IE_LAUNCHED();
     return IE_OK;
@@ -1100,17 +1142,19 @@ static void launch_gemm(const ie_precond* p, const GemmArgs& g, cudaStream_t st)
 
 int precond_apply(const ie_precond* p, const double* r, double* z, double* partials, cudaStream_t st,
                   const int* stop) {
+    const ie_precond::Ws W = apply_ws(const_cast<ie_precond*>(p), st);
+    if (!W.staging) return IE_ERR_CUDA;
     if (p->gemm_ra) {
         // the DMMA kernel gathers its r columns itself; the FFMA variant reads them pre-gathered
         const bool pre = !p->use_dmma || p->dmma_pregather;
         if (pre) {
-            k_gather<<<(unsigned)((p->total_s + 255) / 256), 256, 0, st>>>(r, p->d_idx, p->d_rg, p->total_s, stop);
+            k_gather<<<(unsigned)((p->total_s + 255) / 256), 256, 0, st>>>(r, p->d_idx, W.rg, p->total_s, stop);
             IE_LAUNCHED();
         }
         GemmArgs g;
         g.r = r;
-        g.rg = pre ? p->d_rg : nullptr;
-        g.staging = p->d_staging;
+        g.rg = pre ? W.rg : nullptr;
+        g.staging = W.staging;
         g.meta = p->d_meta;
         g.idx = p->d_idx;
         g.full = p->d_full;
@@ -1135,7 +1179,7 @@ int precond_apply(const ie_precond* p, const double* r, double* z, double* parti
                 default: launch_dmma<10>(p, g, st); break;
             }
             IE_LAUNCHED();
-            return scatter_launch(p, r, z, partials, st, stop);
+            return scatter_launch(p, W.staging, r, z, partials, st, stop);
         }
         switch (p->gemm_ra) {
             case 1: launch_gemm<1>(p, g, st); break;
@@ -1150,12 +1194,12 @@ int precond_apply(const ie_precond* p, const double* r, double* z, double* parti
             default: launch_gemm<10>(p, g, st); break;
         }
         IE_LAUNCHED();
-        return scatter_launch(p, r, z, partials, st, stop);
+        return scatter_launch(p, W.staging, r, z, partials, st, stop);
     }
     ApplyArgs a;
     a.stop = stop;
     a.r = r;
-    a.staging = p->d_staging;
+    a.staging = W.staging;
     a.meta = p->d_meta;
     a.idx = p->d_idx;
     a.fac = p->d_fac;
@@ -1166,11 +1210,11 @@ int precond_apply(const ie_precond* p, const double* r, double* z, double* parti
         const size_t sm = (size_t)p->smax * sizeof(double) + 2 * kBigRows * 8 * sizeof(double);
         if (sm > 48 * 1024) cudaFuncSetAttribute(k_apply_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         const int slots = ((p->smax + kBigRows - 1) / kBigRows + 1) / 2;
-        k_apply_big<<<dim3(slots, (unsigned)p->D), 256, sm, st>>>(a, p->d_part, p->d_pofs);
+        k_apply_big<<<dim3(slots, (unsigned)p->D), 256, sm, st>>>(a, W.part, p->d_pofs);
         IE_LAUNCHED();
-        k_apply_big_sum<<<dim3((p->smax + 255) / 256, (unsigned)p->D), 256, 0, st>>>(a, p->d_part, p->d_pofs);
+        k_apply_big_sum<<<dim3((p->smax + 255) / 256, (unsigned)p->D), 256, 0, st>>>(a, W.part, p->d_pofs);
         IE_LAUNCHED();
-        return scatter_launch(p, r, z, partials, st, stop);
+        return scatter_launch(p, W.staging, r, z, partials, st, stop);
     }
     switch (p->T) {
         case 1: launch_apply_T<1>(p, a, st); break;
@@ -1184,7 +1228,7 @@ int precond_apply(const ie_precond* p, const double* r, double* z, double* parti
         default: set_error("apply: unsupported block size"); return IE_ERR_ARG;
     }
     IE_LAUNCHED();
-    return scatter_launch(p, r, z, partials, st, stop);
+    return scatter_launch(p, W.staging, r, z, partials, st, stop);
 }
 
 }  // namespace ie
@@ -1206,6 +1250,11 @@ extern "C" void ie_precond_destroy(ie_precond* p) {
     cudaFree(p->d_posfix);
     cudaFree(p->d_part);
     cudaFree(p->d_pofs);
+    for (auto& e : p->ws_extra) {
+        cudaFree(e.second.staging);
+        cudaFree(e.second.rg);
+        cudaFree(e.second.part);
+    }
     delete p;
 }
 
@@ -1469,6 +1518,7 @@ extern "C" int ie_precond_create(const ie_geom* g, const int64_t* h_offsets, con
                 pn += (int64_t)(((sizes[k] + ie::kBigRows - 1) / ie::kBigRows + 1) / 2) * sizes[k];
             }
             IE_CHECK_BUILD(cudaMalloc(&p->d_part, std::max<int64_t>(pn, 1) * sizeof(double)));
+            p->part_n = pn;
             IE_CHECK_BUILD(cudaMalloc(&p->d_pofs, D * sizeof(int64_t)));
             IE_CHECK_BUILD(cudaMemcpyAsync(p->d_pofs, pofs.data(), D * sizeof(int64_t), cudaMemcpyHostToDevice, st));
             IE_CHECK_BUILD(cudaStreamSynchronize(st));

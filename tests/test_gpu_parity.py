@@ -569,6 +569,33 @@ class TestShardedCuda:
             assert torch.equal(Y, Yf), world
 
 
+class TestConcurrency:
+    """The reference allows concurrent calls: applies of one
+    preconditioner on different streams use per-stream workspaces."""
+
+    @pytest.mark.parametrize("dim,n,m,w,kind", [(2, 256, 32, 2, "schwarz"), (2, 64, 16, 1, "cbd"),
+                                                (3, 16, 2, 1, "schwarz")])
+    def test_two_streams(self, ie, dim, n, m, w, kind):
+        import torch
+        grid = ie.build_grid(dim, n)
+        op = ie.build_operator(grid, lattice="cell")
+        pre = ie.from_decomposition(op, ie.build_decomposition(grid, m, w, kind))
+        rng = np.random.default_rng(8)
+        rs = [torch.from_numpy(rng.standard_normal(op.n)).cuda() for _ in range(2)]
+        ref = [pre.apply_device(r, torch.empty_like(r)).clone() for r in rs]
+        torch.cuda.synchronize()
+        streams = [torch.cuda.Stream() for _ in range(2)]
+        outs = [[torch.empty_like(rs[0]) for _ in range(20)] for _ in range(2)]
+        for k in range(20):
+            for s_i, st in enumerate(streams):
+                with torch.cuda.stream(st):
+                    pre.apply_device(rs[s_i], outs[s_i][k])
+        torch.cuda.synchronize()
+        for s_i in range(2):
+            for k in range(20):
+                assert torch.equal(outs[s_i][k], ref[s_i])
+
+
 class TestEdgeCases:
     def test_not_positive_definite(self, ie):
         from paper_2108_12574_b200.kernel import KernelOperator
