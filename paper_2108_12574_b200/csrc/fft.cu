@@ -804,18 +804,27 @@ int fft_absmax2(const double* X0, const double* X1, int64_t N, double* part, cud
 }
 
 // Y0 (+ i Y1) = A (X0 + i X1) over all N rows.
+int64_t fft_buf_elems(const ie_fft* f) {
+    int64_t t = 1;
+    for (int d = 0; d < f->dim; ++d) t *= (d == 0 ? f->n : f->M);
+    return t;
+}
+
+// buf_ws / amax_ws: the calling stream's work buffer and chunk-maxima scratch
+// (nullptr: the plan's own)
 int fft_matvec(const ie_fft* f, const double* X0, const double* X1, double* Y0, double* Y1, cudaStream_t st,
-               const int* stop, const double* amax_ext) {
+               const int* stop, const double* amax_ext, double2* buf_ws, double* amax_ws) {
     const int n = f->n, M = f->M, d = f->dim;
     int rc;
     const int two = X1 != nullptr;
+    double* amax_own = amax_ws ? amax_ws : f->d_amax;
     if (two && !amax_ext) {
-        k_absmax2<<<(f->N + 2047) / 2048, 256, 0, st>>>(X0, X1, f->N, f->d_amax, stop);
+        k_absmax2<<<(f->N + 2047) / 2048, 256, 0, st>>>(X0, X1, f->N, amax_own, stop);
         IE_LAUNCHED();
     }
     auto line_launch = [&](LineArgs a, cudaStream_t s) -> int {
         a.stop = stop;
-        if (amax_ext) a.amax = amax_ext;
+        a.amax = amax_ext ? amax_ext : amax_own;
         if (two) {
             a.scale_in = a.in_real;
             a.scale_out = a.out_real;
@@ -839,7 +848,7 @@ int fft_matvec(const ie_fft* f, const double* X0, const double* X1, double* Y0, 
         a.fused = 1;
         return line_launch(a, st);
     }
-    double2* B = f->d_buf;
+    double2* B = buf_ws ? buf_ws : f->d_buf;
     if (d == 2) {  // B: (n, M)
         LineArgs a = base_args(f);  // rows a < n, forward along axis 1
         a.nlines = n;

@@ -36,6 +36,7 @@ int matvec_launch(const ie_matvec* m, const double* X, int64_t ldx, int nrhs, do
                   int64_t row_begin, int64_t row_end, cudaStream_t st, const int* stop,
                   const double* amax = nullptr);
 int precond_prepare_stream(const ie_precond* p, cudaStream_t st);
+int matvec_prepare_stream(const ie_matvec* m, cudaStream_t st);
 int precond_apply(const ie_precond* p, const double* r, double* z, double* partials, cudaStream_t st,
                   const int* stop);
 int matvec_N(const ie_matvec* m);
@@ -507,6 +508,7 @@ extern "C" int ie_pcg_f64(const ie_matvec* A, const ie_precond* T, const double*
             }
             cudaGraph_t g;
             if (T && (rc = precond_prepare_stream(T, W->cap_stream))) return rc;
+            if ((rc = matvec_prepare_stream(A, W->cap_stream))) return rc;
             IE_CUDA(cudaStreamBeginCapture(W->cap_stream, cudaStreamCaptureModeThreadLocal));
             int r2 = enqueue_iter(-1, 1, 1, true, W->cap_stream, false, 0);
             if (!r2) {
@@ -893,6 +895,7 @@ extern "C" int ie_lanczos_f64(const ie_matvec* A, const ie_precond* T, const dou
         if (graph_ok && j >= kGraphAfter && !gexec) {
             IE_CUDA(cudaStreamCreateWithFlags(&cap, cudaStreamNonBlocking));
             if (T && precond_prepare_stream(T, cap)) return IE_ERR_CUDA;
+            if (matvec_prepare_stream(A, cap)) return IE_ERR_CUDA;
             cudaGraph_t g;
             IE_CUDA(cudaStreamBeginCapture(cap, cudaStreamCaptureModeThreadLocal));
             rc = step(cap);

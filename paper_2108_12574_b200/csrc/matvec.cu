@@ -18,6 +18,7 @@
 // split order across CTAs -- identical for any row range and any NRHS.
 #include <math.h>
 
+#include <mutex>
 #include <vector>
 
 #include "common.cuh"
@@ -219,7 +220,8 @@ namespace ie {
 int fft_create(const ie_geom& g, ie_fft** out);
 void fft_destroy(ie_fft* f);
 int fft_matvec(const ie_fft* f, const double* X0, const double* X1, double* Y0, double* Y1, cudaStream_t st,
-               const int* stop, const double* amax);
+               const int* stop, const double* amax, double2* buf_ws, double* amax_ws);
+int64_t fft_buf_elems(const ie_fft* f);
 int fft_band_fwd(const ie_fft* f, const double* X0, const double* X1, int nrows, int parts, double2* out,
                  const double* amax, int namax, cudaStream_t st);
 int fft_band_cols(const ie_fft* f, double2* buf, int c0, int ncols, cudaStream_t st);
@@ -244,6 +246,19 @@ struct ie_matvec {
     int split_len;
     int nsplit;
     double* d_work;  // split partials, nsplit * N * 2 doubles
+    // per-stream scratch (FFT work buffer + chunk maxima, partial-range output,
+    // K1 split partials): the plan's own buffers belong to the first stream
+    // that uses the handle, other streams get their own
+    struct Ws {
+        double2* buf = nullptr;
+        double* amax = nullptr;
+        double* full = nullptr;
+        double* work = nullptr;
+    };
+    std::mutex ws_mu;
+    bool ws0_claimed = false;
+    cudaStream_t ws0_stream = nullptr;
+    std::vector<std::pair<cudaStream_t, Ws>> ws_extra;
 };
 
 namespace ie {
@@ -290,7 +305,7 @@ static int launch_dim(const ie_matvec* m, MatvecArgs a, cudaStream_t st) {
     const size_t smem = (DIM == 3 ? 0 : (size_t)m->ntab * sizeof(LogEntry)) + (size_t)m->TS * NRHS * sizeof(double);
     const int threads = 256;
     dim3 grid((a.nrows + threads * m->R - 1) / (threads * m->R), m->nsplit);
-    a.W = m->nsplit > 1 ? m->d_work : nullptr;
+    a.W = m->nsplit > 1 ? a.W : nullptr;  // the stream's split partials (matvec_launch)
     if (m->R == 2) {
         auto kern = k_matvec<DIM, NRHS, 2>;
         IE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -308,16 +323,65 @@ static int launch_dim(const ie_matvec* m, MatvecArgs a, cudaStream_t st) {
     return IE_OK;
 }
 
+static ie_matvec::Ws mv_ws(ie_matvec* m, cudaStream_t st, bool* ok) {
+    std::lock_guard<std::mutex> lk(m->ws_mu);
+    *ok = true;
+    if (!m->ws0_claimed) {
+        m->ws0_claimed = true;
+        m->ws0_stream = st;
+    }
+    ie_matvec::Ws own;
+    own.buf = nullptr;   // fft_matvec: the plan's own buffer
+    own.amax = nullptr;
+    own.full = m->d_full;
+    own.work = m->d_work;
+    if (st == m->ws0_stream) return own;
+    for (auto& e : m->ws_extra)
+        if (e.first == st) return e.second;
+    ie_matvec::Ws w;
+    bool good = true;
+    if (m->fft) {
+        good = good && cudaMalloc(&w.buf, (size_t)fft_buf_elems(m->fft) * sizeof(double2)) == cudaSuccess;
+        good = good && cudaMalloc(&w.amax, 2 * (size_t)((m->N + 2047) / 2048) * sizeof(double)) == cudaSuccess;
+        good = good && cudaMalloc(&w.full, 2 * (size_t)m->N * sizeof(double)) == cudaSuccess;
+    }
+    if (good && m->d_work)
+        good = cudaMalloc(&w.work, (size_t)m->nsplit * m->N * 2 * sizeof(double)) == cudaSuccess;
+    if (!good) {
+        cudaFree(w.buf);
+        cudaFree(w.amax);
+        cudaFree(w.full);
+        cudaFree(w.work);
+        cudaGetLastError();
+        set_error("matvec: out of device memory for a per-stream workspace");
+        *ok = false;
+        return ie_matvec::Ws{};
+    }
+    m->ws_extra.emplace_back(st, w);
+    return w;
+}
+
+// Allocate the stream's matvec scratch now (before a graph capture on it).
+int matvec_prepare_stream(const ie_matvec* m, cudaStream_t st) {
+    bool ok;
+    mv_ws(const_cast<ie_matvec*>(m), st, &ok);
+    return ok ? IE_OK : IE_ERR_CUDA;
+}
+
 int matvec_launch(const ie_matvec* m, const double* X, int64_t ldx, int nrhs, double* Y, int64_t ldy,
                   int64_t row_begin, int64_t row_end, cudaStream_t st, const int* stop, const double* amax) {
+    bool ok;
+    const ie_matvec::Ws W = mv_ws(const_cast<ie_matvec*>(m), st, &ok);
+    if (!ok) return IE_ERR_CUDA;
     if (m->method == IE_MATVEC_FFT) {
         const double* X1 = nrhs == 2 ? X + ldx : nullptr;
         if (row_begin == 0 && row_end == m->N)
-            return fft_matvec(m->fft, X, X1, Y, nrhs == 2 ? Y + ldy : nullptr, st, stop, amax);
-        int rc = fft_matvec(m->fft, X, X1, m->d_full, nrhs == 2 ? m->d_full + m->N : nullptr, st, stop, amax);
+            return fft_matvec(m->fft, X, X1, Y, nrhs == 2 ? Y + ldy : nullptr, st, stop, amax, W.buf, W.amax);
+        int rc = fft_matvec(m->fft, X, X1, W.full, nrhs == 2 ? W.full + m->N : nullptr, st, stop, amax, W.buf,
+                            W.amax);
         if (rc) return rc;
         for (int q = 0; q < nrhs; ++q)
-            IE_CUDA(cudaMemcpyAsync(Y + q * ldy, m->d_full + (int64_t)q * m->N + row_begin,
+            IE_CUDA(cudaMemcpyAsync(Y + q * ldy, W.full + (int64_t)q * m->N + row_begin,
                                     (row_end - row_begin) * sizeof(double), cudaMemcpyDeviceToDevice, st));
         return IE_OK;
     }
@@ -326,7 +390,7 @@ int matvec_launch(const ie_matvec* m, const double* X, int64_t ldx, int nrhs, do
     a.ldx = ldx;
     a.Y = Y;
     a.ldy = ldy;
-    a.W = nullptr;
+    a.W = W.work;
     a.tab = m->d_tab;
     a.ntab = m->ntab;
     a.n = m->g.n;
@@ -443,6 +507,12 @@ extern "C" void ie_matvec_destroy(ie_matvec* m) {
     if (m->d_full) cudaFree(m->d_full);
     cudaFree(m->d_tab);
     if (m->d_work) cudaFree(m->d_work);
+    for (auto& e : m->ws_extra) {
+        cudaFree(e.second.buf);
+        cudaFree(e.second.amax);
+        cudaFree(e.second.full);
+        cudaFree(e.second.work);
+    }
     delete m;
 }
 

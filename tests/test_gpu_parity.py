@@ -596,6 +596,31 @@ class TestConcurrency:
                 assert torch.equal(outs[s_i][k], ref[s_i])
 
 
+    @pytest.mark.parametrize("method,n", [("fft", 256), ("direct", 64), ("fft", 32)])
+    def test_matvec_two_streams(self, ie, method, n):
+        import torch
+        op = ie.build_operator(ie.build_grid(2, n), lattice="cell")
+        mv = ie.KernelMatvec(op, method=method)
+        rng = np.random.default_rng(9)
+        Xs = [torch.from_numpy(rng.standard_normal((2, op.n))).cuda() for _ in range(2)]
+        ref = []
+        for X in Xs:
+            Y = torch.empty_like(X)
+            mv.matvec_device(X, Y, nrhs=2)
+            ref.append(Y.clone())
+        torch.cuda.synchronize()
+        streams = [torch.cuda.Stream() for _ in range(2)]
+        outs = [[torch.empty_like(Xs[0]) for _ in range(8)] for _ in range(2)]
+        for k in range(8):
+            for i, st in enumerate(streams):
+                with torch.cuda.stream(st):
+                    mv.matvec_device(Xs[i], outs[i][k], nrhs=2, row_begin=0, row_end=op.n)
+        torch.cuda.synchronize()
+        for i in range(2):
+            for k in range(8):
+                assert torch.equal(outs[i][k], ref[i])
+
+
 class TestEdgeCases:
     def test_not_positive_definite(self, ie):
         from paper_2108_12574_b200.kernel import KernelOperator
