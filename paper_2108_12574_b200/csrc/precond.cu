@@ -990,6 +990,82 @@ __global__ void __launch_bounds__(256) k_sweep_pack(SweepArgs a, double* fac, co
     }
 }
 
+// Blocks above kBigMaxS points (up to kFullMaxS; the reference factorises
+// them when dense_limit is raised, e.g. its interface-3d golden suite):
+// assembled straight into the sweep workspace (coordinates decoded per entry,
+// no shared-memory staging), inverted by the sweep, stored FULL (s x s,
+// symmetric) and applied as one warp per row (k_apply_full).
+constexpr int kBigMaxS = 4096;
+constexpr int kFullMaxS = 26000;  // r_k staged in shared memory (8 s bytes)
+
+__global__ void __launch_bounds__(256) k_assemble_ws(const int* idx, const int64_t* ioff, const int* sizes,
+                                                    double* work, const int64_t* wofs, const LogEntry* tab,
+                                                    EntryParams P, int n, int dim) {
+    const int u = blockIdx.y, s = sizes[u];
+    const int* id = idx + ioff[u];
+    double* A = work + wofs[u];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = blockIdx.x * 8 + warp; i < s; i += gridDim.x * 8) {
+        int ci[3] = {0, 0, 0};
+        int t = id[i];
+        for (int d = dim - 1; d >= 0; --d) {
+            ci[d] = t % n;
+            t /= n;
+        }
+        for (int j = lane; j <= i; j += 32) {
+            int tj = id[j], m = 0;
+            for (int d = dim - 1; d >= 0; --d) {
+                const int dd = ci[d] - tj % n;
+                tj /= n;
+                m += dd * dd;
+            }
+            A[(int64_t)i * s + j] = entry_from_m(P, tab, m);
+        }
+    }
+}
+
+// full symmetric -A (both triangles) from the swept lower triangle
+__global__ void __launch_bounds__(256) k_sweep_pack_full(SweepArgs a, double* fac, const int64_t* fofs) {
+    const int b = blockIdx.y, s = a.sizes[b];
+    if (a.info[a.uidx[b]]) return;
+    const double* A = a.work + a.wofs[b];
+    double* out = fac + fofs[a.uidx[b]];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = blockIdx.x * 8 + warp; i < s; i += gridDim.x * 8)
+        for (int j = lane; j <= i; j += 32) {
+            const double v = -A[(int64_t)i * s + j];
+            out[(int64_t)i * s + j] = v;
+            out[(int64_t)j * s + i] = v;
+        }
+}
+
+// z_k = A_k^{-1} r_k with the full inverse: r_k in shared memory, one warp per
+// row (lanes stride the row, fixed-order warp reduction).
+__global__ void __launch_bounds__(256) k_apply_full(ApplyArgs a) {
+    extern __shared__ double rs[];
+    if (a.stop && *a.stop) return;
+    const BlockMeta bm = a.meta[blockIdx.y];
+    const int s = bm.s, r0 = blockIdx.x * 64;
+    if (r0 >= s) return;
+    const int* idx = a.idx + bm.idx_off;
+    for (int j = threadIdx.x; j < s; j += blockDim.x) rs[j] = __ldg(a.r + idx[j]);
+    __syncthreads();
+    const double* F = a.fac + bm.fac_off;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = r0 + warp; i < min(s, r0 + 64); i += 8) {
+        const double* row = F + (int64_t)i * s;
+        double acc0 = 0.0, acc1 = 0.0;
+        int j = lane;
+        for (; j + 32 < s; j += 64) {
+            acc0 = fma(__ldg(row + j), rs[j], acc0);
+            acc1 = fma(__ldg(row + j + 32), rs[j + 32], acc1);
+        }
+        if (j < s) acc0 = fma(__ldg(row + j), rs[j], acc0);
+        const double d = warp_sum(acc0 + acc1);
+        if (lane == 0) a.staging[bm.st_off + i] = d;
+    }
+}
+
 }  // namespace ie
 
 // ------------------------------------------------------------- host side --
@@ -1029,6 +1105,7 @@ struct ie_precond {
     double* d_part = nullptr;      // k_apply_big per-chunk partials
     int64_t* d_pofs = nullptr;     // per block offset into d_part
     int64_t part_n = 0;
+    int full = 0;  // blocks above kBigMaxS: full-storage inverses, k_apply_full
     // per-stream apply workspaces (staging, pre-gathered r, big-block partials):
     // the buffers above belong to the first stream that applies the handle;
     // other streams get their own, so concurrent applies do not share scratch
@@ -1206,6 +1283,17 @@ int precond_apply(const ie_precond* p, const double* r, double* z, double* parti
     a.D = p->D;
     a.wpb = p->wpb;
     a.bpc = p->bpc;
+    if (p->full) {
+        const size_t sm = (size_t)p->smax * sizeof(double);
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_apply_full, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+            attr = true;
+        }
+        k_apply_full<<<dim3((p->smax + 63) / 64, (unsigned)p->D), 256, sm, st>>>(a);
+        IE_LAUNCHED();
+        return scatter_launch(p, W.staging, r, z, partials, st, stop);
+    }
     if (p->d_part) {
         const size_t sm = (size_t)p->smax * sizeof(double) + 2 * kBigRows * 8 * sizeof(double);
         if (sm > 48 * 1024) cudaFuncSetAttribute(k_apply_big, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -1308,6 +1396,12 @@ extern "C" int ie_precond_create(const ie_geom* g, const int64_t* h_offsets, con
             return IE_ERR_ARG;
         }
         T = 64;  // large-block path (k_apply_big)
+    }
+    const bool full = smax > ie::kBigMaxS;
+    if (smax > ie::kFullMaxS) {
+        ie::set_error("ie_precond_create: subdomains above " + std::to_string(ie::kFullMaxS) +
+                      " points are not supported");
+        return IE_ERR_ARG;
     }
     // share_translated bit 0: translation classes, signature = multi-index
     // offsets from the first point.  Bit 1 (share_mirrored_subdomains,
@@ -1418,6 +1512,7 @@ extern "C" int ie_precond_create(const ie_geom* g, const int64_t* h_offsets, con
     }
     const int64_t U = (int64_t)uniq.size();
     auto fac_len = [&](int s) -> int64_t {
+        if (full) return (int64_t)s * s;
         return (int64_t)s * (s + 1) / 2 + (variant == IE_VARIANT_SUBST ? s : 0);
     };
     std::vector<int64_t> ufofs(U), uioff(U), uwofs(U);
@@ -1430,7 +1525,7 @@ extern "C" int ie_precond_create(const ie_geom* g, const int64_t* h_offsets, con
         facn += (fac_len(s) + 31) / 32 * 32;  // 256 B aligned factors
         uioff[u] = idxn;
         idxn += s;
-        if (s > ie::kSmemMaxS) {
+        if (s > ie::kSmemMaxS || full) {
             uwofs[u] = workn;
             workn += (int64_t)s * s;
         } else {
@@ -1492,6 +1587,7 @@ extern "C" int ie_precond_create(const ie_geom* g, const int64_t* h_offsets, con
     p->n_factored = U;
     p->total_s = total;
     p->T = T;
+    p->full = full ? 1 : 0;
     if (smax <= ie::kSmemMaxS) {
         p->wpb = 1;
         p->bpc = 4;
@@ -1510,7 +1606,7 @@ extern "C" int ie_precond_create(const ie_geom* g, const int64_t* h_offsets, con
         // row-chunked multi-CTA apply for large blocks (required above 1024 points)
         int big_min = 1024;
         if (const char* e = getenv("IEDD_B200_BIG_MIN_S")) big_min = atoi(e);
-        if (variant == IE_VARIANT_PACKED_INVERSE && smax > big_min) {
+        if (variant == IE_VARIANT_PACKED_INVERSE && smax > big_min && !full) {
             std::vector<int64_t> pofs(D);
             int64_t pn = 0;
             for (int64_t k = 0; k < D; ++k) {
@@ -1581,7 +1677,8 @@ extern "C" int ie_precond_create(const ie_geom* g, const int64_t* h_offsets, con
     ba.n = g->n;
     ba.dim = g->dim;
     ba.variant = variant;
-    ba.assemble_only = (variant == IE_VARIANT_PACKED_INVERSE && !getenv("IEDD_B200_UNBLOCKED_LARGE")) ? 1 : 0;
+    ba.assemble_only =
+        (variant == IE_VARIANT_PACKED_INVERSE && (full || !getenv("IEDD_B200_UNBLOCKED_LARGE"))) ? 1 : 0;
     size_t smem = 0;
     for (int64_t u = 0; u < U; ++u) {
         const size_t su = (size_t)usizes[u];
@@ -1589,10 +1686,19 @@ extern "C" int ie_precond_create(const ie_geom* g, const int64_t* h_offsets, con
         if (usizes[u] <= ie::kSmemMaxS) need += su * (su | 1) * 8;
         smem = std::max(smem, need);
     }
-    IE_CHECK_BUILD(cudaFuncSetAttribute(ie::k_build, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    ie::k_build<<<(unsigned)U, ie::kBuildThreads, smem, st>>>(ba);
-    IE_CHECK_BUILD(cudaGetLastError());
-    ie::g_launches.fetch_add(1);
+    if (full) {
+        // every block through the workspace: entries decoded per element (no smem staging)
+        IE_CHECK_BUILD(cudaMemsetAsync(d_info, 0, U * sizeof(int), st));
+        ie::k_assemble_ws<<<dim3((unsigned)std::min(1024, (smax + 7) / 8), (unsigned)U), 256, 0, st>>>(
+            d_uidx, d_uioff, d_usz, d_work, d_uwofs, d_tab, ba.P, g->n, g->dim);
+        IE_CHECK_BUILD(cudaGetLastError());
+        ie::g_launches.fetch_add(1);
+    } else {
+        IE_CHECK_BUILD(cudaFuncSetAttribute(ie::k_build, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        ie::k_build<<<(unsigned)U, ie::kBuildThreads, smem, st>>>(ba);
+        IE_CHECK_BUILD(cudaGetLastError());
+        ie::g_launches.fetch_add(1);
+    }
     if (ba.assemble_only && workn) {
         // blocked sweep inversion of the workspace blocks, all of them per launch
         std::vector<int> lsz, lu;
@@ -1648,7 +1754,10 @@ extern "C" int ie_precond_create(const ie_geom* g, const int64_t* h_offsets, con
             ie::k_sweep_update<<<dim3(ntile * (ntile + 1) / 2, nl), 256, 0, st>>>(sa);
             ie::g_launches.fetch_add(3);
         }
-        ie::k_sweep_pack<<<dim3(std::min(64, (lmax + 7) / 8), nl), 256, 0, st>>>(sa, p->d_fac, d_ufofs);
+        if (full)
+            ie::k_sweep_pack_full<<<dim3(std::min(256, (lmax + 7) / 8), nl), 256, 0, st>>>(sa, p->d_fac, d_ufofs);
+        else
+            ie::k_sweep_pack<<<dim3(std::min(64, (lmax + 7) / 8), nl), 256, 0, st>>>(sa, p->d_fac, d_ufofs);
         IE_CHECK_BUILD(cudaGetLastError());
         ie::g_launches.fetch_add(1);
     }

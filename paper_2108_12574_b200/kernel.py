@@ -107,6 +107,10 @@ class KernelOperator:
 
     def assemble_block(self, rows, cols) -> np.ndarray:
         """Dense A[rows, cols], evaluated on the device (kernel.py:170-184)."""
+        return self.assemble_block_device(rows, cols).cpu().numpy()
+
+    def assemble_block_device(self, rows, cols):
+        """As assemble_block, returning the device tensor."""
         torch = _lib.torch_cuda()
         rows = np.ascontiguousarray(np.asarray(rows, dtype=np.int64).ravel())
         cols = np.ascontiguousarray(np.asarray(cols, dtype=np.int64).ravel())
@@ -120,7 +124,7 @@ class KernelOperator:
         rc = _lib.lib().ie_assemble_block_f64(g, _lib.ptr(dr), rows.size, _lib.ptr(dc), cols.size,
                                               _lib.ptr(out), _lib.stream_ptr())
         _lib.check(rc, "assemble_block")
-        return out.cpu().numpy()
+        return out
 
     def dense(self) -> np.ndarray:
         idx = np.arange(self.n, dtype=np.int64)

@@ -74,15 +74,18 @@ class Preconditioner:
 
     def apply_dense(self) -> np.ndarray:
         """Materialise T^{-1} (precond.py:102-116): apply to the unit columns."""
-        if self._handle is None:
-            return np.eye(self.n)
+        return self.apply_dense_device().cpu().numpy()
+
+    def apply_dense_device(self):
+        """T^{-1} as a symmetrised dense device tensor."""
         torch = _lib.torch_cuda()
+        if self._handle is None:
+            return torch.eye(self.n, dtype=torch.float64, device="cuda")
         eye = torch.eye(self.n, dtype=torch.float64, device="cuda")
         out = torch.empty_like(eye)
         for j in range(self.n):
             self.apply_device(eye[j], out[j])
-        t = out.cpu().numpy()
-        return 0.5 * (t + t.T)
+        return 0.5 * (out + out.T)
 
     @property
     def n_subdomains(self) -> int:

@@ -8,7 +8,12 @@ pairs), and the Ritz value comes from a device Sturm-multisection on the
 tridiagonal.  The stopping rule is the reference's (5 consecutive steps with
 |change| <= rtol*max(|lambda|,1), beta^2 <= 0, beta < 1e-14, max_iters).
 
-The dense-spectrum analysis (spectrum.py:37-130) is out of scope."""
+The dense-spectrum analysis (spectrum.py:37-130: preconditioned_spectrum,
+extremal_eigenvector, jacobi_pairing_check) materialises A and T^{-1} on the
+device (K1's entry formula, K3 applied to the unit columns) and solves the
+symmetric congruence G^T A G, T^{-1} = G G^T, with the device's dense
+Cholesky / symmetric eigensolver (torch.linalg, cuSOLVER): a utility around
+the path, not a hot kernel."""
 
 from __future__ import annotations
 
@@ -21,6 +26,7 @@ from .precond import Preconditioner
 from .toeplitz import KernelMatvec
 
 DENSE_LIMIT_SPECTRUM = 4096
+MULTIPLICITY_TOL = 1e-8
 
 
 def extremal_eigenvalue_lanczos(matvec, precond, n: int, which: str = "min", max_iters: int = 400,
@@ -41,3 +47,77 @@ def extremal_eigenvalue_lanczos(matvec, precond, n: int, which: str = "min", max
         raise RuntimeError("Lanczos produced no Ritz values")
     _lib.check(rc, "extremal_eigenvalue_lanczos")
     return (lam.value, steps.value) if return_steps else lam.value
+
+
+# --------------------------------------------------------------------------
+# dense spectra (spectrum.py:29-130)
+# --------------------------------------------------------------------------
+from dataclasses import dataclass, field  # noqa: E402
+
+
+@dataclass(frozen=True)
+class SpectrumReport:
+    lambda_min: float
+    lambda_max: float
+    eigenvalues: np.ndarray = field(repr=False)
+    multiplicity_at_max: int
+    config: dict
+
+
+def _congruence(op, precond):
+    """(G, G^T A G) on the device, T^{-1} = G G^T (spectrum.py:37-45)."""
+    torch = _lib.torch_cuda()
+    tinv = precond.apply_dense_device()
+    g, info = torch.linalg.cholesky_ex(tinv)
+    if int(info.item()) != 0:
+        raise RuntimeError("materialized preconditioner is not numerically SPD")
+    idx = np.arange(op.n, dtype=np.int64)
+    a = op.assemble_block_device(idx, idx)
+    return g, g.T @ (a @ g)
+
+
+def preconditioned_spectrum(op, precond, dense_limit: int = DENSE_LIMIT_SPECTRUM, config: dict | None = None):
+    """All eigenvalues of T^{-1}A (spectrum.py:48-73)."""
+    if op.n > dense_limit:
+        raise ValueError(f"N={op.n} exceeds dense_limit={dense_limit}; raise the limit "
+                         "explicitly for larger dense spectra")
+    torch = _lib.torch_cuda()
+    _, sym = _congruence(op, precond)
+    w = torch.linalg.eigvalsh(sym).cpu().numpy()
+    lam_max = float(w[-1])
+    return SpectrumReport(lambda_min=float(w[0]), lambda_max=lam_max, eigenvalues=w,
+                          multiplicity_at_max=int(np.sum(np.abs(w - lam_max) <= MULTIPLICITY_TOL)),
+                          config=dict(config or {}, N=op.n, kind=precond.kind, D=precond.n_subdomains))
+
+
+def multiplicity_at(report: SpectrumReport, value: float, tol: float) -> int:
+    return int(np.sum(np.abs(report.eigenvalues - value) <= tol))
+
+
+def extremal_eigenvector(op, precond, which: str, dense_limit: int = DENSE_LIMIT_SPECTRUM):
+    """Extremal eigenpair of T^{-1}A (spectrum.py:80-102): unit-norm vector,
+    largest-magnitude entry positive."""
+    if which not in ("min", "max"):
+        raise ValueError(f"which must be 'min' or 'max', got {which!r}")
+    if op.n > dense_limit:
+        raise ValueError(f"N={op.n} exceeds dense_limit={dense_limit}")
+    torch = _lib.torch_cuda()
+    g, sym = _congruence(op, precond)
+    w, vecs = torch.linalg.eigh(sym)
+    col = 0 if which == "min" else -1
+    vec = (g @ vecs[:, col]).cpu().numpy()
+    vec /= np.linalg.norm(vec)
+    if vec[np.argmax(np.abs(vec))] < 0:
+        vec = -vec
+    return float(w[col].item()), vec
+
+
+def jacobi_pairing_check(op, decomposition) -> float:
+    """max_k |lambda_k + lambda_{N+1-k} - 2| for a two-subdomain Jacobi split
+    (spectrum.py:105-114)."""
+    from .precond import from_decomposition
+    if decomposition.kind != "jacobi" or decomposition.n_subdomains != 2:
+        raise ValueError("pairing check needs a two-subdomain Jacobi decomposition")
+    pre = from_decomposition(op, decomposition, dense_limit=op.n)
+    w = preconditioned_spectrum(op, pre, dense_limit=op.n).eigenvalues
+    return float(np.max(np.abs(w + w[::-1] - 2.0)))

@@ -138,8 +138,8 @@ def gen_small(out):
     with open(os.path.join(REF_SRC, "iedd", "goldens.json")) as fh:
         suites = json.load(fh)
     keep = {k: v for k, v in suites.items()
-            if k in ("spectrum-2d", "spectrum-3d", "schwarz-scaling-2d", "iterations-2d",
-                     "iterations-3d", "pairing")}
+            if k in ("spectrum-2d", "spectrum-3d", "schwarz-scaling-2d", "interface-2d", "interface-3d",
+                     "iterations-2d", "iterations-3d", "pairing")}
     with open(os.path.join(out, "ref_goldens.json"), "w") as fh:
         json.dump(keep, fh, indent=1)
 
