@@ -157,3 +157,24 @@ class TestOperatorMetadata:
             ie.from_decomposition(op, d, backend="qr")
         with pytest.raises(ValueError, match="rskel"):
             ie.from_decomposition(op, d, dense_limit=10)
+
+
+class TestGoldenCli:
+    """The golden subcommand's argument handling (cli.py:302-327, 363-390);
+    the suites themselves run on the GPU (test_gpu_parity.TestGoldenRunner)."""
+
+    def test_config_errors(self, capsys):
+        from paper_2108_12574_b200.__main__ import main
+        assert main(["golden"]) == 1
+        assert "no golden suite named" in capsys.readouterr().err
+        assert main(["golden", "nope"]) == 1
+        err = capsys.readouterr().err
+        assert "unknown golden suite 'nope'" in err and "interface-3d" in err
+        assert main(["bogus"]) == 1
+
+    def test_suites_present(self):
+        from paper_2108_12574_b200 import golden
+        g = golden.load_goldens()
+        assert {"spectrum-2d", "spectrum-3d", "schwarz-scaling-2d", "interface-2d", "interface-3d",
+                "iterations-2d", "iterations-3d", "pairing"} <= set(g)
+        assert set(s["check"] for s in g.values()) == set(golden.RUNNERS)
