@@ -12,9 +12,16 @@
 //    not-yet-transformed coordinates are < n, and the last forward axis-0
 //    transform, the symbol multiply and the first inverse transform are one
 //    fused kernel per line (the spectrum never round-trips HBM).
-//  * Each CTA runs a self-sorting Stockham FFT (radix 4, one radix-2 pass
-//    for odd log2 M) over 4096 complex points in shared memory (64 KB):
-//    4096/M lines of length M = 2n <= 4096.
+//  * Each CTA (256 threads; 32 for small transforms) runs a self-sorting
+//    Stockham FFT over 4096 complex points in shared memory -- 4096/M lines
+//    of length M = 2n <= 4096: radix-16 passes with 16 points per thread in
+//    registers, then one radix 8/4/2 pass; split re/im arrays padded one slot
+//    per 16 with a per-line skew (conflict-free), radix-major twiddle tables
+//    staged by cp.async while the lines load.
+//  * The exact power-of-two column scaling keeps the rounding of the small
+//    column (PCG's u vs p differ by up to ~1e10) independent of the large one.
+//  * Band variants (fft_band_*) split the 2D pass across ranks around two
+//    all-to-all transposes (sharded solver).
 #include <math.h>
 #include <stdlib.h>
 
@@ -25,9 +32,6 @@
 namespace ie {
 
 constexpr int kFftPoints = 4096;
-constexpr int kLogFftPoints = 12;
-constexpr int kFftThreads = 256;
-constexpr int kPtsPerThread = kFftPoints / kFftThreads;
 
 struct LineArgs {
     int nlines;   // lines in this pass
@@ -240,25 +244,10 @@ __host__ __device__ constexpr int out_slot(int k) {
 // elements -> the stride-16 Stockham stores of the first pass and the strided
 // loads are bank-conflict free (two wavefronts per warp access).
 __device__ __forceinline__ int padi(int i) { return i + (i >> 4); }
-constexpr int kSmemStride = kFftPoints + kFftPoints / 16;
 
-// One Stockham pass of radix R over all lines (kFftPoints points, 256 threads).
-// exp(-2 pi i m / L) from the quarter-wave table q[r] = (cos, sin)(2 pi r / L),
-// r < L/4, in shared memory
-__device__ __forceinline__ double2 twiddle(const double2* qt, int m, int logL) {
-    const int quad = m >> (logL - 2);
-    const double2 cs = qt[m & ((1 << (logL - 2)) - 1)];
-    // theta = theta_r + quad * pi/2 ; return (cos theta, -sin theta)
-    switch (quad & 3) {
-        case 0: return make_double2(cs.x, -cs.y);
-        case 1: return make_double2(-cs.y, -cs.x);
-        case 2: return make_double2(-cs.x, cs.y);
-        default: return make_double2(cs.y, cs.x);
-    }
-}
-
-// Twiddles of the Ns = 16 pass, radix-major: t16[r * 16 + k] = exp(-2 pi i r k / (16 R)).
-// (Through the quarter-wave table, the 16 k-lanes of that pass would hit one bank.)
+// One Stockham pass of radix R over the CTA's lines (16 points per thread).
+// Twiddles of the Ns = 16 pass, radix-major: t16[r * 16 + k] = exp(-2 pi i r k / (16 R));
+// of the Ns = 256 pass: tws[r * 256 + k] (consecutive k on consecutive lanes).
 template <int R, int S, int TPB>
 __device__ __forceinline__ void stockham(double* sre, double* sim, int logL, int logNs, const double2* tws,
                                          const double2* t16, int skw) {
