@@ -13,10 +13,14 @@
 //
 // Dot products: fixed 2048-element chunk partials (in-CTA fixed tree), then a
 // fixed-order reduction -- deterministic and independent of the launch.
+// Control lives in device state (PcgState / LzState); the steady-state PCG
+// iteration and, after 16 steps, the Lanczos step are each one captured CUDA
+// graph, the host reading the state every few iterations.  The sharded driver
+// (ie_pcg_sharded_f64, end of file) runs the same kernels on row bands with
+// NCCL collectives between them.
 #include <math.h>
-#include <string.h>
-
 #include <stdlib.h>
+#include <string.h>
 
 #include <chrono>
 #include <mutex>

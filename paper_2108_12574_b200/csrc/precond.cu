@@ -1,26 +1,28 @@
-// K2 (block extraction + batched Cholesky) and K3 (Schwarz / block-Jacobi
-// apply) -- replaces precond.from_decomposition(backend="exact") and
-// Preconditioner.apply (/root/reference/pkg/src/iedd/precond.py:157-215,
+// K2 (block extraction + batched Cholesky / inversion) and K3 (Schwarz /
+// block-Jacobi apply) -- replaces precond.from_decomposition(backend="exact")
+// and Preconditioner.apply (/root/reference/pkg/src/iedd/precond.py:157-215,
 // :91-100) with linalg.cholesky / CholeskyFactor.solve (linalg.py:31-58).
 //
-// Build (one CTA per factorised block): gather the block's lattice points,
-// assemble A_k from integer distances (same entry formula as K1), factor
-// A_k = L L^T in place (right-looking, unblocked; in shared memory for
-// s <= kSmemMaxS, else in a global workspace), then
-//   variant PACKED_INVERSE: L^{-1} in place (LAPACK dtrti2 order) and
-//     A_k^{-1} = L^{-T} L^{-1}, stored as the packed upper triangle by columns
-//     (column j = A^{-1}[0..j, j] at j(j+1)/2);
-//   variant SUBST: G = L^T stored packed by rows (row i = G[i, i..s-1]) plus
-//     1/G_ii, for forward/back substitution.
-// Blocks whose point sets are translates of each other have bitwise equal
-// A_k (entries depend on integer differences only), so with
-// share_translated one representative per class is factorised.
-//
-// Apply: k_apply_* (one warp, or WPB warps, per block; lane-owned slots of
-// r_k and z_k in registers) writes z_k into a staging buffer; k_scatter sums,
-// per point, its <= 2^dim staged contributions in ascending block id starting
+// Build.  Blocks whose point sets coincide up to a translation (or, with
+// share_mirrored_subdomains, a grid reflection; points in a canonical order)
+// have bitwise equal A_k -- entries depend on integer differences only -- so
+// one representative per class is factorised.
+//   s <= kSmemMaxS (160): k_build, one CTA per block in shared memory: gather,
+//     assemble from integer distances (the K1 entry formula), right-looking
+//     Cholesky A_k = L L^T, then PACKED_INVERSE: L^{-1} (dtrti2 order) and
+//     A_k^{-1} = L^{-T} L^{-1} packed upper by columns; SUBST: G = L^T packed
+//     by rows + 1/G_ii.
+//   larger blocks: assembled into a global workspace and inverted by the
+//     blocked sweep operator (k_sweep_*, rank-32 updates on FP64 tensor
+//     cores), batched over all large blocks; packed output, or full storage
+//     above kBigMaxS (4096) points.
+// Apply.  Per block (k_apply_packed: warp per block, lane-owned slots in
+// registers; k_apply_subst; k_apply_big: row chunks of one large block over
+// many CTAs; k_apply_full) or per class (k_apply_dmma: Z_c = A_c^{-1} [r_k...]
+// on FP64 tensor cores), each writing z_k into a staging buffer; k_scatter*
+// sums, per point, its staged contributions in ascending block id starting
 // from 0.0 -- the reference's association order (precond.py:97-99), no
-// atomics.
+// atomics.  Scratch (staging, partials) is per stream.
 #include <math.h>
 #include <stdlib.h>
 
