@@ -25,6 +25,7 @@
 #include <math.h>
 #include <stdlib.h>
 
+#include <algorithm>
 #include <vector>
 
 #include "common.cuh"
@@ -73,6 +74,12 @@ struct LineArgs {
     int scale_in;
     int scale_out;
     const int* stop;  // device flag: nonzero -> no-op (PCG early exit)
+    // k_fft8 (radix-8, 8 points per thread): per-pass radix-major twiddles,
+    // lines per CTA, strided (column) thread mapping, per-line smem pitch
+    const double2* tw8;
+    int g8;
+    int strided8;
+    int pitch8;
 };
 
 // 2^-e with 2^e >= max|x| (power of two, exact); 1 for max == 0
@@ -489,6 +496,239 @@ __global__ void __launch_bounds__(TPB, 2) k_fft_lines(LineArgs a) {
     }
 }
 
+// ---------------------------------------------------------------------------
+// k_fft8: the production line FFT for 64 <= L <= 4096.  A line is owned by
+// TPL = L/8 threads, 8 points each; passes are radix 8 (the last one radix
+// 2^(logL mod 3) when logL is not a multiple of 3).  Every Stockham pass reads
+// the thread's positions {j + TPL m : m < 8} (butterfly b of NB = 8/R uses
+// m = b + NB r), so the first pass takes the line load straight from
+// registers and the last pass leaves position j + TPL m in register m: it is
+// stored from registers, or -- in the fused column pass -- multiplied by the
+// symbol and fed to the inverse transform without touching shared memory.
+// 64 registers, up to 512 threads per CTA, 2-4 CTAs per SM; twiddles are
+// per-pass radix-major tables read through the L1 cache.
+template <int LOGL>
+struct Plan8 {
+    static constexpr int L = 1 << LOGL;
+    static constexpr int P = (LOGL + 2) / 3;
+    static constexpr int TPL = L / 8;
+    static constexpr int rlog(int p) { return p < P ? 3 : LOGL - 3 * (P - 1); }  // p = 1..P
+    static constexpr int toff(int p) {  // offset of pass p's table (p >= 2)
+        int o = 0;
+        for (int q = 2; q < p; ++q) o += (1 << rlog(q)) << (3 * (q - 1));
+        return o;
+    }
+};
+
+// in-register DFT_R over the NB-strided inputs v[b + NB r]; outputs in natural order
+template <int S, int R>
+__device__ __forceinline__ void dft_r8(double* vr, double* vi, int b, int NB) {
+    double xr[R], xi[R];
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        xr[r] = vr[b + NB * r];
+        xi[r] = vi[b + NB * r];
+    }
+    dft_reg<R, S>(xr, xi);
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+        vr[b + NB * r] = xr[out_slot<R>(r)];
+        vi[b + NB * r] = xi[out_slot<R>(r)];
+    }
+}
+
+// Stockham pass p of a line: twiddle, butterflies, then (p < P) scatter to the
+// line's shared memory and gather the next pass's inputs.
+template <int S, int LOGL, int PASS>
+__device__ __forceinline__ void pass8(double* vr, double* vi, int j, double* re, double* im,
+                                      const double2* __restrict__ tw8) {
+    using PL = Plan8<LOGL>;
+    constexpr int R = 1 << PL::rlog(PASS);
+    constexpr int NB = 8 / R;
+    constexpr int NS = 1 << (3 * (PASS - 1));
+    constexpr int TPL = PL::TPL;
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+        const int jb = j + TPL * b;
+        const int k = jb & (NS - 1);
+        if (PASS > 1) {
+            const double2* tp = tw8 + PL::toff(PASS) + k;
+#pragma unroll
+            for (int r = 1; r < R; ++r) {
+                const double2 t = __ldg(tp + r * NS);
+                const double ti = S < 0 ? t.y : -t.y;
+                const int m = b + NB * r;
+                const double xr = vr[m];
+                vr[m] = fma(xr, t.x, -vi[m] * ti);
+                vi[m] = fma(xr, ti, vi[m] * t.x);
+            }
+        }
+        dft_r8<S, R>(vr, vi, b, NB);
+    }
+    if (PASS == PL::P) return;  // register m now holds position j + TPL m
+    __syncthreads();  // the previous exchange's reads are done
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+        const int jb = j + TPL * b;
+        const int k = jb & (NS - 1);
+        const int o0 = (jb / NS) * NS * R + k;
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const int q = padi(o0 + NS * r);
+            re[q] = vr[b + NB * r];
+            im[q] = vi[b + NB * r];
+        }
+    }
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+        const int q = padi(j + TPL * m);
+        vr[m] = re[q];
+        vi[m] = im[q];
+    }
+}
+
+template <int S, int LOGL>
+__device__ __forceinline__ void fft8_line(double* vr, double* vi, int j, double* re, double* im,
+                                          const double2* __restrict__ tw8) {
+    constexpr int P = Plan8<LOGL>::P;
+    pass8<S, LOGL, 1>(vr, vi, j, re, im, tw8);
+    if constexpr (P >= 2) pass8<S, LOGL, 2>(vr, vi, j, re, im, tw8);
+    if constexpr (P >= 3) pass8<S, LOGL, 3>(vr, vi, j, re, im, tw8);
+    if constexpr (P >= 4) pass8<S, LOGL, 4>(vr, vi, j, re, im, tw8);
+}
+
+__device__ __forceinline__ int64_t line_off(int64_t so, int64_t si, int64_t sl, int lsplit, int64_t sh, int o, int i,
+                                            int l) {
+    return (int64_t)o * so + (int64_t)i * si +
+           (lsplit < 0 ? (int64_t)l * sl
+                       : (int64_t)(l >> lsplit) * sh + (int64_t)(l & ((1 << lsplit) - 1)) * sl);
+}
+
+__device__ void column_scales_dyn(const LineArgs& a, double* sc) {
+    __shared__ double red[2][512];
+    double m0 = 0.0, m1 = 0.0;
+    for (int c = threadIdx.x; c < a.namax; c += blockDim.x) {
+        m0 = fmax(m0, a.amax[2 * c]);
+        m1 = fmax(m1, a.amax[2 * c + 1]);
+    }
+    red[0][threadIdx.x] = m0;
+    red[1][threadIdx.x] = m1;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+        if (threadIdx.x < o) {
+            red[0][threadIdx.x] = fmax(red[0][threadIdx.x], red[0][threadIdx.x + o]);
+            red[1][threadIdx.x] = fmax(red[1][threadIdx.x], red[1][threadIdx.x + o]);
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        sc[0] = pow2_scale(red[0][0]);
+        sc[1] = pow2_scale(red[1][0]);
+    }
+}
+
+template <int MODE, int LOGL>
+__global__ void __launch_bounds__(512, 2) k_fft8(LineArgs a) {
+    using PL = Plan8<LOGL>;
+    constexpr int L = PL::L, TPL = PL::TPL;
+    constexpr bool in_real = MODE == kFwdRC || MODE == kFusedRR;
+    constexpr bool out_real = MODE == kInvCR || MODE == kFusedRR;
+    constexpr bool fused = MODE == kFusedCC || MODE == kFusedRR;
+    extern __shared__ __align__(16) double sm8[];
+    __shared__ double csc[2];
+    if (a.stop && *a.stop) return;
+    const int G = a.g8, t = threadIdx.x;
+    int g, j;
+    if (a.strided8) {
+        g = t % G;
+        j = t / G;
+    } else {
+        g = t / TPL;
+        j = t % TPL;
+    }
+    double* re = sm8 + (int64_t)g * a.pitch8;
+    double* im = sm8 + (int64_t)(G + g) * a.pitch8;
+    const int line = blockIdx.x * G + g;
+    const bool live = line < a.nlines;
+    const int lgi = a.lg_ninner;
+    const int o = line >> lgi, i = line & ((1 << lgi) - 1);
+    if ((in_real && a.scale_in) || (out_real && a.scale_out)) {
+        column_scales_dyn(a, csc);
+        __syncthreads();
+    }
+    double vr[8], vi[8];
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+        const int l = j + TPL * m;
+        vr[m] = vi[m] = 0.0;
+        if (live && l < a.n_in) {
+            const int64_t off = line_off(a.in_so, a.in_si, a.in_sl, a.in_lsplit, a.in_sh, o, i, l);
+            if constexpr (in_real) {
+                vr[m] = __ldg(a.x0 + off);
+                if (a.x1) vi[m] = __ldg(a.x1 + off);
+            } else {
+                const double2 v = a.in_c[off];
+                vr[m] = v.x;
+                vi[m] = v.y;
+            }
+        }
+    }
+    if constexpr (in_real) {
+        if (a.scale_in) {
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                vr[m] *= csc[0];
+                vi[m] *= csc[1];
+            }
+        }
+    }
+    if constexpr (fused) {
+        fft8_line<-1, LOGL>(vr, vi, j, re, im, a.tw8);
+        // folded real symbol at frequency l = j + TPL m along this line
+        const int np1 = a.n + 1;
+        int s0 = 1;
+        for (int d = 1; d < a.dim; ++d) s0 *= np1;
+        int tmp = i + a.line0, off = 0, stride = 1;
+        for (int d = a.dim - 1; d >= 1; --d) {
+            const int k = tmp & (L - 1);
+            tmp >>= LOGL;
+            off += min(k, L - k) * stride;
+            stride *= np1;
+        }
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+            const int l = j + TPL * m;
+            const double lam = live ? __ldg(a.sym + (int64_t)min(l, L - l) * s0 + off) : 0.0;
+            vr[m] *= lam;
+            vi[m] *= lam;
+        }
+        fft8_line<+1, LOGL>(vr, vi, j, re, im, a.tw8);
+    } else if constexpr (MODE == kFwdCC || MODE == kFwdRC) {
+        fft8_line<-1, LOGL>(vr, vi, j, re, im, a.tw8);
+    } else {
+        fft8_line<+1, LOGL>(vr, vi, j, re, im, a.tw8);
+    }
+    if (!live) return;
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+        const int l = j + TPL * m;
+        if (l >= a.n_out) continue;
+        const int64_t off = line_off(a.out_so, a.out_si, a.out_sl, a.out_lsplit, a.out_sh, o, i, l);
+        if constexpr (out_real) {
+            double x = vr[m], y = vi[m];
+            if (a.scale_out) {
+                x /= csc[0];  // exact: powers of two
+                y /= csc[1];
+            }
+            a.y0[off] = x;
+            if (a.y1) a.y1[off] = y;
+        } else {
+            a.out_c[off] = make_double2(vr[m], vi[m]);
+        }
+    }
+}
+
 // Embedding of the generator, mirror-even per axis, index n left zero
 // (toeplitz.py:19-30): emb[k] = gen[fold(k)] with fold(k) = k (k<n),
 // 2n-k (k>n); entries from the same integer-distance formula as K1/K2.
@@ -535,6 +775,7 @@ struct ie_fft {
     int dim, n, M, logM;
     int N;
     double2* d_tw;
+    double2* d_tw8;  // k_fft8 per-pass radix-major twiddles (M >= 64)
     double* d_sym;
     double2* d_buf;
     double* d_amax;  // 2 * ceil(N/2048) partial maxima
@@ -567,6 +808,57 @@ static int launch_modes(const LineArgs& a, cudaStream_t st) {
     return a.sign < 0 ? launch_mode<kFwdCC, TPB>(a, st) : launch_mode<kInvCC, TPB>(a, st);
 }
 
+template <int MODE, int LOGL>
+static int launch_fft8_l(const LineArgs& a, int tpb, int ctas, size_t smem, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        IE_CUDA(cudaFuncSetAttribute(k_fft8<MODE, LOGL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+        attr = true;
+    }
+    k_fft8<MODE, LOGL><<<ctas, tpb, smem, st>>>(a);
+    IE_LAUNCHED();
+    return IE_OK;
+}
+
+template <int MODE>
+static int launch_fft8_m(const LineArgs& a, int tpb, int ctas, size_t smem, cudaStream_t st) {
+    switch (a.logL) {
+        case 6: return launch_fft8_l<MODE, 6>(a, tpb, ctas, smem, st);
+        case 7: return launch_fft8_l<MODE, 7>(a, tpb, ctas, smem, st);
+        case 8: return launch_fft8_l<MODE, 8>(a, tpb, ctas, smem, st);
+        case 9: return launch_fft8_l<MODE, 9>(a, tpb, ctas, smem, st);
+        case 10: return launch_fft8_l<MODE, 10>(a, tpb, ctas, smem, st);
+        case 11: return launch_fft8_l<MODE, 11>(a, tpb, ctas, smem, st);
+        default: return launch_fft8_l<MODE, 12>(a, tpb, ctas, smem, st);
+    }
+}
+
+// k_fft8 launch: lines per CTA and thread mapping from the access pattern
+static int launch_fft8(LineArgs a, cudaStream_t st) {
+    const int tpl = a.L / 8;
+    const bool cin = a.in_real || a.in_sl == 1, cout = a.out_real || a.out_sl == 1;
+    a.strided8 = cin ? 0 : 1;
+    int G, skew;
+    if (a.strided8) {  // lanes alternate lines: >= 32-B row segments per warp request
+        G = tpl >= 512 ? 1 : std::max(2, 256 / tpl);
+        skew = std::max(1, 16 / G);
+    } else {
+        G = std::max(1, 256 / tpl);
+        skew = std::min(tpl, 8);
+    }
+    (void)cout;
+    a.g8 = G;
+    a.pitch8 = (a.L + a.L / 16 + 15) / 16 * 16 + skew;
+    const int tpb = G * tpl;
+    const int ctas = (a.nlines + G - 1) / G;
+    const size_t smem = (size_t)2 * G * a.pitch8 * sizeof(double);
+    if (a.fused) return a.in_real ? launch_fft8_m<kFusedRR>(a, tpb, ctas, smem, st)
+                                  : launch_fft8_m<kFusedCC>(a, tpb, ctas, smem, st);
+    if (a.in_real) return launch_fft8_m<kFwdRC>(a, tpb, ctas, smem, st);
+    if (a.out_real) return launch_fft8_m<kInvCR>(a, tpb, ctas, smem, st);
+    return a.sign < 0 ? launch_fft8_m<kFwdCC>(a, tpb, ctas, smem, st) : launch_fft8_m<kInvCC>(a, tpb, ctas, smem, st);
+}
+
 static int line_launch(const LineArgs& a_in, cudaStream_t st) {
     LineArgs a = a_in;
     a.lg_ninner = 0;
@@ -574,6 +866,11 @@ static int line_launch(const LineArgs& a_in, cudaStream_t st) {
     if ((1 << a.lg_ninner) != a.ninner) {
         set_error("fft: line layout must be a power of two");
         return IE_ERR_ARG;
+    }
+    {
+        static const bool v1 = getenv("IEDD_B200_FFT_V1") != nullptr;
+        const bool cin = a.in_real || a.in_sl == 1, cout = a.out_real || a.out_sl == 1;
+        if (!v1 && a.tw8 && a.logL >= 6 && a.logL <= 12 && cin == cout) return launch_fft8(a, st);
     }
     // 256-thread CTAs (4096 points) unless that leaves the GPU under-filled and
     // the lines fit a 32-thread CTA (512 points)
@@ -584,6 +881,7 @@ static int line_launch(const LineArgs& a_in, cudaStream_t st) {
 
 static LineArgs base_args(const ie_fft* f) {
     LineArgs a{};
+    a.tw8 = f->d_tw8;
     a.amax = f->d_amax;
     a.namax = (f->N + 2047) / 2048;
     a.L = f->M;
@@ -653,6 +951,19 @@ int fft_create(const ie_geom& g, ie_fft** out) {
     }
     IE_CUDA(cudaMalloc(&f->d_tw, M * sizeof(double2)));
     IE_CUDA(cudaMemcpy(f->d_tw, tw.data(), M * sizeof(double2), cudaMemcpyHostToDevice));
+    f->d_tw8 = nullptr;
+    if (logM >= 6) {
+        // pass p >= 2 (Ns = 8^(p-1), radix R_p): t[r * Ns + k] = exp(-2 pi i r k / (R_p Ns)) = tw[r k M / (R_p Ns)]
+        const int P = (logM + 2) / 3;
+        std::vector<double2> t8;
+        for (int p = 2; p <= P; ++p) {
+            const int rl = p < P ? 3 : logM - 3 * (P - 1), R = 1 << rl, Ns = 1 << (3 * (p - 1));
+            for (int r = 0; r < R; ++r)
+                for (int k = 0; k < Ns; ++k) t8.push_back(tw[(int64_t)r * k * (M / (R * Ns)) % M]);
+        }
+        IE_CUDA(cudaMalloc(&f->d_tw8, t8.size() * sizeof(double2)));
+        IE_CUDA(cudaMemcpy(f->d_tw8, t8.data(), t8.size() * sizeof(double2), cudaMemcpyHostToDevice));
+    }
     IE_CUDA(cudaMalloc(&f->d_sym, totS * sizeof(double)));
     IE_CUDA(cudaMalloc(&f->d_buf, totB * sizeof(double2)));
     // symbol: embed, full forward FFT, fold
@@ -677,6 +988,7 @@ int fft_create(const ie_geom& g, ie_fft** out) {
 void fft_destroy(ie_fft* f) {
     if (!f) return;
     cudaFree(f->d_tw);
+    cudaFree(f->d_tw8);
     cudaFree(f->d_sym);
     cudaFree(f->d_buf);
     cudaFree(f->d_amax);
