@@ -606,30 +606,34 @@ __device__ __forceinline__ int64_t line_off(int64_t so, int64_t si, int64_t sl, 
 }
 
 __device__ void column_scales_dyn(const LineArgs& a, double* sc) {
-    __shared__ double red[2][512];
+    __shared__ double red[2][32];
     double m0 = 0.0, m1 = 0.0;
     for (int c = threadIdx.x; c < a.namax; c += blockDim.x) {
         m0 = fmax(m0, a.amax[2 * c]);
         m1 = fmax(m1, a.amax[2 * c + 1]);
     }
-    red[0][threadIdx.x] = m0;
-    red[1][threadIdx.x] = m1;
-    __syncthreads();
-    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-        if (threadIdx.x < o) {
-            red[0][threadIdx.x] = fmax(red[0][threadIdx.x], red[0][threadIdx.x + o]);
-            red[1][threadIdx.x] = fmax(red[1][threadIdx.x], red[1][threadIdx.x + o]);
-        }
-        __syncthreads();
+    for (int o = 16; o > 0; o >>= 1) {
+        m0 = fmax(m0, __shfl_xor_sync(0xffffffffu, m0, o));
+        m1 = fmax(m1, __shfl_xor_sync(0xffffffffu, m1, o));
     }
+    const int w = threadIdx.x >> 5, nw = (blockDim.x + 31) >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        red[0][w] = m0;
+        red[1][w] = m1;
+    }
+    __syncthreads();
     if (threadIdx.x == 0) {
-        sc[0] = pow2_scale(red[0][0]);
-        sc[1] = pow2_scale(red[1][0]);
+        for (int q = 1; q < nw; ++q) {
+            m0 = fmax(m0, red[0][q]);
+            m1 = fmax(m1, red[1][q]);
+        }
+        sc[0] = pow2_scale(m0);
+        sc[1] = pow2_scale(m1);
     }
 }
 
 template <int MODE, int LOGL>
-__global__ void __launch_bounds__(512, 2) k_fft8(LineArgs a) {
+__global__ void __launch_bounds__(1024, 1) k_fft8(LineArgs a) {
     using PL = Plan8<LOGL>;
     constexpr int L = PL::L, TPL = PL::TPL;
     constexpr bool in_real = MODE == kFwdRC || MODE == kFusedRR;
@@ -839,8 +843,9 @@ static int launch_fft8(LineArgs a, cudaStream_t st) {
     const bool cin = a.in_real || a.in_sl == 1, cout = a.out_real || a.out_sl == 1;
     a.strided8 = cin ? 0 : 1;
     int G, skew;
-    if (a.strided8) {  // lanes alternate lines: >= 32-B row segments per warp request
-        G = tpl >= 512 ? 1 : std::max(2, 256 / tpl);
+    if (a.strided8) {  // lanes alternate lines: 32-B row segments per warp request (G = 2 measured best)
+        static const int gs = getenv("IEDD_B200_FFT_G") ? atoi(getenv("IEDD_B200_FFT_G")) : 2;
+        G = std::max(std::min(gs, 1024 / tpl), std::min(32, 256 / tpl));
         skew = std::max(1, 16 / G);
     } else {
         G = std::max(1, 256 / tpl);
