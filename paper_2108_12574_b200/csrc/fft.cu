@@ -241,6 +241,33 @@ __device__ __forceinline__ void dft_reg(double* r, double* i) {
     }
 }
 
+// dft_reg<8> for inputs 4..7 known to be zero (zero-padded forward lines):
+// the same arithmetic minus the additions of zeros, so bitwise the same result.
+template <int S>
+__device__ __forceinline__ void dft4_half(double* r, double* i, int a0, int a1, int a2, int a3) {
+    const double ar = r[a0], ai = i[a0], br = r[a1], bi = i[a1];
+    const double er = -S * bi, ei = S * br;
+    r[a0] = ar + br;
+    i[a0] = ai + bi;
+    r[a2] = ar - br;
+    i[a2] = ai - bi;
+    r[a1] = ar + er;
+    i[a1] = ai + ei;
+    r[a3] = ar - er;
+    i[a3] = ai - ei;
+}
+
+template <int S>
+__device__ __forceinline__ void dft8_zero_hi(double* r, double* i) {
+    dft4_half<S>(r, i, 0, 2, 4, 6);
+    dft4_half<S>(r, i, 1, 3, 5, 7);
+    rot16<S, 2>(r[3], i[3]);
+    rot16<S, 4>(r[5], i[5]);
+    rot16<S, 6>(r[7], i[7]);
+#pragma unroll
+    for (int k1 = 0; k1 < 4; ++k1) dft2<S>(r[2 * k1], i[2 * k1], r[2 * k1 + 1], i[2 * k1 + 1]);
+}
+
 // register holding DFT output k after dft_reg<R>
 template <int R>
 __host__ __device__ constexpr int out_slot(int k) {
@@ -541,7 +568,7 @@ __device__ __forceinline__ void dft_r8(double* vr, double* vi, int b, int NB) {
 // line's shared memory and gather the next pass's inputs.
 template <int S, int LOGL, int PASS>
 __device__ __forceinline__ void pass8(double* vr, double* vi, int j, double* re, double* im,
-                                      const double2* __restrict__ tw8) {
+                                      const double2* __restrict__ tw8, bool zero_hi = false) {
     using PL = Plan8<LOGL>;
     constexpr int R = 1 << PL::rlog(PASS);
     constexpr int NB = 8 / R;
@@ -563,7 +590,22 @@ __device__ __forceinline__ void pass8(double* vr, double* vi, int j, double* re,
                 vi[m] = fma(xr, ti, vi[m] * t.x);
             }
         }
-        dft_r8<S, R>(vr, vi, b, NB);
+        if (PASS == 1 && zero_hi) {  // R == 8, NB == 1: inputs j + TPL m, m >= 4, are zero padding
+            dft8_zero_hi<S>(vr, vi);
+            double xr[8], xi[8];
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                xr[r] = vr[r];
+                xi[r] = vi[r];
+            }
+#pragma unroll
+            for (int r = 0; r < 8; ++r) {
+                vr[r] = xr[out_slot<8>(r)];
+                vi[r] = xi[out_slot<8>(r)];
+            }
+        } else {
+            dft_r8<S, R>(vr, vi, b, NB);
+        }
     }
     if (PASS == PL::P) return;  // register m now holds position j + TPL m
     __syncthreads();  // the previous exchange's reads are done
@@ -590,9 +632,9 @@ __device__ __forceinline__ void pass8(double* vr, double* vi, int j, double* re,
 
 template <int S, int LOGL>
 __device__ __forceinline__ void fft8_line(double* vr, double* vi, int j, double* re, double* im,
-                                          const double2* __restrict__ tw8) {
+                                          const double2* __restrict__ tw8, bool zero_hi = false) {
     constexpr int P = Plan8<LOGL>::P;
-    pass8<S, LOGL, 1>(vr, vi, j, re, im, tw8);
+    pass8<S, LOGL, 1>(vr, vi, j, re, im, tw8, zero_hi);
     if constexpr (P >= 2) pass8<S, LOGL, 2>(vr, vi, j, re, im, tw8);
     if constexpr (P >= 3) pass8<S, LOGL, 3>(vr, vi, j, re, im, tw8);
     if constexpr (P >= 4) pass8<S, LOGL, 4>(vr, vi, j, re, im, tw8);
@@ -687,8 +729,9 @@ __global__ void __launch_bounds__(1024, 1) k_fft8(LineArgs a) {
             }
         }
     }
+    const bool zero_hi = a.n_in <= L / 2;  // line positions j + TPL m, m >= 4, read as zero
     if constexpr (fused) {
-        fft8_line<-1, LOGL>(vr, vi, j, re, im, a.tw8);
+        fft8_line<-1, LOGL>(vr, vi, j, re, im, a.tw8, zero_hi);
         // folded real symbol at frequency l = j + TPL m along this line
         const int np1 = a.n + 1;
         int s0 = 1;
@@ -709,9 +752,9 @@ __global__ void __launch_bounds__(1024, 1) k_fft8(LineArgs a) {
         }
         fft8_line<+1, LOGL>(vr, vi, j, re, im, a.tw8);
     } else if constexpr (MODE == kFwdCC || MODE == kFwdRC) {
-        fft8_line<-1, LOGL>(vr, vi, j, re, im, a.tw8);
+        fft8_line<-1, LOGL>(vr, vi, j, re, im, a.tw8, zero_hi);
     } else {
-        fft8_line<+1, LOGL>(vr, vi, j, re, im, a.tw8);
+        fft8_line<+1, LOGL>(vr, vi, j, re, im, a.tw8, zero_hi);
     }
     if (!live) return;
 #pragma unroll
