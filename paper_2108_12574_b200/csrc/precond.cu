@@ -491,14 +491,26 @@ __global__ void __launch_bounds__(256, 2) k_apply_dmma(GemmArgs a) {
     }
     cp_async_commit();
     const int nchunks = (s + kGemmKC - 1) / kGemmKC;
+    // a chunk is kc contiguous rows of A: element e = kk * s + i of the chunk goes to
+    // smem row kk, column i; this thread's (kk, i) are the same for every chunk
+    constexpr int kQ = (kGemmKC * kSmemMaxS + 255) / 256;
+    int a_dst[kQ];
+#pragma unroll
+    for (int q = 0; q < kQ; ++q) {
+        const int e = tid + 256 * q;
+        const int kk = e / s;
+        a_dst[q] = kk * AP + (e - kk * s);
+    }
     auto load_chunk = [&](int ch) {
         if (ch < nchunks) {
             double* dst = As + (ch % kDmmaStages) * kGemmKC * AP;
             const int k0 = ch * kGemmKC;
             const int kc = min(kGemmKC, s - k0);
-            for (int e = tid; e < kc * s; e += 256) {
-                const int kk = e / s, i = e - kk * s;
-                cp_async8(dst + kk * AP + i, A + (int64_t)(k0 + kk) * s + i);
+            const double* src = A + (int64_t)k0 * s;
+#pragma unroll
+            for (int q = 0; q < kQ; ++q) {
+                const int e = tid + 256 * q;
+                if (e < kc * s) cp_async8(dst + a_dst[q], src + e);
             }
         }
         cp_async_commit();  // always commit (possibly empty) so group counting stays uniform
