@@ -458,8 +458,6 @@ __global__ void __launch_bounds__(TPB, 2) k_fft_lines(LineArgs a) {
         // A thread's 16 points lie on at most 16 lines: per-point line offsets first,
         // then all 16 symbol loads in flight, then the multiplies.
         const int np1 = a.n + 1;
-        int s0 = 1;
-        for (int d = 1; d < a.dim; ++d) s0 *= np1;
         double lam[16];
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
@@ -473,7 +471,7 @@ __global__ void __launch_bounds__(TPB, 2) k_fft_lines(LineArgs a) {
                 off += min(k, L - k) * stride;
                 stride *= np1;
             }
-            lam[q] = line < a.nlines ? __ldg(a.sym + (int64_t)min(l, L - l) * s0 + off) : 0.0;
+            lam[q] = line < a.nlines ? __ldg(a.sym + (int64_t)off * np1 + min(l, L - l)) : 0.0;
         }
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
@@ -734,8 +732,6 @@ __global__ void __launch_bounds__(1024, 1) k_fft8(LineArgs a) {
         fft8_line<-1, LOGL>(vr, vi, j, re, im, a.tw8, zero_hi);
         // folded real symbol at frequency l = j + TPL m along this line
         const int np1 = a.n + 1;
-        int s0 = 1;
-        for (int d = 1; d < a.dim; ++d) s0 *= np1;
         int tmp = i + a.line0, off = 0, stride = 1;
         for (int d = a.dim - 1; d >= 1; --d) {
             const int k = tmp & (L - 1);
@@ -744,13 +740,18 @@ __global__ void __launch_bounds__(1024, 1) k_fft8(LineArgs a) {
             stride *= np1;
         }
 #pragma unroll
+        const double* symline = a.sym + (int64_t)off * np1;  // axis 0 fastest: contiguous along the line
         for (int m = 0; m < 8; ++m) {
             const int l = j + TPL * m;
-            const double lam = live ? __ldg(a.sym + (int64_t)min(l, L - l) * s0 + off) : 0.0;
+            const double lam = live ? __ldg(symline + min(l, L - l)) : 0.0;
             vr[m] *= lam;
             vi[m] *= lam;
         }
-        fft8_line<+1, LOGL>(vr, vi, j, re, im, a.tw8);
+        // opaque copy of the line position: the inverse recomputes its exchange
+        // addresses instead of keeping the forward's alive (64-register budget)
+        int jj = j;
+        asm volatile("" : "+r"(jj));
+        fft8_line<+1, LOGL>(vr, vi, jj, re, im, a.tw8);
     } else if constexpr (MODE == kFwdCC || MODE == kFwdRC) {
         fft8_line<-1, LOGL>(vr, vi, j, re, im, a.tw8, zero_hi);
     } else {
@@ -798,20 +799,26 @@ __global__ void k_embed(double2* emb, int dim, int n, EntryParams P, const LogEn
     emb[e] = make_double2(zero ? 0.0 : entry_from_m(P, tab, m), 0.0);
 }
 
-// sym[(k_0..k_{d-1}) folded, k <= n] = Re(emb_hat[k]) / M^dim
+// sym[k_0 + (n+1) * rest(k_1..k_{d-1})] = Re(emb_hat[k]) / M^dim, k folded (<= n);
+// axis 0 (the fused column pass's line axis) fastest so a line reads its symbol
+// contiguously; rest = C order over axes 1..d-1 (last fastest)
 __global__ void k_fold_symbol(const double2* emb, double* sym, int dim, int n, double scale) {
     const int np1 = n + 1, M = 2 * n;
     int64_t tot = 1;
     for (int d = 0; d < dim; ++d) tot *= np1;
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (e >= tot) return;
-    int64_t t = e, src = 0, mul = 1;
-    for (int d = dim - 1; d >= 0; --d) {
+    int64_t t = e, mul = 1;
+    const int k0 = (int)(t % np1);
+    t /= np1;
+    int64_t src = 0;
+    for (int d = dim - 1; d >= 1; --d) {
         const int k = (int)(t % np1);
         t /= np1;
         src += (int64_t)k * mul;
         mul *= M;
     }
+    src += (int64_t)k0 * mul;
     sym[e] = emb[src].x * scale;
 }
 
