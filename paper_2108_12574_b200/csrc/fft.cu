@@ -278,6 +278,11 @@ __host__ __device__ constexpr int out_slot(int k) {
 // elements -> the stride-16 Stockham stores of the first pass and the strided
 // loads are bank-conflict free (two wavefronts per warp access).
 __device__ __forceinline__ int padi(int i) { return i + (i >> 4); }
+// k_fft8 exchange padding: one slot per 2^PADS (PADS = 3 for the strided
+// two-line mapping: bank-conflict free for stores and loads, per a half-warp
+// model of 8-byte shared accesses; 4 for the contiguous mapping)
+template <int PADS>
+__device__ __forceinline__ int padq(int i) { return i + (i >> PADS); }
 
 // One Stockham pass of radix R over the CTA's lines (16 points per thread).
 // Twiddles of the Ns = 16 pass, radix-major: t16[r * 16 + k] = exp(-2 pi i r k / (16 R));
@@ -564,7 +569,7 @@ __device__ __forceinline__ void dft_r8(double* vr, double* vi, int b, int NB) {
 
 // Stockham pass p of a line: twiddle, butterflies, then (p < P) scatter to the
 // line's shared memory and gather the next pass's inputs.
-template <int S, int LOGL, int PASS>
+template <int S, int LOGL, int PASS, int PADS>
 __device__ __forceinline__ void pass8(double* vr, double* vi, int j, double* re, double* im,
                                       const double2* __restrict__ tw8, bool zero_hi = false) {
     using PL = Plan8<LOGL>;
@@ -614,7 +619,7 @@ __device__ __forceinline__ void pass8(double* vr, double* vi, int j, double* re,
         const int o0 = (jb / NS) * NS * R + k;
 #pragma unroll
         for (int r = 0; r < R; ++r) {
-            const int q = padi(o0 + NS * r);
+            const int q = padq<PADS>(o0 + NS * r);
             re[q] = vr[b + NB * r];
             im[q] = vi[b + NB * r];
         }
@@ -622,20 +627,20 @@ __device__ __forceinline__ void pass8(double* vr, double* vi, int j, double* re,
     __syncthreads();
 #pragma unroll
     for (int m = 0; m < 8; ++m) {
-        const int q = padi(j + TPL * m);
+        const int q = padq<PADS>(j + TPL * m);
         vr[m] = re[q];
         vi[m] = im[q];
     }
 }
 
-template <int S, int LOGL>
+template <int S, int LOGL, int PADS>
 __device__ __forceinline__ void fft8_line(double* vr, double* vi, int j, double* re, double* im,
                                           const double2* __restrict__ tw8, bool zero_hi = false) {
     constexpr int P = Plan8<LOGL>::P;
-    pass8<S, LOGL, 1>(vr, vi, j, re, im, tw8, zero_hi);
-    if constexpr (P >= 2) pass8<S, LOGL, 2>(vr, vi, j, re, im, tw8);
-    if constexpr (P >= 3) pass8<S, LOGL, 3>(vr, vi, j, re, im, tw8);
-    if constexpr (P >= 4) pass8<S, LOGL, 4>(vr, vi, j, re, im, tw8);
+    pass8<S, LOGL, 1, PADS>(vr, vi, j, re, im, tw8, zero_hi);
+    if constexpr (P >= 2) pass8<S, LOGL, 2, PADS>(vr, vi, j, re, im, tw8);
+    if constexpr (P >= 3) pass8<S, LOGL, 3, PADS>(vr, vi, j, re, im, tw8);
+    if constexpr (P >= 4) pass8<S, LOGL, 4, PADS>(vr, vi, j, re, im, tw8);
 }
 
 __device__ __forceinline__ int64_t line_off(int64_t so, int64_t si, int64_t sl, int lsplit, int64_t sh, int o, int i,
@@ -672,8 +677,9 @@ __device__ void column_scales_dyn(const LineArgs& a, double* sc) {
     }
 }
 
-template <int MODE, int LOGL>
+template <int MODE, int LOGL, bool STRIDED>
 __global__ void __launch_bounds__(1024, 1) k_fft8(LineArgs a) {
+    constexpr int PADS = STRIDED ? 3 : 4;
     using PL = Plan8<LOGL>;
     constexpr int L = PL::L, TPL = PL::TPL;
     constexpr bool in_real = MODE == kFwdRC || MODE == kFusedRR;
@@ -684,7 +690,7 @@ __global__ void __launch_bounds__(1024, 1) k_fft8(LineArgs a) {
     if (a.stop && *a.stop) return;
     const int G = a.g8, t = threadIdx.x;
     int g, j;
-    if (a.strided8) {
+    if constexpr (STRIDED) {
         g = t % G;
         j = t / G;
     } else {
@@ -729,7 +735,7 @@ __global__ void __launch_bounds__(1024, 1) k_fft8(LineArgs a) {
     }
     const bool zero_hi = a.n_in <= L / 2;  // line positions j + TPL m, m >= 4, read as zero
     if constexpr (fused) {
-        fft8_line<-1, LOGL>(vr, vi, j, re, im, a.tw8, zero_hi);
+        fft8_line<-1, LOGL, PADS>(vr, vi, j, re, im, a.tw8, zero_hi);
         // folded real symbol at frequency l = j + TPL m along this line
         const int np1 = a.n + 1;
         int tmp = i + a.line0, off = 0, stride = 1;
@@ -751,11 +757,11 @@ __global__ void __launch_bounds__(1024, 1) k_fft8(LineArgs a) {
         // addresses instead of keeping the forward's alive (64-register budget)
         int jj = j;
         asm volatile("" : "+r"(jj));
-        fft8_line<+1, LOGL>(vr, vi, jj, re, im, a.tw8);
+        fft8_line<+1, LOGL, PADS>(vr, vi, jj, re, im, a.tw8);
     } else if constexpr (MODE == kFwdCC || MODE == kFwdRC) {
-        fft8_line<-1, LOGL>(vr, vi, j, re, im, a.tw8, zero_hi);
+        fft8_line<-1, LOGL, PADS>(vr, vi, j, re, im, a.tw8, zero_hi);
     } else {
-        fft8_line<+1, LOGL>(vr, vi, j, re, im, a.tw8, zero_hi);
+        fft8_line<+1, LOGL, PADS>(vr, vi, j, re, im, a.tw8, zero_hi);
     }
     if (!live) return;
 #pragma unroll
@@ -862,16 +868,26 @@ static int launch_modes(const LineArgs& a, cudaStream_t st) {
     return a.sign < 0 ? launch_mode<kFwdCC, TPB>(a, st) : launch_mode<kInvCC, TPB>(a, st);
 }
 
-template <int MODE, int LOGL>
-static int launch_fft8_l(const LineArgs& a, int tpb, int ctas, size_t smem, cudaStream_t st) {
+template <int MODE, int LOGL, bool STRIDED>
+static int launch_fft8_ls(const LineArgs& a, int tpb, int ctas, size_t smem, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        IE_CUDA(cudaFuncSetAttribute(k_fft8<MODE, LOGL>, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
+        IE_CUDA(cudaFuncSetAttribute(k_fft8<MODE, LOGL, STRIDED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     160 * 1024));
         attr = true;
     }
-    k_fft8<MODE, LOGL><<<ctas, tpb, smem, st>>>(a);
+    k_fft8<MODE, LOGL, STRIDED><<<ctas, tpb, smem, st>>>(a);
     IE_LAUNCHED();
     return IE_OK;
+}
+
+// real-in / real-out lines are always contiguous (launch_fft8)
+template <int MODE, int LOGL>
+static int launch_fft8_l(const LineArgs& a, int tpb, int ctas, size_t smem, cudaStream_t st) {
+    if constexpr (MODE == kFwdCC || MODE == kInvCC || MODE == kFusedCC) {
+        if (a.strided8) return launch_fft8_ls<MODE, LOGL, true>(a, tpb, ctas, smem, st);
+    }
+    return launch_fft8_ls<MODE, LOGL, false>(a, tpb, ctas, smem, st);
 }
 
 template <int MODE>
@@ -903,7 +919,8 @@ static int launch_fft8(LineArgs a, cudaStream_t st) {
     }
     (void)cout;
     a.g8 = G;
-    a.pitch8 = (a.L + a.L / 16 + 15) / 16 * 16 + skew;
+    const int pads = a.strided8 ? 3 : 4;  // k_fft8's PADS
+    a.pitch8 = (a.L + (a.L >> pads) + 15) / 16 * 16 + skew;
     const int tpb = G * tpl;
     const int ctas = (a.nlines + G - 1) / G;
     const size_t smem = (size_t)2 * G * a.pitch8 * sizeof(double);
