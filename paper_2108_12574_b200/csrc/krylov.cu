@@ -22,6 +22,7 @@
 #include <stdlib.h>
 #include <string.h>
 
+#include <algorithm>
 #include <chrono>
 #include <mutex>
 #include <string>
@@ -30,6 +31,7 @@
 #include <nccl.h>
 
 #include "common.cuh"
+#include "pcg_state.cuh"
 
 struct ie_matvec;
 struct ie_precond;
@@ -47,19 +49,9 @@ int matvec_N(const ie_matvec* m);
 uint64_t matvec_uid(const ie_matvec* m);
 uint64_t precond_uid(const ie_precond* p);
 
-constexpr int kChunk = 2048;
-constexpr int kRed = 256;
+constexpr int kChunk = kPcgChunk;
+constexpr int kRed = kPcgRed;
 int dot_chunks(int64_t n) { return (int)((n + kChunk - 1) / kChunk); }
-
-__device__ __forceinline__ double block_tree(double v, double* sh) {
-    sh[threadIdx.x] = v;
-    __syncthreads();
-    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-        if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
-        __syncthreads();
-    }
-    return sh[0];
-}
 
 // mode 0: partial of x.y;  mode 1: partial of |x - y|^2
 __global__ void __launch_bounds__(kRed) k_dot_partials(const double* x, const double* y, int N, int mode,
@@ -83,28 +75,8 @@ __global__ void __launch_bounds__(kRed) k_dot_partials(const double* x, const do
     if (threadIdx.x == 0) part[blockIdx.x] = t;
 }
 
-__device__ double reduce_partials(const double* part, int nch, double* sh) {
-    double loc = 0.0;
-    for (int c = threadIdx.x; c < nch; c += blockDim.x) loc += part[c];
-    return block_tree(loc, sh);
-}
-
-// Device-resident PCG state.  Every iteration kernel returns immediately
-// once `stop` is set, so the host can enqueue iterations ahead and read the
-// status once per batch (pcg.py's control flow runs in k_control_a).
-struct PcgState {
-    double rho[2];  // rho_j = r_j . z_j in slot j & 1 (read and written by different launches)
-    double alpha, beta, denom, nf, tol, fail_value;
-    long long max_iters, n_it, fail_iter;
-    long long it_dev;  // iteration index for graph-replayed iterations (it < 0 in the kernel args)
-    int status;  // 0 running, 1 converged, 2 stagnated, 3 max_iters, 4 breakdown, 5 non-finite
-    int stop;
-};
 
 __global__ void k_set_it(PcgState* s, long long it) { s->it_dev = it; }
-__global__ void k_advance_it(PcgState* s) {
-    if (!s->stop) s->it_dev += 1;
-}
 
 __global__ void k_pcg_init(const double* part, int nch, PcgState* s, double tol, long long max_iters,
                            double* hist) {
@@ -120,6 +92,7 @@ __global__ void k_pcg_init(const double* part, int nch, PcgState* s, double tol,
         s->fail_value = 0.0;
         s->status = 0;
         s->stop = 0;
+        s->ticket = 0;
         hist[0] = 1.0;
         if (s->nf == 0.0) {  // pcg.py:74-78
             hist[0] = 0.0;
@@ -132,26 +105,16 @@ __global__ void k_pcg_init(const double* part, int nch, PcgState* s, double tol,
 // Fused control + update kernels (one CTA per 2048-element chunk).  Every
 // CTA reduces the same fixed-chunk partials in the same order, so all CTAs
 // take the same decision; CTA 0 records it in the state.
-__device__ __forceinline__ double chunk_absmax(double v, double* sh) {
-    sh[threadIdx.x] = v;
-    __syncthreads();
-    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-        if (threadIdx.x < o) sh[threadIdx.x] = fmax(sh[threadIdx.x], sh[threadIdx.x + o]);
-        __syncthreads();
-    }
-    return sh[0];
-}
 
 // After the A-pass of iteration `it`: residual / stagnation check of
 // iteration it-1 (pcg.py:107-119), breakdown test of iteration it
 // (pcg.py:99-103), alpha, then u += alpha p, r -= alpha q and max|u| per chunk.
-__global__ void __launch_bounds__(kRed) k_iter_a(const double* part_pq, const double* part_res, int nch, int do_p,
-                                                 int pending, long long it, PcgState* s, double* hist, double* u,
-                                                 double* r, const double* p, const double* q, int N, double* amax) {
-    __shared__ double sh[kRed];
+// Control: every CTA reduces the same partials in the same order and takes
+// the same decision (returned); CTA 0 records it in the state.
+__device__ __forceinline__ int iter_a_control(const double* part_pq, const double* part_res, int nch, int do_p,
+                                              int pending, long long it, PcgState* s, double* hist, double* sh,
+                                              double* denom_out) {
     __shared__ int decided;
-    if (s->stop) return;
-    if (it < 0) it = s->it_dev;
     double denom = 0.0, res2 = 0.0;
     if (do_p) denom = reduce_partials(part_pq, nch, sh);
     __syncthreads();
@@ -189,9 +152,13 @@ __global__ void __launch_bounds__(kRed) k_iter_a(const double* part_pq, const do
         }
     }
     __syncthreads();
-    if (decided || !do_p) return;
-    const double al = s->rho[(it - 1) & 1] / denom;
-    const int base = blockIdx.x * kChunk;
+    *denom_out = denom;
+    return decided;
+}
+
+__device__ __forceinline__ void iter_a_chunk(int c, double al, double* u, double* r, const double* p,
+                                             const double* q, int N, double* amax, double* sh) {
+    const int base = c * kChunk;
     double m = 0.0;
 #pragma unroll
     for (int e = 0; e < kChunk / kRed; ++e) {
@@ -204,7 +171,19 @@ __global__ void __launch_bounds__(kRed) k_iter_a(const double* part_pq, const do
         }
     }
     m = chunk_absmax(m, sh);
-    if (threadIdx.x == 0) amax[2 * blockIdx.x + 1] = m;
+    if (threadIdx.x == 0) amax[2 * c + 1] = m;
+}
+
+__global__ void __launch_bounds__(kRed) k_iter_a(const double* part_pq, const double* part_res, int nch, int do_p,
+                                                 int pending, long long it, PcgState* s, double* hist, double* u,
+                                                 double* r, const double* p, const double* q, int N, double* amax) {
+    __shared__ double sh[kRed];
+    if (s->stop) return;
+    if (it < 0) it = s->it_dev;
+    double denom;
+    const int decided = iter_a_control(part_pq, part_res, nch, do_p, pending, it, s, hist, sh, &denom);
+    if (decided || !do_p) return;
+    iter_a_chunk(blockIdx.x, s->rho[(it - 1) & 1] / denom, u, r, p, q, N, amax, sh);
 }
 
 // After the apply: rho_it = r.z, beta = rho_it / rho_{it-1}, p = z + beta p,
@@ -213,27 +192,20 @@ __global__ void __launch_bounds__(kRed) k_iter_b(const double* part_rz, int nch,
                                                  double* p, const double* z, int N, double* amax) {
     __shared__ double sh[kRed];
     if (s->stop) return;
-    if (it < 0) it = s->it_dev;
-    const double rz = reduce_partials(part_rz, nch, sh);
-    const double beta = rz / s->rho[(it - 1) & 1];
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        s->beta = beta;
-        s->rho[it & 1] = rz;
-    }
-    const int base = blockIdx.x * kChunk;
-    double m = 0.0;
-#pragma unroll
-    for (int e = 0; e < kChunk / kRed; ++e) {
-        const int i = base + e * kRed + threadIdx.x;
-        if (i < N) {
-            const double pn = __dadd_rn(z[i], __dmul_rn(beta, p[i]));
-            p[i] = pn;
-            m = fmax(m, fabs(pn));
+    const bool replay = it < 0;
+    if (replay) it = s->it_dev;
+    const double beta = iter_b_beta(part_rz, nch, it, s, sh);
+    iter_b_chunk(blockIdx.x, beta, p, z, N, amax, sh);
+    if (replay) {  // graph replay: the last CTA (every CTA has read it_dev) advances the iteration
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            __threadfence();
+            if (atomicAdd(&s->ticket, 1u) == gridDim.x - 1) {
+                s->ticket = 0;
+                s->it_dev += 1;
+            }
         }
     }
-    __syncthreads();
-    m = chunk_absmax(m, sh);
-    if (threadIdx.x == 0) amax[2 * blockIdx.x] = m;
 }
 
 __global__ void k_pcg_rho0(const double* part_rz, int nch, PcgState* s) {
@@ -243,11 +215,10 @@ __global__ void k_pcg_rho0(const double* part_rz, int nch, PcgState* s) {
     if (threadIdx.x == 0) s->rho[0] = rz;
 }
 
-__global__ void k_post_pass(const double* p, const double* q, const double* f, const double* w, int N, int do_p,
-                            int pending, double* part_pq, double* part_res, const int* stop) {
-    __shared__ double sh[kRed];
-    if (*stop) return;
-    const int base = blockIdx.x * kChunk;
+__device__ __forceinline__ void post_pass_chunk(int c, const double* p, const double* q, const double* f,
+                                                const double* w, int N, int do_p, int pending, double* part_pq,
+                                                double* part_res, double* sh) {
+    const int base = c * kChunk;
     double a = 0.0, b = 0.0;
 #pragma unroll
     for (int e = 0; e < kChunk / kRed; ++e) {
@@ -262,13 +233,21 @@ __global__ void k_post_pass(const double* p, const double* q, const double* f, c
     }
     if (do_p) {
         const double t = block_tree(a, sh);
-        if (threadIdx.x == 0) part_pq[blockIdx.x] = t;
+        if (threadIdx.x == 0) part_pq[c] = t;
         __syncthreads();
     }
     if (pending) {
         const double t = block_tree(b, sh);
-        if (threadIdx.x == 0) part_res[blockIdx.x] = t;
+        if (threadIdx.x == 0) part_res[c] = t;
+        __syncthreads();
     }
+}
+
+__global__ void k_post_pass(const double* p, const double* q, const double* f, const double* w, int N, int do_p,
+                            int pending, double* part_pq, double* part_res, const int* stop) {
+    __shared__ double sh[kRed];
+    if (*stop) return;
+    post_pass_chunk(blockIdx.x, p, q, f, w, N, do_p, pending, part_pq, part_res, sh);
 }
 
 __global__ void k_copy_if_running(double* dst, const double* src, int N, const int* stop) {
@@ -514,10 +493,7 @@ extern "C" int ie_pcg_f64(const ie_matvec* A, const ie_precond* T, const double*
             if (T && (rc = precond_prepare_stream(T, W->cap_stream))) return rc;
             if ((rc = matvec_prepare_stream(A, W->cap_stream))) return rc;
             IE_CUDA(cudaStreamBeginCapture(W->cap_stream, cudaStreamCaptureModeThreadLocal));
-            int r2 = enqueue_iter(-1, 1, 1, true, W->cap_stream, false, 0);
-            if (!r2) {
-                k_advance_it<<<1, 1, 0, W->cap_stream>>>(W->st);
-            }
+            int r2 = enqueue_iter(-1, 1, 1, true, W->cap_stream, false, 0);  // k_iter_b advances it_dev
             cudaError_t ce = cudaStreamEndCapture(W->cap_stream, &g);
             if (r2) return r2;
             IE_CUDA(ce);
@@ -1278,8 +1254,7 @@ extern "C" int ie_pcg_sharded_f64(const ie_matvec* A, const ie_precond* T, ie_co
         if (T && (rc = precond_prepare_stream(T, cap_s))) return rc;
         cudaGraph_t gr;
         IE_CUDA(cudaStreamBeginCapture(cap_s, cudaStreamCaptureModeThreadLocal));
-        int r2 = enqueue_iter(-1, 1, 1, true, cap_s);
-        if (!r2) k_advance_it<<<1, 1, 0, cap_s>>>(S);
+        int r2 = enqueue_iter(-1, 1, 1, true, cap_s);  // k_iter_b advances it_dev
         cudaError_t ce = cudaStreamEndCapture(cap_s, &gr);
         if (r2) return r2;
         IE_CUDA(ce);

@@ -35,6 +35,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "pcg_state.cuh"
 
 namespace ie {
 
@@ -44,7 +45,7 @@ int make_log_table_device(const ie_geom& g, LogEntry** d_tab, int* ntab);
 int dot_chunks(int64_t n);
 
 constexpr int kSmemMaxS = 160;
-constexpr int kChunk = 2048;  // dot-product chunk (same as krylov.cu)
+constexpr int kChunk = kPcgChunk;  // dot-product chunk (same as krylov.cu)
 constexpr int kBuildThreads = 512;
 constexpr unsigned kFull = 0xffffffffu;
 
@@ -737,16 +738,13 @@ __global__ void k_gather(const double* r, const int* idx, double* rg, int64_t to
 
 // Per point: z_i = sum of its <= MM staged contributions in ascending block id
 // (fixed-width position table, -1 padded: one dependent load level less than CSR).
-template <int MM>
-__global__ void __launch_bounds__(256) k_scatter_fixed(const double* staging, const int* pos, double* z, int N,
-                                                       const double* r, double* partials, const int* stop, int i0,
-                                                       int i1) {
-    if (stop && *stop) return;
-    __shared__ double sh[256];
-    // points [i0, i1) (chunk-aligned i0; z and the partials are relative to i0)
-    const int base = i0 + blockIdx.x * kChunk;
+// Chunk c of points [i0, i1) (chunk-aligned i0; z and the partials relative to i0).
+template <int MM, int UNR>
+__device__ __forceinline__ void scatter_fixed_chunk(int c, const double* staging, const int* pos, double* z, int N,
+                                                    const double* r, double* partials, int i0, int i1, double* sh) {
+    const int base = i0 + c * kChunk;
     double loc = 0.0;
-#pragma unroll 2
+#pragma unroll UNR
     for (int e = 0; e < kChunk / 256; ++e) {
         const int i = base + e * 256 + threadIdx.x;
         if (i < i1) {
@@ -771,7 +769,17 @@ __global__ void __launch_bounds__(256) k_scatter_fixed(const double* staging, co
         if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
         __syncthreads();
     }
-    if (threadIdx.x == 0) partials[blockIdx.x] = sh[0];
+    if (threadIdx.x == 0) partials[c] = sh[0];
+    __syncthreads();
+}
+
+template <int MM, int UNR>
+__global__ void __launch_bounds__(256) k_scatter_fixed(const double* staging, const int* pos, double* z, int N,
+                                                       const double* r, double* partials, const int* stop, int i0,
+                                                       int i1) {
+    if (stop && *stop) return;
+    __shared__ double sh[256];
+    scatter_fixed_chunk<MM, UNR>(blockIdx.x, staging, pos, z, N, r, partials, i0, i1, sh);
 }
 
 // Per point: z_i = sum of its staged contributions in ascending block id.
@@ -1197,10 +1205,10 @@ static int scatter_launch(const ie_precond* p, const double* staging, const doub
     if (nch <= 0) return IE_OK;
     const double* rr = partials ? r : nullptr;
     switch (p->mm) {
-        case 1: k_scatter_fixed<1><<<nch, 256, 0, st>>>(staging, p->d_posfix, z, p->N, rr, partials, stop, i0, i1); break;
-        case 2: k_scatter_fixed<2><<<nch, 256, 0, st>>>(staging, p->d_posfix, z, p->N, rr, partials, stop, i0, i1); break;
-        case 4: k_scatter_fixed<4><<<nch, 256, 0, st>>>(staging, p->d_posfix, z, p->N, rr, partials, stop, i0, i1); break;
-        case 8: k_scatter_fixed<8><<<nch, 256, 0, st>>>(staging, p->d_posfix, z, p->N, rr, partials, stop, i0, i1); break;
+        case 1: k_scatter_fixed<1, 2><<<nch, 256, 0, st>>>(staging, p->d_posfix, z, p->N, rr, partials, stop, i0, i1); break;
+        case 2: k_scatter_fixed<2, 2><<<nch, 256, 0, st>>>(staging, p->d_posfix, z, p->N, rr, partials, stop, i0, i1); break;
+        case 4: k_scatter_fixed<4, 2><<<nch, 256, 0, st>>>(staging, p->d_posfix, z, p->N, rr, partials, stop, i0, i1); break;
+        case 8: k_scatter_fixed<8, 2><<<nch, 256, 0, st>>>(staging, p->d_posfix, z, p->N, rr, partials, stop, i0, i1); break;
         default: k_scatter<<<nch, 256, 0, st>>>(staging, p->d_ptr, p->d_pos, z, p->N, rr, partials, stop, i0, i1);
     }
     IE_LAUNCHED();
