@@ -32,6 +32,6 @@ void run(int warps_per_cta, int ctas_per_sm) {
     cudaFree(d);
 }
 int main() {
-    run<4>(8, 2); run<8>(8, 2); run<16>(8, 2); run<8>(8, 4); run<16>(8, 4); run<4>(4, 1); run<8>(4, 1);
+    run<4>(8, 2); run<8>(8, 2); run<16>(8, 2); run<8>(8, 4); run<16>(8, 4); run<4>(4, 1); run<8>(4, 1); run<16>(4, 1); run<8>(8, 1); run<16>(8, 1); run<8>(16, 1);
     return 0;
 }
