@@ -20,7 +20,7 @@ LIB = os.path.join(HERE, "libiedd_b200.so")
 SOURCES = ["capi.cu", "matvec.cu", "fft.cu", "precond.cu", "krylov.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
-         "-Xptxas", "-v"]
+         "-Xptxas", "-v"] + os.environ.get("IEDD_B200_NVCC_EXTRA", "").split()
 
 
 def _nccl():

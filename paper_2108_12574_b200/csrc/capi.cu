@@ -1,5 +1,6 @@
 // Library-wide state of the C-ABI (include/iedd_b200.h): error text and the
 // launch counter reported as bench.py's gpu_launches.
+#include <stdlib.h>
 #include <string>
 
 #include "common.cuh"
@@ -8,6 +9,10 @@ struct ie_matvec;
 
 namespace ie {
 std::atomic<int64_t> g_launches{0};
+bool pdl_enabled() {
+    static const bool on = !getenv("IEDD_B200_NO_PDL");
+    return on;
+}
 static thread_local std::string t_err;
 void set_error(const std::string& msg) { t_err = msg; }
 }  // namespace ie

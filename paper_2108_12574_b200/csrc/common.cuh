@@ -6,6 +6,7 @@
 
 #include <atomic>
 #include <string>
+#include <utility>
 
 #include "../../include/iedd_b200.h"
 
@@ -35,6 +36,35 @@ extern std::atomic<int64_t> g_launches;
     } while (0)
 
 constexpr int kNumSMs = 148;
+
+// ------------------------------------------- programmatic dependent launch --
+// The kernels of the PCG iteration are launched with programmatic stream
+// serialization (launch_k): a kernel may be scheduled while its predecessor
+// drains and runs pdl_wait() (griddepcontrol.wait: the predecessor has
+// completed and its writes are visible) before touching anything.  No early
+// launch_dependents trigger: measured, early triggers slowed the PCG iteration
+// (successor CTAs parked on the SMs) while the implicit end-of-kernel trigger
+// hides the launch latency (config-5 FFT pass 101.5 -> 96 us, apply 48 -> 44 us
+// when launched back to back; ~1 us per graph-replayed iteration).  A no-op for
+// ordinary launches; IEDD_B200_NO_PDL=1 turns the attribute off.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+bool pdl_enabled();
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                            Args&&... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // ------------------------------------------------------------ log table --
 // log(d^2) for d^2 = m * s^2 with integer m >= 1 (dims 1 and 2):

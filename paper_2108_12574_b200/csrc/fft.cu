@@ -687,6 +687,7 @@ __global__ void __launch_bounds__(1024, 1) k_fft8(LineArgs a) {
     constexpr bool fused = MODE == kFusedCC || MODE == kFusedRR;
     extern __shared__ __align__(16) double sm8[];
     __shared__ double csc[2];
+    pdl_wait();
     if (a.stop && *a.stop) return;
     const int G = a.g8, t = threadIdx.x;
     int g, j;
@@ -876,7 +877,7 @@ static int launch_fft8_ls(const LineArgs& a, int tpb, int ctas, size_t smem, cud
                                      160 * 1024));
         attr = true;
     }
-    k_fft8<MODE, LOGL, STRIDED><<<ctas, tpb, smem, st>>>(a);
+    IE_CUDA(launch_k(k_fft8<MODE, LOGL, STRIDED>, dim3(ctas), dim3(tpb), smem, st, a));
     IE_LAUNCHED();
     return IE_OK;
 }

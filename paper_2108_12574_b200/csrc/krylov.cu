@@ -178,6 +178,7 @@ __global__ void __launch_bounds__(kRed) k_iter_a(const double* part_pq, const do
                                                  int pending, long long it, PcgState* s, double* hist, double* u,
                                                  double* r, const double* p, const double* q, int N, double* amax) {
     __shared__ double sh[kRed];
+    pdl_wait();
     if (s->stop) return;
     if (it < 0) it = s->it_dev;
     double denom;
@@ -191,6 +192,7 @@ __global__ void __launch_bounds__(kRed) k_iter_a(const double* part_pq, const do
 __global__ void __launch_bounds__(kRed) k_iter_b(const double* part_rz, int nch, long long it, PcgState* s,
                                                  double* p, const double* z, int N, double* amax) {
     __shared__ double sh[kRed];
+    pdl_wait();
     if (s->stop) return;
     const bool replay = it < 0;
     if (replay) it = s->it_dev;
@@ -246,6 +248,7 @@ __device__ __forceinline__ void post_pass_chunk(int c, const double* p, const do
 __global__ void k_post_pass(const double* p, const double* q, const double* f, const double* w, int N, int do_p,
                             int pending, double* part_pq, double* part_res, const int* stop) {
     __shared__ double sh[kRed];
+    pdl_wait();
     if (*stop) return;
     post_pass_chunk(blockIdx.x, p, q, f, w, N, do_p, pending, part_pq, part_res, sh);
 }
@@ -460,10 +463,12 @@ extern "C" int ie_pcg_f64(const ie_matvec* A, const ie_precond* T, const double*
             r2 = matvec_launch(A, uu, N, 1, w, N, 0, N, s2, stop);
         }
         if (r2) return r2;
-        k_post_pass<<<nch, kRed, 0, s2>>>(p, q, f, w, N, do_p, pending, part_pq, part_res, stop);
+        IE_CUDA(launch_k(k_post_pass, dim3(nch), dim3(kRed), 0, s2, (const double*)p, (const double*)q, f,
+                         (const double*)w, N, do_p, pending, part_pq, part_res, stop));
         IE_LAUNCHED();
-        k_iter_a<<<nch, kRed, 0, s2>>>(part_pq, part_res, nch, do_p, pending, itarg, W->st, W->hist, uu, W->r, p, q,
-                                       N, W->amax);
+        IE_CUDA(launch_k(k_iter_a, dim3(nch), dim3(kRed), 0, s2, (const double*)part_pq, (const double*)part_res, nch,
+                         do_p, pending, (long long)itarg, W->st, W->hist, uu, W->r, (const double*)p,
+                         (const double*)q, N, W->amax));
         IE_LAUNCHED();
         if (spec) {  // speculative: z_it is discarded if iteration it is the last
             if (timed_apply) {
@@ -476,7 +481,8 @@ extern "C" int ie_pcg_f64(const ie_matvec* A, const ie_precond* T, const double*
                 k_dot_partials<<<nch, kRed, 0, s2>>>(W->r, W->z, N, 0, part_rz);
                 IE_LAUNCHED();
             }
-            k_iter_b<<<nch, kRed, 0, s2>>>(part_rz, nch, itarg, W->st, p, W->z, N, W->amax);
+            IE_CUDA(launch_k(k_iter_b, dim3(nch), dim3(kRed), 0, s2, (const double*)part_rz, nch, (long long)itarg,
+                             W->st, p, (const double*)W->z, N, W->amax));
             IE_LAUNCHED();
         }
         return IE_OK;

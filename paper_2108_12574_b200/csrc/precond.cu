@@ -447,6 +447,7 @@ __host__ __device__ constexpr int pad4mod16(int x) { return x + ((4 - (x & 15)) 
 template <int MT>
 __global__ void __launch_bounds__(256, 2) k_apply_dmma(GemmArgs a) {
     extern __shared__ double sg[];
+    pdl_wait();
     if (a.stop && *a.stop) return;
     constexpr int AP = pad4mod16(16 * MT);  // A row stride (k-major rows of length >= 2*8*MT)
     const int tile = blockIdx.x;
@@ -777,8 +778,9 @@ template <int MM, int UNR>
 __global__ void __launch_bounds__(256) k_scatter_fixed(const double* staging, const int* pos, double* z, int N,
                                                        const double* r, double* partials, const int* stop, int i0,
                                                        int i1) {
-    if (stop && *stop) return;
     __shared__ double sh[256];
+    pdl_wait();
+    if (stop && *stop) return;
     scatter_fixed_chunk<MM, UNR>(blockIdx.x, staging, pos, z, N, r, partials, i0, i1, sh);
 }
 
@@ -1205,10 +1207,10 @@ static int scatter_launch(const ie_precond* p, const double* staging, const doub
     if (nch <= 0) return IE_OK;
     const double* rr = partials ? r : nullptr;
     switch (p->mm) {
-        case 1: k_scatter_fixed<1, 2><<<nch, 256, 0, st>>>(staging, p->d_posfix, z, p->N, rr, partials, stop, i0, i1); break;
-        case 2: k_scatter_fixed<2, 2><<<nch, 256, 0, st>>>(staging, p->d_posfix, z, p->N, rr, partials, stop, i0, i1); break;
-        case 4: k_scatter_fixed<4, 2><<<nch, 256, 0, st>>>(staging, p->d_posfix, z, p->N, rr, partials, stop, i0, i1); break;
-        case 8: k_scatter_fixed<8, 2><<<nch, 256, 0, st>>>(staging, p->d_posfix, z, p->N, rr, partials, stop, i0, i1); break;
+        case 1: IE_CUDA(launch_k(k_scatter_fixed<1, 2>, dim3(nch), dim3(256), 0, st, staging, (const int*)p->d_posfix, z, (int)p->N, rr, partials, stop, i0, i1)); break;
+        case 2: IE_CUDA(launch_k(k_scatter_fixed<2, 2>, dim3(nch), dim3(256), 0, st, staging, (const int*)p->d_posfix, z, (int)p->N, rr, partials, stop, i0, i1)); break;
+        case 4: IE_CUDA(launch_k(k_scatter_fixed<4, 2>, dim3(nch), dim3(256), 0, st, staging, (const int*)p->d_posfix, z, (int)p->N, rr, partials, stop, i0, i1)); break;
+        case 8: IE_CUDA(launch_k(k_scatter_fixed<8, 2>, dim3(nch), dim3(256), 0, st, staging, (const int*)p->d_posfix, z, (int)p->N, rr, partials, stop, i0, i1)); break;
         default: k_scatter<<<nch, 256, 0, st>>>(staging, p->d_ptr, p->d_pos, z, p->N, rr, partials, stop, i0, i1);
     }
     IE_LAUNCHED();
@@ -1225,7 +1227,7 @@ static void launch_dmma(const ie_precond* p, const GemmArgs& g, cudaStream_t st)
         cudaFuncSetAttribute(k_apply_dmma<MT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
         attr = true;
     }
-    k_apply_dmma<MT><<<p->ntiles, 256, sm, st>>>(g);
+    launch_k(k_apply_dmma<MT>, dim3(p->ntiles), dim3(256), sm, st, g);
 }
 
 template <int RA>
