@@ -239,12 +239,14 @@ def run_ours(args):
         M = 2 * CFG["n"]
         lines = CFG["n"] + 2 * (2 * CFG["n"]) + CFG["n"]
         flops = lines * 5.0 * M * np.log2(M)
-        roof = {"bound": "fp64", "kernel": "k_fft_lines x3 (row fwd, fused column fwd*sym*inv, row inv)",
+        roof = {"bound": "fp64", "kernel": "k_fft8 x3 (row fwd, fused column fwd*sym*inv, row inv)",
                 "achieved": flops / (mv_ms * 1e-3) / 1e12, "unit": "TFLOP/s", "peak": fp64_peak_tflops,
-                "traffic": 93.0e6,
+                "traffic": 92.7e6,
                 "note": "flops = 5 M log2 M per line FFT x 6n lines; peak = live DFMA microbenchmark; "
-                        "traffic = dram bytes of the three launches from profiles/r1_ncu_summary.md "
-                        "(the n x 2n work buffer stays L2-resident); latency/shared-memory bound"}
+                        "traffic = dram read+write bytes of the three launches, ncu --set full "
+                        "(profiles/r1b_ncu_summary.md; the n x 2n work buffer stays L2-resident); "
+                        "bound in practice by the L1/shared-memory data pipe (73% busy in the fused "
+                        "column pass: exchanges 60%, strided column I/O 20%, twiddles 10%)"}
     roof["frac"] = roof["achieved"] / roof["peak"] if roof.get("peak") else None
     roof["share_of_step"] = kern[dom] / step_ms
     out = {
