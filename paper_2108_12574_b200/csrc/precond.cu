@@ -329,6 +329,10 @@ __device__ __forceinline__ void cp_async8(void* smem, const void* gmem) {
     const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
     asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(sa), "l"(gmem));
 }
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem) {
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"(sa), "l"(gmem));
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::); }
 
@@ -471,35 +475,34 @@ __global__ void __launch_bounds__(256, 2) k_apply_dmma(GemmArgs a) {
             if (colbase[jj] >= 0) cp_async8(Bs + jj * bst + i, a.rg + colbase[jj] + i);
         }
     } else {
-        // gather straight from r through the block's point indices: four index
-        // loads in flight per thread, then their cp.async copies
-        for (int e0 = tid; e0 < s * kGemmTN; e0 += 4 * 256) {
-            int gi[4];
+        // gather straight from r through the block's point indices: thread t owns
+        // column t/4 and rows k = t%4 + 4q; all its index loads in flight at once
+        // (one memory round trip), then their cp.async copies
+        constexpr int kGq = (kSmemMaxS + 3) / 4;  // 40
+        const int jj = tid >> 2, k0 = tid & 3;
+        const int64_t cb = colbase[jj];
+        int gi[kGq];
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int e = e0 + u * 256;
-                const int jj = e / s;
-                gi[u] = (e < s * kGemmTN && colbase[jj] >= 0) ? __ldg(a.idx + colbase[jj] + (e - jj * s)) : -1;
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int e = e0 + u * 256;
-                if (gi[u] >= 0) {
-                    const int jj = e / s;
-                    cp_async8(Bs + jj * bst + (e - jj * s), a.r + gi[u]);
-                }
-            }
+        for (int q = 0; q < kGq; ++q) {
+            const int k = k0 + 4 * q;
+            gi[q] = (cb >= 0 && k < s) ? __ldg(a.idx + cb + k) : -1;
         }
+#pragma unroll
+        for (int q = 0; q < kGq; ++q)
+            if (gi[q] >= 0) cp_async8(Bs + jj * bst + k0 + 4 * q, a.r + gi[q]);
     }
     cp_async_commit();
     const int nchunks = (s + kGemmKC - 1) / kGemmKC;
     // a chunk is kc contiguous rows of A: element e = kk * s + i of the chunk goes to
     // smem row kk, column i; this thread's (kk, i) are the same for every chunk
+    // 16-byte copies when every row start is 16-byte aligned (s even, aligned
+    // class offset), else 8-byte; this thread's (kk, i) are the same for every chunk
+    const bool v16 = !(s & 1) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
     constexpr int kQ = (kGemmKC * kSmemMaxS + 255) / 256;
     int a_dst[kQ];
 #pragma unroll
     for (int q = 0; q < kQ; ++q) {
-        const int e = tid + 256 * q;
+        const int e = v16 ? 2 * (tid + 256 * q) : tid + 256 * q;
         const int kk = e / s;
         a_dst[q] = kk * AP + (e - kk * s);
     }
@@ -509,10 +512,18 @@ __global__ void __launch_bounds__(256, 2) k_apply_dmma(GemmArgs a) {
             const int k0 = ch * kGemmKC;
             const int kc = min(kGemmKC, s - k0);
             const double* src = A + (int64_t)k0 * s;
+            if (v16) {
 #pragma unroll
-            for (int q = 0; q < kQ; ++q) {
-                const int e = tid + 256 * q;
-                if (e < kc * s) cp_async8(dst + a_dst[q], src + e);
+                for (int q = 0; q < (kQ + 1) / 2; ++q) {
+                    const int e = 2 * (tid + 256 * q);
+                    if (e < kc * s) cp_async16(dst + a_dst[q], src + e);
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < kQ; ++q) {
+                    const int e = tid + 256 * q;
+                    if (e < kc * s) cp_async8(dst + a_dst[q], src + e);
+                }
             }
         }
         cp_async_commit();  // always commit (possibly empty) so group counting stays uniform
