@@ -306,6 +306,12 @@ constexpr int kGemmTN = 64;
 constexpr int kGemmKC = 8;
 
 
+struct TileDesc {  // one class GEMM tile, read with one load (32 B)
+    int cls, first, cnt, s;
+    long long full_off;
+    long long pad;
+};
+
 struct GemmArgs {
     const double* r;
     const double* rg;  // r gathered into the staging layout (k_gather)
@@ -318,6 +324,8 @@ struct GemmArgs {
     const int* tile_cls;
     const int* tile_first;
     const int* tile_cnt;
+    const TileDesc* tdesc;  // per tile (DMMA kernel)
+    const int* mst;         // staging offset of members[m]
     const int* members;
     const int* stop;
 };
@@ -454,20 +462,29 @@ __global__ void __launch_bounds__(256, 2) k_apply_dmma(GemmArgs a) {
     pdl_wait();
     if (a.stop && *a.stop) return;
     constexpr int AP = pad4mod16(16 * MT);  // A row stride (k-major rows of length >= 2*8*MT)
-    const int tile = blockIdx.x;
-    const int c = a.tile_cls[tile], first = a.tile_first[tile], cnt = a.tile_cnt[tile];
-    const int s = a.cls_s[c];
-    const int bst = pad4mod16((s + kGemmKC - 1) / kGemmKC * kGemmKC);  // covers every k the chunks touch
-    const double* A = a.full + a.full_off[c];
+    const TileDesc td = a.tdesc[blockIdx.x];
+    const int first = td.first, cnt = td.cnt, s = td.s;
+    const int kpad = (s + kGemmKC - 1) / kGemmKC * kGemmKC;  // every k the chunks touch
+    const int bst = pad4mod16(kpad);
+    const double* A = a.full + td.full_off;
     double* Bs = sg;                                // [64][bst] column-major gathered r
     double* As = sg + kGemmTN * bst;                // [stages][KC][AP]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int rh = warp & 1, cq = warp >> 1;
     __shared__ int64_t colbase[kGemmTN];
-    if (tid < kGemmTN) colbase[tid] = tid < cnt ? a.meta[a.members[first + tid]].st_off : -1;
-    // zero A ring (padding rows/cols stay zero) and B (k >= s, missing columns)
-    for (int e = tid; e < kDmmaStages * kGemmKC * AP; e += 256) As[e] = 0.0;
-    for (int e = tid; e < kGemmTN * bst; e += 256) Bs[e] = 0.0;
+    if (tid < kGemmTN) colbase[tid] = tid < cnt ? a.mst[first + tid] : -1;
+    // Output element (row, col) reads only A[.][row] and B[.][col]: rows >= s and
+    // missing columns are never stored, so their smem may hold anything.  When s
+    // is not a multiple of KC the last chunk's rows k >= s must contribute exact
+    // zeros: B rows [s, kpad) are zeroed and the A ring starts zeroed (later
+    // slots keep finite earlier-chunk data there).
+    if (kpad != s) {
+        for (int e = tid; e < kDmmaStages * kGemmKC * AP; e += 256) As[e] = 0.0;
+        for (int e = tid; e < kGemmTN * (kpad - s); e += 256) {
+            const int jj = e / (kpad - s);
+            Bs[jj * bst + s + (e - jj * (kpad - s))] = 0.0;
+        }
+    }
     __syncthreads();
     if (a.rg) {
         for (int e = tid; e < s * kGemmTN; e += 256) {
@@ -1132,6 +1149,8 @@ struct ie_precond {
     int* d_cls_s;
     int* d_tiles;  // [3][ntiles]: class, first member, count
     int* d_members;
+    ie::TileDesc* d_tdesc = nullptr;  // per tile {class, first member, count, s, Ainv offset}
+    int* d_mst = nullptr;         // staging offset of members[m]
     double* d_rg;  // r gathered into the staging layout (GEMM path)
     int use_dmma;  // FP64 tensor-core (mma.sync m8n8k4) class GEMM
     int dmma_pregather = 0;  // IEDD_B200_PREGATHER=1: separate k_gather pass (comparison)
@@ -1276,6 +1295,8 @@ int precond_apply(const ie_precond* p, const double* r, double* z, double* parti
         g.tile_first = p->d_tiles + p->ntiles;
         g.tile_cnt = p->d_tiles + 2 * p->ntiles;
         g.members = p->d_members;
+        g.tdesc = p->d_tdesc;
+        g.mst = p->d_mst;
         g.stop = stop;
         if (p->use_dmma) {
             switch ((((p->smax + 7) / 8) + 1) / 2) {
@@ -1369,6 +1390,8 @@ extern "C" void ie_precond_destroy(ie_precond* p) {
     cudaFree(p->d_cls_s);
     cudaFree(p->d_tiles);
     cudaFree(p->d_members);
+    cudaFree(p->d_tdesc);
+    cudaFree(p->d_mst);
     cudaFree(p->d_rg);
     cudaFree(p->d_posfix);
     cudaFree(p->d_part);
@@ -1841,6 +1864,16 @@ extern "C" int ie_precond_create(const ie_geom* g, const int64_t* h_offsets, con
         if (e == cudaSuccess) e = cudaMalloc(&p->d_cls_s, U * sizeof(int));
         if (e == cudaSuccess) e = cudaMalloc(&p->d_tiles, tiles.size() * sizeof(int));
         if (e == cudaSuccess) e = cudaMalloc(&p->d_members, members.size() * sizeof(int));
+        std::vector<ie::TileDesc> tdesc(tcls.size());
+        for (size_t t = 0; t < tcls.size(); ++t)
+            tdesc[t] = {tcls[t], tfirst[t], tcnt[t], usizes[tcls[t]], (long long)full_off[tcls[t]], 0};
+        std::vector<int> mst(members.size());
+        for (size_t q = 0; q < members.size(); ++q) mst[q] = (int)meta[members[q]].st_off;
+        if (e == cudaSuccess) e = cudaMalloc(&p->d_tdesc, tdesc.size() * sizeof(ie::TileDesc));
+        if (e == cudaSuccess) e = cudaMalloc(&p->d_mst, mst.size() * sizeof(int));
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(p->d_tdesc, tdesc.data(), tdesc.size() * sizeof(ie::TileDesc), cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(p->d_mst, mst.data(), mst.size() * sizeof(int), cudaMemcpyHostToDevice, st);
         if (e == cudaSuccess) e = cudaMalloc(&p->d_rg, total * sizeof(double));
         int64_t* d_fofs2 = nullptr;
         if (e == cudaSuccess) e = cudaMalloc(&d_fofs2, U * sizeof(int64_t));
