@@ -109,25 +109,48 @@ __global__ void k_pcg_init(const double* part, int nch, PcgState* s, double tol,
 // After the A-pass of iteration `it`: residual / stagnation check of
 // iteration it-1 (pcg.py:107-119), breakdown test of iteration it
 // (pcg.py:99-103), alpha, then u += alpha p, r -= alpha q and max|u| per chunk.
-// Control: every CTA reduces the same partials in the same order and takes
-// the same decision (returned); CTA 0 records it in the state.
-__device__ __forceinline__ int iter_a_control(const double* part_pq, const double* part_res, int nch, int do_p,
-                                              int pending, long long it, PcgState* s, double* hist, double* sh,
-                                              double* denom_out) {
+// Every CTA reduces the same partials in the same order and takes the same
+// decision; CTA 0 records it in the state.  Every load that does not depend
+// on the reduction (state scalars, the history entry of the stagnation test,
+// this thread's partials and its p, q chunk values) is issued before it, so
+// the serial prologue costs about one memory round trip.
+__global__ void __launch_bounds__(kRed) k_iter_a(const double* part_pq, const double* part_res, int nch, int do_p,
+                                                 int pending, long long it, PcgState* s, double* hist, double* u,
+                                                 double* r, const double* p, const double* q, int N, double* amax) {
+    __shared__ double sh[kRed];
     __shared__ int decided;
+    pdl_wait();
+    const int stopv = s->stop;
+    if (it < 0) it = s->it_dev;
+    const double rho_prev = s->rho[(it - 1) & 1], nf = s->nf, tol = s->tol;
+    const long long k = it - 1;
+    const double h30 = (pending && k >= 30 && threadIdx.x == 0) ? hist[k - 30] : 0.0;
+    const int base = blockIdx.x * kChunk;
+    double pv[kChunk / kRed], qv[kChunk / kRed];
+#pragma unroll
+    for (int e = 0; e < kChunk / kRed; ++e) {
+        const int i = base + e * kRed + threadIdx.x;
+        pv[e] = (do_p && i < N) ? p[i] : 0.0;
+        qv[e] = (do_p && i < N) ? q[i] : 0.0;
+    }
+    double lp = 0.0, lr = 0.0;
+    for (int c = threadIdx.x; c < nch; c += kRed) {
+        if (do_p) lp += part_pq[c];
+        if (pending) lr += part_res[c];
+    }
+    if (stopv) return;
     double denom = 0.0, res2 = 0.0;
-    if (do_p) denom = reduce_partials(part_pq, nch, sh);
+    if (do_p) denom = block_tree(lp, sh);
     __syncthreads();
-    if (pending) res2 = reduce_partials(part_res, nch, sh);
+    if (pending) res2 = block_tree(lr, sh);
     if (threadIdx.x == 0) {
-        const long long k = it - 1;
         int status = 0;
         double rel = 0.0;
         if (pending) {
-            rel = sqrt(res2) / s->nf;
+            rel = sqrt(res2) / nf;
             if (!isfinite(rel)) status = 5;
-            else if (rel <= s->tol) status = 1;
-            else if (k >= 30 && rel > (1.0 - 1e-3) * hist[k - 30]) status = 2;
+            else if (rel <= tol) status = 1;
+            else if (k >= 30 && rel > (1.0 - 1e-3) * h30) status = 2;
             else if (!do_p) status = 3;
         }
         if (!status && do_p && (!isfinite(denom) || denom <= 0.0)) status = 4;
@@ -147,57 +170,72 @@ __device__ __forceinline__ int iter_a_control(const double* part_pq, const doubl
                 s->stop = 1;
             } else if (do_p) {
                 s->denom = denom;
-                s->alpha = s->rho[(it - 1) & 1] / denom;
+                s->alpha = rho_prev / denom;
             }
         }
     }
     __syncthreads();
-    *denom_out = denom;
-    return decided;
-}
-
-__device__ __forceinline__ void iter_a_chunk(int c, double al, double* u, double* r, const double* p,
-                                             const double* q, int N, double* amax, double* sh) {
-    const int base = c * kChunk;
+    if (decided || !do_p) return;
+    const double al = rho_prev / denom;
     double m = 0.0;
 #pragma unroll
     for (int e = 0; e < kChunk / kRed; ++e) {
         const int i = base + e * kRed + threadIdx.x;
         if (i < N) {
-            const double un = __dadd_rn(u[i], __dmul_rn(al, p[i]));
+            const double un = __dadd_rn(u[i], __dmul_rn(al, pv[e]));
             u[i] = un;
-            r[i] = __dsub_rn(r[i], __dmul_rn(al, q[i]));
+            r[i] = __dsub_rn(r[i], __dmul_rn(al, qv[e]));
             m = fmax(m, fabs(un));
         }
     }
     m = chunk_absmax(m, sh);
-    if (threadIdx.x == 0) amax[2 * c + 1] = m;
-}
-
-__global__ void __launch_bounds__(kRed) k_iter_a(const double* part_pq, const double* part_res, int nch, int do_p,
-                                                 int pending, long long it, PcgState* s, double* hist, double* u,
-                                                 double* r, const double* p, const double* q, int N, double* amax) {
-    __shared__ double sh[kRed];
-    pdl_wait();
-    if (s->stop) return;
-    if (it < 0) it = s->it_dev;
-    double denom;
-    const int decided = iter_a_control(part_pq, part_res, nch, do_p, pending, it, s, hist, sh, &denom);
-    if (decided || !do_p) return;
-    iter_a_chunk(blockIdx.x, s->rho[(it - 1) & 1] / denom, u, r, p, q, N, amax, sh);
+    if (threadIdx.x == 0) amax[2 * blockIdx.x + 1] = m;
 }
 
 // After the apply: rho_it = r.z, beta = rho_it / rho_{it-1}, p = z + beta p,
 // max|p| per chunk.
+// After the apply: rho_it = r.z, beta = rho_it / rho_{it-1}, p = z + beta p,
+// max|p| per chunk; the independent loads (state, partials, this thread's z
+// and p chunk values) are issued ahead of the reduction.  In graph replay the
+// last CTA advances the iteration counter.
 __global__ void __launch_bounds__(kRed) k_iter_b(const double* part_rz, int nch, long long it, PcgState* s,
                                                  double* p, const double* z, int N, double* amax) {
     __shared__ double sh[kRed];
     pdl_wait();
-    if (s->stop) return;
+    const int stopv = s->stop;
     const bool replay = it < 0;
     if (replay) it = s->it_dev;
-    const double beta = iter_b_beta(part_rz, nch, it, s, sh);
-    iter_b_chunk(blockIdx.x, beta, p, z, N, amax, sh);
+    const double rho_prev = s->rho[(it - 1) & 1];
+    const int base = blockIdx.x * kChunk;
+    double zv[kChunk / kRed], pv[kChunk / kRed];
+#pragma unroll
+    for (int e = 0; e < kChunk / kRed; ++e) {
+        const int i = base + e * kRed + threadIdx.x;
+        zv[e] = i < N ? z[i] : 0.0;
+        pv[e] = i < N ? p[i] : 0.0;
+    }
+    double loc = 0.0;
+    for (int c = threadIdx.x; c < nch; c += kRed) loc += part_rz[c];
+    if (stopv) return;
+    const double rz = block_tree(loc, sh);
+    const double beta = rz / rho_prev;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        s->beta = beta;
+        s->rho[it & 1] = rz;
+    }
+    double m = 0.0;
+#pragma unroll
+    for (int e = 0; e < kChunk / kRed; ++e) {
+        const int i = base + e * kRed + threadIdx.x;
+        if (i < N) {
+            const double pn = __dadd_rn(zv[e], __dmul_rn(beta, pv[e]));
+            p[i] = pn;
+            m = fmax(m, fabs(pn));
+        }
+    }
+    __syncthreads();
+    m = chunk_absmax(m, sh);
+    if (threadIdx.x == 0) amax[2 * blockIdx.x] = m;
     if (replay) {  // graph replay: the last CTA (every CTA has read it_dev) advances the iteration
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -217,10 +255,14 @@ __global__ void k_pcg_rho0(const double* part_rz, int nch, PcgState* s) {
     if (threadIdx.x == 0) s->rho[0] = rz;
 }
 
-__device__ __forceinline__ void post_pass_chunk(int c, const double* p, const double* q, const double* f,
-                                                const double* w, int N, int do_p, int pending, double* part_pq,
-                                                double* part_res, double* sh) {
-    const int base = c * kChunk;
+// Chunk partials of p.q (A-pass denominator) and |f - w|^2 (true residual of
+// the previous iterate); the loads are issued before the stop flag is tested.
+__global__ void k_post_pass(const double* p, const double* q, const double* f, const double* w, int N, int do_p,
+                            int pending, double* part_pq, double* part_res, const int* stop) {
+    __shared__ double sh[kRed];
+    pdl_wait();
+    const int stopv = *stop;  // tested after the chunk loads are issued
+    const int base = blockIdx.x * kChunk;
     double a = 0.0, b = 0.0;
 #pragma unroll
     for (int e = 0; e < kChunk / kRed; ++e) {
@@ -233,24 +275,16 @@ __device__ __forceinline__ void post_pass_chunk(int c, const double* p, const do
             }
         }
     }
+    if (stopv) return;
     if (do_p) {
         const double t = block_tree(a, sh);
-        if (threadIdx.x == 0) part_pq[c] = t;
+        if (threadIdx.x == 0) part_pq[blockIdx.x] = t;
         __syncthreads();
     }
     if (pending) {
         const double t = block_tree(b, sh);
-        if (threadIdx.x == 0) part_res[c] = t;
-        __syncthreads();
+        if (threadIdx.x == 0) part_res[blockIdx.x] = t;
     }
-}
-
-__global__ void k_post_pass(const double* p, const double* q, const double* f, const double* w, int N, int do_p,
-                            int pending, double* part_pq, double* part_res, const int* stop) {
-    __shared__ double sh[kRed];
-    pdl_wait();
-    if (*stop) return;
-    post_pass_chunk(blockIdx.x, p, q, f, w, N, do_p, pending, part_pq, part_res, sh);
 }
 
 __global__ void k_copy_if_running(double* dst, const double* src, int N, const int* stop) {

@@ -48,34 +48,4 @@ __device__ __forceinline__ double chunk_absmax(double v, double* sh) {
     return sh[0];
 }
 
-// k_iter_b's update of one chunk: p = z + beta p, max|p| of the chunk into amax[2c]
-__device__ __forceinline__ void iter_b_chunk(int c, double beta, double* p, const double* z, int N, double* amax,
-                                             double* sh) {
-    const int base = c * kPcgChunk;
-    double m = 0.0;
-#pragma unroll
-    for (int e = 0; e < kPcgChunk / kPcgRed; ++e) {
-        const int i = base + e * kPcgRed + threadIdx.x;
-        if (i < N) {
-            const double pn = __dadd_rn(z[i], __dmul_rn(beta, p[i]));
-            p[i] = pn;
-            m = fmax(m, fabs(pn));
-        }
-    }
-    __syncthreads();
-    m = chunk_absmax(m, sh);
-    if (threadIdx.x == 0) amax[2 * c] = m;
-}
-
-// k_iter_b's control: beta = rho_it / rho_{it-1} from the r.z chunk partials
-__device__ __forceinline__ double iter_b_beta(const double* part_rz, int nch, long long it, PcgState* s, double* sh) {
-    const double rz = reduce_partials(part_rz, nch, sh);
-    const double beta = rz / s->rho[(it - 1) & 1];
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        s->beta = beta;
-        s->rho[it & 1] = rz;
-    }
-    return beta;
-}
-
 }  // namespace ie
