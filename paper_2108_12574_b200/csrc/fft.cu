@@ -25,7 +25,12 @@
 #include <math.h>
 #include <stdlib.h>
 
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
 #include <algorithm>
+#include <mutex>
+#include <utility>
 #include <vector>
 
 #include "common.cuh"
@@ -80,6 +85,10 @@ struct LineArgs {
     int g8;
     int strided8;
     int pitch8;
+    // strided fused column pass with TMA tile I/O: the buffer as a 2D FP64
+    // tensor (4n doubles per row, n rows), boxes of {2 G doubles, 256 rows}
+    int tma;
+    CUtensorMap tmap;
 };
 
 // 2^-e with 2^e >= max|x| (power of two, exact); 1 for max == 0
@@ -677,19 +686,34 @@ __device__ void column_scales_dyn(const LineArgs& a, double* sc) {
     }
 }
 
-template <int MODE, int LOGL, bool STRIDED>
-__global__ void __launch_bounds__(1024, 1) k_fft8(LineArgs a) {
+// TMA (tensor) tile copies for the strided column pass
+__device__ __forceinline__ unsigned smem32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];\n" ::
+            "r"(smem32(dst)),
+        "l"(map), "r"(x), "r"(y), "r"(smem32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int x, int y, const void* src) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.tile.bulk_group [%0, {%1, %2}], [%3];\n" ::"l"(map),
+                 "r"(x), "r"(y), "r"(smem32(src))
+                 : "memory");
+}
+
+template <int MODE, int LOGL, bool STRIDED, bool TMA = false>
+__global__ void __launch_bounds__(1024, 1) k_fft8(const __grid_constant__ LineArgs a) {
     constexpr int PADS = STRIDED ? 3 : 4;
     using PL = Plan8<LOGL>;
     constexpr int L = PL::L, TPL = PL::TPL;
     constexpr bool in_real = MODE == kFwdRC || MODE == kFusedRR;
     constexpr bool out_real = MODE == kInvCR || MODE == kFusedRR;
     constexpr bool fused = MODE == kFusedCC || MODE == kFusedRR;
-    extern __shared__ __align__(16) double sm8[];
+    extern __shared__ __align__(128) double sm8[];
     __shared__ double csc[2];
     pdl_wait();
     if (a.stop && *a.stop) return;
-    const int G = a.g8, t = threadIdx.x;
+    const int G = TMA ? 2 : a.g8, t = threadIdx.x;  // the TMA variant is launched with two lines per CTA
     int g, j;
     if constexpr (STRIDED) {
         g = t % G;
@@ -709,8 +733,43 @@ __global__ void __launch_bounds__(1024, 1) k_fft8(LineArgs a) {
         __syncthreads();
     }
     double vr[8], vi[8];
+    constexpr bool tma_mode = TMA && MODE == kFusedCC && STRIDED;
+    if constexpr (tma_mode) {
+        {
+            // the CTA's G columns x n_in rows land densely in shared memory by TMA
+            // (one mbarrier transaction), then each thread reads its 8 points
+            __shared__ __align__(8) uint64_t tbar;
+            if (t == 0) {
+                asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem32(&tbar)));
+                asm volatile("fence.mbarrier_init.release.cluster;\n" ::: "memory");
+            }
+            __syncthreads();
+            if (t == 0) {
+                asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem32(&tbar)),
+                             "r"(a.n_in * G * 16)
+                             : "memory");
+                for (int y = 0; y < a.n_in; y += 256)
+                    tma_load_2d(sm8 + y * G * 2, &a.tmap, 2 * G * (int)blockIdx.x, y, &tbar);
+            }
+            asm volatile(
+                "{\n .reg .pred p;\n TW%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra TW%=;\n}\n" ::"r"(
+                    smem32(&tbar))
+                : "memory");
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                const int l = j + TPL * m;
+                vr[m] = vi[m] = 0.0;
+                if (l < a.n_in) {
+                    const double2 v = reinterpret_cast<const double2*>(sm8)[l * G + g];
+                    vr[m] = v.x;
+                    vi[m] = v.y;
+                }
+            }
+        }
+    }
 #pragma unroll
     for (int m = 0; m < 8; ++m) {
+        if constexpr (tma_mode) break;
         const int l = j + TPL * m;
         vr[m] = vi[m] = 0.0;
         if (live && l < a.n_in) {
@@ -763,6 +822,26 @@ __global__ void __launch_bounds__(1024, 1) k_fft8(LineArgs a) {
         fft8_line<-1, LOGL, PADS>(vr, vi, j, re, im, a.tw8, zero_hi);
     } else {
         fft8_line<+1, LOGL, PADS>(vr, vi, j, re, im, a.tw8, zero_hi);
+    }
+    if constexpr (tma_mode) {
+        {
+            // outputs to a dense [n_out][G] tile in shared memory, then TMA stores
+            __syncthreads();  // the last exchange's reads are done
+#pragma unroll
+            for (int m = 0; m < 8; ++m) {
+                const int l = j + TPL * m;
+                if (l < a.n_out) reinterpret_cast<double2*>(sm8)[l * G + g] = make_double2(vr[m], vi[m]);
+            }
+            asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory");
+            __syncthreads();
+            if (t == 0) {
+                for (int y = 0; y < a.n_out; y += 256)
+                    tma_store_2d(&a.tmap, 2 * G * (int)blockIdx.x, y, sm8 + y * G * 2);
+                asm volatile("cp.async.bulk.commit_group;\n" ::: "memory");
+                asm volatile("cp.async.bulk.wait_group.read 0;\n" ::: "memory");  // smem read; the grid completes the writes
+            }
+            return;
+        }
     }
     if (!live) return;
 #pragma unroll
@@ -840,6 +919,9 @@ struct ie_fft {
     double* d_sym;
     double2* d_buf;
     double* d_amax;  // 2 * ceil(N/2048) partial maxima
+    // TMA descriptors of the 2D work buffers (the plan's and per-stream ones), by address
+    std::mutex tm_mu;
+    std::vector<std::pair<const void*, CUtensorMap>> tmaps;
 };
 
 namespace ie {
@@ -869,15 +951,15 @@ static int launch_modes(const LineArgs& a, cudaStream_t st) {
     return a.sign < 0 ? launch_mode<kFwdCC, TPB>(a, st) : launch_mode<kInvCC, TPB>(a, st);
 }
 
-template <int MODE, int LOGL, bool STRIDED>
+template <int MODE, int LOGL, bool STRIDED, bool TMA = false>
 static int launch_fft8_ls(const LineArgs& a, int tpb, int ctas, size_t smem, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        IE_CUDA(cudaFuncSetAttribute(k_fft8<MODE, LOGL, STRIDED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+        IE_CUDA(cudaFuncSetAttribute(k_fft8<MODE, LOGL, STRIDED, TMA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      160 * 1024));
         attr = true;
     }
-    IE_CUDA(launch_k(k_fft8<MODE, LOGL, STRIDED>, dim3(ctas), dim3(tpb), smem, st, a));
+    IE_CUDA(launch_k(k_fft8<MODE, LOGL, STRIDED, TMA>, dim3(ctas), dim3(tpb), smem, st, a));
     IE_LAUNCHED();
     return IE_OK;
 }
@@ -885,6 +967,9 @@ static int launch_fft8_ls(const LineArgs& a, int tpb, int ctas, size_t smem, cud
 // real-in / real-out lines are always contiguous (launch_fft8)
 template <int MODE, int LOGL>
 static int launch_fft8_l(const LineArgs& a, int tpb, int ctas, size_t smem, cudaStream_t st) {
+    if constexpr (MODE == kFusedCC) {
+        if (a.strided8 && a.tma) return launch_fft8_ls<MODE, LOGL, true, true>(a, tpb, ctas, smem, st);
+    }
     if constexpr (MODE == kFwdCC || MODE == kInvCC || MODE == kFusedCC) {
         if (a.strided8) return launch_fft8_ls<MODE, LOGL, true>(a, tpb, ctas, smem, st);
     }
@@ -904,6 +989,13 @@ static int launch_fft8_m(const LineArgs& a, int tpb, int ctas, size_t smem, cuda
     }
 }
 
+// lines per CTA of a strided (column) k_fft8 launch of line length L
+static int fft8_strided_g(int L) {
+    static const int gs = getenv("IEDD_B200_FFT_G") ? atoi(getenv("IEDD_B200_FFT_G")) : 2;
+    const int tpl = L / 8;
+    return std::max(std::min(gs, 1024 / tpl), std::min(32, 256 / tpl));
+}
+
 // k_fft8 launch: lines per CTA and thread mapping from the access pattern
 static int launch_fft8(LineArgs a, cudaStream_t st) {
     const int tpl = a.L / 8;
@@ -911,8 +1003,7 @@ static int launch_fft8(LineArgs a, cudaStream_t st) {
     a.strided8 = cin ? 0 : 1;
     int G, skew;
     if (a.strided8) {  // lanes alternate lines: 32-B row segments per warp request (G = 2 measured best)
-        static const int gs = getenv("IEDD_B200_FFT_G") ? atoi(getenv("IEDD_B200_FFT_G")) : 2;
-        G = std::max(std::min(gs, 1024 / tpl), std::min(32, 256 / tpl));
+        G = fft8_strided_g(a.L);
         skew = std::max(1, 16 / G);
     } else {
         G = std::max(1, 256 / tpl);
@@ -1184,6 +1275,47 @@ int64_t fft_buf_elems(const ie_fft* f) {
     return t;
 }
 
+// TMA descriptor of a 2D work buffer B (n rows of M complex) for the strided
+// column pass: FP64 elements, inner dimension 2M doubles, boxes {2G, 256}.
+// Built once per buffer address through the driver entry point (no libcuda
+// link); false when unavailable (the pass then uses plain loads and stores).
+static bool tma_map(ie_fft* f, const double2* B, int G, CUtensorMap* out) {
+    static PFN_cuTensorMapEncodeTiled_v12000 enc = nullptr;
+    static bool tried = false;
+    static std::mutex mu;
+    {
+        std::lock_guard<std::mutex> lk(mu);
+        if (!tried) {
+            tried = true;
+            cudaDriverEntryPointQueryResult q;
+            void* fn = nullptr;
+            if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+                q == cudaDriverEntryPointSuccess)
+                enc = (PFN_cuTensorMapEncodeTiled_v12000)fn;
+            cudaGetLastError();
+        }
+    }
+    if (!enc) return false;
+    std::lock_guard<std::mutex> lk(f->tm_mu);
+    for (auto& e : f->tmaps)
+        if (e.first == B) {
+            *out = e.second;
+            return true;
+        }
+    CUtensorMap m;
+    const cuuint64_t dims[2] = {(cuuint64_t)2 * f->M, (cuuint64_t)f->n};
+    const cuuint64_t strides[1] = {(cuuint64_t)f->M * 16};
+    const cuuint32_t box[2] = {(cuuint32_t)(2 * G), 256u};
+    const cuuint32_t estr[2] = {1u, 1u};
+    if (enc(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, (void*)B, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) !=
+        CUDA_SUCCESS)
+        return false;
+    f->tmaps.emplace_back(B, m);
+    *out = m;
+    return true;
+}
+
 // buf_ws / amax_ws: the calling stream's work buffer and chunk-maxima scratch
 // (nullptr: the plan's own)
 int fft_matvec(const ie_fft* f, const double* X0, const double* X1, double* Y0, double* Y1, cudaStream_t st,
@@ -1248,6 +1380,11 @@ int fft_matvec(const ie_fft* f, const double* X0, const double* X1, double* Y0, 
         c.n_in = n;
         c.n_out = n;
         c.fused = 1;
+        // TMA tile I/O when the strided launch uses two column lines per CTA
+        static const bool no_tma = getenv("IEDD_B200_NO_TMA") != nullptr;
+        if (!no_tma && n % 256 == 0 && M >= 64 && M <= 4096 && fft8_strided_g(M) == 2 &&
+            tma_map(const_cast<ie_fft*>(f), B, 2, &c.tmap))
+            c.tma = 1;
         if ((rc = line_launch(c, st))) return rc;
         LineArgs e = base_args(f);  // rows a < n, inverse along axis 1 -> real pair
         e.nlines = n;
