@@ -82,6 +82,8 @@ struct LineArgs {
     // k_fft8 (radix-8, 8 points per thread): per-pass radix-major twiddles,
     // lines per CTA, strided (column) thread mapping, per-line smem pitch
     const double2* tw8;
+    const double2* tw16;  // 16-point plan twiddles (L = 2048)
+    int pts;              // points per thread of the k_fft8 launch (8 or 16)
     int g8;
     int strided8;
     int pitch8;
@@ -652,6 +654,101 @@ __device__ __forceinline__ void fft8_line(double* vr, double* vi, int j, double*
     if constexpr (P >= 4) pass8<S, LOGL, 4, PADS>(vr, vi, j, re, im, tw8);
 }
 
+// 2048-point line with 16 points per thread (128 threads per line): radix 16,
+// 16, 8 -- two shared-memory exchanges instead of the three of the 8-point
+// plan.  Register m holds position j + 128 m before and after (natural order),
+// so the fused column pass keeps the spectrum in registers as with k_fft8.
+// Twiddles tw16: pass 2 t[r*16 + k] = w_256^(r k) (r, k < 16), pass 3
+// t[256 + r*256 + k] = w_2048^(r k) (r < 8, k < 256).
+template <int S, int PADS>
+__device__ __forceinline__ void fft16_line_2048(double* vr, double* vi, int j, double* re, double* im,
+                                                const double2* __restrict__ tw16, bool zero_hi) {
+    constexpr int TPL = 128;
+    // pass 1: Ns = 1, radix 16 over positions j + 128 m -> 16 j + k
+    if (zero_hi) {  // positions >= 1024 (m >= 8) are zero padding: same arithmetic without the zero adds
+#pragma unroll
+        for (int n2 = 0; n2 < 4; ++n2) dft4_half<S>(vr, vi, n2, n2 + 4, n2 + 8, n2 + 12);
+        rot16<S, 1>(vr[5], vi[5]);
+        rot16<S, 2>(vr[9], vi[9]);
+        rot16<S, 3>(vr[13], vi[13]);
+        rot16<S, 2>(vr[6], vi[6]);
+        rot16<S, 4>(vr[10], vi[10]);
+        rot16<S, 6>(vr[14], vi[14]);
+        rot16<S, 3>(vr[7], vi[7]);
+        rot16<S, 6>(vr[11], vi[11]);
+        rot16<S, 9>(vr[15], vi[15]);
+#pragma unroll
+        for (int k1 = 0; k1 < 4; ++k1) dft4<S>(vr, vi, 4 * k1, 4 * k1 + 1, 4 * k1 + 2, 4 * k1 + 3);
+    } else {
+        dft_reg<16, S>(vr, vi);
+    }
+    __syncthreads();  // the previous users of the exchange buffer are done
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+        const int q = padq<PADS>(16 * j + k);
+        re[q] = vr[out_slot<16>(k)];
+        im[q] = vi[out_slot<16>(k)];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {
+        const int q = padq<PADS>(j + TPL * m);
+        vr[m] = re[q];
+        vi[m] = im[q];
+    }
+    // pass 2: Ns = 16, radix 16
+    {
+        const int k = j & 15;
+#pragma unroll
+        for (int r = 1; r < 16; ++r) {
+            const double2 t = __ldg(tw16 + r * 16 + k);
+            const double ti = S < 0 ? t.y : -t.y;
+            const double xr = vr[r];
+            vr[r] = fma(xr, t.x, -vi[r] * ti);
+            vi[r] = fma(xr, ti, vi[r] * t.x);
+        }
+        dft_reg<16, S>(vr, vi);
+        __syncthreads();
+        const int base = (j >> 4) * 256 + k;
+#pragma unroll
+        for (int kk = 0; kk < 16; ++kk) {
+            const int q = padq<PADS>(base + 16 * kk);
+            re[q] = vr[out_slot<16>(kk)];
+            im[q] = vi[out_slot<16>(kk)];
+        }
+        __syncthreads();
+#pragma unroll
+        for (int m = 0; m < 16; ++m) {
+            const int q = padq<PADS>(j + TPL * m);
+            vr[m] = re[q];
+            vi[m] = im[q];
+        }
+    }
+    // pass 3: Ns = 256, radix 8, butterflies b = 0, 1 at jb = j + 128 b over registers b + 2 r;
+    // output k of butterfly b (position jb + 256 k) lands in register b + 2 k
+#pragma unroll
+    for (int b = 0; b < 2; ++b) {
+        const int jb = j + TPL * b;
+        double xr[8], xi[8];
+        xr[0] = vr[b];
+        xi[0] = vi[b];
+#pragma unroll
+        for (int r = 1; r < 8; ++r) {
+            const double2 t = __ldg(tw16 + 256 + r * 256 + jb);
+            const double ti = S < 0 ? t.y : -t.y;
+            const double ar = vr[b + 2 * r], ai = vi[b + 2 * r];
+            xr[r] = fma(ar, t.x, -ai * ti);
+            xi[r] = fma(ar, ti, ai * t.x);
+        }
+        dft_reg<8, S>(xr, xi);
+#pragma unroll
+        for (int r = 0; r < 8; ++r) {
+            vr[b + 2 * r] = xr[out_slot<8>(r)];
+            vi[b + 2 * r] = xi[out_slot<8>(r)];
+        }
+    }
+}
+
 __device__ __forceinline__ int64_t line_off(int64_t so, int64_t si, int64_t sl, int lsplit, int64_t sh, int o, int i,
                                             int l) {
     return (int64_t)o * so + (int64_t)i * si +
@@ -701,11 +798,20 @@ __device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int x, int 
                  : "memory");
 }
 
-template <int MODE, int LOGL, bool STRIDED, bool TMA = false>
-__global__ void __launch_bounds__(1024, 1) k_fft8(const __grid_constant__ LineArgs a) {
+// line FFT of the k_fft8 kernel: 8 points per thread (any L in 64..4096) or 16
+// (L = 2048)
+template <int S, int LOGL, int PADS, int PTS>
+__device__ __forceinline__ void fft_line(double* vr, double* vi, int j, double* re, double* im, const LineArgs& a,
+                                         bool zero_hi) {
+    if constexpr (PTS == 16) fft16_line_2048<S, PADS>(vr, vi, j, re, im, a.tw16, zero_hi);
+    else fft8_line<S, LOGL, PADS>(vr, vi, j, re, im, a.tw8, zero_hi);
+}
+
+template <int MODE, int LOGL, bool STRIDED, bool TMA = false, int PTS = 8>
+__global__ void __launch_bounds__(PTS == 16 ? 256 : 1024, PTS == 16 ? 2 : 1) k_fft8(const __grid_constant__ LineArgs a) {
+    static_assert(PTS == 8 || LOGL == 11, "16 points per thread: 2048-point lines only");
     constexpr int PADS = STRIDED ? 3 : 4;
-    using PL = Plan8<LOGL>;
-    constexpr int L = PL::L, TPL = PL::TPL;
+    constexpr int L = 1 << LOGL, TPL = L / PTS;
     constexpr bool in_real = MODE == kFwdRC || MODE == kFusedRR;
     constexpr bool out_real = MODE == kInvCR || MODE == kFusedRR;
     constexpr bool fused = MODE == kFusedCC || MODE == kFusedRR;
@@ -732,7 +838,7 @@ __global__ void __launch_bounds__(1024, 1) k_fft8(const __grid_constant__ LineAr
         column_scales_dyn(a, csc);
         __syncthreads();
     }
-    double vr[8], vi[8];
+    double vr[PTS], vi[PTS];
     constexpr bool tma_mode = TMA && MODE == kFusedCC && STRIDED;
     if constexpr (tma_mode) {
         {
@@ -756,7 +862,7 @@ __global__ void __launch_bounds__(1024, 1) k_fft8(const __grid_constant__ LineAr
                     smem32(&tbar))
                 : "memory");
 #pragma unroll
-            for (int m = 0; m < 8; ++m) {
+            for (int m = 0; m < PTS; ++m) {
                 const int l = j + TPL * m;
                 vr[m] = vi[m] = 0.0;
                 if (l < a.n_in) {
@@ -768,7 +874,7 @@ __global__ void __launch_bounds__(1024, 1) k_fft8(const __grid_constant__ LineAr
         }
     }
 #pragma unroll
-    for (int m = 0; m < 8; ++m) {
+    for (int m = 0; m < PTS; ++m) {
         if constexpr (tma_mode) break;
         const int l = j + TPL * m;
         vr[m] = vi[m] = 0.0;
@@ -787,15 +893,15 @@ __global__ void __launch_bounds__(1024, 1) k_fft8(const __grid_constant__ LineAr
     if constexpr (in_real) {
         if (a.scale_in) {
 #pragma unroll
-            for (int m = 0; m < 8; ++m) {
+            for (int m = 0; m < PTS; ++m) {
                 vr[m] *= csc[0];
                 vi[m] *= csc[1];
             }
         }
     }
-    const bool zero_hi = a.n_in <= L / 2;  // line positions j + TPL m, m >= 4, read as zero
+    const bool zero_hi = a.n_in <= L / 2;  // line positions j + TPL m, m >= PTS / 2, read as zero
     if constexpr (fused) {
-        fft8_line<-1, LOGL, PADS>(vr, vi, j, re, im, a.tw8, zero_hi);
+        fft_line<-1, LOGL, PADS, PTS>(vr, vi, j, re, im, a, zero_hi);
         // folded real symbol at frequency l = j + TPL m along this line
         const int np1 = a.n + 1;
         int tmp = i + a.line0, off = 0, stride = 1;
@@ -805,9 +911,9 @@ __global__ void __launch_bounds__(1024, 1) k_fft8(const __grid_constant__ LineAr
             off += min(k, L - k) * stride;
             stride *= np1;
         }
-#pragma unroll
         const double* symline = a.sym + (int64_t)off * np1;  // axis 0 fastest: contiguous along the line
-        for (int m = 0; m < 8; ++m) {
+#pragma unroll
+        for (int m = 0; m < PTS; ++m) {
             const int l = j + TPL * m;
             const double lam = live ? __ldg(symline + min(l, L - l)) : 0.0;
             vr[m] *= lam;
@@ -817,18 +923,18 @@ __global__ void __launch_bounds__(1024, 1) k_fft8(const __grid_constant__ LineAr
         // addresses instead of keeping the forward's alive (64-register budget)
         int jj = j;
         asm volatile("" : "+r"(jj));
-        fft8_line<+1, LOGL, PADS>(vr, vi, jj, re, im, a.tw8);
+        fft_line<+1, LOGL, PADS, PTS>(vr, vi, jj, re, im, a, false);
     } else if constexpr (MODE == kFwdCC || MODE == kFwdRC) {
-        fft8_line<-1, LOGL, PADS>(vr, vi, j, re, im, a.tw8, zero_hi);
+        fft_line<-1, LOGL, PADS, PTS>(vr, vi, j, re, im, a, zero_hi);
     } else {
-        fft8_line<+1, LOGL, PADS>(vr, vi, j, re, im, a.tw8, zero_hi);
+        fft_line<+1, LOGL, PADS, PTS>(vr, vi, j, re, im, a, zero_hi);
     }
     if constexpr (tma_mode) {
         {
             // outputs to a dense [n_out][G] tile in shared memory, then TMA stores
             __syncthreads();  // the last exchange's reads are done
 #pragma unroll
-            for (int m = 0; m < 8; ++m) {
+            for (int m = 0; m < PTS; ++m) {
                 const int l = j + TPL * m;
                 if (l < a.n_out) reinterpret_cast<double2*>(sm8)[l * G + g] = make_double2(vr[m], vi[m]);
             }
@@ -845,7 +951,7 @@ __global__ void __launch_bounds__(1024, 1) k_fft8(const __grid_constant__ LineAr
     }
     if (!live) return;
 #pragma unroll
-    for (int m = 0; m < 8; ++m) {
+    for (int m = 0; m < PTS; ++m) {
         const int l = j + TPL * m;
         if (l >= a.n_out) continue;
         const int64_t off = line_off(a.out_so, a.out_si, a.out_sl, a.out_lsplit, a.out_sh, o, i, l);
@@ -916,6 +1022,7 @@ struct ie_fft {
     int N;
     double2* d_tw;
     double2* d_tw8;  // k_fft8 per-pass radix-major twiddles (M >= 64)
+    double2* d_tw16 = nullptr;  // 16-point plan twiddles (M = 2048)
     double* d_sym;
     double2* d_buf;
     double* d_amax;  // 2 * ceil(N/2048) partial maxima
@@ -951,29 +1058,37 @@ static int launch_modes(const LineArgs& a, cudaStream_t st) {
     return a.sign < 0 ? launch_mode<kFwdCC, TPB>(a, st) : launch_mode<kInvCC, TPB>(a, st);
 }
 
-template <int MODE, int LOGL, bool STRIDED, bool TMA = false>
+template <int MODE, int LOGL, bool STRIDED, bool TMA = false, int PTS = 8>
 static int launch_fft8_ls(const LineArgs& a, int tpb, int ctas, size_t smem, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
-        IE_CUDA(cudaFuncSetAttribute(k_fft8<MODE, LOGL, STRIDED, TMA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     160 * 1024));
+        IE_CUDA(cudaFuncSetAttribute(k_fft8<MODE, LOGL, STRIDED, TMA, PTS>,
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
         attr = true;
     }
-    IE_CUDA(launch_k(k_fft8<MODE, LOGL, STRIDED, TMA>, dim3(ctas), dim3(tpb), smem, st, a));
+    IE_CUDA(launch_k(k_fft8<MODE, LOGL, STRIDED, TMA, PTS>, dim3(ctas), dim3(tpb), smem, st, a));
     IE_LAUNCHED();
     return IE_OK;
 }
 
 // real-in / real-out lines are always contiguous (launch_fft8)
-template <int MODE, int LOGL>
-static int launch_fft8_l(const LineArgs& a, int tpb, int ctas, size_t smem, cudaStream_t st) {
+template <int MODE, int LOGL, int PTS>
+static int launch_fft8_lp(const LineArgs& a, int tpb, int ctas, size_t smem, cudaStream_t st) {
     if constexpr (MODE == kFusedCC) {
-        if (a.strided8 && a.tma) return launch_fft8_ls<MODE, LOGL, true, true>(a, tpb, ctas, smem, st);
+        if (a.strided8 && a.tma) return launch_fft8_ls<MODE, LOGL, true, true, PTS>(a, tpb, ctas, smem, st);
     }
     if constexpr (MODE == kFwdCC || MODE == kInvCC || MODE == kFusedCC) {
-        if (a.strided8) return launch_fft8_ls<MODE, LOGL, true>(a, tpb, ctas, smem, st);
+        if (a.strided8) return launch_fft8_ls<MODE, LOGL, true, false, PTS>(a, tpb, ctas, smem, st);
     }
-    return launch_fft8_ls<MODE, LOGL, false>(a, tpb, ctas, smem, st);
+    return launch_fft8_ls<MODE, LOGL, false, false, PTS>(a, tpb, ctas, smem, st);
+}
+
+template <int MODE, int LOGL>
+static int launch_fft8_l(const LineArgs& a, int tpb, int ctas, size_t smem, cudaStream_t st) {
+    if constexpr (LOGL == 11) {
+        if (a.pts == 16) return launch_fft8_lp<MODE, LOGL, 16>(a, tpb, ctas, smem, st);
+    }
+    return launch_fft8_lp<MODE, LOGL, 8>(a, tpb, ctas, smem, st);
 }
 
 template <int MODE>
@@ -998,8 +1113,13 @@ static int fft8_strided_g(int L) {
 
 // k_fft8 launch: lines per CTA and thread mapping from the access pattern
 static int launch_fft8(LineArgs a, cudaStream_t st) {
-    const int tpl = a.L / 8;
+    // 16 points per thread for strided (column) 2048-point lines: two exchanges
+    // instead of three (config-5 fused column pass 52.6 -> 45.9 us); the
+    // contiguous row passes measured faster with 8 (21.5 vs 23.6 us row inverse)
     const bool cin = a.in_real || a.in_sl == 1, cout = a.out_real || a.out_sl == 1;
+    static const bool no16 = getenv("IEDD_B200_FFT8_ONLY") != nullptr;
+    a.pts = (a.logL == 11 && a.tw16 && !cin && !no16) ? 16 : 8;
+    const int tpl = a.L / a.pts;
     a.strided8 = cin ? 0 : 1;
     int G, skew;
     if (a.strided8) {  // lanes alternate lines: 32-B row segments per warp request (G = 2 measured best)
@@ -1046,6 +1166,7 @@ static int line_launch(const LineArgs& a_in, cudaStream_t st) {
 static LineArgs base_args(const ie_fft* f) {
     LineArgs a{};
     a.tw8 = f->d_tw8;
+    a.tw16 = f->d_tw16;
     a.amax = f->d_amax;
     a.namax = (f->N + 2047) / 2048;
     a.L = f->M;
@@ -1128,6 +1249,15 @@ int fft_create(const ie_geom& g, ie_fft** out) {
         IE_CUDA(cudaMalloc(&f->d_tw8, t8.size() * sizeof(double2)));
         IE_CUDA(cudaMemcpy(f->d_tw8, t8.data(), t8.size() * sizeof(double2), cudaMemcpyHostToDevice));
     }
+    if (M == 2048) {  // 16-point plan: pass 2 w_256^(r k) (r, k < 16), pass 3 w_2048^(r k) (r < 8, k < 256)
+        std::vector<double2> t16;
+        for (int r = 0; r < 16; ++r)
+            for (int k = 0; k < 16; ++k) t16.push_back(tw[(int64_t)r * k * (M / 256) % M]);
+        for (int r = 0; r < 8; ++r)
+            for (int k = 0; k < 256; ++k) t16.push_back(tw[(int64_t)r * k % M]);
+        IE_CUDA(cudaMalloc(&f->d_tw16, t16.size() * sizeof(double2)));
+        IE_CUDA(cudaMemcpy(f->d_tw16, t16.data(), t16.size() * sizeof(double2), cudaMemcpyHostToDevice));
+    }
     IE_CUDA(cudaMalloc(&f->d_sym, totS * sizeof(double)));
     IE_CUDA(cudaMalloc(&f->d_buf, totB * sizeof(double2)));
     // symbol: embed, full forward FFT, fold
@@ -1153,6 +1283,7 @@ void fft_destroy(ie_fft* f) {
     if (!f) return;
     cudaFree(f->d_tw);
     cudaFree(f->d_tw8);
+    cudaFree(f->d_tw16);
     cudaFree(f->d_sym);
     cudaFree(f->d_buf);
     cudaFree(f->d_amax);
