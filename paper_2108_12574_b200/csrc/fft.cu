@@ -810,7 +810,9 @@ __device__ __forceinline__ void fft_line(double* vr, double* vi, int j, double* 
 template <int MODE, int LOGL, bool STRIDED, bool TMA = false, int PTS = 8>
 __global__ void __launch_bounds__(PTS == 16 ? 256 : 1024, PTS == 16 ? 2 : 1) k_fft8(const __grid_constant__ LineArgs a) {
     static_assert(PTS == 8 || LOGL == 11, "16 points per thread: 2048-point lines only");
-    constexpr int PADS = STRIDED ? 3 : 4;
+    // exchange padding (bank-conflict free per a half-warp model of 8-byte shared
+    // accesses): one slot per 8 for the strided 8-point mapping, else per 16
+    constexpr int PADS = (STRIDED && PTS == 8) ? 3 : 4;
     constexpr int L = 1 << LOGL, TPL = L / PTS;
     constexpr bool in_real = MODE == kFwdRC || MODE == kFusedRR;
     constexpr bool out_real = MODE == kInvCR || MODE == kFusedRR;
@@ -1131,7 +1133,7 @@ static int launch_fft8(LineArgs a, cudaStream_t st) {
     }
     (void)cout;
     a.g8 = G;
-    const int pads = a.strided8 ? 3 : 4;  // k_fft8's PADS
+    const int pads = (a.strided8 && a.pts == 8) ? 3 : 4;  // k_fft8's PADS
     a.pitch8 = (a.L + (a.L >> pads) + 15) / 16 * 16 + skew;
     const int tpb = G * tpl;
     const int ctas = (a.nlines + G - 1) / G;
