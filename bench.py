@@ -286,7 +286,7 @@ def run_ours(args):
         "clocks": clk,
     }
     if not args.no_cpu:
-        out["cpu_baseline"] = cpu_baseline(max(1, min(3, args.steps)))
+        out["cpu_baseline"] = cpu_baseline(max(1, min(10, args.steps)))  # ~8 s of CPU work
     print(json.dumps(out))
     return out
 
