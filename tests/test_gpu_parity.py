@@ -100,7 +100,7 @@ class TestMatvec:
                 parts.append(yy)
             assert torch.equal(torch.cat(parts), y0)
 
-    @pytest.mark.parametrize("dim,n", [(2, 32), (2, 256), (3, 16), (3, 32), (1, 64), (2, 1024)])
+    @pytest.mark.parametrize("dim,n", [(2, 32), (2, 256), (3, 16), (3, 32), (1, 64), (2, 512), (2, 1024), (2, 2048)])
     def test_fft_two_rhs_and_ranges(self, ie, dim, n):
         import torch
         op = ie.build_operator(ie.build_grid(dim, n), lattice="cell")
