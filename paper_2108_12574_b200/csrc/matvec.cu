@@ -60,7 +60,15 @@ __device__ __forceinline__ void neumaier(double& s, double& c, double v) {
     s = t;
 }
 
-template <int DIM, int NRHS, int R>
+// ADJ: a thread's R rows are R consecutive points of one lattice row (the host
+// guarantees n % R == 0 and row_begin % R == 0).  Then row r at source t has
+// the same squared distance as row r-1 at source t-1, so each source point
+// needs ONE kernel evaluation for all R rows: the values slide through a
+// register window (R-1 extra evaluations per run of sources).  Every row's
+// pair values and summation order are those of the non-ADJ kernel, so the
+// result is bitwise identical; the FP64 work per pair drops from 10 to
+// 2 + 8/R instructions (2-RHS, dims 1/2).
+template <int DIM, int NRHS, int R, bool ADJ = false>
 __global__ void __launch_bounds__(256) k_matvec(MatvecArgs a) {
     extern __shared__ __align__(16) unsigned char smem[];
     if (a.stop && *a.stop) return;
@@ -78,7 +86,7 @@ __global__ void __launch_bounds__(256) k_matvec(MatvecArgs a) {
     bool valid[R];
 #pragma unroll
     for (int r = 0; r < R; ++r) {
-        const int row = blockIdx.x * blockDim.x * R + r * blockDim.x + tid;
+        const int row = ADJ ? (blockIdx.x * blockDim.x + tid) * R + r : blockIdx.x * blockDim.x * R + r * blockDim.x + tid;
         valid[r] = row < a.nrows;
         gi[r] = a.row_begin + (valid[r] ? row : a.nrows - 1);
         int mi[DIM];
@@ -138,6 +146,36 @@ __global__ void __launch_bounds__(256) k_matvec(MatvecArgs a) {
                 db[r] = tb[r] - d0;
             }
             const double* xp = xs + (j - j0) * NRHS;
+            if constexpr (ADJ) {
+                // win[r] = pair value of row r at the current source t
+                double win[R];
+#pragma unroll
+                for (int r = 1; r < R; ++r) {
+                    const int dbt = db[0] + r;
+                    win[r] = pair_value<DIM>(stab, max(dbt * dbt + do2[0], 1));
+                }
+#pragma unroll 4
+                for (int t = 0; t < L; ++t) {
+                    double xv[NRHS];
+                    if constexpr (NRHS == 2) {
+                        const double2 x2 = reinterpret_cast<const double2*>(xp)[t];
+                        xv[0] = x2.x;
+                        xv[1] = x2.y;
+                    } else {
+                        xv[0] = xp[t];
+                    }
+                    const int dbt = db[0] - t;
+                    win[0] = pair_value<DIM>(stab, max(dbt * dbt + do2[0], 1));
+#pragma unroll
+                    for (int r = 0; r < R; ++r)
+#pragma unroll
+                        for (int q = 0; q < NRHS; ++q) ta[r][q] = fma(win[r], xv[q], ta[r][q]);
+#pragma unroll
+                    for (int r = R - 1; r > 0; --r) win[r] = win[r - 1];
+                }
+                j += L;
+                continue;
+            }
 #pragma unroll 4
             for (int t = 0; t < L; ++t) {
                 double xv[NRHS];
@@ -306,8 +344,18 @@ static int launch_dim(const ie_matvec* m, MatvecArgs a, cudaStream_t st) {
     const int threads = 256;
     dim3 grid((a.nrows + threads * m->R - 1) / (threads * m->R), m->nsplit);
     a.W = m->nsplit > 1 ? a.W : nullptr;  // the stream's split partials (matvec_launch)
-    if (m->R == 2) {
-        auto kern = k_matvec<DIM, NRHS, 2>;
+    // adjacent-row variant when each thread's R rows share a lattice row
+    const bool adj = m->R > 1 && m->g.n % m->R == 0 && a.row_begin % m->R == 0 && !getenv("IEDD_B200_K1_NOADJ");
+    if (m->R == 8) {
+        auto kern = adj ? k_matvec<DIM, NRHS, 8, true> : k_matvec<DIM, NRHS, 8, false>;
+        IE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kern<<<grid, threads, smem, st>>>(a);
+    } else if (m->R == 4) {
+        auto kern = adj ? k_matvec<DIM, NRHS, 4, true> : k_matvec<DIM, NRHS, 4, false>;
+        IE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kern<<<grid, threads, smem, st>>>(a);
+    } else if (m->R == 2) {
+        auto kern = adj ? k_matvec<DIM, NRHS, 2, true> : k_matvec<DIM, NRHS, 2, false>;
         IE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         kern<<<grid, threads, smem, st>>>(a);
     } else {
@@ -477,7 +525,9 @@ extern "C" int ie_matvec_create_method(const ie_geom* g, int32_t method, ie_matv
     }
     // Launch plan from N only.
     const int N = m->N;
-    m->R = N >= 131072 ? 2 : 1;
+    // rows per thread: more rows share each kernel evaluation (ADJ window) but
+    // hold more accumulators (R = 16 spills); 8 measured best at config 5
+    m->R = N >= 131072 ? 8 : (N >= 65536 ? 4 : (N >= 16384 ? 2 : 1));
     m->TS = N >= 65536 ? 1024 : 256;
     const int tiles = (N + m->TS - 1) / m->TS;
     const int ctas = (N + 256 * m->R - 1) / (256 * m->R);
