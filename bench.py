@@ -41,9 +41,10 @@ sys.path.insert(0, ROOT)
 METRIC = "Schwarz-PCG iter/s + kernel-matvec pair-evals/s (FP64) vs roofline, 1/2/4/8 GPU"
 CFG = dict(dim=2, n=1024, m=128, w=2, seed=3)
 WORKLOAD = "config5: 2D Laplace single-layer, n=1024 (N=1048576), cell lattice, Schwarz D=128x128 w=2, f~N(0,1) seed 3"
-# FP64 instructions per pair in the 2-RHS inner loop (SASS of k_matvec<2,2,8,true>: 92 DFMA + 4 DADD per
-# 4 sources x 8 rows): each kernel evaluation is shared by the thread's 8 consecutive rows (ADJ window)
-K1_FP64_PER_PAIR_2RHS = 3
+# FP64 instructions per pair in the 2-RHS inner loop: a kernel evaluation (8 FP64 instructions: DADD
+# int->double, DFMA reduction, 5 Horner DFMA, DFMA) shared by the thread's 16 consecutive rows (ADJ
+# window) + 2 DFMA (one per RHS) = 2.5 (SASS of k_matvec<2,2,8,true>: 92 DFMA + 4 DADD per 32 pairs = 3)
+K1_FP64_PER_PAIR_2RHS = 2.5
 
 
 def _peaks():
@@ -271,14 +272,14 @@ def run_ours(args):
         "kernels_ms": kern,
         "roofline": roof,
         "kernel_matvec": {
-            "kernel": "k_matvec<2,2,8,ADJ> (K1 direct sum, log kernel evaluated on the fly, one evaluation "
-                      "shared by 8 consecutive rows, 2 RHS)",
+            "kernel": "k_matvec<2,2,16,ADJ> (K1 direct sum, log kernel evaluated on the fly, one evaluation "
+                      "shared by 16 consecutive rows, 2 RHS)",
             "pair_evals_per_s": pair_rate, "pass_ms": k1_ms,
             "schwarz_pcg_iter_per_s": k1_iters / (k1_step_ms * 1e-3),
             "roofline": {"bound": "fp64", "achieved": k1_tflops, "peak": fp64_peak_tflops, "unit": "TFLOP/s",
                          "frac": k1_tflops / fp64_peak_tflops, "traffic": None,
-                         "note": "flops = 2 x FP64 pipe instructions executed (3 per pair in SASS; a per-pair "
-                                 "log costs 8 of them, shared by 8 rows); peak = live 8-chain DFMA "
+                         "note": "flops = 2 x FP64 pipe instructions executed (2.5 per pair: a log "
+                                 "evaluation costs 8, shared by 16 rows, + 2 DFMA); peak = live 8-chain DFMA "
                                  "microbenchmark on all SMs"}},
         "apply_hbm_roofline_unshared": dict(noshare, bound="hbm", unit="GB/s", algorithmic_bytes=apply_bytes,
                                             peak=peaks.get("hbm_gbs"), kernel="k_apply_packed<5,2>"),

@@ -96,11 +96,23 @@ __global__ void __launch_bounds__(256) k_matvec(MatvecArgs a) {
         tb[r] = mi[DIM - 1];
     }
 
-    double s[R][NRHS], c[R][NRHS];
+    // Neumaier accumulators (updated once per source tile): registers, or for
+    // R >= 16 shared memory [2][R][NRHS][blockDim] after the x tile
+    constexpr bool kSmemAcc = R >= 16;
+    double s[kSmemAcc ? 1 : R][NRHS], c[kSmemAcc ? 1 : R][NRHS];
+    double* sacc = xs + a.TS * NRHS;
+    auto S_ = [&](int r, int q) -> double& {
+        if constexpr (kSmemAcc) return sacc[((0 * R + r) * NRHS + q) * blockDim.x + tid];
+        else return s[r][q];
+    };
+    auto C_ = [&](int r, int q) -> double& {
+        if constexpr (kSmemAcc) return sacc[((1 * R + r) * NRHS + q) * blockDim.x + tid];
+        else return c[r][q];
+    };
 #pragma unroll
     for (int r = 0; r < R; ++r)
 #pragma unroll
-        for (int q = 0; q < NRHS; ++q) s[r][q] = c[r][q] = 0.0;
+        for (int q = 0; q < NRHS; ++q) S_(r, q) = C_(r, q) = 0.0;
 
     const int src0 = blockIdx.y * a.split_len;
     const int src1 = min(a.N, src0 + a.split_len);
@@ -200,7 +212,7 @@ __global__ void __launch_bounds__(256) k_matvec(MatvecArgs a) {
 #pragma unroll
         for (int r = 0; r < R; ++r)
 #pragma unroll
-            for (int q = 0; q < NRHS; ++q) neumaier(s[r][q], c[r][q], ta[r][q]);
+            for (int q = 0; q < NRHS; ++q) neumaier(S_(r, q), C_(r, q), ta[r][q]);
     }
 
     if (a.W != nullptr) {
@@ -210,7 +222,7 @@ __global__ void __launch_bounds__(256) k_matvec(MatvecArgs a) {
             const int row = gi[r] - a.row_begin;
 #pragma unroll
             for (int q = 0; q < NRHS; ++q)
-                a.W[((int64_t)blockIdx.y * a.nrows + row) * NRHS + q] = s[r][q] + c[r][q];
+                a.W[((int64_t)blockIdx.y * a.nrows + row) * NRHS + q] = S_(r, q) + C_(r, q);
         }
         return;
     }
@@ -223,7 +235,7 @@ __global__ void __launch_bounds__(256) k_matvec(MatvecArgs a) {
 #pragma unroll
         for (int q = 0; q < NRHS; ++q) {
             const double xi = a.X[q * a.ldx + gi[r]];
-            a.Y[q * a.ldy + row] = fma(a.alpha, s[r][q] + c[r][q], corr * xi);
+            a.Y[q * a.ldy + row] = fma(a.alpha, S_(r, q) + C_(r, q), corr * xi);
         }
     }
 }
@@ -340,13 +352,18 @@ int make_log_table_device(const ie_geom& g, LogEntry** d_tab, int* ntab) {
 
 template <int DIM, int NRHS>
 static int launch_dim(const ie_matvec* m, MatvecArgs a, cudaStream_t st) {
-    const size_t smem = (DIM == 3 ? 0 : (size_t)m->ntab * sizeof(LogEntry)) + (size_t)m->TS * NRHS * sizeof(double);
+    const size_t smem = (DIM == 3 ? 0 : (size_t)m->ntab * sizeof(LogEntry)) + (size_t)m->TS * NRHS * sizeof(double) +
+                        (m->R >= 16 ? (size_t)2 * m->R * NRHS * 256 * sizeof(double) : 0);
     const int threads = 256;
     dim3 grid((a.nrows + threads * m->R - 1) / (threads * m->R), m->nsplit);
     a.W = m->nsplit > 1 ? a.W : nullptr;  // the stream's split partials (matvec_launch)
     // adjacent-row variant when each thread's R rows share a lattice row
     const bool adj = m->R > 1 && m->g.n % m->R == 0 && a.row_begin % m->R == 0 && !getenv("IEDD_B200_K1_NOADJ");
-    if (m->R == 8) {
+    if (m->R == 16) {
+        auto kern = adj ? k_matvec<DIM, NRHS, 16, true> : k_matvec<DIM, NRHS, 16, false>;
+        IE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        kern<<<grid, threads, smem, st>>>(a);
+    } else if (m->R == 8) {
         auto kern = adj ? k_matvec<DIM, NRHS, 8, true> : k_matvec<DIM, NRHS, 8, false>;
         IE_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
         kern<<<grid, threads, smem, st>>>(a);
@@ -525,9 +542,11 @@ extern "C" int ie_matvec_create_method(const ie_geom* g, int32_t method, ie_matv
     }
     // Launch plan from N only.
     const int N = m->N;
-    // rows per thread: more rows share each kernel evaluation (ADJ window) but
-    // hold more accumulators (R = 16 spills); 8 measured best at config 5
-    m->R = N >= 131072 ? 8 : (N >= 65536 ? 4 : (N >= 16384 ? 2 : 1));
+    // rows per thread: more rows share each kernel evaluation (ADJ window); at
+    // R = 16 the Neumaier accumulators move to shared memory (R = 32 spills).
+    // Config 5 2-RHS pass: R = 2 944 ms, 8 278 ms, 16 242 ms
+    static const int rbig = getenv("IEDD_B200_K1_R") ? atoi(getenv("IEDD_B200_K1_R")) : 16;
+    m->R = N >= 131072 ? rbig : (N >= 65536 ? 4 : (N >= 16384 ? 2 : 1));
     m->TS = N >= 65536 ? 1024 : 256;
     const int tiles = (N + m->TS - 1) / m->TS;
     const int ctas = (N + 256 * m->R - 1) / (256 * m->R);
