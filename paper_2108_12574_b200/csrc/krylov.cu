@@ -177,6 +177,14 @@ __global__ void __launch_bounds__(kRed) k_iter_a(const double* part_pq, const do
     __syncthreads();
     if (decided || !do_p) return;
     const double al = rho_prev / denom;
+    if (!u) {  // u += alpha p runs concurrently in k_update_u (graph side branch)
+#pragma unroll
+        for (int e = 0; e < kChunk / kRed; ++e) {
+            const int i = base + e * kRed + threadIdx.x;
+            if (i < N) r[i] = __dsub_rn(r[i], __dmul_rn(al, qv[e]));
+        }
+        return;
+    }
     double m = 0.0;
 #pragma unroll
     for (int e = 0; e < kChunk / kRed; ++e) {
@@ -185,6 +193,30 @@ __global__ void __launch_bounds__(kRed) k_iter_a(const double* part_pq, const do
             const double un = __dadd_rn(u[i], __dmul_rn(al, pv[e]));
             u[i] = un;
             r[i] = __dsub_rn(r[i], __dmul_rn(al, qv[e]));
+            m = fmax(m, fabs(un));
+        }
+    }
+    m = chunk_absmax(m, sh);
+    if (threadIdx.x == 0) amax[2 * blockIdx.x + 1] = m;
+}
+
+// k_iter_a's u half: u += alpha p and max|u| per chunk, with the alpha CTA 0 of
+// k_iter_a stored (the same quotient every CTA computes).  Off the critical
+// path: it runs beside the preconditioner apply and joins before k_iter_b
+// rewrites p (the next A-pass is u's only consumer).
+__global__ void __launch_bounds__(kRed) k_update_u(const PcgState* s, double* u, const double* p, int N,
+                                                   double* amax) {
+    __shared__ double sh[kRed];
+    if (s->stop) return;
+    const double al = s->alpha;
+    const int base = blockIdx.x * kChunk;
+    double m = 0.0;
+#pragma unroll
+    for (int e = 0; e < kChunk / kRed; ++e) {
+        const int i = base + e * kRed + threadIdx.x;
+        if (i < N) {
+            const double un = __dadd_rn(u[i], __dmul_rn(al, p[i]));
+            u[i] = un;
             m = fmax(m, fabs(un));
         }
     }
@@ -342,6 +374,8 @@ struct PcgWork {
     double* amax = nullptr;  // per-chunk max|p|, max|u| (2-RHS FFT column scaling)
     double* fcopy = nullptr; // the right-hand side (graph-stable address)
     cudaStream_t cap_stream = nullptr;
+    cudaStream_t side_stream = nullptr;  // graph side branch (u update)
+    cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
     cudaGraphExec_t gexec = nullptr;
     uint64_t key_a = 0, key_t = 0;
     int gnodes = 0;  // kernel nodes in the captured iteration
@@ -360,6 +394,9 @@ struct PcgWork {
         cudaFree(fcopy);
         if (gexec) cudaGraphExecDestroy(gexec);
         if (cap_stream) cudaStreamDestroy(cap_stream);
+        if (side_stream) cudaStreamDestroy(side_stream);
+        if (fork_ev) cudaEventDestroy(fork_ev);
+        if (join_ev) cudaEventDestroy(join_ev);
         cudaFree(st);
         if (host) cudaFreeHost(host);
         for (auto e : ev) cudaEventDestroy(e);
@@ -392,6 +429,9 @@ static PcgWork* work_acquire(int N, int64_t cap, int* rc) {
     if (e == cudaSuccess) e = cudaMalloc(&w->amax, 2 * (size_t)nch * 8);
     if (e == cudaSuccess) e = cudaMalloc(&w->fcopy, (size_t)N * 8);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&w->cap_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&w->side_stream, cudaStreamNonBlocking);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&w->fork_ev, cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&w->join_ev, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaMalloc(&w->st, sizeof(PcgState));
     if (e == cudaSuccess) e = cudaMallocHost(&w->host, sizeof(PcgState));
     if (e != cudaSuccess) {
@@ -486,6 +526,7 @@ extern "C" int ie_pcg_f64(const ie_matvec* A, const ie_precond* T, const double*
     // carries u_{it-1} for the deferred true-residual check of iteration it-1.
     // Steady-state iterations (2 <= it < max_iters) replay one captured CUDA
     // graph that reads `it` from the device state.
+    static const bool no_fork = getenv("IEDD_B200_NO_FORK") != nullptr;  // u update in k_iter_a (comparison)
     auto enqueue_iter = [&](int64_t itarg, int do_p, int pending, bool spec, cudaStream_t s2, bool timed_apply,
                             int64_t evi) -> int {
         int r2;
@@ -500,10 +541,19 @@ extern "C" int ie_pcg_f64(const ie_matvec* A, const ie_precond* T, const double*
         IE_CUDA(launch_k(k_post_pass, dim3(nch), dim3(kRed), 0, s2, (const double*)p, (const double*)q, f,
                          (const double*)w, N, do_p, pending, part_pq, part_res, stop));
         IE_LAUNCHED();
+        // in the captured iteration u += alpha p forks onto a side branch beside the apply
+        const bool fork_u = itarg < 0 && do_p && spec && !no_fork;
         IE_CUDA(launch_k(k_iter_a, dim3(nch), dim3(kRed), 0, s2, (const double*)part_pq, (const double*)part_res, nch,
-                         do_p, pending, (long long)itarg, W->st, W->hist, uu, W->r, (const double*)p,
-                         (const double*)q, N, W->amax));
+                         do_p, pending, (long long)itarg, W->st, W->hist, fork_u ? nullptr : uu, W->r,
+                         (const double*)p, (const double*)q, N, W->amax));
         IE_LAUNCHED();
+        if (fork_u) {
+            IE_CUDA(cudaEventRecord(W->fork_ev, s2));
+            IE_CUDA(cudaStreamWaitEvent(W->side_stream, W->fork_ev, 0));
+            k_update_u<<<nch, kRed, 0, W->side_stream>>>(W->st, uu, p, N, W->amax);
+            IE_LAUNCHED();
+            IE_CUDA(cudaEventRecord(W->join_ev, W->side_stream));
+        }
         if (spec) {  // speculative: z_it is discarded if iteration it is the last
             if (timed_apply) {
                 if ((r2 = apply(W->r, W->z, evi))) return r2;
@@ -515,6 +565,8 @@ extern "C" int ie_pcg_f64(const ie_matvec* A, const ie_precond* T, const double*
                 k_dot_partials<<<nch, kRed, 0, s2>>>(W->r, W->z, N, 0, part_rz);
                 IE_LAUNCHED();
             }
+            // k_iter_b rewrites p, which the side branch reads: join first
+            if (fork_u) IE_CUDA(cudaStreamWaitEvent(s2, W->join_ev, 0));
             IE_CUDA(launch_k(k_iter_b, dim3(nch), dim3(kRed), 0, s2, (const double*)part_rz, nch, (long long)itarg,
                              W->st, p, (const double*)W->z, N, W->amax));
             IE_LAUNCHED();
