@@ -130,7 +130,7 @@ __global__ void __launch_bounds__(kRed) k_iter_a(const double* part_pq, const do
 #pragma unroll
     for (int e = 0; e < kChunk / kRed; ++e) {
         const int i = base + e * kRed + threadIdx.x;
-        pv[e] = (do_p && i < N) ? p[i] : 0.0;
+        pv[e] = (do_p && u && i < N) ? p[i] : 0.0;  // p only for the in-kernel u update
         qv[e] = (do_p && i < N) ? q[i] : 0.0;
     }
     double lp = 0.0, lr = 0.0;
