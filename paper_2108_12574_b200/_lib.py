@@ -12,7 +12,7 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libiedd_b200.so")
+LIB_PATH = os.environ.get("IEDD_B200_LIB") or os.path.join(HERE, "libiedd_b200.so")  # override: A/B builds
 
 IE_OK = 0
 IE_ERR_ARG = -1
