@@ -544,9 +544,9 @@ extern "C" int ie_matvec_create_method(const ie_geom* g, int32_t method, ie_matv
     const int N = m->N;
     // rows per thread: more rows share each kernel evaluation (ADJ window); at
     // R = 16 the Neumaier accumulators move to shared memory (R = 32 spills).
-    // Config 5 2-RHS pass: R = 2 944 ms, 8 278 ms, 16 242 ms
-    static const int rbig = getenv("IEDD_B200_K1_R") ? atoi(getenv("IEDD_B200_K1_R")) : 16;
-    m->R = N >= 131072 ? rbig : (N >= 65536 ? 4 : (N >= 16384 ? 2 : 1));
+    // 2-RHS pass, R = 2 -> 16: config 5 944 -> 242 ms, 2D n=256 4.6 -> 1.0 ms,
+    // 3D n=32 0.66 -> 0.35 ms; the launch-bound small sizes prefer 1-2
+    m->R = N >= 16384 ? 16 : (N >= 4096 ? 2 : 1);
     m->TS = N >= 65536 ? 1024 : 256;
     const int tiles = (N + m->TS - 1) / m->TS;
     const int ctas = (N + 256 * m->R - 1) / (256 * m->R);
