@@ -129,6 +129,23 @@ class TestMatvec:
         yr = O.FFTMatvec(O.build_operator(O.build_grid(2, 256), "cell")).matvec(x)
         assert rel(y, yr) <= 1e-12
 
+    @pytest.mark.parametrize("dim,n,rb", [(2, 130, 0), (2, 144, 0), (2, 144, 144 * 3 + 5), (3, 26, 0), (3, 32, 32 * 7)])
+    def test_direct_row_plans(self, ie, dim, n, rb):
+        # K1 with 16 rows per thread: the shared-evaluation (ADJ) kernel when n and
+        # row_begin are multiples of 16, else the per-pair kernel -- same sums
+        import torch
+        op = ie.build_operator(ie.build_grid(dim, n), lattice="cell")
+        N = op.n
+        x = np.random.default_rng(2).standard_normal(N)
+        mv = ie.KernelMatvec(op, method="direct")
+        y = mv.matvec(x)
+        yr = O.FFTMatvec(O.build_operator(O.build_grid(dim, n), "cell")).matvec(x)
+        assert rel(y, yr) <= 1e-12
+        xt = torch.from_numpy(x).cuda()
+        yy = torch.empty(N - rb, dtype=torch.float64, device="cuda")
+        mv.matvec_device(xt, yy, row_begin=rb, row_end=N)
+        assert torch.equal(yy.cpu(), torch.from_numpy(y[rb:]))
+
     def test_length_error(self, ie):
         mv = ie.ToeplitzMatvec(ie.build_operator(ie.build_grid(2, 8)))
         with pytest.raises(ValueError, match="length"):
