@@ -592,6 +592,61 @@ __global__ void __launch_bounds__(256, 2) k_apply_dmma(GemmArgs a) {
         }
 }
 
+// ---------------------------------------------------------------------------
+// Large translation-shared blocks (160 < s <= 1024; above, k_apply_big's row
+// chunks already spread each block): the class GEMV.  A class
+// c's members share Ainv_c (full, row-major); CTA (x, group) owns rows
+// [16x, 16x+16) of Ainv_c -- 2 per warp -- and the group's <= CG members,
+// whose gathered r vectors sit in shared memory.  Each Ainv row is read once
+// (coalesced) for all members, so a class costs one pass over its s^2 doubles
+// spread over s/16 CTAs, instead of one warp streaming the packed factor per
+// block.  Lane-strided dot products, fixed shuffle-tree reduction per member:
+// deterministic.
+constexpr int kCgvCG = 8;     // members per class-GEMV group (shared memory: 8 x s doubles)
+constexpr int kCgvRows = 16;  // Ainv rows per CTA (2 per warp; config 4: 8 -> 43.7 us, 16 -> 33.3, 32 -> 43.4)
+
+struct CgvGroup {
+    int cls, first, cnt, s;
+    long long full_off;
+};
+
+template <int CG>
+__global__ void __launch_bounds__(256) k_apply_cgemv(const double* r, double* staging, const int* idx,
+                                                     const double* full, const CgvGroup* groups, const int* mst,
+                                                     const int* stop, int rows) {
+    extern __shared__ double rs[];  // [CG][s]
+    pdl_wait();
+    if (stop && *stop) return;
+    const CgvGroup G = groups[blockIdx.y];
+    const int s = G.s, tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int r0 = blockIdx.x * rows;
+    if (r0 >= s) return;  // uniform per CTA
+    for (int m = 0; m < G.cnt; ++m) {
+        const int base = mst[G.first + m];
+        for (int j = tid; j < s; j += 256) rs[m * s + j] = __ldg(r + __ldg(idx + base + j));
+    }
+    __syncthreads();
+    for (int row = r0 + warp; row < min(s, r0 + rows); row += 8) {
+        const double* A = full + G.full_off + (int64_t)row * s;
+        double acc[CG];
+#pragma unroll
+        for (int m = 0; m < CG; ++m) acc[m] = 0.0;
+        for (int j = lane; j < s; j += 32) {
+            const double a = __ldg(A + j);
+#pragma unroll
+            for (int m = 0; m < CG; ++m)
+                if (m < G.cnt) acc[m] = fma(a, rs[m * s + j], acc[m]);
+        }
+#pragma unroll
+        for (int m = 0; m < CG; ++m) {
+            double v = acc[m];
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+            if (lane == 0 && m < G.cnt) staging[mst[G.first + m] + row] = v;
+        }
+    }
+}
+
 // packed upper triangle by columns -> full symmetric row-major
 __global__ void k_expand_full(const double* fac, const int64_t* fofs, const int* sizes, double* full,
                               const int64_t* full_off) {
@@ -1156,6 +1211,10 @@ struct ie_precond {
     int dmma_pregather = 0;  // IEDD_B200_PREGATHER=1: separate k_gather pass (comparison)
     int mm;        // fixed-width scatter table width (power of two <= 8), 0: CSR
     int* d_posfix; // [mm][N] staged positions, -1 padded
+    int cgv_groups = 0;                 // > 0: class GEMV apply (large translation-shared blocks)
+    ie::CgvGroup* d_cgv = nullptr;
+    int* d_cgv_mst = nullptr;
+    double* d_cgv_full = nullptr;
     double* d_part = nullptr;      // k_apply_big per-chunk partials
     int64_t* d_pofs = nullptr;     // per block offset into d_part
     int64_t part_n = 0;
@@ -1339,6 +1398,21 @@ int precond_apply(const ie_precond* p, const double* r, double* z, double* parti
     a.D = p->D;
     a.wpb = p->wpb;
     a.bpc = p->bpc;
+    if (p->cgv_groups > 0) {
+        const size_t sm = (size_t)kCgvCG * p->smax * sizeof(double);
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_apply_cgemv<kCgvCG>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024);
+            attr = true;
+        }
+        const int rows = kCgvRows;
+        IE_CUDA(launch_k(k_apply_cgemv<kCgvCG>, dim3((p->smax + rows - 1) / rows, (unsigned)p->cgv_groups),
+                         dim3(256), sm, st,
+                         r, W.staging, (const int*)p->d_idx, (const double*)p->d_cgv_full,
+                         (const CgvGroup*)p->d_cgv, (const int*)p->d_cgv_mst, stop, rows));
+        IE_LAUNCHED();
+        return scatter_launch(p, W.staging, r, z, partials, st, stop);
+    }
     if (p->full) {
         const size_t sm = (size_t)p->smax * sizeof(double);
         static bool attr = false;
@@ -1394,6 +1468,9 @@ extern "C" void ie_precond_destroy(ie_precond* p) {
     cudaFree(p->d_mst);
     cudaFree(p->d_rg);
     cudaFree(p->d_posfix);
+    cudaFree(p->d_cgv);
+    cudaFree(p->d_cgv_mst);
+    cudaFree(p->d_cgv_full);
     cudaFree(p->d_part);
     cudaFree(p->d_pofs);
     for (auto& e : p->ws_extra) {
@@ -1832,6 +1909,58 @@ extern "C" int ie_precond_create(const ie_geom* g, const int64_t* h_offsets, con
         }
     }
     p->gemm_ra = 0;
+    if (share_translated && variant == IE_VARIANT_PACKED_INVERSE && smax > ie::kSmemMaxS && smax <= 1024 &&
+        !getenv("IEDD_B200_NO_CGEMV")) {
+        // large translation-shared blocks: class GEMV (full Ainv per class, members in groups of kCgvCG)
+        std::vector<int64_t> full_off(U);
+        int64_t fulln = 0;
+        for (int64_t u = 0; u < U; ++u) {
+            full_off[u] = fulln;
+            fulln += (int64_t)usizes[u] * usizes[u];
+        }
+        std::vector<std::vector<int>> mem(U);
+        for (int64_t k = 0; k < D; ++k) mem[rep[k]].push_back((int)k);
+        std::vector<ie::CgvGroup> groups;
+        std::vector<int> mst;
+        for (int64_t u = 0; u < U; ++u) {
+            for (size_t q = 0; q < mem[u].size(); q += (size_t)ie::kCgvCG) {
+                const int cnt = (int)std::min<size_t>(ie::kCgvCG, mem[u].size() - q);
+                groups.push_back({(int)u, (int)mst.size(), cnt, usizes[u], (long long)full_off[u]});
+                for (int m = 0; m < cnt; ++m) mst.push_back((int)meta[mem[u][q + m]].st_off);
+            }
+        }
+        int64_t* d_fofs2 = nullptr;
+        int* d_usz2 = nullptr;
+        int64_t* d_foff2 = nullptr;
+        cudaError_t e = cudaMalloc(&p->d_cgv_full, fulln * sizeof(double));
+        if (e == cudaSuccess) e = cudaMalloc(&p->d_cgv, groups.size() * sizeof(ie::CgvGroup));
+        if (e == cudaSuccess) e = cudaMalloc(&p->d_cgv_mst, mst.size() * sizeof(int));
+        if (e == cudaSuccess) e = cudaMalloc(&d_fofs2, U * sizeof(int64_t));
+        if (e == cudaSuccess) e = cudaMalloc(&d_usz2, U * sizeof(int));
+        if (e == cudaSuccess) e = cudaMalloc(&d_foff2, U * sizeof(int64_t));
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(p->d_cgv, groups.data(), groups.size() * sizeof(ie::CgvGroup), cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess)
+            e = cudaMemcpyAsync(p->d_cgv_mst, mst.data(), mst.size() * sizeof(int), cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(d_fofs2, ufofs.data(), U * sizeof(int64_t), cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(d_usz2, usizes.data(), U * sizeof(int), cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) e = cudaMemcpyAsync(d_foff2, full_off.data(), U * sizeof(int64_t), cudaMemcpyHostToDevice, st);
+        if (e == cudaSuccess) {
+            ie::k_expand_full<<<(unsigned)U, 256, 0, st>>>(p->d_fac, d_fofs2, d_usz2, p->d_cgv_full, d_foff2);
+            e = cudaGetLastError();
+            ie::g_launches.fetch_add(1);
+        }
+        if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+        cudaFree(d_fofs2);
+        cudaFree(d_usz2);
+        cudaFree(d_foff2);
+        if (e != cudaSuccess) {
+            ie::set_error(std::string("class gemv setup: ") + cudaGetErrorString(e));
+            ie_precond_destroy(p);
+            return IE_ERR_CUDA;
+        }
+        p->cgv_groups = (int)groups.size();
+    }
     if (share_translated && variant == IE_VARIANT_PACKED_INVERSE && smax <= ie::kSmemMaxS) {
         // classes -> full inverses; members grouped by class (ascending block id) -> tiles of <= 64
         std::vector<int64_t> full_off(U);
