@@ -775,9 +775,23 @@ __global__ void __launch_bounds__(kRed) k_lz_control(const double* part, int nch
     }
     __syncthreads();
     const int target = which == 0 ? 1 : m;  // count(x) >= target  <=>  x > lambda
+    // With the previous Ritz value as the interlacing end of the bracket, the
+    // first round places its points geometrically towards that end (spacing
+    // ratio 2^(64/255): the converging Ritz value sits just beside it); later
+    // rounds subdivide uniformly.  About 4 rounds instead of 7.
+    const bool geo = s->have_est;
     for (int it = 0; it < 16; ++it) {
         const double lo = br[0], hi = br[1];
-        const double x = lo + (hi - lo) * (double)(tid + 1) / (double)(kRed + 1);
+        double x;
+        if (it == 0 && geo) {  // increasing in tid; dense next to the interlacing end
+            const double step = 64.0 / (double)(kRed - 1);
+            x = which == 0 ? hi - (hi - lo) * exp2(-(double)tid * step)               // lo .. hi - 2^-64 (hi - lo)
+                           : lo + (hi - lo) * exp2(-(double)(kRed - 1 - tid) * step);  // lo + 2^-64 (hi - lo) .. hi
+        } else {
+            x = lo + (hi - lo) * (double)(tid + 1) / (double)(kRed + 1);
+        }
+        __shared__ double xs[kRed];
+        xs[tid] = x;
         const bool above = sturm_count(a, b, m, x) >= target;
         const unsigned mk = __ballot_sync(0xffffffffu, above);
         if (lane == 0) above_mask[warp] = mk;
@@ -789,10 +803,9 @@ __global__ void __launch_bounds__(kRed) k_lz_control(const double* part, int nch
                     first = w2 * 32 + __ffs(above_mask[w2]) - 1;
                     break;
                 }
-            const double nlo = first == 0 ? lo : lo + (hi - lo) * (double)first / (double)(kRed + 1);
-            const double nhi = first == kRed ? hi : lo + (hi - lo) * (double)(first + 1) / (double)(kRed + 1);
-            br[0] = nlo;
-            br[1] = nhi;
+            // the points increase with tid: lambda lies between point first-1 and point first
+            br[0] = first == 0 ? lo : xs[first - 1];
+            br[1] = first == kRed ? hi : xs[first];
         }
         __syncthreads();
         const double nlo = br[0], nhi = br[1];
