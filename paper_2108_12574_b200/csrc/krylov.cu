@@ -331,6 +331,37 @@ __global__ void k_reduce_rows(const double* part, int nch, double* out) {
     if (threadIdx.x == 0) out[blockIdx.x] = v;
 }
 
+constexpr int kLzMaxM = 1024;  // tridiagonal size staged in shared memory by k_lz_control
+
+// Sturm count of eigenvalues < x for the symmetric tridiagonal (a, b2 = b^2)
+// from the three-term recurrence of the leading principal minors
+// p_i = (a_i - x) p_{i-1} - b_{i-1}^2 p_{i-2}: the count is the number of sign
+// changes (a zero minor keeps the previous sign, as the pivot form's tiny
+// positive substitute does).  Two dependent FP64 operations per step instead
+// of a division; exact power-of-two rescaling keeps the minors in range.
+__device__ int sturm_count_minors(const double* a, const double* b2, int m, double x) {
+    double pm1 = 1.0, p = a[0] - x;
+    bool neg = p < 0.0;
+    int cnt = neg ? 1 : 0;
+    for (int i = 1; i < m; ++i) {
+        const double pn = fma(a[i] - x, p, -b2[i - 1] * pm1);
+        pm1 = p;
+        p = pn;
+        if (p != 0.0) {
+            const bool n = p < 0.0;
+            cnt += n != neg;
+            neg = n;
+        }
+        const double ap = fabs(p);
+        if (ap > 0x1p+500 || (ap < 0x1p-500 && ap != 0.0)) {
+            const double sc = ap > 1.0 ? 0x1p-500 : 0x1p+500;
+            p *= sc;
+            pm1 *= sc;
+        }
+    }
+    return cnt;
+}
+
 // Sturm count of eigenvalues < x for the symmetric tridiagonal (a, b).
 __device__ int sturm_count(const double* a, const double* b, int m, double x) {
     int cnt = 0;
@@ -775,6 +806,15 @@ __global__ void __launch_bounds__(kRed) k_lz_control(const double* part, int nch
     }
     __syncthreads();
     const int target = which == 0 ? 1 : m;  // count(x) >= target  <=>  x > lambda
+    __shared__ double sa[kLzMaxM], sb2[kLzMaxM];
+    const bool smem_tri = m <= kLzMaxM;
+    if (smem_tri) {
+        for (int i = tid; i < m; i += kRed) {
+            sa[i] = a[i];
+            sb2[i] = i < m - 1 ? b[i] * b[i] : 0.0;
+        }
+        __syncthreads();
+    }
     // With the previous Ritz value as the interlacing end of the bracket, the
     // first round places its points geometrically towards that end (spacing
     // ratio 2^(64/255): the converging Ritz value sits just beside it); later
@@ -792,7 +832,7 @@ __global__ void __launch_bounds__(kRed) k_lz_control(const double* part, int nch
         }
         __shared__ double xs[kRed];
         xs[tid] = x;
-        const bool above = sturm_count(a, b, m, x) >= target;
+        const bool above = (smem_tri ? sturm_count_minors(sa, sb2, m, x) : sturm_count(a, b, m, x)) >= target;
         const unsigned mk = __ballot_sync(0xffffffffu, above);
         if (lane == 0) above_mask[warp] = mk;
         __syncthreads();
