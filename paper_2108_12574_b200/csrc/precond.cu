@@ -555,6 +555,9 @@ __global__ void __launch_bounds__(256, 2) k_apply_dmma(GemmArgs a) {
     const int kq = lane & 3;
     const double* bcol0 = Bs + (cq * 16 + (lane >> 2)) * bst + kq;
     const double* bcol1 = bcol0 + 8 * bst;
+    // n-tiles of this warp holding members (narrow tiles of small decompositions
+    // leave whole warps idle instead of multiplying empty columns)
+    const int nt_live = cnt > cq * 16 + 8 ? 2 : (cnt > cq * 16 ? 1 : 0);
     for (int ch = 0; ch < nchunks; ++ch) {
         // wait until chunk ch (and the B gather) has landed
         asm volatile("cp.async.wait_group %0;\n" ::"n"(kDmmaStages - 2));
@@ -562,17 +565,28 @@ __global__ void __launch_bounds__(256, 2) k_apply_dmma(GemmArgs a) {
         load_chunk(ch + kDmmaStages - 1);
         // slot of chunk ch - 1 is overwritten only after the barrier above
         const double* ac = As + (ch % kDmmaStages) * kGemmKC * AP;
+        if (nt_live == 2) {
 #pragma unroll
-        for (int ks = 0; ks < kGemmKC / 4; ++ks) {
-            const int kg = ch * kGemmKC + ks * 4;
-            const double b0 = bcol0[kg];
-            const double b1 = bcol1[kg];
-            const double* ap = ac + (ks * 4 + kq) * AP + arow;
+            for (int ks = 0; ks < kGemmKC / 4; ++ks) {
+                const int kg = ch * kGemmKC + ks * 4;
+                const double b0 = bcol0[kg];
+                const double b1 = bcol1[kg];
+                const double* ap = ac + (ks * 4 + kq) * AP + arow;
 #pragma unroll
-            for (int m = 0; m < MT; ++m) {
-                const double av = ap[8 * m];
-                dmma884(acc[m][0][0], acc[m][0][1], av, b0);
-                dmma884(acc[m][1][0], acc[m][1][1], av, b1);
+                for (int m = 0; m < MT; ++m) {
+                    const double av = ap[8 * m];
+                    dmma884(acc[m][0][0], acc[m][0][1], av, b0);
+                    dmma884(acc[m][1][0], acc[m][1][1], av, b1);
+                }
+            }
+        } else if (nt_live == 1) {  // narrow tile: this warp's second n-tile is empty
+#pragma unroll
+            for (int ks = 0; ks < kGemmKC / 4; ++ks) {
+                const int kg = ch * kGemmKC + ks * 4;
+                const double b0 = bcol0[kg];
+                const double* ap = ac + (ks * 4 + kq) * AP + arow;
+#pragma unroll
+                for (int m = 0; m < MT; ++m) dmma884(acc[m][0][0], acc[m][0][1], ap[8 * m], b0);
             }
         }
     }
