@@ -412,6 +412,8 @@ struct PcgWork {
     int gnodes = 0;  // kernel nodes in the captured iteration
     PcgState* st = nullptr;
     PcgState* host = nullptr;
+    PcgState* host2 = nullptr;            // second pinned status slot (pipelined polling)
+    cudaEvent_t poll_ev[2] = {nullptr, nullptr};
     std::vector<cudaEvent_t> ev;
     bool busy = false;
     ~PcgWork() {
@@ -430,6 +432,9 @@ struct PcgWork {
         if (join_ev) cudaEventDestroy(join_ev);
         cudaFree(st);
         if (host) cudaFreeHost(host);
+        if (host2) cudaFreeHost(host2);
+        for (auto e : poll_ev)
+            if (e) cudaEventDestroy(e);
         for (auto e : ev) cudaEventDestroy(e);
     }
 };
@@ -465,6 +470,9 @@ static PcgWork* work_acquire(int N, int64_t cap, int* rc) {
     if (e == cudaSuccess) e = cudaEventCreateWithFlags(&w->join_ev, cudaEventDisableTiming);
     if (e == cudaSuccess) e = cudaMalloc(&w->st, sizeof(PcgState));
     if (e == cudaSuccess) e = cudaMallocHost(&w->host, sizeof(PcgState));
+    if (e == cudaSuccess) e = cudaMallocHost(&w->host2, sizeof(PcgState));
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&w->poll_ev[0], cudaEventDisableTiming);
+    if (e == cudaSuccess) e = cudaEventCreateWithFlags(&w->poll_ev[1], cudaEventDisableTiming);
     if (e != cudaSuccess) {
         set_error(std::string("pcg workspace: ") + cudaGetErrorString(e));
         delete w;
@@ -636,7 +644,7 @@ extern "C" int ie_pcg_f64(const ie_matvec* A, const ie_precond* T, const double*
             W->key_t = kt;
         }
     }
-    int64_t it = 1;
+    int64_t it = 1, nbatch = 0;
     for (; it <= max_iters + 1; ++it) {
         const int do_p = it <= max_iters;
         const int pending = it >= 2;
@@ -652,9 +660,20 @@ extern "C" int ie_pcg_f64(const ie_matvec* A, const ie_precond* T, const double*
             if ((rc = enqueue_iter(it, do_p, pending, spec, st, true, it))) return rc;
         }
         if (it % kBatch == 0 || it == max_iters + 1) {
-            IE_CUDA(cudaMemcpyAsync(W->host, W->st, sizeof(PcgState), cudaMemcpyDeviceToHost, st));
-            IE_CUDA(cudaStreamSynchronize(st));
-            if (W->host->stop) break;
+            // pipelined status polling: this batch's state copy is queued behind
+            // it, and the host waits on the PREVIOUS batch's copy, so the GPU
+            // never drains between batches (at most one batch of no-op
+            // iterations -- every kernel returns on the device stop flag --
+            // follows convergence)
+            const int slot = (int)(nbatch & 1);
+            PcgState* hs = slot ? W->host2 : W->host;
+            IE_CUDA(cudaMemcpyAsync(hs, W->st, sizeof(PcgState), cudaMemcpyDeviceToHost, st));
+            IE_CUDA(cudaEventRecord(W->poll_ev[slot], st));
+            if (nbatch > 0) {
+                IE_CUDA(cudaEventSynchronize(W->poll_ev[slot ^ 1]));
+                if ((slot ? W->host : W->host2)->stop) break;
+            }
+            ++nbatch;
         }
     }
     IE_CUDA(cudaMemcpyAsync(W->host, W->st, sizeof(PcgState), cudaMemcpyDeviceToHost, st));
@@ -1418,7 +1437,7 @@ extern "C" int ie_pcg_sharded_f64(const ie_matvec* A, const ie_precond* T, ie_co
     }
     cudaGraphExec_t gexec = W->gexec;
     const int gnodes = W->gnodes;
-    const int64_t kBatch = 4;
+    static const int64_t kBatch = getenv("IEDD_B200_PCG_BATCH") ? atoll(getenv("IEDD_B200_PCG_BATCH")) : 4;
     for (int64_t it = 1; it <= max_iters + 1; ++it) {
         const int do_p = it <= max_iters;
         const int pending = it >= 2;
