@@ -112,9 +112,10 @@ __global__ void k_pcg_init(const double* part, int nch, PcgState* s, double tol,
 // Every CTA reduces the same partials in the same order and takes the same
 // decision; CTA 0 records it in the state.  Every load that does not depend
 // on the reduction (state scalars, the history entry of the stagnation test,
-// this thread's partials and its p, q chunk values) is issued before it, so
+// this thread's partials and its p, q, r chunk values) is issued before it, so
 // the serial prologue costs about one memory round trip.
-__global__ void __launch_bounds__(kRed) k_iter_a(const double* part_pq, const double* part_res, int nch, int do_p,
+template <bool WITH_U>
+__global__ void __launch_bounds__(kRed, 4) k_iter_a(const double* part_pq, const double* part_res, int nch, int do_p,
                                                  int pending, long long it, PcgState* s, double* hist, double* u,
                                                  double* r, const double* p, const double* q, int N, double* amax) {
     __shared__ double sh[kRed];
@@ -126,12 +127,13 @@ __global__ void __launch_bounds__(kRed) k_iter_a(const double* part_pq, const do
     const long long k = it - 1;
     const double h30 = (pending && k >= 30 && threadIdx.x == 0) ? hist[k - 30] : 0.0;
     const int base = blockIdx.x * kChunk;
-    double pv[kChunk / kRed], qv[kChunk / kRed];
+    double pv[kChunk / kRed], qv[kChunk / kRed], rv[kChunk / kRed];
 #pragma unroll
     for (int e = 0; e < kChunk / kRed; ++e) {
         const int i = base + e * kRed + threadIdx.x;
-        pv[e] = (do_p && u && i < N) ? p[i] : 0.0;  // p only for the in-kernel u update
+        pv[e] = (WITH_U && do_p && i < N) ? p[i] : 0.0;  // p only for the in-kernel u update
         qv[e] = (do_p && i < N) ? q[i] : 0.0;
+        rv[e] = (!WITH_U && do_p && i < N) ? r[i] : 0.0;  // hoisted where registers allow
     }
     double lp = 0.0, lr = 0.0;
     for (int c = threadIdx.x; c < nch; c += kRed) {
@@ -177,11 +179,11 @@ __global__ void __launch_bounds__(kRed) k_iter_a(const double* part_pq, const do
     __syncthreads();
     if (decided || !do_p) return;
     const double al = rho_prev / denom;
-    if (!u) {  // u += alpha p runs concurrently in k_update_u (graph side branch)
+    if (!WITH_U) {  // u += alpha p runs concurrently in k_update_u (graph side branch)
 #pragma unroll
         for (int e = 0; e < kChunk / kRed; ++e) {
             const int i = base + e * kRed + threadIdx.x;
-            if (i < N) r[i] = __dsub_rn(r[i], __dmul_rn(al, qv[e]));
+            if (i < N) r[i] = __dsub_rn(rv[e], __dmul_rn(al, qv[e]));
         }
         return;
     }
@@ -210,12 +212,19 @@ __global__ void __launch_bounds__(kRed) k_update_u(const PcgState* s, double* u,
     if (s->stop) return;
     const double al = s->alpha;
     const int base = blockIdx.x * kChunk;
+    double uv[kChunk / kRed], pv[kChunk / kRed];  // all loads ahead of the first store
+#pragma unroll
+    for (int e = 0; e < kChunk / kRed; ++e) {
+        const int i = base + e * kRed + threadIdx.x;
+        uv[e] = i < N ? u[i] : 0.0;
+        pv[e] = i < N ? p[i] : 0.0;
+    }
     double m = 0.0;
 #pragma unroll
     for (int e = 0; e < kChunk / kRed; ++e) {
         const int i = base + e * kRed + threadIdx.x;
         if (i < N) {
-            const double un = __dadd_rn(u[i], __dmul_rn(al, p[i]));
+            const double un = __dadd_rn(uv[e], __dmul_rn(al, pv[e]));
             u[i] = un;
             m = fmax(m, fabs(un));
         }
@@ -582,7 +591,7 @@ extern "C" int ie_pcg_f64(const ie_matvec* A, const ie_precond* T, const double*
         IE_LAUNCHED();
         // in the captured iteration u += alpha p forks onto a side branch beside the apply
         const bool fork_u = itarg < 0 && do_p && spec && !no_fork;
-        IE_CUDA(launch_k(k_iter_a, dim3(nch), dim3(kRed), 0, s2, (const double*)part_pq, (const double*)part_res, nch,
+        IE_CUDA(launch_k(fork_u ? k_iter_a<false> : k_iter_a<true>, dim3(nch), dim3(kRed), 0, s2, (const double*)part_pq, (const double*)part_res, nch,
                          do_p, pending, (long long)itarg, W->st, W->hist, fork_u ? nullptr : uu, W->r,
                          (const double*)p, (const double*)q, N, W->amax));
         IE_LAUNCHED();
@@ -746,9 +755,9 @@ __global__ void k_lz_first(double* V, double* AV, double* avj, const double* w, 
                            int N) {
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= N) return;
-    const double d = s->nrm;
-    V[i] = w[i] / d;
-    const double a = aw[i] / d;
+    const double d = s->nrm, wi = w[i], awi = aw[i];  // both loads ahead of the stores
+    V[i] = wi / d;
+    const double a = awi / d;
     AV[i] = a;
     avj[i] = a;
 }
@@ -760,9 +769,9 @@ __global__ void k_lz_next(double* V, double* AV, double* avj, const double* w, c
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= N) return;
     const int64_t off = (s->j + 1) * (int64_t)N;
-    const double d = s->beta;
-    V[off + i] = w[i] / d;
-    const double a = aw[i] / d;
+    const double d = s->beta, wi = w[i], awi = aw[i];
+    V[off + i] = wi / d;
+    const double a = awi / d;
     AV[off + i] = a;
     avj[i] = a;
 }
@@ -1395,7 +1404,7 @@ extern "C" int ie_pcg_sharded_f64(const ie_matvec* A, const ie_precond* T, ie_co
         IE_LAUNCHED();
         if (do_p && (r2 = allgather_chunks(part_pq, 1, s))) return r2;
         if (pending && (r2 = allgather_chunks(part_res, 1, s))) return r2;
-        k_iter_a<<<nchb, kRed, 0, s>>>(part_pq, part_res, nch, do_p, pending, itarg, S, dh, uu, r, p, q, (int)nb,
+        (uu ? k_iter_a<true> : k_iter_a<false>)<<<nchb, kRed, 0, s>>>(part_pq, part_res, nch, do_p, pending, itarg, S, dh, uu, r, p, q, (int)nb,
                                        amax + 2 * (size_t)c0);
         IE_LAUNCHED();
         if (spec) {

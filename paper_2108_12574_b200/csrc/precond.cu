@@ -459,8 +459,9 @@ __host__ __device__ constexpr int pad4mod16(int x) { return x + ((4 - (x & 15)) 
 template <int MT>
 __global__ void __launch_bounds__(256, 2) k_apply_dmma(GemmArgs a) {
     extern __shared__ double sg[];
-    pdl_wait();
-    if (a.stop && *a.stop) return;
+    // Everything before pdl_wait() reads only setup-time data (tile descriptors,
+    // member offsets, point indices, the shared inverses), so under programmatic
+    // dependent launch it overlaps the tail of the kernel that produces r.
     constexpr int AP = pad4mod16(16 * MT);  // A row stride (k-major rows of length >= 2*8*MT)
     const TileDesc td = a.tdesc[blockIdx.x];
     const int first = td.first, cnt = td.cnt, s = td.s;
@@ -486,29 +487,19 @@ __global__ void __launch_bounds__(256, 2) k_apply_dmma(GemmArgs a) {
         }
     }
     __syncthreads();
-    if (a.rg) {
-        for (int e = tid; e < s * kGemmTN; e += 256) {
-            const int jj = e / s, i = e - jj * s;
-            if (colbase[jj] >= 0) cp_async8(Bs + jj * bst + i, a.rg + colbase[jj] + i);
-        }
-    } else {
-        // gather straight from r through the block's point indices: thread t owns
-        // column t/4 and rows k = t%4 + 4q; all its index loads in flight at once
-        // (one memory round trip), then their cp.async copies
-        constexpr int kGq = (kSmemMaxS + 3) / 4;  // 40
-        const int jj = tid >> 2, k0 = tid & 3;
+    // gather indices straight from the block's point indices: thread t owns
+    // column t/4 and rows k = t%4 + 4q; all its index loads in flight at once
+    constexpr int kGq = (kSmemMaxS + 3) / 4;  // 40
+    const int jj = tid >> 2, k0 = tid & 3;
+    int gi[kGq];
+    if (!a.rg) {
         const int64_t cb = colbase[jj];
-        int gi[kGq];
 #pragma unroll
         for (int q = 0; q < kGq; ++q) {
             const int k = k0 + 4 * q;
             gi[q] = (cb >= 0 && k < s) ? __ldg(a.idx + cb + k) : -1;
         }
-#pragma unroll
-        for (int q = 0; q < kGq; ++q)
-            if (gi[q] >= 0) cp_async8(Bs + jj * bst + k0 + 4 * q, a.r + gi[q]);
     }
-    cp_async_commit();
     const int nchunks = (s + kGemmKC - 1) / kGemmKC;
     // a chunk is kc contiguous rows of A: element e = kk * s + i of the chunk goes to
     // smem row kk, column i; this thread's (kk, i) are the same for every chunk
@@ -523,7 +514,7 @@ __global__ void __launch_bounds__(256, 2) k_apply_dmma(GemmArgs a) {
         const int kk = e / s;
         a_dst[q] = kk * AP + (e - kk * s);
     }
-    auto load_chunk = [&](int ch) {
+    auto issue_chunk = [&](int ch) {
         if (ch < nchunks) {
             double* dst = As + (ch % kDmmaStages) * kGemmKC * AP;
             const int k0 = ch * kGemmKC;
@@ -543,9 +534,29 @@ __global__ void __launch_bounds__(256, 2) k_apply_dmma(GemmArgs a) {
                 }
             }
         }
+    };
+    auto load_chunk = [&](int ch) {
+        issue_chunk(ch);
         cp_async_commit();  // always commit (possibly empty) so group counting stays uniform
     };
-    for (int ch = 0; ch < kDmmaStages - 1; ++ch) load_chunk(ch);
+    issue_chunk(0);  // committed below together with the r gather (group 0)
+    pdl_wait();
+    if (a.stop && *a.stop) {
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
+        return;
+    }
+    if (a.rg) {
+        for (int e = tid; e < s * kGemmTN; e += 256) {
+            const int jc = e / s, i = e - jc * s;
+            if (colbase[jc] >= 0) cp_async8(Bs + jc * bst + i, a.rg + colbase[jc] + i);
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < kGq; ++q)
+            if (gi[q] >= 0) cp_async8(Bs + jj * bst + k0 + 4 * q, a.r + gi[q]);
+    }
+    cp_async_commit();
+    for (int ch = 1; ch < kDmmaStages - 1; ++ch) load_chunk(ch);
     double acc[MT][2][2];
 #pragma unroll
     for (int m = 0; m < MT; ++m)
