@@ -836,10 +836,6 @@ __global__ void __launch_bounds__(PTS == 16 ? 256 : 1024, PTS == 16 ? 2 : 1) k_f
     const bool live = line < a.nlines;
     const int lgi = a.lg_ninner;
     const int o = line >> lgi, i = line & ((1 << lgi) - 1);
-    if ((in_real && a.scale_in) || (out_real && a.scale_out)) {
-        column_scales_dyn(a, csc);
-        __syncthreads();
-    }
     double vr[PTS], vi[PTS];
     constexpr bool tma_mode = TMA && MODE == kFusedCC && STRIDED;
     if constexpr (tma_mode) {
@@ -891,6 +887,12 @@ __global__ void __launch_bounds__(PTS == 16 ? 256 : 1024, PTS == 16 ? 2 : 1) k_f
                 vi[m] = v.y;
             }
         }
+    }
+    // the column scales (a reduction over the max|x| partials) after the line
+    // loads are issued: the two memory round trips overlap
+    if ((in_real && a.scale_in) || (out_real && a.scale_out)) {
+        column_scales_dyn(a, csc);
+        __syncthreads();
     }
     if constexpr (in_real) {
         if (a.scale_in) {
