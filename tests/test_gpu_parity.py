@@ -847,3 +847,31 @@ class TestGoldenRunner:
         lines = []
         rc = golden.run_golden(["interface-3d"], out=lines.append)
         assert rc == golden.EXIT_OK, "\n".join(lines)
+
+
+class TestScatterWidths:
+    """The fixed-width scatter instantiations (1, 2, 4 and 8 staged
+    contributions per point; the batched, prefetching loads) on point counts
+    that are not multiples of the 2,048-point chunk, against the oracle's
+    apply and PCG."""
+
+    @pytest.mark.parametrize("dim,n,m,w,kind", [(1, 3000, 8, 1, "schwarz"), (2, 50, 5, 1, "schwarz"),
+                                                (2, 50, 5, 2, "schwarz"), (3, 14, 7, 1, "schwarz"),
+                                                (2, 50, 5, 0, "jacobi")])
+    def test_apply_and_pcg(self, ie, rng, dim, n, m, w, kind):
+        grid = ie.build_grid(dim, n)
+        op = ie.build_operator(grid, lattice="cell")
+        og = O.build_grid(dim, n)
+        oop = O.build_operator(og, "cell")
+        opre = O.SchwarzPrecond(oop, O.build_decomposition(og, m, w, kind))
+        dec = ie.build_decomposition(grid, m, w, kind)
+        x = rng.standard_normal(op.n)
+        for share in (True, False):
+            pre = ie.from_decomposition(op, dec, share_translated=share)
+            assert rel(pre.apply(x), opre.apply(x)) <= 1e-12
+        pre = ie.from_decomposition(op, dec)
+        u, rep = ie.solve(ie.KernelMatvec(op, method="direct"), pre, x, tol=1e-10)
+        a = oop.dense()
+        ou, orep = O.pcg(lambda v: a @ v, opre, x, tol=1e-10)
+        assert rep.converged == orep.converged and abs(rep.n_it - orep.n_it) <= 2
+        assert rel(u, ou) <= 1e-9
