@@ -866,7 +866,7 @@ __device__ __forceinline__ void scatter_fixed_chunk(int c, const double* staging
             for (int q = 0; q < MM; ++q) pn[g][q] = i < i1 ? __ldg(pos + (int64_t)q * N + i) : -1;
         }
     }
-#pragma unroll 1
+#pragma unroll 1  // fully unrolled (56 registers): no measurable change
     for (int e0 = 0; e0 < kChunk / 256; e0 += G) {
         int pp[G][MM];
 #pragma unroll
