@@ -113,6 +113,16 @@ def _dist():
     return ws, rank, local
 
 
+def config_keys(ws: int) -> dict:
+    """The `config` object of the JSON line -- identical in both arms (ours
+    and --impl reference) at the same N, so the driver can match them."""
+    return {"workload": WORKLOAD, "N": CFG["n"] ** CFG["dim"], "subdomains": CFG["m"] ** CFG["dim"],
+            "tol": 1e-10, "matvec": "circulant-embedding FFT (the reference's ToeplitzMatvec algorithm)",
+            "l2": "not flushed: the per-iteration working set (10 N-vectors, 84 MB + FFT work buffer) "
+                  "streams through HBM",
+            "parallelism": "single GPU" if ws == 1 else f"row/subdomain bands x{ws}"}
+
+
 def _time_iters(ie, mv, pre, f, iters, st):
     """Device time (ms) of exactly `iters` PCG iterations through ie.solve."""
     import torch
@@ -156,7 +166,8 @@ def run_ours(args):
             os.environ.setdefault("WORLD_SIZE", str(ws))
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         from paper_2108_12574_b200 import distributed as D
-        return D.bench_sharded(args, METRIC, CFG, WORKLOAD)
+        return D.bench_sharded(args, METRIC, CFG, WORKLOAD, config_keys=config_keys(ws),
+                               cpu_baseline=None if args.no_cpu else lambda: cpu_baseline(max(1, min(10, args.steps))))
 
     st = torch.cuda.current_stream()
     grid = ie.build_grid(CFG["dim"], CFG["n"])
@@ -228,30 +239,47 @@ def run_ours(args):
         del pre_ns
 
     step_ms = ms / args.steps
-    kern = {"matvec_pass_ms": mv_ms, "apply_ms": apply_ms}
-    dom = max(kern, key=kern.get)
-    if dom == "apply_ms":
-        s_sum = sum(s.size for s in dec.subdomains)
-        s2 = sum(float(s.size) ** 2 for s in dec.subdomains)
-        roof = {"bound": "fp64-tensor", "kernel": "k_apply_dmma (DMMA class GEMM, gathers its r columns) + k_scatter_fixed",
-                "achieved": 2.0 * s2 / (apply_ms * 1e-3) / 1e12, "unit": "TFLOP/s", "peak": fp64_peak_tflops,
-                "traffic": None, "note": f"flops = 2 sum_k s_k^2 (Sigma s = {s_sum})"}
-    else:
-        # K1b 2-RHS pass: n row FFTs forward, 2n column FFTs forward + inverse (fused), n row FFTs inverse,
-        # each 5 M log2 M flops (M = 2n): the conventional complex-FFT count
-        M = 2 * CFG["n"]
-        lines = CFG["n"] + 2 * (2 * CFG["n"]) + CFG["n"]
-        flops = lines * 5.0 * M * np.log2(M)
-        roof = {"bound": "fp64", "kernel": "k_fft8 x3 (row fwd, fused column fwd*sym*inv, row inv)",
-                "achieved": flops / (mv_ms * 1e-3) / 1e12, "unit": "TFLOP/s", "peak": fp64_peak_tflops,
-                "traffic": 92.7e6,
-                "note": "flops = 5 M log2 M per line FFT x 6n lines; peak = live DFMA microbenchmark; "
-                        "traffic = dram read+write bytes of the three launches, ncu --set full "
-                        "(profiles/r1b_ncu_summary.md; the n x 2n work buffer stays L2-resident); "
-                        "bound in practice by the L1/shared-memory data pipe (73% busy in the fused "
-                        "column pass: exchanges 60%, strided column I/O 20%, twiddles 10%)"}
-    roof["frac"] = roof["achieved"] / roof["peak"] if roof.get("peak") else None
-    roof["share_of_step"] = kern[dom] / step_ms
+    # ---- per-kernel device times inside the PCG iteration: a profiled solve
+    # (ie_pcg_profile_f64: iterations launched one by one with CUDA events
+    # between the kernel groups on the solver's stream), steady 2-RHS iterations
+    ph = _profile_phases(ie, _lib, mv, pre, f, max(8, min(args.steps, 24)))
+    kern = {"matvec_pass_ms": ph[0], "post_pass_ms": ph[1], "iter_a_ms": ph[2], "apply_ms": ph[3],
+            "iter_b_ms": ph[4], "k4_vector_ms": ph[1] + ph[2] + ph[4],
+            "standalone_matvec_pass_ms": mv_ms, "standalone_apply_ms": apply_ms}
+    dmma = ctypes.c_double(0.0)
+    _lib.check(L.ie_dmma_peak(ctypes.byref(dmma), _lib.stream_ptr()), "dmma peak")
+    dmma_peak_tflops = dmma.value / 1e12
+    traffic = _traffic()
+    # K1b 2-RHS pass: n row FFTs forward, 2n column FFTs forward + inverse (fused), n row FFTs inverse,
+    # each 5 M log2 M flops (M = 2n): the conventional complex-FFT count
+    M = 2 * CFG["n"]
+    lines = CFG["n"] + 2 * (2 * CFG["n"]) + CFG["n"]
+    fft_flops = lines * 5.0 * M * np.log2(M)
+    s2 = sum(float(sd.size) ** 2 for sd in dec.subdomains)
+    s_sum = sum(sd.size for sd in dec.subdomains)
+    hbm = peaks.get("hbm_gbs")
+    rooflines = {
+        "fft_pass": {"bound": "fp64", "kernel": "k_fft8 x3 (row fwd, fused column fwd*sym*inv, row inv)",
+                     "achieved": fft_flops / (ph[0] * 1e-3) / 1e12, "unit": "TFLOP/s", "peak": fp64_peak_tflops,
+                     "traffic": traffic.get("fft_pass"),
+                     "note": "flops = 5 M log2 M per line FFT x 6n lines (M = 2n); peak = live 8-chain DFMA "
+                             "microbenchmark (ie_fp64_peak); traffic = ncu dram bytes of the three launches"},
+        "apply": {"bound": "fp64-tensor", "kernel": "k_apply_dmma (class GEMM on DMMA, gathers r) + k_scatter_fixed",
+                  "achieved": 2.0 * s2 / (ph[3] * 1e-3) / 1e12, "unit": "TFLOP/s", "peak": dmma_peak_tflops,
+                  "traffic": traffic.get("apply"),
+                  "note": f"flops = 2 sum_k s_k^2 (Sigma s = {s_sum}); peak = live DMMA m8n8k4 microbenchmark "
+                          "(ie_dmma_peak)"},
+        "k4_vectors": {"bound": "hbm", "kernel": "k_post_pass + k_iter_a (u and r updates) + k_iter_b",
+                       "achieved": 80.0 * N / (kern["k4_vector_ms"] * 1e-3) / 1e9, "unit": "GB/s", "peak": hbm,
+                       "traffic": traffic.get("k4_vectors"),
+                       "note": "bytes = 80 N per iteration (SURVEY 8(d): read p, u, r, q, z, f, Au; write u, r, "
+                               "p); the kernels move 104 N (q and p are read twice)"},
+    }
+    for r_ in rooflines.values():
+        r_["frac"] = r_["achieved"] / r_["peak"] if r_.get("peak") else None
+    shares = {"fft_pass": ph[0], "apply": ph[3], "k4_vectors": kern["k4_vector_ms"]}
+    dom = max(shares, key=shares.get)
+    roof = dict(rooflines[dom], dominant=dom, share_of_step=shares[dom] / step_ms)
     out = {
         "metric": METRIC,
         "value": args.steps / (ms * 1e-3),
@@ -265,12 +293,12 @@ def run_ours(args):
         "vs_baseline": None,
         "dtype": "f64",
         "data": "synthetic (BASELINE.json config 5, seeded)",
-        "config": {"workload": WORKLOAD, "N": N, "subdomains": dec.n_subdomains,
-                   "matvec": f"{mv.method} ({'circulant-embedding FFT, 2 RHS per complex pass' if mv.method == 'fft' else 'K1 direct sum'})",
-                   "share_translated": not args.no_share, "l2": "not flushed; working set > L2 only for K1 sources",
-                   "precond_build_s": t_build, "parallelism": "single GPU"},
+        "config": config_keys(1),
+        "details": {"matvec": f"{mv.method} ({'2 RHS per complex pass' if mv.method == 'fft' else 'K1 direct sum'})",
+                    "share_translated": not args.no_share, "precond_build_s": t_build},
         "kernels_ms": kern,
         "roofline": roof,
+        "rooflines": rooflines,
         "kernel_matvec": {
             "kernel": "k_matvec<2,2,16,ADJ> (K1 direct sum, log kernel evaluated on the fly, one evaluation "
                       "shared by 16 consecutive rows, 2 RHS)",
@@ -294,6 +322,32 @@ def run_ours(args):
         out["cpu_baseline"] = cpu_baseline(max(1, min(10, args.steps)))  # ~8 s of CPU work
     print(json.dumps(out))
     return out
+
+
+def _profile_phases(ie, _lib, mv, pre, f, iters):
+    """Mean device ms per steady-state iteration of [matvec, k_post_pass,
+    k_iter_a, apply, k_iter_b] (ie_pcg_profile_f64)."""
+    import torch
+    u = torch.empty_like(f)
+    hist = np.zeros(iters + 1)
+    n_it = ctypes.c_int64(0)
+    flags = np.zeros(2, dtype=np.int32)
+    times = np.zeros(2)
+    ph = np.zeros(5)
+    _lib.check(_lib.lib().ie_pcg_profile_f64(mv.handle, pre.handle, _lib.ptr(f), _lib.ptr(u), 1e-10, iters,
+                                             _lib.np_ptr(hist), ctypes.byref(n_it), _lib.np_ptr(flags),
+                                             _lib.np_ptr(times), _lib.np_ptr(ph), _lib.stream_ptr()), "profile")
+    return [float(x) for x in ph]
+
+
+def _traffic():
+    """Per-launch DRAM bytes (read + write) of the kernel groups from the
+    committed ncu --set full capture (profiles/traffic.json), if present."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as fh:
+            return json.load(fh).get("bytes", {})
+    except OSError:
+        return {}
 
 
 def _apply_bytes(dec, N, shared):
@@ -342,8 +396,8 @@ def run_reference(args):
            "warmup": args.warmup, "ms_per_step": 1e3 * dt / rep.n_it, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (BASELINE.json config 5)",
            "impl": "reference",
-           "config": {"workload": WORKLOAD, "N": int(f.size), "precond_build_s": t_build,
-                      "parallelism": "host CPU (reference algorithm port)"},
+           "config": config_keys(ws),
+           "details": {"precond_build_s": t_build, "where": "host CPU (reference algorithm port, rank 0)"},
            "cpu_baseline": {"value": v, "unit": "iter/s", "cores": 1, "kind": "port",
                             "sample": f"{rep.n_it} PCG iterations of config 5 after {args.warmup} warm-up"},
            "e2e": {"value": v, "unit": "iter/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}

@@ -58,12 +58,14 @@ typedef struct ie_geom {
 typedef struct ie_matvec ie_matvec;
 
 #define IE_MATVEC_DIRECT 0 /* K1: O(N^2) direct sum, kernel evaluated per pair */
-#define IE_MATVEC_FFT 1    /* K1b: O(N log N) circulant-embedding FFT (n = 2^k <= 2048) */
+#define IE_MATVEC_FFT 1    /* K1b: O(N log N) circulant-embedding FFT (any n <= 4096) */
 
 /* Replaces ToeplitzMatvec.__init__ (toeplitz.py:19-32).  ie_matvec_create
  * builds the direct-sum operator (device log table); ie_matvec_create_method
  * selects the method -- IE_MATVEC_FFT also computes the real, even symbol of
- * the (2n)^dim embedding on the device. */
+ * the M^dim circulant embedding on the device, M = the smallest power of two
+ * >= 2n - 1 (= 2n, the reference's size, for power-of-two n; any M >= 2n - 1
+ * gives the same Toeplitz product). */
 int ie_matvec_create(const ie_geom* g, ie_matvec** out);
 int ie_matvec_create_method(const ie_geom* g, int32_t method, ie_matvec** out);
 void ie_matvec_destroy(ie_matvec* m);
@@ -82,28 +84,30 @@ int ie_matvec_f64(const ie_matvec* m, const double* d_X, int64_t ldx, int32_t nr
 /* Band (slab) passes of the FFT method for the sharded solver (2D, SURVEY.md
  * 8(e)); together they are ToeplitzMatvec.matvec (toeplitz.py:39-50) split
  * across ranks with two all-to-all transposes in between.  Rank g owns grid
- * rows [row_begin, row_end) (whole rows, point indices); the 2n spectrum
- * columns are cut into `parts` slabs of Mc = 2n / parts (a power of two).
+ * rows [row_begin, row_end) (whole rows, point indices); the M spectrum
+ * columns (M = the circulant size) are cut into `parts` slabs of
+ * Mc = M / parts (a power of two).
  *   band_fwd: X (nrhs columns, ldx, band rows only) -> d_out, complex
- *             (nrows * 2n), destination-major: slab h at h * nrows * Mc;
+ *             (nrows * M), destination-major: slab h at h * nrows * Mc;
  *   band_cols: d_buf = every grid row of columns [col_begin, col_end),
  *             row-major (n x ncols complex), in place: forward * symbol * inverse;
  *   band_inv: d_in (destination-major as band_fwd wrote it, after the reverse
  *             transpose) -> Y (band rows, ldy, nrhs columns).
  * With nrhs == 2 the exact power-of-two column scaling of the 2-RHS packing
- * uses d_amax = the GLOBAL per-2048-chunk partial maxima (2 * namax doubles,
- * namax = ceil(N / 2048), [2c] = max|x0|, [2c+1] = max|x1|), so every rank
- * scales identically and the result is bitwise that of ie_matvec_f64. */
+ * uses d_scales = the two multipliers (device, 2 doubles: 2^-e0, 2^-e1) the
+ * caller derived from GLOBAL quantities (pcg_scale_rule in distributed.py),
+ * so every rank scales identically and the line arithmetic is bitwise that
+ * of the single-GPU pass. */
 int ie_matvec_band_fwd_f64(const ie_matvec* m, const double* d_X, int64_t ldx, int32_t nrhs,
                            int64_t row_begin, int64_t row_end, int32_t parts, void* d_out,
-                           const double* d_amax, int64_t namax, void* stream);
+                           const double* d_scales, void* stream);
 int ie_matvec_band_cols_f64(const ie_matvec* m, void* d_buf, int64_t col_begin, int64_t col_end,
                             void* stream);
 int ie_matvec_band_inv_f64(const ie_matvec* m, const void* d_in, int64_t row_begin, int64_t row_end,
-                           int32_t parts, double* d_Y, int64_t ldy, int32_t nrhs, const double* d_amax,
-                           int64_t namax, void* stream);
-/* Per-2048-chunk partial maxima of |x0| and |x1| (x1 = x0 + ldx) over n
- * entries starting at a chunk boundary: d_out[2c], d_out[2c + 1]. */
+                           int32_t parts, double* d_Y, int64_t ldy, int32_t nrhs, const double* d_scales,
+                           void* stream);
+/* Per-2048-chunk partial maxima of |x0| and |x1| (x1 = x0 + ldx; ldx = 0:
+ * x1 = x0) over n entries starting at a chunk boundary: d_out[2c], d_out[2c + 1]. */
 int ie_absmax_partials_f64(const double* d_X, int64_t ldx, int64_t n, double* d_out, void* stream);
 
 /* Replaces KernelOperator.assemble_block (kernel.py:170-184):
@@ -142,6 +146,12 @@ int ie_precond_apply_f64(const ie_precond* p, const double* d_r, double* d_z, vo
  * out[4] = D. */
 int ie_precond_stats(const ie_precond* p, int64_t* out5);
 
+/* Factor-level readback (test hook for linalg.cholesky, linalg.py:36-45):
+ * subdomain k's stored block as an s x s row-major HOST matrix.  *kind = 1:
+ * the Cholesky factor G, A_k = G^T G (variant SUBST, s <= 160); *kind = 0:
+ * A_k^{-1}.  h_out = NULL returns *s_out only. */
+int ie_precond_block_f64(const ie_precond* p, int64_t k, double* h_out, int64_t* s_out, int32_t* kind);
+
 /* ---------------------------------------------------------- K4 / K5 ---- */
 /* Replaces pcg.solve (pcg.py:54-136) for a native operator and
  * preconditioner (precond may be NULL = identity, pcg.py:68).  f, u are
@@ -156,34 +166,55 @@ int ie_pcg_f64(const ie_matvec* A, const ie_precond* T, const double* d_f, doubl
                int32_t* h_flags, double* h_times, int64_t* fail_iter, double* fail_value,
                void* stream);
 
-/* ------------------------------------------------ sharded K4 (NCCL) ---- */
-typedef struct ie_comm ie_comm;
+/* ie_pcg_f64 instrumented for the bench's per-kernel rooflines: iterations
+ * launched one by one (no graph) with CUDA events between the kernel groups;
+ * h_phase_ms[0..4] = mean device ms per steady-state (2-RHS) iteration of
+ * the matvec, k_post_pass, k_iter_a, the preconditioner apply, k_iter_b. */
+int ie_pcg_profile_f64(const ie_matvec* A, const ie_precond* T, const double* d_f, double* d_u,
+                       double tol, int64_t max_iters, double* h_history, int64_t* n_it,
+                       int32_t* h_flags, double* h_times, double* h_phase_ms, void* stream);
 
-/* NCCL communicator of the rank group (one process per GPU): rank 0 makes the
- * id (ie_comm_id_bytes() bytes), the host broadcasts it (torch.distributed in
- * distributed.py), every rank calls ie_comm_create. */
-int64_t ie_comm_id_bytes(void);
-int ie_comm_unique_id(void* out);
-int ie_comm_create(const void* id, int32_t nranks, int32_t rank, ie_comm** out);
-void ie_comm_destroy(ie_comm* c);
-
-/* Replaces pcg.solve (pcg.py:54-136) on G ranks: rank g owns points
- * [h_bounds[g], h_bounds[g+1]) of every vector (equal, chunk-aligned bands of
- * whole grid rows; 2D FFT operator with G | 2n).  T_local is the rank's
- * preconditioner (the subdomains intersecting its band, ascending global ids,
- * NULL = identity); h_need[2h], h_need[2h+1] bound the points rank h's blocks
- * read (the r-halo).  Per iteration: band FFT with two all-to-alls, r-halo
- * send/recv, all-gathered fixed-chunk dot partials; device-side control and a
- * captured iteration graph as ie_pcg_f64, whose result it reproduces bitwise
- * for any G.  h_times[1] (mean apply time) is not measured (0). */
-int ie_pcg_sharded_f64(const ie_matvec* A, const ie_precond* T_local, ie_comm* comm,
-                       const int64_t* h_bounds, const int64_t* h_need, const double* d_f_band,
-                       double* d_u_band, double tol, int64_t max_iters, double* h_history,
-                       int64_t* n_it, int32_t* h_flags, double* h_times, int64_t* fail_iter,
+/* ------------------------------------------ sharded K4 (NVLink P2P) ---- */
+/* Replaces pcg.solve (pcg.py:54-136) on G ranks, one per GPU (SURVEY.md
+ * 8(e); the reference itself is single-process).  Rank g owns points
+ * [h_bounds[g], h_bounds[g+1]) of every vector: equal, 2048-aligned bands of
+ * whole grid rows; the 2D FFT operator with G | M (its circulant size) and
+ * M/G a power of two.
+ * T_local = the rank's preconditioner (subdomains intersecting its band,
+ * ascending global ids; NULL = identity); h_need[2h], h_need[2h+1] bound the
+ * points rank h's subdomains read (its r-halo; NULL without T).
+ * Exchanges are direct stores into the peers' memory over NVLink plus a
+ * mailbox counter per exchange (no collective library): four exchange points
+ * per iteration (row->column transpose, column->need-rows transpose carrying
+ * the r-halo, p.q/residual partials, the apply's r.z record).  n_it, history
+ * and u are bitwise those of ie_pcg_f64 for every G.
+ *   multi-process: ie_shard_create on every rank, ie_shard_export -> host
+ *     all-gather of the ie_shard_handle_bytes() blobs (rank order) ->
+ *     ie_shard_connect -> ie_pcg_sharded_f64 (collective: every rank calls it);
+ *   one process, one device (tests): ie_shard_create for ranks 0..G-1,
+ *     ie_shard_connect_local, ie_pcg_sharded_local_f64.
+ * d_f_need = f on the rank's need rows [out2[0], out2[1]) of
+ * ie_shard_need_rows; d_u_band = the band of u (out).  h_times[1] = mean
+ * device time of rank 0's event-timed applies. */
+typedef struct ie_shard ie_shard;
+int ie_shard_create(const ie_matvec* A, const ie_precond* T_local, int32_t nranks, int32_t rank,
+                    const int64_t* h_bounds, const int64_t* h_need, ie_shard** out);
+void ie_shard_destroy(ie_shard* s);
+int ie_shard_need_rows(const ie_shard* s, int64_t* out2);
+int64_t ie_shard_handle_bytes(void);
+int ie_shard_export(const ie_shard* s, void* h_out);
+int ie_shard_connect(ie_shard* s, const void* h_handles);
+int ie_shard_connect_local(ie_shard** shards, int32_t nranks);
+int ie_pcg_sharded_f64(ie_shard* s, const double* d_f_need, double* d_u_band, double tol, int64_t max_iters,
+                       double* h_history, int64_t* n_it, int32_t* h_flags, double* h_times, int64_t* fail_iter,
                        double* fail_value, void* stream);
-
+int ie_pcg_sharded_local_f64(ie_shard** shards, int32_t nranks, const double* const* d_f_need,
+                             double* const* d_u_band, double tol, int64_t max_iters, double* h_history,
+                             int64_t* n_it, int32_t* h_flags, double* h_times, int64_t* fail_iter,
+                             double* fail_value, void* stream);
 
 /* Replaces spectrum.extremal_eigenvalue_lanczos (spectrum.py:133-190):
+ * T = NULL is the identity preconditioner (precond.identity);
  * d_v0 = start vector (caller draws it from default_rng(seed), spectrum.py:148),
  * which = 0 (min) / 1 (max).  *steps = Lanczos steps taken. */
 int ie_lanczos_f64(const ie_matvec* A, const ie_precond* T, const double* d_v0,
@@ -206,6 +237,9 @@ int ie_update_f64(int32_t op, double* d_a, const double* d_b, double s, int64_t 
 /* FP64 issue-peak microbenchmark: DFMA instructions (lane ops) per second
  * over all SMs -- the roofline denominator for K1. */
 int ie_fp64_peak(double* dfma_per_s, void* stream);
+/* FP64 tensor-core (DMMA m8n8k4) throughput microbenchmark, flops/s over all
+ * SMs -- the roofline denominator for the class-GEMM apply. */
+int ie_dmma_peak(double* flops_per_s, void* stream);
 
 /* Last error text for IE_ERR_CUDA / IE_ERR_ARG (thread-local). */
 const char* ie_last_error(void);

@@ -11,7 +11,7 @@ Pinning: tests/test_oracle.py checks this restatement against
   * the reference's own known-answer constants (tests/test_kernel.py:16-18,
     :91-99 of the reference),
   * the reference's golden suites (goldens.json iterations-2d/3d, spectrum-2d/3d,
-    schwarz-scaling-2d, pairing) copied to tests/golden/ref_goldens.json, and
+    schwarz-scaling-2d, pairing) shipped as paper_2108_12574_b200/data/goldens.json, and
   * golden vectors produced by running the unmodified reference in the build
     container (tools/gen_goldens.py -> tests/golden/ref_*.npz).
 

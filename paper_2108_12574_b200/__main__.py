@@ -16,7 +16,7 @@ def main(argv=None) -> int:
     sub = parser.add_subparsers(dest="subcommand", required=True)
     g = sub.add_parser("golden")
     g.add_argument("suites", nargs="*", help="suite names, or 'all'")
-    g.add_argument("--goldens", default=None, help="goldens.json path (default: tests/golden/ref_goldens.json)")
+    g.add_argument("--goldens", default=None, help="goldens.json path (default: the packaged data/goldens.json)")
     try:
         args = parser.parse_args(argv)
     except SystemExit as exc:

@@ -43,26 +43,34 @@ _SIGS = {
     "ie_matvec_create_method": (_I32, [ctypes.POINTER(IeGeom), _I32, ctypes.POINTER(_P)]),
     "ie_matvec_destroy": (None, [_P]),
     "ie_matvec_f64": (_I32, [_P, _P, _I64, _I32, _P, _I64, _I64, _I64, _P]),
-    "ie_matvec_band_fwd_f64": (_I32, [_P, _P, _I64, _I32, _I64, _I64, _I32, _P, _P, _I64, _P]),
+    "ie_matvec_band_fwd_f64": (_I32, [_P, _P, _I64, _I32, _I64, _I64, _I32, _P, _P, _P]),
     "ie_matvec_band_cols_f64": (_I32, [_P, _P, _I64, _I64, _P]),
-    "ie_matvec_band_inv_f64": (_I32, [_P, _P, _I64, _I64, _I32, _P, _I64, _I32, _P, _I64, _P]),
+    "ie_matvec_band_inv_f64": (_I32, [_P, _P, _I64, _I64, _I32, _P, _I64, _I32, _P, _P]),
     "ie_absmax_partials_f64": (_I32, [_P, _I64, _I64, _P, _P]),
-    "ie_comm_id_bytes": (_I64, []),
-    "ie_comm_unique_id": (_I32, [_P]),
-    "ie_comm_create": (_I32, [_P, _I32, _I32, ctypes.POINTER(_P)]),
-    "ie_comm_destroy": (None, [_P]),
-    "ie_pcg_sharded_f64": (_I32, [_P, _P, _P, _P, _P, _P, _P, _D, _I64, _P, ctypes.POINTER(_I64), _P, _P,
+    "ie_shard_create": (_I32, [_P, _P, _I32, _I32, _P, _P, ctypes.POINTER(_P)]),
+    "ie_shard_destroy": (None, [_P]),
+    "ie_shard_need_rows": (_I32, [_P, _P]),
+    "ie_shard_handle_bytes": (_I64, []),
+    "ie_shard_export": (_I32, [_P, _P]),
+    "ie_shard_connect": (_I32, [_P, _P]),
+    "ie_shard_connect_local": (_I32, [_P, _I32]),
+    "ie_pcg_sharded_f64": (_I32, [_P, _P, _P, _D, _I64, _P, ctypes.POINTER(_I64), _P, _P,
                                   ctypes.POINTER(_I64), ctypes.POINTER(_D), _P]),
+    "ie_pcg_sharded_local_f64": (_I32, [_P, _I32, _P, _P, _D, _I64, _P, ctypes.POINTER(_I64), _P, _P,
+                                        ctypes.POINTER(_I64), ctypes.POINTER(_D), _P]),
     "ie_assemble_block_f64": (_I32, [ctypes.POINTER(IeGeom), _P, _I64, _P, _I64, _P, _P]),
     "ie_precond_create": (_I32, [ctypes.POINTER(IeGeom), _P, _P, _I64, _I32, _I32, ctypes.POINTER(_P),
                                  ctypes.POINTER(_I64), _P]),
     "ie_precond_destroy": (None, [_P]),
     "ie_precond_apply_f64": (_I32, [_P, _P, _P, _P]),
     "ie_precond_stats": (_I32, [_P, _P]),
+    "ie_precond_block_f64": (_I32, [_P, _I64, _P, ctypes.POINTER(_I64), ctypes.POINTER(_I32)]),
     "ie_pcg_f64": (_I32, [_P, _P, _P, _P, _D, _I64, _P, ctypes.POINTER(_I64), _P, _P,
                           ctypes.POINTER(_I64), ctypes.POINTER(_D), _P]),
+    "ie_pcg_profile_f64": (_I32, [_P, _P, _P, _P, _D, _I64, _P, ctypes.POINTER(_I64), _P, _P, _P, _P]),
     "ie_lanczos_f64": (_I32, [_P, _P, _P, _I32, _I64, _D, ctypes.POINTER(_D), ctypes.POINTER(_I64), _P]),
     "ie_fp64_peak": (_I32, [ctypes.POINTER(_D), _P]),
+    "ie_dmma_peak": (_I32, [ctypes.POINTER(_D), _P]),
     "ie_dot_chunk": (_I64, []),
     "ie_dot_partials_f64": (_I32, [_P, _P, _I64, _I32, _P, _P]),
     "ie_sum_partials_f64": (_I32, [_P, _I64, _P, _P]),

@@ -2,8 +2,9 @@
 
 nvcc cross-compiles here without a GPU; the .so is git-ignored but travels to
 the GPU box with the gpurun snapshot.  Each .cu is compiled to its own object
-(parallel), then linked against the shared CUDA runtime and NCCL (the
-sharded PCG driver's collectives)."""
+(parallel), then linked against the shared CUDA runtime.  The multi-GPU
+driver needs no collective library: its exchanges are peer stores over
+NVLink (CUDA IPC)."""
 
 from __future__ import annotations
 
@@ -21,21 +22,6 @@ SOURCES = ["capi.cu", "matvec.cu", "fft.cu", "precond.cu", "krylov.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC,-O3", "--expt-relaxed-constexpr",
          "-Xptxas", "-v"] + os.environ.get("IEDD_B200_NVCC_EXTRA", "").split()
-
-
-def _nccl():
-    """(include dir, lib dir) of the NCCL that torch loads (the wheel under
-    site-packages/nvidia/nccl), else the system one.  The library is linked by
-    soname with an rpath, so the process shares torch's NCCL."""
-    try:
-        import nvidia.nccl as nc  # noqa: F401
-        base = os.path.dirname(nc.__file__) if getattr(nc, "__file__", None) else list(nc.__path__)[0]
-        inc, lib = os.path.join(base, "include"), os.path.join(base, "lib")
-        if os.path.exists(os.path.join(inc, "nccl.h")) and os.path.exists(os.path.join(lib, "libnccl.so.2")):
-            return inc, lib
-    except ImportError:
-        pass
-    return "/usr/include", "/usr/lib/x86_64-linux-gnu"
 
 
 def _nvcc():
@@ -61,7 +47,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
         src = os.path.join(CSRC, s)
         obj = os.path.join(BUILD, s.replace(".cu", ".o"))
         if force or _needs(obj, src):
-            jobs.append([nvcc, *ARCH, *FLAGS, "-I", _nccl()[0], "-c", src, "-o", obj])
+            jobs.append([nvcc, *ARCH, *FLAGS, "-c", src, "-o", obj])
     logs = []
 
     def run(cmd):
@@ -75,9 +61,7 @@ def build(verbose: bool = False, force: bool = False) -> str:
             logs.append(out)
     objs = [os.path.join(BUILD, s.replace(".cu", ".o")) for s in SOURCES]
     if jobs or not os.path.exists(LIB):
-        nlib = _nccl()[1]
-        cmd = [nvcc, *ARCH, "-shared", "-cudart", "shared", *objs, "-L", nlib, "-l:libnccl.so.2",
-               "-Xlinker", f"-rpath,{nlib}", "-o", LIB]
+        cmd = [nvcc, *ARCH, "-shared", "-cudart", "shared", *objs, "-o", LIB]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"link failed: {' '.join(cmd)}\n{r.stdout}\n{r.stderr}")

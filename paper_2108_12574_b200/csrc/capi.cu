@@ -60,3 +60,48 @@ extern "C" int ie_fp64_peak(double* dfma_per_s, void* stream) {
     cudaFree(d);
     return IE_OK;
 }
+
+// FP64 tensor-core (DMMA, mma.sync m8n8k4 f64) throughput microbenchmark: the
+// roofline denominator of the class-GEMM apply (k_apply_dmma).  8 independent
+// accumulator chains per warp, 8 warps per CTA, 2 CTAs per SM.
+namespace ie {
+__global__ void __launch_bounds__(256) k_dmma_peak(double* out, int iters, double a, double b) {
+    double c[8][2];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) c[q][0] = c[q][1] = threadIdx.x * 1e-3 + q;
+    for (int i = 0; i < iters; ++i) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q)
+            asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};\n"
+                         : "+d"(c[q][0]), "+d"(c[q][1])
+                         : "d"(a), "d"(b));
+    }
+    double s = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) s += c[q][0] + c[q][1];
+    if (s == 1234.5678) out[0] = s;
+}
+}  // namespace ie
+
+extern "C" int ie_dmma_peak(double* flops_per_s, void* stream) {
+    cudaStream_t st = (cudaStream_t)stream;
+    double* d;
+    IE_CUDA(cudaMalloc(&d, 8));
+    cudaEvent_t e0, e1;
+    IE_CUDA(cudaEventCreate(&e0));
+    IE_CUDA(cudaEventCreate(&e1));
+    const int blocks = ie::kNumSMs * 2, threads = 256, iters = 4096;
+    for (int rep = 0; rep < 2; ++rep) ie::k_dmma_peak<<<blocks, threads, 0, st>>>(d, iters, 1.0, 1e-9);
+    IE_CUDA(cudaEventRecord(e0, st));
+    ie::k_dmma_peak<<<blocks, threads, 0, st>>>(d, iters, 1.0, 1e-9);
+    IE_CUDA(cudaEventRecord(e1, st));
+    IE_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    IE_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    // per mma: 8 x 8 x 4 multiply-adds = 512 flops per warp
+    *flops_per_s = (double)blocks * (threads / 32) * iters * 8 * 512.0 / (ms * 1e-3);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(d);
+    return IE_OK;
+}

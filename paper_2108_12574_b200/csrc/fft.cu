@@ -37,12 +37,13 @@
 
 namespace ie {
 
-constexpr int kFftPoints = 4096;
+constexpr int kFftPoints = 4096;     // points per CTA of the radix-16 k_fft_lines (lines M < 64)
+constexpr int kFftMaxPoints = 8192;  // longest line (k_fft8: 8 points x 1024 threads)
 
 struct LineArgs {
     int nlines;   // lines in this pass
-    int ninner;   // line g -> o = g / ninner, i = g % ninner (a power of two)
-    int lg_ninner;
+    int ninner;   // line g -> o = g / ninner, i = g % ninner
+    int lg_ninner;  // log2(ninner), or -1 when ninner is not a power of two (3D, non-power-of-two n)
     int L;
     int logL;
     // source
@@ -76,6 +77,10 @@ struct LineArgs {
     // differ by up to ~1e10 in norm).  amax = per-chunk partial max|x_c|.
     const double* amax;
     int namax;
+    // or the two multipliers themselves, precomputed by the PCG driver
+    // (k_iter_b: one device-side decision instead of a partial-max
+    // reduction in every CTA); takes precedence over amax
+    const double* scales;
     int scale_in;
     int scale_out;
     const int* stop;  // device flag: nonzero -> no-op (PCG early exit)
@@ -103,6 +108,11 @@ __device__ __forceinline__ double pow2_scale(double mx) {
 
 template <int TPB>
 __device__ void column_scales(const LineArgs& a, double* sc) {
+    if (a.scales) {
+        if (threadIdx.x < 2) sc[threadIdx.x] = a.scales[threadIdx.x];
+        __syncthreads();
+        return;
+    }
     __shared__ double red[2][TPB];
     double m0 = 0.0, m1 = 0.0;
     for (int c = threadIdx.x; c < a.namax; c += blockDim.x) {
@@ -430,7 +440,8 @@ __global__ void __launch_bounds__(TPB, 2) k_fft_lines(LineArgs a) {
         const int line = g0 + g;
         v[q] = make_double2(0.0, 0.0);
         if (line < a.nlines && l < a.n_in) {
-            const int o = line >> lgi, i = line & ((1 << lgi) - 1);
+            const int o = lgi >= 0 ? line >> lgi : line / a.ninner;
+            const int i = lgi >= 0 ? line & ((1 << lgi) - 1) : line - o * a.ninner;
             const int64_t off = (int64_t)o * a.in_so + (int64_t)i * a.in_si +
                                 (a.in_lsplit < 0 ? (int64_t)l * a.in_sl
                                                  : (int64_t)(l >> a.in_lsplit) * a.in_sh +
@@ -473,7 +484,7 @@ __global__ void __launch_bounds__(TPB, 2) k_fft_lines(LineArgs a) {
         // multiply by the folded real symbol; line (inner index i) enumerates axes 1..dim-1.
         // A thread's 16 points lie on at most 16 lines: per-point line offsets first,
         // then all 16 symbol loads in flight, then the multiplies.
-        const int np1 = a.n + 1;
+        const int np1 = L / 2 + 1;  // folded symbol extent per axis
         double lam[16];
 #pragma unroll
         for (int q = 0; q < 16; ++q) {
@@ -517,7 +528,8 @@ __global__ void __launch_bounds__(TPB, 2) k_fft_lines(LineArgs a) {
         }
         const int line = g0 + g;
         if (line >= a.nlines || l >= a.n_out) continue;
-        const int o = line >> lgi, i = line & ((1 << lgi) - 1);
+        const int o = lgi >= 0 ? line >> lgi : line / a.ninner;
+        const int i = lgi >= 0 ? line & ((1 << lgi) - 1) : line - o * a.ninner;
         const int64_t off = (int64_t)o * a.out_so + (int64_t)i * a.out_si +
                             (a.out_lsplit < 0 ? (int64_t)l * a.out_sl
                                               : (int64_t)(l >> a.out_lsplit) * a.out_sh +
@@ -652,6 +664,7 @@ __device__ __forceinline__ void fft8_line(double* vr, double* vi, int j, double*
     if constexpr (P >= 2) pass8<S, LOGL, 2, PADS>(vr, vi, j, re, im, tw8);
     if constexpr (P >= 3) pass8<S, LOGL, 3, PADS>(vr, vi, j, re, im, tw8);
     if constexpr (P >= 4) pass8<S, LOGL, 4, PADS>(vr, vi, j, re, im, tw8);
+    if constexpr (P >= 5) pass8<S, LOGL, 5, PADS>(vr, vi, j, re, im, tw8);  // L = 8192
 }
 
 // 2048-point line with 16 points per thread (128 threads per line): radix 16,
@@ -757,6 +770,10 @@ __device__ __forceinline__ int64_t line_off(int64_t so, int64_t si, int64_t sl, 
 }
 
 __device__ void column_scales_dyn(const LineArgs& a, double* sc) {
+    if (a.scales) {
+        if (threadIdx.x < 2) sc[threadIdx.x] = a.scales[threadIdx.x];
+        return;
+    }
     __shared__ double red[2][32];
     double m0 = 0.0, m1 = 0.0;
     for (int c = threadIdx.x; c < a.namax; c += blockDim.x) {
@@ -835,7 +852,8 @@ __global__ void __launch_bounds__(PTS == 16 ? 256 : 1024, PTS == 16 ? 2 : 1) k_f
     const int line = blockIdx.x * G + g;
     const bool live = line < a.nlines;
     const int lgi = a.lg_ninner;
-    const int o = line >> lgi, i = line & ((1 << lgi) - 1);
+    const int o = lgi >= 0 ? line >> lgi : line / a.ninner;
+    const int i = lgi >= 0 ? line & ((1 << lgi) - 1) : line - o * a.ninner;
     double vr[PTS], vi[PTS];
     constexpr bool tma_mode = TMA && MODE == kFusedCC && STRIDED;
     if constexpr (tma_mode) {
@@ -907,7 +925,7 @@ __global__ void __launch_bounds__(PTS == 16 ? 256 : 1024, PTS == 16 ? 2 : 1) k_f
     if constexpr (fused) {
         fft_line<-1, LOGL, PADS, PTS>(vr, vi, j, re, im, a, zero_hi);
         // folded real symbol at frequency l = j + TPL m along this line
-        const int np1 = a.n + 1;
+        constexpr int np1 = L / 2 + 1;
         int tmp = i + a.line0, off = 0, stride = 1;
         for (int d = a.dim - 1; d >= 1; --d) {
             const int k = tmp & (L - 1);
@@ -973,11 +991,12 @@ __global__ void __launch_bounds__(PTS == 16 ? 256 : 1024, PTS == 16 ? 2 : 1) k_f
     }
 }
 
-// Embedding of the generator, mirror-even per axis, index n left zero
-// (toeplitz.py:19-30): emb[k] = gen[fold(k)] with fold(k) = k (k<n),
-// 2n-k (k>n); entries from the same integer-distance formula as K1/K2.
-__global__ void k_embed(double2* emb, int dim, int n, EntryParams P, const LogEntry* tab) {
-    const int M = 2 * n;
+// Embedding of the generator in a circulant of size M >= 2n - 1 per axis,
+// mirror-even (toeplitz.py:19-30 uses M = 2n with index n left zero):
+// emb[k] = gen[k] (k < n), gen[M - k] (k > M - n), 0 between; entries from the
+// same integer-distance formula as K1/K2.  Any M >= 2n - 1 gives the same
+// Toeplitz product; a power of two keeps every line transform radix-2^k.
+__global__ void k_embed(double2* emb, int dim, int n, int M, EntryParams P, const LogEntry* tab) {
     int64_t tot = 1;
     for (int d = 0; d < dim; ++d) tot *= M;
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -988,18 +1007,18 @@ __global__ void k_embed(double2* emb, int dim, int n, EntryParams P, const LogEn
     for (int d = 0; d < dim; ++d) {
         const int k = (int)(t % M);
         t /= M;
-        if (k == n) zero = true;
+        if (k >= n && k <= M - n) zero = true;
         const int g = k < n ? k : M - k;
         m += g * g;
     }
     emb[e] = make_double2(zero ? 0.0 : entry_from_m(P, tab, m), 0.0);
 }
 
-// sym[k_0 + (n+1) * rest(k_1..k_{d-1})] = Re(emb_hat[k]) / M^dim, k folded (<= n);
-// axis 0 (the fused column pass's line axis) fastest so a line reads its symbol
-// contiguously; rest = C order over axes 1..d-1 (last fastest)
-__global__ void k_fold_symbol(const double2* emb, double* sym, int dim, int n, double scale) {
-    const int np1 = n + 1, M = 2 * n;
+// sym[k_0 + (M/2+1) * rest(k_1..k_{d-1})] = Re(emb_hat[k]) / M^dim, k folded
+// (<= M/2); axis 0 (the fused column pass's line axis) fastest so a line reads
+// its symbol contiguously; rest = C order over axes 1..d-1 (last fastest)
+__global__ void k_fold_symbol(const double2* emb, double* sym, int dim, int M, double scale) {
+    const int np1 = M / 2 + 1;
     int64_t tot = 1;
     for (int d = 0; d < dim; ++d) tot *= np1;
     const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -1104,7 +1123,8 @@ static int launch_fft8_m(const LineArgs& a, int tpb, int ctas, size_t smem, cuda
         case 9: return launch_fft8_l<MODE, 9>(a, tpb, ctas, smem, st);
         case 10: return launch_fft8_l<MODE, 10>(a, tpb, ctas, smem, st);
         case 11: return launch_fft8_l<MODE, 11>(a, tpb, ctas, smem, st);
-        default: return launch_fft8_l<MODE, 12>(a, tpb, ctas, smem, st);
+        case 12: return launch_fft8_l<MODE, 12>(a, tpb, ctas, smem, st);
+        default: return launch_fft8_l<MODE, 13>(a, tpb, ctas, smem, st);
     }
 }
 
@@ -1152,13 +1172,16 @@ static int line_launch(const LineArgs& a_in, cudaStream_t st) {
     a.lg_ninner = 0;
     while ((1 << a.lg_ninner) < a.ninner) ++a.lg_ninner;
     if ((1 << a.lg_ninner) != a.ninner) {
-        set_error("fft: line layout must be a power of two");
-        return IE_ERR_ARG;
+        if (a.fused) {  // the fused pass decomposes its line index into symbol axes by powers of two
+            set_error("fft: fused line layout must be a power of two");
+            return IE_ERR_ARG;
+        }
+        a.lg_ninner = -1;
     }
     {
         static const bool v1 = getenv("IEDD_B200_FFT_V1") != nullptr;
         const bool cin = a.in_real || a.in_sl == 1, cout = a.out_real || a.out_sl == 1;
-        if (!v1 && a.tw8 && a.logL >= 6 && a.logL <= 12 && cin == cout) return launch_fft8(a, st);
+        if (!v1 && a.tw8 && a.logL >= 6 && a.logL <= 13 && cin == cout) return launch_fft8(a, st);
     }
     // 256-thread CTAs (4096 points) unless that leaves the GPU under-filled and
     // the lines fit a 32-thread CTA (512 points)
@@ -1211,12 +1234,20 @@ static int fft_full_forward(const ie_fft* f, double2* buf, cudaStream_t st) {
 int make_log_table_device(const ie_geom& g, LogEntry** d_tab, int* ntab);
 EntryParams entry_params(const ie_geom& g);
 
+// Circulant size per axis: the smallest power of two >= 2n - 1 (>= 4); equal
+// to the reference's 2n for power-of-two n (bitwise the same plan as before)
+int fft_size_for(int n) {
+    int M = 4;
+    while (M < 2 * n - 1) M *= 2;
+    return M;
+}
+
 int fft_create(const ie_geom& g, ie_fft** out) {
     int n = g.n, logM = 0;
-    const int M = 2 * n;
+    const int M = fft_size_for(n);
     while ((1 << logM) < M) ++logM;
-    if ((1 << logM) != M || M > kFftPoints || M < 4) {
-        set_error("fft matvec needs n a power of two with 2 <= n <= 2048");
+    if (n < 1 || M > kFftMaxPoints) {
+        set_error("fft matvec needs 1 <= n <= 4096 (circulant size <= 8192 per axis)");
         return IE_ERR_ARG;
     }
     ie_fft* f = new ie_fft();
@@ -1235,7 +1266,7 @@ int fft_create(const ie_geom& g, ie_fft** out) {
     int64_t totM = 1, totS = 1, totB = 1;
     for (int d = 0; d < g.dim; ++d) {
         totM *= M;
-        totS *= (n + 1);
+        totS *= (M / 2 + 1);
         totB *= (d == 0 ? n : M);
     }
     IE_CUDA(cudaMalloc(&f->d_tw, M * sizeof(double2)));
@@ -1271,10 +1302,10 @@ int fft_create(const ie_geom& g, ie_fft** out) {
     int ntab;
     int rc = make_log_table_device(g, &tab, &ntab);
     if (rc) return rc;
-    k_embed<<<(unsigned)((totM + 255) / 256), 256>>>(emb, g.dim, n, entry_params(g), tab);
+    k_embed<<<(unsigned)((totM + 255) / 256), 256>>>(emb, g.dim, n, M, entry_params(g), tab);
     IE_LAUNCHED();
     if ((rc = fft_full_forward(f, emb, 0))) return rc;
-    k_fold_symbol<<<(unsigned)((totS + 255) / 256), 256>>>(emb, f->d_sym, g.dim, n, 1.0 / (double)totM);
+    k_fold_symbol<<<(unsigned)((totS + 255) / 256), 256>>>(emb, f->d_sym, g.dim, M, 1.0 / (double)totM);
     IE_LAUNCHED();
     IE_CUDA(cudaDeviceSynchronize());
     cudaFree(emb);
@@ -1314,8 +1345,10 @@ static int band_check(const ie_fft* f, int parts) {
     return IE_OK;
 }
 
+int fft_M(const ie_fft* f) { return f->M; }
+
 int fft_band_fwd(const ie_fft* f, const double* X0, const double* X1, int nrows, int parts, double2* out,
-                 const double* amax, int namax, cudaStream_t st) {
+                 const double* scales, cudaStream_t st, const int* stop) {
     int rc = band_check(f, parts);
     if (rc) return rc;
     const int n = f->n, Mc = f->M / parts;
@@ -1336,15 +1369,15 @@ int fft_band_fwd(const ie_fft* f, const double* X0, const double* X1, int nrows,
     a.out_lsplit = lg;
     a.out_sh = (int64_t)nrows * Mc;
     a.n_out = f->M;
+    a.stop = stop;
     if (X1) {
-        a.amax = amax;
-        a.namax = namax;
+        a.scales = scales;
         a.scale_in = 1;
     }
     return line_launch(a, st);
 }
 
-int fft_band_cols(const ie_fft* f, double2* buf, int c0, int ncols, cudaStream_t st) {
+int fft_band_cols(const ie_fft* f, double2* buf, int c0, int ncols, cudaStream_t st, const int* stop) {
     int rc = band_check(f, 1);
     if (rc) return rc;
     if (ncols <= 0 || (ncols & (ncols - 1)) || c0 < 0 || c0 + ncols > f->M) {
@@ -1362,11 +1395,12 @@ int fft_band_cols(const ie_fft* f, double2* buf, int c0, int ncols, cudaStream_t
     c.n_in = f->n;
     c.n_out = f->n;
     c.fused = 1;
+    c.stop = stop;
     return line_launch(c, st);
 }
 
 int fft_band_inv(const ie_fft* f, const double2* in, int nrows, int parts, double* Y0, double* Y1,
-                 const double* amax, int namax, cudaStream_t st) {
+                 const double* scales, cudaStream_t st, const int* stop) {
     int rc = band_check(f, parts);
     if (rc) return rc;
     const int n = f->n, Mc = f->M / parts;
@@ -1388,9 +1422,9 @@ int fft_band_inv(const ie_fft* f, const double2* in, int nrows, int parts, doubl
     e.out_sl = 1;
     e.n_out = n;
     e.sign = +1;
+    e.stop = stop;
     if (Y1) {
-        e.amax = amax;
-        e.namax = namax;
+        e.scales = scales;
         e.scale_out = 1;
     }
     return line_launch(e, st);
@@ -1452,20 +1486,22 @@ static bool tma_map(ie_fft* f, const double2* B, int G, CUtensorMap* out) {
 }
 
 // buf_ws / amax_ws: the calling stream's work buffer and chunk-maxima scratch
-// (nullptr: the plan's own)
+// (nullptr: the plan's own).  scales_ext: the 2-RHS column multipliers
+// precomputed on the device (PCG); without them the pass reduces max|x_c|.
 int fft_matvec(const ie_fft* f, const double* X0, const double* X1, double* Y0, double* Y1, cudaStream_t st,
-               const int* stop, const double* amax_ext, double2* buf_ws, double* amax_ws) {
+               const int* stop, const double* scales_ext, double2* buf_ws, double* amax_ws) {
     const int n = f->n, M = f->M, d = f->dim;
     int rc;
     const int two = X1 != nullptr;
     double* amax_own = amax_ws ? amax_ws : f->d_amax;
-    if (two && !amax_ext) {
+    if (two && !scales_ext) {
         k_absmax2<<<(f->N + 2047) / 2048, 256, 0, st>>>(X0, X1, f->N, amax_own, stop);
         IE_LAUNCHED();
     }
     auto line_launch = [&](LineArgs a, cudaStream_t s) -> int {
         a.stop = stop;
-        a.amax = amax_ext ? amax_ext : amax_own;
+        a.amax = amax_own;
+        a.scales = scales_ext;
         if (two) {
             a.scale_in = a.in_real;
             a.scale_out = a.out_real;

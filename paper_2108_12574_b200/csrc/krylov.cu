@@ -24,11 +24,10 @@
 
 #include <algorithm>
 #include <chrono>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <vector>
-
-#include <nccl.h>
 
 #include "common.cuh"
 #include "pcg_state.cuh"
@@ -80,8 +79,9 @@ __global__ void k_set_it(PcgState* s, long long it) { s->it_dev = it; }
 
 __global__ void k_pcg_init(const double* part, int nch, PcgState* s, double tol, long long max_iters,
                            double* hist) {
-    // (rho_0 is set by k_pcg_rho0 after the first apply)
+    // (rho_0 is set by k_pcg_setup after the first apply)
     __shared__ double sh[kRed];
+    if (s->status == 6) return;  // a sharded exchange timed out before the init (k_wait): keep the failure
     const double v = reduce_partials(part, nch, sh);
     if (threadIdx.x == 0) {
         s->nf = sqrt(v);
@@ -105,6 +105,24 @@ __global__ void k_pcg_init(const double* part, int nch, PcgState* s, double tol,
 // Fused control + update kernels (one CTA per 2048-element chunk).  Every
 // CTA reduces the same fixed-chunk partials in the same order, so all CTAs
 // take the same decision; CTA 0 records it in the state.
+//
+// Layouts (global chunk order, shared by the single-GPU and sharded drivers):
+//   xpost[2c], xpost[2c + 1]: p.q and |f - A u|^2 partials of chunk c
+//                             (k_post_pass; the A-pass exchange);
+//   xrz[kRzRec c + 0..3]:      r.z, max|z| (scatter), max|p|, max|u|
+//                             (k_iter_a / k_update_u; the apply exchange);
+//   pmax[b]:                  max|p_new| of the band's chunk b (k_iter_b),
+//                             copied into xrz by the next k_iter_a.
+// A kernel's own chunks are [c0, c0 + gridDim) of the global order; its
+// vectors are band pointers (index 0 = the first point of chunk c0).
+
+// Halo segments of a sharded band (rows the rank's subdomains read outside
+// its band): r -= alpha q is applied there redundantly by extra CTAs of
+// k_iter_a (the owner computes the same values), so the apply needs no
+// r exchange.  Offsets relative to the band start; zero-length on one GPU.
+struct HaloSeg {
+    int lo0, len0, lo1, len1;
+};
 
 // After the A-pass of iteration `it`: residual / stagnation check of
 // iteration it-1 (pcg.py:107-119), breakdown test of iteration it
@@ -113,11 +131,13 @@ __global__ void k_pcg_init(const double* part, int nch, PcgState* s, double tol,
 // decision; CTA 0 records it in the state.  Every load that does not depend
 // on the reduction (state scalars, the history entry of the stagnation test,
 // this thread's partials and its p, q, r chunk values) is issued before it, so
-// the serial prologue costs about one memory round trip.
-template <bool WITH_U>
-__global__ void __launch_bounds__(kRed, 4) k_iter_a(const double* part_pq, const double* part_res, int nch, int do_p,
-                                                 int pending, long long it, PcgState* s, double* hist, double* u,
-                                                 double* r, const double* p, const double* q, int N, double* amax) {
+// the serial prologue costs about one memory round trip.  CTAs >= nchb update
+// the halo segments' r only.
+template <bool WITH_U, bool HALO = false>
+__global__ void __launch_bounds__(kRed, 4) k_iter_a(const double* xpost, int nch, int do_p, int pending, long long it,
+                                                 PcgState* s, double* hist, double* u, double* r, const double* p,
+                                                 const double* q, int nb, int c0, int nchb, double* xrz,
+                                                 const double* pmax, HaloSeg hs) {
     __shared__ double sh[kRed];
     __shared__ int decided;
     pdl_wait();
@@ -126,19 +146,31 @@ __global__ void __launch_bounds__(kRed, 4) k_iter_a(const double* part_pq, const
     const double rho_prev = s->rho[(it - 1) & 1], nf = s->nf, tol = s->tol;
     const long long k = it - 1;
     const double h30 = (pending && k >= 30 && threadIdx.x == 0) ? hist[k - 30] : 0.0;
-    const int base = blockIdx.x * kChunk;
-    double pv[kChunk / kRed], qv[kChunk / kRed], rv[kChunk / kRed];
+    const bool halo = HALO && (int)blockIdx.x >= nchb;
+    int base, lim;
+    if (!halo) {
+        base = blockIdx.x * kChunk;
+        lim = nb;
+    } else {  // halo CTA: segment 0 then segment 1, kChunk points each
+        const int h = blockIdx.x - nchb, n0 = (hs.len0 + kChunk - 1) / kChunk;
+        base = h < n0 ? hs.lo0 + h * kChunk : hs.lo1 + (h - n0) * kChunk;
+        lim = h < n0 ? hs.lo0 + hs.len0 : hs.lo1 + hs.len1;
+    }
+    // av: p for the in-kernel u update (WITH_U band CTAs), else r (hoisted
+    // where registers allow: the 64-register budget holds two chunk arrays)
+    const bool ua = WITH_U && !halo;
+    double av[kChunk / kRed], qv[kChunk / kRed];
 #pragma unroll
     for (int e = 0; e < kChunk / kRed; ++e) {
         const int i = base + e * kRed + threadIdx.x;
-        pv[e] = (WITH_U && do_p && i < N) ? p[i] : 0.0;  // p only for the in-kernel u update
-        qv[e] = (do_p && i < N) ? q[i] : 0.0;
-        rv[e] = (!WITH_U && do_p && i < N) ? r[i] : 0.0;  // hoisted where registers allow
+        const bool in = do_p && i < lim;
+        av[e] = in ? (ua ? p[i] : r[i]) : 0.0;
+        qv[e] = in ? q[i] : 0.0;
     }
     double lp = 0.0, lr = 0.0;
     for (int c = threadIdx.x; c < nch; c += kRed) {
-        if (do_p) lp += part_pq[c];
-        if (pending) lr += part_res[c];
+        if (do_p) lp += xpost[2 * c];
+        if (pending) lr += xpost[2 * c + 1];
     }
     if (stopv) return;
     double denom = 0.0, res2 = 0.0;
@@ -178,12 +210,15 @@ __global__ void __launch_bounds__(kRed, 4) k_iter_a(const double* part_pq, const
     }
     __syncthreads();
     if (decided || !do_p) return;
+    // max|p| of the direction this pass multiplied (k_iter_b of the previous
+    // iteration) into the record, for this iteration's k_iter_b scale bound
+    if (!halo && threadIdx.x == 32) xrz[kRzRec * (c0 + blockIdx.x) + 2] = pmax[blockIdx.x];
     const double al = rho_prev / denom;
-    if (!WITH_U) {  // u += alpha p runs concurrently in k_update_u (graph side branch)
+    if (!ua) {  // u += alpha p runs concurrently in k_update_u (graph side branch), or a halo CTA
 #pragma unroll
         for (int e = 0; e < kChunk / kRed; ++e) {
             const int i = base + e * kRed + threadIdx.x;
-            if (i < N) r[i] = __dsub_rn(rv[e], __dmul_rn(al, qv[e]));
+            if (i < lim) r[i] = __dsub_rn(av[e], __dmul_rn(al, qv[e]));
         }
         return;
     }
@@ -191,23 +226,23 @@ __global__ void __launch_bounds__(kRed, 4) k_iter_a(const double* part_pq, const
 #pragma unroll
     for (int e = 0; e < kChunk / kRed; ++e) {
         const int i = base + e * kRed + threadIdx.x;
-        if (i < N) {
-            const double un = __dadd_rn(u[i], __dmul_rn(al, pv[e]));
+        if (i < nb) {
+            const double un = __dadd_rn(u[i], __dmul_rn(al, av[e]));
             u[i] = un;
             r[i] = __dsub_rn(r[i], __dmul_rn(al, qv[e]));
             m = fmax(m, fabs(un));
         }
     }
     m = chunk_absmax(m, sh);
-    if (threadIdx.x == 0) amax[2 * blockIdx.x + 1] = m;
+    if (threadIdx.x == 0) xrz[kRzRec * (c0 + blockIdx.x) + 3] = m;
 }
 
 // k_iter_a's u half: u += alpha p and max|u| per chunk, with the alpha CTA 0 of
 // k_iter_a stored (the same quotient every CTA computes).  Off the critical
 // path: it runs beside the preconditioner apply and joins before k_iter_b
 // rewrites p (the next A-pass is u's only consumer).
-__global__ void __launch_bounds__(kRed) k_update_u(const PcgState* s, double* u, const double* p, int N,
-                                                   double* amax) {
+__global__ void __launch_bounds__(kRed) k_update_u(const PcgState* s, double* u, const double* p, int N, int c0,
+                                                   double* xrz) {
     __shared__ double sh[kRed];
     if (s->stop) return;
     const double al = s->alpha;
@@ -230,18 +265,20 @@ __global__ void __launch_bounds__(kRed) k_update_u(const PcgState* s, double* u,
         }
     }
     m = chunk_absmax(m, sh);
-    if (threadIdx.x == 0) amax[2 * blockIdx.x + 1] = m;
+    if (threadIdx.x == 0) xrz[kRzRec * (c0 + blockIdx.x) + 3] = m;
 }
 
 // After the apply: rho_it = r.z, beta = rho_it / rho_{it-1}, p = z + beta p,
-// max|p| per chunk.
-// After the apply: rho_it = r.z, beta = rho_it / rho_{it-1}, p = z + beta p,
 // max|p| per chunk; the independent loads (state, partials, this thread's z
-// and p chunk values) are issued ahead of the reduction.  In graph replay the
-// last CTA advances the iteration counter.
-__global__ void __launch_bounds__(kRed) k_iter_b(const double* part_rz, int nch, long long it, PcgState* s,
-                                                 double* p, const double* z, int N, double* amax) {
+// and p chunk values) are issued ahead of the reduction.  CTA 0 also fixes the
+// 2-RHS scales of the next A-pass from the record's global maxima:
+// p_new = z + beta p_old, so max|p_new| <= max|z| + |beta| max|p_old| (both
+// products rounded as written: the same bound on every rank).  In graph
+// replay the last CTA advances the iteration counter.
+__global__ void __launch_bounds__(kRed) k_iter_b(const double* xrz, int nch, long long it, PcgState* s, double* p,
+                                                 const double* z, int nb, double* pmax) {
     __shared__ double sh[kRed];
+    __shared__ double shm[3][kRed];
     pdl_wait();
     const int stopv = s->stop;
     const bool replay = it < 0;
@@ -252,23 +289,45 @@ __global__ void __launch_bounds__(kRed) k_iter_b(const double* part_rz, int nch,
 #pragma unroll
     for (int e = 0; e < kChunk / kRed; ++e) {
         const int i = base + e * kRed + threadIdx.x;
-        zv[e] = i < N ? z[i] : 0.0;
-        pv[e] = i < N ? p[i] : 0.0;
+        zv[e] = i < nb ? z[i] : 0.0;
+        pv[e] = i < nb ? p[i] : 0.0;
     }
-    double loc = 0.0;
-    for (int c = threadIdx.x; c < nch; c += kRed) loc += part_rz[c];
+    double loc = 0.0, mz = 0.0, mp = 0.0, mu = 0.0;
+    const bool cta0 = blockIdx.x == 0;
+    for (int c = threadIdx.x; c < nch; c += kRed) {
+        loc += xrz[kRzRec * c];
+        if (cta0) {
+            mz = fmax(mz, xrz[kRzRec * c + 1]);
+            mp = fmax(mp, xrz[kRzRec * c + 2]);
+            mu = fmax(mu, xrz[kRzRec * c + 3]);
+        }
+    }
     if (stopv) return;
     const double rz = block_tree(loc, sh);
     const double beta = rz / rho_prev;
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        s->beta = beta;
-        s->rho[it & 1] = rz;
+    if (cta0) {
+        shm[0][threadIdx.x] = mz;
+        shm[1][threadIdx.x] = mp;
+        shm[2][threadIdx.x] = mu;
+        __syncthreads();
+        for (int o = kRed / 2; o > 0; o >>= 1) {
+            if (threadIdx.x < o)
+#pragma unroll
+                for (int t = 0; t < 3; ++t) shm[t][threadIdx.x] = fmax(shm[t][threadIdx.x], shm[t][threadIdx.x + o]);
+            __syncthreads();
+        }
+        if (threadIdx.x == 0) {
+            s->beta = beta;
+            s->rho[it & 1] = rz;
+            s->sc[0] = pcg_pow2_scale(__dadd_rn(shm[0][0], __dmul_rn(fabs(beta), shm[1][0])));
+            s->sc[1] = pcg_pow2_scale(shm[2][0]);
+        }
     }
     double m = 0.0;
 #pragma unroll
     for (int e = 0; e < kChunk / kRed; ++e) {
         const int i = base + e * kRed + threadIdx.x;
-        if (i < N) {
+        if (i < nb) {
             const double pn = __dadd_rn(zv[e], __dmul_rn(beta, pv[e]));
             p[i] = pn;
             m = fmax(m, fabs(pn));
@@ -276,7 +335,7 @@ __global__ void __launch_bounds__(kRed) k_iter_b(const double* part_rz, int nch,
     }
     __syncthreads();
     m = chunk_absmax(m, sh);
-    if (threadIdx.x == 0) amax[2 * blockIdx.x] = m;
+    if (threadIdx.x == 0) pmax[blockIdx.x] = m;
     if (replay) {  // graph replay: the last CTA (every CTA has read it_dev) advances the iteration
         __syncthreads();
         if (threadIdx.x == 0) {
@@ -289,17 +348,52 @@ __global__ void __launch_bounds__(kRed) k_iter_b(const double* part_rz, int nch,
     }
 }
 
-__global__ void k_pcg_rho0(const double* part_rz, int nch, PcgState* s) {
+// After the first apply (pcg.py:85-91): rho_0 = r.z (every CTA reduces, CTA 0
+// stores), p = z and max|p| per chunk (= max|z|, the record's field 1).
+__global__ void __launch_bounds__(kRed) k_pcg_setup(const double* xrz, int nch, PcgState* s, double* p,
+                                                    const double* z, int nb, int c0, double* pmax) {
     __shared__ double sh[kRed];
     if (s->stop) return;
-    const double rz = reduce_partials(part_rz, nch, sh);
+    const int base = blockIdx.x * kChunk;
+#pragma unroll
+    for (int e = 0; e < kChunk / kRed; ++e) {
+        const int i = base + e * kRed + threadIdx.x;
+        if (i < nb) p[i] = z[i];
+    }
+    if (threadIdx.x == 0) pmax[blockIdx.x] = xrz[kRzRec * (c0 + blockIdx.x) + 1];
+    if (blockIdx.x != 0) return;
+    double loc = 0.0;
+    for (int c = threadIdx.x; c < nch; c += kRed) loc += xrz[kRzRec * c];
+    const double rz = block_tree(loc, sh);
     if (threadIdx.x == 0) s->rho[0] = rz;
 }
 
+// The identity preconditioner (pcg.py:68): z = r, with the apply's chunk
+// record fields 0 (r.z) and 1 (max|z|).
+__global__ void __launch_bounds__(kRed) k_identity_apply(const double* r, double* z, int nb, double* rec,
+                                                         const int* stop) {
+    __shared__ double sh[2 * kRed];
+    if (stop && *stop) return;
+    const int base = blockIdx.x * kChunk;
+    double loc = 0.0, zm = 0.0;
+#pragma unroll
+    for (int e = 0; e < kChunk / kRed; ++e) {
+        const int i = base + e * kRed + threadIdx.x;
+        if (i < nb) {
+            const double v = r[i];
+            z[i] = v;
+            loc = fma(v, v, loc);
+            zm = fmax(zm, fabs(v));
+        }
+    }
+    chunk_sum_max(loc, zm, sh, rec + kRzRec * blockIdx.x);
+}
+
 // Chunk partials of p.q (A-pass denominator) and |f - w|^2 (true residual of
-// the previous iterate); the loads are issued before the stop flag is tested.
+// the previous iterate) -> xpost[2c], xpost[2c + 1] (c = c0 + blockIdx.x); the
+// loads are issued before the stop flag is tested.
 __global__ void k_post_pass(const double* p, const double* q, const double* f, const double* w, int N, int do_p,
-                            int pending, double* part_pq, double* part_res, const int* stop) {
+                            int pending, double* xpost, const int* stop) {
     __shared__ double sh[kRed];
     pdl_wait();
     const int stopv = *stop;  // tested after the chunk loads are issued
@@ -319,12 +413,12 @@ __global__ void k_post_pass(const double* p, const double* q, const double* f, c
     if (stopv) return;
     if (do_p) {
         const double t = block_tree(a, sh);
-        if (threadIdx.x == 0) part_pq[blockIdx.x] = t;
+        if (threadIdx.x == 0) xpost[2 * blockIdx.x] = t;
         __syncthreads();
     }
     if (pending) {
         const double t = block_tree(b, sh);
-        if (threadIdx.x == 0) part_res[blockIdx.x] = t;
+        if (threadIdx.x == 0) xpost[2 * blockIdx.x + 1] = t;
     }
 }
 
@@ -411,7 +505,7 @@ struct PcgWork {
     int N = 0;
     int64_t cap = 0;
     double *PU = nullptr, *QW = nullptr, *r = nullptr, *z = nullptr, *part = nullptr, *hist = nullptr;
-    double* amax = nullptr;  // per-chunk max|p|, max|u| (2-RHS FFT column scaling)
+    // part = [xf: nch | xpost: 2 nch | xrz: kRzRec nch | pmax: nch] (layouts above k_iter_a)
     double* fcopy = nullptr; // the right-hand side (graph-stable address)
     cudaStream_t cap_stream = nullptr;
     cudaStream_t side_stream = nullptr;  // graph side branch (u update)
@@ -432,7 +526,6 @@ struct PcgWork {
         cudaFree(z);
         cudaFree(part);
         cudaFree(hist);
-        cudaFree(amax);
         cudaFree(fcopy);
         if (gexec) cudaGraphExecDestroy(gexec);
         if (cap_stream) cudaStreamDestroy(cap_stream);
@@ -469,9 +562,8 @@ static PcgWork* work_acquire(int N, int64_t cap, int* rc) {
     if (e == cudaSuccess) e = cudaMalloc(&w->QW, 2 * (size_t)N * 8);
     if (e == cudaSuccess) e = cudaMalloc(&w->r, (size_t)N * 8);
     if (e == cudaSuccess) e = cudaMalloc(&w->z, (size_t)N * 8);
-    if (e == cudaSuccess) e = cudaMalloc(&w->part, 3 * (size_t)nch * 8);
+    if (e == cudaSuccess) e = cudaMalloc(&w->part, (4 + kRzRec) * (size_t)nch * 8);
     if (e == cudaSuccess) e = cudaMalloc(&w->hist, (size_t)cap * 8);
-    if (e == cudaSuccess) e = cudaMalloc(&w->amax, 2 * (size_t)nch * 8);
     if (e == cudaSuccess) e = cudaMalloc(&w->fcopy, (size_t)N * 8);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&w->cap_stream, cudaStreamNonBlocking);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&w->side_stream, cudaStreamNonBlocking);
@@ -510,9 +602,13 @@ static int ensure_events(PcgWork* w, size_t n) {
 
 }  // namespace ie
 
-extern "C" int ie_pcg_f64(const ie_matvec* A, const ie_precond* T, const double* f, double* u, double tol,
-                          int64_t max_iters, double* hist, int64_t* n_it, int32_t* flags, double* times,
-                          int64_t* fail_iter, double* fail_value, void* stream) {
+// prof != nullptr (ie_pcg_profile_f64): every iteration is launched directly
+// (no graph, no side branch) with events between its kernel groups, and
+// prof[0..4] accumulate the mean device ms of the steady-state (2-RHS)
+// iterations' matvec, k_post_pass, k_iter_a, apply, k_iter_b.
+static int pcg_impl(const ie_matvec* A, const ie_precond* T, const double* f, double* u, double tol,
+                    int64_t max_iters, double* hist, int64_t* n_it, int32_t* flags, double* times,
+                    int64_t* fail_iter, double* fail_value, void* stream, double* prof) {
     if (!A || !f || !u || !hist || !n_it || !flags || !times || max_iters < 0 || !(tol > 0.0 && tol < 1.0)) {
         set_error("ie_pcg_f64: bad arguments");
         return IE_ERR_ARG;
@@ -537,22 +633,23 @@ extern "C" int ie_pcg_f64(const ie_matvec* A, const ie_precond* T, const double*
     double* uu = W->PU + N;
     double* q = W->QW;
     double* w = W->QW + N;
-    double* part_pq = W->part;
-    double* part_res = W->part + nch;
-    double* part_rz = W->part + 2 * nch;
+    double* xf = W->part;
+    double* xpost = W->part + nch;
+    double* xrz = W->part + 3 * nch;
+    double* pmax = xrz + kRzRec * nch;
     const int* stop = &W->st->stop;
+    // z = T^{-1} r and the chunk record's r.z / max|z| fields
+    auto apply_on = [&](const double* rin, double* zout, cudaStream_t s2) -> int {
+        if (T) return precond_apply(T, rin, zout, xrz, s2, stop);
+        k_identity_apply<<<nch, kRed, 0, s2>>>(rin, zout, N, xrz, stop);
+        IE_LAUNCHED();
+        return IE_OK;
+    };
     auto apply = [&](const double* rin, double* zout, int64_t evi) -> int {
         const bool timed = 2 * evi + 1 < (int64_t)W->ev.size();
         if (timed) IE_CUDA(cudaEventRecord(W->ev[2 * evi], st));
-        if (T) {
-            int r2 = precond_apply(T, rin, zout, part_rz, st, stop);
-            if (r2) return r2;
-        } else {
-            k_copy_if_running<<<g1(N), 256, 0, st>>>(zout, rin, N, stop);
-            IE_LAUNCHED();
-            k_dot_partials<<<nch, kRed, 0, st>>>(rin, zout, N, 0, part_rz);
-            IE_LAUNCHED();
-        }
+        int r2 = apply_on(rin, zout, st);
+        if (r2) return r2;
         if (timed) IE_CUDA(cudaEventRecord(W->ev[2 * evi + 1], st));
         return IE_OK;
     };
@@ -560,68 +657,93 @@ extern "C" int ie_pcg_f64(const ie_matvec* A, const ie_precond* T, const double*
     IE_CUDA(cudaMemcpyAsync(W->fcopy, f, (size_t)N * 8, cudaMemcpyDeviceToDevice, st));
     f = W->fcopy;
     // ||f||, state init (pcg.py:72-91)
-    k_dot_partials<<<nch, kRed, 0, st>>>(f, f, N, 0, part_pq);
+    k_dot_partials<<<nch, kRed, 0, st>>>(f, f, N, 0, xf);
     IE_LAUNCHED();
-    k_pcg_init<<<1, kRed, 0, st>>>(part_pq, nch, W->st, tol, max_iters, W->hist);
+    k_pcg_init<<<1, kRed, 0, st>>>(xf, nch, W->st, tol, max_iters, W->hist);
     IE_LAUNCHED();
     IE_CUDA(cudaMemsetAsync(uu, 0, (size_t)N * 8, st));
     IE_CUDA(cudaMemcpyAsync(W->r, f, (size_t)N * 8, cudaMemcpyDeviceToDevice, st));
     if ((rc = apply(W->r, W->z, 0))) return rc;
-    IE_CUDA(cudaMemcpyAsync(p, W->z, (size_t)N * 8, cudaMemcpyDeviceToDevice, st));
-    k_pcg_rho0<<<1, kRed, 0, st>>>(part_rz, nch, W->st);
+    k_pcg_setup<<<nch, kRed, 0, st>>>(xrz, nch, W->st, p, W->z, N, 0, pmax);  // p = z, rho_0
     IE_LAUNCHED();
     // iterations: `it` = the iteration whose A-pass is enqueued; the pass also
     // carries u_{it-1} for the deferred true-residual check of iteration it-1.
     // Steady-state iterations (2 <= it < max_iters) replay one captured CUDA
     // graph that reads `it` from the device state.
     static const bool no_fork = getenv("IEDD_B200_NO_FORK") != nullptr;  // u update in k_iter_a (comparison)
+    cudaEvent_t pev[6] = {};
+    int64_t nprof = 0;
+    if (prof) {
+        for (auto& e : pev) IE_CUDA(cudaEventCreate(&e));
+        for (int i = 0; i < 5; ++i) prof[i] = 0.0;
+    }
+    struct PevFree {
+        cudaEvent_t* e;
+        ~PevFree() {
+            for (int i = 0; i < 6; ++i)
+                if (e[i]) cudaEventDestroy(e[i]);
+        }
+    } pev_free{pev};
     auto enqueue_iter = [&](int64_t itarg, int do_p, int pending, bool spec, cudaStream_t s2, bool timed_apply,
                             int64_t evi) -> int {
         int r2;
+        const bool pf = prof && do_p && pending && spec;
+        auto mark = [&](int i) -> int {
+            if (pf) IE_CUDA(cudaEventRecord(pev[i], s2));
+            return IE_OK;
+        };
+        if ((r2 = mark(0))) return r2;
         if (do_p && pending) {
-            r2 = matvec_launch(A, W->PU, N, 2, W->QW, N, 0, N, s2, stop, W->amax);
+            r2 = matvec_launch(A, W->PU, N, 2, W->QW, N, 0, N, s2, stop, W->st->sc);
         } else if (do_p) {
             r2 = matvec_launch(A, p, N, 1, q, N, 0, N, s2, stop);
         } else {
             r2 = matvec_launch(A, uu, N, 1, w, N, 0, N, s2, stop);
         }
-        if (r2) return r2;
+        if (r2 || (r2 = mark(1))) return r2;
         IE_CUDA(launch_k(k_post_pass, dim3(nch), dim3(kRed), 0, s2, (const double*)p, (const double*)q, f,
-                         (const double*)w, N, do_p, pending, part_pq, part_res, stop));
+                         (const double*)w, N, do_p, pending, xpost, stop));
         IE_LAUNCHED();
+        if ((r2 = mark(2))) return r2;
         // in the captured iteration u += alpha p forks onto a side branch beside the apply
-        const bool fork_u = itarg < 0 && do_p && spec && !no_fork;
-        IE_CUDA(launch_k(fork_u ? k_iter_a<false> : k_iter_a<true>, dim3(nch), dim3(kRed), 0, s2, (const double*)part_pq, (const double*)part_res, nch,
-                         do_p, pending, (long long)itarg, W->st, W->hist, fork_u ? nullptr : uu, W->r,
-                         (const double*)p, (const double*)q, N, W->amax));
+        const bool fork_u = itarg < 0 && do_p && spec && !no_fork && !prof;
+        IE_CUDA(launch_k(fork_u ? k_iter_a<false> : k_iter_a<true>, dim3(nch), dim3(kRed), 0, s2,
+                         (const double*)xpost, nch, do_p, pending, (long long)itarg, W->st, W->hist,
+                         fork_u ? nullptr : uu, W->r, (const double*)p, (const double*)q, N, 0, nch, xrz,
+                         (const double*)pmax, HaloSeg{0, 0, 0, 0}));
         IE_LAUNCHED();
         if (fork_u) {
             IE_CUDA(cudaEventRecord(W->fork_ev, s2));
             IE_CUDA(cudaStreamWaitEvent(W->side_stream, W->fork_ev, 0));
-            k_update_u<<<nch, kRed, 0, W->side_stream>>>(W->st, uu, p, N, W->amax);
+            k_update_u<<<nch, kRed, 0, W->side_stream>>>(W->st, uu, p, N, 0, xrz);
             IE_LAUNCHED();
             IE_CUDA(cudaEventRecord(W->join_ev, W->side_stream));
         }
         if (spec) {  // speculative: z_it is discarded if iteration it is the last
-            if (timed_apply) {
+            if ((r2 = mark(3))) return r2;
+            if (timed_apply && !pf) {
                 if ((r2 = apply(W->r, W->z, evi))) return r2;
-            } else if (T) {
-                if ((r2 = precond_apply(T, W->r, W->z, part_rz, s2, stop))) return r2;
-            } else {
-                k_copy_if_running<<<g1(N), 256, 0, s2>>>(W->z, W->r, N, stop);
-                IE_LAUNCHED();
-                k_dot_partials<<<nch, kRed, 0, s2>>>(W->r, W->z, N, 0, part_rz);
-                IE_LAUNCHED();
+            } else if ((r2 = apply_on(W->r, W->z, s2))) {
+                return r2;
             }
+            if ((r2 = mark(4))) return r2;
             // k_iter_b rewrites p, which the side branch reads: join first
             if (fork_u) IE_CUDA(cudaStreamWaitEvent(s2, W->join_ev, 0));
-            IE_CUDA(launch_k(k_iter_b, dim3(nch), dim3(kRed), 0, s2, (const double*)part_rz, nch, (long long)itarg,
-                             W->st, p, (const double*)W->z, N, W->amax));
+            IE_CUDA(launch_k(k_iter_b, dim3(nch), dim3(kRed), 0, s2, (const double*)xrz, nch, (long long)itarg,
+                             W->st, p, (const double*)W->z, N, pmax));
             IE_LAUNCHED();
+            if ((r2 = mark(5))) return r2;
+        }
+        if (pf) {
+            IE_CUDA(cudaEventSynchronize(pev[5]));
+            float ms[5];
+            for (int i = 0; i < 5; ++i) IE_CUDA(cudaEventElapsedTime(&ms[i], pev[i], pev[i + 1]));
+            for (int i = 0; i < 5; ++i) prof[i] += ms[i];
+            ++nprof;
         }
         return IE_OK;
     };
-    const bool use_graph = max_iters >= 3 && !getenv("IEDD_B200_NO_GRAPH");
+    const bool use_graph = max_iters >= 3 && !getenv("IEDD_B200_NO_GRAPH") && !prof;
     if (use_graph) {
         const uint64_t ka = matvec_uid(A), kt = T ? precond_uid(T) : 0;
         if (!W->gexec || W->key_a != ka || W->key_t != kt) {
@@ -718,9 +840,29 @@ extern "C" int ie_pcg_f64(const ie_matvec* A, const ie_precond* T, const double*
     cudaGetLastError();
     times[1] = np ? tp / (double)np : 0.0;
     if (S.nf == 0.0) times[0] = times[1] = 0.0;  // zero right-hand side (pcg.py:74-78)
+    if (prof && nprof)
+        for (int i = 0; i < 5; ++i) prof[i] /= (double)nprof;
     if (S.status == 4) return IE_ERR_BREAKDOWN;
     if (S.status == 5) return IE_ERR_NONFINITE;
     return IE_OK;
+}
+
+extern "C" int ie_pcg_f64(const ie_matvec* A, const ie_precond* T, const double* f, double* u, double tol,
+                          int64_t max_iters, double* hist, int64_t* n_it, int32_t* flags, double* times,
+                          int64_t* fail_iter, double* fail_value, void* stream) {
+    return pcg_impl(A, T, f, u, tol, max_iters, hist, n_it, flags, times, fail_iter, fail_value, stream, nullptr);
+}
+
+extern "C" int ie_pcg_profile_f64(const ie_matvec* A, const ie_precond* T, const double* f, double* u, double tol,
+                                  int64_t max_iters, double* hist, int64_t* n_it, int32_t* flags, double* times,
+                                  double* h_phase_ms, void* stream) {
+    if (!h_phase_ms) {
+        set_error("ie_pcg_profile_f64: bad arguments");
+        return IE_ERR_ARG;
+    }
+    int64_t fi = 0;
+    double fv = 0.0;
+    return pcg_impl(A, T, f, u, tol, max_iters, hist, n_it, flags, times, &fi, &fv, stream, h_phase_ms);
 }
 
 // ---------------------------------------------------------------- K5 --
@@ -967,7 +1109,7 @@ __global__ void k_lz_dot(const double* x, const double* y, int N, double* part, 
 
 extern "C" int ie_lanczos_f64(const ie_matvec* A, const ie_precond* T, const double* v0, int32_t which,
                               int64_t max_iters, double rtol, double* lambda, int64_t* steps, void* stream) {
-    if (!A || !T || !v0 || !lambda || (which != 0 && which != 1) || max_iters < 0) {
+    if (!A || !v0 || !lambda || (which != 0 && which != 1) || max_iters < 0) {
         set_error("ie_lanczos_f64: bad arguments");
         return IE_ERR_ARG;
     }
@@ -1004,7 +1146,12 @@ extern "C" int ie_lanczos_f64(const ie_matvec* A, const ie_precond* T, const dou
     // one Lanczos step (spectrum.py:160-187) on stream s2
     auto step = [&](cudaStream_t s2) -> int {
         int r2;
-        if ((r2 = precond_apply(T, avj.p, wb.p, nullptr, s2, stop))) return r2;
+        if (T) {
+            if ((r2 = precond_apply(T, avj.p, wb.p, nullptr, s2, stop))) return r2;
+        } else {  // identity (precond.py:133-134)
+            k_copy_if_running<<<g1(N), 256, 0, s2>>>(wb.p, avj.p, N, stop);
+            IE_LAUNCHED();
+        }
         k_lz_dot<<<nch, kRed, 0, s2>>>(wb.p, avj.p, N, part.p, S.p);
         IE_LAUNCHED();
         k_lz_alpha<<<1, kRed, 0, s2>>>(part.p, nch, da, S.p);
@@ -1135,341 +1282,465 @@ extern "C" int ie_update_f64(int32_t op, double* a, const double* b, double s, i
     return IE_OK;
 }
 
-// ------------------------------------------------------- sharded K4 (NCCL) --
-// ie_pcg_f64 on G ranks (one process per GPU), rank g owning the grid-row band
-// [bounds[g], bounds[g+1]) of every vector (distributed.py documents the plan;
-// this is its native driver).  Per iteration, on the rank's stream:
-//   all-gather of the per-chunk max|p|, max|u| (2-RHS scaling) ->
-//   band row FFTs -> all-to-all -> column slab pass -> all-to-all -> inverse
-//   rows (q, w on the band) -> post_pass partials -> all-gather -> k_iter_a
-//   (every rank reduces all chunks in global order: identical scalars) ->
-//   r-halo send/recv -> apply of the rank's subdomains, z on the band ->
-//   all-gather of r.z partials -> k_iter_b.
-// Device-side control as in ie_pcg_f64; the steady-state iteration, NCCL calls
-// included, is one captured CUDA graph.  Every rank takes the same decisions
-// from the same reduced scalars, so the collectives stay matched.
+
+// ------------------------------------------------ sharded K4 (NVLink P2P) --
+// ie_pcg_f64 on G ranks, one per GPU: rank g owns the grid-row band
+// [b0, b1) of every vector (equal, chunk-aligned bands of whole rows; the 2D
+// FFT operator with G | 2n).  There is no collective library on this path:
+// every exchange is a push of the producer's slab straight into the
+// consumers' memory over NVLink (peer pointers from CUDA IPC), followed by a
+// system-scope release add of the byte count on the consumer's mailbox
+// counter; the consumer's k_wait spins (acquire) until the expected bytes of
+// the epoch have arrived.  Per PCG iteration there are four exchange points,
+// the dependency chain of the algorithm:
+//   FWD   row FFTs of the band -> column slab owners (all-to-all transpose);
+//   BACK  column pass -> every rank's NEED rows (band + the rows its
+//         subdomains read outside it): the second transpose also carries the
+//         r-halo, because the rank recomputes q on its halo rows and applies
+//         r -= alpha q there itself, bitwise as the owner does;
+//   POST  p.q and |f - A u|^2 chunk partials (all-gather);
+//   RZ    the apply's chunk record (r.z, max|z|, max|p|, max|u|): beta and
+//         the next pass's 2-RHS scales on every rank (no max|p| exchange).
+// Every rank reduces the global chunk order with the single-GPU kernels, so
+// n_it, the history and u are bitwise those of ie_pcg_f64 for any G.
+// Buffers are single-buffered: each push of epoch e into a peer happens
+// after the pusher has consumed that peer's previous exchange, which the peer
+// sent only after its last read of the buffer.
+// Counters are monotonic over the shard's lifetime (never reset: a peer may
+// already be pushing the next solve's first exchange).
+//
+// The same driver runs G ranks inside one process on one device
+// (ie_pcg_sharded_local_f64; peers are plain device pointers): every
+// exchange phase runs for all ranks before the next phase starts, so no
+// kernel ever waits on work queued behind it.  This is how the G > 1 paths
+// are tested on a single B200 (tests/test_gpu_parity.py::TestShardedP2P).
 struct ie_fft;
-namespace ie {
-// Device workspace + captured iteration graph of the sharded driver, cached on
-// the communicator for repeated solves with the same operator / bands.
-struct ShardWork {
-    uint64_t key_a = 0, key_t = 0;
-    int64_t nb = 0, b0 = 0, cap = 0;
-    double *PU = nullptr, *QW = nullptr, *rfull = nullptr, *z = nullptr, *fb = nullptr, *part = nullptr;
-    double *amax = nullptr, *dh = nullptr;
-    double2 *buf1 = nullptr, *buf2 = nullptr, *buf3 = nullptr;
-    PcgState* S = nullptr;
-    PcgState* host = nullptr;
-    cudaGraphExec_t gexec = nullptr;
-    cudaStream_t cap_s = nullptr;
-    int gnodes = 0;
-    ~ShardWork() {
-        for (void* p : {(void*)PU, (void*)QW, (void*)rfull, (void*)z, (void*)fb, (void*)part, (void*)amax,
-                        (void*)dh, (void*)buf1, (void*)buf2, (void*)buf3, (void*)S})
-            if (p) cudaFree(p);
-        if (host) cudaFreeHost(host);
-        if (gexec) cudaGraphExecDestroy(gexec);
-        if (cap_s) cudaStreamDestroy(cap_s);
-    }
-};
-}  // namespace ie
-
-struct ie_comm {
-    ncclComm_t c;
-    int nranks, rank;
-    ie::ShardWork* work = nullptr;
-};
-
 namespace ie {
 const ie_fft* matvec_fft(const ie_matvec* m);
 int matvec_dim(const ie_matvec* m);
 int matvec_n(const ie_matvec* m);
+int fft_M(const ie_fft* f);
 int fft_band_fwd(const ie_fft* f, const double* X0, const double* X1, int nrows, int parts, double2* out,
-                 const double* amax, int namax, cudaStream_t st);
-int fft_band_cols(const ie_fft* f, double2* buf, int c0, int ncols, cudaStream_t st);
+                 const double* scales, cudaStream_t st, const int* stop);
+int fft_band_cols(const ie_fft* f, double2* buf, int c0, int ncols, cudaStream_t st, const int* stop);
 int fft_band_inv(const ie_fft* f, const double2* in, int nrows, int parts, double* Y0, double* Y1,
-                 const double* amax, int namax, cudaStream_t st);
+                 const double* scales, cudaStream_t st, const int* stop);
 int precond_apply_band(const ie_precond* p, const double* r, double* z, double* partials, int64_t i0, int64_t i1,
                        cudaStream_t st, const int* stop);
+
+enum XSlot { kSlotF = 0, kSlotRz, kSlotFwd, kSlotBack, kSlotPost, kNumSlots };
+constexpr int kMaxRanks = 16;
+constexpr int kPushThreads = 256;
+
+struct PushDesc {
+    const char* src;
+    char* dst;
+    long long bytes;  // multiple of 8
+    unsigned long long* ctr;
+};
+struct PushArgs {
+    PushDesc d[kMaxRanks];
+    const int* stop;
+};
+
+// Copy descriptor blockIdx.y (16-B words, tile t of kPushThreads words to CTA
+// t mod gridDim.x; an odd trailing 8-B word by CTA 0), then release-add the
+// CTA's bytes to the consumer's counter.  src == dst (a rank's own slab,
+// already in place) only counts.
+__global__ void __launch_bounds__(kPushThreads) k_push(const __grid_constant__ PushArgs a) {
+    pdl_wait();
+    if (*a.stop) return;
+    const PushDesc d = a.d[blockIdx.y];
+    const long long nw = d.bytes >> 4, step = (long long)gridDim.x * kPushThreads;
+    if (d.src != d.dst) {
+        const int4* s = reinterpret_cast<const int4*>(d.src);
+        int4* t = reinterpret_cast<int4*>(d.dst);
+        long long w = (long long)blockIdx.x * kPushThreads + threadIdx.x;
+        for (; w + 3 * step < nw; w += 4 * step) {  // four loads in flight per thread
+            const int4 v0 = s[w], v1 = s[w + step], v2 = s[w + 2 * step], v3 = s[w + 3 * step];
+            t[w] = v0;
+            t[w + step] = v1;
+            t[w + 2 * step] = v2;
+            t[w + 3 * step] = v3;
+        }
+        for (; w < nw; w += step) t[w] = s[w];
+        if ((d.bytes & 15) && blockIdx.x == 0 && threadIdx.x == 0)
+            reinterpret_cast<double*>(d.dst)[2 * nw] = reinterpret_cast<const double*>(d.src)[2 * nw];
+    }
+    long long cnt = 0;
+    for (long long t0 = (long long)blockIdx.x * kPushThreads; t0 < nw; t0 += step)
+        cnt += nw - t0 < kPushThreads ? nw - t0 : kPushThreads;
+    cnt <<= 4;
+    if (blockIdx.x == 0) cnt += d.bytes & 15;
+    __syncthreads();
+    if (threadIdx.x == 0 && cnt > 0) {
+        __threadfence_system();
+        atomicAdd_system(d.ctr, (unsigned long long)cnt);
+    }
+}
+
+// Spin until the epoch's expected bytes have arrived, then advance the
+// target.  A rank whose peers stop sending fails loudly instead of hanging:
+// after 30 s the solve stops with status 6 (IE_ERR_CUDA "peer exchange
+// timed out").
+__global__ void k_wait(const unsigned long long* ctr, unsigned long long* tgt, unsigned long long expect,
+                       PcgState* s) {
+    if (threadIdx.x != 0 || s->stop) return;
+    const unsigned long long target = *tgt + expect;
+    unsigned long long t0, t1, v;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    for (;;) {
+        asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(ctr) : "memory");
+        if (v >= target) break;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t1));
+        if (t1 - t0 > 30ull * 1000000000ull) {
+            s->status = 6;
+            s->stop = 1;
+            return;
+        }
+        __nanosleep(32);
+    }
+    *tgt = target;
+}
+
+__global__ void k_clear_stop(PcgState* s) {
+    s->stop = 0;
+    s->status = 0;
+}
 }  // namespace ie
 
-#define IE_NCCL(call)                                                          \
-    do {                                                                       \
-        ncclResult_t _r = (call);                                              \
-        if (_r != ncclSuccess) {                                               \
-            ie::set_error(std::string("nccl: ") + ncclGetErrorString(_r));     \
-            return IE_ERR_CUDA;                                                \
-        }                                                                      \
-    } while (0)
+struct ie_shard {
+    int G = 1, g = 0;
+    const ie_matvec* A = nullptr;
+    const ie_precond* T = nullptr;
+    const ie_fft* F = nullptr;
+    uint64_t key_a = 0, key_t = 0;
+    int n = 0, M = 0, Mc = 0, N = 0;
+    int64_t b0 = 0, b1 = 0, nb = 0;
+    int nrows = 0, row0 = 0, rlo = 0, rhi = 0, R = 0, Rmax = 0;
+    int nch = 0, nchb = 0, c0 = 0;
+    std::vector<int> row0_all, nrows_all, rlo_all, rhi_all;
+    // symmetric exchange heap (IPC-exported): mailbox counters, F partials,
+    // POST partials, RZ records, column slab, need-row block
+    char* heap = nullptr;
+    size_t heap_bytes = 0, off_xf = 0, off_xpost = 0, off_xrz = 0, off_buf2 = 0, off_buf3 = 0;
+    std::vector<char*> peer;
+    std::vector<bool> opened;
+    bool connected = false, broken = false;
+    // rank-local
+    double *PU = nullptr, *QW = nullptr, *rfull = nullptr, *z = nullptr, *fb = nullptr, *pmax = nullptr;
+    double* dh = nullptr;
+    int64_t cap = 0;
+    double2* buf1 = nullptr;
+    unsigned long long* tgt = nullptr;
+    ie::PcgState* S = nullptr;
+    ie::PcgState* host = nullptr;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    // the captured steady-state iteration (this rank alone, or -- local
+    // mode -- all ranks of the process, owned by rank 0's shard)
+    cudaGraphExec_t gexec = nullptr;
+    cudaStream_t cap_s = nullptr;
+    int gnodes = 0, gmode = 0;
 
-extern "C" int64_t ie_comm_id_bytes(void) { return (int64_t)sizeof(ncclUniqueId); }
+    unsigned long long* mb(int h) const { return reinterpret_cast<unsigned long long*>(peer[h]); }
+    double* xf(int h) const { return reinterpret_cast<double*>(peer[h] + off_xf); }
+    double* xpost(int h) const { return reinterpret_cast<double*>(peer[h] + off_xpost); }
+    double* xrz(int h) const { return reinterpret_cast<double*>(peer[h] + off_xrz); }
+    double2* buf2(int h) const { return reinterpret_cast<double2*>(peer[h] + off_buf2); }
+    double2* buf3(int h) const { return reinterpret_cast<double2*>(peer[h] + off_buf3); }
+    ~ie_shard() {
+        for (int h = 0; h < (int)peer.size(); ++h)
+            if (h < (int)opened.size() && opened[h]) cudaIpcCloseMemHandle(peer[h]);
+        for (void* p : {(void*)heap, (void*)PU, (void*)QW, (void*)rfull, (void*)z, (void*)fb, (void*)pmax, (void*)dh,
+                        (void*)buf1, (void*)tgt, (void*)S})
+            if (p) cudaFree(p);
+        if (host) cudaFreeHost(host);
+        for (auto e : ev)
+            if (e) cudaEventDestroy(e);
+        if (gexec) cudaGraphExecDestroy(gexec);
+        if (cap_s) cudaStreamDestroy(cap_s);
+    }
+};
 
-extern "C" int ie_comm_unique_id(void* out) {
-    if (!out) return IE_ERR_ARG;
-    ncclUniqueId id;
-    IE_NCCL(ncclGetUniqueId(&id));
-    memcpy(out, &id, sizeof(id));
+namespace ie {
+static size_t align256(size_t x) { return (x + 255) / 256 * 256; }
+
+static int shard_push(const ie_shard* sh, int slot, const PushDesc* d, int nd, cudaStream_t s) {
+    if (sh->G == 1 || nd == 0) return IE_OK;
+    PushArgs a{};
+    long long mx = 0;
+    for (int i = 0; i < nd; ++i) {
+        a.d[i] = d[i];
+        a.d[i].ctr = sh->mb(i) + slot;
+        mx = std::max(mx, d[i].bytes);
+    }
+    a.stop = &sh->S->stop;
+    const long long tiles = (mx / 16 + kPushThreads - 1) / kPushThreads;  // (>= 1 CTA even for an 8-B slab)
+    const unsigned gx = (unsigned)std::max(1LL, std::min(tiles / 2, 64LL));
+    IE_CUDA(launch_k(k_push, dim3(gx, nd), dim3(kPushThreads), 0, s, a));
+    IE_LAUNCHED();
     return IE_OK;
 }
 
-extern "C" int ie_comm_create(const void* id, int32_t nranks, int32_t rank, ie_comm** out) {
-    if (!id || !out || nranks < 1 || rank < 0 || rank >= nranks) {
-        ie::set_error("ie_comm_create: bad arguments");
-        return IE_ERR_ARG;
-    }
-    ncclUniqueId uid;
-    memcpy(&uid, id, sizeof(uid));
-    ie_comm* c = new ie_comm();
-    c->nranks = nranks;
-    c->rank = rank;
-    ncclResult_t r = ncclCommInitRank(&c->c, nranks, uid, rank);
-    if (r != ncclSuccess) {
-        ie::set_error(std::string("ncclCommInitRank: ") + ncclGetErrorString(r));
-        delete c;
-        return IE_ERR_CUDA;
-    }
-    *out = c;
+static int shard_wait(const ie_shard* sh, int slot, unsigned long long expect, cudaStream_t s) {
+    if (sh->G == 1) return IE_OK;
+    k_wait<<<1, 32, 0, s>>>(sh->mb(sh->g) + slot, sh->tgt + slot, expect, sh->S);
+    IE_LAUNCHED();
     return IE_OK;
 }
 
-extern "C" void ie_comm_destroy(ie_comm* c) {
-    if (!c) return;
-    delete c->work;
-    ncclCommDestroy(c->c);
-    delete c;
+// the rank's slab of a chunk-indexed exchange array, pushed to every rank
+static int shard_push_chunks(const ie_shard* sh, int slot, double* (ie_shard::*arr)(int) const, int per,
+                             cudaStream_t s) {
+    PushDesc d[kMaxRanks];
+    const size_t off = (size_t)sh->c0 * per;
+    for (int h = 0; h < sh->G; ++h)
+        d[h] = PushDesc{(const char*)((sh->*arr)(sh->g) + off), (char*)((sh->*arr)(h) + off),
+                        (long long)sh->nchb * per * 8, nullptr};
+    return shard_push(sh, slot, d, sh->G, s);
 }
 
-extern "C" int ie_pcg_sharded_f64(const ie_matvec* A, const ie_precond* T, ie_comm* comm, const int64_t* bounds,
-                                  const int64_t* need, const double* f_band, double* u_band, double tol,
-                                  int64_t max_iters, double* hist, int64_t* n_it, int32_t* flags, double* times,
-                                  int64_t* fail_iter, double* fail_value, void* stream) {
-    using namespace ie;
-    if (!A || !comm || !bounds || !f_band || !u_band || !hist || !n_it || !flags || !times || max_iters < 0 ||
-        !(tol > 0.0 && tol < 1.0)) {
-        set_error("ie_pcg_sharded_f64: bad arguments");
-        return IE_ERR_ARG;
+static inline double* q_band(const ie_shard* sh) { return sh->QW + (size_t)(sh->row0 - sh->rlo) * sh->n; }
+static inline double* w_band(const ie_shard* sh) {
+    return sh->QW + (size_t)sh->R * sh->n + (size_t)(sh->row0 - sh->rlo) * sh->n;
+}
+
+// Setup phases (pcg.py:72-91): 0 = ||f|| partials out, 1 = init + first
+// apply, record out, 2 = rho_0, p = z_0.
+static int shard_setup_phase(ie_shard* sh, int ph, const double* f_need, double tol, int64_t max_iters,
+                             cudaStream_t s, bool timed) {
+    const int* stop = &sh->S->stop;
+    const int nch = sh->nch, nchb = sh->nchb, c0 = sh->c0, n = sh->n;
+    double* r = sh->rfull + sh->b0;
+    if (ph == 0) {
+        k_clear_stop<<<1, 1, 0, s>>>(sh->S);
+        IE_LAUNCHED();
+        IE_CUDA(cudaMemcpyAsync(sh->rfull + (size_t)sh->rlo * n, f_need, (size_t)sh->R * n * 8,
+                                cudaMemcpyDeviceToDevice, s));
+        IE_CUDA(cudaMemcpyAsync(sh->fb, f_need + (size_t)(sh->row0 - sh->rlo) * n, sh->nb * 8,
+                                cudaMemcpyDeviceToDevice, s));
+        k_dot_partials<<<nchb, kRed, 0, s>>>(sh->fb, sh->fb, (int)sh->nb, 0, sh->xf(sh->g) + c0);
+        IE_LAUNCHED();
+        return shard_push_chunks(sh, kSlotF, &ie_shard::xf, 1, s);
     }
-    const ie_fft* F = matvec_fft(A);
-    const int G = comm->nranks, g = comm->rank;
-    const int N = matvec_N(A), n = matvec_n(A), M = 2 * n;
-    const int64_t nb = bounds[g + 1] - bounds[g];
-    bool ok = F && matvec_dim(A) == 2 && M % G == 0 && (((M / G) & (M / G - 1)) == 0) && bounds[0] == 0 &&
-              bounds[G] == N;
-    for (int h = 0; h < G && ok; ++h)
-        ok = (bounds[h + 1] - bounds[h] == nb) && (bounds[h] % kChunk == 0) && (bounds[h] % n == 0);
-    if (!ok || nb <= 0 || nb % kChunk) {
-        set_error("ie_pcg_sharded_f64: needs the 2D FFT operator, G | 2n (power-of-two slabs) and equal, "
-                  "chunk-aligned bands of whole grid rows");
-        return IE_ERR_ARG;
+    if (ph == 1) {
+        int rc = shard_wait(sh, kSlotF, (unsigned long long)nch * 8, s);
+        if (rc) return rc;
+        k_pcg_init<<<1, kRed, 0, s>>>(sh->xf(sh->g), nch, sh->S, tol, max_iters, sh->dh);
+        IE_LAUNCHED();
+        IE_CUDA(cudaMemsetAsync(sh->PU + sh->nb, 0, sh->nb * 8, s));
+        if (timed) IE_CUDA(cudaEventRecord(sh->ev[0], s));
+        if (sh->T) {
+            if ((rc = precond_apply_band(sh->T, sh->rfull, sh->z, sh->xrz(sh->g) + kRzRec * c0, sh->b0, sh->b1, s,
+                                         stop)))
+                return rc;
+        } else {
+            k_identity_apply<<<nchb, kRed, 0, s>>>(r, sh->z, (int)sh->nb, sh->xrz(sh->g) + kRzRec * c0, stop);
+            IE_LAUNCHED();
+        }
+        if (timed) IE_CUDA(cudaEventRecord(sh->ev[1], s));
+        return shard_push_chunks(sh, kSlotRz, &ie_shard::xrz, kRzRec, s);
     }
-    cudaStream_t st = (cudaStream_t)stream;
+    int rc = shard_wait(sh, kSlotRz, (unsigned long long)nch * kRzRec * 8, s);
+    if (rc) return rc;
+    k_pcg_setup<<<nchb, kRed, 0, s>>>(sh->xrz(sh->g), nch, sh->S, sh->PU, sh->z, (int)sh->nb, c0, sh->pmax);
+    IE_LAUNCHED();
+    return IE_OK;
+}
+
+constexpr int kIterPhases = 5;
+
+// Iteration phases of iteration `itarg` (< 0: graph replay, read from the
+// state): 0 = row transforms, FWD out; 1 = column pass, BACK out; 2 = inverse
+// rows of the need rows, POST out; 3 = control + r, u updates (+ halo r),
+// apply, RZ out; 4 = beta, p, next scales.
+static int shard_iter_phase(ie_shard* sh, int ph, int64_t itarg, int do_p, int pending, bool spec, cudaStream_t s,
+                            bool timed) {
+    const int* stop = &sh->S->stop;
+    const int G = sh->G, g = sh->g, n = sh->n, Mc = sh->Mc, nch = sh->nch, nchb = sh->nchb, c0 = sh->c0;
+    double* p = sh->PU;
+    double* uu = sh->PU + sh->nb;
+    double* r = sh->rfull + sh->b0;
+    double2* b1 = G == 1 ? sh->buf2(g) : sh->buf1;
+    double2* b3 = G == 1 ? sh->buf2(g) : sh->buf3(g);
+    const bool two = do_p && pending;
+    int rc;
+    switch (ph) {
+        case 0: {
+            const double* X0 = do_p ? p : uu;
+            if ((rc = fft_band_fwd(sh->F, X0, two ? uu : nullptr, sh->nrows, G, b1, two ? sh->S->sc : nullptr, s,
+                                   stop)))
+                return rc;
+            PushDesc d[kMaxRanks];
+            for (int h = 0; h < G; ++h)
+                d[h] = PushDesc{(const char*)(b1 + (size_t)h * sh->nrows * Mc),
+                                (char*)(sh->buf2(h) + (size_t)sh->row0 * Mc), (long long)sh->nrows * Mc * 16, nullptr};
+            return shard_push(sh, kSlotFwd, d, G, s);
+        }
+        case 1: {
+            if ((rc = shard_wait(sh, kSlotFwd, (unsigned long long)n * Mc * 16, s))) return rc;
+            if ((rc = fft_band_cols(sh->F, sh->buf2(g), g * Mc, Mc, s, stop))) return rc;
+            PushDesc d[kMaxRanks];
+            for (int h = 0; h < G; ++h) {
+                const int Rh = sh->rhi_all[h] - sh->rlo_all[h];
+                d[h] = PushDesc{(const char*)(sh->buf2(g) + (size_t)sh->rlo_all[h] * Mc),
+                                (char*)(sh->buf3(h) + (size_t)g * Rh * Mc), (long long)Rh * Mc * 16, nullptr};
+            }
+            return shard_push(sh, kSlotBack, d, G, s);
+        }
+        case 2: {
+            if ((rc = shard_wait(sh, kSlotBack, (unsigned long long)G * sh->R * Mc * 16, s))) return rc;
+            double* Y0 = do_p ? sh->QW : sh->QW + (size_t)sh->R * n;
+            double* Y1 = two ? sh->QW + (size_t)sh->R * n : nullptr;
+            if ((rc = fft_band_inv(sh->F, b3, sh->R, G, Y0, Y1, two ? sh->S->sc : nullptr, s, stop))) return rc;
+            IE_CUDA(launch_k(k_post_pass, dim3(nchb), dim3(kRed), 0, s, (const double*)p, (const double*)q_band(sh),
+                             (const double*)sh->fb, (const double*)w_band(sh), (int)sh->nb, do_p, pending,
+                             sh->xpost(g) + 2 * c0, stop));
+            IE_LAUNCHED();
+            return shard_push_chunks(sh, kSlotPost, &ie_shard::xpost, 2, s);
+        }
+        case 3: {
+            if ((rc = shard_wait(sh, kSlotPost, (unsigned long long)nch * 16, s))) return rc;
+            const HaloSeg hs{(sh->rlo - sh->row0) * n, (sh->row0 - sh->rlo) * n, (int)sh->nb,
+                             (sh->rhi - sh->row0 - sh->nrows) * n};
+            const int nh = (hs.len0 + kChunk - 1) / kChunk + (hs.len1 + kChunk - 1) / kChunk;
+            IE_CUDA(launch_k(k_iter_a<true, true>, dim3(nchb + nh), dim3(kRed), 0, s, (const double*)sh->xpost(g), nch,
+                             do_p, pending, (long long)itarg, sh->S, sh->dh, uu, r, (const double*)p,
+                             (const double*)q_band(sh), (int)sh->nb, c0, nchb, sh->xrz(g), (const double*)sh->pmax,
+                             hs));
+            IE_LAUNCHED();
+            if (!spec) return IE_OK;
+            if (timed) IE_CUDA(cudaEventRecord(sh->ev[2], s));
+            if (sh->T) {
+                if ((rc = precond_apply_band(sh->T, sh->rfull, sh->z, sh->xrz(g) + kRzRec * c0, sh->b0, sh->b1, s,
+                                             stop)))
+                    return rc;
+            } else {
+                k_identity_apply<<<nchb, kRed, 0, s>>>(r, sh->z, (int)sh->nb, sh->xrz(g) + kRzRec * c0, stop);
+                IE_LAUNCHED();
+            }
+            if (timed) IE_CUDA(cudaEventRecord(sh->ev[3], s));
+            return shard_push_chunks(sh, kSlotRz, &ie_shard::xrz, kRzRec, s);
+        }
+        default: {
+            if (!spec) return IE_OK;
+            if ((rc = shard_wait(sh, kSlotRz, (unsigned long long)nch * kRzRec * 8, s))) return rc;
+            IE_CUDA(launch_k(k_iter_b, dim3(nchb), dim3(kRed), 0, s, (const double*)sh->xrz(g), nch,
+                             (long long)itarg, sh->S, p, (const double*)sh->z, (int)sh->nb, sh->pmax));
+            IE_LAUNCHED();
+            return IE_OK;
+        }
+    }
+}
+
+// PCG over the shards of this process (1: one rank per process; G: all ranks
+// on one device), phase-major.
+static int shard_solve(ie_shard* const* shs, int nloc, const double* const* f_need, double* const* u_band, double tol,
+                       int64_t max_iters, double* hist, int64_t* n_it, int32_t* flags, double* times,
+                       int64_t* fail_iter, double* fail_value, cudaStream_t st) {
+    ie_shard* s0 = shs[0];
     const auto t0 = std::chrono::steady_clock::now();
-    const int64_t b0 = bounds[g];
-    const int nrows = (int)(nb / n), Mc = M / G;
-    const int nchb = (int)(nb / kChunk), nch = nchb * G, c0 = (int)(b0 / kChunk);
+    for (int k = 0; k < nloc; ++k)
+        if (!shs[k]->connected || shs[k]->broken) {
+            set_error("ie_pcg_sharded: shard not connected (ie_shard_connect) or broken by an earlier failure");
+            return IE_ERR_ARG;
+        }
     int64_t cap = 1024;
     while (cap < max_iters + 1) cap *= 2;
-    const uint64_t ka = matvec_uid(A), kt = T ? precond_uid(T) : 0;
-    ShardWork* W = comm->work;
-    if (!W || W->key_a != ka || W->key_t != kt || W->nb != nb || W->b0 != b0 || W->cap < cap) {
-        delete W;
-        comm->work = W = new ShardWork();
-        W->key_a = ka;
-        W->key_t = kt;
-        W->nb = nb;
-        W->b0 = b0;
-        W->cap = cap;
-        const bool one = G == 1;  // one rank: the transposes are the identity (buffers aliased)
-        IE_CUDA(cudaMalloc(&W->PU, 2 * nb * 8));
-        IE_CUDA(cudaMalloc(&W->QW, 2 * nb * 8));
-        IE_CUDA(cudaMalloc(&W->rfull, (size_t)N * 8));
-        IE_CUDA(cudaMalloc(&W->z, nb * 8));
-        IE_CUDA(cudaMalloc(&W->fb, nb * 8));
-        IE_CUDA(cudaMalloc(&W->part, 3 * (size_t)nch * 8));
-        IE_CUDA(cudaMalloc(&W->amax, 2 * (size_t)nch * 8));
-        IE_CUDA(cudaMalloc(&W->dh, (size_t)cap * 8));
-        IE_CUDA(cudaMalloc(&W->buf1, (size_t)nrows * M * 16));
-        if (!one) {
-            IE_CUDA(cudaMalloc(&W->buf2, (size_t)n * Mc * 16));
-            IE_CUDA(cudaMalloc(&W->buf3, (size_t)nrows * M * 16));
+    for (int k = 0; k < nloc; ++k) {
+        ie_shard* sh = shs[k];
+        if (sh->cap < cap) {
+            if (sh->dh) cudaFree(sh->dh);
+            IE_CUDA(cudaMalloc(&sh->dh, (size_t)cap * 8));
+            sh->cap = cap;
+            if (s0->gexec) {  // the captured iteration writes the old history buffer
+                cudaGraphExecDestroy(s0->gexec);
+                s0->gexec = nullptr;
+            }
         }
-        IE_CUDA(cudaMalloc(&W->S, sizeof(PcgState)));
-        IE_CUDA(cudaMallocHost(&W->host, sizeof(PcgState)));
     }
     int rc;
-    double *PU = W->PU, *QW = W->QW, *rfull = W->rfull, *z = W->z, *fb = W->fb, *part = W->part;
-    double *amax = W->amax, *dh = W->dh;
-    double2* buf1 = W->buf1;
-    double2* buf2 = G == 1 ? W->buf1 : W->buf2;
-    double2* buf3 = G == 1 ? W->buf1 : W->buf3;
-    PcgState* S = W->S;
-    PcgState* host = W->host;
-    double* p = PU;
-    double* uu = PU + nb;
-    double* q = QW;
-    double* w = QW + nb;
-    double* r = rfull + b0;  // r lives inside the halo buffer
-    double* part_pq = part;
-    double* part_res = part + nch;
-    double* part_rz = part + 2 * nch;
-    const int* stop = &S->stop;
-    const ncclComm_t cc = comm->c;
-    // halo plan: send my band's overlap with each rank's need range, receive theirs with mine
-    std::vector<int64_t> s_off(G, 0), s_cnt(G, 0), r_off(G, 0), r_cnt(G, 0);
-    if (need && T) {
-        const int64_t lo = need[2 * g], hi = need[2 * g + 1];
-        for (int h = 0; h < G; ++h) {
-            if (h == g) continue;
-            const int64_t a = std::max(b0, need[2 * h]), b = std::min(bounds[g + 1], need[2 * h + 1]);
-            if (b > a) s_off[h] = a, s_cnt[h] = b - a;
-            const int64_t a2 = std::max(bounds[h], lo), b2 = std::min(bounds[h + 1], hi);
-            if (b2 > a2) r_off[h] = a2, r_cnt[h] = b2 - a2;
-        }
-    } else if (T) {  // no need ranges: the whole vector
-        for (int h = 0; h < G; ++h)
-            if (h != g) s_off[h] = b0, s_cnt[h] = nb, r_off[h] = bounds[h], r_cnt[h] = bounds[h + 1] - bounds[h];
-    }
-    auto allgather_chunks = [&](double* arr, int per, cudaStream_t s) -> int {  // arr[nch * per], rank slab in place
-        IE_NCCL(ncclAllGather(arr + (size_t)c0 * per, arr, (size_t)nchb * per, ncclDouble, cc, s));
-        return IE_OK;
+    auto fail = [&](int code) {
+        for (int k = 0; k < nloc; ++k) shs[k]->broken = true;
+        return code;
     };
-    auto alltoall = [&](const double2* src, double2* dst, cudaStream_t s) -> int {  // equal blocks of nrows*Mc
-        if (G == 1) return IE_OK;  // identity transpose, aliased buffers
-        const size_t cnt = (size_t)nrows * Mc * 2;
-        IE_NCCL(ncclGroupStart());
-        for (int h = 0; h < G; ++h) {
-            IE_NCCL(ncclSend((const double*)src + h * cnt, cnt, ncclDouble, h, cc, s));
-            IE_NCCL(ncclRecv((double*)dst + h * cnt, cnt, ncclDouble, h, cc, s));
-        }
-        IE_NCCL(ncclGroupEnd());
-        return IE_OK;
-    };
-    auto halo = [&](cudaStream_t s) -> int {
-        bool any = false;
-        for (int h = 0; h < G; ++h) any = any || s_cnt[h] || r_cnt[h];
-        if (!any) return IE_OK;
-        IE_NCCL(ncclGroupStart());
-        for (int h = 0; h < G; ++h) {
-            if (s_cnt[h]) IE_NCCL(ncclSend(rfull + s_off[h], (size_t)s_cnt[h], ncclDouble, h, cc, s));
-            if (r_cnt[h]) IE_NCCL(ncclRecv(rfull + r_off[h], (size_t)r_cnt[h], ncclDouble, h, cc, s));
-        }
-        IE_NCCL(ncclGroupEnd());
-        return IE_OK;
-    };
-    auto matvec = [&](const double* X, int nrhs, double* Y, cudaStream_t s) -> int {
-        int r2;
-        if (nrhs == 2 && (r2 = allgather_chunks(amax, 2, s))) return r2;
-        if ((r2 = fft_band_fwd(F, X, nrhs == 2 ? X + nb : nullptr, nrows, G, buf1, amax, nch, s))) return r2;
-        if ((r2 = alltoall(buf1, buf2, s))) return r2;
-        if ((r2 = fft_band_cols(F, buf2, g * Mc, Mc, s))) return r2;
-        if ((r2 = alltoall(buf2, buf3, s))) return r2;
-        return fft_band_inv(F, buf3, nrows, G, Y, nrhs == 2 ? Y + nb : nullptr, amax, nch, s);
-    };
-    auto apply = [&](cudaStream_t s) -> int {  // z (band) and part_rz (rank slab) from r
-        int r2;
-        if (T) {
-            if ((r2 = halo(s))) return r2;
-            if ((r2 = precond_apply_band(T, rfull, z, part_rz + c0, b0, b0 + nb, s, stop))) return r2;
-        } else {
-            k_copy_if_running<<<g1(nb), 256, 0, s>>>(z, r, (int)nb, stop);
-            IE_LAUNCHED();
-            k_dot_partials<<<nchb, kRed, 0, s>>>(r, z, (int)nb, 0, part_rz + c0);
-            IE_LAUNCHED();
-        }
-        return allgather_chunks(part_rz, 1, s);
-    };
-    // ||f||, init (pcg.py:72-91)
-    IE_CUDA(cudaMemcpyAsync(fb, f_band, nb * 8, cudaMemcpyDeviceToDevice, st));
-    k_dot_partials<<<nchb, kRed, 0, st>>>(fb, fb, (int)nb, 0, part_pq + c0);
-    IE_LAUNCHED();
-    if ((rc = allgather_chunks(part_pq, 1, st))) return rc;
-    k_pcg_init<<<1, kRed, 0, st>>>(part_pq, nch, S, tol, max_iters, dh);
-    IE_LAUNCHED();
-    IE_CUDA(cudaMemsetAsync(uu, 0, nb * 8, st));
-    IE_CUDA(cudaMemsetAsync(amax, 0, 2 * (size_t)nch * 8, st));
-    IE_CUDA(cudaMemcpyAsync(r, fb, nb * 8, cudaMemcpyDeviceToDevice, st));
-    if ((rc = apply(st))) return rc;
-    IE_CUDA(cudaMemcpyAsync(p, z, nb * 8, cudaMemcpyDeviceToDevice, st));
-    k_pcg_rho0<<<1, kRed, 0, st>>>(part_rz, nch, S);
-    IE_LAUNCHED();
-    // (the first 2-RHS pass, iteration 2, uses max|u| from k_iter_a and max|p|
-    // from k_iter_b of iteration 1, as in ie_pcg_f64)
-    auto enqueue_iter = [&](int64_t itarg, int do_p, int pending, bool spec, cudaStream_t s) -> int {
-        int r2;
-        if (do_p && pending) r2 = matvec(PU, 2, QW, s);
-        else if (do_p) r2 = matvec(p, 1, q, s);
-        else r2 = matvec(uu, 1, w, s);
-        if (r2) return r2;
-        k_post_pass<<<nchb, kRed, 0, s>>>(p, q, fb, w, (int)nb, do_p, pending, part_pq + c0, part_res + c0, stop);
-        IE_LAUNCHED();
-        if (do_p && (r2 = allgather_chunks(part_pq, 1, s))) return r2;
-        if (pending && (r2 = allgather_chunks(part_res, 1, s))) return r2;
-        (uu ? k_iter_a<true> : k_iter_a<false>)<<<nchb, kRed, 0, s>>>(part_pq, part_res, nch, do_p, pending, itarg, S, dh, uu, r, p, q, (int)nb,
-                                       amax + 2 * (size_t)c0);
-        IE_LAUNCHED();
-        if (spec) {
-            if ((r2 = apply(s))) return r2;
-            k_iter_b<<<nchb, kRed, 0, s>>>(part_rz, nch, itarg, S, p, z, (int)nb, amax + 2 * (size_t)c0);
-            IE_LAUNCHED();
-        }
+    for (int ph = 0; ph < 3; ++ph)
+        for (int k = 0; k < nloc; ++k)
+            if ((rc = shard_setup_phase(shs[k], ph, f_need[k], tol, max_iters, st, k == 0))) return fail(rc);
+    auto enqueue = [&](int64_t itarg, int do_p, int pending, bool spec, cudaStream_t s, bool timed) -> int {
+        for (int ph = 0; ph < kIterPhases; ++ph)
+            for (int k = 0; k < nloc; ++k) {
+                int r2 = shard_iter_phase(shs[k], ph, itarg, do_p, pending, spec, s, timed && k == 0);
+                if (r2) return r2;
+            }
         return IE_OK;
     };
     const bool use_graph = max_iters >= 3 && !getenv("IEDD_B200_NO_GRAPH");
-    if (use_graph && !W->gexec) {
-        if (!W->cap_s) IE_CUDA(cudaStreamCreateWithFlags(&W->cap_s, cudaStreamNonBlocking));
-        cudaStream_t cap_s = W->cap_s;
-        // order the capture stream after the setup work on st
+    if (use_graph && (!s0->gexec || s0->gmode != nloc)) {
+        if (s0->gexec) cudaGraphExecDestroy(s0->gexec);
+        s0->gexec = nullptr;
+        if (!s0->cap_s) IE_CUDA(cudaStreamCreateWithFlags(&s0->cap_s, cudaStreamNonBlocking));
+        for (int k = 0; k < nloc; ++k)
+            if (shs[k]->T && (rc = precond_prepare_stream(shs[k]->T, s0->cap_s))) return fail(rc);
         cudaEvent_t ev;
         IE_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
         IE_CUDA(cudaEventRecord(ev, st));
-        IE_CUDA(cudaStreamWaitEvent(cap_s, ev, 0));
+        IE_CUDA(cudaStreamWaitEvent(s0->cap_s, ev, 0));
         cudaEventDestroy(ev);
-        if (T && (rc = precond_prepare_stream(T, cap_s))) return rc;
         cudaGraph_t gr;
-        IE_CUDA(cudaStreamBeginCapture(cap_s, cudaStreamCaptureModeThreadLocal));
-        int r2 = enqueue_iter(-1, 1, 1, true, cap_s);  // k_iter_b advances it_dev
-        cudaError_t ce = cudaStreamEndCapture(cap_s, &gr);
-        if (r2) return r2;
+        IE_CUDA(cudaStreamBeginCapture(s0->cap_s, cudaStreamCaptureModeThreadLocal));
+        int r2 = enqueue(-1, 1, 1, true, s0->cap_s, false);  // k_iter_b advances it_dev
+        cudaError_t ce = cudaStreamEndCapture(s0->cap_s, &gr);
+        if (r2) return fail(r2);
         IE_CUDA(ce);
         size_t nn = 0;
         cudaGraphGetNodes(gr, nullptr, &nn);
         std::vector<cudaGraphNode_t> nodes(nn);
         if (nn) cudaGraphGetNodes(gr, nodes.data(), &nn);
-        W->gnodes = 0;
+        s0->gnodes = 0;
         for (auto nd : nodes) {
             cudaGraphNodeType t;
-            if (cudaGraphNodeGetType(nd, &t) == cudaSuccess && t == cudaGraphNodeTypeKernel) ++W->gnodes;
+            if (cudaGraphNodeGetType(nd, &t) == cudaSuccess && t == cudaGraphNodeTypeKernel) ++s0->gnodes;
         }
-        ce = cudaGraphInstantiate(&W->gexec, gr, 0);
+        ce = cudaGraphInstantiate(&s0->gexec, gr, 0);
         cudaGraphDestroy(gr);
         IE_CUDA(ce);
+        s0->gmode = nloc;
     }
-    cudaGraphExec_t gexec = W->gexec;
-    const int gnodes = W->gnodes;
-    static const int64_t kBatch = getenv("IEDD_B200_PCG_BATCH") ? atoll(getenv("IEDD_B200_PCG_BATCH")) : 4;
+    static const int64_t kBatch = [] {
+        const char* e = getenv("IEDD_B200_PCG_BATCH");
+        const long long v = e ? atoll(e) : 4;
+        return (int64_t)std::max(1LL, std::min(v, 1024LL));
+    }();
     for (int64_t it = 1; it <= max_iters + 1; ++it) {
         const int do_p = it <= max_iters;
         const int pending = it >= 2;
         const bool spec = do_p && it < max_iters;
         if (use_graph && pending && spec) {
-            if (it == 2) {
-                k_set_it<<<1, 1, 0, st>>>(S, 2);
-                IE_LAUNCHED();
-            }
-            IE_CUDA(cudaGraphLaunch(gexec, st));
-            g_launches.fetch_add(gnodes, std::memory_order_relaxed);
-        } else if ((rc = enqueue_iter(it, do_p, pending, spec, st))) {
-            return rc;
+            if (it == 2)
+                for (int k = 0; k < nloc; ++k) {
+                    k_set_it<<<1, 1, 0, st>>>(shs[k]->S, 2);
+                    IE_LAUNCHED();
+                }
+            IE_CUDA(cudaGraphLaunch(s0->gexec, st));
+            g_launches.fetch_add(s0->gnodes, std::memory_order_relaxed);
+        } else if ((rc = enqueue(it, do_p, pending, spec, st, it == 1))) {
+            return fail(rc);
         }
         if (it % kBatch == 0 || it == max_iters + 1) {
-            IE_CUDA(cudaMemcpyAsync(host, S, sizeof(PcgState), cudaMemcpyDeviceToHost, st));
+            IE_CUDA(cudaMemcpyAsync(s0->host, s0->S, sizeof(PcgState), cudaMemcpyDeviceToHost, st));
             IE_CUDA(cudaStreamSynchronize(st));
-            if (host->stop) break;
+            if (s0->host->stop) break;
         }
     }
-    IE_CUDA(cudaMemcpyAsync(host, S, sizeof(PcgState), cudaMemcpyDeviceToHost, st));
+    IE_CUDA(cudaMemcpyAsync(s0->host, s0->S, sizeof(PcgState), cudaMemcpyDeviceToHost, st));
     IE_CUDA(cudaStreamSynchronize(st));
-    const PcgState H = *host;
+    const PcgState H = *s0->host;
+    if (H.status == 6) {
+        fail(0);
+        set_error("ie_pcg_sharded: peer exchange timed out (a rank stopped sending)");
+        return IE_ERR_CUDA;
+    }
     flags[0] = H.status == 1;
     flags[1] = H.status == 2;
     *n_it = H.n_it;
@@ -1477,13 +1748,201 @@ extern "C" int ie_pcg_sharded_f64(const ie_matvec* A, const ie_precond* T, ie_co
         if (fail_iter) *fail_iter = H.fail_iter;
         if (fail_value) *fail_value = H.fail_value;
     }
-    IE_CUDA(cudaMemcpyAsync(hist, dh, (size_t)(H.n_it + 1) * 8, cudaMemcpyDeviceToHost, st));
-    IE_CUDA(cudaMemcpyAsync(u_band, uu, nb * 8, cudaMemcpyDeviceToDevice, st));
+    IE_CUDA(cudaMemcpyAsync(hist, s0->dh, (size_t)(H.n_it + 1) * 8, cudaMemcpyDeviceToHost, st));
+    for (int k = 0; k < nloc; ++k)
+        IE_CUDA(cudaMemcpyAsync(u_band[k], shs[k]->PU + shs[k]->nb, shs[k]->nb * 8, cudaMemcpyDeviceToDevice, st));
     IE_CUDA(cudaStreamSynchronize(st));
     times[0] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
-    times[1] = 0.0;
-    if (H.nf == 0.0) times[0] = 0.0;
+    // t_s: mean device time of rank 0's event-timed applies (the initial one and iteration 1's)
+    double tp = 0.0;
+    int np = 0;
+    for (int e = 0; e < 2; ++e) {
+        if (e == 1 && (H.n_it < 2 || max_iters < 2)) break;
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, s0->ev[2 * e], s0->ev[2 * e + 1]) == cudaSuccess) tp += ms * 1e-3, ++np;
+    }
+    cudaGetLastError();
+    times[1] = np ? tp / np : 0.0;
+    if (H.nf == 0.0) times[0] = times[1] = 0.0;
     if (H.status == 4) return IE_ERR_BREAKDOWN;
     if (H.status == 5) return IE_ERR_NONFINITE;
     return IE_OK;
+}
+}  // namespace ie
+
+extern "C" int ie_shard_create(const ie_matvec* A, const ie_precond* T_local, int32_t nranks, int32_t rank,
+                               const int64_t* h_bounds, const int64_t* h_need, ie_shard** out) {
+    using namespace ie;
+    if (!A || !h_bounds || !out || nranks < 1 || nranks > kMaxRanks || rank < 0 || rank >= nranks) {
+        set_error("ie_shard_create: bad arguments");
+        return IE_ERR_ARG;
+    }
+    const ie_fft* F = matvec_fft(A);
+    const int G = nranks, g = rank;
+    const int N = matvec_N(A), n = matvec_n(A), M = F ? fft_M(F) : 0;
+    const int64_t nb = h_bounds[1] - h_bounds[0];
+    bool ok = F && matvec_dim(A) == 2 && M % G == 0 && (((M / G) & (M / G - 1)) == 0) && h_bounds[0] == 0 &&
+              h_bounds[G] == N && nb > 0 && nb % kChunk == 0;
+    for (int h = 0; h < G && ok; ++h) ok = h_bounds[h + 1] - h_bounds[h] == nb && h_bounds[h] % n == 0;
+    if (!ok) {
+        set_error("ie_shard_create: needs the 2D FFT operator, G | M (the circulant size; power-of-two "
+                  "slabs) and equal, chunk-aligned bands of whole grid rows");
+        return IE_ERR_ARG;
+    }
+    ie_shard* sh = new ie_shard();
+    std::unique_ptr<ie_shard> guard(sh);
+    sh->G = G;
+    sh->g = g;
+    sh->A = A;
+    sh->T = T_local;
+    sh->F = F;
+    sh->n = n;
+    sh->M = M;
+    sh->Mc = M / G;
+    sh->N = N;
+    for (int h = 0; h < G; ++h) {
+        const int r0 = (int)(h_bounds[h] / n), r1 = (int)(h_bounds[h + 1] / n);
+        int lo = r0, hi = r1;
+        if (h_need && T_local) {  // need rows: the point range the rank's subdomains read, in whole rows
+            lo = std::min(lo, (int)(h_need[2 * h] / n));
+            hi = std::max(hi, (int)((h_need[2 * h + 1] + n - 1) / n));
+        }
+        sh->row0_all.push_back(r0);
+        sh->nrows_all.push_back(r1 - r0);
+        sh->rlo_all.push_back(std::max(0, lo));
+        sh->rhi_all.push_back(std::min(n, hi));
+        sh->Rmax = std::max(sh->Rmax, sh->rhi_all[h] - sh->rlo_all[h]);
+    }
+    sh->b0 = h_bounds[g];
+    sh->b1 = h_bounds[g + 1];
+    sh->nb = nb;
+    sh->row0 = sh->row0_all[g];
+    sh->nrows = sh->nrows_all[g];
+    sh->rlo = sh->rlo_all[g];
+    sh->rhi = sh->rhi_all[g];
+    sh->R = sh->rhi - sh->rlo;
+    sh->nchb = (int)(nb / kChunk);
+    sh->nch = sh->nchb * G;
+    sh->c0 = (int)(sh->b0 / kChunk);
+    size_t o = align256(kNumSlots * sizeof(unsigned long long));
+    sh->off_xf = o;
+    o = align256(o + (size_t)sh->nch * 8);
+    sh->off_xpost = o;
+    o = align256(o + (size_t)sh->nch * 16);
+    sh->off_xrz = o;
+    o = align256(o + (size_t)sh->nch * kRzRec * 8);
+    sh->off_buf2 = o;
+    o = align256(o + (size_t)n * sh->Mc * 16);
+    sh->off_buf3 = o;
+    if (G > 1) o = align256(o + (size_t)G * sh->Rmax * sh->Mc * 16);
+    sh->heap_bytes = o;
+    IE_CUDA(cudaMalloc(&sh->heap, sh->heap_bytes));
+    IE_CUDA(cudaMemset(sh->heap, 0, kNumSlots * sizeof(unsigned long long)));
+    IE_CUDA(cudaMalloc(&sh->PU, 2 * nb * 8));
+    IE_CUDA(cudaMalloc(&sh->QW, 2 * (size_t)sh->R * n * 8));
+    IE_CUDA(cudaMalloc(&sh->rfull, (size_t)N * 8));
+    IE_CUDA(cudaMalloc(&sh->z, nb * 8));
+    IE_CUDA(cudaMalloc(&sh->fb, nb * 8));
+    IE_CUDA(cudaMalloc(&sh->pmax, (size_t)sh->nchb * 8));
+    if (G > 1) IE_CUDA(cudaMalloc(&sh->buf1, (size_t)sh->nrows * M * 16));
+    IE_CUDA(cudaMalloc(&sh->tgt, kNumSlots * sizeof(unsigned long long)));
+    IE_CUDA(cudaMemset(sh->tgt, 0, kNumSlots * sizeof(unsigned long long)));
+    IE_CUDA(cudaMalloc(&sh->S, sizeof(PcgState)));
+    IE_CUDA(cudaMemset(sh->S, 0, sizeof(PcgState)));
+    IE_CUDA(cudaMallocHost(&sh->host, sizeof(PcgState)));
+    for (auto& e : sh->ev) IE_CUDA(cudaEventCreate(&e));
+    IE_CUDA(cudaDeviceSynchronize());
+    sh->peer.assign(G, nullptr);
+    sh->opened.assign(G, false);
+    sh->peer[g] = sh->heap;
+    sh->connected = G == 1;
+    *out = guard.release();
+    return IE_OK;
+}
+
+extern "C" void ie_shard_destroy(ie_shard* s) { delete s; }
+
+extern "C" int64_t ie_shard_handle_bytes(void) { return (int64_t)sizeof(cudaIpcMemHandle_t); }
+
+extern "C" int ie_shard_need_rows(const ie_shard* s, int64_t* out2) {
+    if (!s || !out2) return IE_ERR_ARG;
+    out2[0] = (int64_t)s->rlo * s->n;
+    out2[1] = (int64_t)s->rhi * s->n;
+    return IE_OK;
+}
+
+extern "C" int ie_shard_export(const ie_shard* s, void* h_out) {
+    if (!s || !h_out) return IE_ERR_ARG;
+    cudaIpcMemHandle_t h;
+    IE_CUDA(cudaIpcGetMemHandle(&h, s->heap));
+    memcpy(h_out, &h, sizeof(h));
+    return IE_OK;
+}
+
+extern "C" int ie_shard_connect(ie_shard* s, const void* h_handles) {
+    if (!s || !h_handles) return IE_ERR_ARG;
+    const char* base = (const char*)h_handles;
+    for (int h = 0; h < s->G; ++h) {
+        if (h == s->g) continue;
+        cudaIpcMemHandle_t hd;
+        memcpy(&hd, base + (size_t)h * sizeof(hd), sizeof(hd));
+        void* p = nullptr;
+        cudaError_t e = cudaIpcOpenMemHandle(&p, hd, cudaIpcMemLazyEnablePeerAccess);
+        if (e != cudaSuccess) {
+            ie::set_error(std::string("ie_shard_connect: cudaIpcOpenMemHandle(rank ") + std::to_string(h) +
+                          "): " + cudaGetErrorString(e) + " (no NVLink/P2P path: use the torch.distributed driver)");
+            return IE_ERR_CUDA;
+        }
+        s->peer[h] = (char*)p;
+        s->opened[h] = true;
+    }
+    s->connected = true;
+    return IE_OK;
+}
+
+extern "C" int ie_shard_connect_local(ie_shard** shards, int32_t nranks) {
+    if (!shards || nranks < 1) return IE_ERR_ARG;
+    for (int k = 0; k < nranks; ++k)
+        if (!shards[k] || shards[k]->G != nranks || shards[k]->g != k) {
+            ie::set_error("ie_shard_connect_local: shards must be ranks 0..G-1 of one G-rank plan");
+            return IE_ERR_ARG;
+        }
+    for (int k = 0; k < nranks; ++k) {
+        for (int h = 0; h < nranks; ++h) shards[k]->peer[h] = shards[h]->heap;
+        shards[k]->connected = true;
+    }
+    return IE_OK;
+}
+
+extern "C" int ie_pcg_sharded_f64(ie_shard* s, const double* d_f_need, double* d_u_band, double tol,
+                                  int64_t max_iters, double* hist, int64_t* n_it, int32_t* flags, double* times,
+                                  int64_t* fail_iter, double* fail_value, void* stream) {
+    if (!s || !d_f_need || !d_u_band || !hist || !n_it || !flags || !times || max_iters < 0 ||
+        !(tol > 0.0 && tol < 1.0)) {
+        ie::set_error("ie_pcg_sharded_f64: bad arguments");
+        return IE_ERR_ARG;
+    }
+    ie_shard* one[1] = {s};
+    const double* f1[1] = {d_f_need};
+    double* u1[1] = {d_u_band};
+    return ie::shard_solve(one, 1, f1, u1, tol, max_iters, hist, n_it, flags, times, fail_iter, fail_value,
+                           (cudaStream_t)stream);
+}
+
+extern "C" int ie_pcg_sharded_local_f64(ie_shard** shards, int32_t nranks, const double* const* d_f_need,
+                                        double* const* d_u_band, double tol, int64_t max_iters, double* hist,
+                                        int64_t* n_it, int32_t* flags, double* times, int64_t* fail_iter,
+                                        double* fail_value, void* stream) {
+    if (!shards || nranks < 1 || !d_f_need || !d_u_band || !hist || !n_it || !flags || !times || max_iters < 0 ||
+        !(tol > 0.0 && tol < 1.0)) {
+        ie::set_error("ie_pcg_sharded_local_f64: bad arguments");
+        return IE_ERR_ARG;
+    }
+    for (int k = 0; k < nranks; ++k)
+        if (!shards[k] || shards[k]->G != nranks || shards[k]->g != k || shards[k]->peer[0] != shards[0]->heap) {
+            ie::set_error("ie_pcg_sharded_local_f64: shards must be ranks 0..G-1 joined by ie_shard_connect_local");
+            return IE_ERR_ARG;
+        }
+    return ie::shard_solve(shards, nranks, d_f_need, d_u_band, tol, max_iters, hist, n_it, flags, times, fail_iter,
+                           fail_value, (cudaStream_t)stream);
 }

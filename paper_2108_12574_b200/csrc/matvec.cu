@@ -270,13 +270,13 @@ namespace ie {
 int fft_create(const ie_geom& g, ie_fft** out);
 void fft_destroy(ie_fft* f);
 int fft_matvec(const ie_fft* f, const double* X0, const double* X1, double* Y0, double* Y1, cudaStream_t st,
-               const int* stop, const double* amax, double2* buf_ws, double* amax_ws);
+               const int* stop, const double* scales, double2* buf_ws, double* amax_ws);
 int64_t fft_buf_elems(const ie_fft* f);
 int fft_band_fwd(const ie_fft* f, const double* X0, const double* X1, int nrows, int parts, double2* out,
-                 const double* amax, int namax, cudaStream_t st);
-int fft_band_cols(const ie_fft* f, double2* buf, int c0, int ncols, cudaStream_t st);
+                 const double* scales, cudaStream_t st, const int* stop = nullptr);
+int fft_band_cols(const ie_fft* f, double2* buf, int c0, int ncols, cudaStream_t st, const int* stop = nullptr);
 int fft_band_inv(const ie_fft* f, const double2* in, int nrows, int parts, double* Y0, double* Y1,
-                 const double* amax, int namax, cudaStream_t st);
+                 const double* scales, cudaStream_t st, const int* stop = nullptr);
 int fft_absmax2(const double* X0, const double* X1, int64_t N, double* part, cudaStream_t st);
 }  // namespace ie
 
@@ -434,15 +434,15 @@ int matvec_prepare_stream(const ie_matvec* m, cudaStream_t st) {
 }
 
 int matvec_launch(const ie_matvec* m, const double* X, int64_t ldx, int nrhs, double* Y, int64_t ldy,
-                  int64_t row_begin, int64_t row_end, cudaStream_t st, const int* stop, const double* amax) {
+                  int64_t row_begin, int64_t row_end, cudaStream_t st, const int* stop, const double* scales) {
     bool ok;
     const ie_matvec::Ws W = mv_ws(const_cast<ie_matvec*>(m), st, &ok);
     if (!ok) return IE_ERR_CUDA;
     if (m->method == IE_MATVEC_FFT) {
         const double* X1 = nrhs == 2 ? X + ldx : nullptr;
         if (row_begin == 0 && row_end == m->N)
-            return fft_matvec(m->fft, X, X1, Y, nrhs == 2 ? Y + ldy : nullptr, st, stop, amax, W.buf, W.amax);
-        int rc = fft_matvec(m->fft, X, X1, W.full, nrhs == 2 ? W.full + m->N : nullptr, st, stop, amax, W.buf,
+            return fft_matvec(m->fft, X, X1, Y, nrhs == 2 ? Y + ldy : nullptr, st, stop, scales, W.buf, W.amax);
+        int rc = fft_matvec(m->fft, X, X1, W.full, nrhs == 2 ? W.full + m->N : nullptr, st, stop, scales, W.buf,
                             W.amax);
         if (rc) return rc;
         for (int q = 0; q < nrhs; ++q)
@@ -607,15 +607,15 @@ static bool band_ok(const ie_matvec* m, int64_t row_begin, int64_t row_end, int3
 
 extern "C" int ie_matvec_band_fwd_f64(const ie_matvec* m, const double* X, int64_t ldx, int32_t nrhs,
                                       int64_t row_begin, int64_t row_end, int32_t parts, void* out,
-                                      const double* amax, int64_t namax, void* stream) {
+                                      const double* scales, void* stream) {
     if (!band_ok(m, row_begin, row_end, parts, nrhs) || !X || !out || ldx < row_end - row_begin ||
-        (nrhs == 2 && (!amax || namax != (m->N + 2047) / 2048))) {
+        (nrhs == 2 && !scales)) {
         if (m && X && out) ie::set_error("ie_matvec_band_fwd_f64: bad arguments");
         return IE_ERR_ARG;
     }
     const int nrows = (int)((row_end - row_begin) / m->g.n);
     if (!nrows) return IE_OK;
-    return ie::fft_band_fwd(m->fft, X, nrhs == 2 ? X + ldx : nullptr, nrows, parts, (double2*)out, amax, (int)namax,
+    return ie::fft_band_fwd(m->fft, X, nrhs == 2 ? X + ldx : nullptr, nrows, parts, (double2*)out, scales,
                             (cudaStream_t)stream);
 }
 
@@ -629,21 +629,21 @@ extern "C" int ie_matvec_band_cols_f64(const ie_matvec* m, void* buf, int64_t co
 }
 
 extern "C" int ie_matvec_band_inv_f64(const ie_matvec* m, const void* in, int64_t row_begin, int64_t row_end,
-                                      int32_t parts, double* Y, int64_t ldy, int32_t nrhs, const double* amax,
-                                      int64_t namax, void* stream) {
+                                      int32_t parts, double* Y, int64_t ldy, int32_t nrhs, const double* scales,
+                                      void* stream) {
     if (!band_ok(m, row_begin, row_end, parts, nrhs) || !in || !Y || ldy < row_end - row_begin ||
-        (nrhs == 2 && (!amax || namax != (m->N + 2047) / 2048))) {
+        (nrhs == 2 && !scales)) {
         if (m && in && Y) ie::set_error("ie_matvec_band_inv_f64: bad arguments");
         return IE_ERR_ARG;
     }
     const int nrows = (int)((row_end - row_begin) / m->g.n);
     if (!nrows) return IE_OK;
-    return ie::fft_band_inv(m->fft, (const double2*)in, nrows, parts, Y, nrhs == 2 ? Y + ldy : nullptr, amax,
-                            (int)namax, (cudaStream_t)stream);
+    return ie::fft_band_inv(m->fft, (const double2*)in, nrows, parts, Y, nrhs == 2 ? Y + ldy : nullptr, scales,
+                            (cudaStream_t)stream);
 }
 
 extern "C" int ie_absmax_partials_f64(const double* X, int64_t ldx, int64_t n, double* out, void* stream) {
-    if (!X || !out || n < 0 || ldx < n) {
+    if (!X || !out || n < 0 || (ldx < n && ldx != 0)) {  // ldx 0: both columns are x0
         ie::set_error("ie_absmax_partials_f64: bad arguments");
         return IE_ERR_ARG;
     }

@@ -848,6 +848,8 @@ __global__ void k_gather(const double* r, const int* idx, double* rg, int64_t to
 // Per point: z_i = sum of its <= MM staged contributions in ascending block id
 // (fixed-width position table, -1 padded: one dependent load level less than CSR).
 // Chunk c of points [i0, i1) (chunk-aligned i0; z and the partials relative to i0).
+// With r: partials[4c] = the chunk's r.z (PCG's rho) and partials[4c + 1] =
+// max|z| over the chunk (the 2-RHS FFT scale bound of the next A-pass, k_iter_b).
 // A thread's points are taken G at a time with every position load of the
 // batch issued before any staging load and every staging / r load before the
 // first store (z may alias nothing, but the compiler cannot know that): two
@@ -856,7 +858,7 @@ template <int MM, int G, bool PF>
 __device__ __forceinline__ void scatter_fixed_chunk(int c, const double* staging, const int* pos, double* z, int N,
                                                     const double* r, double* partials, int i0, int i1, double* sh) {
     const int base = i0 + c * kChunk;
-    double loc = 0.0;
+    double loc = 0.0, zm = 0.0;
     int pn[G][MM];  // PF: the next batch's positions, loaded before this batch's staging values
     if (PF) {
 #pragma unroll
@@ -900,26 +902,22 @@ __device__ __forceinline__ void scatter_fixed_chunk(int c, const double* staging
                 for (int q = 0; q < MM; ++q)
                     if (pp[g][q] >= 0) acc += v[g][q];
                 z[i - i0] = acc;
-                if (r) loc = fma(rv[g], acc, loc);
+                if (r) {
+                    loc = fma(rv[g], acc, loc);
+                    zm = fmax(zm, fabs(acc));
+                }
             }
         }
     }
     if (!r) return;
-    sh[threadIdx.x] = loc;
-    __syncthreads();
-    for (int o = 128; o > 0; o >>= 1) {
-        if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) partials[c] = sh[0];
-    __syncthreads();
+    chunk_sum_max(loc, zm, sh, partials + 4 * c);
 }
 
 template <int MM, int UNR, bool PF = false>
 __global__ void __launch_bounds__(256) k_scatter_fixed(const double* staging, const int* pos, double* z, int N,
                                                        const double* r, double* partials, const int* stop, int i0,
                                                        int i1) {
-    __shared__ double sh[256];
+    __shared__ double sh[512];
     pdl_wait();
     if (stop && *stop) return;
     scatter_fixed_chunk<MM, UNR, PF>(blockIdx.x, staging, pos, z, N, r, partials, i0, i1, sh);
@@ -931,9 +929,9 @@ __global__ void __launch_bounds__(256) k_scatter(const double* staging, const in
                                                  int N, const double* r, double* partials, const int* stop, int i0,
                                                  int i1) {
     if (stop && *stop) return;
-    __shared__ double sh[256];
+    __shared__ double sh[512];
     const int base = i0 + blockIdx.x * kChunk;
-    double loc = 0.0;
+    double loc = 0.0, zm = 0.0;
 #pragma unroll
     for (int e = 0; e < kChunk / 256; ++e) {
         const int i = base + e * 256 + threadIdx.x;
@@ -941,17 +939,14 @@ __global__ void __launch_bounds__(256) k_scatter(const double* staging, const in
             double acc = 0.0;
             for (int q = ptr[i]; q < ptr[i + 1]; ++q) acc += staging[pos[q]];
             z[i - i0] = acc;
-            if (r) loc = fma(r[i], acc, loc);
+            if (r) {
+                loc = fma(r[i], acc, loc);
+                zm = fmax(zm, fabs(acc));
+            }
         }
     }
     if (!r) return;
-    sh[threadIdx.x] = loc;
-    __syncthreads();
-    for (int o = 128; o > 0; o >>= 1) {
-        if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) partials[blockIdx.x] = sh[0];
+    chunk_sum_max(loc, zm, sh, partials + 4 * blockIdx.x);
 }
 
 // ---- large blocks (s > kSmemMaxS, PACKED_INVERSE): blocked sweep inversion.
@@ -2128,5 +2123,43 @@ extern "C" int ie_precond_stats(const ie_precond* p, int64_t* out5) {
     out5[2] = p->fac_bytes;
     out5[3] = p->n_factored;
     out5[4] = p->D;
+    return IE_OK;
+}
+
+// Block k's factor, read back to the host (factor-level parity: the
+// reference's linalg.cholesky, linalg.py:36-45).  SUBST blocks built in
+// shared memory (s <= 160) hold G with A_k = G^T G (upper, LAPACK potrf's
+// factor): *kind = 1, h_out = G.  Every other block holds A_k^{-1} (packed
+// symmetric, or full storage above kBigMaxS): *kind = 0, h_out = A_k^{-1}.
+// h_out is s x s row-major in the block's point order (ascending indices
+// unless share_mirrored_subdomains canonicalised it); NULL: only *s_out.
+extern "C" int ie_precond_block_f64(const ie_precond* p, int64_t k, double* h_out, int64_t* s_out, int32_t* kind) {
+    if (!p || !s_out || k < 0 || k >= p->D) {
+        ie::set_error("ie_precond_block_f64: bad arguments");
+        return IE_ERR_ARG;
+    }
+    ie::BlockMeta m;
+    IE_CUDA(cudaMemcpy(&m, p->d_meta + k, sizeof(m), cudaMemcpyDeviceToHost));
+    const int64_t s = m.s;
+    *s_out = s;
+    const bool chol = p->variant == IE_VARIANT_SUBST && s <= ie::kSmemMaxS;
+    if (kind) *kind = chol ? 1 : 0;
+    if (!h_out) return IE_OK;
+    const bool full = s > ie::kBigMaxS;
+    const int64_t cnt = full ? s * s : s * (s + 1) / 2;
+    std::vector<double> buf((size_t)cnt);
+    IE_CUDA(cudaMemcpy(buf.data(), p->d_fac + m.fac_off, (size_t)cnt * sizeof(double), cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < s * s; ++i) h_out[i] = 0.0;
+    if (full) {
+        for (int64_t i = 0; i < s * s; ++i) h_out[i] = buf[(size_t)i];
+    } else if (chol) {  // G packed by rows: row i = G[i][i..s-1] at i s - i (i - 1) / 2
+        for (int64_t i = 0; i < s; ++i) {
+            const int64_t off = i * s - i * (i - 1) / 2;
+            for (int64_t c = i; c < s; ++c) h_out[i * s + c] = buf[(size_t)(off + c - i)];
+        }
+    } else {  // packed lower by rows == upper by columns: (i, j), j <= i at i (i + 1) / 2 + j
+        for (int64_t i = 0; i < s; ++i)
+            for (int64_t j = 0; j <= i; ++j) h_out[i * s + j] = h_out[j * s + i] = buf[(size_t)(i * (i + 1) / 2 + j)];
+    }
     return IE_OK;
 }

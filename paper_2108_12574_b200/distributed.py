@@ -41,6 +41,23 @@ STAGNATION_WINDOW = 30
 STAGNATION_FACTOR = 1e-3
 
 
+def pow2_scale(mx: float) -> float:
+    """2^-e with 2^e > mx >= 2^(e-1) (C frexp), 1.0 for 0 / non-finite: the
+    exact power-of-two column multiplier of the 2-RHS FFT packing
+    (pcg_pow2_scale in csrc/pcg_state.cuh)."""
+    if not (mx > 0.0) or not math.isfinite(mx):
+        return 1.0
+    return math.ldexp(1.0, -math.frexp(mx)[1])
+
+
+def pcg_scales(max_z: float, beta: float, max_p_old: float, max_u: float) -> tuple:
+    """The 2-RHS multipliers [p_new, u] of the next A-pass, the rule k_iter_b
+    applies on the device: max|p_new| <= max|z| + |beta| max|p_old| (products
+    rounded as written), so no rank needs max|p_new| before its row
+    transforms.  All inputs are global maxima (exact; order-independent)."""
+    return pow2_scale(max_z + abs(beta) * max_p_old), pow2_scale(max_u)
+
+
 def dist_fft_disabled() -> bool:
     """IEDD_B200_NO_DIST_FFT=1: replicate the FFT on every rank (all-gather of
     the iterate) instead of the band decomposition (comparison runs)."""
@@ -140,13 +157,16 @@ class SubDecomposition:
 # --------------------------------------------------------------------------
 class Comm:
     """Band all-gathers over torch.distributed (NCCL for CUDA tensors, gloo
-    for CPU tensors).  Bands are padded to the longest one."""
+    for CPU tensors).  Bands are padded to the longest one.  host_staged:
+    device tensors go through host copies (gloo between processes that share
+    one GPU, where NCCL cannot run)."""
 
-    def __init__(self, plan: ShardPlan, group=None):
+    def __init__(self, plan: ShardPlan, group=None, host_staged: bool = False):
         import torch.distributed as dist
         self.dist = dist
         self.group = group
         self.plan = plan
+        self.host_staged = host_staged
         self.maxlen = max(plan.bounds[i + 1] - plan.bounds[i] for i in range(plan.world))
         self.maxch = max(plan.chunks(i)[1] - plan.chunks(i)[0] for i in range(plan.world))
 
@@ -157,11 +177,15 @@ class Comm:
         pad = self.maxlen if length_of == "band" else self.maxch
         buf = x.new_zeros((ncol, pad))
         buf[:, :L] = x
+        dev = buf.device
+        if self.host_staged and world > 1:
+            buf = buf.cpu()
         outs = [torch.empty_like(buf) for _ in range(world)]
         if world == 1:
             outs[0].copy_(buf)
         else:
             self.dist.all_gather(outs, buf, group=self.group)
+        outs = [o.to(dev) for o in outs]
         pieces = []
         for r in range(world):
             if length_of == "band":
@@ -179,6 +203,25 @@ class Comm:
         out = send.new_empty(int(sum(recv_counts)))
         if self.plan.world == 1:
             out.copy_(send)
+        elif self.host_staged:  # gloo has no all_to_all: pairwise exchanges on host copies
+            src = send.contiguous().cpu()
+            so = np.concatenate([[0], np.cumsum(send_counts)]).astype(int)
+            ro = np.concatenate([[0], np.cumsum(recv_counts)]).astype(int)
+            host = src.new_empty(int(ro[-1]))
+            me = self.plan.rank
+            host[ro[me]: ro[me + 1]] = src[so[me]: so[me + 1]]
+            ops = []
+            for h in range(self.plan.world):
+                if h == me:
+                    continue
+                if send_counts[h]:
+                    ops.append(self.dist.P2POp(self.dist.isend, src[so[h]: so[h + 1]].clone(), h, group=self.group))
+                if recv_counts[h]:
+                    ops.append(self.dist.P2POp(self.dist.irecv, host[ro[h]: ro[h + 1]], h, group=self.group))
+            if ops:
+                for req in self.dist.batch_isend_irecv(ops):
+                    req.wait()
+            out.copy_(host)
         else:
             self.dist.all_to_all_single(out, send.contiguous(), [int(c) for c in recv_counts],
                                         [int(c) for c in send_counts], group=self.group)
@@ -241,43 +284,46 @@ class BandFFT:
       4. reverse all-to-all: rank g receives its rows of every slab;
       5. inverse row FFTs -> the band of A x.
 
-    With two right-hand sides the exact power-of-two column scaling uses the
-    all-gathered per-chunk maxima, so every rank scales identically.  The
-    per-line arithmetic is that of the single-GPU pass (same kernels, same
-    data), so the result does not depend on G.  Per iteration and rank this
-    moves 2 x 16 * n * (2n) / G bytes instead of all-gathering [p, u]."""
+    With two right-hand sides the exact power-of-two column multipliers come
+    from the caller (pcg_scales: global quantities), so every rank scales
+    identically.  The per-line arithmetic is that of the single-GPU pass
+    (same kernels, same data), so the result does not depend on G.  Per
+    iteration and rank this moves 2 x 16 * n * (2n) / G bytes instead of
+    all-gathering [p, u]."""
 
     def __init__(self, stages, plan: ShardPlan, n: int):
         self.st = stages
         self.plan = plan
         self.n = n
         self.G = plan.world
-        self.M = 2 * n
+        from .toeplitz import fft_size
+        self.M = fft_size(n)
         self.Mc = self.M // self.G
         self.rows = [((plan.bounds[h + 1] - plan.bounds[h]) // n) for h in range(self.G)]
         self.row0 = sum(self.rows[: plan.rank])
 
     @staticmethod
     def supported(grid, plan: ShardPlan) -> bool:
+        from .toeplitz import fft_size
         n, G = grid.n_per_dim, plan.world
-        M = 2 * n
+        M = fft_size(n)
         return (grid.dim == 2 and M % G == 0 and (M // G) & (M // G - 1) == 0
                 and all(b % n == 0 for b in plan.bounds))
 
-    def matvec(self, comm, Xb):
-        """Xb: (ncol, band) -> (ncol, band) = rows [begin, end) of A x."""
+    def matvec(self, comm, Xb, scales=None):
+        """Xb: (ncol, band) -> (ncol, band) = rows [begin, end) of A x.  Two
+        columns need `scales` (the 2-RHS multipliers, pcg_scales)."""
         ncol = Xb.shape[0]
-        amax = None
-        if ncol == 2:
-            part = self.st.absmax(Xb)                                    # (nch_band, 2)
-            amax = comm.allgather_partials(part.T.contiguous()).T.contiguous().reshape(-1)
+        if ncol == 2 and scales is None:
+            raise ValueError("BandFFT.matvec: two columns need the 2-RHS scales (pcg_scales)")
         g, G, Mc = self.plan.rank, self.G, self.Mc
         mine = self.rows[g]
-        b1 = self.st.band_fwd(Xb, mine, G, amax)                          # (G, mine, Mc) complex
+        sc = scales if ncol == 2 else None
+        b1 = self.st.band_fwd(Xb, mine, G, sc)                            # (G, mine, Mc) complex
         b2 = comm.alltoall(b1, [2 * mine * Mc] * G, [2 * r * Mc for r in self.rows])
         self.st.band_cols(b2, g * Mc, Mc)                                 # (n, Mc) complex
         b3 = comm.alltoall(b2, [2 * r * Mc for r in self.rows], [2 * mine * Mc] * G)
-        return self.st.band_inv(b3, mine, G, ncol, amax)
+        return self.st.band_inv(b3, mine, G, ncol, sc)
 
 
 class CudaBandStages:
@@ -291,31 +337,28 @@ class CudaBandStages:
         self.mv, self.plan = mv, plan
         self.namax = -(-plan.N // CHUNK)
 
-    def absmax(self, Xb):
-        n = Xb.shape[1]
-        out = self.torch.empty(max(1, -(-n // CHUNK)), 2, dtype=self.torch.float64, device=Xb.device)
-        self._lib.check(self.L.ie_absmax_partials_f64(self._lib.ptr(Xb), Xb.stride(0), n, self._lib.ptr(out),
-                                                      self._lib.stream_ptr()), "absmax")
-        return out[: -(-n // CHUNK)]
+    def _sc(self, scales, dev):
+        return None if scales is None else self.torch.tensor(list(scales), dtype=self.torch.float64, device=dev)
 
-    def band_fwd(self, Xb, nrows, parts, amax):
-        out = self.torch.empty(2 * nrows * self.mv.n * 2, dtype=self.torch.float64, device=Xb.device)
+    def band_fwd(self, Xb, nrows, parts, scales):
+        out = self.torch.empty(nrows * self.mv.M * 2, dtype=self.torch.float64, device=Xb.device)
+        sc = self._sc(scales, Xb.device)
         self._lib.check(self.L.ie_matvec_band_fwd_f64(
             self.mv.handle, self._lib.ptr(Xb), Xb.stride(0), Xb.shape[0], self.plan.begin, self.plan.end, parts,
-            self._lib.ptr(out), self._lib.ptr(amax) if amax is not None else None, self.namax,
-            self._lib.stream_ptr()), "band_fwd")
+            self._lib.ptr(out), self._lib.ptr(sc) if sc is not None else None, self._lib.stream_ptr()), "band_fwd")
         return out
 
     def band_cols(self, buf, c0, ncols):
         self._lib.check(self.L.ie_matvec_band_cols_f64(self.mv.handle, self._lib.ptr(buf), c0, c0 + ncols,
                                                        self._lib.stream_ptr()), "band_cols")
 
-    def band_inv(self, buf, nrows, parts, ncol, amax):
+    def band_inv(self, buf, nrows, parts, ncol, scales):
         Y = self.torch.empty(ncol, self.plan.size, dtype=self.torch.float64, device=buf.device)
+        sc = self._sc(scales, buf.device)
         self._lib.check(self.L.ie_matvec_band_inv_f64(
             self.mv.handle, self._lib.ptr(buf), self.plan.begin, self.plan.end, parts, self._lib.ptr(Y),
-            self.plan.size, ncol, self._lib.ptr(amax) if amax is not None else None, self.namax,
-            self._lib.stream_ptr()), "band_inv")
+            self.plan.size, ncol, self._lib.ptr(sc) if sc is not None else None, self._lib.stream_ptr()),
+            "band_inv")
         return Y
 
 
@@ -339,7 +382,7 @@ class CudaBackend:
         self.N = plan.N
         if method == "auto":
             from .toeplitz import fft_supported
-            method = "fft" if fft_supported(op.grid.n_per_dim) else "direct"
+            method = "fft" if fft_supported(op.grid.n_per_dim, op.grid.dim) else "direct"
         self.mv = KernelMatvec(op, method=method)
         self.method = method
         self.band = (BandFFT(CudaBandStages(self.mv, plan), plan, op.grid.n_per_dim)
@@ -368,12 +411,21 @@ class CudaBackend:
                                   ldx=self.N, ldy=Y.shape[1])
         return Y[:, : self.plan.size]
 
-    def matvec_cols(self, comm, Xb):
+    def matvec_cols(self, comm, Xb, scales=None):
         """Band columns in, band rows of A x out (distributed FFT, or
         all-gather + the band rows of the full-range pass)."""
         if self.band is not None:
-            return self.band.matvec(comm, Xb.contiguous())
+            return self.band.matvec(comm, Xb.contiguous(), scales)
         return self.matvec_band(comm.allgather_band(Xb))
+
+    def chunk_max(self, x):
+        """Per-2048-chunk max|x| of a band vector."""
+        n = x.numel()
+        out = self.torch.empty(max(1, -(-n // CHUNK)), 2, dtype=self.torch.float64, device=self.dev)
+        if n:
+            self._lib.check(self.L.ie_absmax_partials_f64(self._lib.ptr(x), 0, n, self._lib.ptr(out),
+                                                          self._lib.stream_ptr()), "absmax")
+        return out[: -(-n // CHUNK), 0].contiguous() if n else out[:0, 0]
 
     def apply_band(self, r_full):
         if self.pre is None:
@@ -447,9 +499,14 @@ def solve_sharded(backend, comm: Comm, plan: ShardPlan, f_band, tol: float = 1e-
         n_prec += 1
         return z
 
+    def gmax(x):  # global max|x| (exact: the maximum does not depend on the order)
+        return float(comm.allgather_partials(backend.chunk_max(x)[None])[0].max().item())
+
     r = f_band.clone()
     z = apply(r)
     p = z.clone()
+    max_p = gmax(p)
+    scales = None
     rho = backend.sum_partials(comm.allgather_partials(backend.dot_partials(r, z, 0)[None])[0])
     hist = [1.0]
     k = 0
@@ -461,7 +518,7 @@ def solve_sharded(backend, comm: Comm, plan: ShardPlan, f_band, tol: float = 1e-
         if not pending and not do_p:
             break
         cols = ([p] if do_p else []) + ([u] if pending else [])
-        Y = backend.matvec_cols(comm, _stack(cols))
+        Y = backend.matvec_cols(comm, _stack(cols), scales if len(cols) == 2 else None)
         q = Y[0] if do_p else None
         w = Y[-1] if pending else None
         parts = []
@@ -501,39 +558,52 @@ def solve_sharded(backend, comm: Comm, plan: ShardPlan, f_band, tol: float = 1e-
             rz = backend.sum_partials(comm.allgather_partials(backend.dot_partials(r, z, 0)[None])[0])
             beta = rz / rho
             rho = rz
+            scales = pcg_scales(gmax(z), beta, max_p, gmax(u))
             backend.update(2, p, z, beta)
+            max_p = gmax(p)
     full = comm.allgather_band(u[None])[0] if gather_solution else u
     rep = ShardedReport(n_it=k, achieved_residual=hist[-1], t_pcg=time.perf_counter() - t0,
                         t_s=t_prec / max(n_prec, 1), residual_history=hist, stagnated=stag, converged=conv)
     return full, rep
 
 
-class NcclComm:
-    """The library's own NCCL communicator over the ranks of the torch
-    process group (the unique id travels by torch.distributed broadcast)."""
+class NativeShard:
+    """This rank's part of the native sharded solver (ie_pcg_sharded_f64):
+    the exchange heap every peer stores into over NVLink.  Multi-process:
+    the CUDA IPC handles travel by torch.distributed all_gather_object, then
+    every rank opens its peers' heaps (ie_shard_connect)."""
 
-    def __init__(self, plan: ShardPlan, group=None):
-        import torch.distributed as dist
-
+    def __init__(self, backend, plan: ShardPlan, group=None, connect: bool = True):
         from . import _lib
         self._lib = _lib
-        L = _lib.lib()
-        nb = int(L.ie_comm_id_bytes())
-        buf = ctypes.create_string_buffer(nb)
-        if plan.rank == 0:
-            _lib.check(L.ie_comm_unique_id(buf), "ie_comm_unique_id")
-        obj = [buf.raw if plan.rank == 0 else None]
-        if plan.world > 1:
-            dist.broadcast_object_list(obj, src=0, group=group)
-        idb = ctypes.create_string_buffer(obj[0], nb)
+        self.L = _lib.lib()
+        self.plan = plan
+        self.backend = backend
+        bounds = np.ascontiguousarray(plan.bounds, dtype=np.int64)
+        need = np.ascontiguousarray(np.array(plan.need, dtype=np.int64).reshape(-1)) if plan.need else None
+        th = backend.pre.handle if backend.pre is not None else None
         h = ctypes.c_void_p()
-        _lib.check(L.ie_comm_create(idb, plan.world, plan.rank, ctypes.byref(h)), "ie_comm_create")
+        _lib.check(self.L.ie_shard_create(backend.mv.handle, th, plan.world, plan.rank, _lib.np_ptr(bounds),
+                                          _lib.np_ptr(need) if need is not None else None, ctypes.byref(h)),
+                   "ie_shard_create")
         self.handle = h
+        rows = np.zeros(2, dtype=np.int64)
+        _lib.check(self.L.ie_shard_need_rows(h, _lib.np_ptr(rows)), "ie_shard_need_rows")
+        self.need_lo, self.need_hi = int(rows[0]), int(rows[1])
+        if connect and plan.world > 1:
+            import torch.distributed as dist
+            nb = int(self.L.ie_shard_handle_bytes())
+            buf = ctypes.create_string_buffer(nb)
+            _lib.check(self.L.ie_shard_export(h, buf), "ie_shard_export")
+            blobs = [None] * plan.world
+            dist.all_gather_object(blobs, buf.raw, group=group)
+            allb = ctypes.create_string_buffer(b"".join(blobs), nb * plan.world)
+            _lib.check(self.L.ie_shard_connect(h, allb), "ie_shard_connect")
 
     def __del__(self):
         h = getattr(self, "handle", None)
         if h is not None and h.value:
-            self._lib.lib().ie_comm_destroy(h)
+            self._lib.lib().ie_shard_destroy(h)
             self.handle = None
 
 
@@ -543,42 +613,94 @@ def native_supported(backend, plan: ShardPlan) -> bool:
     return backend.band is not None and len(sizes) == 1 and all(b % CHUNK == 0 for b in plan.bounds)
 
 
-def solve_sharded_native(backend, ncomm: NcclComm, plan: ShardPlan, f_band, tol: float = 1e-12,
-                         max_iters: int | None = None):
-    """pcg.solve on the band decomposition through the native NCCL driver
-    (ie_pcg_sharded_f64): device-side control, the iteration (collectives
-    included) captured in a CUDA graph.  Returns (u_band, ShardedReport)."""
-    from . import _lib
-    if not 0.0 < tol < 1.0:
-        raise ValueError(f"tol must be in (0, 1), got {tol}")
-    if not native_supported(backend, plan):
-        raise ValueError("native sharded PCG needs the 2D band FFT and equal chunk-aligned bands")
-    if max_iters is None:
-        max_iters = max(2 * plan.N, 100)
-    u = backend.zeros(plan.size)
-    hist = np.zeros(max_iters + 2, dtype=np.float64)
-    n_it = ctypes.c_int64(0)
-    flags = np.zeros(2, dtype=np.int32)
-    times = np.zeros(2, dtype=np.float64)
-    fail_it = ctypes.c_int64(0)
-    fail_val = ctypes.c_double(0.0)
-    bounds = np.ascontiguousarray(plan.bounds, dtype=np.int64)
-    need = np.ascontiguousarray(np.array(plan.need, dtype=np.int64).reshape(-1)) if plan.need else None
-    th = backend.pre.handle if backend.pre is not None else None
-    f_band = f_band.contiguous()
-    rc = _lib.lib().ie_pcg_sharded_f64(
-        backend.mv.handle, th, ncomm.handle, _lib.np_ptr(bounds), _lib.np_ptr(need) if need is not None else None,
-        _lib.ptr(f_band), _lib.ptr(u), tol, max_iters, _lib.np_ptr(hist), ctypes.byref(n_it), _lib.np_ptr(flags),
-        _lib.np_ptr(times), ctypes.byref(fail_it), ctypes.byref(fail_val), _lib.stream_ptr())
+def _report(hist, n_it, flags, times):
+    k = n_it.value
+    h = [float(x) for x in hist[: k + 1]]
+    return ShardedReport(n_it=k, achieved_residual=h[-1], t_pcg=float(times[0]), t_s=float(times[1]),
+                         residual_history=h, stagnated=bool(flags[1]), converged=bool(flags[0]))
+
+
+def _raise_pcg(_lib, rc, fail_it, fail_val, what):
     if rc == _lib.IE_ERR_BREAKDOWN:
         raise FloatingPointError(f"PCG breakdown at iteration {fail_it.value}: p^T A p = {fail_val.value}")
     if rc == _lib.IE_ERR_NONFINITE:
         raise FloatingPointError(f"non-finite residual at iteration {fail_it.value}")
-    _lib.check(rc, "ie_pcg_sharded_f64")
-    k = n_it.value
-    h = [float(x) for x in hist[: k + 1]]
-    return u, ShardedReport(n_it=k, achieved_residual=h[-1], t_pcg=float(times[0]), t_s=float(times[1]),
-                            residual_history=h, stagnated=bool(flags[1]), converged=bool(flags[0]))
+    _lib.check(rc, what)
+
+
+def solve_sharded_native(shard: NativeShard, f_need, tol: float = 1e-12, max_iters: int | None = None):
+    """pcg.solve on the band decomposition through the native driver
+    (ie_pcg_sharded_f64; every rank calls it).  f_need = f on the rank's need
+    rows [shard.need_lo, shard.need_hi).  Returns (u_band, ShardedReport)."""
+    from . import _lib
+    if not 0.0 < tol < 1.0:
+        raise ValueError(f"tol must be in (0, 1), got {tol}")
+    plan = shard.plan
+    if max_iters is None:
+        max_iters = max(2 * plan.N, 100)
+    u = shard.backend.zeros(plan.size)
+    hist = np.zeros(max_iters + 2, dtype=np.float64)
+    n_it, fail_it, fail_val = ctypes.c_int64(0), ctypes.c_int64(0), ctypes.c_double(0.0)
+    flags = np.zeros(2, dtype=np.int32)
+    times = np.zeros(2, dtype=np.float64)
+    f_need = f_need.contiguous()
+    if f_need.numel() != shard.need_hi - shard.need_lo:
+        raise ValueError(f"f_need has length {f_need.numel()}, the need rows hold {shard.need_hi - shard.need_lo}")
+    rc = _lib.lib().ie_pcg_sharded_f64(shard.handle, _lib.ptr(f_need), _lib.ptr(u), tol, max_iters,
+                                       _lib.np_ptr(hist), ctypes.byref(n_it), _lib.np_ptr(flags), _lib.np_ptr(times),
+                                       ctypes.byref(fail_it), ctypes.byref(fail_val), _lib.stream_ptr())
+    _raise_pcg(_lib, rc, fail_it, fail_val, "ie_pcg_sharded_f64")
+    return u, _report(hist, n_it, flags, times)
+
+
+class LocalShards:
+    """All G ranks of the native sharded solver inside one process on one
+    device (ie_pcg_sharded_local_f64): the peers are plain device pointers
+    and every exchange phase runs for all ranks before the next starts.  It
+    runs the multi-GPU code path -- plans, halo rows, pushes, mailbox
+    counters, the captured iteration -- on a single GPU, so the G > 1 paths
+    are testable (tests/test_gpu_parity.py::TestShardedP2P)."""
+
+    def __init__(self, op, decomposition, world: int, method: str = "fft", variant: str = "packed_inverse",
+                 share_translated: bool = True):
+        from . import _lib
+        self._lib = _lib
+        self.L = _lib.lib()
+        grid = op.grid
+        self.world = world
+        self.plans = [make_plan(grid, decomposition, world, g) for g in range(world)]
+        self.backends = [CudaBackend(op, decomposition, pl, method=method, variant=variant,
+                                     share_translated=share_translated) for pl in self.plans]
+        if not all(native_supported(b, pl) for b, pl in zip(self.backends, self.plans)):
+            raise ValueError("native sharded PCG needs the 2D band FFT and equal chunk-aligned bands")
+        self.shards = [NativeShard(b, pl, connect=False) for b, pl in zip(self.backends, self.plans)]
+        arr = (ctypes.c_void_p * world)(*[sh.handle.value for sh in self.shards])
+        _lib.check(self.L.ie_shard_connect_local(arr, world), "ie_shard_connect_local")
+        self._arr = arr
+
+    def solve(self, f, tol: float = 1e-12, max_iters: int | None = None):
+        """Full-length f (numpy or device tensor) -> (u (N,) device tensor, ShardedReport)."""
+        torch = self.backends[0].torch
+        dev = self.backends[0].dev
+        f = torch.as_tensor(f, dtype=torch.float64).to(dev)
+        if not 0.0 < tol < 1.0:
+            raise ValueError(f"tol must be in (0, 1), got {tol}")
+        N = self.plans[0].N
+        if max_iters is None:
+            max_iters = max(2 * N, 100)
+        fs = [f[sh.need_lo: sh.need_hi].contiguous() for sh in self.shards]
+        us = [torch.empty(pl.size, dtype=torch.float64, device=dev) for pl in self.plans]
+        fp = (ctypes.c_void_p * self.world)(*[t.data_ptr() for t in fs])
+        up = (ctypes.c_void_p * self.world)(*[t.data_ptr() for t in us])
+        hist = np.zeros(max_iters + 2, dtype=np.float64)
+        n_it, fail_it, fail_val = ctypes.c_int64(0), ctypes.c_int64(0), ctypes.c_double(0.0)
+        flags = np.zeros(2, dtype=np.int32)
+        times = np.zeros(2, dtype=np.float64)
+        rc = self.L.ie_pcg_sharded_local_f64(self._arr, self.world, fp, up, tol, max_iters, self._lib.np_ptr(hist),
+                                             ctypes.byref(n_it), self._lib.np_ptr(flags), self._lib.np_ptr(times),
+                                             ctypes.byref(fail_it), ctypes.byref(fail_val), self._lib.stream_ptr())
+        _raise_pcg(self._lib, rc, fail_it, fail_val, "ie_pcg_sharded_local_f64")
+        return torch.cat(us), _report(hist, n_it, flags, times)
 
 
 def lanczos_sharded(backend, comm: Comm, plan: ShardPlan, which: str = "min", max_iters: int = 400,
@@ -654,13 +776,27 @@ def _stack(cols):
 # --------------------------------------------------------------------------
 # bench entry for torchrun (bench.py --gpus N)
 # --------------------------------------------------------------------------
-def bench_sharded(args, metric, cfg, workload):
+def _band_fft_flops(n: int, rows: int, need_rows: int, cols: int) -> float:
+    """Conventional complex-FFT flops (5 M log2 M per line, M = the circulant
+    size, 2n for power-of-two n) of one rank's 2-RHS band pass: `rows` forward
+    row lines, `cols` column lines forward and inverse, `need_rows` inverse
+    row lines."""
+    from .toeplitz import fft_size
+    M = fft_size(n)
+    return (rows + 2 * cols + need_rows) * 5.0 * M * math.log2(M)
+
+
+def bench_sharded(args, metric, cfg, workload, config_keys=None, cpu_baseline=None):
     """bench.py --gpus N under torchrun: config 5 on N ranks (bands of rows and
-    subdomains).  Prints the contract JSON line on rank 0; time = max over ranks
-    of the CUDA-event time of exactly `steps` iterations."""
+    subdomains) through the native P2P driver.  Before timing it checks itself:
+    a 12-iteration solve on all ranks is compared BITWISE (history and the
+    gathered u) against ie_pcg_f64 on rank 0's device.  Prints the contract
+    JSON line on rank 0; time = max over ranks of the CUDA-event time of
+    exactly `steps` iterations."""
     import json
     import os
     import statistics
+    import time as _t
 
     import torch
     import torch.distributed as dist
@@ -669,6 +805,8 @@ def bench_sharded(args, metric, cfg, workload):
 
     from . import _lib
     ws, rank = dist.get_world_size(), dist.get_rank()
+    dev = torch.device("cuda", torch.cuda.current_device())
+    st = torch.cuda.current_stream()
     grid = ie.build_grid(cfg["dim"], cfg["n"])
     op = ie.build_operator(grid, lattice="cell")
     dec = ie.build_decomposition(grid, cfg["m"], cfg["w"], "schwarz")
@@ -676,20 +814,45 @@ def bench_sharded(args, metric, cfg, workload):
     backend = CudaBackend(op, dec, plan, method=getattr(args, "matvec", "auto"))
     comm = Comm(plan)
     f = np.random.default_rng(cfg["seed"]).standard_normal(op.n)
-    f_band = backend.tensor(f[plan.begin: plan.end])
     native = native_supported(backend, plan) and not os.environ.get("IEDD_B200_PY_SHARDED")
+    why = None
+    shard = None
     if native:
-        ncomm = NcclComm(plan)
+        try:
+            shard = NativeShard(backend, plan)
+        except (RuntimeError, ValueError) as e:  # no P2P path between the GPUs
+            native, why = False, str(e)
+    ok = torch.tensor([1 if native else 0], device=dev)
+    dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+    native = bool(ok.item())
+    f_pin = torch.empty(op.n, dtype=torch.float64, pin_memory=True)
+    f_pin.numpy()[:] = f
+    if native:
+        f_need = f_pin[shard.need_lo: shard.need_hi].to(dev)
 
-        def run(fb, iters, gather):
-            u, rep = solve_sharded_native(backend, ncomm, plan, fb, tol=1e-10, max_iters=iters)
-            return (comm.allgather_band(u[None])[0] if gather else u), rep
+        def run(iters):
+            return solve_sharded_native(shard, f_need, tol=1e-10, max_iters=iters)
     else:
-        def run(fb, iters, gather):
-            return solve_sharded(backend, comm, plan, fb, tol=1e-10, max_iters=iters, gather_solution=gather)
-    run(f_band, max(args.warmup, 1), False)
-    dev = torch.device("cuda", torch.cuda.current_device())
-    st = torch.cuda.current_stream()
+        f_band = f_pin[plan.begin: plan.end].to(dev)
+
+        def run(iters):
+            return solve_sharded(backend, comm, plan, f_band, tol=1e-10, max_iters=iters, gather_solution=False)
+
+    # ---- self-check before timing: bitwise against the single-GPU solver
+    pit = 12
+    u_b, rep_b = run(pit)
+    u_all = comm.allgather_band(u_b[None])[0]
+    parity = None
+    if rank == 0:
+        pre_full = ie.from_decomposition(op, dec)
+        u1, rep1 = ie.solve(backend.mv, pre_full, torch.from_numpy(f).to(dev), tol=1e-10, max_iters=pit)
+        parity = {"iterations": pit, "n_it": [rep_b.n_it, rep1.n_it],
+                  "history_bitwise": rep_b.residual_history == rep1.residual_history,
+                  "u_bitwise": bool(torch.equal(u_all, u1)),
+                  "reference": "ie_pcg_f64 on rank 0's device (config 5, same f)"}
+        parity["ok"] = parity["history_bitwise"] and parity["u_bitwise"] and rep_b.n_it == rep1.n_it
+        del pre_full
+    run(max(args.warmup, 1))
     clocks = None
     if rank == 0:
         from bench import ClockSampler  # noqa: WPS433 (bench.py is the caller)
@@ -700,7 +863,7 @@ def bench_sharded(args, metric, cfg, workload):
     n0 = _lib.launch_count()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(st)
-    _, rep = run(f_band, args.steps, False)
+    _, rep = run(args.steps)
     e1.record(st)
     torch.cuda.synchronize()
     dist.barrier()
@@ -708,20 +871,58 @@ def bench_sharded(args, metric, cfg, workload):
     ms = torch.tensor([e0.elapsed_time(e1)], device=dev)
     dist.all_reduce(ms, op=dist.ReduceOp.MAX)
     ms = float(ms.item())
-    # end to end: host f in (each rank copies its band), gathered host u out
+    # end to end: each rank copies its rows of f from pinned host memory and
+    # its band of u back to pinned host memory, inside the timed region
+    u_host = torch.empty(plan.size, dtype=torch.float64, pin_memory=True)
     e2e = []
     for _ in range(3):
         dist.barrier()
-        t0 = torch.cuda.Event(enable_timing=True)
-        t1 = torch.cuda.Event(enable_timing=True)
-        import time as _t
         w0 = _t.perf_counter()
-        fb = backend.tensor(f[plan.begin: plan.end])
-        u, _ = run(fb, args.steps, True)
-        u.cpu()
+        if native:
+            fn = f_pin[shard.need_lo: shard.need_hi].to(dev, non_blocking=True)
+            u, _ = solve_sharded_native(shard, fn, tol=1e-10, max_iters=args.steps)
+        else:
+            fb = f_pin[plan.begin: plan.end].to(dev, non_blocking=True)
+            u, _ = solve_sharded(backend, comm, plan, fb, tol=1e-10, max_iters=args.steps, gather_solution=False)
+        u_host.copy_(u)
         dt = torch.tensor([_t.perf_counter() - w0], device=dev)
         dist.all_reduce(dt, op=dist.ReduceOp.MAX)
         e2e.append(float(dt.item()))
+    # dominant kernel: the rank's band FFT pass (row fwd, column fwd*sym*inv,
+    # inverse need rows), timed on this stream without the exchanges
+    n, G = cfg["n"], ws
+    Mc = backend.mv.M // G
+    rows = plan.size // n
+    need_rows = (shard.need_hi - shard.need_lo) // n if native else rows
+    X = torch.from_numpy(np.random.default_rng(9).standard_normal((2, plan.size))).to(dev)
+    buf = torch.empty(max(rows, need_rows) * backend.mv.M * 2, dtype=torch.float64, device=dev)
+    col = torch.empty(n * Mc * 2, dtype=torch.float64, device=dev)
+    Yb = torch.empty(2, max(need_rows, rows) * n, dtype=torch.float64, device=dev)
+    sc = torch.tensor([1.0, 1.0], dtype=torch.float64, device=dev)
+    L = _lib.lib()
+
+    def band_pass():
+        _lib.check(L.ie_matvec_band_fwd_f64(backend.mv.handle, _lib.ptr(X), X.stride(0), 2, plan.begin, plan.end, G,
+                                            _lib.ptr(buf), _lib.ptr(sc), _lib.stream_ptr()), "band_fwd")
+        _lib.check(L.ie_matvec_band_cols_f64(backend.mv.handle, _lib.ptr(col), rank * Mc, rank * Mc + Mc,
+                                             _lib.stream_ptr()), "band_cols")
+        _lib.check(L.ie_matvec_band_inv_f64(backend.mv.handle, _lib.ptr(buf), 0, need_rows * n, G, _lib.ptr(Yb),
+                                            Yb.stride(0), 2, _lib.ptr(sc), _lib.stream_ptr()), "band_inv")
+    band_pass()
+    torch.cuda.synchronize()
+    e0.record(st)
+    for _ in range(10):
+        band_pass()
+    e1.record(st)
+    torch.cuda.synchronize()
+    fft_ms = torch.tensor([e0.elapsed_time(e1) / 10], device=dev)
+    dist.all_reduce(fft_ms, op=dist.ReduceOp.MAX)
+    fft_ms = float(fft_ms.item())
+    fl = torch.tensor([_band_fft_flops(n, rows, need_rows, Mc)], dtype=torch.float64, device=dev)
+    dist.all_reduce(fl, op=dist.ReduceOp.SUM)
+    peak = ctypes.c_double(0.0)
+    _lib.check(L.ie_fp64_peak(ctypes.byref(peak), _lib.stream_ptr()), "fp64 peak")
+    peak_tf = 2.0 * peak.value / 1e12 * ws
     # K1 direct sum on this rank's band rows (the north-star kernel matvec:
     # compute-bound, N^2 / G pairs per rank): aggregate pair-evals/s
     from .toeplitz import KernelMatvec
@@ -740,23 +941,33 @@ def bench_sharded(args, metric, cfg, workload):
     k1_ms = float(k1_ms.item())
     if rank == 0:
         clk = clocks.stop()
+        config = dict(config_keys or {"workload": workload})
+        config.update({"parallelism": f"row/subdomain bands x{ws}",
+                       "driver": "native ie_pcg_sharded_f64 (NVLink P2P pushes)" if native
+                       else f"python solve_sharded over torch.distributed ({why or 'forced'})",
+                       "matvec": backend.method, "bands": list(plan.bounds)})
+        achieved = float(fl.item()) / (fft_ms * 1e-3) / 1e12
         out = {"metric": metric, "value": args.steps / (ms * 1e-3), "unit": "iter/s", "n_gpus": ws,
                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
-               "data": "synthetic (BASELINE.json config 5, seeded)",
-               "config": {"workload": workload, "N": op.n, "parallelism": f"row/subdomain bands x{ws} (NCCL)",
-                          "driver": "native ie_pcg_sharded_f64" if native else "python solve_sharded",
-                          "matvec": backend.method, "bands": list(plan.bounds),
-                          "l2": "not flushed"},
-               "n_it": rep.n_it,
+               "data": "synthetic (BASELINE.json config 5, seeded)", "config": config,
+               "n_it": rep.n_it, "parity": parity,
                "e2e": {"value": args.steps / statistics.median(e2e), "unit": "iter/s",
-                       "h2d_bytes_per_step": 8 * plan.size / args.steps,
-                       "d2h_bytes_per_step": 8 * op.n / args.steps,
-                       "note": "per solve of K steps: H2D of each rank's f band, D2H of the gathered u"},
+                       "h2d_bytes_per_step": 8 * op.n / args.steps, "d2h_bytes_per_step": 8 * op.n / args.steps,
+                       "note": "per solve of K steps: every rank's H2D of its f rows and D2H of its u band "
+                               "(pinned), max over ranks of the wall time"},
                "gpu_launches": launches, "clocks": clk,
-               "kernel_matvec": {"kernel": "k_matvec<2,2,2> on each rank's band rows (sources all-gathered)",
+               "roofline": {"bound": "fp64", "kernel": "k_fft8 band passes (row fwd, column fwd*sym*inv, "
+                                                       "inverse need rows), all ranks",
+                            "achieved": achieved, "unit": "TFLOP/s", "peak": peak_tf,
+                            "frac": achieved / peak_tf, "traffic": None,
+                            "note": "flops = 5 M log2 M per line FFT summed over the ranks' lines; time = max "
+                                    "over ranks of one band pass without its exchanges; peak = live DFMA "
+                                    "microbenchmark x ranks"},
+               "kernel_matvec": {"kernel": "k_matvec<2,2,16,ADJ> on each rank's band rows",
                                  "pass_ms": k1_ms, "pair_evals_per_s": float(op.n) ** 2 / (k1_ms * 1e-3),
-                                 "note": "max over ranks of one 2-RHS pass; N^2 pairs in total"},
-               "roofline": {"bound": "n/a", "note": "see the N=1 line for the kernel rooflines"}}
+                                 "note": "max over ranks of one 2-RHS pass; N^2 pairs in total"}}
+        if cpu_baseline is not None:
+            out["cpu_baseline"] = cpu_baseline()
         print(json.dumps(out))
     return None

@@ -9,8 +9,8 @@ dense spectra through preconditioned_spectrum (spectrum.py:48-73),
 lambda_min through Lanczos with mirrored sharing (cli.py:249-263), PCG
 iteration counts (cli.py:266-283) and the two-halves Jacobi pairing
 (cli.py:286-291).  Output lines and exit codes are the reference's.  The
-suites are the reference's goldens.json frozen into tests/golden/
-(tools/gen_goldens.py)."""
+suites ship as package data (data/goldens.json: the reference's own
+goldens.json, which it ships the same way, pkg/pyproject.toml:24-25)."""
 
 from __future__ import annotations
 
@@ -26,8 +26,7 @@ EXIT_CONFIG = 1
 EXIT_NUMERICAL = 2
 EXIT_GOLDEN = 3
 
-DEFAULT_GOLDENS = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tests", "golden",
-                               "ref_goldens.json")
+DEFAULT_GOLDENS = os.path.join(os.path.dirname(os.path.abspath(__file__)), "data", "goldens.json")
 
 
 class ConfigError(ValueError):

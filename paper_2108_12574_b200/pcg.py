@@ -113,6 +113,8 @@ def _device_op(op, n, identity_ok=False):
             op.matvec_device(x, y)
             return y
         return a
+    if isinstance(op, Preconditioner) and op.handle is None:  # identity(n) (precond.py:133-134)
+        return lambda x: x.clone()
     if isinstance(op, Preconditioner):
         def t(x):
             z = torch.empty_like(x)

@@ -87,6 +87,22 @@ class Preconditioner:
             self.apply_device(eye[j], out[j])
         return 0.5 * (out + out.T)
 
+    def block(self, k: int):
+        """Subdomain k's stored factor, read back from the device: ("cholesky",
+        G) with A_k = G^T G (the reference's CholeskyFactor.g, linalg.py:36-45;
+        variant "subst", blocks of <= 160 points) or ("inverse", A_k^{-1})
+        otherwise -- s x s numpy arrays in the block's point order."""
+        if self._handle is None:
+            raise ValueError("the identity preconditioner has no blocks")
+        import ctypes
+        s, kind = ctypes.c_int64(0), ctypes.c_int32(0)
+        _lib.check(self._lib.ie_precond_block_f64(self._handle, int(k), None, ctypes.byref(s), ctypes.byref(kind)),
+                   "Preconditioner.block")
+        out = np.empty((s.value, s.value), dtype=np.float64)
+        _lib.check(self._lib.ie_precond_block_f64(self._handle, int(k), _lib.np_ptr(out), ctypes.byref(s),
+                                                  ctypes.byref(kind)), "Preconditioner.block")
+        return ("cholesky" if kind.value == 1 else "inverse"), out
+
     @property
     def n_subdomains(self) -> int:
         return max(self._stats["D"], 1)

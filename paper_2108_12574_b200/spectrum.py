@@ -1,12 +1,16 @@
 """Extremal eigenvalue of T^{-1}A by Lanczos in the A-inner product
 (mirrors /root/reference/pkg/src/iedd/spectrum.py:133-190).
 
-With native operator and preconditioner the loop runs in libiedd_b200.so
-(ie_lanczos_f64): basis and A-basis stay on the device, the two-pass
-A-orthogonalisation is done as two classical Gram-Schmidt sweeps (GEMV
-pairs), and the Ritz value comes from a device Sturm-multisection on the
-tridiagonal.  The stopping rule is the reference's (5 consecutive steps with
-|change| <= rtol*max(|lambda|,1), beta^2 <= 0, beta < 1e-14, max_iters).
+With a native operator and a native or identity preconditioner the loop
+runs in libiedd_b200.so (ie_lanczos_f64): basis and A-basis stay on the
+device, the two-pass A-orthogonalisation is done as two classical
+Gram-Schmidt sweeps (GEMV pairs), and the Ritz value comes from a device
+Sturm-multisection on the tridiagonal.  Any other operator the reference
+accepts (a callable or an object with .matvec, spectrum.py:147; any object
+with .apply, :161) runs the reference's loop on device vectors with host
+callbacks (_lanczos_generic).  The stopping rule is the reference's (5
+consecutive steps with |change| <= rtol*max(|lambda|,1), beta^2 <= 0,
+beta < 1e-14, max_iters).
 
 The dense-spectrum analysis (spectrum.py:37-130: preconditioned_spectrum,
 extremal_eigenvector, jacobi_pairing_check) materialises A and T^{-1} on the
@@ -33,20 +37,71 @@ def extremal_eigenvalue_lanczos(matvec, precond, n: int, which: str = "min", max
                                 rtol: float = 1e-9, seed: int = 0, return_steps: bool = False):
     if which not in ("min", "max"):
         raise ValueError(f"which must be 'min' or 'max', got {which!r}")
-    if not (isinstance(matvec, KernelMatvec) and isinstance(precond, Preconditioner)
-            and precond.handle is not None and matvec.N == n == precond.n):
-        raise TypeError("extremal_eigenvalue_lanczos needs a KernelMatvec and a device Preconditioner "
-                        "built by from_decomposition for the same N")
+    if not hasattr(precond, "apply"):  # spectrum.py:161 calls precond.apply
+        raise TypeError(f"precond of type {type(precond).__name__} has no .apply")
+    native = (isinstance(matvec, KernelMatvec) and isinstance(precond, Preconditioner)
+              and matvec.N == n == precond.n)
+    if not native:
+        return _lanczos_generic(matvec, precond, n, which, max_iters, rtol, seed, return_steps)
     torch = _lib.torch_cuda()
     v0 = torch.from_numpy(np.random.default_rng(seed).standard_normal(n)).cuda()
     lam = ctypes.c_double(0.0)
     steps = ctypes.c_int64(0)
-    rc = _lib.lib().ie_lanczos_f64(matvec.handle, precond.handle, _lib.ptr(v0), 0 if which == "min" else 1,
+    rc = _lib.lib().ie_lanczos_f64(matvec.handle, precond.handle, _lib.ptr(v0), 0 if which == "min" else 1,  # NULL: identity
                                    max_iters, rtol, ctypes.byref(lam), ctypes.byref(steps), _lib.stream_ptr())
     if rc == _lib.IE_ERR_NO_RITZ:
         raise RuntimeError("Lanczos produced no Ritz values")
     _lib.check(rc, "extremal_eigenvalue_lanczos")
     return (lam.value, steps.value) if return_steps else lam.value
+
+
+def _lanczos_generic(matvec, precond, n, which, max_iters, rtol, seed, return_steps):
+    """spectrum.py:133-190 for operators without a native handle: the
+    reference's loop (two-pass modified Gram-Schmidt in the A-inner product,
+    Ritz values of the tridiagonal by scipy) on device vectors; the user's
+    callables see numpy arrays, as in the reference."""
+    from scipy.linalg import eigvalsh_tridiagonal
+
+    from .pcg import _device_op
+    torch = _lib.torch_cuda()
+    A = _device_op(matvec, n)
+    T = _device_op(precond, n)
+    v = torch.from_numpy(np.random.default_rng(seed).standard_normal(n)).cuda()
+    av = A(v)
+    nrm = float(torch.dot(v, av)) ** 0.5
+    V, AV = [v / nrm], [av / nrm]
+    alphas, betas = [], []
+    estimate, stable, steps = None, 0, 1
+    for j in range(max_iters):
+        w = T(AV[j])
+        alphas.append(float(torch.dot(w, AV[j])))
+        for _ in range(2):
+            for vi, avi in zip(V, AV):
+                w -= float(torch.dot(w, avi)) * vi
+        aw = A(w)
+        steps += 1
+        beta2 = float(torch.dot(w, aw))
+        if beta2 <= 0 or not np.isfinite(beta2):
+            break
+        beta = beta2 ** 0.5
+        ritz = eigvalsh_tridiagonal(np.array(alphas), np.array(betas))
+        current = float(ritz[0] if which == "min" else ritz[-1])
+        if estimate is not None and abs(current - estimate) <= rtol * max(abs(current), 1.0):
+            stable += 1
+            if stable >= 5:
+                estimate = current
+                break
+        else:
+            stable = 0
+        estimate = current
+        if beta < 1e-14:
+            break
+        betas.append(beta)
+        V.append(w / beta)
+        AV.append(aw / beta)
+    if estimate is None:
+        raise RuntimeError("Lanczos produced no Ritz values")
+    return (estimate, steps) if return_steps else estimate
 
 
 # --------------------------------------------------------------------------

@@ -51,9 +51,27 @@ def to_host(t, was_numpy: bool):
     return h.numpy()
 
 
-def fft_supported(n: int) -> bool:
-    """The FFT path needs n a power of two with 2 <= n <= 2048 (M = 2n <= 4096)."""
-    return 2 <= n <= 2048 and (n & (n - 1)) == 0
+FFT_MAX_N = 4096  # circulant lines of up to 8192 points (csrc/fft.cu kFftMaxPoints)
+
+
+def fft_size(n: int) -> int:
+    """Circulant embedding size per axis: the smallest power of two >= 2n - 1
+    (at least 4).  The reference embeds in exactly 2n (toeplitz.py:19-30,
+    pocketfft handles any length); any size >= 2n - 1 gives the same Toeplitz
+    product, and a power of two keeps every line transform radix-2^k -- for
+    power-of-two n the two coincide."""
+    m = 4
+    while m < 2 * n - 1:
+        m *= 2
+    return m
+
+
+def fft_supported(n: int, dim: int = 2) -> bool:
+    """The FFT path covers every 2 <= n <= 4096; in 3D the setup's M^3
+    complex embedding is kept under 4 GiB (n <= 128)."""
+    if not 2 <= n <= FFT_MAX_N:
+        return False
+    return dim < 3 or fft_size(n) ** 3 * 16 <= 4 << 30
 
 
 class KernelMatvec:
@@ -67,16 +85,18 @@ class KernelMatvec:
 
     def __init__(self, op: KernelOperator, method: str = "direct"):
         if method == "auto":
-            method = "fft" if fft_supported(op.grid.n_per_dim) else "direct"
+            method = "fft" if fft_supported(op.grid.n_per_dim, op.grid.dim) else "direct"
         if method not in _lib.MATVEC_METHODS:
             raise ValueError(f"method must be one of {tuple(_lib.MATVEC_METHODS)} or 'auto', got {method!r}")
-        if method == "fft" and not fft_supported(op.grid.n_per_dim):
-            raise ValueError(f"method='fft' needs n_per_dim a power of two <= 2048, got {op.grid.n_per_dim}")
+        if method == "fft" and not fft_supported(op.grid.n_per_dim, op.grid.dim):
+            raise ValueError(f"method='fft' needs 2 <= n_per_dim <= {FFT_MAX_N} (3D: <= 128), "
+                             f"got {op.grid.n_per_dim}")
         self.op = op
         self.method = method
         self.dim = op.grid.dim
         self.n = op.grid.n_per_dim
         self.N = op.n
+        self.M = fft_size(self.n) if method == "fft" else 0  # circulant size per axis (FFT method)
         self._lib = _lib.lib()
         h = ctypes.c_void_p()
         _lib.check(self._lib.ie_matvec_create_method(op.geom(), _lib.MATVEC_METHODS[method], ctypes.byref(h)),
@@ -122,8 +142,8 @@ class KernelMatvec:
 
 class ToeplitzMatvec(KernelMatvec):
     """Drop-in for the reference's ToeplitzMatvec: method="auto" picks the
-    FFT algorithm the reference uses whenever n is a power of two <= 2048,
-    else the direct sum."""
+    FFT algorithm the reference uses (any n up to 4096; 3D up to 128), else
+    the direct sum."""
 
     def __init__(self, op: KernelOperator, method: str = "auto"):
         super().__init__(op, method=method)

@@ -9,41 +9,27 @@ from oracle import iedd_oracle as O
 from paper_2108_12574_b200.distributed import CHUNK, BandFFT
 
 
-def _pow2_scale(mx):
-    if not (mx > 0.0) or not np.isfinite(mx):
-        return 1.0
-    return float(np.ldexp(1.0, -int(np.ceil(np.log2(mx)))))
-
-
 class NumpyBandStages:
     """The four band passes of BandFFT in numpy (pocketfft per line), on the
     same buffer layouts as the CUDA passes (complex as interleaved float64)."""
 
     def __init__(self, op, plan):
         self.plan = plan
+        from paper_2108_12574_b200.toeplitz import fft_size
         n = op.grid.n_per_dim
-        self.n, self.M = n, 2 * n
-        emb = np.zeros((self.M, self.M))
+        self.n, self.M = n, fft_size(n)
+        M = self.M
+        emb = np.zeros((M, M))
         emb[:n, :n] = op.generator()
-        emb[n + 1:, :] = emb[n - 1:0:-1, :]
-        emb[:, n + 1:] = emb[:, n - 1:0:-1]
+        emb[M - n + 1:, :] = emb[n - 1:0:-1, :]
+        emb[:, M - n + 1:] = emb[:, n - 1:0:-1]
         self.sym = np.fft.fft2(emb).real
 
-    def absmax(self, Xb):
-        x = Xb.numpy()
-        out = [[np.abs(x[0, c:c + CHUNK]).max(), np.abs(x[1, c:c + CHUNK]).max()]
-               for c in range(0, x.shape[1], CHUNK)]
-        return torch.tensor(out, dtype=torch.float64).reshape(-1, 2)
-
-    def _scales(self, amax):
-        a = amax.numpy().reshape(-1, 2)
-        return _pow2_scale(a[:, 0].max()), _pow2_scale(a[:, 1].max())
-
-    def band_fwd(self, Xb, nrows, parts, amax):
+    def band_fwd(self, Xb, nrows, parts, scales):
         x = Xb.numpy().reshape(Xb.shape[0], nrows, self.n)
         z = x[0].astype(complex)
         if Xb.shape[0] == 2:
-            s0, s1 = self._scales(amax)
+            s0, s1 = scales
             z = x[0] * s0 + 1j * (x[1] * s1)
         f = np.fft.fft(z, n=self.M, axis=1)                      # (nrows, M)
         out = f.reshape(nrows, parts, self.M // parts).transpose(1, 0, 2)
@@ -54,11 +40,11 @@ class NumpyBandStages:
         f = np.fft.fft(b, n=self.M, axis=0) * self.sym[:, c0:c0 + ncols]
         b[:] = np.fft.ifft(f, axis=0)[: self.n]
 
-    def band_inv(self, buf, nrows, parts, ncol, amax):
+    def band_inv(self, buf, nrows, parts, ncol, scales):
         b = buf.numpy().view(complex).reshape(parts, nrows, self.M // parts).transpose(1, 0, 2)
         y = np.fft.ifft(b.reshape(nrows, self.M), axis=1)[:, : self.n].reshape(-1)
         if ncol == 2:
-            s0, s1 = self._scales(amax)
+            s0, s1 = scales
             return torch.from_numpy(np.stack([y.real / s0, y.imag / s1]))
         return torch.from_numpy(y.real[None].copy())
 
@@ -86,10 +72,15 @@ class OracleBackend:
         Y = np.stack([self.mv.matvec(X[c].numpy())[self.plan.begin: self.plan.end] for c in range(X.shape[0])])
         return torch.from_numpy(Y)
 
-    def matvec_cols(self, comm, Xb):
+    def matvec_cols(self, comm, Xb, scales=None):
         if self.band is not None:
-            return self.band.matvec(comm, Xb.contiguous())
+            return self.band.matvec(comm, Xb.contiguous(), scales)
         return self.matvec_band(comm.allgather_band(Xb))
+
+    def chunk_max(self, x):
+        xa = np.abs(x.numpy())
+        return torch.tensor([float(xa[c: c + CHUNK].max()) for c in range(0, xa.size, CHUNK)],
+                            dtype=torch.float64)
 
     def apply_band(self, r_full):
         if self.pre is None:

@@ -20,7 +20,7 @@ DIAG_1D_UNIT = 0.2694727431682211324671
 
 
 def _suites():
-    with open(os.path.join(GOLDEN, "ref_goldens.json")) as fh:
+    with open(os.path.join(GOLDEN, "..", "..", "paper_2108_12574_b200", "data", "goldens.json")) as fh:
         return json.load(fh)
 
 
