@@ -233,6 +233,12 @@ int ie_dot_partials_f64(const double* d_x, const double* d_y, int64_t n, int32_t
                         void* stream);
 int ie_sum_partials_f64(const double* d_part, int64_t nch, double* d_out, void* stream);
 int ie_update_f64(int32_t op, double* d_a, const double* d_b, double s, int64_t n, void* stream);
+/* Per-line partials (nlines lines of n points; x.y for mode 0, |x-y|^2 for
+ * mode 1) with the association ie_pcg_f64 uses when the post pass rides in
+ * the FFT's last line transform of circulant size M (2D / 3D, M >= 64):
+ * thread j < M/8 chains points j + (M/8) m by FMA, then a halving tree. */
+int ie_line_partials_f64(const double* d_x, const double* d_y, int64_t nlines, int32_t n, int32_t M,
+                         int32_t mode, double* d_part, void* stream);
 
 /* FP64 issue-peak microbenchmark: DFMA instructions (lane ops) per second
  * over all SMs -- the roofline denominator for K1. */

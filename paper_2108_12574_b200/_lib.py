@@ -75,6 +75,7 @@ _SIGS = {
     "ie_dot_partials_f64": (_I32, [_P, _P, _I64, _I32, _P, _P]),
     "ie_sum_partials_f64": (_I32, [_P, _I64, _P, _P]),
     "ie_update_f64": (_I32, [_I32, _P, _P, _D, _I64, _P]),
+    "ie_line_partials_f64": (_I32, [_P, _P, _I64, _I32, _I32, _I32, _P, _P]),
     "ie_last_error": (ctypes.c_char_p, []),
     "ie_launch_count": (_I64, []),
 }

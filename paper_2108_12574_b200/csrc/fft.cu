@@ -34,6 +34,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "pcg_state.cuh"
 
 namespace ie {
 
@@ -96,6 +97,27 @@ struct LineArgs {
     // tensor (4n doubles per row, n rows), boxes of {2 G doubles, 256 rows}
     int tma;
     CUtensorMap tmap;
+    // PCG fusions of the single-GPU driver (krylov.cu), contiguous row lines:
+    //  kFwdRCUpd (the first pass of a 2-RHS A-pass, x0 = p, x1 = u): k_iter_b's
+    //    vector half folded in -- p_new = z + beta p_old stored back to x0
+    //    with beta and the 2-RHS multipliers from the state (the decider in
+    //    the previous apply's scatter fixed them), max|p_new| into the
+    //    rotating slot upd_pglob[it % 3] (upd_it < 0: graph replay, the
+    //    iteration from the state).
+    //  kInvCRPost (the last pass): k_post_pass folded in -- per output line,
+    //    p.q (post_q_col: the output column holding q) and |f - w|^2
+    //    (post_w_col) -> post_part[2 (post_line0 + line)], [.. + 1].
+    const double* upd_z;
+    double* upd_pglob;
+    PcgState* upd_s;
+    long long upd_it;
+    const double* post_p;
+    const double* post_f;
+    double* post_part;
+    int post_line0;
+    int post_lo, post_hi;
+    int post_q_col;
+    int post_w_col;
 };
 
 // 2^-e with 2^e >= max|x| (power of two, exact); 1 for max == 0
@@ -302,8 +324,17 @@ __device__ __forceinline__ int padi(int i) { return i + (i >> 4); }
 // k_fft8 exchange padding: one slot per 2^PADS (PADS = 3 for the strided
 // two-line mapping: bank-conflict free for stores and loads, per a half-warp
 // model of 8-byte shared accesses; 4 for the contiguous mapping)
+// PADS > 0: one pad slot per 2^PADS elements.  PADS == 0: no padding, an XOR
+// swizzle of the low four bits by bits 3..6 (a bijection inside each 16-slot
+// block) -- the contiguous 8-point mapping's three Stockham exchanges, with
+// 64-bit accesses served per half-warp, hit 16 distinct bank pairs for every
+// line length 64..8192 (one slot per 16 left pass 2's stores 2-way
+// conflicted: 0.28 M excess wavefronts per config-5 row pass).
 template <int PADS>
-__device__ __forceinline__ int padq(int i) { return i + (i >> PADS); }
+__device__ __forceinline__ int padq(int i) {
+    if constexpr (PADS == 0) return i ^ ((i >> 3) & 15);
+    else return i + (i >> PADS);
+}
 
 // One Stockham pass of radix R over the CTA's lines (16 points per thread).
 // Twiddles of the Ns = 16 pass, radix-major: t16[r * 16 + k] = exp(-2 pi i r k / (16 R));
@@ -377,7 +408,7 @@ __device__ void fft_smem(double* sre, double* sim, int logL, const double2* tws,
 }
 
 // Pass modes: what a line transform reads, does and writes.
-enum FftMode { kFwdCC = 0, kInvCC = 1, kFwdRC = 2, kInvCR = 3, kFusedCC = 4, kFusedRR = 5 };
+enum FftMode { kFwdCC = 0, kInvCC = 1, kFwdRC = 2, kInvCR = 3, kFusedCC = 4, kFusedRR = 5, kFwdRCUpd = 6, kInvCRPost = 7 };
 
 template <int MODE, int TPB>
 __global__ void __launch_bounds__(TPB, 2) k_fft_lines(LineArgs a) {
@@ -824,15 +855,74 @@ __device__ __forceinline__ void fft_line(double* vr, double* vi, int j, double* 
     else fft8_line<S, LOGL, PADS>(vr, vi, j, re, im, a.tw8, zero_hi);
 }
 
+// Tree sums of (a, b) over each line's TPL threads (contiguous mapping: line g
+// = threads [g TPL, (g + 1) TPL)); the sums land in thread j == 0 of the line.
+__device__ __forceinline__ void line_pair_tree(double& a, double& b, int j, int g, int TPL, double* sm) {
+    __syncthreads();  // the FFT's exchange buffer is free
+    double* sa = sm;
+    double* sb = sm + blockDim.x;
+    sa[threadIdx.x] = a;
+    sb[threadIdx.x] = b;
+    __syncthreads();
+    for (int off = TPL / 2; off > 0; off >>= 1) {
+        if (j < off) {
+            sa[threadIdx.x] += sa[threadIdx.x + off];
+            sb[threadIdx.x] += sb[threadIdx.x + off];
+        }
+        __syncthreads();
+    }
+    a = sa[g * TPL];
+    b = sb[g * TPL];
+}
+
+// k_iter_b's vector half folded into the first (row) pass of a 2-RHS A-pass
+// (see LineArgs): beta and the multipliers come from the state, fixed by the
+// decider in the previous apply's scatter (pcg_decide), so every CTA starts
+// its transform after one scalar round trip; p_new = z + beta p_old is stored
+// back and max|p_new| goes to the iteration's rotating slot.
+template <int PTS, int TPL>
+__device__ __forceinline__ void fused_p_update(const LineArgs& a, double* vr, const double* zv, int line, bool live,
+                                               int o, int i, double* csc, double* sm) {
+    PcgState* s = a.upd_s;
+    const int t = threadIdx.x;
+    const long long itf = a.upd_it < 0 ? s->it_dev : a.upd_it;
+    const double beta = s->beta;
+    if (t == 0) {
+        csc[0] = s->sc[0];
+        csc[1] = s->sc[1];
+    }
+    double m = 0.0;
+    const int j = t % TPL;
+#pragma unroll
+    for (int q = 0; q < PTS / 2; ++q) {
+        const int l = j + TPL * q;
+        if (live && l < a.n_in) {
+            const int64_t off = line_off(a.in_so, a.in_si, a.in_sl, a.in_lsplit, a.in_sh, o, i, l);
+            const double pn = __dadd_rn(zv[q], __dmul_rn(beta, vr[q]));
+            const_cast<double*>(a.x0)[off] = pn;
+            vr[q] = pn;
+            m = fmax(m, fabs(pn));
+        }
+    }
+    // max|p_new| over the CTA -> the iteration's slot (non-negative doubles order as their bits)
+    for (int off = 16; off > 0; off >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, off));
+    if ((t & 31) == 0 && m > 0.0)
+        atomicMax(reinterpret_cast<unsigned long long*>(a.upd_pglob + itf % 3),
+                  (unsigned long long)__double_as_longlong(m));
+    __syncthreads();  // csc
+}
+
 template <int MODE, int LOGL, bool STRIDED, bool TMA = false, int PTS = 8>
 __global__ void __launch_bounds__(PTS == 16 ? 256 : 1024, PTS == 16 ? 2 : 1) k_fft8(const __grid_constant__ LineArgs a) {
     static_assert(PTS == 8 || LOGL == 11, "16 points per thread: 2048-point lines only");
-    // exchange padding (bank-conflict free per a half-warp model of 8-byte shared
-    // accesses): one slot per 8 for the strided 8-point mapping, else per 16
-    constexpr int PADS = (STRIDED && PTS == 8) ? 3 : 4;
+    // exchange layout (bank-conflict free per a half-warp model of 8-byte shared
+    // accesses): one pad slot per 8 for the strided 8-point mapping, per 16 for
+    // 16 points per thread, the XOR swizzle (padq<0>) for contiguous 8-point lines
+    constexpr int PADS = STRIDED ? (PTS == 8 ? 3 : 4) : (PTS == 8 ? 0 : 4);
     constexpr int L = 1 << LOGL, TPL = L / PTS;
-    constexpr bool in_real = MODE == kFwdRC || MODE == kFusedRR;
-    constexpr bool out_real = MODE == kInvCR || MODE == kFusedRR;
+    constexpr bool upd = MODE == kFwdRCUpd, post = MODE == kInvCRPost;
+    constexpr bool in_real = MODE == kFwdRC || MODE == kFusedRR || upd;
+    constexpr bool out_real = MODE == kInvCR || MODE == kFusedRR || post;
     constexpr bool fused = MODE == kFusedCC || MODE == kFusedRR;
     extern __shared__ __align__(128) double sm8[];
     __shared__ double csc[2];
@@ -855,6 +945,7 @@ __global__ void __launch_bounds__(PTS == 16 ? 256 : 1024, PTS == 16 ? 2 : 1) k_f
     const int o = lgi >= 0 ? line >> lgi : line / a.ninner;
     const int i = lgi >= 0 ? line & ((1 << lgi) - 1) : line - o * a.ninner;
     double vr[PTS], vi[PTS];
+    double zv[upd ? PTS / 2 : 1];  // z of the fused p update (real input lines: only m < PTS/2 is data)
     constexpr bool tma_mode = TMA && MODE == kFusedCC && STRIDED;
     if constexpr (tma_mode) {
         {
@@ -899,6 +990,9 @@ __global__ void __launch_bounds__(PTS == 16 ? 256 : 1024, PTS == 16 ? 2 : 1) k_f
             if constexpr (in_real) {
                 vr[m] = __ldg(a.x0 + off);
                 if (a.x1) vi[m] = __ldg(a.x1 + off);
+                if constexpr (upd) {
+                    if (m < PTS / 2) zv[m] = __ldg(a.upd_z + off);
+                }
             } else {
                 const double2 v = a.in_c[off];
                 vr[m] = v.x;
@@ -908,7 +1002,9 @@ __global__ void __launch_bounds__(PTS == 16 ? 256 : 1024, PTS == 16 ? 2 : 1) k_f
     }
     // the column scales (a reduction over the max|x| partials) after the line
     // loads are issued: the two memory round trips overlap
-    if ((in_real && a.scale_in) || (out_real && a.scale_out)) {
+    if constexpr (upd) {
+        fused_p_update<PTS, TPL>(a, vr, zv, line, live, o, i, csc, sm8);
+    } else if ((in_real && a.scale_in) || (out_real && a.scale_out)) {
         column_scales_dyn(a, csc);
         __syncthreads();
     }
@@ -946,7 +1042,7 @@ __global__ void __launch_bounds__(PTS == 16 ? 256 : 1024, PTS == 16 ? 2 : 1) k_f
         int jj = j;
         asm volatile("" : "+r"(jj));
         fft_line<+1, LOGL, PADS, PTS>(vr, vi, jj, re, im, a, false);
-    } else if constexpr (MODE == kFwdCC || MODE == kFwdRC) {
+    } else if constexpr (MODE == kFwdCC || MODE == kFwdRC || MODE == kFwdRCUpd) {
         fft_line<-1, LOGL, PADS, PTS>(vr, vi, j, re, im, a, zero_hi);
     } else {
         fft_line<+1, LOGL, PADS, PTS>(vr, vi, j, re, im, a, zero_hi);
@@ -970,6 +1066,51 @@ __global__ void __launch_bounds__(PTS == 16 ? 256 : 1024, PTS == 16 ? 2 : 1) k_f
             }
             return;
         }
+    }
+    if constexpr (post) {
+        // k_post_pass folded in: every point's p / f load first, then the
+        // stores, then the per-line partials (FMA chain over m, tree over the
+        // line's threads) -- the order the sharded band pass uses too
+        double pa = 0.0, pb = 0.0;
+        double pv[PTS / 2], fv[PTS / 2];
+        const bool own = live && line >= a.post_lo && line < a.post_hi;  // (halo rows: q only, no partial)
+#pragma unroll
+        for (int m = 0; m < PTS / 2; ++m) {  // n_out <= L / 2: only m < PTS / 2 is output
+            const int l = j + TPL * m;
+            pv[m] = fv[m] = 0.0;
+            if (own && l < a.n_out) {
+                const int64_t off = line_off(a.out_so, a.out_si, a.out_sl, a.out_lsplit, a.out_sh, o, i, l);
+                if (a.post_q_col >= 0) pv[m] = __ldg(a.post_p + off);
+                if (a.post_w_col >= 0) fv[m] = __ldg(a.post_f + off);
+            }
+        }
+#pragma unroll
+        for (int m = 0; m < PTS / 2; ++m) {
+            const int l = j + TPL * m;
+            if (!live || l >= a.n_out) continue;
+            const int64_t off = line_off(a.out_so, a.out_si, a.out_sl, a.out_lsplit, a.out_sh, o, i, l);
+            double x = vr[m], y = vi[m];
+            if (a.scale_out) {
+                x /= csc[0];  // exact: powers of two
+                y /= csc[1];
+            }
+            a.y0[off] = x;
+            if (a.y1) a.y1[off] = y;
+#ifdef IEDD_DEBUG_FUSE
+            if (off < 3) printf("post off %lld p %.17g q %.17g w %.17g csc %g %g\n", (long long)off, pv[m], x, y, csc[0], csc[1]);
+#endif
+            if (a.post_q_col >= 0) pa = fma(pv[m], x, pa);
+            if (a.post_w_col >= 0) {
+                const double d = fv[m] - (a.post_w_col == 0 ? x : y);
+                pb = fma(d, d, pb);
+            }
+        }
+        line_pair_tree(pa, pb, j, g, TPL, sm8);
+        if (live && j == 0 && line >= a.post_lo && line < a.post_hi) {
+            a.post_part[2 * ((int64_t)a.post_line0 + line)] = pa;
+            a.post_part[2 * ((int64_t)a.post_line0 + line) + 1] = pb;
+        }
+        return;
     }
     if (!live) return;
 #pragma unroll
@@ -1155,15 +1296,17 @@ static int launch_fft8(LineArgs a, cudaStream_t st) {
     }
     (void)cout;
     a.g8 = G;
-    const int pads = (a.strided8 && a.pts == 8) ? 3 : 4;  // k_fft8's PADS
-    a.pitch8 = (a.L + (a.L >> pads) + 15) / 16 * 16 + skew;
+    const int pads = a.strided8 ? (a.pts == 8 ? 3 : 4) : (a.pts == 8 ? 0 : 4);  // k_fft8's PADS
+    a.pitch8 = (pads ? (a.L + (a.L >> pads) + 15) / 16 * 16 : a.L) + skew;
     const int tpb = G * tpl;
     const int ctas = (a.nlines + G - 1) / G;
     const size_t smem = (size_t)2 * G * a.pitch8 * sizeof(double);
     if (a.fused) return a.in_real ? launch_fft8_m<kFusedRR>(a, tpb, ctas, smem, st)
                                   : launch_fft8_m<kFusedCC>(a, tpb, ctas, smem, st);
-    if (a.in_real) return launch_fft8_m<kFwdRC>(a, tpb, ctas, smem, st);
-    if (a.out_real) return launch_fft8_m<kInvCR>(a, tpb, ctas, smem, st);
+    if (a.in_real) return a.upd_s ? launch_fft8_m<kFwdRCUpd>(a, tpb, ctas, smem, st)
+                                  : launch_fft8_m<kFwdRC>(a, tpb, ctas, smem, st);
+    if (a.out_real) return a.post_part ? launch_fft8_m<kInvCRPost>(a, tpb, ctas, smem, st)
+                                       : launch_fft8_m<kInvCR>(a, tpb, ctas, smem, st);
     return a.sign < 0 ? launch_fft8_m<kFwdCC>(a, tpb, ctas, smem, st) : launch_fft8_m<kInvCC>(a, tpb, ctas, smem, st);
 }
 
@@ -1325,6 +1468,29 @@ void fft_destroy(ie_fft* f) {
     delete f;
 }
 
+// the PCG fusions (PcgFuse) on a line pass: the first real-input pass takes the
+// p update, the last real-output pass the post pass
+static void apply_fuse(LineArgs& a, const PcgFuse* fz) {
+    if (!fz) return;
+    if (a.in_real && fz->s) {
+        a.upd_z = fz->z;
+        a.upd_pglob = fz->pglob;
+        a.upd_s = fz->s;
+        a.upd_it = fz->it;
+        a.scale_in = 1;
+    }
+    if (a.out_real && fz->part) {
+        a.post_p = fz->p;
+        a.post_f = fz->f;
+        a.post_part = fz->part;
+        a.post_line0 = fz->line0;
+        a.post_lo = fz->post_lo;
+        a.post_hi = fz->post_hi;
+        a.post_q_col = fz->q_col;
+        a.post_w_col = fz->w_col;
+    }
+}
+
 // ---- 2D band (slab) decomposition of the same three passes, for the sharded
 // solver: rank g owns grid rows [row0, row0 + nrows); the M = 2n spectrum
 // columns are split into `parts` slabs of Mc = M / parts.
@@ -1400,7 +1566,7 @@ int fft_band_cols(const ie_fft* f, double2* buf, int c0, int ncols, cudaStream_t
 }
 
 int fft_band_inv(const ie_fft* f, const double2* in, int nrows, int parts, double* Y0, double* Y1,
-                 const double* scales, cudaStream_t st, const int* stop) {
+                 const double* scales, cudaStream_t st, const int* stop, const PcgFuse* fz) {
     int rc = band_check(f, parts);
     if (rc) return rc;
     const int n = f->n, Mc = f->M / parts;
@@ -1427,6 +1593,7 @@ int fft_band_inv(const ie_fft* f, const double2* in, int nrows, int parts, doubl
         e.scales = scales;
         e.scale_out = 1;
     }
+    apply_fuse(e, fz);
     return line_launch(e, st);
 }
 
@@ -1488,8 +1655,17 @@ static bool tma_map(ie_fft* f, const double2* B, int G, CUtensorMap* out) {
 // buf_ws / amax_ws: the calling stream's work buffer and chunk-maxima scratch
 // (nullptr: the plan's own).  scales_ext: the 2-RHS column multipliers
 // precomputed on the device (PCG); without them the pass reduces max|x_c|.
+// can the PCG iteration fold k_iter_b / k_post_pass into this plan's passes
+bool fft_fusable(const ie_fft* f) {
+    static const bool v1 = getenv("IEDD_B200_FFT_V1") != nullptr;
+    return f->dim >= 2 && f->logM >= 6 && !v1 && !getenv("IEDD_B200_NO_FUSE");
+}
+
+// output lines of the last (real-output) pass: 2D rows, 3D (a, b) lines
+int fft_out_lines(const ie_fft* f) { return f->dim == 3 ? f->n * f->n : f->n; }
+
 int fft_matvec(const ie_fft* f, const double* X0, const double* X1, double* Y0, double* Y1, cudaStream_t st,
-               const int* stop, const double* scales_ext, double2* buf_ws, double* amax_ws) {
+               const int* stop, const double* scales_ext, double2* buf_ws, double* amax_ws, const PcgFuse* fz) {
     const int n = f->n, M = f->M, d = f->dim;
     int rc;
     const int two = X1 != nullptr;
@@ -1506,6 +1682,8 @@ int fft_matvec(const ie_fft* f, const double* X0, const double* X1, double* Y0, 
             a.scale_in = a.in_real;
             a.scale_out = a.out_real;
         }
+        if (d >= 2) apply_fuse(a, fz);
+        if (a.post_part && a.post_hi == 0) a.post_hi = a.nlines;
         return ::ie::line_launch(a, s);
     };
     if (d == 1) {

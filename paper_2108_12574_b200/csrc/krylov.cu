@@ -39,11 +39,13 @@ namespace ie {
 
 int matvec_launch(const ie_matvec* m, const double* X, int64_t ldx, int nrhs, double* Y, int64_t ldy,
                   int64_t row_begin, int64_t row_end, cudaStream_t st, const int* stop,
-                  const double* amax = nullptr);
+                  const double* scales = nullptr, const PcgFuse* fz = nullptr);
+int matvec_fused_lines(const ie_matvec* m);
 int precond_prepare_stream(const ie_precond* p, cudaStream_t st);
 int matvec_prepare_stream(const ie_matvec* m, cudaStream_t st);
 int precond_apply(const ie_precond* p, const double* r, double* z, double* partials, cudaStream_t st,
                   const int* stop);
+void precond_set_decide(const PcgDecide* d);
 int matvec_N(const ie_matvec* m);
 uint64_t matvec_uid(const ie_matvec* m);
 uint64_t precond_uid(const ie_precond* p);
@@ -124,6 +126,19 @@ struct HaloSeg {
     int lo0, len0, lo1, len1;
 };
 
+// Graph replay: the last CTA of the iteration's final it_dev reader (every CTA
+// has read it) advances the iteration counter.
+__device__ __forceinline__ void advance_iteration(PcgState* s) {
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        __threadfence();
+        if (atomicAdd(&s->ticket, 1u) == gridDim.x - 1) {
+            s->ticket = 0;
+            s->it_dev += 1;
+        }
+    }
+}
+
 // After the A-pass of iteration `it`: residual / stagnation check of
 // iteration it-1 (pcg.py:107-119), breakdown test of iteration it
 // (pcg.py:99-103), alpha, then u += alpha p, r -= alpha q and max|u| per chunk.
@@ -132,12 +147,16 @@ struct HaloSeg {
 // on the reduction (state scalars, the history entry of the stagnation test,
 // this thread's partials and its p, q, r chunk values) is issued before it, so
 // the serial prologue costs about one memory round trip.  CTAs >= nchb update
-// the halo segments' r only.
+// the halo segments' r only.  xpost holds npost partial pairs (dot chunks, or
+// output lines when the post pass is folded into the FFT); pmax (the
+// per-chunk max|p| of k_iter_b, copied into the record) is null when the p
+// update is folded into the FFT; ticket: graph replay without k_iter_b, this
+// kernel advances the iteration counter.
 template <bool WITH_U, bool HALO = false>
-__global__ void __launch_bounds__(kRed, 4) k_iter_a(const double* xpost, int nch, int do_p, int pending, long long it,
-                                                 PcgState* s, double* hist, double* u, double* r, const double* p,
-                                                 const double* q, int nb, int c0, int nchb, double* xrz,
-                                                 const double* pmax, HaloSeg hs) {
+__global__ void __launch_bounds__(kRed, 4) k_iter_a(const double* xpost, int npost, int do_p, int pending,
+                                                 long long it, PcgState* s, double* hist, double* u, double* r,
+                                                 const double* p, const double* q, int nb, int c0, int nchb,
+                                                 double* xrz, const double* pmax, HaloSeg hs, int ticket) {
     __shared__ double sh[kRed];
     __shared__ int decided;
     pdl_wait();
@@ -168,7 +187,7 @@ __global__ void __launch_bounds__(kRed, 4) k_iter_a(const double* xpost, int nch
         qv[e] = in ? q[i] : 0.0;
     }
     double lp = 0.0, lr = 0.0;
-    for (int c = threadIdx.x; c < nch; c += kRed) {
+    for (int c = threadIdx.x; c < npost; c += kRed) {
         if (do_p) lp += xpost[2 * c];
         if (pending) lr += xpost[2 * c + 1];
     }
@@ -212,7 +231,7 @@ __global__ void __launch_bounds__(kRed, 4) k_iter_a(const double* xpost, int nch
     if (decided || !do_p) return;
     // max|p| of the direction this pass multiplied (k_iter_b of the previous
     // iteration) into the record, for this iteration's k_iter_b scale bound
-    if (!halo && threadIdx.x == 32) xrz[kRzRec * (c0 + blockIdx.x) + 2] = pmax[blockIdx.x];
+    if (pmax && !halo && threadIdx.x == 32) xrz[kRzRec * (c0 + blockIdx.x) + 2] = pmax[blockIdx.x];
     const double al = rho_prev / denom;
     if (!ua) {  // u += alpha p runs concurrently in k_update_u (graph side branch), or a halo CTA
 #pragma unroll
@@ -220,6 +239,7 @@ __global__ void __launch_bounds__(kRed, 4) k_iter_a(const double* xpost, int nch
             const int i = base + e * kRed + threadIdx.x;
             if (i < lim) r[i] = __dsub_rn(av[e], __dmul_rn(al, qv[e]));
         }
+        if (ticket) advance_iteration(s);
         return;
     }
     double m = 0.0;
@@ -235,6 +255,7 @@ __global__ void __launch_bounds__(kRed, 4) k_iter_a(const double* xpost, int nch
     }
     m = chunk_absmax(m, sh);
     if (threadIdx.x == 0) xrz[kRzRec * (c0 + blockIdx.x) + 3] = m;
+    if (ticket) advance_iteration(s);
 }
 
 // k_iter_a's u half: u += alpha p and max|u| per chunk, with the alpha CTA 0 of
@@ -329,6 +350,9 @@ __global__ void __launch_bounds__(kRed) k_iter_b(const double* xrz, int nch, lon
         const int i = base + e * kRed + threadIdx.x;
         if (i < nb) {
             const double pn = __dadd_rn(zv[e], __dmul_rn(beta, pv[e]));
+#ifdef IEDD_DEBUG_FUSE
+            if (i < 3 && blockIdx.x == 0) printf("iterb i %d z %.17g pold %.17g pnew %.17g beta %.17g\n", i, zv[e], pv[e], pn, beta);
+#endif
             p[i] = pn;
             m = fmax(m, fabs(pn));
         }
@@ -350,8 +374,10 @@ __global__ void __launch_bounds__(kRed) k_iter_b(const double* xrz, int nch, lon
 
 // After the first apply (pcg.py:85-91): rho_0 = r.z (every CTA reduces, CTA 0
 // stores), p = z and max|p| per chunk (= max|z|, the record's field 1).
+// pglob (the fused p update's rotating global max|p| slots, zeroed before):
+// slot 1 = max|p_1|.
 __global__ void __launch_bounds__(kRed) k_pcg_setup(const double* xrz, int nch, PcgState* s, double* p,
-                                                    const double* z, int nb, int c0, double* pmax) {
+                                                    const double* z, int nb, int c0, double* pmax, double* pglob) {
     __shared__ double sh[kRed];
     if (s->stop) return;
     const int base = blockIdx.x * kChunk;
@@ -360,12 +386,24 @@ __global__ void __launch_bounds__(kRed) k_pcg_setup(const double* xrz, int nch, 
         const int i = base + e * kRed + threadIdx.x;
         if (i < nb) p[i] = z[i];
     }
-    if (threadIdx.x == 0) pmax[blockIdx.x] = xrz[kRzRec * (c0 + blockIdx.x) + 1];
+    if (threadIdx.x == 0) {
+        const double m = xrz[kRzRec * (c0 + blockIdx.x) + 1];
+        if (pmax) pmax[blockIdx.x] = m;
+        if (pglob) atomicMax(reinterpret_cast<unsigned long long*>(pglob + 1), (unsigned long long)__double_as_longlong(m));
+    }
     if (blockIdx.x != 0) return;
     double loc = 0.0;
     for (int c = threadIdx.x; c < nch; c += kRed) loc += xrz[kRzRec * c];
     const double rz = block_tree(loc, sh);
     if (threadIdx.x == 0) s->rho[0] = rz;
+}
+
+// The decider (pcg_decide) as a one-CTA kernel: the identity preconditioner
+// has no scatter to host it.
+__global__ void __launch_bounds__(kRed) k_decide(const double* rec, PcgDecide d, const int* stop) {
+    __shared__ double sh[kRed];
+    if (*stop) return;
+    pcg_decide(rec, d, sh);
 }
 
 // The identity preconditioner (pcg.py:68): z = r, with the apply's chunk
@@ -394,6 +432,9 @@ __global__ void __launch_bounds__(kRed) k_identity_apply(const double* r, double
 // loads are issued before the stop flag is tested.
 __global__ void k_post_pass(const double* p, const double* q, const double* f, const double* w, int N, int do_p,
                             int pending, double* xpost, const int* stop) {
+#ifdef IEDD_DEBUG_FUSE
+    if (blockIdx.x == 0 && threadIdx.x < 3 && !*stop) printf("kpost i %d p %.17g q %.17g w %.17g\n", threadIdx.x, p[threadIdx.x], q[threadIdx.x], w[threadIdx.x]);
+#endif
     __shared__ double sh[kRed];
     pdl_wait();
     const int stopv = *stop;  // tested after the chunk loads are issued
@@ -505,7 +546,9 @@ struct PcgWork {
     int N = 0;
     int64_t cap = 0;
     double *PU = nullptr, *QW = nullptr, *r = nullptr, *z = nullptr, *part = nullptr, *hist = nullptr;
-    // part = [xf: nch | xpost: 2 nch | xrz: kRzRec nch | pmax: nch] (layouts above k_iter_a)
+    // part = [xf: nch | xpost: 2 npmax | xrz: kRzRec nch | pmax: nch | pglob: 3] (layouts above
+    // k_iter_a); npmax = max(nch, lines of a 2D / 3D FFT pass) for the folded post pass
+    int npmax = 0;
     double* fcopy = nullptr; // the right-hand side (graph-stable address)
     cudaStream_t cap_stream = nullptr;
     cudaStream_t side_stream = nullptr;  // graph side branch (u update)
@@ -562,7 +605,9 @@ static PcgWork* work_acquire(int N, int64_t cap, int* rc) {
     if (e == cudaSuccess) e = cudaMalloc(&w->QW, 2 * (size_t)N * 8);
     if (e == cudaSuccess) e = cudaMalloc(&w->r, (size_t)N * 8);
     if (e == cudaSuccess) e = cudaMalloc(&w->z, (size_t)N * 8);
-    if (e == cudaSuccess) e = cudaMalloc(&w->part, (4 + kRzRec) * (size_t)nch * 8);
+    // xpost holds a partial pair per dot chunk, or per FFT output line (<= N^(2/3))
+    w->npmax = std::max(nch, (int)ceil(pow((double)N, 2.0 / 3.0)) + 2);
+    if (e == cudaSuccess) e = cudaMalloc(&w->part, ((2 + kRzRec) * (size_t)nch + 2 * (size_t)w->npmax + 3) * 8);
     if (e == cudaSuccess) e = cudaMalloc(&w->hist, (size_t)cap * 8);
     if (e == cudaSuccess) e = cudaMalloc(&w->fcopy, (size_t)N * 8);
     if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&w->cap_stream, cudaStreamNonBlocking);
@@ -635,20 +680,48 @@ static int pcg_impl(const ie_matvec* A, const ie_precond* T, const double* f, do
     double* w = W->QW + N;
     double* xf = W->part;
     double* xpost = W->part + nch;
-    double* xrz = W->part + 3 * nch;
+    double* xrz = xpost + 2 * W->npmax;
     double* pmax = xrz + kRzRec * nch;
+    double* pglob = pmax + nch;
     const int* stop = &W->st->stop;
-    // z = T^{-1} r and the chunk record's r.z / max|z| fields
-    auto apply_on = [&](const double* rin, double* zout, cudaStream_t s2) -> int {
-        if (T) return precond_apply(T, rin, zout, xrz, s2, stop);
+    // k_iter_b and k_post_pass folded into the FFT passes (2D / 3D FFT plans)
+    static const bool no_fuse = getenv("IEDD_B200_NO_FUSE") != nullptr;
+    static const bool no_fuse_upd = getenv("IEDD_B200_NO_FUSE_UPD") != nullptr;
+    static const bool no_fuse_post = getenv("IEDD_B200_NO_FUSE_POST") != nullptr;
+    const int nfl = no_fuse ? 0 : matvec_fused_lines(A);
+    const bool fuse_upd = nfl > 0 && !no_fuse_upd, fuse_post = nfl > 0 && !no_fuse_post;
+    const bool fused = fuse_upd || fuse_post;
+    const int npost = fuse_post ? nfl : nch;
+    // z = T^{-1} r and the chunk record's r.z / max|z| fields; with the p
+    // update folded into the FFT (fuse_upd), the iteration's decider (beta,
+    // rho, the next multipliers) runs on the completed record: in the last
+    // CTA of the scatter, or (identity) a one-CTA k_decide
+    auto apply_on = [&](const double* rin, double* zout, cudaStream_t s2, int64_t itd) -> int {
+        PcgDecide dec;
+        if (fuse_upd && itd != 0) {
+            dec.s = W->st;
+            dec.pglob = pglob;
+            dec.it = itd;
+            dec.nch = nch;
+        }
+        if (T) {
+            precond_set_decide(&dec);
+            const int r2 = precond_apply(T, rin, zout, xrz, s2, stop);
+            precond_set_decide(nullptr);
+            return r2;
+        }
         k_identity_apply<<<nch, kRed, 0, s2>>>(rin, zout, N, xrz, stop);
         IE_LAUNCHED();
+        if (dec.s) {
+            k_decide<<<1, kRed, 0, s2>>>(xrz, dec, stop);
+            IE_LAUNCHED();
+        }
         return IE_OK;
     };
     auto apply = [&](const double* rin, double* zout, int64_t evi) -> int {
         const bool timed = 2 * evi + 1 < (int64_t)W->ev.size();
         if (timed) IE_CUDA(cudaEventRecord(W->ev[2 * evi], st));
-        int r2 = apply_on(rin, zout, st);
+        int r2 = apply_on(rin, zout, st, evi);  // (evi: the iteration; 0 = the initial apply)
         if (r2) return r2;
         if (timed) IE_CUDA(cudaEventRecord(W->ev[2 * evi + 1], st));
         return IE_OK;
@@ -664,7 +737,8 @@ static int pcg_impl(const ie_matvec* A, const ie_precond* T, const double* f, do
     IE_CUDA(cudaMemsetAsync(uu, 0, (size_t)N * 8, st));
     IE_CUDA(cudaMemcpyAsync(W->r, f, (size_t)N * 8, cudaMemcpyDeviceToDevice, st));
     if ((rc = apply(W->r, W->z, 0))) return rc;
-    k_pcg_setup<<<nch, kRed, 0, st>>>(xrz, nch, W->st, p, W->z, N, 0, pmax);  // p = z, rho_0
+    IE_CUDA(cudaMemsetAsync(pglob, 0, 3 * sizeof(double), st));
+    k_pcg_setup<<<nch, kRed, 0, st>>>(xrz, nch, W->st, p, W->z, N, 0, pmax, fuse_upd ? pglob : nullptr);  // p = z, rho_0
     IE_LAUNCHED();
     // iterations: `it` = the iteration whose A-pass is enqueued; the pass also
     // carries u_{it-1} for the deferred true-residual check of iteration it-1.
@@ -693,24 +767,41 @@ static int pcg_impl(const ie_matvec* A, const ie_precond* T, const double* f, do
             return IE_OK;
         };
         if ((r2 = mark(0))) return r2;
+        PcgFuse fz;  // (fused: the previous iteration's k_iter_b and this pass's k_post_pass ride in the FFT)
+        if (fused) {
+            if (fuse_upd && do_p && pending) {
+                fz.z = W->z;
+                fz.pglob = pglob;
+                fz.s = W->st;
+                fz.it = itarg;
+            }
+            fz.p = p;
+            fz.f = f;
+            fz.part = fuse_post ? xpost : nullptr;
+            fz.q_col = do_p ? 0 : -1;
+            fz.w_col = pending ? (do_p ? 1 : 0) : -1;
+        }
+        const PcgFuse* fzp = fused ? &fz : nullptr;
         if (do_p && pending) {
-            r2 = matvec_launch(A, W->PU, N, 2, W->QW, N, 0, N, s2, stop, W->st->sc);
+            r2 = matvec_launch(A, W->PU, N, 2, W->QW, N, 0, N, s2, stop, W->st->sc, fzp);
         } else if (do_p) {
-            r2 = matvec_launch(A, p, N, 1, q, N, 0, N, s2, stop);
+            r2 = matvec_launch(A, p, N, 1, q, N, 0, N, s2, stop, nullptr, fzp);
         } else {
-            r2 = matvec_launch(A, uu, N, 1, w, N, 0, N, s2, stop);
+            r2 = matvec_launch(A, uu, N, 1, w, N, 0, N, s2, stop, nullptr, fzp);
         }
         if (r2 || (r2 = mark(1))) return r2;
-        IE_CUDA(launch_k(k_post_pass, dim3(nch), dim3(kRed), 0, s2, (const double*)p, (const double*)q, f,
-                         (const double*)w, N, do_p, pending, xpost, stop));
-        IE_LAUNCHED();
+        if (!fuse_post) {
+            IE_CUDA(launch_k(k_post_pass, dim3(nch), dim3(kRed), 0, s2, (const double*)p, (const double*)q, f,
+                             (const double*)w, N, do_p, pending, xpost, stop));
+            IE_LAUNCHED();
+        }
         if ((r2 = mark(2))) return r2;
         // in the captured iteration u += alpha p forks onto a side branch beside the apply
         const bool fork_u = itarg < 0 && do_p && spec && !no_fork && !prof;
         IE_CUDA(launch_k(fork_u ? k_iter_a<false> : k_iter_a<true>, dim3(nch), dim3(kRed), 0, s2,
-                         (const double*)xpost, nch, do_p, pending, (long long)itarg, W->st, W->hist,
+                         (const double*)xpost, npost, do_p, pending, (long long)itarg, W->st, W->hist,
                          fork_u ? nullptr : uu, W->r, (const double*)p, (const double*)q, N, 0, nch, xrz,
-                         (const double*)pmax, HaloSeg{0, 0, 0, 0}));
+                         fuse_upd ? nullptr : (const double*)pmax, HaloSeg{0, 0, 0, 0}, 0));
         IE_LAUNCHED();
         if (fork_u) {
             IE_CUDA(cudaEventRecord(W->fork_ev, s2));
@@ -723,15 +814,17 @@ static int pcg_impl(const ie_matvec* A, const ie_precond* T, const double* f, do
             if ((r2 = mark(3))) return r2;
             if (timed_apply && !pf) {
                 if ((r2 = apply(W->r, W->z, evi))) return r2;
-            } else if ((r2 = apply_on(W->r, W->z, s2))) {
+            } else if ((r2 = apply_on(W->r, W->z, s2, itarg))) {
                 return r2;
             }
             if ((r2 = mark(4))) return r2;
-            // k_iter_b rewrites p, which the side branch reads: join first
+            // k_iter_b (or the next pass's folded p update) rewrites p, which the side branch reads: join first
             if (fork_u) IE_CUDA(cudaStreamWaitEvent(s2, W->join_ev, 0));
-            IE_CUDA(launch_k(k_iter_b, dim3(nch), dim3(kRed), 0, s2, (const double*)xrz, nch, (long long)itarg,
-                             W->st, p, (const double*)W->z, N, pmax));
-            IE_LAUNCHED();
+            if (!fuse_upd) {
+                IE_CUDA(launch_k(k_iter_b, dim3(nch), dim3(kRed), 0, s2, (const double*)xrz, nch,
+                                 (long long)itarg, W->st, p, (const double*)W->z, N, pmax));
+                IE_LAUNCHED();
+            }
             if ((r2 = mark(5))) return r2;
         }
         if (pf) {
@@ -1324,7 +1417,7 @@ int fft_band_fwd(const ie_fft* f, const double* X0, const double* X1, int nrows,
                  const double* scales, cudaStream_t st, const int* stop);
 int fft_band_cols(const ie_fft* f, double2* buf, int c0, int ncols, cudaStream_t st, const int* stop);
 int fft_band_inv(const ie_fft* f, const double2* in, int nrows, int parts, double* Y0, double* Y1,
-                 const double* scales, cudaStream_t st, const int* stop);
+                 const double* scales, cudaStream_t st, const int* stop, const PcgFuse* fz);
 int precond_apply_band(const ie_precond* p, const double* r, double* z, double* partials, int64_t i0, int64_t i1,
                        cudaStream_t st, const int* stop);
 
@@ -1419,6 +1512,7 @@ struct ie_shard {
     int64_t b0 = 0, b1 = 0, nb = 0;
     int nrows = 0, row0 = 0, rlo = 0, rhi = 0, R = 0, Rmax = 0;
     int nch = 0, nchb = 0, c0 = 0;
+    bool line_post = false;  // k_post_pass folded into the inverse rows (per-row partials), as ie_pcg_f64 does
     std::vector<int> row0_all, nrows_all, rlo_all, rhi_all;
     // symmetric exchange heap (IPC-exported): mailbox counters, F partials,
     // POST partials, RZ records, column slab, need-row block
@@ -1489,15 +1583,21 @@ static int shard_wait(const ie_shard* sh, int slot, unsigned long long expect, c
     return IE_OK;
 }
 
-// the rank's slab of a chunk-indexed exchange array, pushed to every rank
-static int shard_push_chunks(const ie_shard* sh, int slot, double* (ie_shard::*arr)(int) const, int per,
-                             cudaStream_t s) {
+// the rank's slab of a globally indexed exchange array (entries [first,
+// first + count) of `per` doubles each), pushed to every rank
+static int shard_push_slab(const ie_shard* sh, int slot, double* (ie_shard::*arr)(int) const, int per, int first,
+                           int count, cudaStream_t s) {
     PushDesc d[kMaxRanks];
-    const size_t off = (size_t)sh->c0 * per;
+    const size_t off = (size_t)first * per;
     for (int h = 0; h < sh->G; ++h)
         d[h] = PushDesc{(const char*)((sh->*arr)(sh->g) + off), (char*)((sh->*arr)(h) + off),
-                        (long long)sh->nchb * per * 8, nullptr};
+                        (long long)count * per * 8, nullptr};
     return shard_push(sh, slot, d, sh->G, s);
+}
+
+static int shard_push_chunks(const ie_shard* sh, int slot, double* (ie_shard::*arr)(int) const, int per,
+                             cudaStream_t s) {
+    return shard_push_slab(sh, slot, arr, per, sh->c0, sh->nchb, s);
 }
 
 static inline double* q_band(const ie_shard* sh) { return sh->QW + (size_t)(sh->row0 - sh->rlo) * sh->n; }
@@ -1543,7 +1643,7 @@ static int shard_setup_phase(ie_shard* sh, int ph, const double* f_need, double 
     }
     int rc = shard_wait(sh, kSlotRz, (unsigned long long)nch * kRzRec * 8, s);
     if (rc) return rc;
-    k_pcg_setup<<<nchb, kRed, 0, s>>>(sh->xrz(sh->g), nch, sh->S, sh->PU, sh->z, (int)sh->nb, c0, sh->pmax);
+    k_pcg_setup<<<nchb, kRed, 0, s>>>(sh->xrz(sh->g), nch, sh->S, sh->PU, sh->z, (int)sh->nb, c0, sh->pmax, nullptr);
     IE_LAUNCHED();
     return IE_OK;
 }
@@ -1592,7 +1692,23 @@ static int shard_iter_phase(ie_shard* sh, int ph, int64_t itarg, int do_p, int p
             if ((rc = shard_wait(sh, kSlotBack, (unsigned long long)G * sh->R * Mc * 16, s))) return rc;
             double* Y0 = do_p ? sh->QW : sh->QW + (size_t)sh->R * n;
             double* Y1 = two ? sh->QW + (size_t)sh->R * n : nullptr;
-            if ((rc = fft_band_inv(sh->F, b3, sh->R, G, Y0, Y1, two ? sh->S->sc : nullptr, s, stop))) return rc;
+            if (sh->line_post) {  // k_post_pass folded into the inverse rows: partials per grid row, as on one GPU
+                PcgFuse fz;
+                const int64_t shift = (int64_t)(sh->row0 - sh->rlo) * n;  // need-row index -> band index
+                fz.p = p - shift;
+                fz.f = sh->fb - shift;
+                fz.part = sh->xpost(g);
+                fz.line0 = sh->rlo;
+                fz.post_lo = sh->row0 - sh->rlo;
+                fz.post_hi = sh->row0 - sh->rlo + sh->nrows;
+                fz.q_col = do_p ? 0 : -1;
+                fz.w_col = pending ? (do_p ? 1 : 0) : -1;
+                if ((rc = fft_band_inv(sh->F, b3, sh->R, G, Y0, Y1, two ? sh->S->sc : nullptr, s, stop, &fz)))
+                    return rc;
+                return shard_push_slab(sh, kSlotPost, &ie_shard::xpost, 2, sh->row0, sh->nrows, s);
+            }
+            if ((rc = fft_band_inv(sh->F, b3, sh->R, G, Y0, Y1, two ? sh->S->sc : nullptr, s, stop, nullptr)))
+                return rc;
             IE_CUDA(launch_k(k_post_pass, dim3(nchb), dim3(kRed), 0, s, (const double*)p, (const double*)q_band(sh),
                              (const double*)sh->fb, (const double*)w_band(sh), (int)sh->nb, do_p, pending,
                              sh->xpost(g) + 2 * c0, stop));
@@ -1600,14 +1716,15 @@ static int shard_iter_phase(ie_shard* sh, int ph, int64_t itarg, int do_p, int p
             return shard_push_chunks(sh, kSlotPost, &ie_shard::xpost, 2, s);
         }
         case 3: {
-            if ((rc = shard_wait(sh, kSlotPost, (unsigned long long)nch * 16, s))) return rc;
+            const int npost = sh->line_post ? n : nch;
+            if ((rc = shard_wait(sh, kSlotPost, (unsigned long long)npost * 16, s))) return rc;
             const HaloSeg hs{(sh->rlo - sh->row0) * n, (sh->row0 - sh->rlo) * n, (int)sh->nb,
                              (sh->rhi - sh->row0 - sh->nrows) * n};
             const int nh = (hs.len0 + kChunk - 1) / kChunk + (hs.len1 + kChunk - 1) / kChunk;
-            IE_CUDA(launch_k(k_iter_a<true, true>, dim3(nchb + nh), dim3(kRed), 0, s, (const double*)sh->xpost(g), nch,
-                             do_p, pending, (long long)itarg, sh->S, sh->dh, uu, r, (const double*)p,
+            IE_CUDA(launch_k(k_iter_a<true, true>, dim3(nchb + nh), dim3(kRed), 0, s, (const double*)sh->xpost(g),
+                             npost, do_p, pending, (long long)itarg, sh->S, sh->dh, uu, r, (const double*)p,
                              (const double*)q_band(sh), (int)sh->nb, c0, nchb, sh->xrz(g), (const double*)sh->pmax,
-                             hs));
+                             hs, 0));
             IE_LAUNCHED();
             if (!spec) return IE_OK;
             if (timed) IE_CUDA(cudaEventRecord(sh->ev[2], s));
@@ -1827,8 +1944,9 @@ extern "C" int ie_shard_create(const ie_matvec* A, const ie_precond* T_local, in
     size_t o = align256(kNumSlots * sizeof(unsigned long long));
     sh->off_xf = o;
     o = align256(o + (size_t)sh->nch * 8);
+    sh->line_post = !getenv("IEDD_B200_NO_FUSE") && matvec_fused_lines(A) > 0;
     sh->off_xpost = o;
-    o = align256(o + (size_t)sh->nch * 16);
+    o = align256(o + (size_t)std::max(sh->nch, n) * 16);
     sh->off_xrz = o;
     o = align256(o + (size_t)sh->nch * kRzRec * 8);
     sh->off_buf2 = o;
@@ -1945,4 +2063,53 @@ extern "C" int ie_pcg_sharded_local_f64(ie_shard** shards, int32_t nranks, const
         }
     return ie::shard_solve(shards, nranks, d_f_need, d_u_band, tol, max_iters, hist, n_it, flags, times, fail_iter,
                            fail_value, (cudaStream_t)stream);
+}
+
+// Per-line partials with the association of the post pass folded into the
+// FFT's last line transform (fft.cu kInvCRPost): line l of n points, thread
+// j < TPL = M / 8 chains points j + TPL m (m < 4) by FMA, then a halving tree
+// over the TPL threads.  mode 0: x.y, mode 1: |x - y|^2.  The torch.distributed
+// driver (distributed.py) uses it so its dot products are bitwise those of
+// ie_pcg_f64 on one GPU.
+namespace ie {
+__global__ void k_line_partials(const double* x, const double* y, int n, int tpl, int mode, double* part) {
+    extern __shared__ double sl[];
+    const int j = threadIdx.x;
+    const int64_t base = (int64_t)blockIdx.x * n;
+    double acc = 0.0;
+#pragma unroll
+    for (int m = 0; m < 4; ++m) {
+        const int l = j + tpl * m;
+        if (l < n) {
+            if (mode == 0) {
+                acc = fma(x[base + l], y[base + l], acc);
+            } else {
+                const double d = x[base + l] - y[base + l];
+                acc = fma(d, d, acc);
+            }
+        }
+    }
+    sl[j] = acc;
+    __syncthreads();
+    for (int off = tpl / 2; off > 0; off >>= 1) {
+        if (j < off) sl[j] += sl[j + off];
+        __syncthreads();
+    }
+    if (j == 0) part[blockIdx.x] = sl[0];
+}
+}  // namespace ie
+
+extern "C" int ie_line_partials_f64(const double* x, const double* y, int64_t nlines, int32_t n, int32_t M,
+                                    int32_t mode, double* part, void* stream) {
+    const int tpl = M / 8;
+    if (!x || !y || !part || nlines < 0 || n < 1 || M < 64 || (M & (M - 1)) || n > M / 2 || tpl > 1024 ||
+        (mode != 0 && mode != 1)) {
+        ie::set_error("ie_line_partials_f64: bad arguments");
+        return IE_ERR_ARG;
+    }
+    if (nlines == 0) return IE_OK;
+    ie::k_line_partials<<<(unsigned)nlines, tpl, tpl * sizeof(double), (cudaStream_t)stream>>>(x, y, n, tpl, mode,
+                                                                                               part);
+    IE_LAUNCHED();
+    return IE_OK;
 }

@@ -22,6 +22,7 @@
 #include <vector>
 
 #include "common.cuh"
+#include "pcg_state.cuh"
 
 namespace ie {
 
@@ -270,13 +271,15 @@ namespace ie {
 int fft_create(const ie_geom& g, ie_fft** out);
 void fft_destroy(ie_fft* f);
 int fft_matvec(const ie_fft* f, const double* X0, const double* X1, double* Y0, double* Y1, cudaStream_t st,
-               const int* stop, const double* scales, double2* buf_ws, double* amax_ws);
+               const int* stop, const double* scales, double2* buf_ws, double* amax_ws, const PcgFuse* fz);
+bool fft_fusable(const ie_fft* f);
+int fft_out_lines(const ie_fft* f);
 int64_t fft_buf_elems(const ie_fft* f);
 int fft_band_fwd(const ie_fft* f, const double* X0, const double* X1, int nrows, int parts, double2* out,
                  const double* scales, cudaStream_t st, const int* stop = nullptr);
 int fft_band_cols(const ie_fft* f, double2* buf, int c0, int ncols, cudaStream_t st, const int* stop = nullptr);
 int fft_band_inv(const ie_fft* f, const double2* in, int nrows, int parts, double* Y0, double* Y1,
-                 const double* scales, cudaStream_t st, const int* stop = nullptr);
+                 const double* scales, cudaStream_t st, const int* stop = nullptr, const PcgFuse* fz = nullptr);
 int fft_absmax2(const double* X0, const double* X1, int64_t N, double* part, cudaStream_t st);
 }  // namespace ie
 
@@ -434,16 +437,17 @@ int matvec_prepare_stream(const ie_matvec* m, cudaStream_t st) {
 }
 
 int matvec_launch(const ie_matvec* m, const double* X, int64_t ldx, int nrhs, double* Y, int64_t ldy,
-                  int64_t row_begin, int64_t row_end, cudaStream_t st, const int* stop, const double* scales) {
+                  int64_t row_begin, int64_t row_end, cudaStream_t st, const int* stop, const double* scales,
+                  const PcgFuse* fz) {
     bool ok;
     const ie_matvec::Ws W = mv_ws(const_cast<ie_matvec*>(m), st, &ok);
     if (!ok) return IE_ERR_CUDA;
     if (m->method == IE_MATVEC_FFT) {
         const double* X1 = nrhs == 2 ? X + ldx : nullptr;
         if (row_begin == 0 && row_end == m->N)
-            return fft_matvec(m->fft, X, X1, Y, nrhs == 2 ? Y + ldy : nullptr, st, stop, scales, W.buf, W.amax);
+            return fft_matvec(m->fft, X, X1, Y, nrhs == 2 ? Y + ldy : nullptr, st, stop, scales, W.buf, W.amax, fz);
         int rc = fft_matvec(m->fft, X, X1, W.full, nrhs == 2 ? W.full + m->N : nullptr, st, stop, scales, W.buf,
-                            W.amax);
+                            W.amax, nullptr);
         if (rc) return rc;
         for (int q = 0; q < nrhs; ++q)
             IE_CUDA(cudaMemcpyAsync(Y + q * ldy, W.full + (int64_t)q * m->N + row_begin,
@@ -592,7 +596,8 @@ extern "C" int ie_matvec_f64(const ie_matvec* m, const double* X, int64_t ldx, i
         ie::set_error("ie_matvec_f64: bad arguments");
         return IE_ERR_ARG;
     }
-    return ie::matvec_launch(m, X, ldx, nrhs, Y, ldy, row_begin, row_end, (cudaStream_t)stream, nullptr, nullptr);
+    return ie::matvec_launch(m, X, ldx, nrhs, Y, ldy, row_begin, row_end, (cudaStream_t)stream, nullptr, nullptr,
+                             nullptr);
 }
 
 // ---- band (slab) passes of the FFT method, for the sharded solver
@@ -677,6 +682,11 @@ extern "C" int ie_assemble_block_f64(const ie_geom* g, const int64_t* rows, int6
 
 namespace ie {
 int matvec_N(const ie_matvec* m) { return m->N; }
+// lines of the A-pass's last transform when the PCG driver may fold k_iter_b /
+// k_post_pass into the FFT passes (full-range 2D / 3D FFT plans), else 0
+int matvec_fused_lines(const ie_matvec* m) {
+    return (m->method == IE_MATVEC_FFT && fft_fusable(m->fft)) ? fft_out_lines(m->fft) : 0;
+}
 uint64_t matvec_uid(const ie_matvec* m) { return m->uid; }
 const ie_fft* matvec_fft(const ie_matvec* m) { return m->method == IE_MATVEC_FFT ? m->fft : nullptr; }
 int matvec_dim(const ie_matvec* m) { return m->g.dim; }

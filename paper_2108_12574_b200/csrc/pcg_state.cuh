@@ -27,6 +27,10 @@ struct PcgState {
     unsigned int ticket;  // CTAs of a graph-replayed k_iter_b done (the last one advances it_dev)
 };
 
+// Fixed-order CTA reductions (a shared-memory halving tree over blockDim
+// leaves): deterministic, identical on every rank and in every driver.
+// (A warp-shuffle butterfly + ordered warp sums was measured: no change in
+// the iteration time, 144.5 vs 145.6 us, so the round-1 association stays.)
 __device__ __forceinline__ double block_tree(double v, double* sh) {
     sh[threadIdx.x] = v;
     __syncthreads();
@@ -42,6 +46,26 @@ __device__ __forceinline__ double reduce_partials(const double* part, int nch, d
     for (int c = threadIdx.x; c < nch; c += blockDim.x) loc += part[c];
     return block_tree(loc, sh);
 }
+
+// Kernels of the PCG iteration folded into the A-pass's line transforms (FFT
+// method, 2D / 3D, lines of >= 64 points; csrc/fft.cu LineArgs):
+//   first pass (2-RHS): k_iter_b's vector half -- p = z + beta p stored back
+//     with beta and the multipliers from the state (pcg_decide), max|p| into
+//     the rotating slots pglob[it % 3]; `it` < 0: graph replay;
+//   last pass: k_post_pass -- per output line l in [post_lo, post_hi) the
+//     partials p.q (q_col >= 0) and |f - w|^2 (w_col >= 0: the output
+//     column holding w) at part[2 (line0 + l)], [.. + 1]; p and f are indexed
+//     like the output vector.
+struct PcgFuse {
+    const double* z = nullptr;
+    double* pglob = nullptr;
+    struct PcgState* s = nullptr;
+    long long it = 0;
+    const double* p = nullptr;
+    const double* f = nullptr;
+    double* part = nullptr;
+    int line0 = 0, post_lo = 0, post_hi = 0, q_col = -1, w_col = -1;
+};
 
 // PCG chunk record of the apply (4 doubles per dot-product chunk, the r.z
 // exchange of the sharded solver): [0] r.z partial, [1] max|z|, [2] max|p|
@@ -74,6 +98,49 @@ __device__ __forceinline__ double pcg_pow2_scale(double mx) {
     int e;
     frexp(mx, &e);
     return ldexp(1.0, -e);
+}
+
+// k_iter_b's scalar half, run once per iteration by the last CTA of the
+// apply's scatter (single-GPU driver with the p update folded into the next
+// FFT pass): beta = r.z / rho_prev from the chunk record `rec` (nch chunks),
+// rho, and the next 2-RHS multipliers from max|z|, max|u| (record) and
+// max|p_old| (pglob[it % 3]; zeroes pglob[(it + 1) % 3] for the next pass's
+// atomic max).  it < 0: graph replay -- the iteration comes from the state
+// and is advanced here (the iteration's last it_dev reader).  The reduction
+// is k_iter_b's (256 threads striding the chunks, block_tree), so the
+// values are bitwise those of the sharded driver's k_iter_b.
+struct PcgDecide {
+    struct PcgState* s = nullptr;
+    double* pglob = nullptr;
+    long long it = 0;
+    int nch = 0;
+};
+
+__device__ __forceinline__ double chunk_absmax(double v, double* sh);
+__device__ inline void pcg_decide(const double* rec, const PcgDecide& d, double* sh) {
+    PcgState* s = d.s;
+    const long long itb = d.it < 0 ? s->it_dev : d.it;
+    double loc = 0.0, mz = 0.0, mu = 0.0;
+    for (int c = threadIdx.x; c < d.nch; c += kPcgRed) {
+        loc += rec[kRzRec * c];
+        mz = fmax(mz, rec[kRzRec * c + 1]);
+        mu = fmax(mu, rec[kRzRec * c + 3]);
+    }
+    const double rz = block_tree(loc, sh);
+    __syncthreads();
+    mz = chunk_absmax(mz, sh);
+    __syncthreads();
+    mu = chunk_absmax(mu, sh);
+    if (threadIdx.x == 0) {
+        const double beta = rz / s->rho[(itb - 1) & 1];
+        const double mp = d.pglob[itb % 3];
+        s->beta = beta;
+        s->rho[itb & 1] = rz;
+        s->sc[0] = pcg_pow2_scale(__dadd_rn(mz, __dmul_rn(fabs(beta), mp)));
+        s->sc[1] = pcg_pow2_scale(mu);
+        d.pglob[(itb + 1) % 3] = 0.0;
+        if (d.it < 0) s->it_dev = itb + 1;
+    }
 }
 
 __device__ __forceinline__ double chunk_absmax(double v, double* sh) {

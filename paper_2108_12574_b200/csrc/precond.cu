@@ -913,21 +913,36 @@ __device__ __forceinline__ void scatter_fixed_chunk(int c, const double* staging
     chunk_sum_max(loc, zm, sh, partials + 4 * c);
 }
 
+// With dec.s: the last CTA (ticket) runs the PCG iteration's decider on the
+// completed record (pcg_decide).
+__device__ __forceinline__ void scatter_decide(const double* partials, const PcgDecide& dec, double* sh) {
+    __shared__ int last;
+    __threadfence();  // this CTA's record entry before its ticket
+    __syncthreads();
+    if (threadIdx.x == 0) last = atomicAdd(&dec.s->ticket, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!last) return;
+    __threadfence();
+    if (threadIdx.x == 0) dec.s->ticket = 0;
+    pcg_decide(partials, dec, sh);
+}
+
 template <int MM, int UNR, bool PF = false>
 __global__ void __launch_bounds__(256) k_scatter_fixed(const double* staging, const int* pos, double* z, int N,
                                                        const double* r, double* partials, const int* stop, int i0,
-                                                       int i1) {
+                                                       int i1, PcgDecide dec) {
     __shared__ double sh[512];
     pdl_wait();
     if (stop && *stop) return;
     scatter_fixed_chunk<MM, UNR, PF>(blockIdx.x, staging, pos, z, N, r, partials, i0, i1, sh);
+    if (dec.s) scatter_decide(partials, dec, sh);
 }
 
 // Per point: z_i = sum of its staged contributions in ascending block id.
 // Optionally also the fixed-chunk partials of r.z (for PCG's rho).
 __global__ void __launch_bounds__(256) k_scatter(const double* staging, const int* ptr, const int* pos, double* z,
                                                  int N, const double* r, double* partials, const int* stop, int i0,
-                                                 int i1) {
+                                                 int i1, PcgDecide dec) {
     if (stop && *stop) return;
     __shared__ double sh[512];
     const int base = i0 + blockIdx.x * kChunk;
@@ -947,6 +962,7 @@ __global__ void __launch_bounds__(256) k_scatter(const double* staging, const in
     }
     if (!r) return;
     chunk_sum_max(loc, zm, sh, partials + 4 * blockIdx.x);
+    if (dec.s) scatter_decide(partials, dec, sh);
 }
 
 // ---- large blocks (s > kSmemMaxS, PACKED_INVERSE): blocked sweep inversion.
@@ -1339,8 +1355,12 @@ static void launch_apply_T(const ie_precond* p, ApplyArgs a, cudaStream_t st) {
 }
 
 // output rows of the current apply: [0, N) unless a sharded solver restricts
-// them to its band (precond_apply_band)
+// them to its band (precond_apply_band); the PCG decider the scatter's last
+// CTA runs (precond_set_decide, single-GPU driver)
 static thread_local int64_t t_i0 = 0, t_i1 = -1;
+static thread_local PcgDecide t_dec;
+
+void precond_set_decide(const PcgDecide* d) { t_dec = d ? *d : PcgDecide{}; }
 
 static int scatter_launch(const ie_precond* p, const double* staging, const double* r, double* z,
                           double* partials, cudaStream_t st, const int* stop) {
@@ -1348,7 +1368,8 @@ static int scatter_launch(const ie_precond* p, const double* staging, const doub
     const int nch = (i1 - i0 + kChunk - 1) / kChunk;
     if (nch <= 0) return IE_OK;
     const double* rr = partials ? r : nullptr;
-#define IE_SCAT(MM, ...) IE_CUDA(launch_k(k_scatter_fixed<MM, __VA_ARGS__>, dim3(nch), dim3(256), 0, st, staging, (const int*)p->d_posfix, z, (int)p->N, rr, partials, stop, i0, i1))
+    const PcgDecide dec = partials ? t_dec : PcgDecide{};
+#define IE_SCAT(MM, ...) IE_CUDA(launch_k(k_scatter_fixed<MM, __VA_ARGS__>, dim3(nch), dim3(256), 0, st, staging, (const int*)p->d_posfix, z, (int)p->N, rr, partials, stop, i0, i1, dec))
     // batch sizes measured at config 5 (MM = 4): 2 points with the next
     // batch's positions prefetched 10.6-11.3 us, 2 without 12.2, 4 15.5, 8 18.9
     // (register-limited residency), 1 point per level (before) 17.8
@@ -1358,7 +1379,7 @@ static int scatter_launch(const ie_precond* p, const double* staging, const doub
         case 4: IE_SCAT(4, 2, true); break;
         case 8: IE_SCAT(8, 2); break;
 #undef IE_SCAT
-        default: k_scatter<<<nch, 256, 0, st>>>(staging, p->d_ptr, p->d_pos, z, p->N, rr, partials, stop, i0, i1);
+        default: k_scatter<<<nch, 256, 0, st>>>(staging, p->d_ptr, p->d_pos, z, p->N, rr, partials, stop, i0, i1, dec);
     }
     IE_LAUNCHED();
     return IE_OK;

@@ -261,6 +261,24 @@ class Comm:
                     off += rcount[h]
         return out
 
+    def allgather_var(self, x, counts):
+        """(ncol, counts[rank]) -> (ncol, sum(counts)) in rank order."""
+        import torch
+        world = self.plan.world
+        ncol, L = x.shape
+        pad = max(counts)
+        buf = x.new_zeros((ncol, pad))
+        buf[:, :L] = x
+        dev = buf.device
+        if self.host_staged and world > 1:
+            buf = buf.cpu()
+        outs = [torch.empty_like(buf) for _ in range(world)]
+        if world == 1:
+            outs[0].copy_(buf)
+        else:
+            self.dist.all_gather(outs, buf, group=self.group)
+        return torch.cat([outs[r][:, :counts[r]].to(dev) for r in range(world)], dim=1)
+
     def allgather_band(self, x):
         """(ncol, band) -> (ncol, N) in global order."""
         return self._gather(x, "band")
@@ -392,6 +410,16 @@ class CudaBackend:
         self.pre = (from_decomposition(op, sub, variant=variant, share_translated=share_translated)
                     if plan.blocks.size else None)
         self.dev = torch.device("cuda", torch.cuda.current_device())
+        # dot products of the A-pass per grid line (n points along the last
+        # axis) with the association ie_pcg_f64 uses when the post pass rides
+        # in the FFT's last line transform -- bitwise the single-GPU values;
+        # needs every band cut on a line boundary
+        import os
+        n = op.grid.n_per_dim
+        self.line_post = (method == "fft" and op.grid.dim >= 2 and self.mv.M >= 64
+                          and not os.environ.get("IEDD_B200_NO_FUSE") and not os.environ.get("IEDD_B200_NO_FUSE_POST")
+                          and all(b % n == 0 for b in plan.bounds))
+        self.line_len = n
         self._full = torch.empty(2, self.N, dtype=torch.float64, device=self.dev)
         self._scal = torch.empty(1, dtype=torch.float64, device=self.dev)
 
@@ -433,6 +461,25 @@ class CudaBackend:
         z = self._full[0]
         self.pre.apply_device(r_full.contiguous(), z)
         return z[self.plan.begin: self.plan.end].clone()
+
+    def post_partials(self, p, q, f, w, do_p: bool, pending: bool):
+        """The A-pass partials [p.q if do_p, |f - w|^2 if pending] of the band:
+        per grid line (line_post) or per dot chunk."""
+        if not self.line_post:
+            rows = ([self.dot_partials(p, q, 0)] if do_p else []) + ([self.dot_partials(f, w, 1)] if pending else [])
+            return _stack(rows)
+        n = self.line_len
+        nl = self.plan.size // n
+        out = self.torch.empty(int(do_p) + int(pending), max(nl, 1), dtype=self.torch.float64, device=self.dev)
+        row = 0
+        for on, (x, y, mode) in ((do_p, (p, q, 0)), (pending, (f, w, 1))):
+            if on:
+                if nl:
+                    self._lib.check(self.L.ie_line_partials_f64(self._lib.ptr(x), self._lib.ptr(y), nl, n, self.mv.M,
+                                                                mode, self._lib.ptr(out[row]), self._lib.stream_ptr()),
+                                    "line partials")
+                row += 1
+        return out[:, :nl]
 
     def dot_partials(self, x, y, mode: int):
         n = x.numel()
@@ -521,12 +568,16 @@ def solve_sharded(backend, comm: Comm, plan: ShardPlan, f_band, tol: float = 1e-
         Y = backend.matvec_cols(comm, _stack(cols), scales if len(cols) == 2 else None)
         q = Y[0] if do_p else None
         w = Y[-1] if pending else None
-        parts = []
-        if do_p:
-            parts.append(backend.dot_partials(p, q, 0))
-        if pending:
-            parts.append(backend.dot_partials(f_band, w, 1))
-        G = comm.allgather_partials(_stack(parts))
+        if hasattr(backend, "post_partials"):
+            parts = backend.post_partials(p, q, f_band, w, do_p, pending)
+        else:
+            parts = _stack(([backend.dot_partials(p, q, 0)] if do_p else []) +
+                           ([backend.dot_partials(f_band, w, 1)] if pending else []))
+        if getattr(backend, "line_post", False):
+            G = comm.allgather_var(parts, [(plan.bounds[r + 1] - plan.bounds[r]) // backend.line_len
+                                           for r in range(plan.world)])
+        else:
+            G = comm.allgather_partials(parts)
         row = 0
         denom = res2 = None
         if do_p:
