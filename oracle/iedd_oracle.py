@@ -234,9 +234,12 @@ def build_operator(grid: Grid, lattice: str | None = None) -> Operator:
 
 class FFTMatvec:
     """toeplitz.py:11-53: (2n)^d circulant embedding of the multilevel
-    Toeplitz operator, applied with real FFTs."""
+    Toeplitz operator, applied with real FFTs.  workers > 1 (bench.py's CPU
+    reference arm only): the same pocketfft transforms through scipy.fft on
+    that many host threads."""
 
-    def __init__(self, op: Operator):
+    def __init__(self, op: Operator, workers: int = 1):
+        self.workers = workers
         self.dim, self.n = op.grid.dim, op.grid.n_per_dim
         n, d = self.n, self.dim
         emb = np.zeros((2 * n,) * d)
@@ -257,8 +260,13 @@ class FFTMatvec:
             raise ValueError(f"expected vector of length {N}, got shape {v.shape}")
         pad = np.zeros(self.shape_emb)
         pad[(slice(0, self.n),) * self.dim] = v.reshape((self.n,) * self.dim)
-        out = np.fft.irfftn(np.fft.rfftn(pad) * self.symbol, s=self.shape_emb,
-                            axes=tuple(range(self.dim)))
+        if self.workers > 1:
+            import scipy.fft as sfft
+            out = sfft.irfftn(sfft.rfftn(pad, workers=self.workers) * self.symbol, s=self.shape_emb,
+                              axes=tuple(range(self.dim)), workers=self.workers)
+        else:
+            out = np.fft.irfftn(np.fft.rfftn(pad) * self.symbol, s=self.shape_emb,
+                                axes=tuple(range(self.dim)))
         return out[(slice(0, self.n),) * self.dim].reshape(N)
 
     __call__ = matvec
@@ -309,6 +317,71 @@ class SchwarzPrecond:
             inv = sla.cho_solve((g, False), np.eye(idx.size))
             out[np.ix_(idx, idx)] += inv
         return 0.5 * (out + out.T)
+
+
+class PooledApply:
+    """SchwarzPrecond.apply on all host cores (bench.py's CPU reference arm
+    only): worker processes forked after the factorisation (the factors are
+    shared copy-on-write) each solve a contiguous range of blocks with the
+    same two solve_triangular calls into a shared staging buffer; the parent
+    accumulates out[idx_k] += z_k in ascending k (np.add.at applies the updates
+    in order), exactly the reference's sum.  Threads do not help here: the
+    per-block scipy call overhead holds the GIL (measured, c3: 61 ms at 1 and
+    at 8 threads)."""
+
+    def __init__(self, pre: "SchwarzPrecond", nproc: int):
+        import multiprocessing as mp
+        from multiprocessing import shared_memory
+        self.pre = pre
+        self.n = pre.n
+        sizes = np.array([i.size for i in pre.indices])
+        self.off = np.concatenate([[0], np.cumsum(sizes)])
+        self.cat = np.concatenate(pre.indices)
+        self._f = shared_memory.SharedMemory(create=True, size=8 * pre.n)
+        self._z = shared_memory.SharedMemory(create=True, size=8 * int(self.off[-1]))
+        D = len(pre.indices)
+        self.ranges = [(D * t // nproc, D * (t + 1) // nproc) for t in range(nproc)]
+        global _POOL_STATE
+        _POOL_STATE = (pre, self.off, self._f.name, self._z.name)
+        self.pool = mp.get_context("fork").Pool(nproc)
+        self.fbuf = np.ndarray((pre.n,), dtype=np.float64, buffer=self._f.buf)
+        self.zbuf = np.ndarray((int(self.off[-1]),), dtype=np.float64, buffer=self._z.buf)
+
+    def apply(self, f):
+        self.fbuf[:] = np.asarray(f, dtype=float)
+        self.pool.map(_pooled_solve, self.ranges)
+        out = np.zeros(self.n)
+        np.add.at(out, self.cat, self.zbuf)
+        return out
+
+    __call__ = apply
+
+    def close(self):
+        self.pool.terminate()
+        self._f.close()
+        self._f.unlink()
+        self._z.close()
+        self._z.unlink()
+
+
+_POOL_STATE = None
+
+
+def _pooled_solve(rng):
+    from multiprocessing import shared_memory
+    pre, off, fname, zname = _POOL_STATE
+    fs = shared_memory.SharedMemory(name=fname)
+    zs = shared_memory.SharedMemory(name=zname)
+    f = np.ndarray((pre.n,), dtype=np.float64, buffer=fs.buf)
+    z = np.ndarray((int(off[-1]),), dtype=np.float64, buffer=zs.buf)
+    for k in range(*rng):
+        g = pre.factors[k]
+        y = sla.solve_triangular(g, f[pre.indices[k]], trans="T", lower=False, check_finite=False)
+        z[off[k]:off[k + 1]] = sla.solve_triangular(g, y, trans="N", lower=False, check_finite=False)
+    del f, z
+    fs.close()
+    zs.close()
+    return 0
 
 
 # --------------------------------------------------------------------------

@@ -1003,6 +1003,13 @@ def bench_sharded(args, metric, cfg, workload, config_keys=None, cpu_baseline=No
                "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
                "data": "synthetic (BASELINE.json config 5, seeded)", "config": config,
                "n_it": rep.n_it, "parity": parity,
+               "exchange": ({"points_per_iteration": 4,
+                             "bytes_out_per_rank_per_iteration": int(
+                                 rows * backend.mv.M * 16                               # FWD: row spectra
+                                 + need_rows * backend.mv.M * 16                        # BACK: need rows of the slab
+                                 + ws * (rows * 16 + (plan.size // CHUNK) * 32)),       # POST, RZ slabs
+                             "transport": "NVLink peer stores (CUDA IPC) + mailbox counters"}
+                            if native else {"transport": "torch.distributed collectives"}),
                "e2e": {"value": args.steps / statistics.median(e2e), "unit": "iter/s",
                        "h2d_bytes_per_step": 8 * op.n / args.steps, "d2h_bytes_per_step": 8 * op.n / args.steps,
                        "note": "per solve of K steps: every rank's H2D of its f rows and D2H of its u band "
