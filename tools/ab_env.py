@@ -2,6 +2,7 @@
 alternating processes, median of the per-process best of 5 timed solves.
 
   python tools/ab_env.py IEDD_B200_NO_L2PERSIST [reps]
+  python tools/ab_env.py IEDD_B200_LIB=/path/to/other/libiedd_b200.so [reps]
 """
 import json
 import os
@@ -29,7 +30,8 @@ print(json.dumps({"ms_per_iter": best / 50}))
 
 
 def main():
-    var = sys.argv[1]
+    var, _, val = sys.argv[1].partition("=")
+    val = val or "1"
     reps = int(sys.argv[2]) if len(sys.argv) > 2 else 3
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
     res = {"off": [], "on": []}
@@ -38,7 +40,7 @@ def main():
             env = dict(os.environ, IEDD_ROOT=root)
             env.pop(var, None)
             if key == "on":
-                env[var] = "1"
+                env[var] = val
             out = subprocess.run([sys.executable, "-c", CHILD], env=env, capture_output=True, text=True)
             line = [ln for ln in out.stdout.splitlines() if ln.startswith("{")]
             if not line:
