@@ -118,6 +118,25 @@ struct LineArgs {
     int post_lo, post_hi;
     int post_q_col;
     int post_w_col;
+    // Sharded transposes folded into the band passes' stores (krylov.cu
+    // ie_pcg_sharded_*): the complex outputs go straight into the peers'
+    // memory over NVLink, and every CTA release-adds its bytes to each peer's
+    // mailbox counter after its stores.
+    //  peer_mode 1 (band rows forward, FWD): output column l belongs to slab
+    //    h = l >> out_lsplit; element (line o, l) -> peer[h] + o out_so +
+    //    (l & (2^out_lsplit - 1)) out_sl (peer[h] already offset to the
+    //    sender's rows); every line sends peer_line_bytes[h] to each peer;
+    //  peer_mode 2 (column slab, BACK): output row l goes to every rank h whose
+    //    need rows [peer_rlo[h], peer_rhi[h]) contain it (the owner l /
+    //    peer_band_rows and its two neighbours' halos): peer[h] + (l -
+    //    peer_rlo[h]) out_sl + i (peer[h] offset to the sender's slab block).
+    int peer_mode;
+    int npeer;
+    int peer_band_rows;
+    double2* peer[16];
+    unsigned long long* peer_ctr[16];
+    long long peer_line_bytes[16];
+    int peer_rlo[16], peer_rhi[16];
 };
 
 // 2^-e with 2^e >= max|x| (power of two, exact); 1 for max == 0
@@ -1112,6 +1131,36 @@ __global__ void __launch_bounds__(PTS == 16 ? 256 : 1024, PTS == 16 ? 2 : 1) k_f
         }
         return;
     }
+    if constexpr (!out_real && !tma_mode) {
+        if (a.peer_mode) {  // sharded transposes: stores into the peers' buffers, then the mailbox signals
+            if (live) {
+#pragma unroll
+                for (int m = 0; m < PTS; ++m) {
+                    const int l = j + TPL * m;
+                    if (l >= a.n_out) continue;
+                    const double2 v = make_double2(vr[m], vi[m]);
+                    if (a.peer_mode == 1) {
+                        a.peer[l >> a.out_lsplit][(int64_t)o * a.out_so + (int64_t)i * a.out_si +
+                                                  (int64_t)(l & ((1 << a.out_lsplit) - 1)) * a.out_sl] = v;
+                    } else {
+                        const int own = l / a.peer_band_rows;
+                        for (int h = max(0, own - 1); h <= min(a.npeer - 1, own + 1); ++h)
+                            if (l >= a.peer_rlo[h] && l < a.peer_rhi[h])
+                                a.peer[h][(int64_t)(l - a.peer_rlo[h]) * a.out_sl + i] = v;
+                    }
+                }
+            }
+            __syncthreads();
+            if ((int)threadIdx.x < a.npeer) {
+                const int G8 = TMA ? 2 : a.g8;
+                const long long lines = min(G8, a.nlines - (int)blockIdx.x * G8);
+                __threadfence_system();
+                atomicAdd_system(a.peer_ctr[threadIdx.x],
+                                 (unsigned long long)(lines * a.peer_line_bytes[threadIdx.x]));
+            }
+            return;
+        }
+    }
     if (!live) return;
 #pragma unroll
     for (int m = 0; m < PTS; ++m) {
@@ -1513,8 +1562,22 @@ static int band_check(const ie_fft* f, int parts) {
 
 int fft_M(const ie_fft* f) { return f->M; }
 
+static void apply_peers(LineArgs& a, const PeerStores* ps) {
+    if (!ps || !ps->mode) return;
+    a.peer_mode = ps->mode;
+    a.npeer = ps->npeer;
+    a.peer_band_rows = ps->band_rows;
+    for (int h = 0; h < ps->npeer; ++h) {
+        a.peer[h] = ps->peer[h];
+        a.peer_ctr[h] = ps->ctr[h];
+        a.peer_line_bytes[h] = ps->line_bytes[h];
+        a.peer_rlo[h] = ps->rlo[h];
+        a.peer_rhi[h] = ps->rhi[h];
+    }
+}
+
 int fft_band_fwd(const ie_fft* f, const double* X0, const double* X1, int nrows, int parts, double2* out,
-                 const double* scales, cudaStream_t st, const int* stop) {
+                 const double* scales, cudaStream_t st, const int* stop, const PeerStores* ps) {
     int rc = band_check(f, parts);
     if (rc) return rc;
     const int n = f->n, Mc = f->M / parts;
@@ -1540,10 +1603,12 @@ int fft_band_fwd(const ie_fft* f, const double* X0, const double* X1, int nrows,
         a.scales = scales;
         a.scale_in = 1;
     }
+    apply_peers(a, ps);
     return line_launch(a, st);
 }
 
-int fft_band_cols(const ie_fft* f, double2* buf, int c0, int ncols, cudaStream_t st, const int* stop) {
+int fft_band_cols(const ie_fft* f, double2* buf, int c0, int ncols, cudaStream_t st, const int* stop,
+                  const PeerStores* ps) {
     int rc = band_check(f, 1);
     if (rc) return rc;
     if (ncols <= 0 || (ncols & (ncols - 1)) || c0 < 0 || c0 + ncols > f->M) {
@@ -1562,6 +1627,7 @@ int fft_band_cols(const ie_fft* f, double2* buf, int c0, int ncols, cudaStream_t
     c.n_out = f->n;
     c.fused = 1;
     c.stop = stop;
+    apply_peers(c, ps);
     return line_launch(c, st);
 }
 

@@ -1414,8 +1414,9 @@ int matvec_dim(const ie_matvec* m);
 int matvec_n(const ie_matvec* m);
 int fft_M(const ie_fft* f);
 int fft_band_fwd(const ie_fft* f, const double* X0, const double* X1, int nrows, int parts, double2* out,
-                 const double* scales, cudaStream_t st, const int* stop);
-int fft_band_cols(const ie_fft* f, double2* buf, int c0, int ncols, cudaStream_t st, const int* stop);
+                 const double* scales, cudaStream_t st, const int* stop, const PeerStores* ps);
+int fft_band_cols(const ie_fft* f, double2* buf, int c0, int ncols, cudaStream_t st, const int* stop,
+                  const PeerStores* ps);
 int fft_band_inv(const ie_fft* f, const double2* in, int nrows, int parts, double* Y0, double* Y1,
                  const double* scales, cudaStream_t st, const int* stop, const PcgFuse* fz);
 int precond_apply_band(const ie_precond* p, const double* r, double* z, double* partials, int64_t i0, int64_t i1,
@@ -1513,6 +1514,7 @@ struct ie_shard {
     int nrows = 0, row0 = 0, rlo = 0, rhi = 0, R = 0, Rmax = 0;
     int nch = 0, nchb = 0, c0 = 0;
     bool line_post = false;  // k_post_pass folded into the inverse rows (per-row partials), as ie_pcg_f64 does
+    bool fused_transposes = true;  // FWD / BACK written by the band passes into the peers (no push kernels)
     std::vector<int> row0_all, nrows_all, rlo_all, rhi_all;
     // symmetric exchange heap (IPC-exported): mailbox counters, F partials,
     // POST partials, RZ records, column slab, need-row block
@@ -1668,8 +1670,20 @@ static int shard_iter_phase(ie_shard* sh, int ph, int64_t itarg, int do_p, int p
     switch (ph) {
         case 0: {
             const double* X0 = do_p ? p : uu;
+            if (G > 1 && sh->fused_transposes) {  // the row spectra go straight into the slab owners' buffers
+                PeerStores ps;
+                ps.mode = 1;
+                ps.npeer = G;
+                for (int h = 0; h < G; ++h) {
+                    ps.peer[h] = sh->buf2(h) + (size_t)sh->row0 * Mc;
+                    ps.ctr[h] = sh->mb(h) + kSlotFwd;
+                    ps.line_bytes[h] = (long long)Mc * 16;
+                }
+                return fft_band_fwd(sh->F, X0, two ? uu : nullptr, sh->nrows, G, b1, two ? sh->S->sc : nullptr, s,
+                                    stop, &ps);
+            }
             if ((rc = fft_band_fwd(sh->F, X0, two ? uu : nullptr, sh->nrows, G, b1, two ? sh->S->sc : nullptr, s,
-                                   stop)))
+                                   stop, nullptr)))
                 return rc;
             PushDesc d[kMaxRanks];
             for (int h = 0; h < G; ++h)
@@ -1679,7 +1693,22 @@ static int shard_iter_phase(ie_shard* sh, int ph, int64_t itarg, int do_p, int p
         }
         case 1: {
             if ((rc = shard_wait(sh, kSlotFwd, (unsigned long long)n * Mc * 16, s))) return rc;
-            if ((rc = fft_band_cols(sh->F, sh->buf2(g), g * Mc, Mc, s, stop))) return rc;
+            if (G > 1 && sh->fused_transposes) {  // the column results go straight into every rank's need rows
+                PeerStores ps;
+                ps.mode = 2;
+                ps.npeer = G;
+                ps.band_rows = sh->nrows;
+                for (int h = 0; h < G; ++h) {
+                    const int Rh = sh->rhi_all[h] - sh->rlo_all[h];
+                    ps.peer[h] = sh->buf3(h) + (size_t)g * Rh * Mc;
+                    ps.ctr[h] = sh->mb(h) + kSlotBack;
+                    ps.line_bytes[h] = (long long)Rh * 16;
+                    ps.rlo[h] = sh->rlo_all[h];
+                    ps.rhi[h] = sh->rhi_all[h];
+                }
+                return fft_band_cols(sh->F, sh->buf2(g), g * Mc, Mc, s, stop, &ps);
+            }
+            if ((rc = fft_band_cols(sh->F, sh->buf2(g), g * Mc, Mc, s, stop, nullptr))) return rc;
             PushDesc d[kMaxRanks];
             for (int h = 0; h < G; ++h) {
                 const int Rh = sh->rhi_all[h] - sh->rlo_all[h];
@@ -1945,6 +1974,7 @@ extern "C" int ie_shard_create(const ie_matvec* A, const ie_precond* T_local, in
     sh->off_xf = o;
     o = align256(o + (size_t)sh->nch * 8);
     sh->line_post = !getenv("IEDD_B200_NO_FUSE") && matvec_fused_lines(A) > 0;
+    sh->fused_transposes = !getenv("IEDD_B200_PUSH_TRANSPOSES");
     sh->off_xpost = o;
     o = align256(o + (size_t)std::max(sh->nch, n) * 16);
     sh->off_xrz = o;

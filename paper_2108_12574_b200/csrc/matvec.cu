@@ -276,8 +276,9 @@ bool fft_fusable(const ie_fft* f);
 int fft_out_lines(const ie_fft* f);
 int64_t fft_buf_elems(const ie_fft* f);
 int fft_band_fwd(const ie_fft* f, const double* X0, const double* X1, int nrows, int parts, double2* out,
-                 const double* scales, cudaStream_t st, const int* stop = nullptr);
-int fft_band_cols(const ie_fft* f, double2* buf, int c0, int ncols, cudaStream_t st, const int* stop = nullptr);
+                 const double* scales, cudaStream_t st, const int* stop = nullptr, const PeerStores* ps = nullptr);
+int fft_band_cols(const ie_fft* f, double2* buf, int c0, int ncols, cudaStream_t st, const int* stop = nullptr,
+                  const PeerStores* ps = nullptr);
 int fft_band_inv(const ie_fft* f, const double2* in, int nrows, int parts, double* Y0, double* Y1,
                  const double* scales, cudaStream_t st, const int* stop = nullptr, const PcgFuse* fz = nullptr);
 int fft_absmax2(const double* X0, const double* X1, int64_t N, double* part, cudaStream_t st);

@@ -67,6 +67,17 @@ struct PcgFuse {
     int line0 = 0, post_lo = 0, post_hi = 0, q_col = -1, w_col = -1;
 };
 
+// The sharded driver's transposes folded into the band FFT passes (see
+// LineArgs peer_*): mode 1 = row spectra -> column-slab owners, mode 2 =
+// column slab -> every rank's need rows.
+struct PeerStores {
+    int mode = 0, npeer = 0, band_rows = 0;
+    double2* peer[16] = {};
+    unsigned long long* ctr[16] = {};
+    long long line_bytes[16] = {};
+    int rlo[16] = {}, rhi[16] = {};
+};
+
 // PCG chunk record of the apply (4 doubles per dot-product chunk, the r.z
 // exchange of the sharded solver): [0] r.z partial, [1] max|z|, [2] max|p|
 // of the current search direction, [3] max|u| of the current iterate.
