@@ -137,6 +137,11 @@ struct LineArgs {
     unsigned long long* peer_ctr[16];
     long long peer_line_bytes[16];
     int peer_rlo[16], peer_rhi[16];
+    // sharded POST exchange folded into kInvCRPost: the line partials also go
+    // to every peer's array (same index), then the CTA's bytes to its mailbox
+    int post_npeer;
+    double* post_peer[16];
+    unsigned long long* post_ctr[16];
 };
 
 // 2^-e with 2^e >= max|x| (power of two, exact); 1 for max == 0
@@ -1126,8 +1131,24 @@ __global__ void __launch_bounds__(PTS == 16 ? 256 : 1024, PTS == 16 ? 2 : 1) k_f
         }
         line_pair_tree(pa, pb, j, g, TPL, sm8);
         if (live && j == 0 && line >= a.post_lo && line < a.post_hi) {
-            a.post_part[2 * ((int64_t)a.post_line0 + line)] = pa;
-            a.post_part[2 * ((int64_t)a.post_line0 + line) + 1] = pb;
+            const int64_t ix = 2 * ((int64_t)a.post_line0 + line);
+            a.post_part[ix] = pa;
+            a.post_part[ix + 1] = pb;
+            for (int h = 0; h < a.post_npeer; ++h) {
+                a.post_peer[h][ix] = pa;
+                a.post_peer[h][ix + 1] = pb;
+            }
+        }
+        if (a.post_npeer) {  // every CTA signals the bytes its owned lines sent
+            __syncthreads();
+            if ((int)threadIdx.x < a.post_npeer) {
+                const int G8 = a.g8, l0 = (int)blockIdx.x * G8;
+                const int lo = max(l0, a.post_lo), hi = min(min(l0 + G8, a.nlines), a.post_hi);
+                if (hi > lo) {
+                    __threadfence_system();
+                    atomicAdd_system(a.post_ctr[threadIdx.x], (unsigned long long)(hi - lo) * 16ull);
+                }
+            }
         }
         return;
     }
@@ -1529,6 +1550,11 @@ static void apply_fuse(LineArgs& a, const PcgFuse* fz) {
         a.scale_in = 1;
     }
     if (a.out_real && fz->part) {
+        a.post_npeer = fz->npeer;
+        for (int h = 0; h < fz->npeer; ++h) {
+            a.post_peer[h] = fz->part_peer[h];
+            a.post_ctr[h] = fz->part_ctr[h];
+        }
         a.post_p = fz->p;
         a.post_f = fz->f;
         a.post_part = fz->part;

@@ -46,6 +46,7 @@ int matvec_prepare_stream(const ie_matvec* m, cudaStream_t st);
 int precond_apply(const ie_precond* p, const double* r, double* z, double* partials, cudaStream_t st,
                   const int* stop);
 void precond_set_decide(const PcgDecide* d);
+void precond_set_peer_record(const PeerRec* r);
 int matvec_N(const ie_matvec* m);
 uint64_t matvec_uid(const ie_matvec* m);
 uint64_t precond_uid(const ie_precond* p);
@@ -1732,6 +1733,14 @@ static int shard_iter_phase(ie_shard* sh, int ph, int64_t itarg, int do_p, int p
                 fz.post_hi = sh->row0 - sh->rlo + sh->nrows;
                 fz.q_col = do_p ? 0 : -1;
                 fz.w_col = pending ? (do_p ? 1 : 0) : -1;
+                if (G > 1 && sh->fused_transposes) {  // the partials go straight to every rank (own one included)
+                    fz.npeer = G;
+                    for (int h = 0; h < G; ++h) {
+                        fz.part_peer[h] = sh->xpost(h);
+                        fz.part_ctr[h] = sh->mb(h) + kSlotPost;
+                    }
+                    return fft_band_inv(sh->F, b3, sh->R, G, Y0, Y1, two ? sh->S->sc : nullptr, s, stop, &fz);
+                }
                 if ((rc = fft_band_inv(sh->F, b3, sh->R, G, Y0, Y1, two ? sh->S->sc : nullptr, s, stop, &fz)))
                     return rc;
                 return shard_push_slab(sh, kSlotPost, &ie_shard::xpost, 2, sh->row0, sh->nrows, s);
@@ -1757,15 +1766,26 @@ static int shard_iter_phase(ie_shard* sh, int ph, int64_t itarg, int do_p, int p
             IE_LAUNCHED();
             if (!spec) return IE_OK;
             if (timed) IE_CUDA(cudaEventRecord(sh->ev[2], s));
+            const bool fold_rz = G > 1 && sh->fused_transposes && sh->T;  // the scatter pushes its records
             if (sh->T) {
-                if ((rc = precond_apply_band(sh->T, sh->rfull, sh->z, sh->xrz(g) + kRzRec * c0, sh->b0, sh->b1, s,
-                                             stop)))
-                    return rc;
+                PeerRec pr;
+                if (fold_rz) {
+                    pr.n = G;
+                    for (int h = 0; h < G; ++h) {
+                        pr.dst[h] = sh->xrz(h) + kRzRec * c0;
+                        pr.ctr[h] = sh->mb(h) + kSlotRz;
+                    }
+                }
+                precond_set_peer_record(&pr);
+                rc = precond_apply_band(sh->T, sh->rfull, sh->z, sh->xrz(g) + kRzRec * c0, sh->b0, sh->b1, s, stop);
+                precond_set_peer_record(nullptr);
+                if (rc) return rc;
             } else {
                 k_identity_apply<<<nchb, kRed, 0, s>>>(r, sh->z, (int)sh->nb, sh->xrz(g) + kRzRec * c0, stop);
                 IE_LAUNCHED();
             }
             if (timed) IE_CUDA(cudaEventRecord(sh->ev[3], s));
+            if (fold_rz) return IE_OK;
             return shard_push_chunks(sh, kSlotRz, &ie_shard::xrz, kRzRec, s);
         }
         default: {

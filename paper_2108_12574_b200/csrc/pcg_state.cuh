@@ -65,6 +65,10 @@ struct PcgFuse {
     const double* f = nullptr;
     double* part = nullptr;
     int line0 = 0, post_lo = 0, post_hi = 0, q_col = -1, w_col = -1;
+    // sharded: the partials also written into the peers' arrays + mailbox
+    int npeer = 0;
+    double* part_peer[16] = {};
+    unsigned long long* part_ctr[16] = {};
 };
 
 // The sharded driver's transposes folded into the band FFT passes (see
@@ -76,6 +80,15 @@ struct PeerStores {
     unsigned long long* ctr[16] = {};
     long long line_bytes[16] = {};
     int rlo[16] = {}, rhi[16] = {};
+};
+
+// The sharded RZ exchange folded into the apply's scatter: each CTA copies its
+// chunk's record (all kRzRec fields) into every rank's array at the same index
+// and release-adds the bytes to that rank's mailbox.
+struct PeerRec {
+    int n = 0;
+    double* dst[16] = {};
+    unsigned long long* ctr[16] = {};
 };
 
 // PCG chunk record of the apply (4 doubles per dot-product chunk, the r.z

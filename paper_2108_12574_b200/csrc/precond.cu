@@ -913,6 +913,18 @@ __device__ __forceinline__ void scatter_fixed_chunk(int c, const double* staging
     chunk_sum_max(loc, zm, sh, partials + 4 * c);
 }
 
+// With pr.n: the chunk's record (the 4 fields; 2 and 3 came from k_iter_a)
+// is pushed to every rank of the sharded solver (pcg_state.cuh PeerRec).
+__device__ __forceinline__ void scatter_push_record(const double* rec, const PeerRec& pr) {
+    __syncthreads();  // the record's fields 0 / 1 (thread 0) are written
+    if ((int)threadIdx.x < pr.n) {
+        const double4 v = *reinterpret_cast<const double4*>(rec);
+        *reinterpret_cast<double4*>(pr.dst[threadIdx.x] + kRzRec * blockIdx.x) = v;
+        __threadfence_system();
+        atomicAdd_system(pr.ctr[threadIdx.x], (unsigned long long)(kRzRec * 8));
+    }
+}
+
 // With dec.s: the last CTA (ticket) runs the PCG iteration's decider on the
 // completed record (pcg_decide).
 __device__ __forceinline__ void scatter_decide(const double* partials, const PcgDecide& dec, double* sh) {
@@ -930,11 +942,12 @@ __device__ __forceinline__ void scatter_decide(const double* partials, const Pcg
 template <int MM, int UNR, bool PF = false>
 __global__ void __launch_bounds__(256) k_scatter_fixed(const double* staging, const int* pos, double* z, int N,
                                                        const double* r, double* partials, const int* stop, int i0,
-                                                       int i1, PcgDecide dec) {
+                                                       int i1, PcgDecide dec, PeerRec pr) {
     __shared__ double sh[512];
     pdl_wait();
     if (stop && *stop) return;
     scatter_fixed_chunk<MM, UNR, PF>(blockIdx.x, staging, pos, z, N, r, partials, i0, i1, sh);
+    if (pr.n && r) scatter_push_record(partials + kRzRec * blockIdx.x, pr);
     if (dec.s) scatter_decide(partials, dec, sh);
 }
 
@@ -942,7 +955,7 @@ __global__ void __launch_bounds__(256) k_scatter_fixed(const double* staging, co
 // Optionally also the fixed-chunk partials of r.z (for PCG's rho).
 __global__ void __launch_bounds__(256) k_scatter(const double* staging, const int* ptr, const int* pos, double* z,
                                                  int N, const double* r, double* partials, const int* stop, int i0,
-                                                 int i1, PcgDecide dec) {
+                                                 int i1, PcgDecide dec, PeerRec pr) {
     if (stop && *stop) return;
     __shared__ double sh[512];
     const int base = i0 + blockIdx.x * kChunk;
@@ -962,6 +975,7 @@ __global__ void __launch_bounds__(256) k_scatter(const double* staging, const in
     }
     if (!r) return;
     chunk_sum_max(loc, zm, sh, partials + 4 * blockIdx.x);
+    if (pr.n) scatter_push_record(partials + kRzRec * blockIdx.x, pr);
     if (dec.s) scatter_decide(partials, dec, sh);
 }
 
@@ -1359,8 +1373,10 @@ static void launch_apply_T(const ie_precond* p, ApplyArgs a, cudaStream_t st) {
 // CTA runs (precond_set_decide, single-GPU driver)
 static thread_local int64_t t_i0 = 0, t_i1 = -1;
 static thread_local PcgDecide t_dec;
+static thread_local PeerRec t_prec;
 
 void precond_set_decide(const PcgDecide* d) { t_dec = d ? *d : PcgDecide{}; }
+void precond_set_peer_record(const PeerRec* r) { t_prec = r ? *r : PeerRec{}; }
 
 static int scatter_launch(const ie_precond* p, const double* staging, const double* r, double* z,
                           double* partials, cudaStream_t st, const int* stop) {
@@ -1369,7 +1385,8 @@ static int scatter_launch(const ie_precond* p, const double* staging, const doub
     if (nch <= 0) return IE_OK;
     const double* rr = partials ? r : nullptr;
     const PcgDecide dec = partials ? t_dec : PcgDecide{};
-#define IE_SCAT(MM, ...) IE_CUDA(launch_k(k_scatter_fixed<MM, __VA_ARGS__>, dim3(nch), dim3(256), 0, st, staging, (const int*)p->d_posfix, z, (int)p->N, rr, partials, stop, i0, i1, dec))
+    const PeerRec prec = partials ? t_prec : PeerRec{};
+#define IE_SCAT(MM, ...) IE_CUDA(launch_k(k_scatter_fixed<MM, __VA_ARGS__>, dim3(nch), dim3(256), 0, st, staging, (const int*)p->d_posfix, z, (int)p->N, rr, partials, stop, i0, i1, dec, prec))
     // batch sizes measured at config 5 (MM = 4): 2 points with the next
     // batch's positions prefetched 10.6-11.3 us, 2 without 12.2, 4 15.5, 8 18.9
     // (register-limited residency), 1 point per level (before) 17.8
@@ -1379,7 +1396,7 @@ static int scatter_launch(const ie_precond* p, const double* staging, const doub
         case 4: IE_SCAT(4, 2, true); break;
         case 8: IE_SCAT(8, 2); break;
 #undef IE_SCAT
-        default: k_scatter<<<nch, 256, 0, st>>>(staging, p->d_ptr, p->d_pos, z, p->N, rr, partials, stop, i0, i1, dec);
+        default: k_scatter<<<nch, 256, 0, st>>>(staging, p->d_ptr, p->d_pos, z, p->N, rr, partials, stop, i0, i1, dec, prec);
     }
     IE_LAUNCHED();
     return IE_OK;
