@@ -713,7 +713,7 @@ class LocalShards:
     are testable (tests/test_gpu_parity.py::TestShardedP2P)."""
 
     def __init__(self, op, decomposition, world: int, method: str = "fft", variant: str = "packed_inverse",
-                 share_translated: bool = True):
+                 share_translated: bool = True, identity: bool = False):
         from . import _lib
         self._lib = _lib
         self.L = _lib.lib()
@@ -722,6 +722,9 @@ class LocalShards:
         self.plans = [make_plan(grid, decomposition, world, g) for g in range(world)]
         self.backends = [CudaBackend(op, decomposition, pl, method=method, variant=variant,
                                      share_translated=share_translated) for pl in self.plans]
+        if identity:  # precond=None (pcg.py:68): the identity on every rank, no halo
+            for b in self.backends:
+                b.pre = None
         if not all(native_supported(b, pl) for b, pl in zip(self.backends, self.plans)):
             raise ValueError("native sharded PCG needs the 2D band FFT and equal chunk-aligned bands")
         self.shards = [NativeShard(b, pl, connect=False) for b, pl in zip(self.backends, self.plans)]

@@ -714,6 +714,19 @@ class TestShardedP2P:
         assert rep.n_it == 12 and rep.residual_history == rep_n.residual_history
         assert np.array_equal(u.cpu().numpy(), u_n)
 
+    @pytest.mark.parametrize("world", [2, 4])
+    def test_identity_preconditioner_bitwise(self, ie, world):
+        """precond=None on every rank (k_identity_apply, no halo rows)."""
+        from paper_2108_12574_b200 import distributed as D
+        grid = ie.build_grid(2, 128)
+        op = ie.build_operator(grid, lattice="cell")
+        dec = ie.build_decomposition(grid, 16, 1, "schwarz")
+        f = np.random.default_rng(5).standard_normal(op.n)
+        u, rep = D.LocalShards(op, dec, world, identity=True).solve(f, tol=1e-6, max_iters=40)
+        u_n, rep_n = ie.solve(ie.KernelMatvec(op, method="fft"), None, f, tol=1e-6, max_iters=40)
+        assert rep.n_it == rep_n.n_it and rep.residual_history == rep_n.residual_history
+        assert np.array_equal(u.cpu().numpy(), u_n)
+
     def test_plan_errors(self, ie):
         from paper_2108_12574_b200 import distributed as D
         grid = ie.build_grid(2, 64)
