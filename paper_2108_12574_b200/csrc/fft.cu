@@ -152,6 +152,14 @@ __device__ __forceinline__ double pow2_scale(double mx) {
     return ldexp(1.0, -e);
 }
 
+// 1 / c when x * (1 / c) rounds exactly as x / c for every x: c a normal power
+// of two (its reciprocal is then exact); 0 otherwise (callers divide)
+__device__ __forceinline__ double exact_recip(double c) {
+    const unsigned long long b = (unsigned long long)__double_as_longlong(c);
+    const unsigned ex = (unsigned)(b >> 52) & 0x7ffu;
+    return ((b & 0xfffffffffffffull) == 0 && ex != 0 && ex != 0x7ffu) ? 1.0 / c : 0.0;
+}
+
 template <int TPB>
 __device__ void column_scales(const LineArgs& a, double* sc) {
     if (a.scales) {
@@ -355,7 +363,7 @@ __device__ __forceinline__ int padi(int i) { return i + (i >> 4); }
 // line length 64..8192 (one slot per 16 left pass 2's stores 2-way
 // conflicted: 0.28 M excess wavefronts per config-5 row pass).
 template <int PADS>
-__device__ __forceinline__ int padq(int i) {
+__host__ __device__ __forceinline__ constexpr int padq(int i) {
     if constexpr (PADS == 0) return i ^ ((i >> 3) & 15);
     else return i + (i >> PADS);
 }
@@ -645,11 +653,44 @@ __device__ __forceinline__ void dft_r8(double* vr, double* vi, int b, int NB) {
     }
 }
 
-// Stockham pass p of a line: twiddle, butterflies, then (p < P) scatter to the
-// line's shared memory and gather the next pass's inputs.
+// gather positions j + TPL m (m < 8) of a line from the exchange buffer.  With
+// the XOR swizzle (PADS == 0), padq(j + TPL m) = padq(j) ^ padq(TPL m), and for
+// TPL >= 128 (a multiple of 16 above j's swizzled bits) that is padq(j) + TPL m:
+// one base register and immediate offsets.
+template <int PADS, int TPL>
+__device__ __forceinline__ void load8(double* vr, double* vi, int j, const double* re, const double* im) {
+    const int qj = PADS == 0 ? padq<0>(j) : 0;
+#pragma unroll
+    for (int m = 0; m < 8; ++m) {
+        const int q = PADS != 0 ? padq<PADS>(j + TPL * m) : (TPL >= 128 ? qj + TPL * m : (qj ^ padq<0>(TPL * m)));
+        vr[m] = re[q];
+        vi[m] = im[q];
+    }
+}
+
+// twiddles of Stockham pass PASS (> 1) for the thread's NB butterflies:
+// t[b (R - 1) + r - 1] = tw8[toff + k_b + r NS]
+template <int LOGL, int PASS>
+__device__ __forceinline__ void load_tw8(double2* t, int j, const double2* __restrict__ tw8) {
+    using PL = Plan8<LOGL>;
+    constexpr int R = 1 << PL::rlog(PASS);
+    constexpr int NB = 8 / R;
+    constexpr int NS = 1 << (3 * (PASS - 1));
+#pragma unroll
+    for (int b = 0; b < NB; ++b) {
+        const int k = (j + PL::TPL * b) & (NS - 1);
+#pragma unroll
+        for (int r = 1; r < R; ++r) t[b * (R - 1) + r - 1] = __ldg(tw8 + PL::toff(PASS) + k + r * NS);
+    }
+}
+
+// Stockham pass p of a line: twiddle (t: this pass's twiddles, loaded by the
+// previous pass), butterflies, then (p < P) scatter to the line's shared
+// memory, load the next pass's twiddles into t while the barrier drains (the
+// line's registers are free between the stores and the gathers), gather.
 template <int S, int LOGL, int PASS, int PADS>
 __device__ __forceinline__ void pass8(double* vr, double* vi, int j, double* re, double* im,
-                                      const double2* __restrict__ tw8, bool zero_hi = false) {
+                                      const double2* __restrict__ tw8, double2* t, bool zero_hi = false) {
     using PL = Plan8<LOGL>;
     constexpr int R = 1 << PL::rlog(PASS);
     constexpr int NB = 8 / R;
@@ -657,18 +698,15 @@ __device__ __forceinline__ void pass8(double* vr, double* vi, int j, double* re,
     constexpr int TPL = PL::TPL;
 #pragma unroll
     for (int b = 0; b < NB; ++b) {
-        const int jb = j + TPL * b;
-        const int k = jb & (NS - 1);
         if (PASS > 1) {
-            const double2* tp = tw8 + PL::toff(PASS) + k;
 #pragma unroll
             for (int r = 1; r < R; ++r) {
-                const double2 t = __ldg(tp + r * NS);
-                const double ti = S < 0 ? t.y : -t.y;
+                const double2 tt = t[b * (R - 1) + r - 1];
+                const double ti = S < 0 ? tt.y : -tt.y;
                 const int m = b + NB * r;
                 const double xr = vr[m];
-                vr[m] = fma(xr, t.x, -vi[m] * ti);
-                vi[m] = fma(xr, ti, vi[m] * t.x);
+                vr[m] = fma(xr, tt.x, -vi[m] * ti);
+                vi[m] = fma(xr, ti, vi[m] * tt.x);
             }
         }
         if (PASS == 1 && zero_hi) {  // R == 8, NB == 1: inputs j + TPL m, m >= 4, are zero padding
@@ -688,26 +726,28 @@ __device__ __forceinline__ void pass8(double* vr, double* vi, int j, double* re,
             dft_r8<S, R>(vr, vi, b, NB);
         }
     }
-    if (PASS == PL::P) return;  // register m now holds position j + TPL m
-    __syncthreads();  // the previous exchange's reads are done
+    if constexpr (PASS == PL::P) {
+        return;  // register m now holds position j + TPL m
+    } else {
+        __syncthreads();  // the previous exchange's reads are done
 #pragma unroll
-    for (int b = 0; b < NB; ++b) {
-        const int jb = j + TPL * b;
-        const int k = jb & (NS - 1);
-        const int o0 = (jb / NS) * NS * R + k;
+        for (int b = 0; b < NB; ++b) {
+            const int jb = j + TPL * b;
+            const int k = jb & (NS - 1);
+            const int o0 = (jb / NS) * NS * R + k;
+            // PADS == 0: the swizzle is XOR-linear and o0, NS r have disjoint bits,
+            // so padq(o0 + NS r) = padq(o0) ^ padq(NS r): one XOR with an immediate
+            const int q0 = PADS == 0 ? padq<0>(o0) : 0;
 #pragma unroll
-        for (int r = 0; r < R; ++r) {
-            const int q = padq<PADS>(o0 + NS * r);
-            re[q] = vr[b + NB * r];
-            im[q] = vi[b + NB * r];
+            for (int r = 0; r < R; ++r) {
+                const int q = PADS == 0 ? (q0 ^ padq<0>(NS * r)) : padq<PADS>(o0 + NS * r);
+                re[q] = vr[b + NB * r];
+                im[q] = vi[b + NB * r];
+            }
         }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int m = 0; m < 8; ++m) {
-        const int q = padq<PADS>(j + TPL * m);
-        vr[m] = re[q];
-        vi[m] = im[q];
+        load_tw8<LOGL, PASS + 1>(t, j, tw8);
+        __syncthreads();
+        load8<PADS, TPL>(vr, vi, j, re, im);
     }
 }
 
@@ -715,11 +755,12 @@ template <int S, int LOGL, int PADS>
 __device__ __forceinline__ void fft8_line(double* vr, double* vi, int j, double* re, double* im,
                                           const double2* __restrict__ tw8, bool zero_hi = false) {
     constexpr int P = Plan8<LOGL>::P;
-    pass8<S, LOGL, 1, PADS>(vr, vi, j, re, im, tw8, zero_hi);
-    if constexpr (P >= 2) pass8<S, LOGL, 2, PADS>(vr, vi, j, re, im, tw8);
-    if constexpr (P >= 3) pass8<S, LOGL, 3, PADS>(vr, vi, j, re, im, tw8);
-    if constexpr (P >= 4) pass8<S, LOGL, 4, PADS>(vr, vi, j, re, im, tw8);
-    if constexpr (P >= 5) pass8<S, LOGL, 5, PADS>(vr, vi, j, re, im, tw8);  // L = 8192
+    double2 t[7];
+    pass8<S, LOGL, 1, PADS>(vr, vi, j, re, im, tw8, t, zero_hi);
+    if constexpr (P >= 2) pass8<S, LOGL, 2, PADS>(vr, vi, j, re, im, tw8, t);
+    if constexpr (P >= 3) pass8<S, LOGL, 3, PADS>(vr, vi, j, re, im, tw8, t);
+    if constexpr (P >= 4) pass8<S, LOGL, 4, PADS>(vr, vi, j, re, im, tw8, t);
+    if constexpr (P >= 5) pass8<S, LOGL, 5, PADS>(vr, vi, j, re, im, tw8, t);  // L = 8192
 }
 
 // 2048-point line with 16 points per thread (128 threads per line): radix 16,
@@ -757,6 +798,12 @@ __device__ __forceinline__ void fft16_line_2048(double* vr, double* vi, int j, d
         re[q] = vr[out_slot<16>(k)];
         im[q] = vi[out_slot<16>(k)];
     }
+    // the next pass's twiddles are loaded while the exchange barrier drains (the
+    // line's registers are free between the stores and the gathers)
+    const int k = j & 15;
+    double2 t2[15];
+#pragma unroll
+    for (int r = 1; r < 16; ++r) t2[r - 1] = __ldg(tw16 + r * 16 + k);
     __syncthreads();
 #pragma unroll
     for (int m = 0; m < 16; ++m) {
@@ -765,11 +812,11 @@ __device__ __forceinline__ void fft16_line_2048(double* vr, double* vi, int j, d
         vi[m] = im[q];
     }
     // pass 2: Ns = 16, radix 16
+    double2 t3[14];
     {
-        const int k = j & 15;
 #pragma unroll
         for (int r = 1; r < 16; ++r) {
-            const double2 t = __ldg(tw16 + r * 16 + k);
+            const double2 t = t2[r - 1];
             const double ti = S < 0 ? t.y : -t.y;
             const double xr = vr[r];
             vr[r] = fma(xr, t.x, -vi[r] * ti);
@@ -784,6 +831,10 @@ __device__ __forceinline__ void fft16_line_2048(double* vr, double* vi, int j, d
             re[q] = vr[out_slot<16>(kk)];
             im[q] = vi[out_slot<16>(kk)];
         }
+#pragma unroll
+        for (int b = 0; b < 2; ++b)
+#pragma unroll
+            for (int r = 1; r < 8; ++r) t3[7 * b + r - 1] = __ldg(tw16 + 256 + r * 256 + j + TPL * b);
         __syncthreads();
 #pragma unroll
         for (int m = 0; m < 16; ++m) {
@@ -796,13 +847,12 @@ __device__ __forceinline__ void fft16_line_2048(double* vr, double* vi, int j, d
     // output k of butterfly b (position jb + 256 k) lands in register b + 2 k
 #pragma unroll
     for (int b = 0; b < 2; ++b) {
-        const int jb = j + TPL * b;
         double xr[8], xi[8];
         xr[0] = vr[b];
         xi[0] = vi[b];
 #pragma unroll
         for (int r = 1; r < 8; ++r) {
-            const double2 t = __ldg(tw16 + 256 + r * 256 + jb);
+            const double2 t = t3[7 * b + r - 1];
             const double ti = S < 0 ? t.y : -t.y;
             const double ar = vr[b + 2 * r], ai = vi[b + 2 * r];
             xr[r] = fma(ar, t.x, -ai * ti);
@@ -936,6 +986,51 @@ __device__ __forceinline__ void fused_p_update(const LineArgs& a, double* vr, co
     __syncthreads();  // csc
 }
 
+// shared-memory pitch of one staged folded-symbol line (fused TMA column pass)
+__host__ __device__ constexpr int sym_pitch(int L) { return (L / 2 + 1 + 7) / 16 * 16 + 8; }
+
+// the folded symbol of fused line `line` (axes 1..dim-1 from the line index,
+// axis 0 contiguous along the line; see k_fold_symbol)
+__device__ __forceinline__ const double* sym_line(const LineArgs& a, int line) {
+    const int lgi = a.lg_ninner;
+    const int i = lgi >= 0 ? line & ((1 << lgi) - 1) : line % a.ninner;
+    const int L = a.L, np1 = L / 2 + 1;
+    int tmp = i + a.line0, off = 0, stride = 1;
+    for (int d = a.dim - 1; d >= 1; --d) {
+        const int k = tmp & (L - 1);
+        tmp >>= a.logL;
+        off += min(k, L - k) * stride;
+        stride *= np1;
+    }
+    return a.sym + (int64_t)off * np1;
+}
+
+// the output side of the exact 2-RHS column scaling: x / c_0, y / c_1 (powers
+// of two), as multiplications by the exact reciprocals (a division is a
+// ~10-instruction sequence); division kept for a non-power-of-two multiplier
+struct OutScale {
+    double r0 = 1.0, r1 = 1.0, c0 = 1.0, c1 = 1.0;
+    bool div = false;
+    __device__ __forceinline__ OutScale(const LineArgs& a, const double* csc) {
+        if (a.scale_out) {
+            c0 = csc[0];
+            c1 = csc[1];
+            r0 = exact_recip(c0);
+            r1 = exact_recip(c1);
+            div = r0 == 0.0 || r1 == 0.0;
+        }
+    }
+    __device__ __forceinline__ void apply(double& x, double& y) const {
+        if (div) {
+            x /= c0;
+            y /= c1;
+        } else {
+            x *= r0;
+            y *= r1;
+        }
+    }
+};
+
 template <int MODE, int LOGL, bool STRIDED, bool TMA = false, int PTS = 8>
 __global__ void __launch_bounds__(PTS == 16 ? 256 : 1024, PTS == 16 ? 2 : 1) k_fft8(const __grid_constant__ LineArgs a) {
     static_assert(PTS == 8 || LOGL == 11, "16 points per thread: 2048-point lines only");
@@ -944,6 +1039,9 @@ __global__ void __launch_bounds__(PTS == 16 ? 256 : 1024, PTS == 16 ? 2 : 1) k_f
     // 16 points per thread, the XOR swizzle (padq<0>) for contiguous 8-point lines
     constexpr int PADS = STRIDED ? (PTS == 8 ? 3 : 4) : (PTS == 8 ? 0 : 4);
     constexpr int L = 1 << LOGL, TPL = L / PTS;
+    // folded symbol line length and its shared-memory pitch (== 8 mod 16
+    // doubles: the two column lines of a warp hit disjoint bank halves)
+    constexpr int kNp1 = L / 2 + 1, kSymPitch = sym_pitch(L);
     constexpr bool upd = MODE == kFwdRCUpd, post = MODE == kInvCRPost;
     constexpr bool in_real = MODE == kFwdRC || MODE == kFusedRR || upd;
     constexpr bool out_real = MODE == kInvCR || MODE == kFusedRR || post;
@@ -952,7 +1050,12 @@ __global__ void __launch_bounds__(PTS == 16 ? 256 : 1024, PTS == 16 ? 2 : 1) k_f
     __shared__ double csc[2];
     pdl_wait();
     if (a.stop && *a.stop) return;
-    const int G = TMA ? 2 : a.g8, t = threadIdx.x;  // the TMA variant is launched with two lines per CTA
+    // contiguous 8-point lines: the host's lines per CTA and pitch (L + skew) as
+    // compile-time constants, so im[q] is re[q] plus an immediate offset
+    constexpr bool cpitch = !STRIDED && PTS == 8;
+    constexpr int CG = TPL >= 256 ? 1 : 256 / TPL, CPITCH = L + (TPL < 8 ? TPL : 8);
+    // the TMA variant is launched with two lines per CTA
+    const int G = TMA ? 2 : (cpitch ? CG : a.g8), t = threadIdx.x;
     int g, j;
     if constexpr (STRIDED) {
         g = t % G;
@@ -961,8 +1064,9 @@ __global__ void __launch_bounds__(PTS == 16 ? 256 : 1024, PTS == 16 ? 2 : 1) k_f
         g = t / TPL;
         j = t % TPL;
     }
-    double* re = sm8 + (int64_t)g * a.pitch8;
-    double* im = sm8 + (int64_t)(G + g) * a.pitch8;
+    const int pitch = cpitch ? CPITCH : a.pitch8;
+    double* re = sm8 + (int64_t)g * pitch;
+    double* im = sm8 + (int64_t)(G + g) * pitch;
     const int line = blockIdx.x * G + g;
     const bool live = line < a.nlines;
     const int lgi = a.lg_ninner;
@@ -988,6 +1092,18 @@ __global__ void __launch_bounds__(PTS == 16 ? 256 : 1024, PTS == 16 ? 2 : 1) k_f
                 for (int y = 0; y < a.n_in; y += 256)
                     tma_load_2d(sm8 + y * G * 2, &a.tmap, 2 * G * (int)blockIdx.x, y, &tbar);
             }
+            // the folded symbol lines of the CTA's G columns -> shared memory
+            // behind the exchange buffers (cp.async, in flight with the tile)
+            double* ssym = sm8 + (int64_t)2 * G * pitch;
+            for (int gl = 0; gl < G; ++gl) {
+                if ((int)blockIdx.x * G + gl >= a.nlines) break;
+                const double* sl = sym_line(a, blockIdx.x * G + gl);
+                for (int e = t; e < kNp1; e += blockDim.x)
+                    asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(smem32(ssym + gl * kSymPitch + e)),
+                                 "l"(sl + e)
+                                 : "memory");
+            }
+            asm volatile("cp.async.commit_group;\n" ::: "memory");
             asm volatile(
                 "{\n .reg .pred p;\n TW%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], 0;\n @!p bra TW%=;\n}\n" ::"r"(
                     smem32(&tbar))
@@ -1002,15 +1118,12 @@ __global__ void __launch_bounds__(PTS == 16 ? 256 : 1024, PTS == 16 ? 2 : 1) k_f
                     vi[m] = v.y;
                 }
             }
+            // own copies landed; the forward transform's first barrier publishes them
+            asm volatile("cp.async.wait_all;\n" ::: "memory");
         }
     }
-#pragma unroll
-    for (int m = 0; m < PTS; ++m) {
-        if constexpr (tma_mode) break;
-        const int l = j + TPL * m;
-        vr[m] = vi[m] = 0.0;
-        if (live && l < a.n_in) {
-            const int64_t off = line_off(a.in_so, a.in_si, a.in_sl, a.in_lsplit, a.in_sh, o, i, l);
+    if constexpr (!tma_mode) {
+        auto load_pt = [&](int m, int64_t off) {
             if constexpr (in_real) {
                 vr[m] = __ldg(a.x0 + off);
                 if (a.x1) vi[m] = __ldg(a.x1 + off);
@@ -1021,6 +1134,20 @@ __global__ void __launch_bounds__(PTS == 16 ? 256 : 1024, PTS == 16 ? 2 : 1) k_f
                 const double2 v = a.in_c[off];
                 vr[m] = v.x;
                 vi[m] = v.y;
+            }
+        };
+#pragma unroll
+        for (int m = 0; m < PTS; ++m) vr[m] = vi[m] = 0.0;
+        if (a.in_lsplit < 0 && a.in_sl == 1) {  // contiguous line: one base offset, immediate strides
+            const int64_t ib = (int64_t)o * a.in_so + (int64_t)i * a.in_si + j;
+#pragma unroll
+            for (int m = 0; m < PTS; ++m)
+                if (live && j + TPL * m < a.n_in) load_pt(m, ib + TPL * m);
+        } else {
+#pragma unroll
+            for (int m = 0; m < PTS; ++m) {
+                const int l = j + TPL * m;
+                if (live && l < a.n_in) load_pt(m, line_off(a.in_so, a.in_si, a.in_sl, a.in_lsplit, a.in_sh, o, i, l));
             }
         }
     }
@@ -1045,21 +1172,24 @@ __global__ void __launch_bounds__(PTS == 16 ? 256 : 1024, PTS == 16 ? 2 : 1) k_f
     if constexpr (fused) {
         fft_line<-1, LOGL, PADS, PTS>(vr, vi, j, re, im, a, zero_hi);
         // folded real symbol at frequency l = j + TPL m along this line
-        constexpr int np1 = L / 2 + 1;
-        int tmp = i + a.line0, off = 0, stride = 1;
-        for (int d = a.dim - 1; d >= 1; --d) {
-            const int k = tmp & (L - 1);
-            tmp >>= LOGL;
-            off += min(k, L - k) * stride;
-            stride *= np1;
-        }
-        const double* symline = a.sym + (int64_t)off * np1;  // axis 0 fastest: contiguous along the line
+        if constexpr (tma_mode) {  // staged in shared memory at kernel start
+            const double* ss = sm8 + (int64_t)2 * G * pitch + g * kSymPitch;
 #pragma unroll
-        for (int m = 0; m < PTS; ++m) {
-            const int l = j + TPL * m;
-            const double lam = live ? __ldg(symline + min(l, L - l)) : 0.0;
-            vr[m] *= lam;
-            vi[m] *= lam;
+            for (int m = 0; m < PTS; ++m) {
+                const int l = j + TPL * m;
+                const double lam = live ? ss[min(l, L - l)] : 0.0;
+                vr[m] *= lam;
+                vi[m] *= lam;
+            }
+        } else {
+            const double* symline = sym_line(a, line);
+#pragma unroll
+            for (int m = 0; m < PTS; ++m) {
+                const int l = j + TPL * m;
+                const double lam = live ? __ldg(symline + min(l, L - l)) : 0.0;
+                vr[m] *= lam;
+                vi[m] *= lam;
+            }
         }
         // opaque copy of the line position: the inverse recomputes its exchange
         // addresses instead of keeping the forward's alive (64-register budget)
@@ -1098,26 +1228,30 @@ __global__ void __launch_bounds__(PTS == 16 ? 256 : 1024, PTS == 16 ? 2 : 1) k_f
         double pa = 0.0, pb = 0.0;
         double pv[PTS / 2], fv[PTS / 2];
         const bool own = live && line >= a.post_lo && line < a.post_hi;  // (halo rows: q only, no partial)
+        const bool olin = a.out_lsplit < 0 && a.out_sl == 1;
+        const int64_t ob = (int64_t)o * a.out_so + (int64_t)i * a.out_si + j;
+        auto ooff = [&](int m) {
+            return olin ? ob + TPL * m
+                        : line_off(a.out_so, a.out_si, a.out_sl, a.out_lsplit, a.out_sh, o, i, j + TPL * m);
+        };
 #pragma unroll
         for (int m = 0; m < PTS / 2; ++m) {  // n_out <= L / 2: only m < PTS / 2 is output
             const int l = j + TPL * m;
             pv[m] = fv[m] = 0.0;
             if (own && l < a.n_out) {
-                const int64_t off = line_off(a.out_so, a.out_si, a.out_sl, a.out_lsplit, a.out_sh, o, i, l);
+                const int64_t off = ooff(m);
                 if (a.post_q_col >= 0) pv[m] = __ldg(a.post_p + off);
                 if (a.post_w_col >= 0) fv[m] = __ldg(a.post_f + off);
             }
         }
+        const OutScale os(a, csc);
 #pragma unroll
         for (int m = 0; m < PTS / 2; ++m) {
             const int l = j + TPL * m;
             if (!live || l >= a.n_out) continue;
-            const int64_t off = line_off(a.out_so, a.out_si, a.out_sl, a.out_lsplit, a.out_sh, o, i, l);
+            const int64_t off = ooff(m);
             double x = vr[m], y = vi[m];
-            if (a.scale_out) {
-                x /= csc[0];  // exact: powers of two
-                y /= csc[1];
-            }
+            os.apply(x, y);
             a.y0[off] = x;
             if (a.y1) a.y1[off] = y;
 #ifdef IEDD_DEBUG_FUSE
@@ -1183,21 +1317,27 @@ __global__ void __launch_bounds__(PTS == 16 ? 256 : 1024, PTS == 16 ? 2 : 1) k_f
         }
     }
     if (!live) return;
-#pragma unroll
-    for (int m = 0; m < PTS; ++m) {
-        const int l = j + TPL * m;
-        if (l >= a.n_out) continue;
-        const int64_t off = line_off(a.out_so, a.out_si, a.out_sl, a.out_lsplit, a.out_sh, o, i, l);
+    const OutScale os(a, csc);
+    auto store_pt = [&](int m, int64_t off) {
         if constexpr (out_real) {
             double x = vr[m], y = vi[m];
-            if (a.scale_out) {
-                x /= csc[0];  // exact: powers of two
-                y /= csc[1];
-            }
+            os.apply(x, y);
             a.y0[off] = x;
             if (a.y1) a.y1[off] = y;
         } else {
             a.out_c[off] = make_double2(vr[m], vi[m]);
+        }
+    };
+    if (a.out_lsplit < 0 && a.out_sl == 1) {  // contiguous line
+        const int64_t ob = (int64_t)o * a.out_so + (int64_t)i * a.out_si + j;
+#pragma unroll
+        for (int m = 0; m < PTS; ++m)
+            if (j + TPL * m < a.n_out) store_pt(m, ob + TPL * m);
+    } else {
+#pragma unroll
+        for (int m = 0; m < PTS; ++m) {
+            const int l = j + TPL * m;
+            if (l < a.n_out) store_pt(m, line_off(a.out_so, a.out_si, a.out_sl, a.out_lsplit, a.out_sh, o, i, l));
         }
     }
 }
@@ -1365,12 +1505,13 @@ static int launch_fft8(LineArgs a, cudaStream_t st) {
         skew = std::min(tpl, 8);
     }
     (void)cout;
-    a.g8 = G;
+    a.g8 = G;  // (k_fft8 hard-codes G and pitch8 of the contiguous 8-point case: keep in step)
     const int pads = a.strided8 ? (a.pts == 8 ? 3 : 4) : (a.pts == 8 ? 0 : 4);  // k_fft8's PADS
     a.pitch8 = (pads ? (a.L + (a.L >> pads) + 15) / 16 * 16 : a.L) + skew;
     const int tpb = G * tpl;
     const int ctas = (a.nlines + G - 1) / G;
-    const size_t smem = (size_t)2 * G * a.pitch8 * sizeof(double);
+    size_t smem = (size_t)2 * G * a.pitch8 * sizeof(double);
+    if (a.fused && a.tma && a.strided8) smem += (size_t)G * sym_pitch(a.L) * sizeof(double);  // staged symbol
     if (a.fused) return a.in_real ? launch_fft8_m<kFusedRR>(a, tpb, ctas, smem, st)
                                   : launch_fft8_m<kFusedCC>(a, tpb, ctas, smem, st);
     if (a.in_real) return a.upd_s ? launch_fft8_m<kFwdRCUpd>(a, tpb, ctas, smem, st)
