@@ -154,10 +154,13 @@ __device__ __forceinline__ double pow2_scale(double mx) {
 
 // 1 / c when x * (1 / c) rounds exactly as x / c for every x: c a normal power
 // of two (its reciprocal is then exact); 0 otherwise (callers divide)
+// (c = +2^(ex - 1023), ex in [1, 2045]: 1 / c = 2^(1023 - ex), biased exponent 2046 - ex)
 __device__ __forceinline__ double exact_recip(double c) {
     const unsigned long long b = (unsigned long long)__double_as_longlong(c);
-    const unsigned ex = (unsigned)(b >> 52) & 0x7ffu;
-    return ((b & 0xfffffffffffffull) == 0 && ex != 0 && ex != 0x7ffu) ? 1.0 / c : 0.0;
+    const unsigned ex = (unsigned)(b >> 52);  // sign bit included: negative c -> 0
+    return ((b & 0xfffffffffffffull) == 0 && ex >= 1u && ex <= 2045u)
+               ? __longlong_as_double((long long)(2046ull - ex) << 52)
+               : 0.0;
 }
 
 template <int TPB>
@@ -931,22 +934,42 @@ __device__ __forceinline__ void fft_line(double* vr, double* vi, int j, double* 
 
 // Tree sums of (a, b) over each line's TPL threads (contiguous mapping: line g
 // = threads [g TPL, (g + 1) TPL)); the sums land in thread j == 0 of the line.
+// The halving tree a[j] += a[j + off], off = TPL/2 .. 1: levels with off >= 32
+// through shared memory, the last five inside the line's first warp by
+// shuffles (lane j + off -> j: the same pairs, so the same sums bit for bit).
 __device__ __forceinline__ void line_pair_tree(double& a, double& b, int j, int g, int TPL, double* sm) {
-    __syncthreads();  // the FFT's exchange buffer is free
-    double* sa = sm;
-    double* sb = sm + blockDim.x;
-    sa[threadIdx.x] = a;
-    sb[threadIdx.x] = b;
-    __syncthreads();
-    for (int off = TPL / 2; off > 0; off >>= 1) {
-        if (j < off) {
-            sa[threadIdx.x] += sa[threadIdx.x + off];
-            sb[threadIdx.x] += sb[threadIdx.x + off];
-        }
+    if (TPL > 32) {
+        __syncthreads();  // the FFT's exchange buffer is free
+        double* sa = sm;
+        double* sb = sm + blockDim.x;
+        sa[threadIdx.x] = a;
+        sb[threadIdx.x] = b;
         __syncthreads();
+        for (int off = TPL / 2; off >= 32; off >>= 1) {
+            if (j < off) {
+                sa[threadIdx.x] += sa[threadIdx.x + off];
+                sb[threadIdx.x] += sb[threadIdx.x + off];
+            }
+            __syncthreads();
+        }
+        if (j < 32) {
+            a = sa[threadIdx.x];
+            b = sb[threadIdx.x];
+        }
     }
-    a = sa[g * TPL];
-    b = sb[g * TPL];
+    // lines of <= 32 threads are warp-aligned (TPL a power of two)
+    if (j < 32) {
+        const unsigned mask = 0xffffffffu;  // whole warps: blockDim is a multiple of 32, lines warp-aligned
+        for (int off = min(TPL, 32) / 2; off > 0; off >>= 1) {
+            const double ao = __shfl_down_sync(mask, a, off, min(TPL, 32));
+            const double bo = __shfl_down_sync(mask, b, off, min(TPL, 32));
+            if (j < off) {
+                a += ao;
+                b += bo;
+            }
+        }
+    }
+    // (the sums are consumed by thread j == 0 of each line only)
 }
 
 // k_iter_b's vector half folded into the first (row) pass of a 2-RHS A-pass

@@ -9,3 +9,6 @@ for k in a: print(k, 'SAME' if a[k]==b[k] else 'DIFF', a[k], b[k])
 PY
 KREGEX=k_fft8 bash tools/lab/ab_lib.sh
 cat gpurun_out/ab_lib.log
+if [ -n "$NCU_TAG" ]; then
+IEDD_B200_NO_GRAPH=1 ncu --set full --import-source on --clock-control none --profile-from-start off -k regex:k_fft8 --launch-skip 6 --launch-count 3 -f -o gpurun_out/$NCU_TAG python tools/pcg_launches.py > gpurun_out/$NCU_TAG.log 2>&1
+fi
