@@ -29,6 +29,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <atomic>
 #include <mutex>
 #include <utility>
 #include <vector>
@@ -1457,11 +1458,15 @@ static int launch_modes(const LineArgs& a, cudaStream_t st) {
 
 template <int MODE, int LOGL, bool STRIDED, bool TMA = false, int PTS = 8>
 static int launch_fft8_ls(const LineArgs& a, int tpb, int ctas, size_t smem, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
+    // opt-in dynamic shared memory: raised to the largest request seen (the
+    // fused TMA pass at L = 4096 with staged symbol lines needs ~180 KB)
+    static std::atomic<size_t> attr{0};
+    size_t cur = attr.load();
+    if (smem > 48 * 1024 && smem > cur) {
         IE_CUDA(cudaFuncSetAttribute(k_fft8<MODE, LOGL, STRIDED, TMA, PTS>,
-                                     cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024));
-        attr = true;
+                                     cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        while (cur < smem && !attr.compare_exchange_weak(cur, smem)) {
+        }
     }
     IE_CUDA(launch_k(k_fft8<MODE, LOGL, STRIDED, TMA, PTS>, dim3(ctas), dim3(tpb), smem, st, a));
     IE_LAUNCHED();

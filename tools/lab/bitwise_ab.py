@@ -23,7 +23,7 @@ def h(t):
 
 
 out = {}
-for dim, n in ((2, 1024), (2, 1000), (2, 256), (3, 32), (1, 4096)):
+for dim, n in ((2, 1024), (2, 2048), (2, 1000), (2, 256), (3, 32), (3, 64), (1, 4096)):
     op = ie.build_operator(ie.build_grid(dim, n), lattice="cell")
     mv = ie.ToeplitzMatvec(op)
     rng = np.random.default_rng(7)

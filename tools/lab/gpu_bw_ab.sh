@@ -1,4 +1,5 @@
 set -x
+python -m pytest tests -m gpu -x -q 2>&1 | tail -2
 mkdir -p gpurun_out
 python tools/lab/bitwise_ab.py > gpurun_out/bw_new.json 2> gpurun_out/bw_new.err
 IEDD_B200_LIB=$PWD/tools/lab/lib_base.so python tools/lab/bitwise_ab.py > gpurun_out/bw_base.json 2> gpurun_out/bw_base.err
