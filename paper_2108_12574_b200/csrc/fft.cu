@@ -1521,7 +1521,8 @@ static int launch_fft8(LineArgs a, cudaStream_t st) {
     // contiguous row passes measured faster with 8 (21.5 vs 23.6 us row inverse)
     const bool cin = a.in_real || a.in_sl == 1, cout = a.out_real || a.out_sl == 1;
     static const bool no16 = getenv("IEDD_B200_FFT8_ONLY") != nullptr;
-    a.pts = (a.logL == 11 && a.tw16 && !cin && !no16) ? 16 : 8;
+    static const bool rows16 = getenv("IEDD_B200_ROWS16") != nullptr;  // comparison: 16 points on rows too
+    a.pts = (a.logL == 11 && a.tw16 && (!cin || rows16) && !no16) ? 16 : 8;
     const int tpl = a.L / a.pts;
     a.strided8 = cin ? 0 : 1;
     int G, skew;
