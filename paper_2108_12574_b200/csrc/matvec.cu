@@ -17,6 +17,7 @@
 // plain FMA chain inside a tile, Neumaier-compensated across tiles, fixed
 // split order across CTAs -- identical for any row range and any NRHS.
 #include <math.h>
+#include <cmath>
 
 #include <mutex>
 #include <vector>
@@ -558,6 +559,25 @@ extern "C" int ie_matvec_create_method(const ie_geom* g, int32_t method, ie_matv
     int nsplit = (4 * ie::kNumSMs + ctas - 1) / ctas;
     if (nsplit > tiles) nsplit = tiles;
     if (nsplit < 1) nsplit = 1;
+    if (m->R == 16 && !getenv("IEDD_B200_K1_SPLIT_V1")) {
+        // R = 16 keeps one CTA per SM resident (190 KB of shared memory), so the
+        // grid runs in rounds of kNumSMs CTAs: pick the split count whose last
+        // round is fullest.  Config 5: 256 row CTAs x 3 splits = 5.19 rounds ran
+        // as 6 (ncu: 242.6 ms, FP64 pipe 71% busy); x 4 = 6.92 rounds run as 7.
+        double best = -1.0;
+        int best_ns = nsplit;
+        for (int tps = tiles; tps >= 1; --tps) {
+            const int ns = (tiles + tps - 1) / tps;
+            if (ns > 32) break;
+            const double rounds = (double)ctas * ns / ie::kNumSMs;
+            const double score = rounds / std::ceil(rounds) - 0.002 * ns;
+            if (score > best) {
+                best = score;
+                best_ns = ns;
+            }
+        }
+        nsplit = best_ns;
+    }
     const int tiles_per_split = (tiles + nsplit - 1) / nsplit;
     m->split_len = tiles_per_split * m->TS;
     m->nsplit = (N + m->split_len - 1) / m->split_len;

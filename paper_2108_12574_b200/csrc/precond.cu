@@ -618,6 +618,211 @@ __global__ void __launch_bounds__(256, 2) k_apply_dmma(GemmArgs a) {
 }
 
 // ---------------------------------------------------------------------------
+// k_apply_dmma2: k_apply_dmma with the n8-tile columns dealt to the warps so
+// that the four SM sub-partitions issue the same number of DMMAs (same
+// fragments and k order per output element: bitwise the same Z).  ncu of
+// k_apply_dmma at config 5 (tiles of 56 columns = 7 n-tiles): the column
+// quarters hold 2, 2, 2, 1 n-tiles and warp w runs on sub-partition w % 4, so
+// sub-partitions 0/1 issued 4 units per CTA against 3 on 2/3 (DMMA sub-pipe
+// active 52% on average, 59% on the busy pair; 38% of the stall samples at the
+// chunk barrier).  Here n-tile t goes to column group t % 4 (slot t / 4), which
+// alternates the two sub-partition pairs, and an odd last n-tile is split by
+// rows between the two pairs ([0, H) and [H, MT) m-tiles).
+// Measured and dropped on the way: the r gather pipelined chunk by chunk with
+// the A ring (35.2 vs 35.0 us alone, +1.3 us per PCG iteration); two tiles in
+// the halves of one 512-thread CTA per SM with swapped quarters (32.0 us
+// alone, but +3 us per iteration: the CTA owns the SM, so neither the
+// side-branch u update nor the next kernel's CTAs slip in while it drains);
+// the same swap chosen by a per-SM ticket across two 256-thread CTAs (34.7).
+enum { kColNone = 0, kColFull = 1, kColLo = 2, kColHi = 3 };
+template <int MT, int MODE>
+__device__ __forceinline__ constexpr bool dmma_row_on(int m) {
+    return MODE == kColFull || (MODE == kColLo && m < (MT + 1) / 2) || (MODE == kColHi && m >= (MT + 1) / 2);
+}
+template <int MT, int M0, int M1>
+__device__ __forceinline__ void dmma_chunk(double (&acc)[MT][2][2], const double* ac, const double* bcol0,
+                                           const double* bcol1, int kbase, int kq, int arow) {
+    constexpr int AP = pad4mod16(16 * MT);
+#pragma unroll
+    for (int ks = 0; ks < kGemmKC / 4; ++ks) {
+        const int kg = kbase + ks * 4;
+        const double b0 = M0 != kColNone ? bcol0[kg] : 0.0;
+        const double b1 = M1 != kColNone ? bcol1[kg] : 0.0;
+        const double* ap = ac + (ks * 4 + kq) * AP + arow;
+#pragma unroll
+        for (int m = 0; m < MT; ++m) {
+            constexpr bool dummy = false;
+            (void)dummy;
+            const bool on0 = dmma_row_on<MT, M0>(m), on1 = dmma_row_on<MT, M1>(m);
+            if (on0 || on1) {
+                const double av = ap[8 * m];
+                if (on0) dmma884(acc[m][0][0], acc[m][0][1], av, b0);
+                if (on1) dmma884(acc[m][1][0], acc[m][1][1], av, b1);
+            }
+        }
+    }
+}
+
+template <int MT>
+__global__ void __launch_bounds__(256, 2) k_apply_dmma2(GemmArgs a) {
+    extern __shared__ double sg[];
+    constexpr int AP = pad4mod16(16 * MT);
+    constexpr int H = (MT + 1) / 2;
+    const TileDesc td = a.tdesc[blockIdx.x];
+    const int first = td.first, cnt = td.cnt, s = td.s;
+    const int kpad = (s + kGemmKC - 1) / kGemmKC * kGemmKC;
+    const int bst = pad4mod16(kpad);
+    const double* A = a.full + td.full_off;
+    double* Bs = sg;                  // [64][bst] column-major gathered r
+    double* As = sg + kGemmTN * bst;  // [stages][KC][AP]
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int rh = warp & 1, cq = warp >> 1;
+    __shared__ int colbase[kGemmTN];
+    if (tid < kGemmTN) colbase[tid] = tid < cnt ? a.mst[first + tid] : -1;
+    if (kpad != s) {  // see k_apply_dmma: the last chunk's rows k >= s contribute exact zeros
+        for (int e = tid; e < kDmmaStages * kGemmKC * AP; e += 256) As[e] = 0.0;
+        for (int e = tid; e < kGemmTN * (kpad - s); e += 256) {
+            const int jc = e / (kpad - s);
+            Bs[jc * bst + s + (e - jc * (kpad - s))] = 0.0;
+        }
+    }
+    __syncthreads();
+    // gather plan: warp w owns columns w + 8 c, its lanes consecutive rows (lane +
+    // 32 i): an index load touches one or two 128-byte lines and a gather the
+    // three or four lattice rows its 32 block points lie on (k_apply_dmma's
+    // thread = (column, row mod 4) mapping: eight columns, so eight or more
+    // lines per warp instruction -- the L1 tag stage, one line per clock, made
+    // the prologue a quarter of the kernel)
+    constexpr int kGc = kGemmTN / 8, kGi = (kSmemMaxS + 31) / 32;  // 8 x 5
+    int gi[kGc * kGi];
+    if (!a.rg) {
+#pragma unroll
+        for (int c = 0; c < kGc; ++c) {
+            const int cb = colbase[warp + 8 * c];
+#pragma unroll
+            for (int i = 0; i < kGi; ++i) {
+                const int k = lane + 32 * i;
+                gi[c * kGi + i] = (cb >= 0 && k < s) ? __ldg(a.idx + cb + k) : -1;
+            }
+        }
+    }
+    const int nchunks = (s + kGemmKC - 1) / kGemmKC;
+    const bool v16 = !(s & 1) && ((reinterpret_cast<uintptr_t>(A) & 15) == 0);
+    constexpr int kQ = (kGemmKC * kSmemMaxS + 255) / 256;
+    int a_dst[kQ];
+#pragma unroll
+    for (int q = 0; q < kQ; ++q) {
+        const int e = v16 ? 2 * (tid + 256 * q) : tid + 256 * q;
+        const int kk = e / s;
+        a_dst[q] = kk * AP + (e - kk * s);
+    }
+    auto issue_chunk = [&](int ch) {
+        if (ch < nchunks) {
+            double* dst = As + (ch % kDmmaStages) * kGemmKC * AP;
+            const int kb = ch * kGemmKC;
+            const int kc = min(kGemmKC, s - kb);
+            const double* src = A + (int64_t)kb * s;
+            if (v16) {
+#pragma unroll
+                for (int q = 0; q < (kQ + 1) / 2; ++q) {
+                    const int e = 2 * (tid + 256 * q);
+                    if (e < kc * s) cp_async16(dst + a_dst[q], src + e);
+                }
+            } else {
+#pragma unroll
+                for (int q = 0; q < kQ; ++q) {
+                    const int e = tid + 256 * q;
+                    if (e < kc * s) cp_async8(dst + a_dst[q], src + e);
+                }
+            }
+        }
+    };
+    auto load_chunk = [&](int ch) {
+        issue_chunk(ch);
+        cp_async_commit();
+    };
+    issue_chunk(0);  // committed below together with the r gather (group 0)
+    pdl_wait();
+    if (a.stop && *a.stop) {
+        asm volatile("cp.async.wait_all;\n" ::: "memory");
+        return;
+    }
+    if (a.rg) {
+        for (int e = tid; e < s * kGemmTN; e += 256) {
+            const int jc = e / s, i = e - jc * s;
+            if (colbase[jc] >= 0) cp_async8(Bs + jc * bst + i, a.rg + colbase[jc] + i);
+        }
+    } else {
+#pragma unroll
+        for (int c = 0; c < kGc; ++c)
+#pragma unroll
+            for (int i = 0; i < kGi; ++i)
+                if (gi[c * kGi + i] >= 0) cp_async8(Bs + (warp + 8 * c) * bst + lane + 32 * i, a.r + gi[c * kGi + i]);
+    }
+    cp_async_commit();
+    for (int ch = 1; ch < kDmmaStages - 1; ++ch) load_chunk(ch);
+    double acc[MT][2][2];
+#pragma unroll
+    for (int m = 0; m < MT; ++m)
+#pragma unroll
+        for (int nt = 0; nt < 2; ++nt) acc[m][nt][0] = acc[m][nt][1] = 0.0;
+    // this warp's two column slots: n-tile 4 sl + cq, or the upper rows of an odd last n-tile
+    const int NT = (cnt + 7) >> 3;
+    int col[2], mode[2];
+#pragma unroll
+    for (int sl = 0; sl < 2; ++sl) {
+        const int t = 4 * sl + cq;
+        col[sl] = 0;
+        mode[sl] = kColNone;
+        if (t < NT) {
+            col[sl] = t;
+            mode[sl] = ((NT & 1) && t == NT - 1) ? kColLo : kColFull;
+        } else if ((NT & 1) && t == NT) {
+            col[sl] = t - 1;
+            mode[sl] = kColHi;
+        }
+    }
+    const int code = mode[0] * 4 + mode[1];
+    const int arow = rh * 8 * MT + (lane >> 2);  // + 8 m
+    const int kq = lane & 3;
+    const double* bcol0 = Bs + (col[0] * 8 + (lane >> 2)) * bst + kq;
+    const double* bcol1 = Bs + (col[1] * 8 + (lane >> 2)) * bst + kq;
+    for (int ch = 0; ch < nchunks; ++ch) {
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(kDmmaStages - 2));
+        __syncthreads();
+        load_chunk(ch + kDmmaStages - 1);
+        const double* ac = As + (ch % kDmmaStages) * kGemmKC * AP;
+        const int kb = ch * kGemmKC;
+        switch (code) {  // warp-uniform
+            case kColFull * 4 + kColFull: dmma_chunk<MT, kColFull, kColFull>(acc, ac, bcol0, bcol1, kb, kq, arow); break;
+            case kColFull * 4 + kColLo: dmma_chunk<MT, kColFull, kColLo>(acc, ac, bcol0, bcol1, kb, kq, arow); break;
+            case kColFull * 4 + kColHi: dmma_chunk<MT, kColFull, kColHi>(acc, ac, bcol0, bcol1, kb, kq, arow); break;
+            case kColFull * 4 + kColNone: dmma_chunk<MT, kColFull, kColNone>(acc, ac, bcol0, bcol1, kb, kq, arow); break;
+            case kColLo * 4 + kColNone: dmma_chunk<MT, kColLo, kColNone>(acc, ac, bcol0, bcol1, kb, kq, arow); break;
+            case kColHi * 4 + kColNone: dmma_chunk<MT, kColHi, kColNone>(acc, ac, bcol0, bcol1, kb, kq, arow); break;
+            default: break;
+        }
+    }
+    // store: C[row][col] with row = rh*8*MT + 8m + (lane>>2), col = 8 col[sl] + 2*(lane&3) + i
+#pragma unroll
+    for (int sl = 0; sl < 2; ++sl) {
+        if (mode[sl] == kColNone) continue;
+        const int mlo = mode[sl] == kColHi ? H : 0, mhi = mode[sl] == kColLo ? H : MT;
+#pragma unroll
+        for (int i2 = 0; i2 < 2; ++i2) {
+            const int jc = col[sl] * 8 + 2 * (lane & 3) + i2;
+            if (jc >= cnt) continue;
+            const int64_t st = colbase[jc];
+#pragma unroll
+            for (int m = 0; m < MT; ++m) {
+                const int row = rh * 8 * MT + 8 * m + (lane >> 2);
+                if (m >= mlo && m < mhi && row < s) a.staging[st + row] = acc[m][sl][i2];
+            }
+        }
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Large translation-shared blocks (160 < s <= 1024; above, k_apply_big's row
 // chunks already spread each block): the class GEMV.  A class
 // c's members share Ainv_c (full, row-major); CTA (x, group) owns rows
@@ -1292,6 +1497,7 @@ struct ie_precond {
     double* d_rg;  // r gathered into the staging layout (GEMM path)
     int use_dmma;  // FP64 tensor-core (mma.sync m8n8k4) class GEMM
     int dmma_pregather = 0;  // IEDD_B200_PREGATHER=1: separate k_gather pass (comparison)
+    int dmma_v1 = 0;  // IEDD_B200_DMMA_V1=1: one tile per 256-thread CTA, up-front gather (comparison)
     int mm;        // fixed-width scatter table width (power of two <= 8), 0: CSR
     int* d_posfix; // [mm][N] staged positions, -1 padded
     int cgv_groups = 0;                 // > 0: class GEMV apply (large translation-shared blocks)
@@ -1415,6 +1621,22 @@ static void launch_dmma(const ie_precond* p, const GemmArgs& g, cudaStream_t st)
     launch_k(k_apply_dmma<MT>, dim3(p->ntiles), dim3(256), sm, st, g);
 }
 
+// k_apply_dmma2: shared memory sized to the decomposition's largest block
+template <int MT>
+static void launch_dmma2(const ie_precond* p, const GemmArgs& g, cudaStream_t st) {
+    constexpr int AP = pad4mod16(16 * MT);
+    const int bst = pad4mod16((p->smax + kGemmKC - 1) / kGemmKC * kGemmKC);
+    const size_t sm = ((size_t)kGemmTN * bst + (size_t)kDmmaStages * kGemmKC * AP) * sizeof(double);
+    static bool attr = false;
+    if (!attr) {
+        const int bmax = pad4mod16((kSmemMaxS + kGemmKC - 1) / kGemmKC * kGemmKC);
+        cudaFuncSetAttribute(k_apply_dmma2<MT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)(((size_t)kGemmTN * bmax + kDmmaStages * kGemmKC * AP) * sizeof(double)));
+        attr = true;
+    }
+    launch_k(k_apply_dmma2<MT>, dim3(p->ntiles), dim3(256), sm, st, g);
+}
+
 template <int RA>
 static void launch_gemm(const ie_precond* p, const GemmArgs& g, cudaStream_t st) {
     const size_t sm = ((size_t)kGemmTN * (kSmemMaxS + 1) + 2 + 2 * (size_t)kGemmKC * 16 * RA) * sizeof(double);
@@ -1453,6 +1675,22 @@ int precond_apply(const ie_precond* p, const double* r, double* z, double* parti
         g.tdesc = p->d_tdesc;
         g.mst = p->d_mst;
         g.stop = stop;
+        if (p->use_dmma && !p->dmma_v1) {
+            switch ((((p->smax + 7) / 8) + 1) / 2) {
+                case 1: launch_dmma2<1>(p, g, st); break;
+                case 2: launch_dmma2<2>(p, g, st); break;
+                case 3: launch_dmma2<3>(p, g, st); break;
+                case 4: launch_dmma2<4>(p, g, st); break;
+                case 5: launch_dmma2<5>(p, g, st); break;
+                case 6: launch_dmma2<6>(p, g, st); break;
+                case 7: launch_dmma2<7>(p, g, st); break;
+                case 8: launch_dmma2<8>(p, g, st); break;
+                case 9: launch_dmma2<9>(p, g, st); break;
+                default: launch_dmma2<10>(p, g, st); break;
+            }
+            IE_LAUNCHED();
+            return scatter_launch(p, W.staging, r, z, partials, st, stop);
+        }
         if (p->use_dmma) {
             switch ((((p->smax + 7) / 8) + 1) / 2) {
                 case 1: launch_dmma<1>(p, g, st); break;
@@ -2123,6 +2361,7 @@ extern "C" int ie_precond_create(const ie_geom* g, const int64_t* h_offsets, con
         const char* env = getenv("IEDD_B200_APPLY_GEMM");
         p->use_dmma = !(env && std::string(env) == "dfma");
         p->dmma_pregather = getenv("IEDD_B200_PREGATHER") ? 1 : 0;
+        p->dmma_v1 = getenv("IEDD_B200_DMMA_V1") ? 1 : 0;
     }
     *out = p;
     return IE_OK;
