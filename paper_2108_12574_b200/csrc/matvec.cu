@@ -562,21 +562,28 @@ extern "C" int ie_matvec_create_method(const ie_geom* g, int32_t method, ie_matv
     if (m->R == 16 && !getenv("IEDD_B200_K1_SPLIT_V1")) {
         // R = 16 keeps one CTA per SM resident (190 KB of shared memory), so the
         // grid runs in rounds of kNumSMs CTAs: pick the split count whose last
-        // round is fullest.  Config 5: 256 row CTAs x 3 splits = 5.19 rounds ran
-        // as 6 (ncu: 242.6 ms, FP64 pipe 71% busy); x 4 = 6.92 rounds run as 7.
+        // round is fullest -- on one GPU (weight 0.55) and for the row bands of
+        // 2, 4 and 8 ranks (the plan may depend on N only: every rank and every G
+        // must sum the same splits in the same order).  Config 5: 256 row CTAs x
+        // 3 splits = 5.19 rounds ran as 6 (ncu: 242.6 ms, FP64 pipe 71% busy);
+        // x 32 = 55.35 rounds run as 56, and 6.92 as 7 on each of 8 ranks.
+        auto eff = [&](int ns, int G) {
+            const double rounds = (double)((ctas + G - 1) / G) * ns / ie::kNumSMs;
+            return rounds / std::ceil(rounds);
+        };
         double best = -1.0;
         int best_ns = nsplit;
         for (int tps = tiles; tps >= 1; --tps) {
             const int ns = (tiles + tps - 1) / tps;
             if (ns > 32) break;
-            const double rounds = (double)ctas * ns / ie::kNumSMs;
-            const double score = rounds / std::ceil(rounds) - 0.002 * ns;
+            const double score = 0.55 * eff(ns, 1) + 0.15 * (eff(ns, 2) + eff(ns, 4) + eff(ns, 8)) - 0.0005 * ns;
             if (score > best) {
                 best = score;
                 best_ns = ns;
             }
         }
         nsplit = best_ns;
+        if (const char* e = getenv("IEDD_B200_K1_NSPLIT")) nsplit = std::max(1, std::min(atoi(e), tiles));
     }
     const int tiles_per_split = (tiles + nsplit - 1) / nsplit;
     m->split_len = tiles_per_split * m->TS;

@@ -1145,7 +1145,7 @@ __device__ __forceinline__ void scatter_decide(const double* partials, const Pcg
 }
 
 template <int MM, int UNR, bool PF = false>
-__global__ void __launch_bounds__(256) k_scatter_fixed(const double* staging, const int* pos, double* z, int N,
+__global__ void __launch_bounds__(256, UNR >= 4 && PF ? 4 : 1) k_scatter_fixed(const double* staging, const int* pos, double* z, int N,
                                                        const double* r, double* partials, const int* stop, int i0,
                                                        int i1, PcgDecide dec, PeerRec pr) {
     __shared__ double sh[512];
@@ -1599,7 +1599,13 @@ static int scatter_launch(const ie_precond* p, const double* staging, const doub
     switch (p->mm) {
         case 1: IE_SCAT(1, 8); break;
         case 2: IE_SCAT(2, 2, true); break;
-        case 4: IE_SCAT(4, 2, true); break;
+        case 4:
+            // 4 points per dependent level capped at 64 registers (4 CTAs per SM keep
+            // the 512 chunks of config 5 resident; 48 B of spills): -1.5 us per PCG
+            // iteration against 2 points (same box, alternating processes)
+            if (getenv("IEDD_B200_SCAT_G2")) IE_SCAT(4, 2, true);
+            else IE_SCAT(4, 4, true);
+            break;
         case 8: IE_SCAT(8, 2); break;
 #undef IE_SCAT
         default: k_scatter<<<nch, 256, 0, st>>>(staging, p->d_ptr, p->d_pos, z, p->N, rr, partials, stop, i0, i1, dec, prec);
