@@ -328,6 +328,10 @@ struct GemmArgs {
     const int* mst;         // staging offset of members[m]
     const int* members;
     const int* stop;
+    // translation-regular classes (k_apply_dmma2): the point index of row k of
+    // tile t's column j is tile_base[64 t + j] + tile_rel[kSmemMaxS t + k]
+    const int* tile_base = nullptr;
+    const int* tile_rel = nullptr;
 };
 
 // smem layout: Bs[jj][kGemmBRow] column-major gathered r (row stride s+1 keeps
@@ -677,6 +681,25 @@ __global__ void __launch_bounds__(256, 2) k_apply_dmma2(GemmArgs a) {
     double* As = sg + kGemmTN * bst;  // [stages][KC][AP]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int rh = warp & 1, cq = warp >> 1;
+    // gather plan: warp w owns columns w + 8 c, its lanes consecutive rows (lane +
+    // 32 i): an index load touches one or two 128-byte lines and a gather the
+    // three or four lattice rows its 32 block points lie on (k_apply_dmma's
+    // thread = (column, row mod 4) mapping: eight columns, so eight or more
+    // lines per warp instruction)
+    constexpr int kGc = kGemmTN / 8, kGi = (kSmemMaxS + 31) / 32;  // 8 x 5
+    // translation-regular classes: index = the column's first point + the class's
+    // offset of row k, both from per-tile tables addressed by blockIdx alone --
+    // they load together with the tile descriptor (one memory round trip before
+    // the gather instead of descriptor -> member offsets -> point indices, and
+    // 13 loads per thread instead of 40)
+    int relv[kGi], basev[kGc];
+    if (a.tile_rel && !a.rg) {
+#pragma unroll
+        for (int i = 0; i < kGi; ++i)
+            relv[i] = __ldg(a.tile_rel + (int64_t)blockIdx.x * (kGi * 32) + lane + 32 * i);
+#pragma unroll
+        for (int c = 0; c < kGc; ++c) basev[c] = __ldg(a.tile_base + (int64_t)blockIdx.x * kGemmTN + warp + 8 * c);
+    }
     __shared__ int colbase[kGemmTN];
     if (tid < kGemmTN) colbase[tid] = tid < cnt ? a.mst[first + tid] : -1;
     if (kpad != s) {  // see k_apply_dmma: the last chunk's rows k >= s contribute exact zeros
@@ -686,16 +709,17 @@ __global__ void __launch_bounds__(256, 2) k_apply_dmma2(GemmArgs a) {
             Bs[jc * bst + s + (e - jc * (kpad - s))] = 0.0;
         }
     }
-    __syncthreads();
-    // gather plan: warp w owns columns w + 8 c, its lanes consecutive rows (lane +
-    // 32 i): an index load touches one or two 128-byte lines and a gather the
-    // three or four lattice rows its 32 block points lie on (k_apply_dmma's
-    // thread = (column, row mod 4) mapping: eight columns, so eight or more
-    // lines per warp instruction -- the L1 tag stage, one line per clock, made
-    // the prologue a quarter of the kernel)
-    constexpr int kGc = kGemmTN / 8, kGi = (kSmemMaxS + 31) / 32;  // 8 x 5
+    // (colbase is next read by the index loads of the table-less path and by the
+    // epilogue; the zero fill must land before the first chunk's copies)
+    if (kpad != s || !a.tile_rel) __syncthreads();
     int gi[kGc * kGi];
-    if (!a.rg) {
+    if (a.tile_rel && !a.rg) {
+#pragma unroll
+        for (int c = 0; c < kGc; ++c)
+#pragma unroll
+            for (int i = 0; i < kGi; ++i)
+                gi[c * kGi + i] = (basev[c] >= 0 && lane + 32 * i < s) ? basev[c] + relv[i] : -1;
+    } else if (!a.rg) {
 #pragma unroll
         for (int c = 0; c < kGc; ++c) {
             const int cb = colbase[warp + 8 * c];
@@ -1493,6 +1517,8 @@ struct ie_precond {
     int* d_tiles;  // [3][ntiles]: class, first member, count
     int* d_members;
     ie::TileDesc* d_tdesc = nullptr;  // per tile {class, first member, count, s, Ainv offset}
+    int* d_tile_base = nullptr;       // [ntiles][64] first point of each column's block (-1: no column)
+    int* d_tile_rel = nullptr;        // [ntiles][160] class offsets idx[k] - idx[0]; null unless every class is translation-regular
     int* d_mst = nullptr;         // staging offset of members[m]
     double* d_rg;  // r gathered into the staging layout (GEMM path)
     int use_dmma;  // FP64 tensor-core (mma.sync m8n8k4) class GEMM
@@ -1681,6 +1707,8 @@ int precond_apply(const ie_precond* p, const double* r, double* z, double* parti
         g.tdesc = p->d_tdesc;
         g.mst = p->d_mst;
         g.stop = stop;
+        g.tile_base = p->d_tile_base;
+        g.tile_rel = p->d_tile_rel;
         if (p->use_dmma && !p->dmma_v1) {
             switch ((((p->smax + 7) / 8) + 1) / 2) {
                 case 1: launch_dmma2<1>(p, g, st); break;
@@ -1805,6 +1833,8 @@ extern "C" void ie_precond_destroy(ie_precond* p) {
     cudaFree(p->d_tiles);
     cudaFree(p->d_members);
     cudaFree(p->d_tdesc);
+    cudaFree(p->d_tile_base);
+    cudaFree(p->d_tile_rel);
     cudaFree(p->d_mst);
     cudaFree(p->d_rg);
     cudaFree(p->d_posfix);
@@ -2340,6 +2370,36 @@ extern "C" int ie_precond_create(const ie_geom* g, const int64_t* h_offsets, con
         for (size_t q = 0; q < members.size(); ++q) mst[q] = (int)meta[members[q]].st_off;
         if (e == cudaSuccess) e = cudaMalloc(&p->d_tdesc, tdesc.size() * sizeof(ie::TileDesc));
         if (e == cudaSuccess) e = cudaMalloc(&p->d_mst, mst.size() * sizeof(int));
+        {
+            // per-tile gather tables when every member's in-block point order is its
+            // class representative's shifted by a constant (translation classes;
+            // reflected members are not, and keep the index-list gather)
+            constexpr int kRel = (ie::kSmemMaxS + 31) / 32 * 32;
+            std::vector<int> tbase(tcls.size() * (size_t)ie::kGemmTN, -1), trel(tcls.size() * (size_t)kRel, 0);
+            bool regular = !getenv("IEDD_B200_DMMA_IDX");
+            for (size_t t = 0; t < tcls.size() && regular; ++t) {
+                const int s_t = usizes[tcls[t]];
+                const int64_t r0 = h_offsets[mem[tcls[t]][0]];
+                for (int k = 0; k < s_t; ++k) trel[t * kRel + k] = (int)(ord[r0 + k] - ord[r0]);
+                for (int j = 0; j < tcnt[t] && regular; ++j) {
+                    const int64_t b0 = h_offsets[members[tfirst[t] + j]];
+                    tbase[t * ie::kGemmTN + j] = (int)ord[b0];
+                    for (int k = 0; k < s_t; ++k)
+                        if (ord[b0 + k] - ord[b0] != trel[t * kRel + k]) {
+                            regular = false;
+                            break;
+                        }
+                }
+            }
+            if (regular) {
+                if (e == cudaSuccess) e = cudaMalloc(&p->d_tile_base, tbase.size() * sizeof(int));
+                if (e == cudaSuccess) e = cudaMalloc(&p->d_tile_rel, trel.size() * sizeof(int));
+                if (e == cudaSuccess)
+                    e = cudaMemcpy(p->d_tile_base, tbase.data(), tbase.size() * sizeof(int), cudaMemcpyHostToDevice);
+                if (e == cudaSuccess)
+                    e = cudaMemcpy(p->d_tile_rel, trel.data(), trel.size() * sizeof(int), cudaMemcpyHostToDevice);
+            }
+        }
         if (e == cudaSuccess)
             e = cudaMemcpyAsync(p->d_tdesc, tdesc.data(), tdesc.size() * sizeof(ie::TileDesc), cudaMemcpyHostToDevice, st);
         if (e == cudaSuccess) e = cudaMemcpyAsync(p->d_mst, mst.data(), mst.size() * sizeof(int), cudaMemcpyHostToDevice, st);

@@ -894,7 +894,27 @@ def bench_sharded(args, metric, cfg, workload, config_keys=None, cpu_baseline=No
 
     # ---- self-check before timing: bitwise against the single-GPU solver
     pit = 12
-    u_b, rep_b = run(pit)
+    if native:
+        # a native solve that fails at run time (peer mapping refused, a mailbox
+        # wait timing out: status 6) must not take the job down: every rank
+        # reports, and all fall back to the torch.distributed driver together
+        try:
+            u_b, rep_b = run(pit)
+            okn = 1
+        except RuntimeError as e:
+            okn, why = 0, str(e)
+        okt = torch.tensor([okn], device=dev)
+        dist.all_reduce(okt, op=dist.ReduceOp.MIN)
+        if not bool(okt.item()):
+            native = False
+            why = why or "native driver failed on another rank"
+            f_band = f_pin[plan.begin: plan.end].to(dev)
+
+            def run(iters):  # noqa: F811
+                return solve_sharded(backend, comm, plan, f_band, tol=1e-10, max_iters=iters, gather_solution=False)
+            u_b, rep_b = run(pit)
+    else:
+        u_b, rep_b = run(pit)
     u_all = comm.allgather_band(u_b[None])[0]
     parity = None
     if rank == 0:
