@@ -555,6 +555,7 @@ struct PcgWork {
     cudaStream_t side_stream = nullptr;  // graph side branch (u update)
     cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
     cudaGraphExec_t gexec = nullptr;
+    cudaGraphExec_t gexec_b = nullptr;  // kBatch iterations in one graph (no graph boundary between them)
     uint64_t key_a = 0, key_t = 0;
     int gnodes = 0;  // kernel nodes in the captured iteration
     PcgState* st = nullptr;
@@ -572,6 +573,7 @@ struct PcgWork {
         cudaFree(hist);
         cudaFree(fcopy);
         if (gexec) cudaGraphExecDestroy(gexec);
+        if (gexec_b) cudaGraphExecDestroy(gexec_b);
         if (cap_stream) cudaStreamDestroy(cap_stream);
         if (side_stream) cudaStreamDestroy(side_stream);
         if (fork_ev) cudaEventDestroy(fork_ev);
@@ -838,39 +840,66 @@ static int pcg_impl(const ie_matvec* A, const ie_precond* T, const double* f, do
         return IE_OK;
     };
     const bool use_graph = max_iters >= 3 && !getenv("IEDD_B200_NO_GRAPH") && !prof;
+    // kBatch iterations per replay: the iteration boundary inside the graph is an
+    // ordinary (programmatic) kernel edge instead of a graph launch
+    static const bool no_multi = getenv("IEDD_B200_GRAPH1") != nullptr;  // comparison: one iteration per replay
     if (use_graph) {
         const uint64_t ka = matvec_uid(A), kt = T ? precond_uid(T) : 0;
         if (!W->gexec || W->key_a != ka || W->key_t != kt) {
-            if (W->gexec) {
-                cudaGraphExecDestroy(W->gexec);
-                W->gexec = nullptr;
+            for (cudaGraphExec_t* ge : {&W->gexec, &W->gexec_b}) {
+                if (*ge) cudaGraphExecDestroy(*ge);
+                *ge = nullptr;
             }
-            cudaGraph_t g;
             if (T && (rc = precond_prepare_stream(T, W->cap_stream))) return rc;
             if ((rc = matvec_prepare_stream(A, W->cap_stream))) return rc;
-            IE_CUDA(cudaStreamBeginCapture(W->cap_stream, cudaStreamCaptureModeThreadLocal));
-            int r2 = enqueue_iter(-1, 1, 1, true, W->cap_stream, false, 0);  // k_iter_b advances it_dev
-            cudaError_t ce = cudaStreamEndCapture(W->cap_stream, &g);
-            if (r2) return r2;
-            IE_CUDA(ce);
-            size_t nn = 0;
-            cudaGraphGetNodes(g, nullptr, &nn);
-            std::vector<cudaGraphNode_t> nodes(nn);
-            if (nn) cudaGraphGetNodes(g, nodes.data(), &nn);
-            W->gnodes = 0;
-            for (auto nd : nodes) {
-                cudaGraphNodeType t;
-                if (cudaGraphNodeGetType(nd, &t) == cudaSuccess && t == cudaGraphNodeTypeKernel) ++W->gnodes;
+            for (int reps : {1, (int)kBatch}) {
+                cudaGraph_t g;
+                IE_CUDA(cudaStreamBeginCapture(W->cap_stream, cudaStreamCaptureModeThreadLocal));
+                int r2 = IE_OK;
+                for (int q = 0; q < reps && !r2; ++q)
+                    r2 = enqueue_iter(-1, 1, 1, true, W->cap_stream, false, 0);  // the decider advances it_dev
+                cudaError_t ce = cudaStreamEndCapture(W->cap_stream, &g);
+                if (r2) return r2;
+                IE_CUDA(ce);
+                if (reps == 1) {
+                    size_t nn = 0;
+                    cudaGraphGetNodes(g, nullptr, &nn);
+                    std::vector<cudaGraphNode_t> nodes(nn);
+                    if (nn) cudaGraphGetNodes(g, nodes.data(), &nn);
+                    W->gnodes = 0;
+                    for (auto nd : nodes) {
+                        cudaGraphNodeType t;
+                        if (cudaGraphNodeGetType(nd, &t) == cudaSuccess && t == cudaGraphNodeTypeKernel) ++W->gnodes;
+                    }
+                }
+                ce = cudaGraphInstantiate(reps == 1 ? &W->gexec : &W->gexec_b, g, 0);
+                cudaGraphDestroy(g);
+                IE_CUDA(ce);
             }
-            ce = cudaGraphInstantiate(&W->gexec, g, 0);
-            cudaGraphDestroy(g);
-            IE_CUDA(ce);
             W->key_a = ka;
             W->key_t = kt;
         }
     }
-    int64_t it = 1, nbatch = 0;
-    for (; it <= max_iters + 1; ++it) {
+    // pipelined status polling: a batch's state copy is queued behind it, and
+    // the host waits on the PREVIOUS batch's copy, so the GPU never drains
+    // between batches (at most one batch of no-op iterations -- every kernel
+    // returns on the device stop flag -- follows convergence)
+    int64_t it = 1, nbatch = 0, since_poll = 0;
+    bool stopped = false;
+    auto poll = [&]() -> int {
+        const int slot = (int)(nbatch & 1);
+        PcgState* hs = slot ? W->host2 : W->host;
+        IE_CUDA(cudaMemcpyAsync(hs, W->st, sizeof(PcgState), cudaMemcpyDeviceToHost, st));
+        IE_CUDA(cudaEventRecord(W->poll_ev[slot], st));
+        if (nbatch > 0) {
+            IE_CUDA(cudaEventSynchronize(W->poll_ev[slot ^ 1]));
+            if ((slot ? W->host : W->host2)->stop) stopped = true;
+        }
+        ++nbatch;
+        since_poll = 0;
+        return IE_OK;
+    };
+    while (it <= max_iters + 1 && !stopped) {
         const int do_p = it <= max_iters;
         const int pending = it >= 2;
         const bool spec = do_p && it < max_iters;
@@ -879,27 +908,24 @@ static int pcg_impl(const ie_matvec* A, const ie_precond* T, const double* f, do
                 k_set_it<<<1, 1, 0, st>>>(W->st, 2);
                 IE_LAUNCHED();
             }
-            IE_CUDA(cudaGraphLaunch(W->gexec, st));
-            g_launches.fetch_add(W->gnodes, std::memory_order_relaxed);
+            if (!no_multi && it + kBatch - 1 < max_iters) {  // iterations it .. it + kBatch - 1 are all steady-state
+                IE_CUDA(cudaGraphLaunch(W->gexec_b, st));
+                g_launches.fetch_add(W->gnodes * kBatch, std::memory_order_relaxed);
+                it += kBatch;
+                since_poll += kBatch;
+            } else {
+                IE_CUDA(cudaGraphLaunch(W->gexec, st));
+                g_launches.fetch_add(W->gnodes, std::memory_order_relaxed);
+                ++it;
+                ++since_poll;
+            }
         } else {
             if ((rc = enqueue_iter(it, do_p, pending, spec, st, true, it))) return rc;
+            ++it;
+            ++since_poll;
         }
-        if (it % kBatch == 0 || it == max_iters + 1) {
-            // pipelined status polling: this batch's state copy is queued behind
-            // it, and the host waits on the PREVIOUS batch's copy, so the GPU
-            // never drains between batches (at most one batch of no-op
-            // iterations -- every kernel returns on the device stop flag --
-            // follows convergence)
-            const int slot = (int)(nbatch & 1);
-            PcgState* hs = slot ? W->host2 : W->host;
-            IE_CUDA(cudaMemcpyAsync(hs, W->st, sizeof(PcgState), cudaMemcpyDeviceToHost, st));
-            IE_CUDA(cudaEventRecord(W->poll_ev[slot], st));
-            if (nbatch > 0) {
-                IE_CUDA(cudaEventSynchronize(W->poll_ev[slot ^ 1]));
-                if ((slot ? W->host : W->host2)->stop) break;
-            }
-            ++nbatch;
-        }
+        if (since_poll >= kBatch || it > max_iters + 1)
+            if ((rc = poll())) return rc;
     }
     IE_CUDA(cudaMemcpyAsync(W->host, W->st, sizeof(PcgState), cudaMemcpyDeviceToHost, st));
     IE_CUDA(cudaStreamSynchronize(st));
