@@ -264,12 +264,12 @@ def run_ours(args):
                      "traffic": traffic.get("fft_pass"),
                      "note": "flops = 5 M log2 M per line FFT x 6n lines (M = 2n); peak = live 8-chain DFMA "
                              "microbenchmark (ie_fp64_peak); traffic = ncu dram bytes of the three launches"},
-        "apply": {"bound": "fp64-tensor", "kernel": "k_apply_dmma (class GEMM on DMMA, gathers r) + k_scatter_fixed",
+        "apply": {"bound": "fp64-tensor", "kernel": "k_apply_dmma2 (class GEMM on DMMA, gathers r) + k_scatter_fixed (+ the iteration's decider)",
                   "achieved": 2.0 * s2 / (ph[3] * 1e-3) / 1e12, "unit": "TFLOP/s", "peak": dmma_peak_tflops,
                   "traffic": traffic.get("apply"),
                   "note": f"flops = 2 sum_k s_k^2 (Sigma s = {s_sum}); peak = live DMMA m8n8k4 microbenchmark "
                           "(ie_dmma_peak)"},
-        "k4_vectors": {"bound": "hbm", "kernel": "k_post_pass + k_iter_a (u and r updates) + k_iter_b",
+        "k4_vectors": {"bound": "hbm", "kernel": "k_iter_a (r update, control) + k_update_u; the post pass and the p update ride in the FFT row passes",
                        "achieved": 80.0 * N / (kern["k4_vector_ms"] * 1e-3) / 1e9, "unit": "GB/s", "peak": hbm,
                        "traffic": traffic.get("k4_vectors"),
                        "note": "bytes = 80 N per iteration (SURVEY 8(d): read p, u, r, q, z, f, Au; write u, r, "

@@ -13,6 +13,12 @@ bool pdl_enabled() {
     static const bool on = !getenv("IEDD_B200_NO_PDL");
     return on;
 }
+int pdl_early_mask() {
+    // default 5: k_iter_a (-0.7 us per config-5 iteration) and the scatter (-0.5 us); k_apply_dmma2's
+    // early trigger costs +5 us (the scatter's CTAs park beside the last tiles)
+    static const int m = getenv("IEDD_B200_EARLY") ? atoi(getenv("IEDD_B200_EARLY")) : 5;
+    return pdl_enabled() ? m : 0;
+}
 static thread_local std::string t_err;
 void set_error(const std::string& msg) { t_err = msg; }
 }  // namespace ie

@@ -41,14 +41,23 @@ constexpr int kNumSMs = 148;
 // The kernels of the PCG iteration are launched with programmatic stream
 // serialization (launch_k): a kernel may be scheduled while its predecessor
 // drains and runs pdl_wait() (griddepcontrol.wait: the predecessor has
-// completed and its writes are visible) before touching anything.  No early
-// launch_dependents trigger: measured, early triggers slowed the PCG iteration
-// (successor CTAs parked on the SMs) while the implicit end-of-kernel trigger
-// hides the launch latency (config-5 FFT pass 101.5 -> 96 us, apply 48 -> 44 us
-// when launched back to back; ~1 us per graph-replayed iteration).  A no-op for
-// ordinary launches; IEDD_B200_NO_PDL=1 turns the attribute off.
+// completed and its writes are visible) before touching anything.  Early
+// launch_dependents triggers in every kernel slowed the PCG iteration (196 vs
+// 186 us: successor CTAs parked on the SMs beside later waves of the primary),
+// while the implicit end-of-kernel trigger hides the launch latency (config-5
+// FFT pass 101.5 -> 96 us, apply 48 -> 44 us when launched back to back; ~1 us
+// per graph-replayed iteration).  Round 2: early triggers only in kernels whose
+// whole grid is resident in one wave -- k_iter_a (-0.7 us per config-5
+// iteration) and the apply's scatter (-0.5 us); in k_apply_dmma2 it costs +5 us
+// (pdl_early_mask).  A no-op for ordinary launches; IEDD_B200_NO_PDL=1 turns
+// the attribute off.
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;\n" ::: "memory"); }
+// Early trigger, only in kernels whose whole grid is resident in one wave (the
+// successor's CTAs can then only take the slots this grid's CTAs free as they
+// exit; they run their setup-time prologue and block in pdl_wait()).
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); }
 bool pdl_enabled();
+int pdl_early_mask();  // IEDD_B200_EARLY: bit 0 k_iter_a, bit 1 k_apply_dmma2, bit 2 k_scatter_fixed
 
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_k(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,

@@ -160,6 +160,7 @@ __global__ void __launch_bounds__(kRed, 4) k_iter_a(const double* xpost, int npo
                                                  double* xrz, const double* pmax, HaloSeg hs, int ticket) {
     __shared__ double sh[kRed];
     __shared__ int decided;
+    if (ticket & 2) pdl_trigger();  // (ticket bit 1: early trigger; bit 0: advance the iteration counter)
     pdl_wait();
     const int stopv = s->stop;
     if (it < 0) it = s->it_dev;
@@ -240,7 +241,7 @@ __global__ void __launch_bounds__(kRed, 4) k_iter_a(const double* xpost, int npo
             const int i = base + e * kRed + threadIdx.x;
             if (i < lim) r[i] = __dsub_rn(av[e], __dmul_rn(al, qv[e]));
         }
-        if (ticket) advance_iteration(s);
+        if (ticket & 1) advance_iteration(s);
         return;
     }
     double m = 0.0;
@@ -256,7 +257,7 @@ __global__ void __launch_bounds__(kRed, 4) k_iter_a(const double* xpost, int npo
     }
     m = chunk_absmax(m, sh);
     if (threadIdx.x == 0) xrz[kRzRec * (c0 + blockIdx.x) + 3] = m;
-    if (ticket) advance_iteration(s);
+    if (ticket & 1) advance_iteration(s);
 }
 
 // k_iter_a's u half: u += alpha p and max|u| per chunk, with the alpha CTA 0 of
@@ -706,6 +707,7 @@ static int pcg_impl(const ie_matvec* A, const ie_precond* T, const double* f, do
             dec.pglob = pglob;
             dec.it = itd;
             dec.nch = nch;
+            dec.early = (pdl_early_mask() & 4) ? 1 : 0;
         }
         if (T) {
             precond_set_decide(&dec);
@@ -804,7 +806,8 @@ static int pcg_impl(const ie_matvec* A, const ie_precond* T, const double* f, do
         IE_CUDA(launch_k(fork_u ? k_iter_a<false> : k_iter_a<true>, dim3(nch), dim3(kRed), 0, s2,
                          (const double*)xpost, npost, do_p, pending, (long long)itarg, W->st, W->hist,
                          fork_u ? nullptr : uu, W->r, (const double*)p, (const double*)q, N, 0, nch, xrz,
-                         fuse_upd ? nullptr : (const double*)pmax, HaloSeg{0, 0, 0, 0}, 0));
+                         fuse_upd ? nullptr : (const double*)pmax, HaloSeg{0, 0, 0, 0},
+                         (pdl_early_mask() & 1) ? 2 : 0));
         IE_LAUNCHED();
         if (fork_u) {
             IE_CUDA(cudaEventRecord(W->fork_ev, s2));

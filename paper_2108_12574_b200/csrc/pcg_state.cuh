@@ -138,6 +138,7 @@ struct PcgDecide {
     double* pglob = nullptr;
     long long it = 0;
     int nch = 0;
+    int early = 0;  // the scatter triggers its dependents at entry (pdl_trigger)
 };
 
 __device__ __forceinline__ double chunk_absmax(double v, double* sh);

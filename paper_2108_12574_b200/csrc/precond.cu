@@ -332,6 +332,7 @@ struct GemmArgs {
     // tile t's column j is tile_base[64 t + j] + tile_rel[kSmemMaxS t + k]
     const int* tile_base = nullptr;
     const int* tile_rel = nullptr;
+    int early = 0;  // k_apply_dmma2 triggers its dependents at entry
 };
 
 // smem layout: Bs[jj][kGemmBRow] column-major gathered r (row stride s+1 keeps
@@ -672,6 +673,7 @@ __global__ void __launch_bounds__(256, 2) k_apply_dmma2(GemmArgs a) {
     extern __shared__ double sg[];
     constexpr int AP = pad4mod16(16 * MT);
     constexpr int H = (MT + 1) / 2;
+    if (a.early) pdl_trigger();
     const TileDesc td = a.tdesc[blockIdx.x];
     const int first = td.first, cnt = td.cnt, s = td.s;
     const int kpad = (s + kGemmKC - 1) / kGemmKC * kGemmKC;
@@ -1173,6 +1175,7 @@ __global__ void __launch_bounds__(256, UNR >= 4 && PF ? 4 : 1) k_scatter_fixed(c
                                                        const double* r, double* partials, const int* stop, int i0,
                                                        int i1, PcgDecide dec, PeerRec pr) {
     __shared__ double sh[512];
+    if (dec.early) pdl_trigger();
     pdl_wait();
     if (stop && *stop) return;
     scatter_fixed_chunk<MM, UNR, PF>(blockIdx.x, staging, pos, z, N, r, partials, i0, i1, sh);
@@ -1709,6 +1712,7 @@ int precond_apply(const ie_precond* p, const double* r, double* z, double* parti
         g.stop = stop;
         g.tile_base = p->d_tile_base;
         g.tile_rel = p->d_tile_rel;
+        g.early = (pdl_early_mask() & 2) ? 1 : 0;
         if (p->use_dmma && !p->dmma_v1) {
             switch ((((p->smax + 7) / 8) + 1) / 2) {
                 case 1: launch_dmma2<1>(p, g, st); break;
