@@ -566,7 +566,8 @@ extern "C" int ie_matvec_create_method(const ie_geom* g, int32_t method, ie_matv
         // 2, 4 and 8 ranks (the plan may depend on N only: every rank and every G
         // must sum the same splits in the same order).  Config 5: 256 row CTAs x
         // 3 splits = 5.19 rounds ran as 6 (ncu: 242.6 ms, FP64 pipe 71% busy);
-        // x 32 = 55.35 rounds run as 56, and 6.92 as 7 on each of 8 ranks.
+        // x 23 = 39.78 rounds run as 40 (211.4 ms), 19.89 / 9.95 / 4.97 on the
+        // bands of 2 / 4 / 8 ranks.
         auto eff = [&](int ns, int G) {
             const double rounds = (double)((ctas + G - 1) / G) * ns / ie::kNumSMs;
             return rounds / std::ceil(rounds);
