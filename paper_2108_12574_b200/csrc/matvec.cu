@@ -168,7 +168,7 @@ __global__ void __launch_bounds__(256) k_matvec(MatvecArgs a) {
                     const int dbt = db[0] + r;
                     win[r] = pair_value<DIM>(stab, max(dbt * dbt + do2[0], 1));
                 }
-#pragma unroll 4
+#pragma unroll 8
                 for (int t = 0; t < L; ++t) {
                     double xv[NRHS];
                     if constexpr (NRHS == 2) {
