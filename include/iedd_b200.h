@@ -166,6 +166,15 @@ int ie_pcg_f64(const ie_matvec* A, const ie_precond* T, const double* d_f, doubl
                int32_t* h_flags, double* h_times, int64_t* fail_iter, double* fail_value,
                void* stream);
 
+/* ie_pcg_f64 with the solution delivered to page-locked HOST memory h_u (the
+ * reference's solve returns a host array, pcg.py:133-136): the device-to-host
+ * copy starts when u is final -- after the last iteration's update, beside the
+ * closing true-residual pass -- instead of after the solve.  Same solve
+ * otherwise (bitwise). */
+int ie_pcg_host_f64(const ie_matvec* A, const ie_precond* T, const double* d_f, double* h_u,
+                    double tol, int64_t max_iters, double* h_history, int64_t* n_it,
+                    int32_t* h_flags, double* h_times, int64_t* fail_iter, double* fail_value,
+                    void* stream);
 /* ie_pcg_f64 instrumented for the bench's per-kernel rooflines: iterations
  * launched one by one (no graph) with CUDA events between the kernel groups;
  * h_phase_ms[0..4] = mean device ms per steady-state (2-RHS) iteration of

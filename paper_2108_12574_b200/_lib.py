@@ -67,6 +67,8 @@ _SIGS = {
     "ie_precond_block_f64": (_I32, [_P, _I64, _P, ctypes.POINTER(_I64), ctypes.POINTER(_I32)]),
     "ie_pcg_f64": (_I32, [_P, _P, _P, _P, _D, _I64, _P, ctypes.POINTER(_I64), _P, _P,
                           ctypes.POINTER(_I64), ctypes.POINTER(_D), _P]),
+    "ie_pcg_host_f64": (_I32, [_P, _P, _P, _P, _D, _I64, _P, ctypes.POINTER(_I64), _P, _P,
+                          ctypes.POINTER(_I64), ctypes.POINTER(_D), _P]),
     "ie_pcg_profile_f64": (_I32, [_P, _P, _P, _P, _D, _I64, _P, ctypes.POINTER(_I64), _P, _P, _P, _P]),
     "ie_lanczos_f64": (_I32, [_P, _P, _P, _I32, _I64, _D, ctypes.POINTER(_D), ctypes.POINTER(_I64), _P]),
     "ie_fp64_peak": (_I32, [ctypes.POINTER(_D), _P]),

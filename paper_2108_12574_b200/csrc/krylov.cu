@@ -657,8 +657,9 @@ static int ensure_events(PcgWork* w, size_t n) {
 // iterations' matvec, k_post_pass, k_iter_a, apply, k_iter_b.
 static int pcg_impl(const ie_matvec* A, const ie_precond* T, const double* f, double* u, double tol,
                     int64_t max_iters, double* hist, int64_t* n_it, int32_t* flags, double* times,
-                    int64_t* fail_iter, double* fail_value, void* stream, double* prof) {
-    if (!A || !f || !u || !hist || !n_it || !flags || !times || max_iters < 0 || !(tol > 0.0 && tol < 1.0)) {
+                    int64_t* fail_iter, double* fail_value, void* stream, double* prof, double* h_u = nullptr) {
+    if (!A || !f || (!u && !h_u) || !hist || !n_it || !flags || !times || max_iters < 0 ||
+        !(tol > 0.0 && tol < 1.0)) {
         set_error("ie_pcg_f64: bad arguments");
         return IE_ERR_ARG;
     }
@@ -888,7 +889,7 @@ static int pcg_impl(const ie_matvec* A, const ie_precond* T, const double* f, do
     // between batches (at most one batch of no-op iterations -- every kernel
     // returns on the device stop flag -- follows convergence)
     int64_t it = 1, nbatch = 0, since_poll = 0;
-    bool stopped = false;
+    bool stopped = false, u_copied = false;
     auto poll = [&]() -> int {
         const int slot = (int)(nbatch & 1);
         PcgState* hs = slot ? W->host2 : W->host;
@@ -924,14 +925,31 @@ static int pcg_impl(const ie_matvec* A, const ie_precond* T, const double* f, do
             }
         } else {
             if ((rc = enqueue_iter(it, do_p, pending, spec, st, true, it))) return rc;
+            if (h_u && it == max_iters && !u_copied) {
+                // u is final after this iteration's k_iter_a (every later kernel only reads
+                // it, and after a stop every kernel is a no-op): its copy to the host runs
+                // on the side stream beside the closing true-residual pass
+                IE_CUDA(cudaEventRecord(W->fork_ev, st));
+                IE_CUDA(cudaStreamWaitEvent(W->side_stream, W->fork_ev, 0));
+                IE_CUDA(cudaMemcpyAsync(h_u, uu, (size_t)N * 8, cudaMemcpyDeviceToHost, W->side_stream));
+                IE_CUDA(cudaEventRecord(W->join_ev, W->side_stream));
+                u_copied = true;
+            }
             ++it;
             ++since_poll;
         }
         if (since_poll >= kBatch || it > max_iters + 1)
             if ((rc = poll())) return rc;
     }
+    // one closing round trip: the state, the history (its first entries
+    // speculatively: n_it is only known from the state) and u
+    const int64_t nh0 = std::min<int64_t>(max_iters + 1, 4096);
     IE_CUDA(cudaMemcpyAsync(W->host, W->st, sizeof(PcgState), cudaMemcpyDeviceToHost, st));
+    IE_CUDA(cudaMemcpyAsync(hist, W->hist, (size_t)nh0 * 8, cudaMemcpyDeviceToHost, st));
+    if (u) IE_CUDA(cudaMemcpyAsync(u, uu, (size_t)N * 8, cudaMemcpyDeviceToDevice, st));
+    if (h_u && !u_copied) IE_CUDA(cudaMemcpyAsync(h_u, uu, (size_t)N * 8, cudaMemcpyDeviceToHost, st));
     IE_CUDA(cudaStreamSynchronize(st));
+    if (u_copied) IE_CUDA(cudaEventSynchronize(W->join_ev));
     const PcgState S = *W->host;
     flags[0] = S.status == 1;
     flags[1] = S.status == 2;
@@ -941,9 +959,10 @@ static int pcg_impl(const ie_matvec* A, const ie_precond* T, const double* f, do
         if (fail_value) *fail_value = S.fail_value;
     }
     const int64_t nh = S.n_it + 1;
-    IE_CUDA(cudaMemcpyAsync(hist, W->hist, (size_t)nh * 8, cudaMemcpyDeviceToHost, st));
-    IE_CUDA(cudaMemcpyAsync(u, uu, (size_t)N * 8, cudaMemcpyDeviceToDevice, st));
-    IE_CUDA(cudaStreamSynchronize(st));
+    if (nh > nh0) {
+        IE_CUDA(cudaMemcpyAsync(hist + nh0, W->hist + nh0, (size_t)(nh - nh0) * 8, cudaMemcpyDeviceToHost, st));
+        IE_CUDA(cudaStreamSynchronize(st));
+    }
     times[0] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     // t_s: mean device time of the applies the reference performs (initial + iterations 1..n_it-1)
     double tp = 0.0;
@@ -974,6 +993,17 @@ extern "C" int ie_pcg_f64(const ie_matvec* A, const ie_precond* T, const double*
                           int64_t max_iters, double* hist, int64_t* n_it, int32_t* flags, double* times,
                           int64_t* fail_iter, double* fail_value, void* stream) {
     return pcg_impl(A, T, f, u, tol, max_iters, hist, n_it, flags, times, fail_iter, fail_value, stream, nullptr);
+}
+
+extern "C" int ie_pcg_host_f64(const ie_matvec* A, const ie_precond* T, const double* f, double* h_u, double tol,
+                               int64_t max_iters, double* hist, int64_t* n_it, int32_t* flags, double* times,
+                               int64_t* fail_iter, double* fail_value, void* stream) {
+    if (!h_u) {
+        set_error("ie_pcg_host_f64: bad arguments");
+        return IE_ERR_ARG;
+    }
+    return pcg_impl(A, T, f, nullptr, tol, max_iters, hist, n_it, flags, times, fail_iter, fail_value, stream, nullptr,
+                    h_u);
 }
 
 extern "C" int ie_pcg_profile_f64(const ie_matvec* A, const ie_precond* T, const double* f, double* u, double tol,

@@ -79,7 +79,9 @@ def _solve_native(A: KernelMatvec, T, f, tol, max_iters):
     n = A.N
     if max_iters is None:
         max_iters = max(2 * n, 100)
-    u = torch.empty_like(fd)
+    # numpy in -> numpy out: u goes straight to page-locked host memory, its copy
+    # overlapping the closing residual pass (ie_pcg_host_f64)
+    u = torch.empty(n, dtype=torch.float64, pin_memory=True) if was_np else torch.empty_like(fd)
     hist = np.zeros(max_iters + 1, dtype=np.float64)
     n_it = ctypes.c_int64(0)
     flags = np.zeros(2, dtype=np.int32)
@@ -87,7 +89,8 @@ def _solve_native(A: KernelMatvec, T, f, tol, max_iters):
     fail_it = ctypes.c_int64(0)
     fail_val = ctypes.c_double(0.0)
     th = T.handle if (T is not None and T.handle is not None) else None
-    rc = _lib.lib().ie_pcg_f64(A.handle, th, _lib.ptr(fd), _lib.ptr(u), tol, max_iters,
+    entry = _lib.lib().ie_pcg_host_f64 if was_np else _lib.lib().ie_pcg_f64
+    rc = entry(A.handle, th, _lib.ptr(fd), _lib.ptr(u), tol, max_iters,
                                _lib.np_ptr(hist), ctypes.byref(n_it), _lib.np_ptr(flags), _lib.np_ptr(times),
                                ctypes.byref(fail_it), ctypes.byref(fail_val), _lib.stream_ptr())
     if rc == _lib.IE_ERR_BREAKDOWN:
@@ -99,7 +102,7 @@ def _solve_native(A: KernelMatvec, T, f, tol, max_iters):
     history = [float(x) for x in hist[: k + 1]]
     rep = PcgReport(n_it=k, achieved_residual=history[-1], t_pcg=float(times[0]), t_s=float(times[1]),
                     residual_history=history, stagnated=bool(flags[1]), converged=bool(flags[0]))
-    return to_host(u, was_np), rep
+    return (u.numpy() if was_np else u), rep
 
 
 def _device_op(op, n, identity_ok=False):
