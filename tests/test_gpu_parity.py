@@ -881,6 +881,34 @@ class TestDeterminism:
             u, r = ie.solve(mv, pre, f, tol=1e-10)
             assert r.residual_history == r0.residual_history and torch.equal(u, u0)
 
+    def test_graph_batches_and_host_output_bitwise(self, ie):
+        """The steady iterations replay graphs of 4 or 1 iterations (whatever
+        fits before max_iters) and numpy callers get u through ie_pcg_host_f64
+        (copy overlapped with the closing pass): every max_iters around the
+        batch boundaries must give a prefix of the long run's history, and the
+        numpy path the device path's u, bit for bit."""
+        import torch
+        grid = ie.build_grid(2, 128)
+        op = ie.build_operator(grid, lattice="cell")
+        mv = ie.ToeplitzMatvec(op)
+        pre = ie.from_decomposition(op, ie.build_decomposition(grid, 16, 2, "schwarz"))
+        f_np = np.random.default_rng(5).standard_normal(op.n)
+        f = torch.from_numpy(f_np).cuda()
+        u_long, long = ie.solve(mv, pre, f, tol=1e-8)  # stops inside a 4-iteration graph: the rest are no-ops
+        assert long.converged and long.n_it > 18
+        u_h, rh = ie.solve(mv, pre, f_np, tol=1e-8)
+        assert rh.n_it == long.n_it and rh.residual_history == long.residual_history
+        assert isinstance(u_h, np.ndarray) and np.array_equal(u_h, u_long.cpu().numpy())
+        for K in (1, 2, 3, 4, 5, 6, 7, 8, 9, 10, 13, 14, 17):
+            u_d, rd = ie.solve(mv, pre, f, tol=1e-14, max_iters=K)
+            u_h, rh = ie.solve(mv, pre, f_np, tol=1e-14, max_iters=K)
+            # entries 0..K-1 come from the same 2-RHS passes as the long run's; entry K from
+            # the closing u-only pass (the other column of the complex transform is zero)
+            assert rd.n_it == K and rd.residual_history[:K] == long.residual_history[:K], K
+            assert abs(rd.residual_history[K] - long.residual_history[K]) <= 1e-10 * long.residual_history[K], K
+            assert rh.residual_history == rd.residual_history, K
+            assert np.array_equal(u_h, u_d.cpu().numpy()), K
+
     def test_repeated_apply_and_matvec_bitwise(self, ie):
         import torch
         grid = ie.build_grid(2, 1024)
