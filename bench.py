@@ -321,10 +321,72 @@ def run_ours(args):
         "gpu_launches": launches,
         "clocks": clk,
     }
+    if not args.no_configs:
+        out["configs"] = _other_configs(ie)
     if not args.no_cpu:
         out["cpu_baseline"] = cpu_baseline(max(1, min(10, args.steps)))  # ~8 s of CPU work
     print(json.dumps(out))
     return out
+
+
+def _other_configs(ie):
+    """BASELINE.json's other configs (parity-test cases, not bench lines) through
+    the drop-in API in the same run: converged PCG solves of c1 / c3 / c4 and
+    the Lanczos lambda_min of c2 / c4 (best of 3 wall times after a warm-up
+    call, the factorisation timed once), next to the iteration counts and
+    t_pcg the unmodified reference recorded when the goldens were frozen
+    (tools/gen_goldens.py, in the build container: other host, so context only)."""
+    import torch
+    gold = os.path.join(os.path.dirname(os.path.abspath(__file__)), "tests", "golden")
+
+    def timed(fn, reps=3):
+        fn()
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            r = fn()
+            torch.cuda.synchronize()
+            ts.append(time.perf_counter() - t0)
+        return min(ts), r
+
+    res = {}
+    for name, (dim, n, m, w, seed, kinds) in {"c1": (2, 32, 4, 1, 0, ("schwarz", "jacobi")),
+                                              "c3": (2, 256, 32, 2, 1, ("schwarz",)),
+                                              "c4": (3, 32, 4, 1, 2, ("schwarz",))}.items():
+        grid = ie.build_grid(dim, n)
+        op = ie.build_operator(grid, lattice="cell")
+        mv = ie.ToeplitzMatvec(op)
+        f = np.random.default_rng(seed).standard_normal(op.n)
+        try:
+            g = dict(np.load(os.path.join(gold, f"ref_{name}.npz")))
+        except OSError:
+            g = {}
+        for kind in kinds:
+            dec = ie.build_decomposition(grid, m, w, kind)
+            ie.from_decomposition(op, dec)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            pre = ie.from_decomposition(op, dec)
+            torch.cuda.synchronize()
+            t_f = time.perf_counter() - t0
+            t, (_, rep) = timed(lambda: ie.solve(mv, pre, f, tol=1e-10))
+            row = {"n_it": rep.n_it, "converged": bool(rep.converged), "t_pcg_s": t, "t_build_s": t_f}
+            if f"{kind}_meta" in g:
+                row["reference_n_it"] = int(g[f"{kind}_meta"][0])
+                row["reference_t_pcg_s"] = float(g[f"{kind}_times"][1])
+            res[f"{name} {kind} pcg"] = row
+    for name, (dim, n, m, w, kind, mi) in {"c2 schwarz": (2, 64, 8, 1, "schwarz", 300),
+                                           "c2 jacobi": (2, 64, 8, 1, "jacobi", 300),
+                                           "c4 schwarz": (3, 32, 4, 1, "schwarz", 200)}.items():
+        grid = ie.build_grid(dim, n)
+        op = ie.build_operator(grid, lattice="cell")
+        mv = ie.ToeplitzMatvec(op)
+        pre = ie.from_decomposition(op, ie.build_decomposition(grid, m, w, kind))
+        t, (lam, steps) = timed(lambda: ie.extremal_eigenvalue_lanczos(mv, pre, op.n, which="min", max_iters=mi,
+                                                                      return_steps=True))
+        res[f"{name} lanczos lambda_min"] = {"lambda": lam, "steps": steps, "t_s": t}
+    return res
 
 
 def _profile_phases(ie, _lib, mv, pre, f, iters):
@@ -431,6 +493,7 @@ def main():
     ap.add_argument("--no-cpu", action="store_true", help="skip the cpu_baseline leg")
     ap.add_argument("--matvec", default="auto", choices=["auto", "fft", "direct"])
     ap.add_argument("--skip-noshare", action="store_true", help="skip the unshared-factor apply measurement")
+    ap.add_argument("--no-configs", action="store_true", help="skip the c1-c4 solves / Lanczos runs (the configs block)")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)
