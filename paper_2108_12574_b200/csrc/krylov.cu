@@ -466,6 +466,7 @@ __global__ void k_post_pass(const double* p, const double* q, const double* f, c
 }
 
 __global__ void k_copy_if_running(double* dst, const double* src, int N, const int* stop) {
+    pdl_wait();  // (launched with programmatic serialization inside the Lanczos step)
     if (*stop) return;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < N) dst[i] = src[i];
@@ -1060,6 +1061,7 @@ __global__ void k_lz_first(double* V, double* AV, double* avj, const double* w, 
 // V[j+1] = w / beta, AV[j+1] = aw / beta, avj = AV[j+1]  (spectrum.py:186-187)
 __global__ void k_lz_next(double* V, double* AV, double* avj, const double* w, const double* aw, const LzState* s,
                           int N) {
+    pdl_wait();  // (launched with programmatic serialization inside the Lanczos step)
     if (s->stop) return;
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= N) return;
@@ -1072,10 +1074,12 @@ __global__ void k_lz_next(double* V, double* AV, double* avj, const double* w, c
 }
 
 __global__ void k_lz_advance(LzState* s) {
+    pdl_wait();  // (launched with programmatic serialization inside the Lanczos step)
     if (!s->stop) s->j += 1;
 }
 
 __global__ void k_lz_alpha(const double* part, int nch, double* alphas, const LzState* s) {
+    pdl_wait();  // (launched with programmatic serialization inside the Lanczos step)
     __shared__ double sh[kRed];
     if (s->stop) return;
     const double v = reduce_partials(part, nch, sh);
@@ -1088,6 +1092,7 @@ __global__ void k_lz_alpha(const double* part, int nch, double* alphas, const Lz
 // lambda_max(T_m) >= lambda_max(T_{m-1})), which brackets one side.
 __global__ void __launch_bounds__(kRed) k_lz_control(const double* part, int nch, const double* a, double* b,
                                                      int which, double rtol, LzState* s) {
+    pdl_wait();  // (launched with programmatic serialization inside the Lanczos step)
     __shared__ double sh[kRed];
     __shared__ double br[2];
     __shared__ unsigned above_mask[kRed / 32];
@@ -1202,6 +1207,7 @@ __global__ void __launch_bounds__(kRed) k_lz_control(const double* part, int nch
 
 // c_i = AV_i . w for i <= j (grid rows above j exit)
 __global__ void k_lz_gemv_t(const double* AV, const double* w, int N, double* part, int nch, const LzState* s) {
+    pdl_wait();  // (launched with programmatic serialization inside the Lanczos step)
     __shared__ double sh[kRed];
     if (s->stop || blockIdx.y > s->j) return;
     const double* v = AV + (int64_t)blockIdx.y * N;
@@ -1217,6 +1223,7 @@ __global__ void k_lz_gemv_t(const double* AV, const double* w, int N, double* pa
 }
 
 __global__ void k_lz_reduce_rows(const double* part, int nch, double* out, const LzState* s) {
+    pdl_wait();  // (launched with programmatic serialization inside the Lanczos step)
     __shared__ double sh[kRed];
     if (s->stop || blockIdx.x > s->j) return;
     const double v = reduce_partials(part + (int64_t)blockIdx.x * nch, nch, sh);
@@ -1228,6 +1235,7 @@ __global__ void k_lz_reduce_rows(const double* part, int nch, double* out, const
 // warp order (fixed association: deterministic).
 __global__ void __launch_bounds__(256) k_lz_gemv_sub(double* w, const double* V, const double* c, int N,
                                                      const LzState* s) {
+    pdl_wait();  // (launched with programmatic serialization inside the Lanczos step)
     __shared__ double part8[8][32];
     if (s->stop) return;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -1247,6 +1255,7 @@ __global__ void __launch_bounds__(256) k_lz_gemv_sub(double* w, const double* V,
 }
 
 __global__ void k_lz_dot(const double* x, const double* y, int N, double* part, const LzState* s) {
+    pdl_wait();  // (launched with programmatic serialization inside the Lanczos step)
     __shared__ double sh[kRed];
     if (s->stop) return;
     const int base = blockIdx.x * kChunk;
@@ -1302,29 +1311,29 @@ extern "C" int ie_lanczos_f64(const ie_matvec* A, const ie_precond* T, const dou
         if (T) {
             if ((r2 = precond_apply(T, avj.p, wb.p, nullptr, s2, stop))) return r2;
         } else {  // identity (precond.py:133-134)
-            k_copy_if_running<<<g1(N), 256, 0, s2>>>(wb.p, avj.p, N, stop);
+            IE_CUDA(launch_k(k_copy_if_running, dim3(g1(N)), dim3(256), 0, s2, wb.p, (const double*)avj.p, N, stop));
             IE_LAUNCHED();
         }
-        k_lz_dot<<<nch, kRed, 0, s2>>>(wb.p, avj.p, N, part.p, S.p);
+        IE_CUDA(launch_k(k_lz_dot, dim3(nch), dim3(kRed), 0, s2, (const double*)wb.p, (const double*)avj.p, N, part.p, (const LzState*)S.p));
         IE_LAUNCHED();
-        k_lz_alpha<<<1, kRed, 0, s2>>>(part.p, nch, da, S.p);
+        IE_CUDA(launch_k(k_lz_alpha, dim3(1), dim3(kRed), 0, s2, (const double*)part.p, nch, da, (const LzState*)S.p));
         IE_LAUNCHED();
         for (int pass = 0; pass < 2; ++pass) {  // two-pass A-orthogonalisation (CGS2)
-            k_lz_gemv_t<<<dim3(nch, (unsigned)nb_max), kRed, 0, s2>>>(AV.p, wb.p, N, part.p, nch, S.p);
+            IE_CUDA(launch_k(k_lz_gemv_t, dim3(nch, (unsigned)nb_max), dim3(kRed), 0, s2, (const double*)AV.p, (const double*)wb.p, N, part.p, nch, (const LzState*)S.p));
             IE_LAUNCHED();
-            k_lz_reduce_rows<<<(unsigned)nb_max, kRed, 0, s2>>>(part.p, nch, cbuf.p, S.p);
+            IE_CUDA(launch_k(k_lz_reduce_rows, dim3((unsigned)nb_max), dim3(kRed), 0, s2, (const double*)part.p, nch, cbuf.p, (const LzState*)S.p));
             IE_LAUNCHED();
-            k_lz_gemv_sub<<<(unsigned)((N + 31) / 32), 256, 0, s2>>>(wb.p, V.p, cbuf.p, N, S.p);
+            IE_CUDA(launch_k(k_lz_gemv_sub, dim3((unsigned)((N + 31) / 32)), dim3(256), 0, s2, wb.p, (const double*)V.p, (const double*)cbuf.p, N, (const LzState*)S.p));
             IE_LAUNCHED();
         }
         if ((r2 = matvec_launch(A, wb.p, N, 1, awb.p, N, 0, N, s2, stop))) return r2;
-        k_lz_dot<<<nch, kRed, 0, s2>>>(wb.p, awb.p, N, part.p, S.p);
+        IE_CUDA(launch_k(k_lz_dot, dim3(nch), dim3(kRed), 0, s2, (const double*)wb.p, (const double*)awb.p, N, part.p, (const LzState*)S.p));
         IE_LAUNCHED();
-        k_lz_control<<<1, kRed, 0, s2>>>(part.p, nch, da, db, which, rtol, S.p);
+        IE_CUDA(launch_k(k_lz_control, dim3(1), dim3(kRed), 0, s2, (const double*)part.p, nch, (const double*)da, db, which, rtol, S.p));
         IE_LAUNCHED();
-        k_lz_next<<<g1(N), 256, 0, s2>>>(V.p, AV.p, avj.p, wb.p, awb.p, S.p, N);
+        IE_CUDA(launch_k(k_lz_next, dim3(g1(N)), dim3(256), 0, s2, V.p, AV.p, avj.p, (const double*)wb.p, (const double*)awb.p, (const LzState*)S.p, N));
         IE_LAUNCHED();
-        k_lz_advance<<<1, 1, 0, s2>>>(S.p);
+        IE_CUDA(launch_k(k_lz_advance, dim3(1), dim3(1), 0, s2, S.p));
         IE_LAUNCHED();
         return IE_OK;
     };
