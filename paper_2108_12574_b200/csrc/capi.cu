@@ -1,6 +1,8 @@
 // Library-wide state of the C-ABI (include/iedd_b200.h): error text and the
 // launch counter reported as bench.py's gpu_launches.
 #include <stdlib.h>
+#include <mutex>
+#include <algorithm>
 #include <string>
 
 #include "common.cuh"
@@ -18,6 +20,34 @@ int pdl_early_mask() {
     // early trigger costs +5 us (the scatter's CTAs park beside the last tiles)
     static const int m = getenv("IEDD_B200_EARLY") ? atoi(getenv("IEDD_B200_EARLY")) : 5;
     return pdl_enabled() ? m : 0;
+}
+float l2_persist_request(size_t bytes) {
+    static std::mutex mu;
+    static size_t limit = 0, cap = 0;
+    static bool off = getenv("IEDD_B200_NO_L2PERSIST") != nullptr;
+    if (off || !bytes) return 0.f;
+    std::lock_guard<std::mutex> lk(mu);
+    if (!cap) {
+        int dev = 0, mx = 0, l2 = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, dev) != cudaSuccess ||
+            cudaDeviceGetAttribute(&l2, cudaDevAttrL2CacheSize, dev) != cudaSuccess || mx <= 0) {
+            cudaGetLastError();
+            off = true;
+            return 0.f;
+        }
+        cap = std::min<size_t>((size_t)mx, (size_t)l2 / 4);
+    }
+    const size_t want = std::min(cap, (bytes + bytes / 7 + ((size_t)1 << 20)) & ~(((size_t)1 << 20) - 1));
+    if (want > limit) {
+        if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) != cudaSuccess) {
+            cudaGetLastError();
+            off = true;
+            return 0.f;
+        }
+        limit = want;
+    }
+    return bytes <= limit ? 1.0f : (float)((double)limit / (double)bytes);
 }
 static thread_local std::string t_err;
 void set_error(const std::string& msg) { t_err = msg; }

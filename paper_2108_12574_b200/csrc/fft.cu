@@ -110,6 +110,7 @@ struct LineArgs {
     //    (post_w_col) -> post_part[2 (post_line0 + line)], [.. + 1].
     const double* upd_z;
     double* upd_pglob;
+    int post_skip_w;  // PcgFuse::skip_w_store
     PcgState* upd_s;
     long long upd_it;
     const double* post_p;
@@ -1276,8 +1277,8 @@ __global__ void __launch_bounds__(PTS == 16 ? 256 : 1024, PTS == 16 ? 2 : 1) k_f
             const int64_t off = ooff(m);
             double x = vr[m], y = vi[m];
             os.apply(x, y);
-            a.y0[off] = x;
-            if (a.y1) a.y1[off] = y;
+            if (!(a.post_skip_w && a.post_w_col == 0)) a.y0[off] = x;
+            if (a.y1 && !(a.post_skip_w && a.post_w_col == 1)) a.y1[off] = y;
 #ifdef IEDD_DEBUG_FUSE
             if (off < 3) printf("post off %lld p %.17g q %.17g w %.17g csc %g %g\n", (long long)off, pv[m], x, y, csc[0], csc[1]);
 #endif
@@ -1727,6 +1728,7 @@ static void apply_fuse(LineArgs& a, const PcgFuse* fz) {
         }
         a.post_p = fz->p;
         a.post_f = fz->f;
+        a.post_skip_w = fz->skip_w_store;
         a.post_part = fz->part;
         a.post_line0 = fz->line0;
         a.post_lo = fz->post_lo;

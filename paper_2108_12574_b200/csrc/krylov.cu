@@ -752,6 +752,7 @@ static int pcg_impl(const ie_matvec* A, const ie_precond* T, const double* f, do
     // Steady-state iterations (2 <= it < max_iters) replay one captured CUDA
     // graph that reads `it` from the device state.
     static const bool no_fork = getenv("IEDD_B200_NO_FORK") != nullptr;  // u update in k_iter_a (comparison)
+    static const bool keep_w = getenv("IEDD_B200_KEEP_W") != nullptr;    // store the w = A u column (comparison)
     cudaEvent_t pev[6] = {};
     int64_t nprof = 0;
     if (prof) {
@@ -787,6 +788,7 @@ static int pcg_impl(const ie_matvec* A, const ie_precond* T, const double* f, do
             fz.part = fuse_post ? xpost : nullptr;
             fz.q_col = do_p ? 0 : -1;
             fz.w_col = pending ? (do_p ? 1 : 0) : -1;
+            fz.skip_w_store = fuse_post && !keep_w;
         }
         const PcgFuse* fzp = fused ? &fz : nullptr;
         if (do_p && pending) {

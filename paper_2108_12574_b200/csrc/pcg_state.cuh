@@ -65,6 +65,8 @@ struct PcgFuse {
     const double* f = nullptr;
     double* part = nullptr;
     int line0 = 0, post_lo = 0, post_hi = 0, q_col = -1, w_col = -1;
+    // the w = A u column is consumed by the folded post pass alone: its store is skipped
+    int skip_w_store = 0;
     // sharded: the partials also written into the peers' arrays + mailbox
     int npeer = 0;
     double* part_peer[16] = {};

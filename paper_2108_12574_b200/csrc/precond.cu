@@ -1529,6 +1529,7 @@ struct ie_precond {
     int dmma_v1 = 0;  // IEDD_B200_DMMA_V1=1: one tile per 256-thread CTA, up-front gather (comparison)
     int mm;        // fixed-width scatter table width (power of two <= 8), 0: CSR
     int* d_posfix; // [mm][N] staged positions, -1 padded
+    float pos_hit = 0.f;  // hit ratio of its persisting L2 window (l2_persist_request)
     int cgv_groups = 0;                 // > 0: class GEMV apply (large translation-shared blocks)
     ie::CgvGroup* d_cgv = nullptr;
     int* d_cgv_mst = nullptr;
@@ -1632,8 +1633,15 @@ static int scatter_launch(const ie_precond* p, const double* staging, const doub
             // 4 points per dependent level capped at 64 registers (4 CTAs per SM keep
             // the 512 chunks of config 5 resident; 48 B of spills): -1.5 us per PCG
             // iteration against 2 points (same box, alternating processes)
-            if (getenv("IEDD_B200_SCAT_G2")) IE_SCAT(4, 2, true);
-            else IE_SCAT(4, 4, true);
+            if (getenv("IEDD_B200_SCAT_G2")) {
+                IE_SCAT(4, 2, true);
+            } else {
+                // 4 points per dependent level capped at 64 registers; the position table
+                // (read unchanged by every apply) holds a persisting L2 window
+                IE_CUDA(launch_k_win(k_scatter_fixed<4, 4, true>, dim3(nch), dim3(256), 0, st, p->d_posfix,
+                                     (size_t)4 * p->N * sizeof(int), p->pos_hit, staging, (const int*)p->d_posfix, z,
+                                     (int)p->N, rr, partials, stop, i0, i1, dec, prec));
+            }
             break;
         case 8: IE_SCAT(8, 2); break;
 #undef IE_SCAT
@@ -2137,6 +2145,7 @@ extern "C" int ie_precond_create(const ie_geom* g, const int64_t* h_offsets, con
     if (mm) {
         IE_CHECK_BUILD(cudaMalloc(&p->d_posfix, posfix.size() * sizeof(int)));
         IE_CHECK_BUILD(cudaMemcpyAsync(p->d_posfix, posfix.data(), posfix.size() * sizeof(int), cudaMemcpyHostToDevice, st));
+        if (p->mm == 4) p->pos_hit = ie::l2_persist_request(posfix.size() * sizeof(int));
     }
 
     // --- factorise the representatives
