@@ -38,7 +38,8 @@ float l2_persist_request(size_t bytes) {
         }
         cap = std::min<size_t>((size_t)mx, (size_t)l2 / 4);
     }
-    const size_t want = std::min(cap, (bytes + bytes / 7 + ((size_t)1 << 20)) & ~(((size_t)1 << 20) - 1));
+    size_t want = std::min(cap, (bytes + bytes / 7 + ((size_t)1 << 20)) & ~(((size_t)1 << 20) - 1));
+    if (const char* e = getenv("IEDD_B200_L2_SETASIDE_MB")) want = (size_t)atoi(e) << 20;  // experiment
     if (want > limit) {
         if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want) != cudaSuccess) {
             cudaGetLastError();

@@ -1622,7 +1622,9 @@ static int scatter_launch(const ie_precond* p, const double* staging, const doub
     const double* rr = partials ? r : nullptr;
     const PcgDecide dec = partials ? t_dec : PcgDecide{};
     const PeerRec prec = partials ? t_prec : PeerRec{};
-#define IE_SCAT(MM, ...) IE_CUDA(launch_k(k_scatter_fixed<MM, __VA_ARGS__>, dim3(nch), dim3(256), 0, st, staging, (const int*)p->d_posfix, z, (int)p->N, rr, partials, stop, i0, i1, dec, prec))
+    // the position table (read unchanged by every apply, on a dependent-load chain)
+    // holds a persisting L2 window (l2_persist_request at creation)
+#define IE_SCAT(MM, ...) IE_CUDA(launch_k_win(k_scatter_fixed<MM, __VA_ARGS__>, dim3(nch), dim3(256), 0, st, p->d_posfix, (size_t)MM * p->N * sizeof(int), p->pos_hit, staging, (const int*)p->d_posfix, z, (int)p->N, rr, partials, stop, i0, i1, dec, prec))
     // batch sizes measured at config 5 (MM = 4): 2 points with the next
     // batch's positions prefetched 10.6-11.3 us, 2 without 12.2, 4 15.5, 8 18.9
     // (register-limited residency), 1 point per level (before) 17.8
@@ -1633,15 +1635,8 @@ static int scatter_launch(const ie_precond* p, const double* staging, const doub
             // 4 points per dependent level capped at 64 registers (4 CTAs per SM keep
             // the 512 chunks of config 5 resident; 48 B of spills): -1.5 us per PCG
             // iteration against 2 points (same box, alternating processes)
-            if (getenv("IEDD_B200_SCAT_G2")) {
-                IE_SCAT(4, 2, true);
-            } else {
-                // 4 points per dependent level capped at 64 registers; the position table
-                // (read unchanged by every apply) holds a persisting L2 window
-                IE_CUDA(launch_k_win(k_scatter_fixed<4, 4, true>, dim3(nch), dim3(256), 0, st, p->d_posfix,
-                                     (size_t)4 * p->N * sizeof(int), p->pos_hit, staging, (const int*)p->d_posfix, z,
-                                     (int)p->N, rr, partials, stop, i0, i1, dec, prec));
-            }
+            if (getenv("IEDD_B200_SCAT_G2")) IE_SCAT(4, 2, true);
+            else IE_SCAT(4, 4, true);
             break;
         case 8: IE_SCAT(8, 2); break;
 #undef IE_SCAT
@@ -2145,7 +2140,7 @@ extern "C" int ie_precond_create(const ie_geom* g, const int64_t* h_offsets, con
     if (mm) {
         IE_CHECK_BUILD(cudaMalloc(&p->d_posfix, posfix.size() * sizeof(int)));
         IE_CHECK_BUILD(cudaMemcpyAsync(p->d_posfix, posfix.data(), posfix.size() * sizeof(int), cudaMemcpyHostToDevice, st));
-        if (p->mm == 4) p->pos_hit = ie::l2_persist_request(posfix.size() * sizeof(int));
+        p->pos_hit = ie::l2_persist_request(posfix.size() * sizeof(int));
     }
 
     // --- factorise the representatives
