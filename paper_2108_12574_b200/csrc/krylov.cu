@@ -46,6 +46,8 @@ int matvec_prepare_stream(const ie_matvec* m, cudaStream_t st);
 int precond_apply(const ie_precond* p, const double* r, double* z, double* partials, cudaStream_t st,
                   const int* stop);
 void precond_set_decide(const PcgDecide* d);
+void precond_set_staging(double* buf, size_t bytes);
+double* matvec_scratch(const ie_matvec* m, cudaStream_t st, size_t* bytes);
 void precond_set_peer_record(const PeerRec* r);
 int matvec_N(const ie_matvec* m);
 uint64_t matvec_uid(const ie_matvec* m);
@@ -690,6 +692,14 @@ static int pcg_impl(const ie_matvec* A, const ie_precond* T, const double* f, do
     double* pmax = xrz + kRzRec * nch;
     double* pglob = pmax + nch;
     const int* stop = &W->st->stop;
+    // Buffers with disjoint lifetimes share storage, so the iteration's working
+    // set fits the L2 (config 5: ~128 MB of vectors, work buffer, staging and
+    // tables cycled through a 126 MB L2): z (scatter -> next pass's p update)
+    // lives in q's storage (row inverse -> k_iter_a), and the apply's staging
+    // buffer (class GEMM -> scatter) in the FFT work buffer (row forward -> row
+    // inverse).  IEDD_B200_NO_ALIAS=1: separate buffers (comparison).
+    static const bool alias = getenv("IEDD_B200_NO_ALIAS") == nullptr;
+    double* const zv = alias ? q : W->z;
     // k_iter_b and k_post_pass folded into the FFT passes (2D / 3D FFT plans)
     static const bool no_fuse = getenv("IEDD_B200_NO_FUSE") != nullptr;
     static const bool no_fuse_upd = getenv("IEDD_B200_NO_FUSE_UPD") != nullptr;
@@ -713,7 +723,13 @@ static int pcg_impl(const ie_matvec* A, const ie_precond* T, const double* f, do
         }
         if (T) {
             precond_set_decide(&dec);
+            if (alias) {  // the stream's idle FFT work buffer is the apply's staging buffer
+                size_t sb = 0;
+                double* sbuf = matvec_scratch(A, s2, &sb);
+                precond_set_staging(sbuf, sb);
+            }
             const int r2 = precond_apply(T, rin, zout, xrz, s2, stop);
+            precond_set_staging(nullptr, 0);
             precond_set_decide(nullptr);
             return r2;
         }
@@ -743,9 +759,9 @@ static int pcg_impl(const ie_matvec* A, const ie_precond* T, const double* f, do
     IE_LAUNCHED();
     IE_CUDA(cudaMemsetAsync(uu, 0, (size_t)N * 8, st));
     IE_CUDA(cudaMemcpyAsync(W->r, f, (size_t)N * 8, cudaMemcpyDeviceToDevice, st));
-    if ((rc = apply(W->r, W->z, 0))) return rc;
+    if ((rc = apply(W->r, zv, 0))) return rc;
     IE_CUDA(cudaMemsetAsync(pglob, 0, 3 * sizeof(double), st));
-    k_pcg_setup<<<nch, kRed, 0, st>>>(xrz, nch, W->st, p, W->z, N, 0, pmax, fuse_upd ? pglob : nullptr);  // p = z, rho_0
+    k_pcg_setup<<<nch, kRed, 0, st>>>(xrz, nch, W->st, p, zv, N, 0, pmax, fuse_upd ? pglob : nullptr);  // p = z, rho_0
     IE_LAUNCHED();
     // iterations: `it` = the iteration whose A-pass is enqueued; the pass also
     // carries u_{it-1} for the deferred true-residual check of iteration it-1.
@@ -778,7 +794,7 @@ static int pcg_impl(const ie_matvec* A, const ie_precond* T, const double* f, do
         PcgFuse fz;  // (fused: the previous iteration's k_iter_b and this pass's k_post_pass ride in the FFT)
         if (fused) {
             if (fuse_upd && do_p && pending) {
-                fz.z = W->z;
+                fz.z = zv;
                 fz.pglob = pglob;
                 fz.s = W->st;
                 fz.it = itarg;
@@ -823,8 +839,8 @@ static int pcg_impl(const ie_matvec* A, const ie_precond* T, const double* f, do
         if (spec) {  // speculative: z_it is discarded if iteration it is the last
             if ((r2 = mark(3))) return r2;
             if (timed_apply && !pf) {
-                if ((r2 = apply(W->r, W->z, evi))) return r2;
-            } else if ((r2 = apply_on(W->r, W->z, s2, itarg))) {
+                if ((r2 = apply(W->r, zv, evi))) return r2;
+            } else if ((r2 = apply_on(W->r, zv, s2, itarg))) {
                 return r2;
             }
             if ((r2 = mark(4))) return r2;
@@ -832,7 +848,7 @@ static int pcg_impl(const ie_matvec* A, const ie_precond* T, const double* f, do
             if (fork_u) IE_CUDA(cudaStreamWaitEvent(s2, W->join_ev, 0));
             if (!fuse_upd) {
                 IE_CUDA(launch_k(k_iter_b, dim3(nch), dim3(kRed), 0, s2, (const double*)xrz, nch,
-                                 (long long)itarg, W->st, p, (const double*)W->z, N, pmax));
+                                 (long long)itarg, W->st, p, (const double*)zv, N, pmax));
                 IE_LAUNCHED();
             }
             if ((r2 = mark(5))) return r2;

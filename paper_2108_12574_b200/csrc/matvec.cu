@@ -431,6 +431,19 @@ static ie_matvec::Ws mv_ws(ie_matvec* m, cudaStream_t st, bool* ok) {
     return w;
 }
 
+// The stream's FFT work buffer (null for the direct sum): between two A-passes
+// on that stream nothing in it is live, so the PCG lends it to the apply as
+// its staging buffer (one working set less in the L2).
+double* matvec_scratch(const ie_matvec* m, cudaStream_t st, size_t* bytes) {
+    *bytes = 0;
+    if (m->method != IE_MATVEC_FFT) return nullptr;
+    bool ok;
+    const ie_matvec::Ws W = mv_ws(const_cast<ie_matvec*>(m), st, &ok);
+    if (!ok || !W.buf) return nullptr;
+    *bytes = (size_t)fft_buf_elems(m->fft) * sizeof(double2);
+    return reinterpret_cast<double*>(W.buf);
+}
+
 // Allocate the stream's matvec scratch now (before a graph capture on it).
 int matvec_prepare_stream(const ie_matvec* m, cudaStream_t st) {
     bool ok;

@@ -1612,6 +1612,14 @@ static thread_local PcgDecide t_dec;
 static thread_local PeerRec t_prec;
 
 void precond_set_decide(const PcgDecide* d) { t_dec = d ? *d : PcgDecide{}; }
+// staging buffer lent by the caller for the next applies of this thread (the
+// PCG passes the matvec's idle FFT work buffer); used when large enough
+static thread_local double* t_staging = nullptr;
+static thread_local size_t t_staging_bytes = 0;
+void precond_set_staging(double* buf, size_t bytes) {
+    t_staging = buf;
+    t_staging_bytes = buf ? bytes : 0;
+}
 void precond_set_peer_record(const PeerRec* r) { t_prec = r ? *r : PeerRec{}; }
 
 static int scatter_launch(const ie_precond* p, const double* staging, const double* r, double* z,
@@ -1688,8 +1696,9 @@ static void launch_gemm(const ie_precond* p, const GemmArgs& g, cudaStream_t st)
 
 int precond_apply(const ie_precond* p, const double* r, double* z, double* partials, cudaStream_t st,
                   const int* stop) {
-    const ie_precond::Ws W = apply_ws(const_cast<ie_precond*>(p), st);
+    ie_precond::Ws W = apply_ws(const_cast<ie_precond*>(p), st);
     if (!W.staging) return IE_ERR_CUDA;
+    if (t_staging && t_staging_bytes >= (size_t)p->total_s * sizeof(double)) W.staging = t_staging;
     if (p->gemm_ra) {
         // the DMMA kernel gathers its r columns itself; the FFMA variant reads them pre-gathered
         const bool pre = !p->use_dmma || p->dmma_pregather;
