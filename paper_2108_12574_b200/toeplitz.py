@@ -35,7 +35,10 @@ def to_device_vector(v, n: int):
     a = np.asarray(v, dtype=float)
     if a.shape != (n,):
         raise ValueError(f"expected vector of length {n}, got shape {a.shape}")
-    return torch.from_numpy(np.ascontiguousarray(a)).to("cuda", non_blocking=False), True
+    # (non_blocking: from page-locked memory the copy is stream-ordered and the host
+    # goes on to enqueue the kernels behind it; from pageable memory it is staged
+    # synchronously either way)
+    return torch.from_numpy(np.ascontiguousarray(a)).to("cuda", non_blocking=True), True
 
 
 def to_host(t, was_numpy: bool):
