@@ -231,6 +231,25 @@ class TestApply:
         c = ie.from_decomposition(op, d, share_translated=True, variant="subst")
         assert rel(c.apply(r), b.apply(r)) <= 1e-13
 
+    @pytest.mark.parametrize("n,m,w,kind", [(512, 64, 2, "schwarz"), (768, 96, 2, "schwarz"), (832, 104, 2, "schwarz"),
+                                            (896, 112, 2, "schwarz"), (1152, 144, 2, "schwarz"), (640, 64, 1, "schwarz"),
+                                            (704, 64, 0, "jacobi"), (832, 104, 1, "schwarz")])
+    def test_class_gemm_tile_shapes(self, ie, n, m, w, kind):
+        """k_apply_dmma2 deals the n8-tile columns of a tile over the warps by
+        the tile's width (D / 296 blocks: 14, 32, 37, 43, 64 ... columns here, so
+        2, 4, 5, 6, 8 n-tiles, odd ones split by rows) and gathers through
+        per-tile tables; blocks of 100 to 144 points (kpad != s included).  The
+        per-block packed kernel (unshared factors) is the independent check."""
+        grid = ie.build_grid(2, n)
+        op = ie.build_operator(grid, lattice="cell")
+        d = ie.build_decomposition(grid, m, w, kind)
+        a = ie.from_decomposition(op, d, share_translated=True)
+        b = ie.from_decomposition(op, d, share_translated=False)
+        r = np.random.default_rng(n + w).standard_normal(op.n)
+        za, zb = a.apply(r), b.apply(r)
+        assert rel(za, zb) <= 1e-13
+        assert np.array_equal(za, a.apply(r))
+
     def test_gemm_apply_deterministic(self, ie, rng):
         grid = ie.build_grid(2, 256)
         op = ie.build_operator(grid, lattice="cell")
