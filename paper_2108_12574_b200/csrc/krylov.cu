@@ -160,7 +160,7 @@ __global__ void __launch_bounds__(kRed, 4) k_iter_a(const double* xpost, int npo
                                                  long long it, PcgState* s, double* hist, double* u, double* r,
                                                  const double* p, const double* q, int nb, int c0, int nchb,
                                                  double* xrz, const double* pmax, HaloSeg hs, int ticket) {
-    __shared__ double sh[kRed];
+    __shared__ double sh[2 * kRed];
     __shared__ int decided;
     if (ticket & 2) pdl_trigger();  // (ticket bit 1: early trigger; bit 0: advance the iteration counter)
     pdl_wait();
@@ -197,9 +197,15 @@ __global__ void __launch_bounds__(kRed, 4) k_iter_a(const double* xpost, int npo
     }
     if (stopv) return;
     double denom = 0.0, res2 = 0.0;
-    if (do_p) denom = block_tree(lp, sh);
-    __syncthreads();
-    if (pending) res2 = block_tree(lr, sh);
+    if (do_p && pending) {  // both sums in one pass over the tree levels (same pairs)
+        denom = lp;
+        res2 = lr;
+        block_tree2(denom, res2, sh);
+    } else {
+        if (do_p) denom = block_tree(lp, sh);
+        __syncthreads();
+        if (pending) res2 = block_tree(lr, sh);
+    }
     if (threadIdx.x == 0) {
         int status = 0;
         double rel = 0.0;

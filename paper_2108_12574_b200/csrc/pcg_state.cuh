@@ -31,14 +31,51 @@ struct PcgState {
 // leaves): deterministic, identical on every rank and in every driver.
 // (A warp-shuffle butterfly + ordered warp sums was measured: no change in
 // the iteration time, 144.5 vs 145.6 us, so the round-1 association stays.)
+// Levels with a partner >= 32 threads away go through shared memory; the last
+// five run inside warp 0 by shuffles (lane t takes lane t + o: the same pairs in
+// the same order, so the same bits), then one broadcast.
 __device__ __forceinline__ double block_tree(double v, double* sh) {
     sh[threadIdx.x] = v;
     __syncthreads();
-    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    for (int o = blockDim.x / 2; o >= 32; o >>= 1) {
         if (threadIdx.x < o) sh[threadIdx.x] += sh[threadIdx.x + o];
         __syncthreads();
     }
+    if (threadIdx.x < 32) {
+        double a = sh[threadIdx.x];
+        for (int o = min(16, (int)blockDim.x / 2); o > 0; o >>= 1) a += __shfl_down_sync(0xffffffffu, a, o);
+        if (threadIdx.x == 0) sh[0] = a;
+    }
+    __syncthreads();
     return sh[0];
+}
+// two trees at once (each value keeps block_tree's pairs): sh holds 2 blockDim doubles
+__device__ __forceinline__ void block_tree2(double& va, double& vb, double* sh) {
+    double* sb = sh + blockDim.x;
+    sh[threadIdx.x] = va;
+    sb[threadIdx.x] = vb;
+    __syncthreads();
+    for (int o = blockDim.x / 2; o >= 32; o >>= 1) {
+        if (threadIdx.x < o) {
+            sh[threadIdx.x] += sh[threadIdx.x + o];
+            sb[threadIdx.x] += sb[threadIdx.x + o];
+        }
+        __syncthreads();
+    }
+    if (threadIdx.x < 32) {
+        double a = sh[threadIdx.x], b = sb[threadIdx.x];
+        for (int o = min(16, (int)blockDim.x / 2); o > 0; o >>= 1) {
+            a += __shfl_down_sync(0xffffffffu, a, o);
+            b += __shfl_down_sync(0xffffffffu, b, o);
+        }
+        if (threadIdx.x == 0) {
+            sh[0] = a;
+            sb[0] = b;
+        }
+    }
+    __syncthreads();
+    va = sh[0];
+    vb = sb[0];
 }
 
 __device__ __forceinline__ double reduce_partials(const double* part, int nch, double* sh) {
