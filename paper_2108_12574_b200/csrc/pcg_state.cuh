@@ -141,16 +141,23 @@ __device__ __forceinline__ void chunk_sum_max(double v, double m, double* sh, do
     sh[threadIdx.x] = v;
     sh[blockDim.x + threadIdx.x] = m;
     __syncthreads();
-    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    for (int o = blockDim.x / 2; o >= 32; o >>= 1) {
         if (threadIdx.x < o) {
             sh[threadIdx.x] += sh[threadIdx.x + o];
             sh[blockDim.x + threadIdx.x] = fmax(sh[blockDim.x + threadIdx.x], sh[blockDim.x + threadIdx.x + o]);
         }
         __syncthreads();
     }
-    if (threadIdx.x == 0) {
-        out[0] = sh[0];
-        out[1] = sh[blockDim.x];
+    if (threadIdx.x < 32) {  // the last five levels inside warp 0 (the sum keeps its pairs; a maximum has no order)
+        double a = sh[threadIdx.x], b = sh[blockDim.x + threadIdx.x];
+        for (int o = min(16, (int)blockDim.x / 2); o > 0; o >>= 1) {
+            a += __shfl_down_sync(0xffffffffu, a, o);
+            b = fmax(b, __shfl_down_sync(0xffffffffu, b, o));
+        }
+        if (threadIdx.x == 0) {
+            out[0] = a;
+            out[1] = b;
+        }
     }
     __syncthreads();
 }
@@ -184,6 +191,9 @@ __device__ __forceinline__ double chunk_absmax(double v, double* sh);
 __device__ inline void pcg_decide(const double* rec, const PcgDecide& d, double* sh) {
     PcgState* s = d.s;
     const long long itb = d.it < 0 ? s->it_dev : d.it;
+    // thread 0's scalars are requested before the reductions (one round trip less in the tail)
+    const double rho_prev = threadIdx.x == 0 ? s->rho[(itb - 1) & 1] : 0.0;
+    const double mp = threadIdx.x == 0 ? d.pglob[itb % 3] : 0.0;
     double loc = 0.0, mz = 0.0, mu = 0.0;
     for (int c = threadIdx.x; c < d.nch; c += kPcgRed) {
         loc += rec[kRzRec * c];
@@ -196,8 +206,7 @@ __device__ inline void pcg_decide(const double* rec, const PcgDecide& d, double*
     __syncthreads();
     mu = chunk_absmax(mu, sh);
     if (threadIdx.x == 0) {
-        const double beta = rz / s->rho[(itb - 1) & 1];
-        const double mp = d.pglob[itb % 3];
+        const double beta = rz / rho_prev;
         s->beta = beta;
         s->rho[itb & 1] = rz;
         s->sc[0] = pcg_pow2_scale(__dadd_rn(mz, __dmul_rn(fabs(beta), mp)));
@@ -208,13 +217,14 @@ __device__ inline void pcg_decide(const double* rec, const PcgDecide& d, double*
 }
 
 __device__ __forceinline__ double chunk_absmax(double v, double* sh) {
-    sh[threadIdx.x] = v;
+    // a maximum has no rounding: warp shuffles, then the warp maxima through shared memory
+    for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+    __syncthreads();  // (sh may still be read by a previous reduction's last stage)
+    if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
     __syncthreads();
-    for (int o = blockDim.x / 2; o > 0; o >>= 1) {
-        if (threadIdx.x < o) sh[threadIdx.x] = fmax(sh[threadIdx.x], sh[threadIdx.x + o]);
-        __syncthreads();
-    }
-    return sh[0];
+    double m = sh[0];
+    for (int w = 1; w < (int)(blockDim.x >> 5); ++w) m = fmax(m, sh[w]);
+    return m;
 }
 
 }  // namespace ie
