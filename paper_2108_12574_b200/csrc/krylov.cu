@@ -80,6 +80,28 @@ __global__ void __launch_bounds__(kRed) k_dot_partials(const double* x, const do
 }
 
 
+// The solve's opening in one pass over f: the graph-stable copy of f, r = f,
+// u = 0 and the chunk partials of f.f (k_dot_partials' chain and tree per chunk).
+__global__ void __launch_bounds__(kRed) k_pcg_begin(const double* f, double* fcopy, double* r, double* u, int N,
+                                                    double* part) {
+    __shared__ double sh[kRed];
+    const int base = blockIdx.x * kChunk;
+    double loc = 0.0;
+#pragma unroll
+    for (int e = 0; e < kChunk / kRed; ++e) {
+        const int i = base + e * kRed + threadIdx.x;
+        if (i < N) {
+            const double v = f[i];
+            fcopy[i] = v;
+            r[i] = v;
+            u[i] = 0.0;
+            loc = fma(v, v, loc);
+        }
+    }
+    const double t = block_tree(loc, sh);
+    if (threadIdx.x == 0) part[blockIdx.x] = t;
+}
+
 __global__ void k_set_it(PcgState* s, long long it) { s->it_dev = it; }
 
 __global__ void k_pcg_init(const double* part, int nch, PcgState* s, double tol, long long max_iters,
@@ -756,15 +778,13 @@ static int pcg_impl(const ie_matvec* A, const ie_precond* T, const double* f, do
         return IE_OK;
     };
     // the right-hand side at a stable address (captured graphs reference it)
-    IE_CUDA(cudaMemcpyAsync(W->fcopy, f, (size_t)N * 8, cudaMemcpyDeviceToDevice, st));
+    // (k_pcg_begin: the copy, r = f, u = 0 and ||f||^2's chunk partials in one pass)
+    k_pcg_begin<<<nch, kRed, 0, st>>>(f, W->fcopy, W->r, uu, N, xf);
+    IE_LAUNCHED();
     f = W->fcopy;
     // ||f||, state init (pcg.py:72-91)
-    k_dot_partials<<<nch, kRed, 0, st>>>(f, f, N, 0, xf);
-    IE_LAUNCHED();
     k_pcg_init<<<1, kRed, 0, st>>>(xf, nch, W->st, tol, max_iters, W->hist);
     IE_LAUNCHED();
-    IE_CUDA(cudaMemsetAsync(uu, 0, (size_t)N * 8, st));
-    IE_CUDA(cudaMemcpyAsync(W->r, f, (size_t)N * 8, cudaMemcpyDeviceToDevice, st));
     if ((rc = apply(W->r, zv, 0))) return rc;
     IE_CUDA(cudaMemsetAsync(pglob, 0, 3 * sizeof(double), st));
     k_pcg_setup<<<nch, kRed, 0, st>>>(xrz, nch, W->st, p, zv, N, 0, pmax, fuse_upd ? pglob : nullptr);  // p = z, rho_0
