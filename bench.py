@@ -322,7 +322,10 @@ def run_ours(args):
         "clocks": clk,
     }
     if not args.no_configs:
-        out["configs"] = _other_configs(ie)
+        try:
+            out["configs"] = _other_configs(ie)
+        except Exception as e:  # the side block must never cost the bench line
+            out["configs"] = {"error": f"{type(e).__name__}: {e}"}
     if not args.no_cpu:
         out["cpu_baseline"] = cpu_baseline(max(1, min(10, args.steps)))  # ~8 s of CPU work
     print(json.dumps(out))
