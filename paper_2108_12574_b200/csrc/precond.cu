@@ -1171,7 +1171,7 @@ __device__ __forceinline__ void scatter_decide(const double* partials, const Pcg
 }
 
 template <int MM, int UNR, bool PF = false>
-__global__ void __launch_bounds__(256, UNR >= 4 && PF ? 4 : 1) k_scatter_fixed(const double* staging, const int* pos, double* z, int N,
+__global__ void __launch_bounds__(256, UNR >= 4 && MM >= 4 ? 4 : 1) k_scatter_fixed(const double* staging, const int* pos, double* z, int N,
                                                        const double* r, double* partials, const int* stop, int i0,
                                                        int i1, PcgDecide dec, PeerRec pr) {
     __shared__ double sh[512];
@@ -1641,10 +1641,13 @@ static int scatter_launch(const ie_precond* p, const double* staging, const doub
         case 2: IE_SCAT(2, 2, true); break;
         case 4:
             // 4 points per dependent level capped at 64 registers (4 CTAs per SM keep
-            // the 512 chunks of config 5 resident; 48 B of spills): -1.5 us per PCG
-            // iteration against 2 points (same box, alternating processes)
+            // the 512 chunks of config 5 resident): -1.5 us per PCG iteration against
+            // 2 points; with the table pinned in L2 the next batch's position prefetch
+            // (48 B of spills at this cap) only costs: -3.0 us without it (same box,
+            // alternating processes); 8 points per level spills 152 B: +6.4 us
             if (getenv("IEDD_B200_SCAT_G2")) IE_SCAT(4, 2, true);
-            else IE_SCAT(4, 4, true);
+            else if (getenv("IEDD_B200_SCAT_PF")) IE_SCAT(4, 4, true);
+            else IE_SCAT(4, 4, false);
             break;
         case 8: IE_SCAT(8, 2); break;
 #undef IE_SCAT
