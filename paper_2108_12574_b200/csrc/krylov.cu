@@ -120,6 +120,8 @@ __global__ void k_pcg_init(const double* part, int nch, PcgState* s, double tol,
         s->status = 0;
         s->stop = 0;
         s->ticket = 0;
+        s->last_rel = 1.0;
+        s->last_k = 0;
         hist[0] = 1.0;
         if (s->nf == 0.0) {  // pcg.py:74-78
             hist[0] = 0.0;
@@ -241,7 +243,11 @@ __global__ void __launch_bounds__(kRed, 4) k_iter_a(const double* xpost, int npo
         if (!status && do_p && (!isfinite(denom) || denom <= 0.0)) status = 4;
         decided = status;
         if (blockIdx.x == 0) {
-            if (pending && status != 5) hist[k] = rel;
+            if (pending && status != 5) {
+                hist[k] = rel;
+                s->last_rel = rel;
+                s->last_k = k;
+            }
             if (status) {
                 s->status = status;
                 s->n_it = k;
@@ -588,6 +594,7 @@ struct PcgWork {
     cudaEvent_t fork_ev = nullptr, join_ev = nullptr;
     cudaGraphExec_t gexec = nullptr;
     cudaGraphExec_t gexec_b = nullptr;  // kBatch iterations in one graph (no graph boundary between them)
+    cudaGraphExec_t gexec_m = nullptr;  // 4 iterations (the remainder of a long batch size)
     uint64_t key_a = 0, key_t = 0;
     int gnodes = 0;  // kernel nodes in the captured iteration
     PcgState* st = nullptr;
@@ -606,6 +613,7 @@ struct PcgWork {
         cudaFree(fcopy);
         if (gexec) cudaGraphExecDestroy(gexec);
         if (gexec_b) cudaGraphExecDestroy(gexec_b);
+        if (gexec_m) cudaGraphExecDestroy(gexec_m);
         if (cap_stream) cudaStreamDestroy(cap_stream);
         if (side_stream) cudaStreamDestroy(side_stream);
         if (fork_ev) cudaEventDestroy(fork_ev);
@@ -708,7 +716,14 @@ static int pcg_impl(const ie_matvec* A, const ie_precond* T, const double* f, do
         ~Release() { work_release(w); }
     } rel_guard{W};
     // apply events: pair 0 = initial apply, pair it = speculative apply of iteration it
-    const int64_t kBatch = 4;
+    // steady iterations per graph replay (= per status poll).  Every replay boundary
+    // costs ~10 us of idle GPU (graph launch + the poll's state copy), so large
+    // problems take 16 (config 5: 4 -> 8 -1.3 us, -> 16 -2.0 us per iteration); a
+    // converged solve runs up to two batches of no-op iterations (every kernel
+    // returns on the stop flag, ~12 us per iteration), which small problems, whose
+    // real iterations cost little more, cannot afford
+    static const long long kb_env = getenv("IEDD_B200_KBATCH") ? atoll(getenv("IEDD_B200_KBATCH")) : 0;
+    const int64_t kBatch = kb_env > 0 ? std::min<long long>(kb_env, 64) : (N >= (1 << 18) ? 16 : 4);
     if ((rc = ensure_events(W, 2 * (size_t)(std::min<int64_t>(cap, 4096) + 2)))) return rc;
     double* p = W->PU;
     double* uu = W->PU + N;
@@ -895,13 +910,14 @@ static int pcg_impl(const ie_matvec* A, const ie_precond* T, const double* f, do
     if (use_graph) {
         const uint64_t ka = matvec_uid(A), kt = T ? precond_uid(T) : 0;
         if (!W->gexec || W->key_a != ka || W->key_t != kt) {
-            for (cudaGraphExec_t* ge : {&W->gexec, &W->gexec_b}) {
+            for (cudaGraphExec_t* ge : {&W->gexec, &W->gexec_b, &W->gexec_m}) {
                 if (*ge) cudaGraphExecDestroy(*ge);
                 *ge = nullptr;
             }
             if (T && (rc = precond_prepare_stream(T, W->cap_stream))) return rc;
             if ((rc = matvec_prepare_stream(A, W->cap_stream))) return rc;
-            for (int reps : {1, (int)kBatch}) {
+            for (int reps : {1, (int)kBatch, kBatch > 4 ? 4 : 0}) {
+                if (!reps) continue;
                 cudaGraph_t g;
                 IE_CUDA(cudaStreamBeginCapture(W->cap_stream, cudaStreamCaptureModeThreadLocal));
                 int r2 = IE_OK;
@@ -921,7 +937,7 @@ static int pcg_impl(const ie_matvec* A, const ie_precond* T, const double* f, do
                         if (cudaGraphNodeGetType(nd, &t) == cudaSuccess && t == cudaGraphNodeTypeKernel) ++W->gnodes;
                     }
                 }
-                ce = cudaGraphInstantiate(reps == 1 ? &W->gexec : &W->gexec_b, g, 0);
+                ce = cudaGraphInstantiate(reps == 1 ? &W->gexec : (reps == (int)kBatch ? &W->gexec_b : &W->gexec_m), g, 0);
                 cudaGraphDestroy(g);
                 IE_CUDA(ce);
             }
@@ -935,6 +951,10 @@ static int pcg_impl(const ie_matvec* A, const ie_precond* T, const double* f, do
     // returns on the device stop flag -- follows convergence)
     int64_t it = 1, nbatch = 0, since_poll = 0;
     bool stopped = false, u_copied = false;
+    // (iteration, true residual) of the last two polled states: the batch-size policy's view
+    long long smp_k[2] = {-1, -1};
+    double smp_r[2] = {0.0, 0.0};
+    int nsmp = 0;
     auto poll = [&]() -> int {
         const int slot = (int)(nbatch & 1);
         PcgState* hs = slot ? W->host2 : W->host;
@@ -942,11 +962,31 @@ static int pcg_impl(const ie_matvec* A, const ie_precond* T, const double* f, do
         IE_CUDA(cudaEventRecord(W->poll_ev[slot], st));
         if (nbatch > 0) {
             IE_CUDA(cudaEventSynchronize(W->poll_ev[slot ^ 1]));
-            if ((slot ? W->host : W->host2)->stop) stopped = true;
+            const PcgState* prev = slot ? W->host : W->host2;
+            if (prev->stop) stopped = true;
+            if (prev->last_k > smp_k[1]) {
+                smp_k[0] = smp_k[1];
+                smp_r[0] = smp_r[1];
+                smp_k[1] = prev->last_k;
+                smp_r[1] = prev->last_rel;
+                if (nsmp < 2) ++nsmp;
+            }
         }
         ++nbatch;
         since_poll = 0;
         return IE_OK;
+    };
+    // Long batches (kBatch > 4) only while convergence is not in sight: a run the
+    // caller bounded to a few batches, or an extrapolation of the polled residuals
+    // that leaves at least three batches to go; otherwise 4-iteration replays (a
+    // converged solve runs at most two of its batches as no-op iterations).
+    auto long_batch = [&]() -> bool {
+        if (kBatch <= 4) return true;  // (the "long" graph is the 4-iteration one)
+        if (max_iters <= 4 * kBatch) return true;
+        if (nsmp < 2 || !(smp_r[1] > 0.0) || !(smp_r[0] > 0.0)) return false;
+        if (!(smp_r[1] < smp_r[0])) return true;  // not converging now
+        const double rate = std::log(smp_r[1] / smp_r[0]) / (double)(smp_k[1] - smp_k[0]);
+        return std::log(tol / smp_r[1]) / rate >= 3.0 * (double)kBatch;
     };
     while (it <= max_iters + 1 && !stopped) {
         const int do_p = it <= max_iters;
@@ -957,11 +997,16 @@ static int pcg_impl(const ie_matvec* A, const ie_precond* T, const double* f, do
                 k_set_it<<<1, 1, 0, st>>>(W->st, 2);
                 IE_LAUNCHED();
             }
-            if (!no_multi && it + kBatch - 1 < max_iters) {  // iterations it .. it + kBatch - 1 are all steady-state
+            if (!no_multi && it + kBatch - 1 < max_iters && long_batch()) {  // iterations it .. it + kBatch - 1 are all steady-state
                 IE_CUDA(cudaGraphLaunch(W->gexec_b, st));
                 g_launches.fetch_add(W->gnodes * kBatch, std::memory_order_relaxed);
                 it += kBatch;
                 since_poll += kBatch;
+            } else if (!no_multi && W->gexec_m && it + 3 < max_iters) {
+                IE_CUDA(cudaGraphLaunch(W->gexec_m, st));
+                g_launches.fetch_add(W->gnodes * 4, std::memory_order_relaxed);
+                it += 4;
+                since_poll += 4;
             } else {
                 IE_CUDA(cudaGraphLaunch(W->gexec, st));
                 g_launches.fetch_add(W->gnodes, std::memory_order_relaxed);
@@ -983,7 +1028,7 @@ static int pcg_impl(const ie_matvec* A, const ie_precond* T, const double* f, do
             ++it;
             ++since_poll;
         }
-        if (since_poll >= kBatch || it > max_iters + 1)
+        if (since_poll >= 4 || it > max_iters + 1)
             if ((rc = poll())) return rc;
     }
     // one closing round trip: the state, the history (its first entries

@@ -25,6 +25,9 @@ struct PcgState {
     int status;  // 0 running, 1 converged, 2 stagnated, 3 max_iters, 4 breakdown, 5 non-finite
     int stop;
     unsigned int ticket;  // CTAs of a graph-replayed k_iter_b done (the last one advances it_dev)
+    // the latest true residual and its iteration (the host's batch-size policy reads them from the polled state)
+    double last_rel;
+    long long last_k;
 };
 
 // Fixed-order CTA reductions (a shared-memory halving tree over blockDim
