@@ -1028,7 +1028,9 @@ static int pcg_impl(const ie_matvec* A, const ie_precond* T, const double* f, do
             ++it;
             ++since_poll;
         }
-        if (since_poll >= 4 || it > max_iters + 1)
+        // (no poll when at most four iterations remain: they are enqueued either way
+        // and the closing copy follows)
+        if ((since_poll >= 4 && max_iters - it > 4) || it > max_iters + 1)
             if ((rc = poll())) return rc;
     }
     // one closing round trip: the state, the history (its first entries
